@@ -1,0 +1,226 @@
+/*
+ * tfs.h -- C ABI of libtfs, the B200 (sm_100a) hot path of the large-vocabulary language-model
+ * training step of Abadi et al., "TensorFlow: A system for large-scale machine learning"
+ * (arXiv 1605.08695): the sharded embedding lookup Part -> Gather -> Stitch (§4.2),
+ * the sampled-softmax output layer (§6.4) and the sparse ScatterAdd/SGD
+ * update.  "P:n" cites /root/reference/PAPER.md line n; "R-k" cites
+ * reading k of DESIGN.md §3 (where the paper is silent or garbled).
+ *
+ * CONVENTIONS (every entry point)
+ *  - Buffers are DEVICE pointers owned by the caller (e.g. torch CUDA tensors), unless a
+ *    parameter says "host".  The library never allocates device memory and never synchronises
+ *    the stream, except tfs_sampler_init (a one-off setup call).  Scratch comes from a
+ *    caller-provided workspace `ws` of at least the bytes the matching *_workspace_bytes()
+ *    query returns; ws must be 256-byte aligned.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
+ *    stream-ordered and asynchronous.
+ *  - The returned tfs_status reports ARGUMENT errors only, detected on the host before any
+ *    launch (nothing is launched then).  DATA errors (an id outside its table, a bad stitch
+ *    permutation, an exhausted sampler) are written to the caller's device-resident
+ *    tfs_device_error: `code` and the SMALLEST offending input position in `index`
+ *    (deterministic).  Offending elements are skipped (never read or written out of bounds);
+ *    the output rows they would have produced are unspecified.  The caller zeroes the error
+ *    slot (code 0, index INT64_MAX) before use; `err` may be NULL to skip reporting.
+ *  - Ids are int64 at the boundary.  Integer outputs are bit-exact and run-to-run
+ *    deterministic; floating-point outputs are run-to-run bit-identical (no float atomics:
+ *    every reduction has a fixed order).
+ *  - sm_100a only: on any other device every compute call returns TFS_ERR_UNSUPPORTED.
+ *    There is no CPU fallback.
+ */
+#ifndef TFS_H
+#define TFS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TFS_OK = 0,
+  TFS_ERR_INVALID_ARGUMENT = 1,
+  TFS_ERR_OUT_OF_RANGE = 2,
+  TFS_ERR_BAD_POSITIONS = 3,
+  TFS_ERR_WORKSPACE_TOO_SMALL = 4,
+  TFS_ERR_CUDA = 5,
+  TFS_ERR_UNSUPPORTED = 7,
+  TFS_ERR_SAMPLER_EXHAUSTED = 8
+} tfs_status;
+
+typedef enum { TFS_F32 = 0, TFS_BF16 = 1 } tfs_dtype;
+
+/* Device-resident data-error slot.  index = smallest offending input position. */
+typedef struct {
+  int32_t code;
+  int32_t _pad;
+  int64_t index;
+} tfs_device_error;
+
+/* Library version (major*10000 + minor*100 + patch) and status strings. */
+int32_t tfs_version(void);
+const char* tfs_status_string(int32_t status);
+/* Message of the last TFS_ERR_CUDA on this host thread (copied into buf, NUL-terminated). */
+int32_t tfs_last_error_detail(char* buf, size_t len);
+/* TFS_OK if `device` is an sm_100 (B200-class) GPU, TFS_ERR_UNSUPPORTED otherwise. */
+int32_t tfs_device_check(int32_t device);
+
+/* ==== Part =========================================================================
+ * "The dynamic partition (Part) operation divides the incoming indices into variable-sized
+ * tensors that contain the indices destined for each shard."
+ * Default (assignments == NULL): owner = ids[i] mod num_shards, out_local = ids[i] div
+ * num_shards (R-1); ids must lie in [0, vocab) (else TFS_ERR_OUT_OF_RANGE at i, R-5).
+ * Explicit mode (assignments != NULL, int32[n]): owner = assignments[i] in [0, num_shards),
+ * out_local = ids[i] unchanged; vocab is ignored.
+ * Output is shard-major and STABLE (original order within a shard, R-2): out_local[j] and
+ * out_positions[j] (original index i of the element placed at slot j) for j < n;
+ * out_counts[s] = number of elements of shard s (int64[num_shards]).
+ * 1 <= num_shards <= 256.  n == 0 writes zero counts. */
+size_t tfs_partition_workspace_bytes(int64_t n, int32_t num_shards);
+int32_t tfs_partition(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
+                      const int32_t* assignments, int64_t* out_local, int64_t* out_positions,
+                      int64_t* out_counts, void* ws, size_t ws_bytes, tfs_device_error* err,
+                      void* stream);
+
+/* ==== Gather =======================================================================
+ * "Gather, which extracts a sparse set of rows from a tensor", colocated with the variable.
+ * out[j, :] = table[ids[j], :] for j < n; duplicates allowed; table is row-major [rows x dim].
+ * table_dtype must be TFS_F32.  out_dtype TFS_F32 copies bits; TFS_BF16 rounds to nearest
+ * even.  ids outside [0, rows) -> TFS_ERR_OUT_OF_RANGE at the smallest j.  dim >= 1; rows are
+ * read with 16-byte vectors when dim % 4 == 0 and the pointers are 16-byte aligned. */
+int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int32_t table_dtype,
+                   const int64_t* ids, int64_t n, void* out, int32_t out_dtype,
+                   tfs_device_error* err, void* stream);
+
+/* ==== Stitch =======================================================================
+ * The "dynamic static" (read: dynamic stitch, R-3) op "reassembles the partial results from
+ * each shard into a single result tensor": out[positions[j], :] = rows[j, :] for j < n.
+ * Rows are opaque: row_bytes bytes each (a multiple of 4).  positions must be a permutation
+ * of 0..n-1; when err != NULL it is validated (TFS_ERR_BAD_POSITIONS at the smallest j whose
+ * position is out of range or already claimed by an earlier j, R-4) using ws.  With
+ * err == NULL no workspace is needed and the permutation is trusted. */
+size_t tfs_stitch_workspace_bytes(int64_t n);
+int32_t tfs_stitch(const int64_t* positions, const void* rows, int64_t n, int64_t row_bytes,
+                   void* out, void* ws, size_t ws_bytes, tfs_device_error* err, void* stream);
+
+/* ==== Log-uniform candidate sampler (R-6..R-10, R-17, R-24) ==========
+ * "a set of randomly sampled false classes"; "We sample 512 classes for each batch".
+ * Distribution P(k) = ln((k+2)/(k+1)) / ln(V+1) over frequency-ranked ids (R-6), drawn by
+ * Philox4x32-10 (ctr = (i, step_hi, step_lo, replica), key = (seed_lo, seed_hi)) -> 53-bit
+ * m = ((w0 << 32) | w1) >> 11 -> k = min{k : m < Thr[k]}, Thr[k] = floor(2^53 ln(k+2)/ln(V+1))
+ * evaluated in host long double, Thr[V-1] = 2^53 (R-17).
+ * unique != 0: the first S DISTINCT draws in draw order, num_tries T = draws consumed (R-8);
+ * unique == 0: s_j = draw j, T = S.  Expected counts ec(k) = -expm1(T log1p(-p_k)) (unique) or
+ * S p_k; the log of ec is written (as fp32) for every sampled id and every label (R-10, R-24).
+ *
+ * Setup: `state` is a device buffer of tfs_sampler_state_bytes(vocab) bytes.
+ * tfs_sampler_init fills it (threshold table computed on the host, uploaded synchronously;
+ * per-id scratch initialised) and returns in *out_max_draws (host) a draw budget for
+ * (vocab, S): the smallest N whose expected number of distinct draws exceeds S by 10 standard
+ * deviations (Chernoff; failure probability < 1e-21).  Sampling with that budget never needs
+ * the host; if the budget is ever exhausted the error slot gets TFS_ERR_SAMPLER_EXHAUSTED.
+ * The state is reused across calls (each call restores its scratch); calls sharing a state
+ * must be stream-ordered.  step_dev (device, nullable): if given, the step counter is read
+ * from device memory when the kernels run (so a captured CUDA graph can advance it between
+ * replays) and `step` is ignored.  out_sampled int64[S]; out_log_ec_sampled f32[S];
+ * out_log_ec_labels f32[n_labels]; out_num_tries int64[1] (device). */
+size_t tfs_sampler_state_bytes(int64_t vocab);
+int32_t tfs_sampler_init(int64_t vocab, int32_t num_sampled, int32_t unique, void* state,
+                         int64_t* out_max_draws /* host */, void* stream);
+size_t tfs_sampler_workspace_bytes(int64_t max_draws);
+int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int32_t num_sampled,
+                               int32_t unique, int64_t max_draws, uint64_t seed, uint64_t step,
+                               const uint64_t* step_dev, uint32_t replica,
+                               const int64_t* labels, int64_t n_labels,
+                               int64_t* out_sampled, float* out_log_ec_sampled,
+                               float* out_log_ec_labels, int64_t* out_num_tries, void* ws,
+                               size_t ws_bytes, tfs_device_error* err, void* stream);
+
+/* ==== Sampled softmax forward + backward (DESIGN §3 O9-O11) ==========
+ * "performs a sparse multiplication based on the true class for an example and a set of
+ * randomly sampled false classes".  For tokens t < B and candidates j < S (R-7: one candidate
+ * set per replica and step, shared by its B tokens):
+ *   z_t  = h_t . w_true_t + b_true_t - [Q] log_ec_true_t
+ *   Z_tj = h_t . w_s_j    + b_s_j    - [Q] log_ec_s_j,  excluded if [HITS] and s_j == y_t (R-9)
+ *   lse_t = log(e^{z_t} + sum_j e^{Z_tj});  loss_t = lse_t - z_t;  loss_sum = c sum_t loss_t
+ *   g_t = c (e^{z_t - lse_t} - 1);  G_tj = c e^{Z_tj - lse_t} (0 if excluded);  c = grad_scale
+ *   dh_t = g_t w_true_t + sum_j G_tj w_s_j;  dw_true_t = g_t h_t;  db_true_t = g_t
+ *   dw_s_j = sum_t G_tj h_t;  db_s_j = sum_t G_tj.
+ * Layouts: h, w_true, dh, dw_true [B x dim]; w_s, dw_s [S x dim]; all fp32 row-major; vectors
+ * fp32 [B] / [S]; labels, sampled int64.  labels/sampled are only compared for the hit mask.
+ * operand_dtype TFS_F32: fp32 products, fp32 accumulation (parity mode, max rel err 1e-5).
+ * operand_dtype TFS_BF16: h, w_true, w_s rounded to bf16 (RNE) and G rounded to bf16 before
+ * the dh / dw_s / db_s reductions; tensor-core (tcgen05) GEMMs with fp32 accumulation; all
+ * other math fp32 (R-18).  Requires dim % 64 == 0 for the tensor-core path.
+ * loss, lse, loss_sum may be NULL; the five gradient outputs are required. */
+enum { TFS_SUBTRACT_LOG_Q = 1u, TFS_REMOVE_ACCIDENTAL_HITS = 2u };
+typedef struct {
+  int64_t B, S;
+  int32_t dim;
+  int32_t operand_dtype;
+  uint32_t flags;
+  float grad_scale;
+  const float* h;
+  const int64_t* labels;
+  const float* w_true;
+  const float* b_true;
+  const float* log_ec_true;
+  const int64_t* sampled;
+  const float* w_s;
+  const float* b_s;
+  const float* log_ec_s;
+  float* loss;
+  float* lse;
+  float* loss_sum;
+  float* dh;
+  float* dw_true;
+  float* db_true;
+  float* dw_s;
+  float* db_s;
+} tfs_ssm_args;
+size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype);
+int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, size_t ws_bytes,
+                                    void* stream);
+
+/* ==== Sort-reduce of a sparse gradient (R-16) =======================================
+ * The gradient of Gather is a sparse (ids, rows) pair; before it is routed to the owner
+ * shards the rows of equal ids are summed.  Output: U unique ids in ascending (owner, local)
+ * order (owner = id mod num_shards, local = id div num_shards), out_local[u] = local id,
+ * out_rows[u, :] = sum of rows[i, :] over i with ids[i] == id, summed in increasing i (a fixed
+ * order), optional second value stream rows2/out_rows2 (width 1, e.g. the bias gradient)
+ * reduced with the same segments; out_counts[s] = unique ids owned by shard s;
+ * *out_num_unique (device int64) = U.  Outputs are sized for U <= n.  ids in [0, vocab). */
+size_t tfs_sort_reduce_workspace_bytes(int64_t n, int32_t dim);
+int32_t tfs_sort_reduce(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
+                        const float* rows, int32_t dim, const float* rows2, int64_t* out_local,
+                        float* out_rows, float* out_rows2, int64_t* out_counts,
+                        int64_t* out_num_unique, void* ws, size_t ws_bytes,
+                        tfs_device_error* err, void* stream);
+
+/* ==== ScatterAdd + SGD ===========================
+ * "SGD ... the update rule is W' <- W - alpha x dL/dW.  A parameter server can implement SGD by
+ * using -= as the write operation"; the update acts "on just the values that were originally
+ * gathered".  For every distinct id r among ids[0..n): g = sum over i with ids[i] == r of
+ * grad_rows[i, :], accumulated in fp32 in a FIXED order (stable sort by id, i.e. increasing i,
+ * R-16), then table[r, :] -= lr * g.  Untouched rows are not written.  Optional companion
+ * table2/grad2 (width 1, e.g. the bias b with db) is updated with the same segments.
+ * ids outside [0, rows) -> TFS_ERR_OUT_OF_RANGE at the smallest i (those i are skipped).
+ * n == 0 is a no-op. */
+size_t tfs_scatter_add_sgd_workspace_bytes(int64_t n, int32_t dim);
+int32_t tfs_scatter_add_sgd(float* table, int64_t rows, int32_t dim, const int64_t* ids,
+                            const float* grad_rows, int64_t n, float lr, float* table2,
+                            const float* grad2, void* ws, size_t ws_bytes,
+                            tfs_device_error* err, void* stream);
+
+/* ==== Diagnostics ===============================================================================
+ * C[ks][M x N] = A[M x K] . B[N x K]^T on the tcgen05 path (bf16 operands, K-major, leading
+ * dimensions lda/ldb in elements, multiples of 8; fp32 out, one [M x N] slab per K split;
+ * the effective split count is returned in *out_ksplit).  Used by the GEMM unit test. */
+int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
+                            int32_t N, int32_t K, int32_t ksplit, float* C, int32_t* out_ksplit,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TFS_H */

@@ -1,0 +1,110 @@
+// common.cuh -- shared host/device helpers of libtfs (the CUDA product path).
+// Nothing here is shared with oracle/ (the CPU oracle has its own code end to end).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/tfs.h"
+
+namespace tfs {
+
+constexpr int kNumSMsB200 = 148;
+
+// ---- host-side error plumbing -----------------------------------------------------------------
+void set_last_error(const char* where, cudaError_t e);
+int32_t device_supported();  // TFS_OK on sm_100, else TFS_ERR_UNSUPPORTED (cached per device)
+int num_sms();               // SM count of the current device (cached)
+
+#define TFS_CUDA_TRY(expr)                                \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) {                              \
+      ::tfs::set_last_error(#expr, _e);                   \
+      return TFS_ERR_CUDA;                                \
+    }                                                     \
+  } while (0)
+
+#define TFS_LAUNCH_CHECK()                                \
+  do {                                                    \
+    cudaError_t _e = cudaGetLastError();                  \
+    if (_e != cudaSuccess) {                              \
+      ::tfs::set_last_error("kernel launch", _e);         \
+      return TFS_ERR_CUDA;                                \
+    }                                                     \
+  } while (0)
+
+#define TFS_REQUIRE(cond)                                 \
+  do {                                                    \
+    if (!(cond)) return TFS_ERR_INVALID_ARGUMENT;         \
+  } while (0)
+
+#define TFS_SUPPORTED()                                   \
+  do {                                                    \
+    int32_t _s = ::tfs::device_supported();               \
+    if (_s != TFS_OK) return _s;                          \
+  } while (0)
+
+// ---- workspace carving: 256-byte aligned slices of the caller's workspace ---------------------
+struct Carver {
+  char* base;
+  size_t cap;
+  size_t used = 0;
+  Carver(void* b, size_t c) : base((char*)b), cap(c) {}
+  template <class T>
+  T* take(size_t count) {
+    size_t off = (used + 255) & ~size_t(255);
+    used = off + count * sizeof(T);
+    return base ? (T*)(base + off) : nullptr;
+  }
+  bool fits() const { return used <= cap; }
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline cudaStream_t as_stream(void* s) { return (cudaStream_t)s; }
+
+// ---- device helpers ----------------------------------------------------------------------------
+__device__ __forceinline__ void report_error(tfs_device_error* err, int32_t code, int64_t index) {
+  if (err == nullptr) return;
+  atomicMin((unsigned long long*)&err->index, (unsigned long long)index);
+  atomicCAS(&err->code, 0, code);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint16_t f32_to_bf16_bits(float x) {
+  __nv_bfloat16 b = __float2bfloat16_rn(x);
+  return *reinterpret_cast<uint16_t*>(&b);
+}
+
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  return (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
+}
+
+}  // namespace tfs
+
+// ---- internal launchers shared between translation units --------------------------------------
+namespace tfs {
+
+// Stable digit sort engine (partition / radix).  See sort.cu.
+enum DigitMode : int { kDigitMod = 0, kDigitAssign = 1, kDigitRadix = 2 };
+
+// Stable LSD radix sort of (uint32 key, uint32 val) pairs; keys < 2^key_bits.  Result in
+// keys_out/vals_out.  Scratch from the carver.
+size_t radix_sort_ws_bytes(int64_t n);
+int32_t radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+                         uint32_t* vals_out, int64_t n, int key_bits, void* ws, size_t ws_bytes,
+                         cudaStream_t st);
+
+}  // namespace tfs

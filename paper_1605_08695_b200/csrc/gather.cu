@@ -1,0 +1,298 @@
+// gather.cu -- Gather and Stitch row movers, plus the library's
+// status/diagnostic entry points.
+//
+// Both movers are HBM-bound row copies: one warp per row, 16-byte vector
+// accesses (a 512-wide fp32 row is 128 float4 = 4 per lane), two rows in flight per warp, and
+// a grid of 8 CTAs x 8 warps per SM so ~64 KB of loads are outstanding per SM.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace tfs {
+
+static thread_local char g_last_error[512] = {0};
+
+void set_last_error(const char* where, cudaError_t e) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%s)", where, cudaGetErrorName(e),
+           cudaGetErrorString(e));
+}
+
+int32_t device_supported() {
+  static std::mutex mu;
+  static int cached[64];
+  static bool init = false;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TFS_ERR_UNSUPPORTED;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!init) {
+    for (int i = 0; i < 64; ++i) cached[i] = -1;
+    init = true;
+  }
+  if (cached[dev] < 0) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cached[dev] = (major == 10 && minor == 0) ? TFS_OK : TFS_ERR_UNSUPPORTED;
+  }
+  return cached[dev];
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return kNumSMsB200;
+  if (cached[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : kNumSMsB200;
+  }
+  return cached[dev];
+}
+
+// ------------------------------------------------------------------------------------------------
+template <bool BF16OUT>
+__global__ void __launch_bounds__(256) gather_vec4_kernel(const float* __restrict__ table,
+                                                          int64_t rows, int32_t dim,
+                                                          const int64_t* __restrict__ ids,
+                                                          int64_t n, void* __restrict__ out,
+                                                          tfs_device_error* err) {
+  const int lane = threadIdx.x & 31;
+  const int n4 = dim >> 2;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t j0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 2; j0 < n; j0 += nwarps * 2) {
+    int64_t id[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u;
+      id[u] = j < n ? __ldg(ids + j) : 0;
+      ok[u] = j < n && id[u] >= 0 && id[u] < rows;
+      if (j < n && !ok[u] && lane == 0) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
+    }
+    for (int c0 = 0; c0 < n4; c0 += 128) {  // 4 float4 per lane per row per sweep
+      float4 v[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float4* src = (const float4*)(table + id[u] * dim);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q * 32 + lane;
+          v[u][q] = (ok[u] && c < n4) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+        const int64_t j = j0 + u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q * 32 + lane;
+          if (c >= n4) continue;
+          if (BF16OUT) {
+            uint2 p;
+            p.x = pack_bf16x2(v[u][q].x, v[u][q].y);
+            p.y = pack_bf16x2(v[u][q].z, v[u][q].w);
+            ((uint2*)out)[j * n4 + c] = p;
+          } else {
+            ((float4*)out)[j * n4 + c] = v[u][q];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <bool BF16OUT>
+__global__ void gather_scalar_kernel(const float* __restrict__ table, int64_t rows, int32_t dim,
+                                     const int64_t* __restrict__ ids, int64_t n,
+                                     void* __restrict__ out, tfs_device_error* err) {
+  const int64_t total = n * dim;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / dim;
+    const int c = (int)(e - j * dim);
+    const int64_t id = ids[j];
+    if (id < 0 || id >= rows) {
+      if (c == 0) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
+      continue;
+    }
+    const float v = table[id * dim + c];
+    if (BF16OUT)
+      ((uint16_t*)out)[e] = f32_to_bf16_bits(v);
+    else
+      ((float*)out)[e] = v;
+  }
+}
+
+// Stitch: out[positions[j]] = rows[j].  With validation, claim[p] = min j claiming p.
+__global__ void stitch_claim_kernel(const int64_t* positions, int64_t n,
+                                    unsigned long long* claim, tfs_device_error* err) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = positions[j];
+    if (p < 0 || p >= n)
+      report_error(err, TFS_ERR_BAD_POSITIONS, j);
+    else
+      atomicMin(claim + p, (unsigned long long)j);
+  }
+}
+
+__global__ void __launch_bounds__(256) stitch_vec4_kernel(const int64_t* __restrict__ positions,
+                                                          const uint4* __restrict__ rows,
+                                                          int64_t n, int64_t row_vecs,
+                                                          uint4* __restrict__ out,
+                                                          const unsigned long long* claim,
+                                                          tfs_device_error* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t j = blockIdx.x * 8 + (threadIdx.x >> 5); j < n; j += nwarps) {
+    const int64_t p = __ldg(positions + j);
+    bool ok = p >= 0 && p < n;
+    if (claim != nullptr && ok && claim[p] != (unsigned long long)j) {
+      ok = false;
+      if (lane == 0) report_error(err, TFS_ERR_BAD_POSITIONS, j);
+    }
+    if (!ok) continue;
+    const uint4* src = rows + j * row_vecs;
+    uint4* dst = out + p * row_vecs;
+    for (int64_t c0 = 0; c0 < row_vecs; c0 += 128) {
+      uint4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t c = c0 + q * 32 + lane;
+        if (c < row_vecs) v[q] = __ldg(src + c);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t c = c0 + q * 32 + lane;
+        if (c < row_vecs) dst[c] = v[q];
+      }
+    }
+  }
+}
+
+__global__ void stitch_word_kernel(const int64_t* __restrict__ positions,
+                                   const uint32_t* __restrict__ rows, int64_t n,
+                                   int64_t row_words, uint32_t* __restrict__ out,
+                                   const unsigned long long* claim, tfs_device_error* err) {
+  const int64_t total = n * row_words;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / row_words;
+    const int64_t c = e - j * row_words;
+    const int64_t p = positions[j];
+    bool ok = p >= 0 && p < n;
+    if (claim != nullptr && ok && claim[p] != (unsigned long long)j) {
+      ok = false;
+      if (c == 0) report_error(err, TFS_ERR_BAD_POSITIONS, j);
+    }
+    if (ok) out[p * row_words + c] = rows[e];
+  }
+}
+
+static int grid_for_rows(int64_t n, int rows_per_warp) {
+  const int64_t blocks = cdiv(cdiv(n, rows_per_warp), 8);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 8ll * num_sms()));
+}
+
+}  // namespace tfs
+
+using namespace tfs;
+
+extern "C" int32_t tfs_version(void) { return 100; }
+
+extern "C" const char* tfs_status_string(int32_t s) {
+  switch (s) {
+    case TFS_OK: return "ok";
+    case TFS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case TFS_ERR_OUT_OF_RANGE: return "id out of range";
+    case TFS_ERR_BAD_POSITIONS: return "stitch positions are not a permutation";
+    case TFS_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case TFS_ERR_CUDA: return "CUDA error";
+    case TFS_ERR_UNSUPPORTED: return "unsupported device (libtfs needs sm_100a)";
+    case TFS_ERR_SAMPLER_EXHAUSTED: return "sampler draw budget exhausted";
+    default: return "unknown status";
+  }
+}
+
+extern "C" int32_t tfs_last_error_detail(char* buf, size_t len) {
+  if (buf == nullptr || len == 0) return TFS_ERR_INVALID_ARGUMENT;
+  strncpy(buf, g_last_error, len - 1);
+  buf[len - 1] = 0;
+  return TFS_OK;
+}
+
+extern "C" int32_t tfs_device_check(int32_t device) {
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess)
+    return TFS_ERR_UNSUPPORTED;
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  return (major == 10 && minor == 0) ? TFS_OK : TFS_ERR_UNSUPPORTED;
+}
+
+extern "C" int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int32_t table_dtype,
+                              const int64_t* ids, int64_t n, void* out, int32_t out_dtype,
+                              tfs_device_error* err, void* stream) {
+  TFS_REQUIRE(n >= 0 && dim >= 1 && rows >= 0);
+  TFS_REQUIRE(table_dtype == TFS_F32 && (out_dtype == TFS_F32 || out_dtype == TFS_BF16));
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(table && ids && out);
+  TFS_SUPPORTED();
+  cudaStream_t st = as_stream(stream);
+  const bool bf = out_dtype == TFS_BF16;
+  const bool vec = (dim % 4 == 0) && ((uintptr_t)table % 16 == 0) &&
+                   ((uintptr_t)out % (bf ? 8 : 16) == 0);
+  if (vec) {
+    const int grid = grid_for_rows(n, 2);
+    if (bf)
+      gather_vec4_kernel<true><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
+    else
+      gather_vec4_kernel<false><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
+  } else {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * dim, 256), 8ll * num_sms()));
+    if (bf)
+      gather_scalar_kernel<true><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
+    else
+      gather_scalar_kernel<false><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
+  }
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+extern "C" size_t tfs_stitch_workspace_bytes(int64_t n) {
+  return (size_t)std::max<int64_t>(n, 1) * sizeof(unsigned long long) + 256;
+}
+
+extern "C" int32_t tfs_stitch(const int64_t* positions, const void* rows, int64_t n,
+                              int64_t row_bytes, void* out, void* ws, size_t ws_bytes,
+                              tfs_device_error* err, void* stream) {
+  TFS_REQUIRE(n >= 0 && row_bytes >= 4 && row_bytes % 4 == 0);
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(positions && rows && out);
+  TFS_SUPPORTED();
+  cudaStream_t st = as_stream(stream);
+  unsigned long long* claim = nullptr;
+  if (err != nullptr) {
+    if (ws == nullptr || ws_bytes < tfs_stitch_workspace_bytes(n)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+    claim = (unsigned long long*)ws;
+    TFS_CUDA_TRY(cudaMemsetAsync(claim, 0xff, sizeof(unsigned long long) * n, st));
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4ll * num_sms()));
+    stitch_claim_kernel<<<g, 256, 0, st>>>(positions, n, claim, err);
+  }
+  const bool vec = row_bytes % 16 == 0 && ((uintptr_t)rows % 16 == 0) && ((uintptr_t)out % 16 == 0);
+  if (vec) {
+    stitch_vec4_kernel<<<grid_for_rows(n, 1), 256, 0, st>>>(
+        positions, (const uint4*)rows, n, row_bytes / 16, (uint4*)out, claim, err);
+  } else {
+    const int64_t words = row_bytes / 4;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * words, 256), 8ll * num_sms()));
+    stitch_word_kernel<<<g, 256, 0, st>>>(positions, (const uint32_t*)rows, n, words,
+                                          (uint32_t*)out, claim, err);
+  }
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}

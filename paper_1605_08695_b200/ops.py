@@ -1,0 +1,215 @@
+"""Torch-tensor front end of the libtfs C ABI: one function per entry point of include/tfs.h,
+same names, argument marshalling only (every step runs in the CUDA kernels of libtfs.so).
+
+Tensors must live on the current CUDA device; calls are enqueued on the current torch stream.
+Data errors (bad ids / positions) land in a device error slot; ``ErrorSlot.check()`` reads it
+(that read synchronises, so hot loops check once at the end).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import (TFS_BF16, TFS_F32, TFS_REMOVE_ACCIDENTAL_HITS, TFS_SUBTRACT_LOG_Q, SsmArgs,
+                   TfsError, check)
+
+INT64_MAX = (1 << 63) - 1
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+class ErrorSlot:
+    """Device-resident tfs_device_error {int32 code; int32 pad; int64 index}."""
+
+    def __init__(self, device=None):
+        self.buf = torch.zeros(2, dtype=torch.int64, device=device or "cuda")
+        self.reset()
+
+    def reset(self):
+        self.buf[0] = 0
+        self.buf[1] = INT64_MAX
+
+    @property
+    def ptr(self):
+        return ctypes.c_void_p(self.buf.data_ptr())
+
+    def read(self):
+        v = self.buf.tolist()
+        return int(v[0]) & 0xFFFFFFFF, int(v[1])
+
+    def check(self, what: str):
+        code, idx = self.read()
+        if code != 0:
+            raise TfsError(code, what, idx)
+
+
+def _err(err):
+    return None if err is None else err.ptr
+
+
+# ---------------------------------------------------------------------------------------------
+def partition(ids, vocab: int, num_shards: int, assignments=None, err: ErrorSlot = None,
+              out=None, ws=None):
+    """Part: returns (local_ids, positions, counts), shard-major, stable."""
+    n = ids.numel()
+    dev = ids.device
+    if out is None:
+        out = (torch.empty(n, dtype=torch.int64, device=dev),
+               torch.empty(n, dtype=torch.int64, device=dev),
+               torch.empty(num_shards, dtype=torch.int64, device=dev))
+    local, pos, counts = out
+    L = _lib.lib()
+    if ws is None:
+        ws = _ws(L.tfs_partition_workspace_bytes(n, num_shards), dev)
+    check(L.tfs_partition(_p(ids), n, vocab, num_shards, _p(assignments), _p(local), _p(pos),
+                          _p(counts), _p(ws), ws.numel(), _err(err), _stream()), "tfs_partition")
+    return local, pos, counts
+
+
+def gather(table, ids, out_dtype=torch.float32, err: ErrorSlot = None, out=None):
+    """Gather: out[j] = table[ids[j]] (fp32 copy or bf16 RNE)."""
+    rows = table.shape[0]
+    dim = 1 if table.dim() == 1 else table.shape[1]
+    n = ids.numel()
+    if out is None:
+        out = torch.empty((n, dim), dtype=out_dtype, device=table.device)
+    od = TFS_BF16 if out.dtype == torch.bfloat16 else TFS_F32
+    check(_lib.lib().tfs_gather(_p(table), rows, dim, TFS_F32, _p(ids), n, _p(out), od, _err(err),
+                                _stream()), "tfs_gather")
+    return out
+
+
+def stitch(positions, rows, err: ErrorSlot = None, out=None):
+    """Stitch: out[positions[j]] = rows[j]."""
+    n = positions.numel()
+    if out is None:
+        out = torch.empty_like(rows)
+    row_bytes = rows[0].numel() * rows.element_size() if n else 4
+    L = _lib.lib()
+    ws = _ws(L.tfs_stitch_workspace_bytes(n), rows.device) if err is not None else None
+    check(L.tfs_stitch(_p(positions), _p(rows), n, row_bytes, _p(out), _p(ws),
+                       0 if ws is None else ws.numel(), _err(err), _stream()), "tfs_stitch")
+    return out
+
+
+class Sampler:
+    """Log-uniform candidate sampler with its device state."""
+
+    def __init__(self, vocab: int, num_sampled: int, unique: bool = True, device=None):
+        self.vocab, self.num_sampled, self.unique = vocab, num_sampled, bool(unique)
+        self.device = torch.device(device or "cuda")
+        L = _lib.lib()
+        self.state = _ws(L.tfs_sampler_state_bytes(vocab), self.device)
+        md = ctypes.c_int64(0)
+        check(L.tfs_sampler_init(vocab, num_sampled, int(unique), _p(self.state), ctypes.byref(md),
+                                 _stream()), "tfs_sampler_init")
+        self.max_draws = int(md.value)
+        self.ws = _ws(L.tfs_sampler_workspace_bytes(self.max_draws), self.device)
+
+    def sample(self, seed: int, step: int, replica: int, labels, step_dev=None,
+               err: ErrorSlot = None, out=None):
+        """Returns (sampled int64[S], log_ec_sampled f32[S], log_ec_labels f32[B], T int64[1])."""
+        S = self.num_sampled
+        dev = self.device
+        if out is None:
+            out = (torch.empty(S, dtype=torch.int64, device=dev),
+                   torch.empty(S, dtype=torch.float32, device=dev),
+                   torch.empty(labels.numel(), dtype=torch.float32, device=dev),
+                   torch.empty(1, dtype=torch.int64, device=dev))
+        s, les, ley, T = out
+        check(_lib.lib().tfs_log_uniform_sample(
+            _p(self.state), self.vocab, S, int(self.unique), self.max_draws, seed, step,
+            _p(step_dev), replica, _p(labels), labels.numel(), _p(s), _p(les), _p(ley), _p(T),
+            _p(self.ws), self.ws.numel(), _err(err), _stream()), "tfs_log_uniform_sample")
+        return s, les, ley, T
+
+
+def ssm_workspace(B: int, S: int, dim: int, operand_dtype: int, device) -> torch.Tensor:
+    return _ws(_lib.lib().tfs_ssm_workspace_bytes(B, S, dim, operand_dtype), device)
+
+
+def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, log_ec_s, *,
+                    flags=TFS_SUBTRACT_LOG_Q | TFS_REMOVE_ACCIDENTAL_HITS, grad_scale=1.0,
+                    operand_dtype=TFS_BF16, out=None, ws=None):
+    """Sampled softmax forward + backward.  Returns a dict of fp32 tensors:
+    loss, lse, loss_sum, dh, dw_true, db_true, dw_s, db_s."""
+    B, d = h.shape
+    S = sampled.numel()
+    dev = h.device
+    if out is None:
+        f = lambda *s: torch.empty(*s, dtype=torch.float32, device=dev)
+        out = {"loss": f(B), "lse": f(B), "loss_sum": f(1), "dh": f(B, d), "dw_true": f(B, d),
+               "db_true": f(B), "dw_s": f(S, d), "db_s": f(S)}
+    if ws is None:
+        ws = ssm_workspace(B, S, d, operand_dtype, dev)
+    a = SsmArgs(B, S, d, operand_dtype, flags, float(grad_scale),
+                _p(h), _p(labels), _p(w_true), _p(b_true), _p(log_ec_true), _p(sampled), _p(w_s),
+                _p(b_s), _p(log_ec_s), _p(out["loss"]), _p(out["lse"]), _p(out["loss_sum"]),
+                _p(out["dh"]), _p(out["dw_true"]), _p(out["db_true"]), _p(out["dw_s"]),
+                _p(out["db_s"]))
+    check(_lib.lib().tfs_sampled_softmax_fwd_bwd(ctypes.byref(a), _p(ws), ws.numel(), _stream()),
+          "tfs_sampled_softmax_fwd_bwd")
+    return out
+
+
+def sort_reduce(ids, vocab: int, num_shards: int, rows, rows2=None, err: ErrorSlot = None,
+                out=None, ws=None):
+    """Sum gradient rows of equal ids; unique ids in (owner, local) order.
+    Returns (local int64[n], sums [n, dim], sums2 [n] | None, counts int64[R], U int64[1]);
+    only the first U entries are meaningful."""
+    n = ids.numel()
+    dim = rows.shape[1] if rows.dim() == 2 else 1
+    dev = ids.device
+    if out is None:
+        out = (torch.empty(n, dtype=torch.int64, device=dev),
+               torch.empty((n, dim), dtype=torch.float32, device=dev),
+               None if rows2 is None else torch.empty(n, dtype=torch.float32, device=dev),
+               torch.empty(num_shards, dtype=torch.int64, device=dev),
+               torch.empty(1, dtype=torch.int64, device=dev))
+    local, sums, sums2, counts, U = out
+    L = _lib.lib()
+    if ws is None:
+        ws = _ws(L.tfs_sort_reduce_workspace_bytes(n, dim), dev)
+    check(L.tfs_sort_reduce(_p(ids), n, vocab, num_shards, _p(rows), dim, _p(rows2), _p(local),
+                            _p(sums), _p(sums2), _p(counts), _p(U), _p(ws), ws.numel(), _err(err),
+                            _stream()), "tfs_sort_reduce")
+    return local, sums, sums2, counts, U
+
+
+def scatter_add_sgd(table, ids, grad, lr: float, table2=None, grad2=None, err: ErrorSlot = None,
+                    ws=None):
+    """ScatterAdd-SGD: table[ids[i]] -= lr * grad[i], duplicates summed in a fixed
+    order; optional width-1 companion (table2, grad2).  In place."""
+    rows = table.shape[0]
+    dim = 1 if table.dim() == 1 else table.shape[1]
+    n = ids.numel()
+    L = _lib.lib()
+    if ws is None:
+        ws = _ws(L.tfs_scatter_add_sgd_workspace_bytes(n, dim), table.device)
+    check(L.tfs_scatter_add_sgd(_p(table), rows, dim, _p(ids), _p(grad), n, float(lr),
+                                _p(table2), _p(grad2), _p(ws), ws.numel(), _err(err), _stream()),
+          "tfs_scatter_add_sgd")
+    return table
+
+
+def debug_gemm_bf16(A, B, ksplit: int = 1):
+    """C[ks] = A . B^T on the tcgen05 path (diagnostics)."""
+    M, K = A.shape
+    N = B.shape[0]
+    C = torch.empty((max(ksplit, 1), M, N), dtype=torch.float32, device=A.device)
+    ks = ctypes.c_int32(0)
+    check(_lib.lib().tfs_debug_gemm_bf16(_p(A), A.stride(0), _p(B), B.stride(0), M, N, K, ksplit,
+                                         _p(C), ctypes.byref(ks), _stream()), "tfs_debug_gemm_bf16")
+    return C[: ks.value]
