@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark: words/sec of the embed + sampled-softmax training step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload X] [--impl tfs|reference]
+
+One JSON line on rank 0.  A "step" is one pass of the whole hot path of SURVEY §8(a) -- sample,
+Part, route, Gather, route back, Stitch, sampled-softmax forward + backward, sort-reduce, route,
+ScatterAdd-SGD -- over one synthetic batch of B tokens per GPU (weak scaling: B fixed per GPU).
+Default workload X: V = 800,000, d = 512, B = 2,560 (128 x 20) per GPU, S = 8,192 per GPU,
+Zipf(1.0) ids, bf16 tensor-core operands with fp32 accumulation and fp32 master tables.
+
+Timing: W untimed warm-up steps; K timed steps, each preceded by an L2 flush (a 256 MiB write,
+outside the timed interval); per-step CUDA events on the launching stream; barrier + sync on
+both sides; max over ranks.  value = N*B*K / max-rank time.  e2e: the same K steps through the
+public API with the inputs copied from pinned host memory and the loss read back every step.
+``--impl reference`` times the CPU oracle (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "words/sec for embed+sampled-softmax step at 1/2/4/8 B200; HBM GB/s"
+UNIT = "words/sec"
+N_BATCHES = 16
+FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--workload", default="X", choices=sorted(workloads.WORKLOADS))
+    p.add_argument("--impl", default="tfs", choices=["tfs", "reference"])
+    p.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graph")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--phase-steps", type=int, default=20, help="instrumented eager steps")
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Polls NVML every 5 ms for SM clock and throttle reasons (start before, stop after)."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, torch_device):
+        self.samples = []
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            props = torch.cuda.get_device_properties(torch_device)
+            h = None
+            try:
+                bus = "%08x:%02x:%02x.0" % (props.pci_domain_id, props.pci_bus_id,
+                                           props.pci_device_id)
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(torch_device.index or 0)
+            self.h = h
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report it, never fake numbers
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.time(), sm, r))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if not self.ok:
+            return
+        self.stop = False
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def finish(self, t0, t1):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "NVML unavailable"}
+        self.stop = True
+        self.t.join()
+        win = [s for s in self.samples if t0 <= s[0] <= t1] or self.samples
+        busy = [s for s in win if not (s[2] & 0x1)] or win
+        reasons = set()
+        for _, _, r in busy:
+            for bit, name in self.REASONS.items():
+                if r & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([s[1] for s in busy]) if busy else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(busy)}
+
+
+# ---------------------------------------------------------------------------- oracle timing
+def oracle_steps(w, n_steps, tokens, log=None):
+    """The CPU oracle (oracle/step.py, single-threaded C++ + numpy glue) on a bounded sample:
+    `tokens` of the B tokens of each batch, full V / S / d.  Returns (words, seconds)."""
+    import oracle  # noqa: F401  (test infrastructure: bench's cpu_baseline / reference legs)
+    from oracle import step as ostep
+    E, W, b = workloads.tables(w.vocab, w.dim)
+    cfg = ostep.StepConfig(vocab=w.vocab, dim=w.dim, num_sampled=w.num_sampled or w.vocab,
+                           num_shards=1, lr=0.1, seed=workloads.SAMPLER_SEED,
+                           full_softmax=(w.num_sampled == 0), inplace=True)
+    words = 0
+    secs = 0.0
+    for i in range(n_steps):
+        x, y = workloads.batch(w, 1, 0, step=i % N_BATCHES)
+        cfg.step = i
+        t = time.perf_counter()
+        E, W, b, _ = ostep.step(E, W, b, [x[:tokens]], [y[:tokens]], cfg)
+        secs += time.perf_counter() - t
+        words += tokens
+    return words, secs
+
+
+def run_reference(args):
+    """Reference arm: the oracle as it stands, on host cores, same metric/unit/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = workloads.WORKLOADS[args.workload]
+    tokens = 16
+    oracle_steps(w, args.warmup, tokens)
+    words, secs = oracle_steps(w, args.steps, tokens)
+    value = words / secs
+    sample = (f"{tokens} of {w.tokens_per_replica(1)} tokens per step, V={w.vocab}, "
+              f"d={w.dim}, S={w.num_sampled or w.vocab}; single-threaded oracle")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "vocab": w.vocab, "dim": w.dim,
+                       "tokens_per_step": tokens, "num_sampled": w.num_sampled},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------- GPU timing
+def graph_kernel_nodes(graph):
+    """Number of kernel nodes in a captured CUDA graph (cuda-python), or None."""
+    try:
+        from cuda.bindings import runtime as rt
+        g = graph.raw_cuda_graph()
+        err, _, n = rt.cudaGraphGetNodes(g, 0)
+        err, nodes, n = rt.cudaGraphGetNodes(g, n)
+        k = 0
+        for nd in nodes:
+            err, t = rt.cudaGraphNodeGetType(nd)
+            if t == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+                k += 1
+        return k
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_1605_08695_b200 import _lib, ops
+    from paper_1605_08695_b200 import step as gstep
+    from paper_1605_08695_b200._lib import TFS_BF16, TFS_F32
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    router = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        router = gstep.Router()
+    w = workloads.WORKLOADS[args.workload]
+    R = world
+    B = w.tokens_per_replica(R)
+    S = w.num_sampled
+    d = w.dim
+    dtype = TFS_BF16 if args.dtype == "bf16" else TFS_F32
+    cfg = gstep.StepConfig(vocab=w.vocab, dim=d, tokens=B, num_sampled=S, lr=0.1,
+                           seed=workloads.SAMPLER_SEED, operand_dtype=dtype,
+                           full_softmax=(S == 0))
+    E, W, b = workloads.tables_device(w.vocab, d, R, rank, dev)
+    st = gstep.ShardedStep(cfg, E, W, b, router)
+    # 16 distinct pre-generated batches per rank, resident in HBM and in pinned host memory.
+    xs_h, ys_h = [], []
+    for i in range(N_BATCHES):
+        x, y = workloads.batch(w, R, rank, step=i)
+        xs_h.append(torch.from_numpy(x).pin_memory())
+        ys_h.append(torch.from_numpy(y).pin_memory())
+    xs_d = [t.to(dev) for t in xs_h]
+    ys_d = [t.to(dev) for t in ys_h]
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    use_graph = (R == 1) and not args.no_graph
+    L = _lib.lib()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- one counted eager step: how many libtfs kernels a step launches
+    c0 = L.tfs_debug_launch_count()
+    st.run(xs_d[0], ys_d[0], 0)
+    torch.cuda.synchronize()
+    launches_per_step = L.tfs_debug_launch_count() - c0
+    st.err.check("bench step")
+    step_no = 1
+
+    if use_graph:
+        st.x.copy_(xs_d[0])
+        st.y.copy_(ys_d[0])
+        st.capture(first_step=step_no)
+        kernel_nodes = graph_kernel_nodes(st.graph)
+
+    def one_step(i):
+        nonlocal step_no
+        if use_graph:
+            st.x.copy_(xs_d[i % N_BATCHES])
+            st.y.copy_(ys_d[i % N_BATCHES])
+            out = st.replay()
+        else:
+            out = st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], step_no)
+        step_no += 1
+        return out
+
+    for i in range(args.warmup):
+        one_step(i)
+    barrier()
+
+    # ---- timed region: K steps, L2 flushed before each (outside the events)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    t_wall0 = time.time()
+    for i in range(args.steps):
+        flush.zero_()
+        starts[i].record()
+        one_step(i)
+        ends[i].record()
+    barrier()
+    t_wall1 = time.time()
+    per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    local_ms = sum(per_step)
+    clk = clocks.finish(t_wall0, t_wall1)
+    if world > 1:
+        tt = torch.tensor([local_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    else:
+        total_ms = local_ms
+    st.err.check("bench timed steps")
+    words = R * B * args.steps
+    value = words / (total_ms / 1e3)
+
+    # ---- e2e: public API with host buffers (H2D of x, y and D2H of the loss every step)
+    loss_host = torch.empty(args.steps, dtype=torch.float32).pin_memory()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        if use_graph:
+            st.x.copy_(xs_h[i % N_BATCHES], non_blocking=True)
+            st.y.copy_(ys_h[i % N_BATCHES], non_blocking=True)
+            out = st.replay()
+        else:
+            xd = xs_h[i % N_BATCHES].to(dev, non_blocking=True)
+            yd = ys_h[i % N_BATCHES].to(dev, non_blocking=True)
+            out = st.run(xd, yd, step_no)
+        step_no += 1
+        loss_host[i:i + 1].copy_(out, non_blocking=True)
+    e1.record()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    assert np.all(np.isfinite(loss_host.numpy()))
+    e2e_value = words / (e2e_ms / 1e3)
+
+    # ---- instrumented eager steps: per-phase device time (roofline of the dominant op)
+    phases = {}
+    n_ph = max(1, min(args.phase_steps, args.steps))
+    if R == 1:
+        st.phase_events = []
+        for i in range(n_ph):
+            flush.zero_()
+            st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], step_no)
+            step_no += 1
+        torch.cuda.synchronize()
+        for name, s_, e_ in st.phase_events:
+            phases.setdefault(name, []).append(s_.elapsed_time(e_))
+        st.phase_events = None
+        phases = {k: sum(v) / len(v) for k, v in phases.items()}
+    st.err.check("bench instrumented steps")
+
+    peaks, peak_src = load_peaks()
+    roofline = None
+    if "sampled_softmax" in phases:
+        flop = 6.0 * B * S * d
+        t = phases["sampled_softmax"] / 1e3
+        achieved = flop / t / 1e12
+        peak = peaks.get("bf16_tflops_sustained", 1407.0)
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic_ssm.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(args.workload)
+            except Exception:
+                traffic = None
+        roofline = {"kernel": "tfs_sampled_softmax_fwd_bwd (4 tcgen05 GEMM passes + epilogues)",
+                    "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "peak_source": f"{peak_src} bf16 sustained",
+                    "algorithmic": "6*B*S*d flops per launch (3 GEMMs; the logits recompute "
+                                   "is overhead)",
+                    "ms": phases["sampled_softmax"]}
+    hbm = None
+    if "gather" in phases and "scatter_sgd" in phases:
+        # algorithmic bytes: gather reads n ids + n rows and writes n rows (fp32, d floats);
+        # scatter-SGD reads grad rows + table rows and writes table rows of the unique ids.
+        row = 4 * d
+        n_g = 2 * B + S
+        g_bytes = n_g * 8 + 2 * n_g * row + 2 * (B + S) * 4
+        t_g = phases["gather"] / 1e3
+        hbm = {"gather_GBps": g_bytes / t_g / 1e9,
+               "gather_frac": g_bytes / t_g / 1e9 / peaks.get("hbm_gbs", 6538.6),
+               "peak": peaks.get("hbm_gbs", 6538.6), "unit": "GB/s"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tokens = 128
+        words_o, secs_o = oracle_steps(w, 3, tokens)
+        cpu = {"value": words_o / secs_o, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"3 oracle steps of {tokens} of the {B} tokens of a batch (full "
+                         f"V={w.vocab}, S={S or w.vocab}, d={d}); single-threaded C++ oracle "
+                         f"+ numpy glue; {secs_o:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": args.workload, "vocab": w.vocab, "dim": d,
+                       "tokens_per_gpu": B, "global_batch": R * B, "num_sampled": S,
+                       "zipf_s": w.zipf_s, "parallelism": f"vocab-sharded x{R} (ids mod R), "
+                       f"data-parallel x{R}", "l2": "flushed before every timed step "
+                       "(256 MiB write outside the timed interval)",
+                       "cuda_graph": use_graph, "batches": N_BATCHES},
+            "clocks": clk,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * B * 8,
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches_per_step": launches_per_step,
+            "roofline": roofline,
+            "hbm": hbm,
+            "phases_ms": phases,
+            "per_step_ms_p10_p50_p90": [float(np.percentile(per_step, q)) for q in (10, 50, 90)],
+            "cpu_baseline": cpu,
+        }
+        if use_graph:
+            line["graph_kernel_nodes"] = kernel_nodes
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -219,6 +219,10 @@ int32_t tfs_scatter_add_sgd(float* table, int64_t rows, int32_t dim, const int64
 int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
                             int32_t N, int32_t K, int32_t ksplit, float* C, int32_t* out_ksplit,
                             void* stream);
+/* Total number of CUDA kernels this process has launched through libtfs (host counter,
+ * incremented at every launch site; graph replays are not counted).  Used by bench.py to
+ * report gpu_launches. */
+int64_t tfs_debug_launch_count(void);
 
 #ifdef __cplusplus
 }

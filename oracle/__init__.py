@@ -222,9 +222,13 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
     return out
 
 
-def scatter_add_sgd(table, ids, grad, lr):
-    """Sparse SGD.  Returns the updated COPY of table."""
-    table = np.array(table, dtype=np.float32, copy=True, order="C")
+def scatter_add_sgd(table, ids, grad, lr, inplace=False):
+    """Sparse SGD.  Returns the updated COPY of table (or updates a
+    C-contiguous float32 `table` in place when inplace=True -- same arithmetic)."""
+    if inplace:
+        assert table.dtype == np.float32 and table.flags["C_CONTIGUOUS"]
+    else:
+        table = np.array(table, dtype=np.float32, copy=True, order="C")
     rows = table.shape[0]
     dim = 1 if table.ndim == 1 else table.shape[1]
     ids = _c(ids, np.int64)

@@ -32,6 +32,7 @@ class StepConfig:
     flags: int = SUBTRACT_LOG_Q | REMOVE_ACCIDENTAL_HITS
     bf16: bool = False
     full_softmax: bool = False   # candidates = all V classes, no sampler (config F)
+    inplace: bool = False        # update E, W, b in place (same arithmetic; saves table copies)
 
 
 @dataclass
@@ -141,7 +142,7 @@ def step(E, W, b, xs, ys, cfg: StepConfig):
         g_b.append(np.concatenate([t.ssm["db_true"], t.ssm["db_s"]]))
 
     # O13 one synchronous SGD apply of the summed sparse gradient.
-    E2 = scatter_add_sgd(E, np.concatenate(ids_e), np.concatenate(g_e), cfg.lr)
-    W2 = scatter_add_sgd(W, np.concatenate(ids_w), np.concatenate(g_w), cfg.lr)
-    b2 = scatter_add_sgd(b, np.concatenate(ids_w), np.concatenate(g_b), cfg.lr)
+    E2 = scatter_add_sgd(E, np.concatenate(ids_e), np.concatenate(g_e), cfg.lr, cfg.inplace)
+    W2 = scatter_add_sgd(W, np.concatenate(ids_w), np.concatenate(g_w), cfg.lr, cfg.inplace)
+    b2 = scatter_add_sgd(b, np.concatenate(ids_w), np.concatenate(g_b), cfg.lr, cfg.inplace)
     return E2, W2, b2, traces

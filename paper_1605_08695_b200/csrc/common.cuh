@@ -17,6 +17,7 @@ constexpr int kNumSMsB200 = 148;
 void set_last_error(const char* where, cudaError_t e);
 int32_t device_supported();  // TFS_OK on sm_100, else TFS_ERR_UNSUPPORTED (cached per device)
 int num_sms();               // SM count of the current device (cached)
+void launched(int n = 1);    // count kernel launches (tfs_debug_launch_count)
 
 #define TFS_CUDA_TRY(expr)                                \
   do {                                                    \

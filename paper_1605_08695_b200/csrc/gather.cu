@@ -5,6 +5,7 @@
 // accesses (a 512-wide fp32 row is 128 float4 = 4 per lane), two rows in flight per warp, and
 // a grid of 8 CTAs x 8 warps per SM so ~64 KB of loads are outstanding per SM.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -14,6 +15,9 @@
 namespace tfs {
 
 static thread_local char g_last_error[512] = {0};
+static std::atomic<long long> g_launches{0};
+
+void launched(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_last_error(const char* where, cudaError_t e) {
   snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%s)", where, cudaGetErrorName(e),
@@ -205,6 +209,8 @@ using namespace tfs;
 
 extern "C" int32_t tfs_version(void) { return 100; }
 
+extern "C" int64_t tfs_debug_launch_count(void) { return g_launches.load(); }
+
 extern "C" const char* tfs_status_string(int32_t s) {
   switch (s) {
     case TFS_OK: return "ok";
@@ -259,6 +265,7 @@ extern "C" int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int3
     else
       gather_scalar_kernel<false><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
   }
+  ::tfs::launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }
@@ -281,17 +288,17 @@ extern "C" int32_t tfs_stitch(const int64_t* positions, const void* rows, int64_
     claim = (unsigned long long*)ws;
     TFS_CUDA_TRY(cudaMemsetAsync(claim, 0xff, sizeof(unsigned long long) * n, st));
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4ll * num_sms()));
-    stitch_claim_kernel<<<g, 256, 0, st>>>(positions, n, claim, err);
+    stitch_claim_kernel<<<g, 256, 0, st>>>(positions, n, claim, err); ::tfs::launched();
   }
   const bool vec = row_bytes % 16 == 0 && ((uintptr_t)rows % 16 == 0) && ((uintptr_t)out % 16 == 0);
   if (vec) {
     stitch_vec4_kernel<<<grid_for_rows(n, 1), 256, 0, st>>>(
-        positions, (const uint4*)rows, n, row_bytes / 16, (uint4*)out, claim, err);
+        positions, (const uint4*)rows, n, row_bytes / 16, (uint4*)out, claim, err); ::tfs::launched();
   } else {
     const int64_t words = row_bytes / 4;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * words, 256), 8ll * num_sms()));
     stitch_word_kernel<<<g, 256, 0, st>>>(positions, (const uint32_t*)rows, n, words,
-                                          (uint32_t*)out, claim, err);
+                                          (uint32_t*)out, claim, err); ::tfs::launched();
   }
   TFS_LAUNCH_CHECK();
   return TFS_OK;

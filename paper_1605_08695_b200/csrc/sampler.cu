@@ -284,12 +284,12 @@ extern "C" int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int3
   SamplerState s = carve_state((void*)state, vocab);
   const double log_v1 = std::log((double)vocab + 1.0);
   if (num_sampled == 0) {
-    set_i64_kernel<<<1, 1, 0, st>>>(out_num_tries, 0);
+    set_i64_kernel<<<1, 1, 0, st>>>(out_num_tries, 0); ::tfs::launched();
   } else if (!unique) {
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(num_sampled, 256), 4 * num_sms()));
     sample_draw_kernel<<<g, 256, 0, st>>>(s.thr, vocab, log_v1, num_sampled, seed, step, step_dev, replica,
-                                          0, nullptr, nullptr, out_sampled);
-    set_i64_kernel<<<1, 1, 0, st>>>(out_num_tries, num_sampled);
+                                          0, nullptr, nullptr, out_sampled); ::tfs::launched();
+    set_i64_kernel<<<1, 1, 0, st>>>(out_num_tries, num_sampled); ::tfs::launched();
   } else {
     if (ws_bytes < tfs_sampler_workspace_bytes(max_draws)) return TFS_ERR_WORKSPACE_TOO_SMALL;
     Carver c(ws, ws_bytes);
@@ -298,17 +298,17 @@ extern "C" int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int3
     uint32_t* blk = c.take<uint32_t>(nblk + 1);
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(max_draws, 256), 4 * num_sms()));
     sample_draw_kernel<<<g, 256, 0, st>>>(s.thr, vocab, log_v1, max_draws, seed, step, step_dev, replica,
-                                          1, draws, s.firstpos, nullptr);
-    sample_count_kernel<<<nblk, kSelThreads, 0, st>>>(draws, s.firstpos, max_draws, blk);
+                                          1, draws, s.firstpos, nullptr); ::tfs::launched();
+    sample_count_kernel<<<nblk, kSelThreads, 0, st>>>(draws, s.firstpos, max_draws, blk); ::tfs::launched();
     sample_select_kernel<<<nblk, kSelThreads, 0, st>>>(draws, s.firstpos, max_draws, blk, nblk,
-                                                       num_sampled, out_sampled, out_num_tries, err);
+                                                       num_sampled, out_sampled, out_num_tries, err); ::tfs::launched();
     TFS_LAUNCH_CHECK();
     const int64_t total = std::max<int64_t>(max_draws, num_sampled + n_labels);
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 4 * num_sms()));
     sample_finish_kernel<<<g2, 256, 0, st>>>(draws, s.firstpos, max_draws, 1, vocab, log_v1,
                                              num_sampled, out_sampled, labels, n_labels,
                                              out_num_tries, out_log_ec_sampled, out_log_ec_labels,
-                                             err);
+                                             err); ::tfs::launched();
     TFS_LAUNCH_CHECK();
     return TFS_OK;
   }
@@ -318,7 +318,7 @@ extern "C" int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int3
     sample_finish_kernel<<<g2, 256, 0, st>>>(nullptr, nullptr, 0, unique, vocab, log_v1,
                                              num_sampled, out_sampled, labels, n_labels,
                                              out_num_tries, out_log_ec_sampled, out_log_ec_labels,
-                                             err);
+                                             err); ::tfs::launched();
   }
   TFS_LAUNCH_CHECK();
   return TFS_OK;

@@ -59,7 +59,7 @@ static int32_t launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const S
                                       (int)kSmemBytes));
     attr_done = true;
   }
-  gemm_kernel<MODE><<<grid, kThreads, kSmemBytes, st>>>(ta, tb, g, ep);
+  gemm_kernel<MODE><<<grid, kThreads, kSmemBytes, st>>>(ta, tb, g, ep); ::tfs::launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }
@@ -414,21 +414,21 @@ static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     SimtParams p{a->b_s, le_s, a->sampled, a->labels, hits, nullptr, nullptr, w.Z, S};
     dim3 grid((unsigned)cdiv(S, 64), (unsigned)cdiv(B, 64));
     simt_gemm_kernel<kSimtLogits><<<grid, 256, 0, st>>>((int)B, (int)S, d, a->h, d, 1, a->w_s, 1,
-                                                         d, p);
+                                                         d, p); ::tfs::launched();
   }
   f32_row_kernel<<<(unsigned)B, 256, 0, st>>>(S, d, a->h, a->w_true, a->b_true, le_t,
                                               a->grad_scale, w.Z, S, a->loss, a->lse, a->dw_true,
-                                              a->db_true);
+                                              a->db_true); ::tfs::launched();
   {  // dh = G W_s + g * w_true
     SimtParams p{nullptr, nullptr, nullptr, nullptr, 0, a->db_true, a->w_true, a->dh, d};
     dim3 grid((unsigned)cdiv(d, 64), (unsigned)cdiv(B, 64));
-    simt_gemm_kernel<kSimtDh><<<grid, 256, 0, st>>>((int)B, d, (int)S, w.Z, S, 1, a->w_s, d, 1, p);
+    simt_gemm_kernel<kSimtDh><<<grid, 256, 0, st>>>((int)B, d, (int)S, w.Z, S, 1, a->w_s, d, 1, p); ::tfs::launched();
   }
   if (S > 0) {  // dW_s = G^T h ; db_s = column sums of G
     SimtParams p{nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, a->dw_s, d};
     dim3 grid((unsigned)cdiv(d, 64), (unsigned)cdiv(S, 64));
-    simt_gemm_kernel<kSimtStore><<<grid, 256, 0, st>>>((int)S, d, (int)B, w.Z, 1, S, a->h, d, 1, p);
-    colsum_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.Z, B, S, S, a->db_s);
+    simt_gemm_kernel<kSimtStore><<<grid, 256, 0, st>>>((int)S, d, (int)B, w.Z, 1, S, a->h, d, 1, p); ::tfs::launched();
+    colsum_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.Z, B, S, S, a->db_s); ::tfs::launched();
   }
   TFS_LAUNCH_CHECK();
   return TFS_OK;
@@ -446,10 +446,11 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
 
   // Operands: bf16 copies in both layouts (each GEMM reads K-major tiles).
   to_bf16_and_transpose_kernel<<<dim3((unsigned)cdiv(d, 32), (unsigned)cdiv(B, 32)), 256, 0, st>>>(
-      a->h, B, d, w.hb, w.hT, w.Bp);
-  if (S > 0)
+      a->h, B, d, w.hb, w.hT, w.Bp); ::tfs::launched();
+  if (S > 0) {
     to_bf16_and_transpose_kernel<<<dim3((unsigned)cdiv(d, 32), (unsigned)cdiv(S, 32)), 256, 0,
-                                   st>>>(a->w_s, S, d, w.wsb, w.wsT, w.Sp);
+                                   st>>>(a->w_s, S, d, w.wsb, w.wsT, w.Sp); ::tfs::launched();
+  }
   TFS_LAUNCH_CHECK();
 
   umma::EpiParams ep{};
@@ -466,7 +467,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   }
   bf16_combine_kernel<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(
       B, d, a->h, a->w_true, a->b_true, le_t, w.stats, 2 * num_n, a->grad_scale, a->loss,
-      a->lse, a->dw_true, a->db_true);
+      a->lse, a->dw_true, a->db_true); ::tfs::launched();
   TFS_LAUNCH_CHECK();
   // lse is needed by pass 2: use the caller's buffer if given, else scratch in dh_part's tail.
   if (S > 0) {  // pass 2: G = c exp(Z - lse) -> bf16 G, G^T; column partial sums for db_s
@@ -479,7 +480,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     ep.dbs_part = w.dbs_part;
     rc = umma::launch(umma::kGrad, w.hb, d, w.wsb, d, (int)B, (int)S, d, 1, ep, st, nullptr);
     if (rc != TFS_OK) return rc;
-    dbs_finalize_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.dbs_part, 4 * num_m, S, a->db_s);
+    dbs_finalize_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.dbs_part, 4 * num_m, S, a->db_s); ::tfs::launched();
   }
   // dh = G W_s (split-K partials) + g * bf16(w_true)
   int ks = 1;
@@ -494,7 +495,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     TFS_CUDA_TRY(cudaMemsetAsync(w.dh_part, 0, sizeof(float) * B * d, st));
   }
   dh_finalize_kernel<<<grid1d(B * d), 256, 0, st>>>(w.dh_part, ks, B * d, B, d, a->db_true,
-                                                    a->w_true, a->dh);
+                                                    a->w_true, a->dh); ::tfs::launched();
   // dW_s = G^T h
   if (S > 0) {
     umma::EpiParams e3{};
@@ -506,8 +507,9 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     rc = umma::launch(umma::kStore, w.GT, w.Bp, w.hT, w.Bp, (int)S, d, (int)B, w.ks_dws, e3, st,
                       &ks2);
     if (rc != TFS_OK) return rc;
-    if (split)
-      split_sum_kernel<<<grid1d(S * d), 256, 0, st>>>(w.dws_part, ks2, S * d, S * d, a->dw_s);
+    if (split) {
+      split_sum_kernel<<<grid1d(S * d), 256, 0, st>>>(w.dws_part, ks2, S * d, S * d, a->dw_s); ::tfs::launched();
+    }
   }
   TFS_LAUNCH_CHECK();
   return TFS_OK;
@@ -554,7 +556,7 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
   if (rc != TFS_OK) return rc;
   if (a->loss_sum) {
     TFS_REQUIRE(a->loss != nullptr);
-    loss_sum_kernel<<<1, 256, 0, st>>>(a->loss, a->B, a->grad_scale, a->loss_sum);
+    loss_sum_kernel<<<1, 256, 0, st>>>(a->loss, a->B, a->grad_scale, a->loss_sum); ::tfs::launched();
     TFS_LAUNCH_CHECK();
   }
   return TFS_OK;

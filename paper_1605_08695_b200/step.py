@@ -21,6 +21,7 @@ device memory, advanced inside the graph).  With R > 1 each route needs its coun
 """
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 
 import torch
@@ -77,6 +78,24 @@ class Router:
         return out
 
 
+class _PhaseTimer:
+    SPIN_CYCLES = 200_000  # ~0.1 ms at 1.9 GHz: lets the host queue the phase ahead
+
+    def __init__(self, st, name):
+        self.st, self.name = st, name
+
+    def __enter__(self):
+        torch.cuda._sleep(self.SPIN_CYCLES)
+        self.start = torch.cuda.Event(enable_timing=True)
+        self.end = torch.cuda.Event(enable_timing=True)
+        self.start.record()
+
+    def __exit__(self, *exc):
+        self.end.record()
+        self.st.phase_events.append((self.name, self.start, self.end))
+        return False
+
+
 class ShardedStep:
     """Owns rank r's shard of E, W, b and the per-step buffers; ``run`` does one step."""
 
@@ -120,6 +139,8 @@ class ShardedStep:
         self.part_x = (torch.empty(B, **i64), torch.empty(B, **i64), torch.empty(R, **i64))
         self.part_w = (torch.empty(B + S, **i64), torch.empty(B + S, **i64), torch.empty(R, **i64))
         self.ws_part = ops._ws(L.tfs_partition_workspace_bytes(B + S, R), dev)
+        self.ws_part_x = ops._ws(L.tfs_partition_workspace_bytes(B, R), dev)
+        self.side_stream = torch.cuda.Stream(device=dev)
         self.h = torch.empty((B, d), **f32)
         self.w_rows = torch.empty((B + S, d), **f32)
         self.b_rows = torch.empty(B + S, **f32)
@@ -144,7 +165,7 @@ class ShardedStep:
             self.sr_w = (torch.empty(B + S, **i64), torch.empty((B + S, d), **f32),
                          torch.empty(B + S, **f32), torch.empty(R, **i64), torch.empty(1, **i64))
         self.graph = None
-        self.launches_per_step = None
+        self.phase_events = None  # list of (phase, start, end) when instrumented
 
     # ------------------------------------------------------------------------------------------
     def _sample(self, step: int | None):
@@ -163,24 +184,76 @@ class ShardedStep:
                             operand_dtype=self.cfg.operand_dtype, out=self.ssm_out,
                             ws=self.ws_ssm)
 
+    def _ph(self, name: str):
+        """Phase marker: with ``self.phase_events`` set (bench instrumentation, eager only) the
+        phase is bracketed by CUDA events on the current stream, preceded by a short device
+        spin so the host has queued the whole phase before its start event fires."""
+        if self.phase_events is None:
+            return contextlib.nullcontext()
+        return _PhaseTimer(self, name)
+
     def _local_step(self, step: int | None):
-        """R = 1: every route is the identity (send buffer == receive buffer)."""
+        """R = 1: every route is the identity (send buffer == receive buffer).
+
+        The embedding lookup (E) and the softmax-row lookup (W, b) are independent until the
+        sampled softmax, and so are their sparse updates afterwards: outside instrumentation
+        the E path runs on a side stream concurrently with the W path (fork / join through
+        stream waits, which CUDA-graph capture records as graph edges)."""
+        if self.phase_events is not None:
+            return self._local_step_serial(step)
         V, B = self.cfg.vocab, self.B
-        self.qw[:B].copy_(self.y)
+        main = torch.cuda.current_stream()
+        side = self.side_stream
+        side.wait_stream(main)
+        with torch.cuda.stream(side):                      # E path
+            xl, xpos, _ = ops.partition(self.x, V, 1, err=self.err, out=self.part_x,
+                                        ws=self.ws_part_x)
+            ops.gather(self.E, xl, out=self.rows_e, err=self.err)
+            ops.stitch(xpos, self.rows_e, out=self.h)
+        self.qw[:B].copy_(self.y)                          # W path
         self._sample(step)
-        xl, xpos, _ = ops.partition(self.x, V, 1, err=self.err, out=self.part_x, ws=self.ws_part)
-        wl, wpos, _ = ops.partition(self.qw, V, 1, err=self.err, out=self.part_w, ws=self.ws_part)
-        ops.gather(self.E, xl, out=self.rows_e, err=self.err)
+        wl, wpos, _ = ops.partition(self.qw, V, 1, err=self.err, out=self.part_w,
+                                    ws=self.ws_part)
         ops.gather(self.W, wl, out=self.rows_w, err=self.err)
         ops.gather(self.b, wl, out=self.rows_b, err=self.err)
-        ops.stitch(xpos, self.rows_e, out=self.h)
         ops.stitch(wpos, self.rows_w, out=self.w_rows)
         ops.stitch(wpos, self.rows_b.view(-1), out=self.b_rows)
+        main.wait_stream(side)
         self._softmax()
-        ops.scatter_add_sgd(self.E, self.x, self.ssm_out["dh"], self.cfg.lr, err=self.err,
-                            ws=self.ws_sgd_e)
-        ops.scatter_add_sgd(self.W, self.qw, self.dw, self.cfg.lr, table2=self.b, grad2=self.db,
-                            err=self.err, ws=self.ws_sgd_w)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            ops.scatter_add_sgd(self.E, self.x, self.ssm_out["dh"], self.cfg.lr, err=self.err,
+                                ws=self.ws_sgd_e)
+        ops.scatter_add_sgd(self.W, self.qw, self.dw, self.cfg.lr, table2=self.b,
+                            grad2=self.db, err=self.err, ws=self.ws_sgd_w)
+        main.wait_stream(side)
+
+    def _local_step_serial(self, step: int | None):
+        """The same step on one stream, bracketed into phases (bench instrumentation)."""
+        V, B = self.cfg.vocab, self.B
+        with self._ph("sample"):
+            self.qw[:B].copy_(self.y)
+            self._sample(step)
+        with self._ph("partition"):
+            xl, xpos, _ = ops.partition(self.x, V, 1, err=self.err, out=self.part_x,
+                                        ws=self.ws_part_x)
+            wl, wpos, _ = ops.partition(self.qw, V, 1, err=self.err, out=self.part_w,
+                                        ws=self.ws_part)
+        with self._ph("gather"):
+            ops.gather(self.E, xl, out=self.rows_e, err=self.err)
+            ops.gather(self.W, wl, out=self.rows_w, err=self.err)
+            ops.gather(self.b, wl, out=self.rows_b, err=self.err)
+        with self._ph("stitch"):
+            ops.stitch(xpos, self.rows_e, out=self.h)
+            ops.stitch(wpos, self.rows_w, out=self.w_rows)
+            ops.stitch(wpos, self.rows_b.view(-1), out=self.b_rows)
+        with self._ph("sampled_softmax"):
+            self._softmax()
+        with self._ph("scatter_sgd"):
+            ops.scatter_add_sgd(self.E, self.x, self.ssm_out["dh"], self.cfg.lr, err=self.err,
+                                ws=self.ws_sgd_e)
+            ops.scatter_add_sgd(self.W, self.qw, self.dw, self.cfg.lr, table2=self.b,
+                                grad2=self.db, err=self.err, ws=self.ws_sgd_w)
 
     def _dist_step(self, step: int | None):
         """R > 1: Part -> route -> Gather -> route back -> Stitch -> softmax -> sort-reduce ->
@@ -189,7 +262,8 @@ class ShardedStep:
         rt = self.router
         self.qw[:B].copy_(self.y)
         self._sample(step)
-        xl, xpos, xcnt = ops.partition(self.x, V, R, err=self.err, out=self.part_x, ws=self.ws_part)
+        xl, xpos, xcnt = ops.partition(self.x, V, R, err=self.err, out=self.part_x,
+                                       ws=self.ws_part_x)
         wl, wpos, wcnt = ops.partition(self.qw, V, R, err=self.err, out=self.part_w, ws=self.ws_part)
         (sx, sw), (rx, rw) = rt.exchange_counts(torch.stack([xcnt, wcnt], dim=1))
         ids_x = rt.route(xl, sx, rx)

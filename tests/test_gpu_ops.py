@@ -283,3 +283,30 @@ def test_scatter_add_sgd_errors_and_empty():
     ops.scatter_add_sgd(table, T(ids), T(np.ones((5, 4), np.float32)), 1.0, err=err)
     assert err.read() == (2, 2)
     assert table[1].tolist() == [-1.0] * 4 and table[3].tolist() == [-1.0] * 4
+
+
+@pytest.mark.parametrize("dim", [512, 6])
+def test_heavy_hitter_segments(dim):
+    """One id repeated 15,000 times plus a Zipf tail: exercises the piece path (segments of more
+    than 32 rows summed as 64-row pieces combined in piece order)."""
+    rows_t, n = 3000, 20000
+    rng = np.random.default_rng(dim)
+    ids = workloads.zipf_ids(rng, rows_t, 1.2, n)
+    ids[rng.permutation(n)[:15000]] = 5
+    table = rng.standard_normal((rows_t, dim)).astype(np.float32)
+    g = rng.standard_normal((n, dim)).astype(np.float32)
+    dt = T(table)
+    ops.scatter_add_sgd(dt, T(ids), T(g), 0.5)
+    ref = oracle.scatter_add_sgd(table, ids, g.astype(np.float64), 0.5)
+    touched = np.unique(ids)
+    got = dt.cpu().numpy()
+    assert rel(got[touched] - table[touched], ref[touched] - table[touched]) <= 1e-5
+    local, sums, _, counts, U = ops.sort_reduce(T(ids), rows_t, 4, T(g))
+    ol, osum, oc = oracle.sort_reduce(ids, 4, g.astype(np.float64))
+    u = int(U.item())
+    assert np.array_equal(local[:u].cpu().numpy(), ol) and np.array_equal(counts.cpu().numpy(), oc)
+    assert rel(sums[:u].cpu().numpy(), osum) <= 1e-5
+    # determinism of the piece path
+    dt2 = T(table)
+    ops.scatter_add_sgd(dt2, T(ids), T(g), 0.5)
+    assert torch.equal(dt.cpu(), dt2.cpu())

@@ -74,3 +74,22 @@ def tables(vocab: int, dim: int, seed: int = TABLE_SEED):
     b = (rng.random(vocab, dtype=np.float32) - np.float32(0.5)) * np.float32(0.2)
     return E, W, b
 
+
+
+def shard_rows_count(vocab: int, num_shards: int, shard: int) -> int:
+    """Rows of shard r under the id-mod-R layout: n_r = ceil((V - r) / R)."""
+    return -(-(vocab - shard) // num_shards)
+
+
+def tables_device(vocab: int, dim: int, num_shards: int, shard: int, device, seed: int = TABLE_SEED):
+    """Bench-scale variant of ``tables``: shard r's rows generated directly on the GPU with a
+    seeded torch generator (same distributions; a different stream of random numbers than the
+    numpy generator, so parity tests use ``tables``).  Returns (E_r, W_r, b_r)."""
+    import torch
+    n = shard_rows_count(vocab, num_shards, shard)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1000003 + shard)
+    E = torch.rand((n, dim), generator=g, device=device, dtype=torch.float32).sub_(0.5)
+    W = torch.rand((n, dim), generator=g, device=device, dtype=torch.float32).sub_(0.5)
+    b = torch.rand(n, generator=g, device=device, dtype=torch.float32).sub_(0.5).mul_(0.2)
+    return E, W, b
