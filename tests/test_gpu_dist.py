@@ -1,0 +1,86 @@
+"""Multi-GPU parity of the sharded step (R = 2 ranks over NCCL) against the oracle step with R
+simulated shards: sampled ids bit-exact per replica, per-token loss, and each rank's updated
+shard of E, W, b (normwise rel, R-19).  Needs >= 2 GPUs (gpurun --gpus 2); skipped otherwise."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def rel(g, o):
+    return float(np.max(np.abs(g - o)) / max(np.max(np.abs(o)), 1e-300)) if o.size else 0.0
+
+
+def _worker(rank, world, port, name, dtype, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import oracle  # noqa: F401
+    from oracle import step as ostep
+    import workloads
+    from paper_1605_08695_b200 import step as gstep
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        w = workloads.WORKLOADS[name]
+        V, R = w.vocab, world
+        E, W, b = workloads.tables(V, w.dim)
+        xs, ys = zip(*[workloads.batch(w, R, r) for r in range(R)])
+        cfg = gstep.StepConfig(vocab=V, dim=w.dim, tokens=xs[0].size, num_sampled=w.num_sampled,
+                               lr=1.0, seed=workloads.SAMPLER_SEED, operand_dtype=dtype)
+        st = gstep.ShardedStep(cfg, torch.from_numpy(E[rank::R].copy()).to(dev),
+                               torch.from_numpy(W[rank::R].copy()).to(dev),
+                               torch.from_numpy(b[rank::R].copy()).to(dev), gstep.Router())
+        st.run(torch.from_numpy(xs[rank]).to(dev), torch.from_numpy(ys[rank]).to(dev), 2)
+        torch.cuda.synchronize()
+        st.err.check("dist step")
+        ocfg = ostep.StepConfig(vocab=V, dim=w.dim, num_sampled=w.num_sampled, num_shards=R,
+                                lr=1.0, seed=workloads.SAMPLER_SEED, step=2, bf16=(dtype == 1))
+        E2, W2, b2, tr = ostep.step(E, W, b, list(xs), list(ys), ocfg)
+        B = xs[0].size
+        res = {"sampled": np.array_equal(st.qw[B:].cpu().numpy(), tr[rank].sampled),
+               "loss": rel(st.ssm_out["loss"].cpu().numpy(), tr[rank].ssm["loss"])}
+        for nm, T0, Tg, To in (("E", E, st.E, E2), ("W", W, st.W, W2), ("b", b, st.b, b2)):
+            g = Tg.cpu().numpy()
+            t0, to = T0[rank::R], To[rank::R]
+            touched = np.nonzero(np.any((to != t0).reshape(t0.shape[0], -1), axis=1))[0]
+            untouched = np.setdiff1d(np.arange(t0.shape[0]), touched)
+            res[nm + "_untouched"] = bool(np.array_equal(g[untouched], t0[untouched]))
+            res[nm] = rel(g[touched] - t0[touched], to[touched] - t0[touched])
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("name,dtype,tol", [("T", 0, 1e-5), ("L", 1, 2e-3)])
+def test_dist_step_matches_oracle(name, dtype, tol):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, dtype, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, r in res:
+        assert r["sampled"], rank
+        assert r["loss"] <= tol, (rank, r)
+        for nm in ("E", "W", "b"):
+            assert r[nm + "_untouched"], (rank, nm)
+            assert r[nm] <= tol, (rank, nm, r[nm])
