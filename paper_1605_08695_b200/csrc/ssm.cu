@@ -35,43 +35,51 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-int32_t make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t ld,
-                       uint32_t box_rows) {
+// Tensor map of one operand.  K-major [rows x K]: box {BK, box_rows}; MN-major [K x rows]:
+// box {64 (MN), BK} -- the kernel issues rows/64 such boxes per stage.  128-byte swizzle.
+static int32_t make_tmap(CUtensorMap* map, const Operand& op, uint64_t rows, uint64_t k,
+                         uint32_t box_rows) {
   auto fn = encode_fn();
   if (fn == nullptr) return TFS_ERR_CUDA;
-  cuuint64_t dims[2] = {k, rows};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  if (((uintptr_t)op.base & 15) != 0 || (op.ld * 2) % 16 != 0) return TFS_ERR_INVALID_ARGUMENT;
+  cuuint64_t dims[2], strides[1] = {(cuuint64_t)op.ld * 2};
+  cuuint32_t box[2], estr[2] = {1, 1};
+  if (op.mn) {
+    dims[0] = rows; dims[1] = k;
+    box[0] = kMNBox; box[1] = BK;
+  } else {
+    dims[0] = k; dims[1] = rows;
+    box[0] = BK; box[1] = box_rows;
+  }
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(op.base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? TFS_OK : TFS_ERR_INVALID_ARGUMENT;
 }
 
-template <int MODE>
+template <int MODE, bool A_MN, bool B_MN>
 static int32_t launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const Shape& g,
                            const EpiParams& ep, int grid, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE>,
+    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, A_MN, B_MN>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmemBytes));
     attr_done = true;
   }
-  gemm_kernel<MODE><<<grid, kThreads, kSmemBytes, st>>>(ta, tb, g, ep); ::tfs::launched();
+  gemm_kernel<MODE, A_MN, B_MN><<<grid, kThreads, kSmemBytes, st>>>(ta, tb, g, ep);
+  launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }
 
-// Returns the effective number of K splits in *ksplit_eff.
-int32_t launch(int mode, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
-               int K, int ksplit, const EpiParams& ep, cudaStream_t st, int* ksplit_eff) {
+int32_t launch(int mode, Operand A, Operand B, int M, int N, int K, int ksplit,
+               const EpiParams& ep, cudaStream_t st, int* ksplit_eff) {
   if (M <= 0 || N <= 0 || K <= 0) return TFS_ERR_INVALID_ARGUMENT;
   CUtensorMap ta, tb;
-  int32_t rc = make_tmap_bf16(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BM);
+  int32_t rc = make_tmap(&ta, A, (uint64_t)M, (uint64_t)K, BM);
   if (rc != TFS_OK) return rc;
-  rc = make_tmap_bf16(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, BN);
+  rc = make_tmap(&tb, B, (uint64_t)N, (uint64_t)K, BN);
   if (rc != TFS_OK) return rc;
   Shape g;
   g.M = M;
@@ -86,10 +94,21 @@ int32_t launch(int mode, const void* A, int64_t lda, const void* B, int64_t ldb,
   g.num_units = g.num_m * g.num_n * g.ksplit;
   if (ksplit_eff) *ksplit_eff = g.ksplit;
   const int grid = std::min(g.num_units, num_sms());
+  const int sel = (A.mn ? 1 : 0) | (B.mn ? 2 : 0);
   switch (mode) {
-    case kStats: return launch_mode<kStats>(ta, tb, g, ep, grid, st);
-    case kGrad: return launch_mode<kGrad>(ta, tb, g, ep, grid, st);
-    default: return launch_mode<kStore>(ta, tb, g, ep, grid, st);
+    case kStats:
+      if (sel != 0) return TFS_ERR_INVALID_ARGUMENT;
+      return launch_mode<kStats, false, false>(ta, tb, g, ep, grid, st);
+    case kGrad:
+      if (sel != 0) return TFS_ERR_INVALID_ARGUMENT;
+      return launch_mode<kGrad, false, false>(ta, tb, g, ep, grid, st);
+    default:
+      switch (sel) {
+        case 0: return launch_mode<kStore, false, false>(ta, tb, g, ep, grid, st);
+        case 1: return launch_mode<kStore, true, false>(ta, tb, g, ep, grid, st);
+        case 2: return launch_mode<kStore, false, true>(ta, tb, g, ep, grid, st);
+        default: return launch_mode<kStore, true, true>(ta, tb, g, ep, grid, st);
+      }
   }
 }
 
@@ -251,36 +270,43 @@ __global__ void colsum_kernel(const float* G, int64_t B, int64_t S, int64_t ldg,
 
 // =============================================================================================
 // bf16 tensor-core path: small kernels around the GEMMs
-// fp32 [R x C] -> bf16 [R x C] and bf16 transpose [C x ldT]
-__global__ void __launch_bounds__(256) to_bf16_and_transpose_kernel(const float* src, int64_t R,
-                                                                    int32_t C, uint16_t* dst,
-                                                                    uint16_t* dstT, int64_t ldT) {
-  __shared__ uint16_t tile[32][34];
-  const int64_t r0 = (int64_t)blockIdx.y * 32;
-  const int c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t r = r0 + ty + 8 * i;
-    const int c = c0 + tx;
-    uint16_t b = 0;
-    if (r < R && c < C) {
-      b = f32_to_bf16_bits(src[r * C + c]);
-      dst[r * C + c] = b;
-    }
-    tile[ty + 8 * i][tx] = b;
+// fp32 -> bf16 (RNE), 4 elements per thread.
+__global__ void to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
+  const int64_t n4 = n >> 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(src)[i];
+    reinterpret_cast<uint2*>(dst)[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
   }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int c = c0 + ty + 8 * i;
-    const int64_t r = r0 + tx;
-    if (r < R && c < C) dstT[(int64_t)c * ldT + r] = tile[tx][ty + 8 * i];
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = f32_to_bf16_bits(src[i]);
+}
+
+// Per-column epilogue parameters, padded to a multiple of the 256-column tile:
+// cb[j] = (b_s[j] - [Q] log_ec_s[j]) * log2(e) (-inf beyond S), sid[j] = s_j (-1 beyond S);
+// per-row label y32[t] (-2 = never matches when accidental hits are kept).
+__global__ void column_params_kernel(const float* b_s, const float* le_s, const int64_t* sampled,
+                                     int64_t S, int64_t S_pad, const int64_t* labels, int64_t B,
+                                     int remove_hits, float* cb, int32_t* sid, int32_t* y32) {
+  const int64_t total = S_pad + B;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < S) {
+      cb[e] = (b_s[e] - (le_s ? le_s[e] : 0.f)) * umma::kLog2e;
+      sid[e] = (int32_t)sampled[e];
+    } else if (e < S_pad) {
+      cb[e] = -INFINITY;
+      sid[e] = -1;
+    } else {
+      const int64_t t = e - S_pad;
+      y32[t] = remove_hits ? (int32_t)labels[t] : -2;
+    }
   }
 }
 
-// Warp per token: true logit on bf16-rounded operands, combine the per-half-tile (max, sumexp)
-// partials in tile order, then loss / g / dW_true / db_true.
+// Warp per token: true logit on bf16-rounded operands, combine the per-half-tile (max, sum)
+// partials (log2 domain) in tile order, then loss / g / dW_true / db_true.
 __global__ void __launch_bounds__(256) bf16_combine_kernel(
     int64_t B, int32_t d, const float* h, const float* w_true, const float* b_true,
     const float* le_true, const float2* stats, int nparts, float c, float* loss, float* lse_out,
@@ -295,19 +321,20 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   const float z = part + b_true[t] - (le_true ? le_true[t] : 0.f);
-  float m = z;
+  const float z2 = z * umma::kLog2e;
+  float m = z2;
   for (int p = lane; p < nparts; p += 32) m = fmaxf(m, stats[(int64_t)p * B + t].x);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float s = lane == 0 ? __expf(z - m) : 0.f;
+  float s = lane == 0 ? exp2f(z2 - m) : 0.f;
   for (int p = lane; p < nparts; p += 32) {
     const float2 st = stats[(int64_t)p * B + t];
-    if (st.y > 0.f) s += st.y * __expf(st.x - m);
+    if (st.y > 0.f) s += st.y * exp2f(st.x - m);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const float lse = m + __logf(s);
-  const float g = c * (__expf(z - lse) - 1.f);
+  const float lse = (m + log2f(s)) * 0.6931471805599453f;
+  const float g = c * (expf(z - lse) - 1.f);
   for (int k = lane; k < d; k += 32) dw_true[t * d + k] = g * bf16_round(ht[k]);
   if (lane == 0) {
     if (loss) loss[t] = lse - z;
@@ -353,10 +380,11 @@ struct F32Ws {
   float* Z;
 };
 struct Bf16Ws {
-  uint16_t *hb, *hT, *wsb, *wsT, *G, *GT;
+  uint16_t *hb, *wsb, *G;
   float2* stats;
-  float *dbs_part, *dh_part, *dws_part;
-  int64_t Bp, Sp;
+  float *dbs_part, *dh_part, *dws_part, *cb;
+  int32_t *sid, *y32;
+  int64_t Sp, Spad;
   int ks_dh, ks_dws;
 };
 
@@ -376,22 +404,24 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, F32Ws* f
     if (f) f->Z = Z;
     return c.used + 256;
   }
-  const int64_t Bp = (B + 7) / 8 * 8, Sp = (S + 7) / 8 * 8;
-  const int num_m = (int)cdiv(B, umma::BM), num_n = (int)cdiv(S, umma::BN);
+  const int64_t Sp = (S + 7) / 8 * 8;
+  const int64_t Spad = std::max<int64_t>(cdiv(S, umma::BN), 1) * umma::BN;
+  const int num_m = (int)cdiv(B, umma::BM);
+  const int num_n = (int)cdiv(S, umma::BN);
   const int ks_dh = pick_split(B, d, S), ks_dws = pick_split(S, d, B);
   Bf16Ws x;
   x.hb = c.take<uint16_t>(B * d);
-  x.hT = c.take<uint16_t>((size_t)d * Bp);
   x.wsb = c.take<uint16_t>(S * d);
-  x.wsT = c.take<uint16_t>((size_t)d * Sp);
   x.G = c.take<uint16_t>(B * Sp);
-  x.GT = c.take<uint16_t>(S * Bp);
   x.stats = c.take<float2>((size_t)2 * num_n * B);
   x.dbs_part = c.take<float>((size_t)4 * num_m * S);
   x.dh_part = c.take<float>((size_t)ks_dh * B * d);
   x.dws_part = c.take<float>((size_t)(ks_dws > 1 ? ks_dws : 0) * S * d);
-  x.Bp = Bp;
+  x.cb = c.take<float>(Spad);
+  x.sid = c.take<int32_t>(Spad);
+  x.y32 = c.take<int32_t>(B);
   x.Sp = Sp;
+  x.Spad = Spad;
   x.ks_dh = ks_dh;
   x.ks_dws = ks_dws;
   if (w) *w = x;
@@ -414,21 +444,26 @@ static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     SimtParams p{a->b_s, le_s, a->sampled, a->labels, hits, nullptr, nullptr, w.Z, S};
     dim3 grid((unsigned)cdiv(S, 64), (unsigned)cdiv(B, 64));
     simt_gemm_kernel<kSimtLogits><<<grid, 256, 0, st>>>((int)B, (int)S, d, a->h, d, 1, a->w_s, 1,
-                                                         d, p); ::tfs::launched();
+                                                         d, p);
+    launched();
   }
   f32_row_kernel<<<(unsigned)B, 256, 0, st>>>(S, d, a->h, a->w_true, a->b_true, le_t,
                                               a->grad_scale, w.Z, S, a->loss, a->lse, a->dw_true,
-                                              a->db_true); ::tfs::launched();
+                                              a->db_true);
+  launched();
   {  // dh = G W_s + g * w_true
     SimtParams p{nullptr, nullptr, nullptr, nullptr, 0, a->db_true, a->w_true, a->dh, d};
     dim3 grid((unsigned)cdiv(d, 64), (unsigned)cdiv(B, 64));
-    simt_gemm_kernel<kSimtDh><<<grid, 256, 0, st>>>((int)B, d, (int)S, w.Z, S, 1, a->w_s, d, 1, p); ::tfs::launched();
+    simt_gemm_kernel<kSimtDh><<<grid, 256, 0, st>>>((int)B, d, (int)S, w.Z, S, 1, a->w_s, d, 1, p);
+    launched();
   }
   if (S > 0) {  // dW_s = G^T h ; db_s = column sums of G
     SimtParams p{nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, a->dw_s, d};
     dim3 grid((unsigned)cdiv(d, 64), (unsigned)cdiv(S, 64));
-    simt_gemm_kernel<kSimtStore><<<grid, 256, 0, st>>>((int)S, d, (int)B, w.Z, 1, S, a->h, d, 1, p); ::tfs::launched();
-    colsum_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.Z, B, S, S, a->db_s); ::tfs::launched();
+    simt_gemm_kernel<kSimtStore><<<grid, 256, 0, st>>>((int)S, d, (int)B, w.Z, 1, S, a->h, d, 1, p);
+    launched();
+    colsum_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.Z, B, S, S, a->db_s);
+    launched();
   }
   TFS_LAUNCH_CHECK();
   return TFS_OK;
@@ -444,59 +479,63 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
   const int num_m = (int)cdiv(B, umma::BM), num_n = (int)cdiv(S, umma::BN);
 
-  // Operands: bf16 copies in both layouts (each GEMM reads K-major tiles).
-  to_bf16_and_transpose_kernel<<<dim3((unsigned)cdiv(d, 32), (unsigned)cdiv(B, 32)), 256, 0, st>>>(
-      a->h, B, d, w.hb, w.hT, w.Bp); ::tfs::launched();
+  // Operands in bf16 (row-major; every GEMM reads them K- or MN-major as it needs).
+  to_bf16_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(a->h, B * d, w.hb);
+  launched();
   if (S > 0) {
-    to_bf16_and_transpose_kernel<<<dim3((unsigned)cdiv(d, 32), (unsigned)cdiv(S, 32)), 256, 0,
-                                   st>>>(a->w_s, S, d, w.wsb, w.wsT, w.Sp); ::tfs::launched();
+    to_bf16_kernel<<<grid1d(S * d / 4), 256, 0, st>>>(a->w_s, S * d, w.wsb);
+    launched();
   }
+  column_params_kernel<<<grid1d(w.Spad + B), 256, 0, st>>>(
+      a->b_s, le_s, a->sampled, S, w.Spad, a->labels, B, hits, w.cb, w.sid, w.y32);
+  launched();
   TFS_LAUNCH_CHECK();
 
+  using umma::Operand;
   umma::EpiParams ep{};
-  ep.b_s = a->b_s;
-  ep.le_s = le_s;
-  ep.sampled = a->sampled;
-  ep.labels = a->labels;
-  ep.remove_hits = hits;
+  ep.cb = w.cb;
+  ep.sid = w.sid;
+  ep.y = w.y32;
   int32_t rc;
-  if (S > 0) {  // pass 1: per-row (max, sumexp) of each half tile
+  const Operand hK{w.hb, d, false}, wsK{w.wsb, d, false};
+  if (S > 0) {  // pass 1: per-row (max, sum 2^x) of each half tile, log2 domain
     ep.stats = w.stats;
-    rc = umma::launch(umma::kStats, w.hb, d, w.wsb, d, (int)B, (int)S, d, 1, ep, st, nullptr);
+    rc = umma::launch(umma::kStats, hK, wsK, (int)B, (int)S, d, 1, ep, st, nullptr);
     if (rc != TFS_OK) return rc;
   }
   bf16_combine_kernel<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(
       B, d, a->h, a->w_true, a->b_true, le_t, w.stats, 2 * num_n, a->grad_scale, a->loss,
-      a->lse, a->dw_true, a->db_true); ::tfs::launched();
+      a->lse, a->dw_true, a->db_true);
+  launched();
   TFS_LAUNCH_CHECK();
-  // lse is needed by pass 2: use the caller's buffer if given, else scratch in dh_part's tail.
-  if (S > 0) {  // pass 2: G = c exp(Z - lse) -> bf16 G, G^T; column partial sums for db_s
+  if (S > 0) {  // pass 2: G = c exp(Z - lse) -> bf16 G; column partial sums for db_s
     ep.lse = a->lse;
     ep.c = a->grad_scale;
     ep.G = w.G;
     ep.ldG = w.Sp;
-    ep.GT = w.GT;
-    ep.ldGT = w.Bp;
     ep.dbs_part = w.dbs_part;
-    rc = umma::launch(umma::kGrad, w.hb, d, w.wsb, d, (int)B, (int)S, d, 1, ep, st, nullptr);
+    rc = umma::launch(umma::kGrad, hK, wsK, (int)B, (int)S, d, 1, ep, st, nullptr);
     if (rc != TFS_OK) return rc;
-    dbs_finalize_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.dbs_part, 4 * num_m, S, a->db_s); ::tfs::launched();
+    dbs_finalize_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.dbs_part, 4 * num_m, S, a->db_s);
+    launched();
   }
-  // dh = G W_s (split-K partials) + g * bf16(w_true)
+  // dh = G W_s (split-K partials) + g * bf16(w_true):  A = G K-major, B = W_s MN-major.
   int ks = 1;
   if (S > 0) {
     umma::EpiParams e2{};
     e2.out = w.dh_part;
     e2.ldo = d;
     e2.split_stride = B * d;
-    rc = umma::launch(umma::kStore, w.G, w.Sp, w.wsT, w.Sp, (int)B, d, (int)S, w.ks_dh, e2, st, &ks);
+    rc = umma::launch(umma::kStore, Operand{w.G, w.Sp, false}, Operand{w.wsb, d, true}, (int)B, d,
+                      (int)S, w.ks_dh, e2, st, &ks);
     if (rc != TFS_OK) return rc;
   } else {
     TFS_CUDA_TRY(cudaMemsetAsync(w.dh_part, 0, sizeof(float) * B * d, st));
   }
   dh_finalize_kernel<<<grid1d(B * d), 256, 0, st>>>(w.dh_part, ks, B * d, B, d, a->db_true,
-                                                    a->w_true, a->dh); ::tfs::launched();
-  // dW_s = G^T h
+                                                    a->w_true, a->dh);
+  launched();
+  // dW_s = G^T h:  A = G MN-major, B = h MN-major.
   if (S > 0) {
     umma::EpiParams e3{};
     const bool split = w.ks_dws > 1;
@@ -504,11 +543,12 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     e3.ldo = d;
     e3.split_stride = S * d;
     int ks2 = 1;
-    rc = umma::launch(umma::kStore, w.GT, w.Bp, w.hT, w.Bp, (int)S, d, (int)B, w.ks_dws, e3, st,
-                      &ks2);
+    rc = umma::launch(umma::kStore, Operand{w.G, w.Sp, true}, Operand{w.hb, d, true}, (int)S, d,
+                      (int)B, w.ks_dws, e3, st, &ks2);
     if (rc != TFS_OK) return rc;
     if (split) {
-      split_sum_kernel<<<grid1d(S * d), 256, 0, st>>>(w.dws_part, ks2, S * d, S * d, a->dw_s); ::tfs::launched();
+      split_sum_kernel<<<grid1d(S * d), 256, 0, st>>>(w.dws_part, ks2, S * d, S * d, a->dw_s);
+      launched();
     }
   }
   TFS_LAUNCH_CHECK();
@@ -564,9 +604,10 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
 
 // Diagnostics: C[ks][M x N] (fp32) = A[M x K] . B[N x K]^T with bf16 operands on the tcgen05
 // path.  Exposed for the GEMM unit test only.
-extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb,
-                                       int32_t M, int32_t N, int32_t K, int32_t ksplit, float* C,
-                                       int32_t* out_ksplit, void* stream) {
+extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B,
+                                       int64_t ldb, int32_t b_mn, int32_t M, int32_t N, int32_t K,
+                                       int32_t ksplit, float* C, int32_t* out_ksplit,
+                                       void* stream) {
   TFS_REQUIRE(A && B && C && M > 0 && N > 0 && K > 0 && lda % 8 == 0 && ldb % 8 == 0);
   TFS_SUPPORTED();
   umma::EpiParams e{};
@@ -574,7 +615,9 @@ extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, const void* B
   e.ldo = N;
   e.split_stride = (int64_t)M * N;
   int ks = 1;
-  int32_t rc = umma::launch(umma::kStore, A, lda, B, ldb, M, N, K, ksplit, e, as_stream(stream), &ks);
+  int32_t rc = umma::launch(umma::kStore, umma::Operand{A, lda, a_mn != 0},
+                            umma::Operand{B, ldb, b_mn != 0}, M, N, K, ksplit, e,
+                            as_stream(stream), &ks);
   if (out_ksplit) *out_ksplit = ks;
   return rc;
 }

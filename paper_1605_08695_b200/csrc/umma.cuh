@@ -1,9 +1,11 @@
 // umma.cuh -- hand-written sm_100a tensor-core GEMM (tcgen05.mma + TMEM + TMA + mbarriers) with
-// the sampled-softmax epilogues fused in.  C[m, n] = sum_k A[m, k] * B[n, k], A and B bf16,
-// K-major (row-major with K contiguous), fp32 accumulation in TMEM.
+// the sampled-softmax epilogues fused in.  C[m, n] = sum_k A(m, k) * B(n, k), bf16 operands,
+// fp32 accumulation in TMEM.  Each operand is either K-major (row-major [rows x K]) or
+// MN-major (row-major [K x rows]: the transposed view), selected per launch, so the softmax
+// backward reads G, W_s and h in the layout they already have -- no transposed copies.
 //
 // CTA = 12 warps, persistent over (m-tile, n-tile, k-split) units:
-//   warp 0      TMA producer (one lane): 128x64 A tile + 256x64 B tile per stage, 128B swizzle,
+//   warp 0      TMA producer (one lane): A 128x64 and B 256x64 per stage, 128-byte swizzle,
 //               4-stage smem ring guarded by full/empty mbarriers.
 //   warp 1      MMA issuer (one lane): 4 x tcgen05.mma.kind::f16 (M=128, N=256, K=16) per stage
 //               into one of two 256-column TMEM accumulators; tcgen05.commit frees the stage /
@@ -12,8 +14,8 @@
 //   warps 4-11  epilogue: warp w reads TMEM lanes 32*(w%4).. (its 32 rows), columns
 //               [128*((w-4)/4), +128) in 32-column tcgen05.ld chunks, applies the fused epilogue
 //               and frees the accumulator, so the epilogue of tile i overlaps the MMAs of i+1.
-// Epilogue modes: STATS (row max / sum-exp of the corrected logits per half
-// tile), GRAD (G = c exp(Z - lse) -> bf16 G and G^T + column sums for db), STORE (fp32 out).
+// Epilogue modes: STATS (row max / sum of 2^x of the corrected logits per half
+// tile, log2 domain), GRAD (G = c exp(Z - lse) -> bf16 G + column sums for db), STORE (fp32).
 #pragma once
 
 #include <cuda.h>
@@ -29,15 +31,22 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + kEpiWarps * 32;  // 384
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
 constexpr int B_BYTES = BN * BK * 2;            // 32 KB
+constexpr int kMNBox = 64;                      // MN-major TMA box: 64 elements (128 B) x BK rows
+constexpr int kMNBoxBytes = kMNBox * BK * 2;    // 8 KB
 constexpr int kTmemCols = 512;
-constexpr uint32_t kIdesc = (1u << 4)                      // D format f32
-                            | (1u << 7)                    // A format bf16
-                            | (1u << 10)                   // B format bf16
-                            | ((uint32_t)(BN >> 3) << 17)  // N
-                            | ((uint32_t)(BM >> 4) << 24); // M
-constexpr int kEpiStageFloats = 256;
+constexpr float kLog2e = 1.4426950408889634f;
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)STAGES * (A_BYTES + B_BYTES) +
-                              256 /*barriers*/ + 2 * kEpiStageFloats * (4 + 8) /*cb + sid*/;
+                              256 /*barriers*/;
+
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+  return (1u << 4)                       // D format f32
+         | (1u << 7)                     // A format bf16
+         | (1u << 10)                    // B format bf16
+         | ((a_mn ? 1u : 0u) << 15)      // A major (0 = K, 1 = MN)
+         | ((b_mn ? 1u : 0u) << 16)      // B major
+         | ((uint32_t)(BN >> 3) << 17)   // N
+         | ((uint32_t)(BM >> 4) << 24);  // M
+}
 
 enum Mode : int { kStats = 0, kGrad = 1, kStore = 2 };
 
@@ -48,19 +57,16 @@ struct Shape {
 };
 
 struct EpiParams {
-  // STATS / GRAD: corrected logit Z = acc + col_bias[n], excluded when sid[n] == labels[m].
-  const float* b_s;
-  const float* le_s;  // may be null (no log-Q correction)
-  const int64_t* sampled;
-  const int64_t* labels;
-  int remove_hits;
-  float2* stats;  // STATS: [(2*num_n) x M] (max, sumexp) per half tile
-  const float* lse;  // GRAD
-  float c;           // GRAD
+  // STATS / GRAD: corrected logit in log2 units  v = acc * log2(e) + cb[n], excluded (-> -inf)
+  // when sid[n] == y[m].  cb / sid are padded to a multiple of BN (cb = -inf, sid = -1).
+  const float* cb;
+  const int32_t* sid;
+  const int32_t* y;
+  float2* stats;     // STATS: [(2*num_n) x M] (max, sum of 2^(v - max)) per half tile
+  const float* lse;  // GRAD: natural-log lse per row
+  float c;           // GRAD: gradient scale
   uint16_t* G;       // GRAD: bf16 [M x ldG]
   int64_t ldG;
-  uint16_t* GT;      // GRAD: bf16 [N x ldGT]
-  int64_t ldGT;
   float* dbs_part;   // GRAD: [(4*num_m) x N] column sums of bf16(G)
   float* out;        // STORE: fp32, out[ks * split_stride + m * ldo + n]
   int64_t ldo;
@@ -109,22 +115,30 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+// Shared-memory matrix descriptor, 128-byte swizzle.  lbo / sbo in bytes:
+//  K-major: 8-row core groups 1024 B apart (sbo); lbo unused (16 B).
+//  MN-major: lbo = stride between 64-element MN blocks, sbo = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;             // leading byte offset (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;   // stride byte offset: 8 rows x 128 B
-  d |= (uint64_t)1 << 46;             // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
 }
+template <bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k16) {
+  // K advance of 16 elements: +32 B inside the swizzled row (K-major), +16 rows (MN-major).
+  return MN ? desc_sw128(base + (uint32_t)k16 * 2048u, kMNBoxBytes, 1024)
+            : desc_sw128(base + (uint32_t)k16 * 32u, 16, 1024);
+}
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
-                                          uint32_t accumulate) {
+                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
@@ -149,8 +163,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void epi_bar_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __device__ __forceinline__ void decode_unit(const Shape& g, int u, int& mt, int& nt, int& ks,
@@ -184,7 +200,23 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
   return v[0];
 }
 
-template <int MODE>
+// Corrected logits of one 32-column chunk in log2 units (-inf where excluded).
+__device__ __forceinline__ void corrected_logits(const EpiParams& ep, int col0, int32_t y,
+                                                 float (&v)[32]) {
+  const float4* cb4 = reinterpret_cast<const float4*>(ep.cb + col0);
+  const int4* sid4 = reinterpret_cast<const int4*>(ep.sid + col0);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 c = __ldg(cb4 + q);
+    const int4 s = __ldg(sid4 + q);
+    v[4 * q + 0] = s.x == y ? -INFINITY : fmaf(v[4 * q + 0], kLog2e, c.x);
+    v[4 * q + 1] = s.y == y ? -INFINITY : fmaf(v[4 * q + 1], kLog2e, c.y);
+    v[4 * q + 2] = s.z == y ? -INFINITY : fmaf(v[4 * q + 2], kLog2e, c.z);
+    v[4 * q + 3] = s.w == y ? -INFINITY : fmaf(v[4 * q + 3], kLog2e, c.w);
+  }
+}
+
+template <int MODE, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 Shape g, EpiParams ep) {
@@ -197,8 +229,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  float* s_cb = (float*)(smem + STAGES * (A_BYTES + B_BYTES) + 256);  // [2][256]
-  int64_t* s_sid = (int64_t*)(s_cb + 2 * kEpiStageFloats);            // [2][256]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -237,8 +267,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           mbar_expect_tx(full + stage, A_BYTES + B_BYTES);
-          tma_load_2d(sA + stage * A_BYTES, &tmA, kb * BK, mt * BM, full + stage);
-          tma_load_2d(sB + stage * B_BYTES, &tmB, kb * BK, nt * BN, full + stage);
+          uint8_t* a = sA + stage * A_BYTES;
+          uint8_t* b = sB + stage * B_BYTES;
+          if (A_MN) {
+#pragma unroll
+            for (int q = 0; q < BM / kMNBox; ++q)
+              tma_load_2d(a + q * kMNBoxBytes, &tmA, mt * BM + q * kMNBox, kb * BK, full + stage);
+          } else {
+            tma_load_2d(a, &tmA, kb * BK, mt * BM, full + stage);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int q = 0; q < BN / kMNBox; ++q)
+              tma_load_2d(b + q * kMNBoxBytes, &tmB, nt * BN + q * kMNBox, kb * BK, full + stage);
+          } else {
+            tma_load_2d(b, &tmB, kb * BK, nt * BN, full + stage);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -249,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ================================ MMA issuer ==================================
     if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int u = blockIdx.x; u < g.num_units; u += gridDim.x) {
@@ -264,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d_tmem, desc_sw128(a0 + k * 32), desc_sw128(b0 + k * 32),
+            umma_bf16(d_tmem, operand_desc<A_MN>(a0, k), operand_desc<B_MN>(b0, k), idesc,
                       (kb > kb0 || k > 0) ? 1u : 0u);
           umma_commit(empty + stage);
           if (++stage == STAGES) {
@@ -279,10 +324,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ================================ Epilogue ====================================
-    const int ew = warp - 4;          // 0..7
-    const int quarter = warp & 3;     // TMEM lane quarter this warp may access
-    const int half = ew >> 2;         // column half of the 256-wide tile
-    const int etid = threadIdx.x - 128;
+    const int ew = warp - 4;       // 0..7
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = ew >> 2;      // column half of the 256-wide tile
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < g.num_units; u += gridDim.x) {
@@ -290,21 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode_unit(g, u, mt, nt, ks, kb0, kb1);
       const int row = mt * BM + quarter * 32 + lane;
       const bool row_ok = row < g.M;
-      float* cb = s_cb + acc * kEpiStageFloats;
-      int64_t* sid = s_sid + acc * kEpiStageFloats;
-      if (MODE != kStore) {  // stage the tile's column parameters (double-buffered)
-        const int n = nt * BN + etid;
-        if (n < g.N) {
-          cb[etid] = ep.b_s[n] - (ep.le_s ? ep.le_s[n] : 0.f);
-          sid[etid] = ep.sampled[n];
-        } else {
-          cb[etid] = 0.f;
-          sid[etid] = INT64_MIN;  // column beyond N: always excluded
-        }
-        epi_bar_sync();
-      }
-      const int64_t y = (MODE != kStore && row_ok) ? ep.labels[row] : INT64_MIN + 1;
-      const float lse_row = (MODE == kGrad && row_ok) ? ep.lse[row] : 0.f;
+      int32_t y = -2;
+      float lse2 = 0.f;
+      if (MODE != kStore && row_ok) y = ep.y[row];
+      if (MODE == kGrad && row_ok) lse2 = ep.lse[row] * kLog2e;
       float run_m = -INFINITY, run_s = 0.f;
 
       mbar_wait(tfull + acc, acc_phase);
@@ -316,33 +349,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + ct), v);
         if (MODE == kStats) {
-          float cm = -INFINITY;
+          corrected_logits(ep, col0, y, v);
+          float m4[4];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int64_t s = sid[ct + i];
-            const bool excl = s == INT64_MIN || (ep.remove_hits && s == y);
-            v[i] = excl ? -INFINITY : v[i] + cb[ct + i];
-            cm = fmaxf(cm, v[i]);
-          }
+          for (int q = 0; q < 4; ++q)
+            m4[q] = fmaxf(fmaxf(fmaxf(v[q], v[q + 4]), fmaxf(v[q + 8], v[q + 12])),
+                          fmaxf(fmaxf(v[q + 16], v[q + 20]), fmaxf(v[q + 24], v[q + 28])));
+          const float cm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
           if (cm > -INFINITY) {
             const float nm = fmaxf(run_m, cm);
-            float s = run_s * __expf(run_m - nm);
+            float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int i = 0; i < 32; ++i) s += __expf(v[i] - nm);
-            run_s = s;
+            for (int i = 0; i < 32; ++i) s4[i & 3] += fast_exp2(v[i] - nm);
+            run_s = run_s * fast_exp2(run_m - nm) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
             run_m = nm;
           }
         } else if (MODE == kGrad) {
+          corrected_logits(ep, col0, y, v);
           uint32_t packed[16];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int64_t s = sid[ct + i];
-            const bool excl = !row_ok || s == INT64_MIN || (ep.remove_hits && s == y);
-            const float gval = excl ? 0.f : ep.c * __expf(v[i] + cb[ct + i] - lse_row);
-            v[i] = bf16_round(gval);
+          for (int i = 0; i < 16; ++i) {
+            const float g0 = row_ok ? ep.c * fast_exp2(v[2 * i] - lse2) : 0.f;
+            const float g1 = row_ok ? ep.c * fast_exp2(v[2 * i + 1] - lse2) : 0.f;
+            packed[i] = pack_bf16x2(g0, g1);
+            v[2 * i] = __uint_as_float(packed[i] << 16);              // bf16(g0) as fp32
+            v[2 * i + 1] = __uint_as_float(packed[i] & 0xffff0000u);  // bf16(g1) as fp32
           }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
           if (row_ok) {
             uint16_t* gr = ep.G + (int64_t)row * ep.ldG + col0;
             if (col0 + 32 <= g.N) {
@@ -354,11 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                if (col0 + i < g.N) gr[i] = f32_to_bf16_bits(v[i]);
+                if (col0 + i < g.N)
+                  gr[i] = (uint16_t)((i & 1) ? (packed[i >> 1] >> 16) : (packed[i >> 1] & 0xffffu));
             }
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < g.N) ep.GT[(int64_t)(col0 + i) * ep.ldGT + row] = f32_to_bf16_bits(v[i]);
           }
           const float colsum = transpose_reduce32(v, lane);
           if (col0 + lane < g.N)
@@ -396,10 +426,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---- host side ------------------------------------------------------------------------------------
-int32_t make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t ld,
-                       uint32_t box_rows);
-int32_t launch(int mode, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
-               int K, int ksplit, const EpiParams& ep, cudaStream_t st, int* ksplit_eff);
+// Operand view: base pointer, row stride `ld` (elements), and whether it is MN-major.  K-major:
+// element (r, k) at base[r * ld + k]; MN-major: element (r, k) at base[k * ld + r].
+struct Operand {
+  const void* base;
+  int64_t ld;
+  bool mn;
+};
+
+int32_t launch(int mode, Operand A, Operand B, int M, int N, int K, int ksplit,
+               const EpiParams& ep, cudaStream_t st, int* ksplit_eff);
 
 }  // namespace umma
 }  // namespace tfs

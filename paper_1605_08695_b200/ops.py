@@ -204,12 +204,14 @@ def scatter_add_sgd(table, ids, grad, lr: float, table2=None, grad2=None, err: E
     return table
 
 
-def debug_gemm_bf16(A, B, ksplit: int = 1):
-    """C[ks] = A . B^T on the tcgen05 path (diagnostics)."""
-    M, K = A.shape
-    N = B.shape[0]
+def debug_gemm_bf16(A, B, ksplit: int = 1, a_mn: bool = False, b_mn: bool = False):
+    """C[ks] = sum_k A(m, k) B(n, k) on the tcgen05 path (diagnostics).  A is [M, K] (K-major)
+    or, with a_mn, [K, M] (MN-major); likewise B is [N, K] or [K, N]."""
+    M, K = (A.shape[1], A.shape[0]) if a_mn else A.shape
+    N = B.shape[1] if b_mn else B.shape[0]
     C = torch.empty((max(ksplit, 1), M, N), dtype=torch.float32, device=A.device)
     ks = ctypes.c_int32(0)
-    check(_lib.lib().tfs_debug_gemm_bf16(_p(A), A.stride(0), _p(B), B.stride(0), M, N, K, ksplit,
-                                         _p(C), ctypes.byref(ks), _stream()), "tfs_debug_gemm_bf16")
+    check(_lib.lib().tfs_debug_gemm_bf16(_p(A), A.stride(0), int(a_mn), _p(B), B.stride(0),
+                                         int(b_mn), M, N, K, ksplit, _p(C), ctypes.byref(ks),
+                                         _stream()), "tfs_debug_gemm_bf16")
     return C[: ks.value]

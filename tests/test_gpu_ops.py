@@ -46,18 +46,23 @@ def T(a, dtype=None):
 
 
 # ------------------------------------------------------------------------------------- GEMM unit
-@pytest.mark.parametrize("M,N,K,ks", [(128, 256, 64, 1), (256, 512, 512, 1), (300, 700, 192, 1),
-                                      (2560, 512, 8192, 4), (37, 19, 64, 1), (1000, 256, 2560, 3)])
-def test_tcgen05_gemm_matches_torch(M, N, K, ks):
+@pytest.mark.parametrize("M,N,K,ks", [(128, 256, 64, 1), (256, 512, 512, 1), (300, 704, 192, 1),
+                                      (2560, 512, 8192, 4), (40, 24, 64, 1), (1000, 256, 2560, 3)])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+def test_tcgen05_gemm_matches_torch(M, N, K, ks, a_mn, b_mn):
+    """C = A B^T with each operand read K-major ([rows, K]) or MN-major ([K, rows])."""
     g = torch.Generator().manual_seed(M * 7 + N)
     A = torch.randn(M, K, generator=g).to(torch.bfloat16)
     B = torch.randn(N, K, generator=g).to(torch.bfloat16)
-    Kp = (K + 7) // 8 * 8
-    Ad = torch.zeros(M, Kp, dtype=torch.bfloat16, device=DEV)
-    Bd = torch.zeros(N, Kp, dtype=torch.bfloat16, device=DEV)
-    Ad[:, :K] = A.to(DEV)
-    Bd[:, :K] = B.to(DEV)
-    C = ops.debug_gemm_bf16(Ad[:, :K] if Kp == K else Ad, Bd[:, :K] if Kp == K else Bd, ks)
+    def place(X, mn):  # row stride padded to a multiple of 8 elements (16 bytes)
+        X = X.T if mn else X
+        r, c = X.shape
+        buf = torch.zeros(r, (c + 7) // 8 * 8, dtype=torch.bfloat16, device=DEV)
+        buf[:, :c] = X.to(DEV)
+        return buf[:, :c]
+
+    Ad, Bd = place(A, a_mn), place(B, b_mn)
+    C = ops.debug_gemm_bf16(Ad, Bd, ks, a_mn=a_mn, b_mn=b_mn)
     got = C.sum(0).cpu().double()
     ref = A.double() @ B.double().T
     err = (got - ref).abs().max().item() / ref.abs().max().item()
