@@ -391,11 +391,14 @@ struct SegJob {
   float* table;
   float* table2;
   float lr;
-  // write mode (sort_reduce): out_local[s], out_rows[s]
+  // write mode (sort_reduce): out_local[u], out_rows[u]
   int64_t* out_local;
   float* out_rows;
   float* out_rows2;
   int64_t nloc;
+  // apply mode: sums of the segments that lie inside one chunk, [U x dim] (+ [U])
+  float* sums;
+  float* sums2;
   // partials of segments crossing chunk boundaries: slot 2c = the piece in chunk c of the
   // segment that started before chunk c; slot 2c+1 = the piece of the segment that starts in
   // chunk c and continues after it.
@@ -410,95 +413,77 @@ struct D4 {
 __device__ __forceinline__ void add4(D4& a, const float4& v) {
   a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
 }
-
-// ScatterAdd-SGD: T = fl32(T - lr * g) evaluated in fp64; sort_reduce: out = fl32(g).
-__device__ __forceinline__ void emit4(const SegJob& j, uint32_t s, uint32_t key, int c4,
-                                      const D4& v) {
-  if (j.table != nullptr) {
-    float4* t = (float4*)(j.table + (int64_t)key * j.dim) + c4;
-    float4 w = *t;
-    const double lr = (double)j.lr;
-    w.x = (float)((double)w.x - lr * v.x);
-    w.y = (float)((double)w.y - lr * v.y);
-    w.z = (float)((double)w.z - lr * v.z);
-    w.w = (float)((double)w.w - lr * v.w);
-    *t = w;
-  } else {
-    ((float4*)(j.out_rows + (int64_t)s * j.dim))[c4] =
-        make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w);
-  }
+__device__ __forceinline__ void add4(D4& a, const D4& v) {
+  a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+}
+__device__ __forceinline__ float4 to_f4(const D4& v) {
+  return make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w);
 }
 
-__device__ __forceinline__ void emit1(const SegJob& j, uint32_t s, uint32_t key, int c, double v) {
-  if (j.table != nullptr) {
-    float* t = j.table + (int64_t)key * j.dim + c;
-    *t = (float)((double)*t - (double)j.lr * v);
-  } else {
-    j.out_rows[(int64_t)s * j.dim + c] = (float)v;
-  }
+// Where a finished piece of one segment goes (warp-uniform decision).
+struct PieceDst {
+  int kind;  // 0 whole segment, 1 head slot (started before the chunk), 2 tail slot
+  int64_t slot;
+};
+__device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_after, int64_t chunk) {
+  if (starts_before) return PieceDst{1, 2 * chunk};
+  if (ends_after) return PieceDst{2, 2 * chunk + 1};
+  return PieceDst{0, 0};
 }
 
-__device__ __forceinline__ void emit_companion(const SegJob& j, uint32_t s, uint32_t key,
-                                               double v) {
-  if (j.table != nullptr) {
-    if (j.table2) j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * v);
-  } else if (j.out_rows2) {
-    j.out_rows2[s] = (float)v;
-  }
-}
-
-// Where the piece of segment s that lives in chunk `chunk` goes: -1 = it is the whole segment
-// (emit now), else the partial slot index.
-__device__ __forceinline__ int64_t piece_slot(const SegJob& j, uint32_t s, int64_t chunk) {
-  const int64_t c0 = (int64_t)j.seg_start[s] / kChunk;
-  const int64_t c1 = ((int64_t)j.seg_start[s + 1] - 1) / kChunk;
-  if (c0 == c1) return -1;
-  return chunk == c0 ? 2 * chunk + 1 : 2 * chunk;
-}
-
-// One warp per chunk of kChunk sorted rows, float4 columns (dim % 4 == 0).
+// One warp per chunk of kChunk sorted rows, float4 columns (dim % 4 == 0).  Only gradient rows
+// are read; every decision uses per-lane data loaded up front (no dependent lookups).
 __global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j) {
   const int lane = threadIdx.x & 31;
   const int64_t chunk = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t base = chunk * kChunk;
   if (base >= j.n) return;
   const int cnt = (int)min((int64_t)kChunk, j.n - base);
-  uint32_t perm_l = 0, seg_l = 0;
+  uint32_t perm_l = 0, seg_l = 0, key_l = 0;
   float r2_l = 0.f;
   if (lane < cnt) {
     perm_l = j.perm[base + lane];
     seg_l = j.seg_of[base + lane];
+    key_l = j.keys[base + lane];
     if (j.rows2) r2_l = j.rows2[perm_l];
   }
+  // Does the first segment start before this chunk / the last one continue after it?
+  uint32_t edge = 0;
+  if (lane == 0 && base > 0) edge = j.keys[base - 1] == j.keys[base];
+  if (lane == 1 && base + cnt < j.n) edge = j.keys[base + cnt] == j.keys[base + cnt - 1];
+  const bool first_before = __shfl_sync(0xffffffffu, edge, 0) != 0;
+  const bool last_after = __shfl_sync(0xffffffffu, edge, 1) != 0;
+  const bool write_mode = j.table == nullptr;
   const int n4 = j.dim >> 2;
   for (int c4_0 = 0; c4_0 < n4; c4_0 += 128) {
     D4 acc[4];
     double acc2 = 0.0;
+    int r_start = 0;
     uint32_t cur = __shfl_sync(0xffffffffu, seg_l, 0);
-    auto flush = [&](uint32_t s) {
-      const uint32_t key = j.keys[j.seg_start[s]];
-      if (key >= j.invalid_key) return;
-      const int64_t slot = piece_slot(j, s, chunk);
-      if (slot < 0) {
+    uint32_t cur_key = __shfl_sync(0xffffffffu, key_l, 0);
+    auto flush = [&](int r_end) {
+      if (cur_key >= j.invalid_key) return;
+      const PieceDst dst = piece_dst(r_start == 0 && first_before, r_end == cnt && last_after,
+                                     chunk);
+      if (dst.kind == 0) {
+        float* o = write_mode ? j.out_rows : j.sums;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int c4 = c4_0 + v * 32 + lane;
-          if (c4 < n4) emit4(j, s, key, c4, acc[v]);
+          if (c4 < n4) reinterpret_cast<float4*>(o + (int64_t)cur * j.dim)[c4] = to_f4(acc[v]);
         }
-        if (j.rows2 && lane == 0 && c4_0 == 0) emit_companion(j, s, key, acc2);
+        if (j.rows2 && lane == 0 && c4_0 == 0) {
+          float* o2 = write_mode ? j.out_rows2 : j.sums2;
+          o2[cur] = (float)acc2;
+        }
       } else {
-        double* p = j.part + slot * j.dim;
+        double* p = j.part + dst.slot * j.dim;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int c4 = c4_0 + v * 32 + lane;
-          if (c4 < n4) {
-            p[4 * c4 + 0] = acc[v].x;
-            p[4 * c4 + 1] = acc[v].y;
-            p[4 * c4 + 2] = acc[v].z;
-            p[4 * c4 + 3] = acc[v].w;
-          }
+          if (c4 < n4) reinterpret_cast<D4*>(p)[c4] = acc[v];
         }
-        if (j.rows2 && lane == 0 && c4_0 == 0) j.part2[slot] = acc2;
+        if (j.rows2 && lane == 0 && c4_0 == 0) j.part2[dst.slot] = acc2;
       }
     };
 #pragma unroll
@@ -519,10 +504,13 @@ __global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j) {
       for (int u = 0; u < 4; ++u) {
         if (r0 + u >= cnt) break;
         const uint32_t s = __shfl_sync(0xffffffffu, seg_l, r0 + u);
+        const uint32_t k = __shfl_sync(0xffffffffu, key_l, r0 + u);
         const float r2 = __shfl_sync(0xffffffffu, r2_l, r0 + u);
         if (s != cur) {
-          flush(cur);
+          flush(r0 + u);
           cur = s;
+          cur_key = k;
+          r_start = r0 + u;
 #pragma unroll
           for (int v = 0; v < 4; ++v) acc[v] = D4{0.0, 0.0, 0.0, 0.0};
           acc2 = 0.0;
@@ -532,7 +520,7 @@ __global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j) {
         acc2 += r2;
       }
     }
-    flush(cur);
+    flush(cnt);
   }
 }
 
@@ -543,69 +531,132 @@ __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
   const int64_t base = chunk * kChunk;
   if (base >= j.n) return;
   const int cnt = (int)min((int64_t)kChunk, j.n - base);
-  uint32_t perm_l = 0, seg_l = 0;
+  uint32_t perm_l = 0, seg_l = 0, key_l = 0;
   float r2_l = 0.f;
   if (lane < cnt) {
     perm_l = j.perm[base + lane];
     seg_l = j.seg_of[base + lane];
+    key_l = j.keys[base + lane];
     if (j.rows2) r2_l = j.rows2[perm_l];
   }
+  uint32_t edge = 0;
+  if (lane == 0 && base > 0) edge = j.keys[base - 1] == j.keys[base];
+  if (lane == 1 && base + cnt < j.n) edge = j.keys[base + cnt] == j.keys[base + cnt - 1];
+  const bool first_before = __shfl_sync(0xffffffffu, edge, 0) != 0;
+  const bool last_after = __shfl_sync(0xffffffffu, edge, 1) != 0;
+  const bool write_mode = j.table == nullptr;
   for (int c0 = 0; c0 < j.dim; c0 += 32) {
     const int c = c0 + lane;
     double acc = 0.0, acc2 = 0.0;
+    int r_start = 0;
     uint32_t cur = __shfl_sync(0xffffffffu, seg_l, 0);
-    auto flush = [&](uint32_t s) {
-      const uint32_t key = j.keys[j.seg_start[s]];
-      if (key >= j.invalid_key) return;
-      const int64_t slot = piece_slot(j, s, chunk);
-      if (slot < 0) {
-        if (c < j.dim) emit1(j, s, key, c, acc);
-        if (j.rows2 && lane == 0 && c0 == 0) emit_companion(j, s, key, acc2);
+    uint32_t cur_key = __shfl_sync(0xffffffffu, key_l, 0);
+    auto flush = [&](int r_end) {
+      if (cur_key >= j.invalid_key) return;
+      const PieceDst dst = piece_dst(r_start == 0 && first_before, r_end == cnt && last_after,
+                                     chunk);
+      if (dst.kind == 0) {
+        float* o = write_mode ? j.out_rows : j.sums;
+        if (c < j.dim) o[(int64_t)cur * j.dim + c] = (float)acc;
+        if (j.rows2 && lane == 0 && c0 == 0) (write_mode ? j.out_rows2 : j.sums2)[cur] = (float)acc2;
       } else {
-        if (c < j.dim) j.part[slot * j.dim + c] = acc;
-        if (j.rows2 && lane == 0 && c0 == 0) j.part2[slot] = acc2;
+        if (c < j.dim) j.part[dst.slot * j.dim + c] = acc;
+        if (j.rows2 && lane == 0 && c0 == 0) j.part2[dst.slot] = acc2;
       }
     };
     for (int r = 0; r < cnt; ++r) {
       const uint32_t pr = __shfl_sync(0xffffffffu, perm_l, r);
       const uint32_t s = __shfl_sync(0xffffffffu, seg_l, r);
+      const uint32_t k = __shfl_sync(0xffffffffu, key_l, r);
       const float r2 = __shfl_sync(0xffffffffu, r2_l, r);
       const float xv = c < j.dim ? j.rows[(int64_t)pr * j.dim + c] : 0.f;
       if (s != cur) {
-        flush(cur);
+        flush(r);
         cur = s;
+        cur_key = k;
+        r_start = r;
         acc = 0.0;
         acc2 = 0.0;
       }
       acc += xv;
       acc2 += r2;
     }
-    flush(cur);
+    flush(cnt);
   }
 }
 
-// One warp per segment: out_local, and the chunk-order sum of the partials of segments that
-// cross chunk boundaries.
-__global__ void __launch_bounds__(256) seg_cross_kernel(SegJob j) {
-  const int lane = threadIdx.x & 31;
+// One thread per (segment, column group): finish segments that cross chunk boundaries (their
+// chunk partials added in chunk order) and, in apply mode, T[key] = fl32(T - lr * sum) for
+// every segment; in write mode, out_local for every segment.  Fully parallel, coalesced.
+template <bool VEC>
+__global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
   const int64_t U = *j.num_unique;
-  const int64_t warps = (int64_t)gridDim.x * 8;
-  for (int64_t s = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); s < U; s += warps) {
-    const uint32_t a = j.seg_start[s], b = j.seg_start[s + 1];
+  const int cols = VEC ? (j.dim >> 2) : j.dim;
+  const int64_t total = U * cols;
+  const bool write_mode = j.table == nullptr;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = e / cols;
+    const int c = (int)(e - u * cols);
+    const uint32_t a = j.seg_start[u], b = j.seg_start[u + 1];
     const uint32_t key = j.keys[a];
     if (key >= j.invalid_key) continue;
-    if (j.out_local && lane == 0) j.out_local[s] = (int64_t)(key % (uint32_t)j.nloc);
+    if (write_mode && c == 0 && j.out_local) j.out_local[u] = (int64_t)(key % (uint32_t)j.nloc);
     const int64_t c0 = a / kChunk, c1 = (b - 1) / kChunk;
-    if (c0 == c1) continue;
-    for (int c = lane; c < j.dim; c += 32) {
-      double acc = j.part[(2 * c0 + 1) * j.dim + c];
-      for (int64_t ch = c0 + 1; ch <= c1; ++ch) acc += j.part[(2 * ch) * j.dim + c];
-      emit1(j, (uint32_t)s, key, c, acc);
+    const bool cross = c0 != c1;
+    if (write_mode && !cross) continue;  // the chunk kernel already wrote it
+    if (VEC) {
+      D4 acc;
+      if (cross) {
+        acc = reinterpret_cast<const D4*>(j.part + (2 * c0 + 1) * j.dim)[c];
+#pragma unroll 4
+        for (int64_t ch = c0 + 1; ch <= c1; ++ch)
+          add4(acc, reinterpret_cast<const D4*>(j.part + (2 * ch) * j.dim)[c]);
+      } else {
+        const float4 s = reinterpret_cast<const float4*>(j.sums + u * j.dim)[c];
+        acc = D4{s.x, s.y, s.z, s.w};
+      }
+      if (write_mode) {
+        reinterpret_cast<float4*>(j.out_rows + u * j.dim)[c] = to_f4(acc);
+      } else {
+        float4* t = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c;
+        float4 w = *t;
+        const double lr = (double)j.lr;
+        w.x = (float)((double)w.x - lr * acc.x);
+        w.y = (float)((double)w.y - lr * acc.y);
+        w.z = (float)((double)w.z - lr * acc.z);
+        w.w = (float)((double)w.w - lr * acc.w);
+        *t = w;
+      }
+    } else {
+      double acc;
+      if (cross) {
+        acc = j.part[(2 * c0 + 1) * j.dim + c];
+#pragma unroll 4
+        for (int64_t ch = c0 + 1; ch <= c1; ++ch) acc += j.part[(2 * ch) * j.dim + c];
+      } else {
+        acc = j.sums[u * j.dim + c];
+      }
+      if (write_mode) {
+        j.out_rows[u * j.dim + c] = (float)acc;
+      } else {
+        float* t = j.table + (int64_t)key * j.dim + c;
+        *t = (float)((double)*t - (double)j.lr * acc);
+      }
     }
-    if (j.rows2 && lane == 0) {
-      double acc = j.part2[2 * c0 + 1];
-      for (int64_t ch = c0 + 1; ch <= c1; ++ch) acc += j.part2[2 * ch];
-      emit_companion(j, (uint32_t)s, key, acc);
+    if (c == 0 && j.rows2) {
+      double acc2;
+      if (cross) {
+        acc2 = j.part2[2 * c0 + 1];
+        for (int64_t ch = c0 + 1; ch <= c1; ++ch) acc2 += j.part2[2 * ch];
+      } else {
+        acc2 = write_mode ? 0.0 : j.sums2[u];
+      }
+      if (write_mode) {
+        j.out_rows2[u] = (float)acc2;
+      } else if (j.table2) {
+        j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * acc2);
+      }
     }
   }
 }
@@ -632,6 +683,7 @@ __global__ void owner_counts_kernel(const uint32_t* keys, const uint32_t* seg_st
 struct SegScratch {
   uint32_t *k0, *v0, *k1, *v1, *seg_start, *seg_of, *tile_cnt;
   double *part, *part2;
+  float *sums, *sums2;
   int64_t* num_unique;
   void* sort_ws;
   size_t sort_ws_bytes;
@@ -651,6 +703,8 @@ static size_t seg_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws,
   x.tile_cnt = c.take<uint32_t>(ntiles + 1);
   x.part = c.take<double>((size_t)2 * nchunks * dim);
   x.part2 = c.take<double>((size_t)2 * nchunks);
+  x.sums = c.take<float>((size_t)n * dim);
+  x.sums2 = c.take<float>((size_t)n);
   x.num_unique = c.take<int64_t>(1);
   x.sort_ws_bytes = radix_sort_ws_bytes(n);
   x.sort_ws = c.take<char>(x.sort_ws_bytes);
@@ -687,18 +741,26 @@ static void bind(SegJob& j, const SegScratch& s, int64_t n) {
   j.n = n;
   j.part = s.part;
   j.part2 = s.part2;
+  j.sums = s.sums;
+  j.sums2 = s.sums2;
 }
 
 static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
   const int64_t nchunks = cdiv(n, kChunk);
   const int grid = (int)std::max<int64_t>(1, cdiv(nchunks, 8));
-  if ((j.dim & 3) == 0 && ((uintptr_t)j.rows & 15) == 0)
+  const bool vec = (j.dim & 3) == 0 && ((uintptr_t)j.rows & 15) == 0 &&
+                   (j.table ? ((uintptr_t)j.table & 15) == 0 : ((uintptr_t)j.out_rows & 15) == 0);
+  if (vec)
     seg_chunk_vec4_kernel<<<grid, 256, 0, st>>>(j);
   else
     seg_chunk_scalar_kernel<<<grid, 256, 0, st>>>(j);
   launched();
-  const int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 8 * num_sms()));
-  seg_cross_kernel<<<cgrid, 256, 0, st>>>(j);
+  const int64_t work = n * (vec ? (j.dim >> 2) : j.dim);  // U <= n
+  const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, 256), 16 * num_sms()));
+  if (vec)
+    seg_apply_kernel<true><<<agrid, 256, 0, st>>>(j);
+  else
+    seg_apply_kernel<false><<<agrid, 256, 0, st>>>(j);
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
