@@ -213,14 +213,15 @@ int32_t tfs_scatter_add_sgd(float* table, int64_t rows, int32_t dim, const int64
                             tfs_device_error* err, void* stream);
 
 /* ==== Diagnostics ===============================================================================
- * C[ks][M x N] = sum_k A(m, k) B(n, k) on the tcgen05 path (bf16 operands; fp32 out, one
- * [M x N] slab per K split; the effective split count is returned in *out_ksplit).  a_mn == 0:
- * A is K-major, A(m, k) = A[m * lda + k]; a_mn != 0: MN-major, A(m, k) = A[k * lda + m]; same
- * for B with ldb.  lda / ldb in elements, multiples of 8; bases 16-byte aligned.  Used by the
- * GEMM unit tests. */
+ * C[M x N] (fp32, row-major) = sum_k A(m, k) B(n, k) on the tcgen05 path with bf16 operands,
+ * K split `ksplit` ways and the splits reduced in-kernel in split order (deterministic).
+ * a_mn == 0: A is K-major, A(m, k) = A[m * lda + k]; a_mn != 0: MN-major, A(m, k) =
+ * A[k * lda + m]; same for B with ldb.  lda / ldb in elements, multiples of 8; bases 16-byte
+ * aligned.  Workspace: tfs_debug_gemm_workspace_bytes.  Used by the GEMM unit tests. */
+size_t tfs_debug_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t ksplit);
 int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb,
                             int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t ksplit,
-                            float* C, int32_t* out_ksplit, void* stream);
+                            float* C, void* ws, size_t ws_bytes, void* stream);
 /* Total number of CUDA kernels this process has launched through libtfs (host counter,
  * incremented at every launch site; graph replays are not counted).  Used by bench.py to
  * report gpu_launches. */

@@ -57,59 +57,88 @@ static int32_t make_tmap(CUtensorMap* map, const Operand& op, uint64_t rows, uin
   return r == CUDA_SUCCESS ? TFS_OK : TFS_ERR_INVALID_ARGUMENT;
 }
 
-template <int MODE, bool A_MN, bool B_MN>
-static int32_t launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const Shape& g,
-                           const EpiParams& ep, int grid, cudaStream_t st) {
+int tiles_of(int M, int N) { return (int)(cdiv(M, BM) * cdiv(N, BN)); }
+
+int effective_split(int K, int ksplit) {
+  const int kb = (int)cdiv(K, BK);
+  ksplit = std::max(1, std::min(ksplit, kb));
+  const int per = (int)cdiv(kb, ksplit);
+  return (int)cdiv(kb, per);
+}
+
+size_t part_floats(int M, int N, int ksplit) {
+  return ksplit > 1 ? (size_t)ksplit * M * N : 0;
+}
+
+static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int K, int ksplit) {
+  if (M <= 0 || N <= 0 || K <= 0) return TFS_ERR_INVALID_ARGUMENT;
+  int32_t rc = make_tmap(&p.ta, A, (uint64_t)M, (uint64_t)K, BM);
+  if (rc != TFS_OK) return rc;
+  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, BN);
+  if (rc != TFS_OK) return rc;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.num_m = (int)cdiv(M, BM);
+  p.num_n = (int)cdiv(N, BN);
+  p.kb_total = (int)cdiv(K, BK);
+  ksplit = std::max(1, std::min(ksplit, p.kb_total));
+  p.kb_per_split = (int)cdiv(p.kb_total, ksplit);
+  p.ksplit = (int)cdiv(p.kb_total, p.kb_per_split);
+  p.units = p.num_m * p.num_n * p.ksplit;
+  p.a_mn = A.mn;
+  p.b_mn = B.mn;
+  return TFS_OK;
+}
+
+template <int MODE>
+static int32_t launch_params(const Params& P, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, A_MN, B_MN>,
+    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmemBytes));
     attr_done = true;
   }
-  gemm_kernel<MODE, A_MN, B_MN><<<grid, kThreads, kSmemBytes, st>>>(ta, tb, g, ep);
+  const int grid = std::min(P.total_units, num_sms());
+  gemm_kernel<MODE><<<grid, kThreads, kSmemBytes, st>>>(P);
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }
 
-int32_t launch(int mode, Operand A, Operand B, int M, int N, int K, int ksplit,
-               const EpiParams& ep, cudaStream_t st, int* ksplit_eff) {
-  if (M <= 0 || N <= 0 || K <= 0) return TFS_ERR_INVALID_ARGUMENT;
-  CUtensorMap ta, tb;
-  int32_t rc = make_tmap(&ta, A, (uint64_t)M, (uint64_t)K, BM);
+int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K,
+                             const EpiParams& ep, cudaStream_t st) {
+  if (A.mn || B.mn) return TFS_ERR_INVALID_ARGUMENT;
+  Params P{};
+  int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1);
   if (rc != TFS_OK) return rc;
-  rc = make_tmap(&tb, B, (uint64_t)N, (uint64_t)K, BN);
-  if (rc != TFS_OK) return rc;
-  Shape g;
-  g.M = M;
-  g.N = N;
-  g.K = K;
-  g.num_m = (int)cdiv(M, BM);
-  g.num_n = (int)cdiv(N, BN);
-  g.kb_total = (int)cdiv(K, BK);
-  ksplit = std::max(1, std::min(ksplit, g.kb_total));
-  g.kb_per_split = (int)cdiv(g.kb_total, ksplit);
-  g.ksplit = (int)cdiv(g.kb_total, g.kb_per_split);
-  g.num_units = g.num_m * g.num_n * g.ksplit;
-  if (ksplit_eff) *ksplit_eff = g.ksplit;
-  const int grid = std::min(g.num_units, num_sms());
-  const int sel = (A.mn ? 1 : 0) | (B.mn ? 2 : 0);
-  switch (mode) {
-    case kStats:
-      if (sel != 0) return TFS_ERR_INVALID_ARGUMENT;
-      return launch_mode<kStats, false, false>(ta, tb, g, ep, grid, st);
-    case kGrad:
-      if (sel != 0) return TFS_ERR_INVALID_ARGUMENT;
-      return launch_mode<kGrad, false, false>(ta, tb, g, ep, grid, st);
-    default:
-      switch (sel) {
-        case 0: return launch_mode<kStore, false, false>(ta, tb, g, ep, grid, st);
-        case 1: return launch_mode<kStore, true, false>(ta, tb, g, ep, grid, st);
-        case 2: return launch_mode<kStore, false, true>(ta, tb, g, ep, grid, st);
-        default: return launch_mode<kStore, true, true>(ta, tb, g, ep, grid, st);
-      }
+  P.nprob = 1;
+  P.total_units = P.p[0].units;
+  P.ep = ep;
+  return mode == kStats ? launch_params<kStats>(P, st) : launch_params<kGrad>(P, st);
+}
+
+// Up to two STORE GEMMs in one persistent launch; the caller orders them by unit size.
+int32_t launch_store(const Gemm* g, int count, cudaStream_t st) {
+  if (count < 1 || count > 2) return TFS_ERR_INVALID_ARGUMENT;
+  Params P{};
+  P.nprob = count;
+  P.total_units = 0;
+  for (int i = 0; i < count; ++i) {
+    Problem& p = P.p[i];
+    int32_t rc = fill_problem(p, g[i].A, g[i].B, g[i].M, g[i].N, g[i].K, g[i].ksplit);
+    if (rc != TFS_OK) return rc;
+    if (p.ksplit > 1 && g[i].part == nullptr) return TFS_ERR_INVALID_ARGUMENT;
+    p.out = g[i].out;
+    p.ldo = g[i].ldo;
+    p.part = g[i].part;
+    p.g = g[i].g;
+    p.wt = g[i].wt;
+    p.ldw = g[i].ldw;
+    P.total_units += p.units;
   }
+  return launch_params<kStore>(P, st);
 }
 
 }  // namespace umma
@@ -343,28 +372,30 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
   }
 }
 
-// dh = sum_s part[s] (split order) + g * bf16(w_true)
-__global__ void dh_finalize_kernel(const float* part, int nsplit, int64_t split_stride, int64_t B,
-                                   int32_t d, const float* g, const float* w_true, float* dh) {
-  const int64_t total = B * d;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+// out = sum_s part[s] (split order) [+ g[row] * bf16(wt)]; float4 columns (N % 4 == 0).
+__global__ void split_finalize_kernel(const float* part, int nsplit, int64_t M, int32_t N,
+                                      const float* g, const float* wt, float* out) {
+  const int64_t n4 = (int64_t)M * N / 4;
+  const int64_t stride4 = (int64_t)M * N / 4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4;
        e += (int64_t)gridDim.x * blockDim.x) {
-    float acc = part[e];
-    for (int s = 1; s < nsplit; ++s) acc += part[s * split_stride + e];
-    const int64_t t = e / d;
-    dh[e] = acc + g[t] * bf16_round(w_true[e]);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < nsplit; ++s) {
+      const float4 x = reinterpret_cast<const float4*>(part)[s * stride4 + e];
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    if (g != nullptr) {
+      const float gr = g[(4 * e) / N];
+      const float4 w = reinterpret_cast<const float4*>(wt)[e];
+      acc.x += gr * bf16_round(w.x);
+      acc.y += gr * bf16_round(w.y);
+      acc.z += gr * bf16_round(w.z);
+      acc.w += gr * bf16_round(w.w);
+    }
+    reinterpret_cast<float4*>(out)[e] = acc;
   }
 }
 
-__global__ void split_sum_kernel(const float* part, int nsplit, int64_t split_stride,
-                                 int64_t total, float* out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    float acc = part[e];
-    for (int s = 1; s < nsplit; ++s) acc += part[s * split_stride + e];
-    out[e] = acc;
-  }
-}
 
 // db_s[j] = sum over the 4*num_m row-quarter partials in order.
 __global__ void dbs_finalize_kernel(const float* part, int nrows, int64_t S, float* db_s) {
@@ -382,18 +413,25 @@ struct F32Ws {
 struct Bf16Ws {
   uint16_t *hb, *wsb, *G;
   float2* stats;
-  float *dbs_part, *dh_part, *dws_part, *cb;
+  float *dbs_part, *cb, *part_dh, *part_dws;
   int32_t *sid, *y32;
   int64_t Sp, Spad;
   int ks_dh, ks_dws;
 };
 
-static int pick_split(int64_t M, int64_t N, int64_t K) {
-  const int64_t base = cdiv(M, umma::BM) * cdiv(N, umma::BN);
-  const int64_t kb = cdiv(K, umma::BK);
-  int64_t ks = cdiv(num_sms(), base);
-  ks = std::max<int64_t>(1, std::min<int64_t>({ks, kb, 8}));
-  return (int)ks;
+// Split-K plan for the backward pair (dW_s: M=S, K=B; dh: M=B, K=S; both N=d) run in one
+// persistent launch: aim for ~2 units per SM of roughly equal k-block count.
+static void plan_backward(int64_t B, int64_t S, int32_t d, int* ks_dh, int* ks_dws) {
+  const int64_t t_dh = umma::tiles_of((int)B, d), t_dws = umma::tiles_of((int)S, d);
+  const int64_t kb_dh = cdiv(S, umma::BK), kb_dws = cdiv(B, umma::BK);
+  const int64_t work = t_dh * kb_dh + t_dws * kb_dws;
+  const int64_t target = std::max<int64_t>(16, cdiv(work, 2 * num_sms()));
+  auto split = [&](int64_t kb) {
+    if (kb <= target + target / 4) return 1;
+    return (int)std::min<int64_t>(16, cdiv(kb, target));
+  };
+  *ks_dh = umma::effective_split((int)S, split(kb_dh));
+  *ks_dws = umma::effective_split((int)B, split(kb_dws));
 }
 
 static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, F32Ws* f, Bf16Ws* w,
@@ -408,15 +446,16 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, F32Ws* f
   const int64_t Spad = std::max<int64_t>(cdiv(S, umma::BN), 1) * umma::BN;
   const int num_m = (int)cdiv(B, umma::BM);
   const int num_n = (int)cdiv(S, umma::BN);
-  const int ks_dh = pick_split(B, d, S), ks_dws = pick_split(S, d, B);
+  int ks_dh = 1, ks_dws = 1;
+  if (S > 0 && B > 0) plan_backward(B, S, d, &ks_dh, &ks_dws);
   Bf16Ws x;
   x.hb = c.take<uint16_t>(B * d);
   x.wsb = c.take<uint16_t>(S * d);
   x.G = c.take<uint16_t>(B * Sp);
   x.stats = c.take<float2>((size_t)2 * num_n * B);
   x.dbs_part = c.take<float>((size_t)4 * num_m * S);
-  x.dh_part = c.take<float>((size_t)ks_dh * B * d);
-  x.dws_part = c.take<float>((size_t)(ks_dws > 1 ? ks_dws : 0) * S * d);
+  x.part_dh = c.take<float>(umma::part_floats((int)B, d, ks_dh));
+  x.part_dws = c.take<float>(umma::part_floats((int)S, d, ks_dws));
   x.cb = c.take<float>(Spad);
   x.sid = c.take<int32_t>(Spad);
   x.y32 = c.take<int32_t>(B);
@@ -500,7 +539,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const Operand hK{w.hb, d, false}, wsK{w.wsb, d, false};
   if (S > 0) {  // pass 1: per-row (max, sum 2^x) of each half tile, log2 domain
     ep.stats = w.stats;
-    rc = umma::launch(umma::kStats, hK, wsK, (int)B, (int)S, d, 1, ep, st, nullptr);
+    rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, ep, st);
     if (rc != TFS_OK) return rc;
   }
   bf16_combine_kernel<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(
@@ -508,48 +547,47 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
       a->lse, a->dw_true, a->db_true);
   launched();
   TFS_LAUNCH_CHECK();
-  if (S > 0) {  // pass 2: G = c exp(Z - lse) -> bf16 G; column partial sums for db_s
-    ep.lse = a->lse;
-    ep.c = a->grad_scale;
-    ep.G = w.G;
-    ep.ldG = w.Sp;
-    ep.dbs_part = w.dbs_part;
-    rc = umma::launch(umma::kGrad, hK, wsK, (int)B, (int)S, d, 1, ep, st, nullptr);
-    if (rc != TFS_OK) return rc;
-    dbs_finalize_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.dbs_part, 4 * num_m, S, a->db_s);
+  if (S == 0) {  // no candidates: dh = g * bf16(w_true)
+    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true,
+                                                             a->w_true, a->dh);
+    launched();
+    TFS_LAUNCH_CHECK();
+    return TFS_OK;
+  }
+  // pass 2: G = c exp(Z - lse) -> bf16 G; column partial sums for db_s
+  ep.lse = a->lse;
+  ep.c = a->grad_scale;
+  ep.G = w.G;
+  ep.ldG = w.Sp;
+  ep.dbs_part = w.dbs_part;
+  rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, ep, st);
+  if (rc != TFS_OK) return rc;
+  dbs_finalize_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.dbs_part, 4 * num_m, S, a->db_s);
+  launched();
+  // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
+  // (A = G K-major, B = W_s MN-major) in one persistent launch; split partials are reduced in
+  // split order by the finalize pass, which also adds the true-class term of dh.
+  umma::Gemm g[2];
+  const bool dws_split = w.ks_dws > 1, dh_split = w.ks_dh > 1;
+  g[0] = umma::Gemm{Operand{w.G, w.Sp, true}, Operand{w.hb, d, true}, (int)S, d, (int)B,
+                    w.ks_dws, a->dw_s, d, w.part_dws, nullptr, nullptr, 0};
+  g[1] = umma::Gemm{Operand{w.G, w.Sp, false}, Operand{w.wsb, d, true}, (int)B, d, (int)S,
+                    w.ks_dh, a->dh, d, w.part_dh, dh_split ? nullptr : a->db_true,
+                    dh_split ? nullptr : a->w_true, d};
+  // larger units first so the static round-robin schedule balances the SMs
+  const int64_t u0 = cdiv(B, umma::BK) / w.ks_dws, u1 = cdiv(S, umma::BK) / w.ks_dh;
+  if (u1 > u0) std::swap(g[0], g[1]);
+  rc = umma::launch_store(g, 2, st);
+  if (rc != TFS_OK) return rc;
+  if (dh_split) {
+    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(w.part_dh, w.ks_dh, B, d, a->db_true,
+                                                             a->w_true, a->dh);
     launched();
   }
-  // dh = G W_s (split-K partials) + g * bf16(w_true):  A = G K-major, B = W_s MN-major.
-  int ks = 1;
-  if (S > 0) {
-    umma::EpiParams e2{};
-    e2.out = w.dh_part;
-    e2.ldo = d;
-    e2.split_stride = B * d;
-    rc = umma::launch(umma::kStore, Operand{w.G, w.Sp, false}, Operand{w.wsb, d, true}, (int)B, d,
-                      (int)S, w.ks_dh, e2, st, &ks);
-    if (rc != TFS_OK) return rc;
-  } else {
-    TFS_CUDA_TRY(cudaMemsetAsync(w.dh_part, 0, sizeof(float) * B * d, st));
-  }
-  dh_finalize_kernel<<<grid1d(B * d), 256, 0, st>>>(w.dh_part, ks, B * d, B, d, a->db_true,
-                                                    a->w_true, a->dh);
-  launched();
-  // dW_s = G^T h:  A = G MN-major, B = h MN-major.
-  if (S > 0) {
-    umma::EpiParams e3{};
-    const bool split = w.ks_dws > 1;
-    e3.out = split ? w.dws_part : a->dw_s;
-    e3.ldo = d;
-    e3.split_stride = S * d;
-    int ks2 = 1;
-    rc = umma::launch(umma::kStore, Operand{w.G, w.Sp, true}, Operand{w.hb, d, true}, (int)S, d,
-                      (int)B, w.ks_dws, e3, st, &ks2);
-    if (rc != TFS_OK) return rc;
-    if (split) {
-      split_sum_kernel<<<grid1d(S * d), 256, 0, st>>>(w.dws_part, ks2, S * d, S * d, a->dw_s);
-      launched();
-    }
+  if (dws_split) {
+    split_finalize_kernel<<<grid1d(S * d / 4), 256, 0, st>>>(w.part_dws, w.ks_dws, S, d, nullptr,
+                                                             nullptr, a->dw_s);
+    launched();
   }
   TFS_LAUNCH_CHECK();
   return TFS_OK;
@@ -604,20 +642,31 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
 
 // Diagnostics: C[ks][M x N] (fp32) = A[M x K] . B[N x K]^T with bf16 operands on the tcgen05
 // path.  Exposed for the GEMM unit test only.
+extern "C" size_t tfs_debug_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K,
+                                                 int32_t ksplit) {
+  const int ks = umma::effective_split(K, ksplit);
+  return umma::part_floats(M, N, ks) * sizeof(float) + 256;
+}
+
 extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B,
                                        int64_t ldb, int32_t b_mn, int32_t M, int32_t N, int32_t K,
-                                       int32_t ksplit, float* C, int32_t* out_ksplit,
+                                       int32_t ksplit, float* C, void* ws, size_t ws_bytes,
                                        void* stream) {
   TFS_REQUIRE(A && B && C && M > 0 && N > 0 && K > 0 && lda % 8 == 0 && ldb % 8 == 0);
   TFS_SUPPORTED();
-  umma::EpiParams e{};
-  e.out = C;
-  e.ldo = N;
-  e.split_stride = (int64_t)M * N;
-  int ks = 1;
-  int32_t rc = umma::launch(umma::kStore, umma::Operand{A, lda, a_mn != 0},
-                            umma::Operand{B, ldb, b_mn != 0}, M, N, K, ksplit, e,
-                            as_stream(stream), &ks);
-  if (out_ksplit) *out_ksplit = ks;
-  return rc;
+  if (ws_bytes < tfs_debug_gemm_workspace_bytes(M, N, K, ksplit)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = as_stream(stream);
+  const int ks = umma::effective_split(K, ksplit);
+  Carver c(ws, ws_bytes);
+  float* part = c.take<float>(umma::part_floats(M, N, ks));
+  umma::Gemm g{umma::Operand{A, lda, a_mn != 0}, umma::Operand{B, ldb, b_mn != 0}, M, N, K, ks,
+               C, N, part, nullptr, nullptr, 0};
+  int32_t rc = umma::launch_store(&g, 1, st);
+  if (rc != TFS_OK || ks == 1) return rc;
+  if (N % 4 != 0) return TFS_ERR_INVALID_ARGUMENT;
+  split_finalize_kernel<<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, nullptr,
+                                                                    nullptr, C);
+  launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
 }

@@ -4,7 +4,7 @@
 // MN-major (row-major [K x rows]: the transposed view), selected per launch, so the softmax
 // backward reads G, W_s and h in the layout they already have -- no transposed copies.
 //
-// CTA = 12 warps, persistent over (m-tile, n-tile, k-split) units:
+// CTA = 12 warps, persistent over (problem, m-tile, n-tile, k-split) units:
 //   warp 0      TMA producer (one lane): A 128x64 and B 256x64 per stage, 128-byte swizzle,
 //               4-stage smem ring guarded by full/empty mbarriers.
 //   warp 1      MMA issuer (one lane): 4 x tcgen05.mma.kind::f16 (M=128, N=256, K=16) per stage
@@ -36,7 +36,7 @@ constexpr int kMNBoxBytes = kMNBox * BK * 2;    // 8 KB
 constexpr int kTmemCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)STAGES * (A_BYTES + B_BYTES) +
-                              256 /*barriers*/;
+                              256 /*barriers + flags*/;
 
 __host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
   return (1u << 4)                       // D format f32
@@ -50,11 +50,7 @@ __host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
 
 enum Mode : int { kStats = 0, kGrad = 1, kStore = 2 };
 
-struct Shape {
-  int M, N, K;
-  int num_m, num_n, ksplit, kb_per_split, kb_total;
-  int num_units;
-};
+
 
 struct EpiParams {
   // STATS / GRAD: corrected logit in log2 units  v = acc * log2(e) + cb[n], excluded (-> -inf)
@@ -68,9 +64,30 @@ struct EpiParams {
   uint16_t* G;       // GRAD: bf16 [M x ldG]
   int64_t ldG;
   float* dbs_part;   // GRAD: [(4*num_m) x N] column sums of bf16(G)
-  float* out;        // STORE: fp32, out[ks * split_stride + m * ldo + n]
+};
+
+// One GEMM of a launch (a launch may carry two: the softmax backward runs dh and dW_s together
+// so their tiles share the 148 SMs).  STORE epilogue: out[m, n] = acc (+ g[m] * bf16(wt[m, n]))
+// when ksplit == 1; with K split `ksplit` ways each split writes its partial to
+// part[ks][m][n] and a finalize pass adds them in split order (fixed order: deterministic).
+struct Problem {
+  CUtensorMap ta, tb;
+  int M, N, K;
+  int num_m, num_n, ksplit, kb_per_split, kb_total, units;
+  int a_mn, b_mn;
+  float* out;
   int64_t ldo;
-  int64_t split_stride;
+  float* part;      // [ksplit x M x N] fp32 (ksplit > 1)
+  const float* g;   // optional row scale of the extra term
+  const float* wt;  // optional [M x ldw] fp32 matrix of the extra term (bf16-rounded)
+  int64_t ldw;
+};
+
+struct Params {
+  Problem p[2];
+  int nprob;
+  int total_units;
+  EpiParams ep;
 };
 
 // ---- PTX wrappers -----------------------------------------------------------------------------
@@ -126,10 +143,9 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uin
   d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
 }
-template <bool MN>
-__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k16) {
+__device__ __forceinline__ uint64_t operand_desc(bool mn, uint32_t base, int k16) {
   // K advance of 16 elements: +32 B inside the swizzled row (K-major), +16 rows (MN-major).
-  return MN ? desc_sw128(base + (uint32_t)k16 * 2048u, kMNBoxBytes, 1024)
+  return mn ? desc_sw128(base + (uint32_t)k16 * 2048u, kMNBoxBytes, 1024)
             : desc_sw128(base + (uint32_t)k16 * 32u, 16, 1024);
 }
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
@@ -163,20 +179,30 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void epi_bar_sync() {  // the 8 epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+}
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-__device__ __forceinline__ void decode_unit(const Shape& g, int u, int& mt, int& nt, int& ks,
-                                            int& kb0, int& kb1) {
-  ks = u % g.ksplit;
-  const int r = u / g.ksplit;
-  mt = r % g.num_m;
-  nt = r / g.num_m;
-  kb0 = ks * g.kb_per_split;
-  kb1 = min(g.kb_total, kb0 + g.kb_per_split);
+struct Unit {
+  int pi, mt, nt, ks, kb0, kb1;
+};
+__device__ __forceinline__ Unit decode_unit(const Params& P, int u) {
+  Unit r;
+  r.pi = (P.nprob > 1 && u >= P.p[0].units) ? 1 : 0;
+  const Problem& q = P.p[r.pi];
+  const int v = r.pi ? u - P.p[0].units : u;
+  r.ks = v % q.ksplit;
+  const int t = v / q.ksplit;
+  r.mt = t % q.num_m;
+  r.nt = t / q.num_m;
+  r.kb0 = r.ks * q.kb_per_split;
+  r.kb1 = min(q.kb_total, r.kb0 + q.kb_per_split);
+  return r;
 }
 
 // Sum over the 32 lanes of v[i] for every i; afterwards lane l holds the sum for column l.
@@ -216,10 +242,8 @@ __device__ __forceinline__ void corrected_logits(const EpiParams& ep, int col0, 
   }
 }
 
-template <int MODE, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                Shape g, EpiParams ep) {
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Params P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -229,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  const EpiParams& ep = P.ep;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -242,8 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tempty + a, kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+    for (int i = 0; i < P.nprob; ++i) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&P.p[i].ta) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&P.p[i].tb) : "memory");
+    }
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -261,27 +288,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < g.num_units; u += gridDim.x) {
-        int mt, nt, ks, kb0, kb1;
-        decode_unit(g, u, mt, nt, ks, kb0, kb1);
-        for (int kb = kb0; kb < kb1; ++kb) {
+      for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
+        const Unit t = decode_unit(P, u);
+        const Problem& q = P.p[t.pi];
+        for (int kb = t.kb0; kb < t.kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           mbar_expect_tx(full + stage, A_BYTES + B_BYTES);
           uint8_t* a = sA + stage * A_BYTES;
           uint8_t* b = sB + stage * B_BYTES;
-          if (A_MN) {
+          if (q.a_mn) {
 #pragma unroll
-            for (int q = 0; q < BM / kMNBox; ++q)
-              tma_load_2d(a + q * kMNBoxBytes, &tmA, mt * BM + q * kMNBox, kb * BK, full + stage);
+            for (int i = 0; i < BM / kMNBox; ++i)
+              tma_load_2d(a + i * kMNBoxBytes, &q.ta, t.mt * BM + i * kMNBox, kb * BK, full + stage);
           } else {
-            tma_load_2d(a, &tmA, kb * BK, mt * BM, full + stage);
+            tma_load_2d(a, &q.ta, kb * BK, t.mt * BM, full + stage);
           }
-          if (B_MN) {
+          if (q.b_mn) {
 #pragma unroll
-            for (int q = 0; q < BN / kMNBox; ++q)
-              tma_load_2d(b + q * kMNBoxBytes, &tmB, nt * BN + q * kMNBox, kb * BK, full + stage);
+            for (int i = 0; i < BN / kMNBox; ++i)
+              tma_load_2d(b + i * kMNBoxBytes, &q.tb, t.nt * BN + i * kMNBox, kb * BK, full + stage);
           } else {
-            tma_load_2d(b, &tmB, kb * BK, nt * BN, full + stage);
+            tma_load_2d(b, &q.tb, kb * BK, t.nt * BN, full + stage);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -293,24 +320,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ================================ MMA issuer ==================================
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int u = blockIdx.x; u < g.num_units; u += gridDim.x) {
-        int mt, nt, ks, kb0, kb1;
-        decode_unit(g, u, mt, nt, ks, kb0, kb1);
+      for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
+        const Unit t = decode_unit(P, u);
+        const bool amn = P.p[t.pi].a_mn != 0, bmn = P.p[t.pi].b_mn != 0;
+        const uint32_t idesc = make_idesc(amn, bmn);
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = t.kb0; kb < t.kb1; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d_tmem, operand_desc<A_MN>(a0, k), operand_desc<B_MN>(b0, k), idesc,
-                      (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_bf16(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
+                      (kb > t.kb0 || k > 0) ? 1u : 0u);
           umma_commit(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
@@ -329,11 +356,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;      // column half of the 256-wide tile
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < g.num_units; u += gridDim.x) {
-      int mt, nt, ks, kb0, kb1;
-      decode_unit(g, u, mt, nt, ks, kb0, kb1);
-      const int row = mt * BM + quarter * 32 + lane;
-      const bool row_ok = row < g.M;
+    for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
+      const Unit t = decode_unit(P, u);
+      const Problem& q = P.p[t.pi];
+      const int rt = quarter * 32 + lane;  // row within the tile
+      const int row = t.mt * BM + rt;
+      const bool row_ok = row < q.M;
       int32_t y = -2;
       float lse2 = 0.f;
       if (MODE != kStore && row_ok) y = ep.y[row];
@@ -345,16 +373,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         const int ct = half * 128 + c * 32;  // column within the tile
-        const int col0 = nt * BN + ct;
+        const int col0 = t.nt * BN + ct;
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + ct), v);
         if (MODE == kStats) {
           corrected_logits(ep, col0, y, v);
           float m4[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            m4[q] = fmaxf(fmaxf(fmaxf(v[q], v[q + 4]), fmaxf(v[q + 8], v[q + 12])),
-                          fmaxf(fmaxf(v[q + 16], v[q + 20]), fmaxf(v[q + 24], v[q + 28])));
+          for (int i = 0; i < 4; ++i)
+            m4[i] = fmaxf(fmaxf(fmaxf(v[i], v[i + 4]), fmaxf(v[i + 8], v[i + 12])),
+                          fmaxf(fmaxf(v[i + 16], v[i + 20]), fmaxf(v[i + 24], v[i + 28])));
           const float cm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
           if (cm > -INFINITY) {
             const float nm = fmaxf(run_m, cm);
@@ -377,34 +405,52 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (row_ok) {
             uint16_t* gr = ep.G + (int64_t)row * ep.ldG + col0;
-            if (col0 + 32 <= g.N) {
+            if (col0 + 32 <= q.N) {
               uint4* d4 = (uint4*)gr;
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                d4[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
-                                   packed[4 * q + 3]);
+              for (int i = 0; i < 4; ++i)
+                d4[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                                   packed[4 * i + 3]);
             } else {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                if (col0 + i < g.N)
+                if (col0 + i < q.N)
                   gr[i] = (uint16_t)((i & 1) ? (packed[i >> 1] >> 16) : (packed[i >> 1] & 0xffffu));
             }
           }
           const float colsum = transpose_reduce32(v, lane);
-          if (col0 + lane < g.N)
-            ep.dbs_part[(int64_t)(mt * 4 + quarter) * g.N + col0 + lane] = colsum;
-        } else {
+          if (col0 + lane < q.N)
+            ep.dbs_part[(int64_t)(t.mt * 4 + quarter) * q.N + col0 + lane] = colsum;
+        } else if (q.ksplit > 1) {
+          // split partial, row-major [ksplit][M][N]; reduced (in split order) by a finalize pass
           if (row_ok) {
-            float* o = ep.out + (int64_t)ks * ep.split_stride + (int64_t)row * ep.ldo + col0;
-            if (col0 + 32 <= g.N) {
+            float* o = q.part + ((int64_t)t.ks * q.M + row) * q.N + col0;
+            if (col0 + 32 <= q.N) {
 #pragma unroll
-              for (int q = 0; q < 8; ++q)
-                ((float4*)o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              for (int i = 0; i < 8; ++i)
+                ((float4*)o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             } else {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                if (col0 + i < g.N) o[i] = v[i];
+                if (col0 + i < q.N) o[i] = v[i];
             }
+          }
+        } else if (row_ok) {
+          if (q.g != nullptr) {
+            const float gr = q.g[row];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < q.N) v[i] += gr * bf16_round(q.wt[(int64_t)row * q.ldw + col0 + i]);
+          }
+          float* o = q.out + (int64_t)row * q.ldo + col0;
+          if (col0 + 32 <= q.N) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              ((float4*)o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < q.N) o[i] = v[i];
           }
         }
       }
@@ -412,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
       if (MODE == kStats && row_ok)
-        ep.stats[(int64_t)(nt * 2 + half) * g.M + row] = make_float2(run_m, run_s);
+        ep.stats[(int64_t)(t.nt * 2 + half) * q.M + row] = make_float2(run_m, run_s);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -434,8 +480,26 @@ struct Operand {
   bool mn;
 };
 
-int32_t launch(int mode, Operand A, Operand B, int M, int N, int K, int ksplit,
-               const EpiParams& ep, cudaStream_t st, int* ksplit_eff);
+// One GEMM to launch.  ksplit > 1 needs part (ksplit x M x N fp32).
+struct Gemm {
+  Operand A, B;
+  int M, N, K, ksplit;
+  float* out;
+  int64_t ldo;
+  float* part;
+  const float* g;
+  const float* wt;
+  int64_t ldw;
+};
+
+// Scratch size (floats) of the split partials of a GEMM.
+size_t part_floats(int M, int N, int ksplit);
+int tiles_of(int M, int N);
+int effective_split(int K, int ksplit);
+
+int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K,
+                             const EpiParams& ep, cudaStream_t st);
+int32_t launch_store(const Gemm* g, int count, cudaStream_t st);
 
 }  // namespace umma
 }  // namespace tfs

@@ -209,9 +209,10 @@ def debug_gemm_bf16(A, B, ksplit: int = 1, a_mn: bool = False, b_mn: bool = Fals
     or, with a_mn, [K, M] (MN-major); likewise B is [N, K] or [K, N]."""
     M, K = (A.shape[1], A.shape[0]) if a_mn else A.shape
     N = B.shape[1] if b_mn else B.shape[0]
-    C = torch.empty((max(ksplit, 1), M, N), dtype=torch.float32, device=A.device)
-    ks = ctypes.c_int32(0)
-    check(_lib.lib().tfs_debug_gemm_bf16(_p(A), A.stride(0), int(a_mn), _p(B), B.stride(0),
-                                         int(b_mn), M, N, K, ksplit, _p(C), ctypes.byref(ks),
-                                         _stream()), "tfs_debug_gemm_bf16")
-    return C[: ks.value]
+    C = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    L = _lib.lib()
+    ws = _ws(L.tfs_debug_gemm_workspace_bytes(M, N, K, ksplit), A.device)
+    check(L.tfs_debug_gemm_bf16(_p(A), A.stride(0), int(a_mn), _p(B), B.stride(0), int(b_mn),
+                                M, N, K, ksplit, _p(C), _p(ws), ws.numel(), _stream()),
+          "tfs_debug_gemm_bf16")
+    return C
