@@ -6,7 +6,7 @@
 // Design: latency/HBM-bound integer work.  A tile of 1024 items per 256-thread
 // CTA; per-tile digit histograms; every CTA computes its own global offsets from the (small)
 // histogram table, so a pass is two launches with no separate scan.  Within a tile the rank
-// of an item among equal digits comes from warp __match_any_sync + popc and a per-round
+// of an item among equal digits comes from an 8-ballot warp digit match + popc and a per-round
 // warp-order prefix, which makes the scatter stable (original order kept: R-2).
 //
 // Segmented sums over the id-sorted rows use a FIXED reduction structure (R-16): the sorted
@@ -26,7 +26,7 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = 4;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 1024 items per CTA
 constexpr int kMaxBuckets = 256;
-constexpr int kChunk = 16;  // sorted rows per warp in the segmented sums
+constexpr int kChunk = 8;  // sorted rows per warp in the segmented sums
 
 struct DigitSrc {
   int mode;
@@ -100,6 +100,20 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
   __syncthreads();
   if (total) *total = all;
   return base + x - v;
+}
+
+// Lanes holding the same 8-bit digit as this lane (valid lanes only): 8 ballots, one per digit
+// bit -- much cheaper than a general match on this part.
+__device__ __forceinline__ uint32_t match_digit8(int dg, bool valid) {
+  const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+  uint32_t peers = valid ? vmask : 0u;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const bool bit = (dg >> b) & 1;
+    const uint32_t m = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
 }
 
 __global__ void __launch_bounds__(kSortThreads) digit_hist_kernel(DigitSrc src, int64_t n,
@@ -185,7 +199,7 @@ __global__ void __launch_bounds__(kSortThreads) digit_scatter_kernel(DigitSrc sr
     const int dg = it[j].digit;
     for (int b = tid; b < kSortWarps * nb; b += kSortThreads) wcnt[b / nb][b % nb] = 0;
     __syncthreads();
-    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t peers = match_digit8(dg & 0xff, dg >= 0);
     const uint32_t rank = __popc(peers & lanemask_lt());
     if (dg >= 0 && rank == 0) wcnt[warp][dg] = __popc(peers);
     __syncthreads();
@@ -404,6 +418,9 @@ struct SegJob {
   // chunk c and continues after it.
   double* part;   // [2 * nchunks x dim]
   double* part2;  // [2 * nchunks]
+  // segments that cross a chunk boundary (appended by the chunk kernel; order is irrelevant)
+  uint32_t* cross_list;
+  uint32_t* cross_count;
 };
 
 struct D4 {
@@ -431,21 +448,27 @@ __device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_afte
   return PieceDst{0, 0};
 }
 
-// One warp per chunk of kChunk sorted rows, float4 columns (dim % 4 == 0).  Only gradient rows
-// are read; every decision uses per-lane data loaded up front (no dependent lookups).
-__global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j) {
+// One warp per (chunk of kChunk sorted rows, slice of 32 float4 columns), dim % 4 == 0.
+// All kChunk gradient rows -- and, in apply mode, the table row of every segment that lies
+// inside the chunk -- are loaded at once; each segment's rows are added in sorted order in
+// fp64 and the segment is applied (T = fl32(T - lr * g)) or written directly.  Pieces of
+// segments that cross a chunk boundary go to partial slots and the segment to cross_list.
+__global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j, int nslices) {
   const int lane = threadIdx.x & 31;
-  const int64_t chunk = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t chunk = gw / nslices;
+  const int slice = (int)(gw - chunk * nslices);
   const int64_t base = chunk * kChunk;
   if (base >= j.n) return;
   const int cnt = (int)min((int64_t)kChunk, j.n - base);
+  const bool write_mode = j.table == nullptr;
   uint32_t perm_l = 0, seg_l = 0, key_l = 0;
   float r2_l = 0.f;
   if (lane < cnt) {
     perm_l = j.perm[base + lane];
     seg_l = j.seg_of[base + lane];
     key_l = j.keys[base + lane];
-    if (j.rows2) r2_l = j.rows2[perm_l];
+    if (j.rows2 && slice == 0) r2_l = j.rows2[perm_l];
   }
   // Does the first segment start before this chunk / the last one continue after it?
   uint32_t edge = 0;
@@ -453,74 +476,122 @@ __global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j) {
   if (lane == 1 && base + cnt < j.n) edge = j.keys[base + cnt] == j.keys[base + cnt - 1];
   const bool first_before = __shfl_sync(0xffffffffu, edge, 0) != 0;
   const bool last_after = __shfl_sync(0xffffffffu, edge, 1) != 0;
-  const bool write_mode = j.table == nullptr;
+  // Segment structure of the chunk as bit masks over rows.
+  const uint32_t key_prev = __shfl_up_sync(0xffffffffu, key_l, 1);
+  const bool head_l = lane < cnt && (lane == 0 ? !first_before : key_l != key_prev);
+  const uint32_t H = __ballot_sync(0xffffffffu, head_l);                 // segment starts
+  const bool end_l = lane < cnt && (lane == cnt - 1 ? !last_after : ((H >> (lane + 1)) & 1));
+  const uint32_t E = __ballot_sync(0xffffffffu, end_l);                  // segment ends
+  const bool whole_l = end_l && (H & ((2u << lane) - 1u)) != 0 && key_l < j.invalid_key;
+  const uint32_t WE = __ballot_sync(0xffffffffu, whole_l);               // ends of whole segments
   const int n4 = j.dim >> 2;
-  for (int c4_0 = 0; c4_0 < n4; c4_0 += 128) {
-    D4 acc[4];
-    double acc2 = 0.0;
-    int r_start = 0;
-    uint32_t cur = __shfl_sync(0xffffffffu, seg_l, 0);
-    uint32_t cur_key = __shfl_sync(0xffffffffu, key_l, 0);
-    auto flush = [&](int r_end) {
-      if (cur_key >= j.invalid_key) return;
-      const PieceDst dst = piece_dst(r_start == 0 && first_before, r_end == cnt && last_after,
-                                     chunk);
-      if (dst.kind == 0) {
-        float* o = write_mode ? j.out_rows : j.sums;
+  const int c4 = slice * 32 + lane;
+  const bool col_ok = c4 < n4;
+  float4 x[kChunk], t[kChunk];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int c4 = c4_0 + v * 32 + lane;
-          if (c4 < n4) reinterpret_cast<float4*>(o + (int64_t)cur * j.dim)[c4] = to_f4(acc[v]);
-        }
-        if (j.rows2 && lane == 0 && c4_0 == 0) {
-          float* o2 = write_mode ? j.out_rows2 : j.sums2;
-          o2[cur] = (float)acc2;
+  for (int r = 0; r < kChunk; ++r) {  // every row of the chunk in flight at once
+    const uint32_t pr = __shfl_sync(0xffffffffu, perm_l, r);
+    const uint32_t kr = __shfl_sync(0xffffffffu, key_l, r);
+    x[r] = (r < cnt && col_ok) ? __ldg((const float4*)(j.rows + (int64_t)pr * j.dim) + c4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    t[r] = (!write_mode && ((WE >> r) & 1) && col_ok)
+               ? *((const float4*)(j.table + (int64_t)kr * j.dim) + c4)
+               : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  D4 acc = D4{0.0, 0.0, 0.0, 0.0};
+  double acc2 = 0.0;
+  int r_start = 0;
+#pragma unroll
+  for (int r = 0; r < kChunk; ++r) {
+    if (r >= cnt) break;
+    const float r2 = __shfl_sync(0xffffffffu, r2_l, r);
+    if (r > 0 && ((H >> r) & 1)) {
+      acc = D4{0.0, 0.0, 0.0, 0.0};
+      acc2 = 0.0;
+      r_start = r;
+    }
+    add4(acc, x[r]);
+    acc2 += r2;
+    if (!(((E >> r) & 1) || r == cnt - 1)) continue;
+    // ---- the piece [r_start, r] is complete
+    const uint32_t sg = __shfl_sync(0xffffffffu, seg_l, r);
+    const uint32_t kr = __shfl_sync(0xffffffffu, key_l, r);
+    if (kr >= j.invalid_key) continue;
+    const bool starts_before = r_start == 0 && first_before;
+    const bool ends_after = r == cnt - 1 && last_after;
+    if (!starts_before && !ends_after) {  // whole segment: apply / write now
+      if (write_mode) {
+        if (col_ok) reinterpret_cast<float4*>(j.out_rows + (int64_t)sg * j.dim)[c4] = to_f4(acc);
+        if (lane == 0 && slice == 0) {
+          if (j.out_local) j.out_local[sg] = (int64_t)(kr % (uint32_t)j.nloc);
+          if (j.rows2) j.out_rows2[sg] = (float)acc2;
         }
       } else {
-        double* p = j.part + dst.slot * j.dim;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int c4 = c4_0 + v * 32 + lane;
-          if (c4 < n4) reinterpret_cast<D4*>(p)[c4] = acc[v];
+        if (col_ok) {
+          const double lr = (double)j.lr;
+          float4 w = t[r];
+          w.x = (float)((double)w.x - lr * acc.x);
+          w.y = (float)((double)w.y - lr * acc.y);
+          w.z = (float)((double)w.z - lr * acc.z);
+          w.w = (float)((double)w.w - lr * acc.w);
+          *((float4*)(j.table + (int64_t)kr * j.dim) + c4) = w;
         }
-        if (j.rows2 && lane == 0 && c4_0 == 0) j.part2[dst.slot] = acc2;
+        if (j.table2 && lane == 0 && slice == 0)
+          j.table2[kr] = (float)((double)j.table2[kr] - (double)j.lr * acc2);
       }
-    };
-#pragma unroll
-    for (int v = 0; v < 4; ++v) acc[v] = D4{0.0, 0.0, 0.0, 0.0};
-    for (int r0 = 0; r0 < cnt; r0 += 4) {
-      float4 x[4][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {  // four rows' loads in flight
-        const uint32_t pr = __shfl_sync(0xffffffffu, perm_l, r0 + u);
-        const float4* row = (const float4*)(j.rows + (int64_t)pr * j.dim);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int c4 = c4_0 + v * 32 + lane;
-          x[u][v] = (r0 + u < cnt && c4 < n4) ? __ldg(row + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (r0 + u >= cnt) break;
-        const uint32_t s = __shfl_sync(0xffffffffu, seg_l, r0 + u);
-        const uint32_t k = __shfl_sync(0xffffffffu, key_l, r0 + u);
-        const float r2 = __shfl_sync(0xffffffffu, r2_l, r0 + u);
-        if (s != cur) {
-          flush(r0 + u);
-          cur = s;
-          cur_key = k;
-          r_start = r0 + u;
-#pragma unroll
-          for (int v = 0; v < 4; ++v) acc[v] = D4{0.0, 0.0, 0.0, 0.0};
-          acc2 = 0.0;
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) add4(acc[v], x[u][v]);
-        acc2 += r2;
+    } else {
+      const int64_t slot = starts_before ? 2 * chunk : 2 * chunk + 1;
+      if (col_ok) reinterpret_cast<D4*>(j.part + slot * j.dim)[c4] = acc;
+      if (lane == 0 && slice == 0) {
+        if (j.rows2) j.part2[slot] = acc2;
+        if (!starts_before) j.cross_list[atomicAdd(j.cross_count, 1u)] = sg;
       }
     }
-    flush(cnt);
+  }
+}
+
+// One thread per (crossing segment, float4 column): chunk partials added in chunk order,
+// then applied / written.
+__global__ void __launch_bounds__(256) seg_cross_vec4_kernel(SegJob j) {
+  const uint32_t ncross = *j.cross_count;
+  const int n4 = j.dim >> 2;
+  const int64_t total = (int64_t)ncross * n4;
+  const bool write_mode = j.table == nullptr;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / n4;
+    const int c = (int)(e - q * n4);
+    const uint32_t s = j.cross_list[q];
+    const uint32_t a = j.seg_start[s], b = j.seg_start[s + 1];
+    const uint32_t key = j.keys[a];
+    const int64_t c0 = a / kChunk, c1 = (b - 1) / kChunk;
+    D4 acc = reinterpret_cast<const D4*>(j.part + (2 * c0 + 1) * j.dim)[c];
+#pragma unroll 16
+    for (int64_t ch = c0 + 1; ch <= c1; ++ch)
+      add4(acc, reinterpret_cast<const D4*>(j.part + (2 * ch) * j.dim)[c]);
+    if (write_mode) {
+      reinterpret_cast<float4*>(j.out_rows + (int64_t)s * j.dim)[c] = to_f4(acc);
+    } else {
+      float4* tp = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c;
+      float4 w = *tp;
+      const double lr = (double)j.lr;
+      w.x = (float)((double)w.x - lr * acc.x);
+      w.y = (float)((double)w.y - lr * acc.y);
+      w.z = (float)((double)w.z - lr * acc.z);
+      w.w = (float)((double)w.w - lr * acc.w);
+      *tp = w;
+    }
+    if (c == 0) {
+      if (write_mode && j.out_local) j.out_local[s] = (int64_t)(key % (uint32_t)j.nloc);
+      if (j.rows2) {
+        double acc2 = j.part2[2 * c0 + 1];
+        for (int64_t ch = c0 + 1; ch <= c1; ++ch) acc2 += j.part2[2 * ch];
+        if (write_mode)
+          j.out_rows2[s] = (float)acc2;
+        else if (j.table2)
+          j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * acc2);
+      }
+    }
   }
 }
 
@@ -684,6 +755,7 @@ struct SegScratch {
   uint32_t *k0, *v0, *k1, *v1, *seg_start, *seg_of, *tile_cnt;
   double *part, *part2;
   float *sums, *sums2;
+  uint32_t *cross_list, *cross_count;
   int64_t* num_unique;
   void* sort_ws;
   size_t sort_ws_bytes;
@@ -705,6 +777,8 @@ static size_t seg_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws,
   x.part2 = c.take<double>((size_t)2 * nchunks);
   x.sums = c.take<float>((size_t)n * dim);
   x.sums2 = c.take<float>((size_t)n);
+  x.cross_list = c.take<uint32_t>((size_t)nchunks + 1);
+  x.cross_count = c.take<uint32_t>(1);
   x.num_unique = c.take<int64_t>(1);
   x.sort_ws_bytes = radix_sort_ws_bytes(n);
   x.sort_ws = c.take<char>(x.sort_ws_bytes);
@@ -712,9 +786,177 @@ static size_t seg_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws,
   return c.used + 256;
 }
 
+// Single-CTA sort + segmentation for n <= kSmallMax (both lookups of the X workload): keys are
+// built, radix-sorted (8-bit LSD passes, stable) and segmented entirely in shared memory by
+// one 1024-thread CTA -- one launch instead of nine.  Warp w owns the contiguous input range
+// [w * per, (w + 1) * per); its digit counts are private (no per-round CTA barriers), and one
+// CTA-wide exclusive scan over the (digit, warp) counters in digit-major order per pass makes
+// the scatter stable (equal digits keep warp order, and lane order inside a warp).
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallMax = 4096;  // above this the multi-CTA passes are faster
+constexpr int kCntWords = 32 * 257;
+
+__device__ __forceinline__ uint32_t cta1024_exclusive_scan(uint32_t v, uint32_t* wsum,
+                                                           uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = wsum[lane], z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z - w;  // exclusive warp offsets
+    if (lane == 31) wsum[32] = z;
+  }
+  __syncthreads();
+  const uint32_t r = wsum[warp] + x - v;
+  if (total) *total = wsum[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1) sort_segment_small_kernel(
+    const int64_t* ids, int n, int64_t limit, int32_t R, int64_t nloc, int composite, int passes,
+    uint32_t* keys_out, uint32_t* perm_out, uint32_t* seg_start, uint32_t* seg_of,
+    int64_t* num_unique, tfs_device_error* err) {
+  extern __shared__ uint32_t sm[];
+  __shared__ uint32_t wsum[33];
+  const int cap = (n + 31) & ~31;
+  // counters: warp w, digit d at cnt[w * 257 + d] (pitch 257: conflict-free per-warp updates
+  // and digit-major scans)
+  uint32_t* cnt = sm;
+  uint32_t* ka = cnt + kCntWords;
+  uint32_t* kb = ka + cap;
+  uint16_t* va = (uint16_t*)(kb + cap);
+  uint16_t* vb = va + cap;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  for (int i = tid; i < n; i += kSmallThreads) {
+    const int64_t id = ids[i];
+    uint32_t key;
+    if (id < 0 || id >= limit) {
+      report_error(err, TFS_ERR_OUT_OF_RANGE, i);
+      key = composite ? (uint32_t)(R * nloc) : (uint32_t)limit;
+    } else {
+      key = composite ? (uint32_t)((id % R) * nloc + id / R) : (uint32_t)id;
+    }
+    ka[i] = key;
+    va[i] = (uint16_t)i;
+  }
+  const int per = (((n + 31) / 32) + 31) & ~31;  // items per warp, a multiple of 32
+  const int lo = min(n, warp * per), hi = min(n, lo + per);
+  __syncthreads();
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t* ks = ka;
+    const uint16_t* vs = va;
+    uint32_t* kd = kb;
+    uint16_t* vd = vb;
+    const int shift = 8 * p;
+    for (int d = lane; d < 256; d += 32) cnt[warp * 257 + d] = 0;
+    __syncwarp();
+    for (int base = lo; base < hi; base += 32) {  // sweep 1: this warp's digit counts
+      const int i = base + lane;
+      const int dg = i < hi ? (int)((ks[i] >> shift) & 0xffu) : 256;
+      const uint32_t peers = match_digit8(dg & 0xff, dg < 256);
+      if (dg < 256 && lane == __ffs(peers) - 1) cnt[warp * 257 + dg] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive scan of the 8192 counters in (digit, warp) order; 8 per thread
+      // entry e = d * 32 + w of the digit-major order lives at cnt[w * 257 + d]
+      uint32_t c[8], s = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = tid * 8 + j;
+        c[j] = cnt[(e & 31) * 257 + (e >> 5)];
+        s += c[j];
+      }
+      uint32_t run = cta1024_exclusive_scan(s, wsum, nullptr);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = tid * 8 + j;
+        cnt[(e & 31) * 257 + (e >> 5)] = run;
+        run += c[j];
+      }
+    }
+    __syncthreads();
+    for (int base = lo; base < hi; base += 32) {  // sweep 2: stable scatter
+      const int i = base + lane;
+      const bool valid = i < hi;
+      const uint32_t k = valid ? ks[i] : 0u;
+      const int dg = valid ? (int)((k >> shift) & 0xffu) : 256;
+      const uint32_t peers = match_digit8(dg & 0xff, valid);
+      uint32_t off = 0;
+      if (valid) {
+        off = cnt[warp * 257 + dg];
+        const uint32_t pos = off + __popc(peers & lanemask_lt());
+        kd[pos] = k;
+        vd[pos] = vs[i];
+      }
+      __syncwarp();
+      if (valid && lane == __ffs(peers) - 1) cnt[warp * 257 + dg] = off + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    uint32_t* kt = ka; ka = kb; kb = kt;
+    uint16_t* vt = va; va = vb; vb = vt;
+  }
+  // Segments of the sorted keys: heads, segment starts, segment of every position.
+  const uint32_t* k = ka;
+  const uint16_t* v = va;
+  const int per_t = (n + kSmallThreads - 1) / kSmallThreads;
+  const int t0 = min(n, tid * per_t), t1 = min(n, t0 + per_t);
+  uint32_t h = 0;
+  for (int i = t0; i < t1; ++i) h += (i == 0 || k[i] != k[i - 1]);
+  uint32_t total;
+  uint32_t pos = cta1024_exclusive_scan(h, wsum, &total);
+  for (int i = t0; i < t1; ++i) {
+    if (i == 0 || k[i] != k[i - 1]) seg_start[pos++] = (uint32_t)i;
+    seg_of[i] = pos - 1;
+    keys_out[i] = k[i];
+    perm_out[i] = v[i];
+  }
+  if (tid == 0) {
+    *num_unique = total;
+    seg_start[total] = (uint32_t)n;
+  }
+}
+
+static size_t small_sort_smem(int64_t n) {
+  const int64_t cap = (n + 31) & ~31;
+  return (size_t)(kCntWords * 4 + cap * 4 * 2 + cap * 2 * 2);
+}
+
 static int32_t sort_and_segment(const int64_t* ids, int64_t n, int64_t limit, int32_t R,
                                 int64_t nloc, int composite, uint32_t key_max, SegScratch& s,
                                 tfs_device_error* err, cudaStream_t st) {
+  if (n <= kSmallMax) {
+    const size_t smem = small_sort_smem(n);
+    static bool attr = false;
+    if (!attr) {
+      TFS_CUDA_TRY(cudaFuncSetAttribute(sort_segment_small_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)small_sort_smem(kSmallMax)));
+      attr = true;
+    }
+    const int bits = bits_for(key_max);
+    const int passes = bits <= 8 ? 1 : (bits + 7) / 8;
+    sort_segment_small_kernel<<<1, kSmallThreads, smem, st>>>(
+        ids, (int)n, limit, R, nloc, composite, passes, s.k1, s.v1, s.seg_start, s.seg_of,
+        s.num_unique, err);
+    launched();
+    TFS_LAUNCH_CHECK();
+    return TFS_OK;
+  }
   const int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
   make_keys_kernel<<<grid, 256, 0, st>>>(ids, n, limit, R, nloc, composite, s.k0, s.v0, err);
   launched();
@@ -743,6 +985,8 @@ static void bind(SegJob& j, const SegScratch& s, int64_t n) {
   j.part2 = s.part2;
   j.sums = s.sums;
   j.sums2 = s.sums2;
+  j.cross_list = s.cross_list;
+  j.cross_count = s.cross_count;
 }
 
 static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
@@ -750,18 +994,24 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, cdiv(nchunks, 8));
   const bool vec = (j.dim & 3) == 0 && ((uintptr_t)j.rows & 15) == 0 &&
                    (j.table ? ((uintptr_t)j.table & 15) == 0 : ((uintptr_t)j.out_rows & 15) == 0);
-  if (vec)
-    seg_chunk_vec4_kernel<<<grid, 256, 0, st>>>(j);
-  else
+  if (vec) {
+    TFS_CUDA_TRY(cudaMemsetAsync(j.cross_count, 0, sizeof(uint32_t), st));
+    const int nslices = (int)cdiv(j.dim >> 2, 32);
+    const int vgrid = (int)std::max<int64_t>(1, cdiv(nchunks * nslices, 8));
+    seg_chunk_vec4_kernel<<<vgrid, 256, 0, st>>>(j, nslices);
+    launched();
+    const int64_t work = (nchunks + 1) * (j.dim >> 2);  // crossing segments <= nchunks
+    const int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, 256), 4 * num_sms()));
+    seg_cross_vec4_kernel<<<cgrid, 256, 0, st>>>(j);
+    launched();
+  } else {
     seg_chunk_scalar_kernel<<<grid, 256, 0, st>>>(j);
-  launched();
-  const int64_t work = n * (vec ? (j.dim >> 2) : j.dim);  // U <= n
-  const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, 256), 16 * num_sms()));
-  if (vec)
-    seg_apply_kernel<true><<<agrid, 256, 0, st>>>(j);
-  else
+    launched();
+    const int64_t work = n * j.dim;  // U <= n
+    const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, 256), 16 * num_sms()));
     seg_apply_kernel<false><<<agrid, 256, 0, st>>>(j);
-  launched();
+    launched();
+  }
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }
