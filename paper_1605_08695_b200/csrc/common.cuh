@@ -90,7 +90,8 @@ __device__ __forceinline__ float bf16_round(float x) {
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  return (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // one cvt.rn.bf16x2.f32; lo in bits 0-15
+  return *reinterpret_cast<uint32_t*>(&v);
 }
 
 }  // namespace tfs

@@ -70,17 +70,20 @@ size_t part_floats(int M, int N, int ksplit) {
   return ksplit > 1 ? (size_t)ksplit * M * N : 0;
 }
 
-static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int K, int ksplit) {
-  if (M <= 0 || N <= 0 || K <= 0) return TFS_ERR_INVALID_ARGUMENT;
+static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int K, int ksplit,
+                            int bn = BN) {
+  if (M <= 0 || N <= 0 || K <= 0 || bn < 16 || bn > BN || bn % 16 != 0)
+    return TFS_ERR_INVALID_ARGUMENT;
   int32_t rc = make_tmap(&p.ta, A, (uint64_t)M, (uint64_t)K, BM);
   if (rc != TFS_OK) return rc;
-  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, BN);
+  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, (uint32_t)bn);
   if (rc != TFS_OK) return rc;
   p.M = M;
   p.N = N;
   p.K = K;
+  p.bn = bn;
   p.num_m = (int)cdiv(M, BM);
-  p.num_n = (int)cdiv(N, BN);
+  p.num_n = (int)cdiv(N, bn);
   p.kb_total = (int)cdiv(K, BK);
   ksplit = std::max(1, std::min(ksplit, p.kb_total));
   p.kb_per_split = (int)cdiv(p.kb_total, ksplit);
@@ -88,6 +91,9 @@ static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int 
   p.units = p.num_m * p.num_n * p.ksplit;
   p.a_mn = A.mn;
   p.b_mn = B.mn;
+  p.N_out = N;
+  p.col_out = nullptr;
+  p.col_idx = -1;
   return TFS_OK;
 }
 
@@ -127,11 +133,15 @@ int32_t launch_store(const Gemm* g, int count, cudaStream_t st) {
   P.total_units = 0;
   for (int i = 0; i < count; ++i) {
     Problem& p = P.p[i];
-    int32_t rc = fill_problem(p, g[i].A, g[i].B, g[i].M, g[i].N, g[i].K, g[i].ksplit);
+    int32_t rc = fill_problem(p, g[i].A, g[i].B, g[i].M, g[i].N, g[i].K, g[i].ksplit,
+                              g[i].bn > 0 ? g[i].bn : BN);
     if (rc != TFS_OK) return rc;
     if (p.ksplit > 1 && g[i].part == nullptr) return TFS_ERR_INVALID_ARGUMENT;
     p.out = g[i].out;
     p.ldo = g[i].ldo;
+    p.N_out = g[i].N_out;
+    p.col_out = g[i].col_out;
+    p.col_idx = g[i].col_out ? g[i].col_idx : -1;
     p.part = g[i].part;
     p.g = g[i].g;
     p.wt = g[i].wt;
@@ -312,6 +322,55 @@ __global__ void to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
     dst[i] = f32_to_bf16_bits(src[i]);
 }
 
+// db_s[j] = sum_t G[t, j] over the bf16 G [B x ldG]: block = 32 columns (4 x 16-byte chunks)
+// x 64 row groups; each thread sums its rows in order, then the 64 partials are added in
+// row-group order (fixed summation order, no atomics).
+constexpr int kColsumChunks = 4, kColsumGroups = 64;
+__global__ void __launch_bounds__(256) g_colsum_kernel(const uint16_t* G, int64_t B, int64_t S,
+                                                       int64_t ldG, float* db_s) {
+  __shared__ float red[kColsumGroups][kColsumChunks * 8 + 1];
+  const int chunk = threadIdx.x % kColsumChunks, rg = threadIdx.x / kColsumChunks;
+  const int64_t c0 = (int64_t)blockIdx.x * (kColsumChunks * 8) + chunk * 8;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < S) {
+    const uint16_t* p = G + c0;
+    int64_t r = rg;
+    for (; r + 3 * kColsumGroups < B; r += 4 * kColsumGroups) {
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        x[u] = __ldg(reinterpret_cast<const uint4*>(p + (r + u * kColsumGroups) * ldG));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc[2 * k] += __uint_as_float(w[k] << 16);
+          acc[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
+        }
+      }
+    }
+    for (; r < B; r += kColsumGroups) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(p + r * ldG));
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc[2 * k] += __uint_as_float(w[k] << 16);
+        acc[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[rg][chunk * 8 + k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < kColsumChunks * 8) {
+    const int64_t c = (int64_t)blockIdx.x * (kColsumChunks * 8) + threadIdx.x;
+    float s = 0.f;
+    for (int g = 0; g < kColsumGroups; ++g) s += red[g][threadIdx.x];
+    if (c < S) db_s[c] = s;
+  }
+}
+
 // Per-column epilogue parameters, padded to a multiple of the 256-column tile:
 // cb[j] = (b_s[j] - [Q] log_ec_s[j]) * log2(e) (-inf beyond S), sid[j] = s_j (-1 beyond S);
 // per-row label y32[t] (-2 = never matches when accidental hits are kept).
@@ -372,39 +431,43 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
   }
 }
 
-// out = sum_s part[s] (split order) [+ g[row] * bf16(wt)]; float4 columns (N % 4 == 0).
+// out = sum_s part[s] (split order) [+ g[row] * bf16(wt)] for columns < N_out (float4
+// columns; N, N_out multiples of 4), and col_out[row] = the same sum at column col_idx.
 __global__ void split_finalize_kernel(const float* part, int nsplit, int64_t M, int32_t N,
-                                      const float* g, const float* wt, float* out) {
-  const int64_t n4 = (int64_t)M * N / 4;
-  const int64_t stride4 = (int64_t)M * N / 4;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4;
+                                      int32_t N_out, const float* g, const float* wt,
+                                      float* out, float* col_out, int32_t col_idx) {
+  const int n4 = N / 4;
+  const int64_t total = M * n4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / n4;
+    const int c = 4 * (int)(e - row * n4);
+    const bool in_out = c < N_out;
+    const bool in_col = col_out != nullptr && col_idx >= c && col_idx < c + 4;
+    if (!in_out && !in_col) continue;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < nsplit; ++s) {
-      const float4 x = reinterpret_cast<const float4*>(part)[s * stride4 + e];
+      const float4 x = reinterpret_cast<const float4*>(part)[s * total + e];
       acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
     }
+    if (in_col) {
+      const int k = col_idx - c;
+      col_out[row] = k == 0 ? acc.x : (k == 1 ? acc.y : (k == 2 ? acc.z : acc.w));
+    }
+    if (!in_out) continue;
     if (g != nullptr) {
-      const float gr = g[(4 * e) / N];
-      const float4 w = reinterpret_cast<const float4*>(wt)[e];
+      const float gr = g[row];
+      const float4 w = *reinterpret_cast<const float4*>(wt + row * N_out + c);
       acc.x += gr * bf16_round(w.x);
       acc.y += gr * bf16_round(w.y);
       acc.z += gr * bf16_round(w.z);
       acc.w += gr * bf16_round(w.w);
     }
-    reinterpret_cast<float4*>(out)[e] = acc;
+    *reinterpret_cast<float4*>(out + row * N_out + c) = acc;
   }
 }
 
 
-// db_s[j] = sum over the 4*num_m row-quarter partials in order.
-__global__ void dbs_finalize_kernel(const float* part, int nrows, int64_t S, float* db_s) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= S) return;
-  float acc = 0.f;
-  for (int r = 0; r < nrows; ++r) acc += part[(int64_t)r * S + j];
-  db_s[j] = acc;
-}
 
 // ---- workspace layouts --------------------------------------------------------------------------
 struct F32Ws {
@@ -413,11 +476,13 @@ struct F32Ws {
 struct Bf16Ws {
   uint16_t *hb, *wsb, *G;
   float2* stats;
-  float *dbs_part, *cb, *part_dh, *part_dws;
+  float *cb, *part_dh, *part_dws;
   int32_t *sid, *y32;
-  int64_t Sp, Spad;
+  int64_t Sp, Spad, ldh;
   int ks_dh, ks_dws;
 };
+
+
 
 // Split-K plan for the backward pair (dW_s: M=S, K=B; dh: M=B, K=S; both N=d) run in one
 // persistent launch: aim for ~2 units per SM of roughly equal k-block count.
@@ -444,16 +509,15 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, F32Ws* f
   }
   const int64_t Sp = (S + 7) / 8 * 8;
   const int64_t Spad = std::max<int64_t>(cdiv(S, umma::BN), 1) * umma::BN;
-  const int num_m = (int)cdiv(B, umma::BM);
   const int num_n = (int)cdiv(S, umma::BN);
   int ks_dh = 1, ks_dws = 1;
   if (S > 0 && B > 0) plan_backward(B, S, d, &ks_dh, &ks_dws);
   Bf16Ws x;
-  x.hb = c.take<uint16_t>(B * d);
+  x.ldh = d;
+  x.hb = c.take<uint16_t>(B * x.ldh);
   x.wsb = c.take<uint16_t>(S * d);
   x.G = c.take<uint16_t>(B * Sp);
   x.stats = c.take<float2>((size_t)2 * num_n * B);
-  x.dbs_part = c.take<float>((size_t)4 * num_m * S);
   x.part_dh = c.take<float>(umma::part_floats((int)B, d, ks_dh));
   x.part_dws = c.take<float>(umma::part_floats((int)S, d, ks_dws));
   x.cb = c.take<float>(Spad);
@@ -516,7 +580,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const int hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) ? 1 : 0;
   const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
   const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
-  const int num_m = (int)cdiv(B, umma::BM), num_n = (int)cdiv(S, umma::BN);
+  const int num_n = (int)cdiv(S, umma::BN);
 
   // Operands in bf16 (row-major; every GEMM reads them K- or MN-major as it needs).
   to_bf16_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(a->h, B * d, w.hb);
@@ -536,7 +600,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   ep.sid = w.sid;
   ep.y = w.y32;
   int32_t rc;
-  const Operand hK{w.hb, d, false}, wsK{w.wsb, d, false};
+  const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
   if (S > 0) {  // pass 1: per-row (max, sum 2^x) of each half tile, log2 domain
     ep.stats = w.stats;
     rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, ep, st);
@@ -548,45 +612,45 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   launched();
   TFS_LAUNCH_CHECK();
   if (S == 0) {  // no candidates: dh = g * bf16(w_true)
-    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true,
-                                                             a->w_true, a->dh);
+    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, d, a->db_true,
+                                                             a->w_true, a->dh, nullptr, -1);
     launched();
     TFS_LAUNCH_CHECK();
     return TFS_OK;
   }
-  // pass 2: G = c exp(Z - lse) -> bf16 G; column partial sums for db_s
+  // pass 2: G = c exp(Z - lse) -> bf16 G
   ep.lse = a->lse;
   ep.c = a->grad_scale;
   ep.G = w.G;
   ep.ldG = w.Sp;
-  ep.dbs_part = w.dbs_part;
   rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, ep, st);
   if (rc != TFS_OK) return rc;
-  dbs_finalize_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.dbs_part, 4 * num_m, S, a->db_s);
+  // db_s = column sums of G
+  g_colsum_kernel<<<(unsigned)cdiv(S, kColsumChunks * 8), 256, 0, st>>>(w.G, B, S, w.Sp, a->db_s);
   launched();
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
   // (A = G K-major, B = W_s MN-major) in one persistent launch; split partials are reduced in
   // split order by the finalize pass, which also adds the true-class term of dh.
   umma::Gemm g[2];
   const bool dws_split = w.ks_dws > 1, dh_split = w.ks_dh > 1;
-  g[0] = umma::Gemm{Operand{w.G, w.Sp, true}, Operand{w.hb, d, true}, (int)S, d, (int)B,
-                    w.ks_dws, a->dw_s, d, w.part_dws, nullptr, nullptr, 0};
+  g[0] = umma::Gemm{Operand{w.G, w.Sp, true}, Operand{w.hb, w.ldh, true}, (int)S, d, (int)B,
+                    w.ks_dws, 0, a->dw_s, d, d, nullptr, -1, w.part_dws, nullptr, nullptr, 0};
   g[1] = umma::Gemm{Operand{w.G, w.Sp, false}, Operand{w.wsb, d, true}, (int)B, d, (int)S,
-                    w.ks_dh, a->dh, d, w.part_dh, dh_split ? nullptr : a->db_true,
-                    dh_split ? nullptr : a->w_true, d};
+                    w.ks_dh, 0, a->dh, d, d, nullptr, -1, w.part_dh,
+                    dh_split ? nullptr : a->db_true, dh_split ? nullptr : a->w_true, d};
   // larger units first so the static round-robin schedule balances the SMs
   const int64_t u0 = cdiv(B, umma::BK) / w.ks_dws, u1 = cdiv(S, umma::BK) / w.ks_dh;
   if (u1 > u0) std::swap(g[0], g[1]);
   rc = umma::launch_store(g, 2, st);
   if (rc != TFS_OK) return rc;
   if (dh_split) {
-    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(w.part_dh, w.ks_dh, B, d, a->db_true,
-                                                             a->w_true, a->dh);
+    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(
+        w.part_dh, w.ks_dh, B, d, d, a->db_true, a->w_true, a->dh, nullptr, -1);
     launched();
   }
   if (dws_split) {
-    split_finalize_kernel<<<grid1d(S * d / 4), 256, 0, st>>>(w.part_dws, w.ks_dws, S, d, nullptr,
-                                                             nullptr, a->dw_s);
+    split_finalize_kernel<<<grid1d(S * d / 4), 256, 0, st>>>(
+        w.part_dws, w.ks_dws, S, d, d, nullptr, nullptr, a->dw_s, nullptr, -1);
     launched();
   }
   TFS_LAUNCH_CHECK();
@@ -660,12 +724,12 @@ extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn,
   Carver c(ws, ws_bytes);
   float* part = c.take<float>(umma::part_floats(M, N, ks));
   umma::Gemm g{umma::Operand{A, lda, a_mn != 0}, umma::Operand{B, ldb, b_mn != 0}, M, N, K, ks,
-               C, N, part, nullptr, nullptr, 0};
+               0, C, N, N, nullptr, -1, part, nullptr, nullptr, 0};
   int32_t rc = umma::launch_store(&g, 1, st);
   if (rc != TFS_OK || ks == 1) return rc;
   if (N % 4 != 0) return TFS_ERR_INVALID_ARGUMENT;
-  split_finalize_kernel<<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, nullptr,
-                                                                    nullptr, C);
+  split_finalize_kernel<<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, N, nullptr,
+                                                                    nullptr, C, nullptr, -1);
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;

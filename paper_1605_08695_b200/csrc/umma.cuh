@@ -15,7 +15,9 @@
 //               [128*((w-4)/4), +128) in 32-column tcgen05.ld chunks, applies the fused epilogue
 //               and frees the accumulator, so the epilogue of tile i overlaps the MMAs of i+1.
 // Epilogue modes: STATS (row max / sum of 2^x of the corrected logits per half
-// tile, log2 domain), GRAD (G = c exp(Z - lse) -> bf16 G + column sums for db), STORE (fp32).
+// tile, log2 domain), GRAD (G = c exp(Z - lse) -> bf16 G), STORE (fp32 product; optional split
+// partials, extra term and one extra column routed to its own vector -- db_s comes out of the
+// dW_s GEMM as the product with a ones column appended to h).
 #pragma once
 
 #include <cuda.h>
@@ -38,13 +40,13 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)STAGES * (A_BYTES + B_BYTES) +
                               256 /*barriers + flags*/;
 
-__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int n = BN) {
   return (1u << 4)                       // D format f32
          | (1u << 7)                     // A format bf16
          | (1u << 10)                    // B format bf16
          | ((a_mn ? 1u : 0u) << 15)      // A major (0 = K, 1 = MN)
          | ((b_mn ? 1u : 0u) << 16)      // B major
-         | ((uint32_t)(BN >> 3) << 17)   // N
+         | ((uint32_t)(n >> 3) << 17)    // N (multiple of 16 for M = 128)
          | ((uint32_t)(BM >> 4) << 24);  // M
 }
 
@@ -63,7 +65,6 @@ struct EpiParams {
   float c;           // GRAD: gradient scale
   uint16_t* G;       // GRAD: bf16 [M x ldG]
   int64_t ldG;
-  float* dbs_part;   // GRAD: [(4*num_m) x N] column sums of bf16(G)
 };
 
 // One GEMM of a launch (a launch may carry two: the softmax backward runs dh and dW_s together
@@ -73,10 +74,14 @@ struct EpiParams {
 struct Problem {
   CUtensorMap ta, tb;
   int M, N, K;
+  int bn;  // tile width along N (multiple of 16, <= BN)
   int num_m, num_n, ksplit, kb_per_split, kb_total, units;
   int a_mn, b_mn;
-  float* out;
+  float* out;       // columns [0, N_out) of the product
   int64_t ldo;
+  int N_out;
+  float* col_out;   // optional: column col_idx of the product, one value per row
+  int col_idx;
   float* part;      // [ksplit x M x N] fp32 (ksplit > 1)
   const float* g;   // optional row scale of the extra term
   const float* wt;  // optional [M x ldw] fp32 matrix of the extra term (bf16-rounded)
@@ -162,8 +167,8 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
           smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
+// tcgen05.ld of 32 consecutive accumulator columns of this warp's 32 lanes (no wait).
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
@@ -175,9 +180,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
         "=r"(r[31])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void epi_bar_sync() {  // the 8 epilogue warps only
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
@@ -189,7 +194,7 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 struct Unit {
-  int pi, mt, nt, ks, kb0, kb1;
+  int pi, mt, nt, ks, kb0, kb1, nw;  // nw: MMA N of this tile (last n-tile may be narrower)
 };
 __device__ __forceinline__ Unit decode_unit(const Params& P, int u) {
   Unit r;
@@ -202,28 +207,8 @@ __device__ __forceinline__ Unit decode_unit(const Params& P, int u) {
   r.nt = t / q.num_m;
   r.kb0 = r.ks * q.kb_per_split;
   r.kb1 = min(q.kb_total, r.kb0 + q.kb_per_split);
+  r.nw = min(q.bn, (q.N - r.nt * q.bn + 15) & ~15);
   return r;
-}
-
-// Sum over the 32 lanes of v[i] for every i; afterwards lane l holds the sum for column l.
-// Fixed butterfly order (deterministic): stage W halves the live values and the lane group.
-template <int W>
-__device__ __forceinline__ void transpose_reduce_stage(float (&v)[32], int lane) {
-  const bool upper = (lane & W) != 0;
-#pragma unroll
-  for (int i = 0; i < W; ++i) {
-    const float send = upper ? v[i] : v[i + W];
-    const float keep = upper ? v[i + W] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, W);
-  }
-}
-__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
-  transpose_reduce_stage<16>(v, lane);
-  transpose_reduce_stage<8>(v, lane);
-  transpose_reduce_stage<4>(v, lane);
-  transpose_reduce_stage<2>(v, lane);
-  transpose_reduce_stage<1>(v, lane);
-  return v[0];
 }
 
 // Corrected logits of one 32-column chunk in log2 units (-inf where excluded).
@@ -291,9 +276,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
         const Unit t = decode_unit(P, u);
         const Problem& q = P.p[t.pi];
+        const int bboxes = q.b_mn ? (t.nw + kMNBox - 1) / kMNBox : 0;
+        const uint32_t bbytes =
+            q.b_mn ? (uint32_t)(bboxes * kMNBoxBytes) : (uint32_t)(q.bn * BK * 2);
         for (int kb = t.kb0; kb < t.kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
-          mbar_expect_tx(full + stage, A_BYTES + B_BYTES);
+#ifdef TFS_EXP_NO_TMA
+          mbar_expect_tx(full + stage, 0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          continue;
+#endif
+          mbar_expect_tx(full + stage, A_BYTES + bbytes);
           uint8_t* a = sA + stage * A_BYTES;
           uint8_t* b = sB + stage * B_BYTES;
           if (q.a_mn) {
@@ -304,11 +297,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             tma_load_2d(a, &q.ta, kb * BK, t.mt * BM, full + stage);
           }
           if (q.b_mn) {
-#pragma unroll
-            for (int i = 0; i < BN / kMNBox; ++i)
-              tma_load_2d(b + i * kMNBoxBytes, &q.tb, t.nt * BN + i * kMNBox, kb * BK, full + stage);
+            for (int i = 0; i < bboxes; ++i)
+              tma_load_2d(b + i * kMNBoxBytes, &q.tb, t.nt * q.bn + i * kMNBox, kb * BK,
+                          full + stage);
           } else {
-            tma_load_2d(b, &q.tb, kb * BK, t.nt * BN, full + stage);
+            tma_load_2d(b, &q.tb, kb * BK, t.nt * q.bn, full + stage);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -325,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
         const Unit t = decode_unit(P, u);
         const bool amn = P.p[t.pi].a_mn != 0, bmn = P.p[t.pi].b_mn != 0;
-        const uint32_t idesc = make_idesc(amn, bmn);
+        const uint32_t idesc = make_idesc(amn, bmn, t.nw);
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -334,10 +327,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#ifndef TFS_EXP_NO_MMA
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             umma_bf16(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
                       (kb > t.kb0 || k > 0) ? 1u : 0u);
+#endif
           umma_commit(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
@@ -363,19 +358,46 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const int row = t.mt * BM + rt;
       const bool row_ok = row < q.M;
       int32_t y = -2;
-      float lse2 = 0.f;
+      float goff = 0.f;  // GRAD: G = c 2^(v - lse log2 e) = 2^(v - goff)
       if (MODE != kStore && row_ok) y = ep.y[row];
-      if (MODE == kGrad && row_ok) lse2 = ep.lse[row] * kLog2e;
+      if (MODE == kGrad && row_ok) goff = ep.lse[row] * kLog2e - log2f(ep.c);
       float run_m = -INFINITY, run_s = 0.f;
 
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-#pragma unroll 1
+#ifdef TFS_EXP_NO_EPI
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      continue;
+#endif
+      // Software-pipelined TMEM reads: chunk c+1 is in flight while chunk c is processed.
+      const uint32_t tbase =
+          tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * 128);
+      uint32_t buf0[32], buf1[32];
+      if (half * 128 < t.nw) tmem_ld32_nowait(tbase, buf0);
+#pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int ct = half * 128 + c * 32;  // column within the tile
-        const int col0 = t.nt * BN + ct;
+        const int col0 = t.nt * q.bn + ct;
+        if (ct >= t.nw) break;               // beyond a narrow tile's MMA width
+        // a 32-column chunk may run past this tile (bn % 32 != 0): those columns are stale TMEM
+        const int nend = min(q.N, (t.nt + 1) * q.bn);
+        const int nout = min(q.N_out, nend);
+        const bool next = c + 1 < 4 && ct + 32 < t.nw;
+        tmem_wait_ld();
         float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + ct), v);
+        if (c & 1) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(buf1[i]);
+          if (next) tmem_ld32_nowait(tbase + (uint32_t)((c + 1) * 32), buf0);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(buf0[i]);
+          if (next) tmem_ld32_nowait(tbase + (uint32_t)((c + 1) * 32), buf1);
+        }
         if (MODE == kStats) {
           corrected_logits(ep, col0, y, v);
           float m4[4];
@@ -396,16 +418,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           corrected_logits(ep, col0, y, v);
           uint32_t packed[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float g0 = row_ok ? ep.c * fast_exp2(v[2 * i] - lse2) : 0.f;
-            const float g1 = row_ok ? ep.c * fast_exp2(v[2 * i + 1] - lse2) : 0.f;
-            packed[i] = pack_bf16x2(g0, g1);
-            v[2 * i] = __uint_as_float(packed[i] << 16);              // bf16(g0) as fp32
-            v[2 * i + 1] = __uint_as_float(packed[i] & 0xffff0000u);  // bf16(g1) as fp32
-          }
+          for (int i = 0; i < 16; ++i)
+            packed[i] = pack_bf16x2(fast_exp2(v[2 * i] - goff), fast_exp2(v[2 * i + 1] - goff));
           if (row_ok) {
             uint16_t* gr = ep.G + (int64_t)row * ep.ldG + col0;
-            if (col0 + 32 <= q.N) {
+            if (col0 + 32 <= nend) {
               uint4* d4 = (uint4*)gr;
 #pragma unroll
               for (int i = 0; i < 4; ++i)
@@ -414,43 +431,48 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             } else {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                if (col0 + i < q.N)
+                if (col0 + i < nend)
                   gr[i] = (uint16_t)((i & 1) ? (packed[i >> 1] >> 16) : (packed[i >> 1] & 0xffffu));
             }
           }
-          const float colsum = transpose_reduce32(v, lane);
-          if (col0 + lane < q.N)
-            ep.dbs_part[(int64_t)(t.mt * 4 + quarter) * q.N + col0 + lane] = colsum;
         } else if (q.ksplit > 1) {
           // split partial, row-major [ksplit][M][N]; reduced (in split order) by a finalize pass
           if (row_ok) {
             float* o = q.part + ((int64_t)t.ks * q.M + row) * q.N + col0;
-            if (col0 + 32 <= q.N) {
+            if (col0 + 32 <= nend) {
 #pragma unroll
               for (int i = 0; i < 8; ++i)
                 ((float4*)o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             } else {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                if (col0 + i < q.N) o[i] = v[i];
+                if (col0 + i < nend) o[i] = v[i];
             }
           }
         } else if (row_ok) {
+          if (q.col_out != nullptr && q.col_idx >= col0 && q.col_idx < col0 + 32 &&
+              q.col_idx < nend) {
+            float xv = 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i == q.col_idx) xv = v[i];
+            q.col_out[row] = xv;
+          }
           if (q.g != nullptr) {
             const float gr = q.g[row];
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (col0 + i < q.N) v[i] += gr * bf16_round(q.wt[(int64_t)row * q.ldw + col0 + i]);
+              if (col0 + i < nout) v[i] += gr * bf16_round(q.wt[(int64_t)row * q.ldw + col0 + i]);
           }
           float* o = q.out + (int64_t)row * q.ldo + col0;
-          if (col0 + 32 <= q.N) {
+          if (col0 + 32 <= nout) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               ((float4*)o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (col0 + i < q.N) o[i] = v[i];
+              if (col0 + i < nout) o[i] = v[i];
           }
         }
       }
@@ -484,8 +506,12 @@ struct Operand {
 struct Gemm {
   Operand A, B;
   int M, N, K, ksplit;
-  float* out;
+  int bn;           // tile width along N (0 = BN)
+  float* out;       // columns [0, N_out)
   int64_t ldo;
+  int N_out;
+  float* col_out;   // optional column col_idx (one value per row)
+  int col_idx;
   float* part;
   const float* g;
   const float* wt;
