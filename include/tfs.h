@@ -152,7 +152,12 @@ int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int32_t num_sam
  * operand_dtype TFS_BF16: h, w_true, w_s rounded to bf16 (RNE) and G rounded to bf16 before
  * the dh / dw_s / db_s reductions; tensor-core (tcgen05) GEMMs with fp32 accumulation; all
  * other math fp32 (R-18).  Requires dim % 64 == 0 for the tensor-core path.
- * loss, lse, loss_sum may be NULL; the five gradient outputs are required. */
+ * loss, lse, loss_sum may be NULL; the five gradient outputs are required.
+ * vocab > 0 promises labels and sampled lie in [0, vocab) and lets the bf16 path find
+ * accidental hits through a candidate map of 8 * vocab bytes at the START of the workspace
+ * (tfs_ssm_workspace_bytes includes it): that region must be zero before the first call on a
+ * workspace (e.g. zero-filled at allocation) and every call leaves it zero again.  vocab == 0:
+ * no map, the hit test compares every (token, candidate) id pair (same result, slower). */
 enum { TFS_SUBTRACT_LOG_Q = 1u, TFS_REMOVE_ACCIDENTAL_HITS = 2u };
 typedef struct {
   int64_t B, S;
@@ -177,8 +182,10 @@ typedef struct {
   float* db_true;
   float* dw_s;
   float* db_s;
+  int64_t vocab;
 } tfs_ssm_args;
-size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype);
+size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype,
+                               int64_t vocab);
 int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, size_t ws_bytes,
                                     void* stream);
 
@@ -214,10 +221,10 @@ int32_t tfs_scatter_add_sgd(float* table, int64_t rows, int32_t dim, const int64
 
 /* ==== Diagnostics ===============================================================================
  * C[M x N] (fp32, row-major) = sum_k A(m, k) B(n, k) on the tcgen05 path with bf16 operands,
- * K split `ksplit` ways and the splits reduced in-kernel in split order (deterministic).
- * a_mn == 0: A is K-major, A(m, k) = A[m * lda + k]; a_mn != 0: MN-major, A(m, k) =
- * A[k * lda + m]; same for B with ldb.  lda / ldb in elements, multiples of 8; bases 16-byte
- * aligned.  Workspace: tfs_debug_gemm_workspace_bytes.  Used by the GEMM unit tests. */
+ * K split `ksplit` ways and the splits reduced by a finalize pass in split order
+ * (deterministic).  a_mn == 0: A is K-major, A(m, k) = A[m * lda + k]; a_mn != 0: MN-major,
+ * A(m, k) = A[k * lda + m]; same for B with ldb.  lda / ldb in elements, multiples of 8; N a
+ * multiple of 4 (else TFS_ERR_INVALID_ARGUMENT); bases 16-byte aligned.  Workspace: tfs_debug_gemm_workspace_bytes.  Used by the GEMM unit tests. */
 size_t tfs_debug_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t ksplit);
 int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb,
                             int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t ksplit,

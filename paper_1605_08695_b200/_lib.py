@@ -52,7 +52,7 @@ class SsmArgs(ctypes.Structure):
         ("h", P), ("labels", P), ("w_true", P), ("b_true", P), ("log_ec_true", P),
         ("sampled", P), ("w_s", P), ("b_s", P), ("log_ec_s", P),
         ("loss", P), ("lse", P), ("loss_sum", P), ("dh", P), ("dw_true", P), ("db_true", P),
-        ("dw_s", P), ("db_s", P),
+        ("dw_s", P), ("db_s", P), ("vocab", I64),
     ]
 
 
@@ -71,7 +71,7 @@ _SIGNATURES = {
     "tfs_sampler_workspace_bytes": ([I64], SZ),
     "tfs_log_uniform_sample": ([P, I64, I32, I32, I64, U64, U64, P, U32, P, I64, P, P, P, P, P,
                                 SZ, P, P], I32),
-    "tfs_ssm_workspace_bytes": ([I64, I64, I32, I32], SZ),
+    "tfs_ssm_workspace_bytes": ([I64, I64, I32, I32, I64], SZ),
     "tfs_sampled_softmax_fwd_bwd": ([ctypes.POINTER(SsmArgs), P, SZ, P], I32),
     "tfs_sort_reduce_workspace_bytes": ([I64, I32], SZ),
     "tfs_sort_reduce": ([P, I64, I64, I32, P, I32, P, P, P, P, P, P, P, SZ, P, P], I32),

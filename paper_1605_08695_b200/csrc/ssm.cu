@@ -57,7 +57,27 @@ static int32_t make_tmap(CUtensorMap* map, const Operand& op, uint64_t rows, uin
   return r == CUDA_SUCCESS ? TFS_OK : TFS_ERR_INVALID_ARGUMENT;
 }
 
-int tiles_of(int M, int N) { return (int)(cdiv(M, BM) * cdiv(N, BN)); }
+// Store map of an epilogue output: row-major [rows x cols] (x depth planes `plane` elements
+// apart), element size esize, box = 64 bytes x 32 rows, 64-byte swizzle (the staging layout).
+static int32_t make_store_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, void* base,
+                              uint64_t cols, uint64_t rows, uint64_t ld, uint64_t depth,
+                              uint64_t plane) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return TFS_ERR_CUDA;
+  if (((uintptr_t)base & 15) != 0 || (ld * esize) % 16 != 0 || (plane * esize) % 16 != 0)
+    return TFS_ERR_INVALID_ARGUMENT;
+  const cuuint32_t rank = depth > 1 ? 3 : 2;
+  cuuint64_t dims[3] = {cols, rows, depth};
+  cuuint64_t strides[2] = {ld * esize, plane * esize};
+  cuuint32_t box[3] = {(cuuint32_t)(64 / esize), 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, dt, rank, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TFS_OK : TFS_ERR_INVALID_ARGUMENT;
+}
+
+int tiles_of(int M, int N) { return (int)(cdiv(M, PM) * cdiv(N, BN)); }
 
 int effective_split(int K, int ksplit) {
   const int kb = (int)cdiv(K, BK);
@@ -70,20 +90,17 @@ size_t part_floats(int M, int N, int ksplit) {
   return ksplit > 1 ? (size_t)ksplit * M * N : 0;
 }
 
-static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int K, int ksplit,
-                            int bn = BN) {
-  if (M <= 0 || N <= 0 || K <= 0 || bn < 16 || bn > BN || bn % 16 != 0)
-    return TFS_ERR_INVALID_ARGUMENT;
+static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int K, int ksplit) {
+  if (M <= 0 || N <= 0 || K <= 0) return TFS_ERR_INVALID_ARGUMENT;
   int32_t rc = make_tmap(&p.ta, A, (uint64_t)M, (uint64_t)K, BM);
   if (rc != TFS_OK) return rc;
-  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, (uint32_t)bn);
+  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, BNC);
   if (rc != TFS_OK) return rc;
   p.M = M;
   p.N = N;
   p.K = K;
-  p.bn = bn;
-  p.num_m = (int)cdiv(M, BM);
-  p.num_n = (int)cdiv(N, bn);
+  p.num_m = (int)cdiv(M, PM);
+  p.num_n = (int)cdiv(N, BN);
   p.kb_total = (int)cdiv(K, BK);
   ksplit = std::max(1, std::min(ksplit, p.kb_total));
   p.kb_per_split = (int)cdiv(p.kb_total, ksplit);
@@ -91,9 +108,6 @@ static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int 
   p.units = p.num_m * p.num_n * p.ksplit;
   p.a_mn = A.mn;
   p.b_mn = B.mn;
-  p.N_out = N;
-  p.col_out = nullptr;
-  p.col_idx = -1;
   return TFS_OK;
 }
 
@@ -106,21 +120,39 @@ static int32_t launch_params(const Params& P, cudaStream_t st) {
                                       (int)kSmemBytes));
     attr_done = true;
   }
-  const int grid = std::min(P.total_units, num_sms());
-  gemm_kernel<MODE><<<grid, kThreads, kSmemBytes, st>>>(P);
+  // persistent: one CTA (or CTA pair: a cluster of 2 on one TPC) per SM (or per two SMs)
+  const int groups = std::min(P.total_units, num_sms() / kCta);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(kCta * groups));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kCta > 1 ? 1 : 0;  // plain launch for single-CTA tiles
+  TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE>, P));
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }
 
 int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K,
-                             const EpiParams& ep, cudaStream_t st) {
+                             EpiParams ep, uint16_t* G, int64_t ldG, cudaStream_t st) {
   if (A.mn || B.mn) return TFS_ERR_INVALID_ARGUMENT;
   Params P{};
   int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1);
   if (rc != TFS_OK) return rc;
   P.nprob = 1;
   P.total_units = P.p[0].units;
+  if (mode == kGrad) {
+    rc = make_store_map(&ep.tG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, G, (uint64_t)N,
+                        (uint64_t)M, (uint64_t)ldG, 1, 0);
+    if (rc != TFS_OK) return rc;
+  }
   P.ep = ep;
   return mode == kStats ? launch_params<kStats>(P, st) : launch_params<kGrad>(P, st);
 }
@@ -133,16 +165,18 @@ int32_t launch_store(const Gemm* g, int count, cudaStream_t st) {
   P.total_units = 0;
   for (int i = 0; i < count; ++i) {
     Problem& p = P.p[i];
-    int32_t rc = fill_problem(p, g[i].A, g[i].B, g[i].M, g[i].N, g[i].K, g[i].ksplit,
-                              g[i].bn > 0 ? g[i].bn : BN);
+    int32_t rc = fill_problem(p, g[i].A, g[i].B, g[i].M, g[i].N, g[i].K, g[i].ksplit);
     if (rc != TFS_OK) return rc;
-    if (p.ksplit > 1 && g[i].part == nullptr) return TFS_ERR_INVALID_ARGUMENT;
-    p.out = g[i].out;
-    p.ldo = g[i].ldo;
-    p.N_out = g[i].N_out;
-    p.col_out = g[i].col_out;
-    p.col_idx = g[i].col_out ? g[i].col_idx : -1;
-    p.part = g[i].part;
+    if (p.ksplit > 1) {
+      if (g[i].part == nullptr || g[i].g != nullptr) return TFS_ERR_INVALID_ARGUMENT;
+      rc = make_store_map(&p.to, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g[i].part, (uint64_t)p.N,
+                          (uint64_t)p.M, (uint64_t)p.N, (uint64_t)p.ksplit,
+                          (uint64_t)p.M * p.N);
+    } else {
+      rc = make_store_map(&p.to, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g[i].out, (uint64_t)p.N,
+                          (uint64_t)p.M, (uint64_t)g[i].ldo, 1, 0);
+    }
+    if (rc != TFS_OK) return rc;
     p.g = g[i].g;
     p.wt = g[i].wt;
     p.ldw = g[i].ldw;
@@ -326,8 +360,18 @@ __global__ void to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
 // x 64 row groups; each thread sums its rows in order, then the 64 partials are added in
 // row-group order (fixed summation order, no atomics).
 constexpr int kColsumChunks = 4, kColsumGroups = 64;
+// Also returns the candidate map to all-zero (the GRAD pass was its last reader).
 __global__ void __launch_bounds__(256) g_colsum_kernel(const uint16_t* G, int64_t B, int64_t S,
-                                                       int64_t ldG, float* db_s) {
+                                                       int64_t ldG, float* db_s,
+                                                       const int64_t* sampled, int2* cmap,
+                                                       int64_t vocab) {
+  if (cmap != nullptr) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < S;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t k = sampled[j];
+      if (k >= 0 && k < vocab) cmap[k] = make_int2(0, 0);
+    }
+  }
   __shared__ float red[kColsumGroups][kColsumChunks * 8 + 1];
   const int chunk = threadIdx.x % kColsumChunks, rg = threadIdx.x / kColsumChunks;
   const int64_t c0 = (int64_t)blockIdx.x * (kColsumChunks * 8) + chunk * 8;
@@ -371,24 +415,58 @@ __global__ void __launch_bounds__(256) g_colsum_kernel(const uint16_t* G, int64_
   }
 }
 
-// Per-column epilogue parameters, padded to a multiple of the 256-column tile:
-// cb[j] = (b_s[j] - [Q] log_ec_s[j]) * log2(e) (-inf beyond S), sid[j] = s_j (-1 beyond S);
-// per-row label y32[t] (-2 = never matches when accidental hits are kept).
-__global__ void column_params_kernel(const float* b_s, const float* le_s, const int64_t* sampled,
-                                     int64_t S, int64_t S_pad, const int64_t* labels, int64_t B,
-                                     int remove_hits, float* cb, int32_t* sid, int32_t* y32) {
-  const int64_t total = S_pad + B;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    if (e < S) {
-      cb[e] = (b_s[e] - (le_s ? le_s[e] : 0.f)) * umma::kLog2e;
-      sid[e] = (int32_t)sampled[e];
-    } else if (e < S_pad) {
-      cb[e] = -INFINITY;
-      sid[e] = -1;
-    } else {
-      const int64_t t = e - S_pad;
-      y32[t] = remove_hits ? (int32_t)labels[t] : -2;
+// ---- operand conversion + column parameters + candidate map, one launch ---------------------
+// h and W_s -> bf16 (RNE).  Per column (padded to a multiple of the 256-column tile):
+// cb[j] = (b_s[j] - [Q] log_ec_s[j]) * log2(e) (-inf beyond S), sid[j] = s_j (-1 beyond S).
+// With accidental-hit removal and a vocabulary bound, the candidate map (first in the
+// workspace, zero between calls) receives, for every id k among the candidates,
+//   cmap[k] = {max over j with s_j = k of (2^30 - j), max of (j + 1)}
+// (integer atomics: order-independent), so the epilogue finds the columns [lo, hi] that hold a
+// row's label with one load and compares ids only in chunks that intersect that range.
+constexpr int32_t kMapLoBase = 1 << 30;
+__global__ void __launch_bounds__(256) prep_kernel(const float* h, int64_t nh4, const float* w_s,
+                                                   int64_t nw4, uint16_t* hb, uint16_t* wsb,
+                                                   const float* b_s, const float* le_s,
+                                                   const int64_t* sampled, int64_t S,
+                                                   int64_t S_pad, int2* cmap, int64_t vocab,
+                                                   float* cb, int32_t* sid) {
+  constexpr int U = 4;  // independent loads in flight per thread
+  const int64_t total = nh4 + nw4 + S_pad;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < total; e0 += U * stride) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      v[u] = e < nh4 ? __ldg(reinterpret_cast<const float4*>(h) + e)
+                     : (e < nh4 + nw4 ? __ldg(reinterpret_cast<const float4*>(w_s) + (e - nh4))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < nh4 + nw4) {
+        const uint2 o = make_uint2(pack_bf16x2(v[u].x, v[u].y), pack_bf16x2(v[u].z, v[u].w));
+        if (e < nh4)
+          reinterpret_cast<uint2*>(hb)[e] = o;
+        else
+          reinterpret_cast<uint2*>(wsb)[e - nh4] = o;
+      } else if (e < total) {
+        const int64_t j = e - nh4 - nw4;
+        if (j < S) {
+          const int64_t k = sampled[j];
+          cb[j] = (b_s[j] - (le_s ? le_s[j] : 0.f)) * umma::kLog2e;
+          sid[j] = (int32_t)k;
+          if (cmap != nullptr && k >= 0 && k < vocab) {
+            int32_t* m = reinterpret_cast<int32_t*>(cmap + k);
+            atomicMax(m, kMapLoBase - (int32_t)j);
+            atomicMax(m + 1, (int32_t)j + 1);
+          }
+        } else {
+          cb[j] = -INFINITY;
+          sid[j] = -1;
+        }
+      }
     }
   }
 }
@@ -431,43 +509,31 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
   }
 }
 
-// out = sum_s part[s] (split order) [+ g[row] * bf16(wt)] for columns < N_out (float4
-// columns; N, N_out multiples of 4), and col_out[row] = the same sum at column col_idx.
+// out = sum_s part[s] (split order) [+ g[row] * bf16(wt)] (float4 columns; N % 4 == 0).
 __global__ void split_finalize_kernel(const float* part, int nsplit, int64_t M, int32_t N,
-                                      int32_t N_out, const float* g, const float* wt,
-                                      float* out, float* col_out, int32_t col_idx) {
+                                      const float* g, const float* wt, float* out) {
   const int n4 = N / 4;
   const int64_t total = M * n4;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = e / n4;
     const int c = 4 * (int)(e - row * n4);
-    const bool in_out = c < N_out;
-    const bool in_col = col_out != nullptr && col_idx >= c && col_idx < c + 4;
-    if (!in_out && !in_col) continue;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < nsplit; ++s) {
       const float4 x = reinterpret_cast<const float4*>(part)[s * total + e];
       acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
     }
-    if (in_col) {
-      const int k = col_idx - c;
-      col_out[row] = k == 0 ? acc.x : (k == 1 ? acc.y : (k == 2 ? acc.z : acc.w));
-    }
-    if (!in_out) continue;
     if (g != nullptr) {
       const float gr = g[row];
-      const float4 w = *reinterpret_cast<const float4*>(wt + row * N_out + c);
+      const float4 w = *reinterpret_cast<const float4*>(wt + row * N + c);
       acc.x += gr * bf16_round(w.x);
       acc.y += gr * bf16_round(w.y);
       acc.z += gr * bf16_round(w.z);
       acc.w += gr * bf16_round(w.w);
     }
-    *reinterpret_cast<float4*>(out + row * N_out + c) = acc;
+    *reinterpret_cast<float4*>(out + row * N + c) = acc;
   }
 }
-
-
 
 // ---- workspace layouts --------------------------------------------------------------------------
 struct F32Ws {
@@ -477,7 +543,7 @@ struct Bf16Ws {
   uint16_t *hb, *wsb, *G;
   float2* stats;
   float *cb, *part_dh, *part_dws;
-  int32_t *sid, *y32;
+  int32_t* sid;
   int64_t Sp, Spad, ldh;
   int ks_dh, ks_dws;
 };
@@ -485,12 +551,12 @@ struct Bf16Ws {
 
 
 // Split-K plan for the backward pair (dW_s: M=S, K=B; dh: M=B, K=S; both N=d) run in one
-// persistent launch: aim for ~2 units per SM of roughly equal k-block count.
+// persistent launch: aim for ~2 units per CTA pair of roughly equal k-block count.
 static void plan_backward(int64_t B, int64_t S, int32_t d, int* ks_dh, int* ks_dws) {
   const int64_t t_dh = umma::tiles_of((int)B, d), t_dws = umma::tiles_of((int)S, d);
   const int64_t kb_dh = cdiv(S, umma::BK), kb_dws = cdiv(B, umma::BK);
   const int64_t work = t_dh * kb_dh + t_dws * kb_dws;
-  const int64_t target = std::max<int64_t>(16, cdiv(work, 2 * num_sms()));
+  const int64_t target = std::max<int64_t>(16, cdiv(work, 2 * (num_sms() / umma::kCta)));
   auto split = [&](int64_t kb) {
     if (kb <= target + target / 4) return 1;
     return (int)std::min<int64_t>(16, cdiv(kb, target));
@@ -499,9 +565,15 @@ static void plan_backward(int64_t B, int64_t S, int32_t d, int* ks_dh, int* ks_d
   *ks_dws = umma::effective_split((int)B, split(kb_dws));
 }
 
-static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, F32Ws* f, Bf16Ws* w,
-                        void* base) {
+// The candidate map (bf16 path, vocab > 0) comes first: offset 0, size depending on vocab only,
+// so a zero-filled workspace stays valid across calls of any shape.
+static size_t map_bytes(int64_t vocab) {
+  return vocab > 0 ? ((size_t)vocab * sizeof(int2) + 255) / 256 * 256 : 0;
+}
+static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, int64_t vocab, F32Ws* f,
+                        Bf16Ws* w, void* base) {
   Carver c(base, (size_t)-1);
+  c.used = map_bytes(vocab);
   if (dtype == TFS_F32) {
     float* Z = c.take<float>((size_t)std::max<int64_t>(B * S, 1));
     if (f) f->Z = Z;
@@ -522,7 +594,6 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, F32Ws* f
   x.part_dws = c.take<float>(umma::part_floats((int)S, d, ks_dws));
   x.cb = c.take<float>(Spad);
   x.sid = c.take<int32_t>(Spad);
-  x.y32 = c.take<int32_t>(B);
   x.Sp = Sp;
   x.Spad = Spad;
   x.ks_dh = ks_dh;
@@ -537,7 +608,7 @@ static int grid1d(int64_t n, int threads = 256) {
 
 static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   F32Ws w;
-  ws_layout(a->B, a->S, a->dim, TFS_F32, &w, nullptr, ws);
+  ws_layout(a->B, a->S, a->dim, TFS_F32, a->vocab, &w, nullptr, ws);
   const int64_t B = a->B, S = a->S;
   const int32_t d = a->dim;
   const int hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) ? 1 : 0;
@@ -574,7 +645,7 @@ static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
 
 static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   Bf16Ws w;
-  ws_layout(a->B, a->S, a->dim, TFS_BF16, nullptr, &w, ws);
+  ws_layout(a->B, a->S, a->dim, TFS_BF16, a->vocab, nullptr, &w, ws);
   const int64_t B = a->B, S = a->S;
   const int32_t d = a->dim;
   const int hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) ? 1 : 0;
@@ -582,15 +653,13 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
   const int num_n = (int)cdiv(S, umma::BN);
 
-  // Operands in bf16 (row-major; every GEMM reads them K- or MN-major as it needs).
-  to_bf16_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(a->h, B * d, w.hb);
-  launched();
-  if (S > 0) {
-    to_bf16_kernel<<<grid1d(S * d / 4), 256, 0, st>>>(a->w_s, S * d, w.wsb);
-    launched();
-  }
-  column_params_kernel<<<grid1d(w.Spad + B), 256, 0, st>>>(
-      a->b_s, le_s, a->sampled, S, w.Spad, a->labels, B, hits, w.cb, w.sid, w.y32);
+  // Operands in bf16 (row-major; every GEMM reads them K- or MN-major as it needs), column
+  // parameters and the candidate map: one launch.
+  const int64_t V = hits ? a->vocab : 0;
+  int2* cmap = V > 0 ? reinterpret_cast<int2*>(ws) : nullptr;
+  prep_kernel<<<grid1d(((B + S) * d / 4 + w.Spad) / 4), 256, 0, st>>>(
+      a->h, B * d / 4, a->w_s, S * d / 4, w.hb, w.wsb, a->b_s, le_s, a->sampled, S, w.Spad, cmap,
+      V, w.cb, w.sid);
   launched();
   TFS_LAUNCH_CHECK();
 
@@ -598,12 +667,15 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   umma::EpiParams ep{};
   ep.cb = w.cb;
   ep.sid = w.sid;
-  ep.y = w.y32;
+  ep.labels = hits ? a->labels : nullptr;
+  ep.cmap = cmap;
+  ep.vocab = V;
+  ep.S_pad = (int)w.Spad;
   int32_t rc;
   const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
   if (S > 0) {  // pass 1: per-row (max, sum 2^x) of each half tile, log2 domain
     ep.stats = w.stats;
-    rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, ep, st);
+    rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, ep, nullptr, 0, st);
     if (rc != TFS_OK) return rc;
   }
   bf16_combine_kernel<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(
@@ -612,8 +684,8 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   launched();
   TFS_LAUNCH_CHECK();
   if (S == 0) {  // no candidates: dh = g * bf16(w_true)
-    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, d, a->db_true,
-                                                             a->w_true, a->dh, nullptr, -1);
+    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true,
+                                                             a->w_true, a->dh);
     launched();
     TFS_LAUNCH_CHECK();
     return TFS_OK;
@@ -621,12 +693,11 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   // pass 2: G = c exp(Z - lse) -> bf16 G
   ep.lse = a->lse;
   ep.c = a->grad_scale;
-  ep.G = w.G;
-  ep.ldG = w.Sp;
-  rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, ep, st);
+  rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, ep, w.G, w.Sp, st);
   if (rc != TFS_OK) return rc;
   // db_s = column sums of G
-  g_colsum_kernel<<<(unsigned)cdiv(S, kColsumChunks * 8), 256, 0, st>>>(w.G, B, S, w.Sp, a->db_s);
+  g_colsum_kernel<<<(unsigned)cdiv(S, kColsumChunks * 8), 256, 0, st>>>(w.G, B, S, w.Sp, a->db_s,
+                                                                       a->sampled, cmap, V);
   launched();
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
   // (A = G K-major, B = W_s MN-major) in one persistent launch; split partials are reduced in
@@ -634,10 +705,10 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   umma::Gemm g[2];
   const bool dws_split = w.ks_dws > 1, dh_split = w.ks_dh > 1;
   g[0] = umma::Gemm{Operand{w.G, w.Sp, true}, Operand{w.hb, w.ldh, true}, (int)S, d, (int)B,
-                    w.ks_dws, 0, a->dw_s, d, d, nullptr, -1, w.part_dws, nullptr, nullptr, 0};
+                    w.ks_dws, a->dw_s, d, w.part_dws, nullptr, nullptr, 0};
   g[1] = umma::Gemm{Operand{w.G, w.Sp, false}, Operand{w.wsb, d, true}, (int)B, d, (int)S,
-                    w.ks_dh, 0, a->dh, d, d, nullptr, -1, w.part_dh,
-                    dh_split ? nullptr : a->db_true, dh_split ? nullptr : a->w_true, d};
+                    w.ks_dh, a->dh, d, w.part_dh, dh_split ? nullptr : a->db_true,
+                    dh_split ? nullptr : a->w_true, d};
   // larger units first so the static round-robin schedule balances the SMs
   const int64_t u0 = cdiv(B, umma::BK) / w.ks_dws, u1 = cdiv(S, umma::BK) / w.ks_dh;
   if (u1 > u0) std::swap(g[0], g[1]);
@@ -645,12 +716,12 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   if (rc != TFS_OK) return rc;
   if (dh_split) {
     split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(
-        w.part_dh, w.ks_dh, B, d, d, a->db_true, a->w_true, a->dh, nullptr, -1);
+        w.part_dh, w.ks_dh, B, d, a->db_true, a->w_true, a->dh);
     launched();
   }
   if (dws_split) {
     split_finalize_kernel<<<grid1d(S * d / 4), 256, 0, st>>>(
-        w.part_dws, w.ks_dws, S, d, d, nullptr, nullptr, a->dw_s, nullptr, -1);
+        w.part_dws, w.ks_dws, S, d, nullptr, nullptr, a->dw_s);
     launched();
   }
   TFS_LAUNCH_CHECK();
@@ -661,8 +732,9 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
 
 using namespace tfs;
 
-extern "C" size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype) {
-  return ws_layout(B, S, dim, operand_dtype, nullptr, nullptr, nullptr);
+extern "C" size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype,
+                                          int64_t vocab) {
+  return ws_layout(B, S, dim, operand_dtype, vocab, nullptr, nullptr, nullptr);
 }
 
 extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, size_t ws_bytes,
@@ -690,7 +762,7 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
     TFS_REQUIRE(((uintptr_t)a->dw_s & 15) == 0 || a->S == 0);
   }
   TFS_SUPPORTED();
-  if (ws_bytes < tfs_ssm_workspace_bytes(a->B, a->S, a->dim, a->operand_dtype))
+  if (ws_bytes < tfs_ssm_workspace_bytes(a->B, a->S, a->dim, a->operand_dtype, a->vocab))
     return TFS_ERR_WORKSPACE_TOO_SMALL;
   TFS_REQUIRE(((uintptr_t)ws & 255) == 0);
   cudaStream_t st = as_stream(stream);
@@ -716,7 +788,8 @@ extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn,
                                        int64_t ldb, int32_t b_mn, int32_t M, int32_t N, int32_t K,
                                        int32_t ksplit, float* C, void* ws, size_t ws_bytes,
                                        void* stream) {
-  TFS_REQUIRE(A && B && C && M > 0 && N > 0 && K > 0 && lda % 8 == 0 && ldb % 8 == 0);
+  TFS_REQUIRE(A && B && C && M > 0 && N > 0 && K > 0 && lda % 8 == 0 && ldb % 8 == 0 &&
+              N % 4 == 0);
   TFS_SUPPORTED();
   if (ws_bytes < tfs_debug_gemm_workspace_bytes(M, N, K, ksplit)) return TFS_ERR_WORKSPACE_TOO_SMALL;
   cudaStream_t st = as_stream(stream);
@@ -724,12 +797,11 @@ extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn,
   Carver c(ws, ws_bytes);
   float* part = c.take<float>(umma::part_floats(M, N, ks));
   umma::Gemm g{umma::Operand{A, lda, a_mn != 0}, umma::Operand{B, ldb, b_mn != 0}, M, N, K, ks,
-               0, C, N, N, nullptr, -1, part, nullptr, nullptr, 0};
+               C, N, part, nullptr, nullptr, 0};
   int32_t rc = umma::launch_store(&g, 1, st);
   if (rc != TFS_OK || ks == 1) return rc;
-  if (N % 4 != 0) return TFS_ERR_INVALID_ARGUMENT;
-  split_finalize_kernel<<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, N, nullptr,
-                                                                    nullptr, C, nullptr, -1);
+  split_finalize_kernel<<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, nullptr,
+                                                                    nullptr, C);
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;

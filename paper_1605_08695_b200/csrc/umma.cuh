@@ -4,20 +4,25 @@
 // MN-major (row-major [K x rows]: the transposed view), selected per launch, so the softmax
 // backward reads G, W_s and h in the layout they already have -- no transposed copies.
 //
-// CTA = 12 warps, persistent over (problem, m-tile, n-tile, k-split) units:
-//   warp 0      TMA producer (one lane): A 128x64 and B 256x64 per stage, 128-byte swizzle,
-//               4-stage smem ring guarded by full/empty mbarriers.
-//   warp 1      MMA issuer (one lane): 4 x tcgen05.mma.kind::f16 (M=128, N=256, K=16) per stage
-//               into one of two 256-column TMEM accumulators; tcgen05.commit frees the stage /
-//               publishes the accumulator.
-//   warp 2      TMEM allocator (512 columns = both accumulators).
+// CTA pairs (clusters of 2, tcgen05 cta_group::2): a pair owns a 256 x 256 output tile, CTA r
+// holding rows [128 r, +128) of it (A half) and B rows [r N/2, +N/2) of the operand; the
+// leader's single MMA thread multiplies across both CTAs' smem (per-CTA operand traffic per MMA
+// is 2/3 of a 1-CTA 128 x 256 tile).  Persistent over (problem, m-pair, n-tile, k-split) units.
+// CTA = 12 warps:
+//   warp 0      TMA producer (one lane, both CTAs): A 128x64 + B 128x64 per stage, 128-byte
+//               swizzle, 6-stage ring; both CTAs' loads complete on the leader's full barrier.
+//   warp 1      MMA issuer (one lane, leader only): 4 x tcgen05.mma.cta_group::2.kind::f16
+//               (M=256, N<=256, K=16) per stage into one of two 256-column TMEM accumulators;
+//               tcgen05.commit multicasts stage release / accumulator ready to both CTAs.
+//   warp 2      TMEM allocator (512 columns = both accumulators, cta_group::2).
 //   warps 4-11  epilogue: warp w reads TMEM lanes 32*(w%4).. (its 32 rows), columns
 //               [128*((w-4)/4), +128) in 32-column tcgen05.ld chunks, applies the fused epilogue
 //               and frees the accumulator, so the epilogue of tile i overlaps the MMAs of i+1.
+//               Results leave through per-warp swizzled smem buffers and TMA bulk-tensor stores
+//               (full 64-byte row segments, bounds clipped by the tensor map).
 // Epilogue modes: STATS (row max / sum of 2^x of the corrected logits per half
-// tile, log2 domain), GRAD (G = c exp(Z - lse) -> bf16 G), STORE (fp32 product; optional split
-// partials, extra term and one extra column routed to its own vector -- db_s comes out of the
-// dW_s GEMM as the product with a ones column appended to h).
+// tile, log2 domain), GRAD (G = c exp(Z - lse) -> bf16 G), STORE (fp32 product or split-K
+// partial, optional extra term g[m] * bf16(wt[m, n])).
 #pragma once
 
 #include <cuda.h>
@@ -28,43 +33,64 @@
 namespace tfs {
 namespace umma {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+#ifndef TFS_UMMA_CTAS
+#define TFS_UMMA_CTAS 1
+#endif
+constexpr int kCta = TFS_UMMA_CTAS;  // 1: one CTA per tile; 2: CTA pairs (cta_group::2)
+static_assert(kCta == 1 || kCta == 2, "kCta");
+constexpr int BM = 128, BN = 256, BK = 64;      // BM: rows per CTA; BN: tile N
+constexpr int STAGES = kCta == 2 ? 6 : 4;
+constexpr int PM = kCta * BM;                   // rows per tile
+constexpr int BNC = BN / kCta;                  // B rows per CTA
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + kEpiWarps * 32;  // 384
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
-constexpr int B_BYTES = BN * BK * 2;            // 32 KB
+constexpr int B_BYTES = BNC * BK * 2;           // 32 KB (16 KB per CTA of a pair)
 constexpr int kMNBox = 64;                      // MN-major TMA box: 64 elements (128 B) x BK rows
 constexpr int kMNBoxBytes = kMNBox * BK * 2;    // 8 KB
 constexpr int kTmemCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)STAGES * (A_BYTES + B_BYTES) +
-                              256 /*barriers + flags*/;
+// Epilogue staging: two 2 KB buffers per epilogue warp (32 rows x 64 B, 64-byte swizzle), the
+// source of the TMA stores; and the column offsets cb of each (accumulator, half tile).
+constexpr int kStageBytes = 2048;
+constexpr int kEpiSmem = kEpiWarps * 2 * kStageBytes;  // 32 KB
+constexpr int kCbSmem = 2 * 2 * 128 * 4;               // 2 KB
+constexpr int kBarBytes = 256;  // (2 STAGES + 4) mbarriers + the TMEM address slot
+static_assert((2 * STAGES + 4) * 8 + 4 <= kBarBytes, "barrier area too small");
+constexpr size_t kSmemBytes =
+    (size_t)STAGES * (A_BYTES + B_BYTES) + kEpiSmem + kCbSmem + kBarBytes;  // 231680 B
+static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 
+// Instruction descriptor of tcgen05.mma.kind::f16: bf16 x bf16 -> f32, M = 256 (pair), N = n.
 __host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int n = BN) {
   return (1u << 4)                       // D format f32
          | (1u << 7)                     // A format bf16
          | (1u << 10)                    // B format bf16
          | ((a_mn ? 1u : 0u) << 15)      // A major (0 = K, 1 = MN)
          | ((b_mn ? 1u : 0u) << 16)      // B major
-         | ((uint32_t)(n >> 3) << 17)    // N (multiple of 16 for M = 128)
-         | ((uint32_t)(BM >> 4) << 24);  // M
+         | ((uint32_t)(n >> 3) << 17)    // N (multiple of 16)
+         | ((uint32_t)(PM >> 4) << 24);  // M
 }
 
 enum Mode : int { kStats = 0, kGrad = 1, kStore = 2 };
 
-
-
 struct EpiParams {
   // STATS / GRAD: corrected logit in log2 units  v = acc * log2(e) + cb[n], excluded (-> -inf)
   // when sid[n] == y[m].  cb / sid are padded to a multiple of BN (cb = -inf, sid = -1).
+  // labels == nullptr: nothing is excluded.  Else the columns whose id equals the row's label
+  // all lie in [lo, hi] from the candidate map (cmap[y] = {2^30 - lo, hi + 1}, {0, 0}: none;
+  // without a map (vocab == 0) the range is every column), and the per-element id compare runs
+  // only for chunks that intersect that range.
+  CUtensorMap tG;      // GRAD: store map of bf16 G [M x ldG], box {32, 32}, 64-byte swizzle
   const float* cb;
   const int32_t* sid;
-  const int32_t* y;
-  float2* stats;     // STATS: [(2*num_n) x M] (max, sum of 2^(v - max)) per half tile
-  const float* lse;  // GRAD: natural-log lse per row
-  float c;           // GRAD: gradient scale
-  uint16_t* G;       // GRAD: bf16 [M x ldG]
-  int64_t ldG;
+  const int64_t* labels;
+  const int2* cmap;
+  int64_t vocab;
+  int S_pad;
+  float2* stats;       // STATS: [(2*num_n) x M] (max, sum of 2^(v - max)) per half tile
+  const float* lse;    // GRAD: natural-log lse per row
+  float c;             // GRAD: gradient scale
 };
 
 // One GEMM of a launch (a launch may carry two: the softmax backward runs dh and dW_s together
@@ -73,17 +99,11 @@ struct EpiParams {
 // part[ks][m][n] and a finalize pass adds them in split order (fixed order: deterministic).
 struct Problem {
   CUtensorMap ta, tb;
+  CUtensorMap to;   // STORE: fp32 out [M x ldo] (2D) or part [ksplit x M x N] (3D), box 16x32
   int M, N, K;
-  int bn;  // tile width along N (multiple of 16, <= BN)
   int num_m, num_n, ksplit, kb_per_split, kb_total, units;
   int a_mn, b_mn;
-  float* out;       // columns [0, N_out) of the product
-  int64_t ldo;
-  int N_out;
-  float* col_out;   // optional: column col_idx of the product, one value per row
-  int col_idx;
-  float* part;      // [ksplit x M x N] fp32 (ksplit > 1)
-  const float* g;   // optional row scale of the extra term
+  const float* g;   // optional row scale of the extra term (ksplit == 1 only)
   const float* wt;  // optional [M x ldw] fp32 matrix of the extra term (bf16-rounded)
   int64_t ldw;
 };
@@ -131,6 +151,76 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// Pair variant: the completion goes to the LEADER CTA's mbarrier (peer bit cleared).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t leader_bar) {
+  if constexpr (kCta == 2) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+  }
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  if constexpr (kCta == 1) return 0;
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {  // both CTAs of a pair (else the CTA)
+  if constexpr (kCta == 2)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+  else
+    __syncthreads();
+}
+// Arrive on the mbarrier at the same smem offset in the leader CTA (rank 0) of the pair.
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  if constexpr (kCta == 2) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(0));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+                 : "memory");
+  } else {
+    mbar_arrive(bar);
+  }
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   (uint64_t)map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          (uint64_t)map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// Wait until at most N committed bulk stores of this thread still read their smem source.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {  // generic-proxy smem writes -> TMA
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -158,14 +248,24 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+      "tcgen05.mma.cta_group::%5.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "n"(kCta));
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
+// Arrive (once MMAs issued so far complete) on the mbarrier at this offset (in both CTAs of a
+// pair).
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  if constexpr (kCta == 2) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  }
 }
 // tcgen05.ld of 32 consecutive accumulator columns of this warp's 32 lanes (no wait).
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
@@ -184,9 +284,6 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[3
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void epi_bar_sync() {  // the 8 epilogue warps only
-  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-}
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -203,37 +300,32 @@ __device__ __forceinline__ Unit decode_unit(const Params& P, int u) {
   const int v = r.pi ? u - P.p[0].units : u;
   r.ks = v % q.ksplit;
   const int t = v / q.ksplit;
-  r.mt = t % q.num_m;
+  r.mt = t % q.num_m;  // m-pair index (PM rows)
   r.nt = t / q.num_m;
   r.kb0 = r.ks * q.kb_per_split;
   r.kb1 = min(q.kb_total, r.kb0 + q.kb_per_split);
-  r.nw = min(q.bn, (q.N - r.nt * q.bn + 15) & ~15);
+  // whole 32-column chunks, so every epilogue chunk lies inside the MMA width
+  r.nw = min(BN, (q.N - r.nt * BN + 31) & ~31);
   return r;
 }
 
-// Corrected logits of one 32-column chunk in log2 units (-inf where excluded).
-__device__ __forceinline__ void corrected_logits(const EpiParams& ep, int col0, int32_t y,
-                                                 float (&v)[32]) {
-  const float4* cb4 = reinterpret_cast<const float4*>(ep.cb + col0);
-  const int4* sid4 = reinterpret_cast<const int4*>(ep.sid + col0);
+// One 32-row x 64-byte slab of this warp into a 64-byte-swizzled staging buffer (16-byte
+// chunk k of row r lands at chunk k ^ ((r >> 1) & 3): conflict-free, the TMA SWIZZLE_64B layout).
+__device__ __forceinline__ void stage_row64(uint8_t* buf, int lane, const uint4 (&x)[4]) {
+  const int sw = (lane >> 1) & 3;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 c = __ldg(cb4 + q);
-    const int4 s = __ldg(sid4 + q);
-    v[4 * q + 0] = s.x == y ? -INFINITY : fmaf(v[4 * q + 0], kLog2e, c.x);
-    v[4 * q + 1] = s.y == y ? -INFINITY : fmaf(v[4 * q + 1], kLog2e, c.y);
-    v[4 * q + 2] = s.z == y ? -INFINITY : fmaf(v[4 * q + 2], kLog2e, c.z);
-    v[4 * q + 3] = s.w == y ? -INFINITY : fmaf(v[4 * q + 3], kLog2e, c.w);
-  }
+  for (int k = 0; k < 4; ++k)
+    *reinterpret_cast<uint4*>(buf + lane * 64 + ((k ^ sw) << 4)) = x[k];
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Params P) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = (uint64_t*)(smem + STAGES * (A_BYTES + B_BYTES));
+  uint8_t* sE = sB + STAGES * B_BYTES;                 // epilogue staging
+  float* sCb = reinterpret_cast<float*>(sE + kEpiSmem);  // [acc][half][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + kEpiSmem + kCbSmem);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -241,15 +333,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const EpiParams& ep = P.ep;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMAs)
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x / kCta, npairs = gridDim.x / kCta;  // tile-owning CTA groups
 
   if (warp == 0 && lane == 0) {
+    if ((smem_u32(smem) & 1023u) != 0) __trap();  // swizzled tiles need 1 KB alignment
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(full + s, 1);   // leader: its expect_tx arrival + both CTAs' TMA bytes
+      mbar_init(empty + s, 1);  // the leader's multicast commit
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, kEpiWarps);
+      mbar_init(tempty + a, kCta * kEpiWarps);  // leader: epilogue warps of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < P.nprob; ++i) {
@@ -258,13 +354,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::%2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+                 "r"(kTmemCols), "n"(kCta));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::%0.sync.aligned;" ::"n"(kCta));
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -273,35 +369,38 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
+      for (int u = pair; u < P.total_units; u += npairs) {
         const Unit t = decode_unit(P, u);
         const Problem& q = P.p[t.pi];
-        const int bboxes = q.b_mn ? (t.nw + kMNBox - 1) / kMNBox : 0;
-        const uint32_t bbytes =
-            q.b_mn ? (uint32_t)(bboxes * kMNBoxBytes) : (uint32_t)(q.bn * BK * 2);
+        const int nh = t.nw / kCta;  // B rows this CTA holds
+        const int bboxes = q.b_mn ? (nh + kMNBox - 1) / kMNBox : 0;
+        const uint32_t bbytes = q.b_mn ? (uint32_t)(bboxes * kMNBoxBytes) : (uint32_t)B_BYTES;
+        const int arow = t.mt * PM + (int)rank * BM;
+        const int bcol = t.nt * BN + (int)rank * nh;
         for (int kb = t.kb0; kb < t.kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
+          // the leader's barrier (peer bit cleared)
+          const uint32_t fb = smem_u32(full + stage) & (kCta == 2 ? 0xFEFFFFFFu : 0xFFFFFFFFu);
 #ifdef TFS_EXP_NO_TMA
-          mbar_expect_tx(full + stage, 0);
+          if (leader) mbar_expect_tx(full + stage, 0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
 #endif
-          mbar_expect_tx(full + stage, A_BYTES + bbytes);
+          if (leader) mbar_expect_tx(full + stage, kCta * (A_BYTES + bbytes));
           uint8_t* a = sA + stage * A_BYTES;
           uint8_t* b = sB + stage * B_BYTES;
           if (q.a_mn) {
 #pragma unroll
             for (int i = 0; i < BM / kMNBox; ++i)
-              tma_load_2d(a + i * kMNBoxBytes, &q.ta, t.mt * BM + i * kMNBox, kb * BK, full + stage);
+              tma_load_2d_pair(a + i * kMNBoxBytes, &q.ta, arow + i * kMNBox, kb * BK, fb);
           } else {
-            tma_load_2d(a, &q.ta, kb * BK, t.mt * BM, full + stage);
+            tma_load_2d_pair(a, &q.ta, kb * BK, arow, fb);
           }
           if (q.b_mn) {
             for (int i = 0; i < bboxes; ++i)
-              tma_load_2d(b + i * kMNBoxBytes, &q.tb, t.nt * q.bn + i * kMNBox, kb * BK,
-                          full + stage);
+              tma_load_2d_pair(b + i * kMNBoxBytes, &q.tb, bcol + i * kMNBox, kb * BK, fb);
           } else {
-            tma_load_2d(b, &q.tb, kb * BK, t.nt * q.bn, full + stage);
+            tma_load_2d_pair(b, &q.tb, kb * BK, bcol, fb);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -312,10 +411,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // ================================ MMA issuer ==================================
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
+      for (int u = pair; u < P.total_units; u += npairs) {
         const Unit t = decode_unit(P, u);
         const bool amn = P.p[t.pi].a_mn != 0, bmn = P.p[t.pi].b_mn != 0;
         const uint32_t idesc = make_idesc(amn, bmn, t.nw);
@@ -332,14 +431,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           for (int k = 0; k < BK / 16; ++k)
             umma_bf16(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
                       (kb > t.kb0 || k > 0) ? 1u : 0u);
+#else
+          (void)a0; (void)b0; (void)d_tmem;
 #endif
-          umma_commit(empty + stage);
+          umma_commit_pair(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(tfull + acc);
+        umma_commit_pair(tfull + acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -349,18 +450,49 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const int ew = warp - 4;       // 0..7
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int half = ew >> 2;      // column half of the 256-wide tile
+    uint8_t* stg = sE + ew * 2 * kStageBytes;
+    uint32_t nst = 0;              // TMA stores issued by this warp (staging buffer parity)
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
+    for (int u = pair; u < P.total_units; u += npairs) {
       const Unit t = decode_unit(P, u);
-      const Problem& q = P.p[t.pi];
-      const int rt = quarter * 32 + lane;  // row within the tile
-      const int row = t.mt * BM + rt;
-      const bool row_ok = row < q.M;
+      const Problem& q = P.p[MODE == kStore ? t.pi : 0];
+      const int M = q.M;
+      const int row0 = t.mt * PM + (int)rank * BM + quarter * 32;  // this warp's 32-row slab
+      const int row = row0 + lane;
+      const bool row_ok = row < M;
+      const int nw = t.nw;
       int32_t y = -2;
+      int hlo = 1 << 30, hhi = -1;
       float goff = 0.f;  // GRAD: G = c 2^(v - lse log2 e) = 2^(v - goff)
-      if (MODE != kStore && row_ok) y = ep.y[row];
-      if (MODE == kGrad && row_ok) goff = ep.lse[row] * kLog2e - log2f(ep.c);
+      float* cbh = sCb + (acc * 2 + half) * 128;
+      if (MODE != kStore) {
+        // this half tile's 128 column offsets -> smem (each warp of the half loads 32); the
+        // buffer of this accumulator was last read two tiles ago, before the previous barrier
+#ifndef TFS_EXP_CB_GLOBAL
+        cbh[quarter * 32 + lane] = __ldg(ep.cb + t.nt * BN + half * 128 + quarter * 32 + lane);
+#endif
+        if (row_ok) {
+          if (ep.labels != nullptr) {
+            const int64_t yl = __ldg(ep.labels + row);
+            y = (int32_t)yl;
+            if (ep.cmap == nullptr) {
+              hlo = 0;
+              hhi = ep.S_pad;
+            } else if (yl >= 0 && yl < ep.vocab) {
+              const int2 m = __ldg(ep.cmap + yl);
+              if (m.y > 0) {
+                hlo = (1 << 30) - m.x;
+                hhi = m.y - 1;
+              }
+            }
+          }
+          if (MODE == kGrad) goff = __ldg(ep.lse + row) * kLog2e - log2f(ep.c);
+        }
+#ifndef TFS_EXP_CB_GLOBAL
+        named_bar_sync(2 + half, 128);
+#endif
+      }
       float run_m = -INFINITY, run_s = 0.f;
 
       mbar_wait(tfull + acc, acc_phase);
@@ -368,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #ifdef TFS_EXP_NO_EPI
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + acc);
+      if (lane == 0) mbar_arrive_leader(tempty + acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
       continue;
@@ -377,16 +509,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const uint32_t tbase =
           tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * 128);
       uint32_t buf0[32], buf1[32];
-      if (half * 128 < t.nw) tmem_ld32_nowait(tbase, buf0);
+      if (half * 128 < nw) tmem_ld32_nowait(tbase, buf0);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int ct = half * 128 + c * 32;  // column within the tile
-        const int col0 = t.nt * q.bn + ct;
-        if (ct >= t.nw) break;               // beyond a narrow tile's MMA width
-        // a 32-column chunk may run past this tile (bn % 32 != 0): those columns are stale TMEM
-        const int nend = min(q.N, (t.nt + 1) * q.bn);
-        const int nout = min(q.N_out, nend);
-        const bool next = c + 1 < 4 && ct + 32 < t.nw;
+        if (ct >= nw) break;                 // beyond a narrow tile's MMA width
+        const int col0 = t.nt * BN + ct;
+        const bool next = c + 1 < 4 && ct + 32 < nw;
         tmem_wait_ld();
         float v[32];
         if (c & 1) {
@@ -398,8 +527,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(buf0[i]);
           if (next) tmem_ld32_nowait(tbase + (uint32_t)((c + 1) * 32), buf1);
         }
+        if (MODE != kStore) {
+          // corrected logits in log2 units; accidental hits (rare) -> -inf
+#ifdef TFS_EXP_CB_GLOBAL
+          const float4* cb4 = reinterpret_cast<const float4*>(ep.cb + col0);
+#else
+          const float4* cb4 = reinterpret_cast<const float4*>(cbh + c * 32);
+#endif
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float4 cc = cb4[k];
+            v[4 * k + 0] = fmaf(v[4 * k + 0], kLog2e, cc.x);
+            v[4 * k + 1] = fmaf(v[4 * k + 1], kLog2e, cc.y);
+            v[4 * k + 2] = fmaf(v[4 * k + 2], kLog2e, cc.z);
+            v[4 * k + 3] = fmaf(v[4 * k + 3], kLog2e, cc.w);
+          }
+          const bool mine = hlo <= col0 + 31 && hhi >= col0;
+#ifndef TFS_EXP_NO_HITS
+          if (__any_sync(0xffffffffu, mine)) {
+            if (mine) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (col0 + i >= hlo && col0 + i <= hhi && __ldg(ep.sid + col0 + i) == y)
+                  v[i] = -INFINITY;
+            }
+          }
+#endif
+        }
         if (MODE == kStats) {
-          corrected_logits(ep, col0, y, v);
           float m4[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -415,81 +570,79 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             run_m = nm;
           }
         } else if (MODE == kGrad) {
-          corrected_logits(ep, col0, y, v);
-          uint32_t packed[16];
+          uint4 x[4];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            packed[i] = pack_bf16x2(fast_exp2(v[2 * i] - goff), fast_exp2(v[2 * i + 1] - goff));
-          if (row_ok) {
-            uint16_t* gr = ep.G + (int64_t)row * ep.ldG + col0;
-            if (col0 + 32 <= nend) {
-              uint4* d4 = (uint4*)gr;
+          for (int k = 0; k < 4; ++k) {
+            uint32_t p[4];
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                d4[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
-                                   packed[4 * i + 3]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (col0 + i < nend)
-                  gr[i] = (uint16_t)((i & 1) ? (packed[i >> 1] >> 16) : (packed[i >> 1] & 0xffffu));
-            }
+            for (int j = 0; j < 4; ++j)
+              p[j] = pack_bf16x2(fast_exp2(v[8 * k + 2 * j] - goff),
+                                 fast_exp2(v[8 * k + 2 * j + 1] - goff));
+            x[k] = make_uint4(p[0], p[1], p[2], p[3]);
           }
-        } else if (q.ksplit > 1) {
-          // split partial, row-major [ksplit][M][N]; reduced (in split order) by a finalize pass
-          if (row_ok) {
-            float* o = q.part + ((int64_t)t.ks * q.M + row) * q.N + col0;
-            if (col0 + 32 <= nend) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                ((float4*)o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (col0 + i < nend) o[i] = v[i];
-            }
+          uint8_t* sb = stg + (nst & 1) * kStageBytes;
+          if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
+          __syncwarp();
+          stage_row64(sb, lane, x);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&ep.tG, sb, col0, row0);
+            bulk_commit();
           }
-        } else if (row_ok) {
-          if (q.col_out != nullptr && q.col_idx >= col0 && q.col_idx < col0 + 32 &&
-              q.col_idx < nend) {
-            float xv = 0.f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i == q.col_idx) xv = v[i];
-            q.col_out[row] = xv;
-          }
-          if (q.g != nullptr) {
+          ++nst;
+        } else {
+          if (q.g != nullptr && row_ok) {
             const float gr = q.g[row];
+            const float* w = q.wt + (int64_t)row * q.ldw + col0;
+            const int N = q.N;
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (col0 + i < nout) v[i] += gr * bf16_round(q.wt[(int64_t)row * q.ldw + col0 + i]);
+              if (col0 + i < N) v[i] += gr * bf16_round(w[i]);
           }
-          float* o = q.out + (int64_t)row * q.ldo + col0;
-          if (col0 + 32 <= nout) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              ((float4*)o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          } else {
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint4 x[4];
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < nout) o[i] = v[i];
+            for (int k = 0; k < 4; ++k)
+              x[k] = make_uint4(__float_as_uint(v[16 * h2 + 4 * k]),
+                                __float_as_uint(v[16 * h2 + 4 * k + 1]),
+                                __float_as_uint(v[16 * h2 + 4 * k + 2]),
+                                __float_as_uint(v[16 * h2 + 4 * k + 3]));
+            uint8_t* sb = stg + (nst & 1) * kStageBytes;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            stage_row64(sb, lane, x);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              if (q.ksplit > 1)
+                tma_store_3d(&q.to, sb, col0 + 16 * h2, row0, t.ks);
+              else
+                tma_store_2d(&q.to, sb, col0 + 16 * h2, row0);
+              bulk_commit();
+            }
+            ++nst;
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + acc);
+      if (lane == 0) mbar_arrive_leader(tempty + acc);  // the leader's barrier
       if (MODE == kStats && row_ok)
-        ep.stats[(int64_t)(t.nt * 2 + half) * q.M + row] = make_float2(run_m, run_s);
+        ep.stats[(int64_t)(t.nt * 2 + half) * M + row] = make_float2(run_m, run_s);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (lane == 0) bulk_wait_read<0>();  // staging smem must outlive the last store's read
   }
-  __syncthreads();
+  // Neither CTA may leave (or free TMEM) while its peer can still reach its smem / TMEM.
+  tc_fence_before();
+  cluster_sync_all();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::%2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols), "n"(kCta));
   }
 }
 
@@ -502,16 +655,12 @@ struct Operand {
   bool mn;
 };
 
-// One GEMM to launch.  ksplit > 1 needs part (ksplit x M x N fp32).
+// One GEMM to launch.  ksplit > 1 needs part (ksplit x M x N fp32).  N, ldo multiples of 4.
 struct Gemm {
   Operand A, B;
   int M, N, K, ksplit;
-  int bn;           // tile width along N (0 = BN)
-  float* out;       // columns [0, N_out)
+  float* out;       // [M x ldo]
   int64_t ldo;
-  int N_out;
-  float* col_out;   // optional column col_idx (one value per row)
-  int col_idx;
   float* part;
   const float* g;
   const float* wt;
@@ -523,8 +672,9 @@ size_t part_floats(int M, int N, int ksplit);
 int tiles_of(int M, int N);
 int effective_split(int K, int ksplit);
 
+// STATS / GRAD launch; for GRAD, G (bf16 [M x ldG], ldG % 8 == 0) receives the gradient.
 int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K,
-                             const EpiParams& ep, cudaStream_t st);
+                             EpiParams ep, uint16_t* G, int64_t ldG, cudaStream_t st);
 int32_t launch_store(const Gemm* g, int count, cudaStream_t st);
 
 }  // namespace umma

@@ -136,15 +136,19 @@ class Sampler:
         return s, les, ley, T
 
 
-def ssm_workspace(B: int, S: int, dim: int, operand_dtype: int, device) -> torch.Tensor:
-    return _ws(_lib.lib().tfs_ssm_workspace_bytes(B, S, dim, operand_dtype), device)
+def ssm_workspace(B: int, S: int, dim: int, operand_dtype: int, device, vocab: int = 0):
+    """Zero-filled: with vocab > 0 its head holds the candidate map, which must start (and
+    stays) zero."""
+    n = _lib.lib().tfs_ssm_workspace_bytes(B, S, dim, operand_dtype, vocab)
+    return torch.zeros(max(int(n), 256), dtype=torch.uint8, device=device)
 
 
 def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, log_ec_s, *,
                     flags=TFS_SUBTRACT_LOG_Q | TFS_REMOVE_ACCIDENTAL_HITS, grad_scale=1.0,
-                    operand_dtype=TFS_BF16, out=None, ws=None):
+                    operand_dtype=TFS_BF16, vocab: int = 0, out=None, ws=None):
     """Sampled softmax forward + backward.  Returns a dict of fp32 tensors:
-    loss, lse, loss_sum, dh, dw_true, db_true, dw_s, db_s."""
+    loss, lse, loss_sum, dh, dw_true, db_true, dw_s, db_s.  vocab > 0: labels and sampled lie
+    in [0, vocab) (enables the candidate map; ws must come from ssm_workspace(..., vocab))."""
     B, d = h.shape
     S = sampled.numel()
     dev = h.device
@@ -153,12 +157,12 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
         out = {"loss": f(B), "lse": f(B), "loss_sum": f(1), "dh": f(B, d), "dw_true": f(B, d),
                "db_true": f(B), "dw_s": f(S, d), "db_s": f(S)}
     if ws is None:
-        ws = ssm_workspace(B, S, d, operand_dtype, dev)
+        ws = ssm_workspace(B, S, d, operand_dtype, dev, vocab)
     a = SsmArgs(B, S, d, operand_dtype, flags, float(grad_scale),
                 _p(h), _p(labels), _p(w_true), _p(b_true), _p(log_ec_true), _p(sampled), _p(w_s),
                 _p(b_s), _p(log_ec_s), _p(out["loss"]), _p(out["lse"]), _p(out["loss_sum"]),
                 _p(out["dh"]), _p(out["dw_true"]), _p(out["db_true"]), _p(out["dw_s"]),
-                _p(out["db_s"]))
+                _p(out["db_s"]), int(vocab))
     check(_lib.lib().tfs_sampled_softmax_fwd_bwd(ctypes.byref(a), _p(ws), ws.numel(), _stream()),
           "tfs_sampled_softmax_fwd_bwd")
     return out

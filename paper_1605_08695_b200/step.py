@@ -150,7 +150,7 @@ class ShardedStep:
         self.db = torch.empty(B + S, **f32)
         self.ssm_out.update({"dw_true": self.dw[:B], "db_true": self.db[:B], "dw_s": self.dw[B:],
                              "db_s": self.db[B:]})
-        self.ws_ssm = ops.ssm_workspace(B, S, d, cfg.operand_dtype, dev)
+        self.ws_ssm = ops.ssm_workspace(B, S, d, cfg.operand_dtype, dev, V)
         if R == 1:
             self.rows_e = torch.empty((B, d), **f32)
             self.rows_w = torch.empty((B + S, d), **f32)
@@ -181,8 +181,8 @@ class ShardedStep:
         ops.sampled_softmax(self.h, self.y, self.w_rows[:B], self.b_rows[:B], self.ley,
                             self.qw[B:], self.w_rows[B:], self.b_rows[B:], self.les,
                             flags=self.flags, grad_scale=self.c,
-                            operand_dtype=self.cfg.operand_dtype, out=self.ssm_out,
-                            ws=self.ws_ssm)
+                            operand_dtype=self.cfg.operand_dtype, vocab=self.cfg.vocab,
+                            out=self.ssm_out, ws=self.ws_ssm)
 
     def _ph(self, name: str):
         """Phase marker: with ``self.phase_events`` set (bench instrumentation, eager only) the

@@ -70,7 +70,9 @@ def test_host_validation_without_gpu(lib):
                                    None, 0, None, None) == 1
     # workspace queries are pure host arithmetic
     assert lib.tfs_partition_workspace_bytes(10000, 8) > 0
-    assert lib.tfs_ssm_workspace_bytes(2560, 8192, 512, 1) > 2560 * 8192 * 2
+    assert lib.tfs_ssm_workspace_bytes(2560, 8192, 512, 1, 0) > 2560 * 8192 * 2
+    assert (lib.tfs_ssm_workspace_bytes(2560, 8192, 512, 1, 800000)
+            >= lib.tfs_ssm_workspace_bytes(2560, 8192, 512, 1, 0) + 8 * 800000)
 
 
 def test_product_does_not_import_oracle():

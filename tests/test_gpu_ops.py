@@ -168,25 +168,27 @@ def test_sampler_step_from_device_matches_host_step():
 
 
 # --------------------------------------------------------------------------------- Sampled softmax
-def _ssm_case(B, S, V, d, seed, hit_frac=0.2, logq=True):
+def _ssm_case(B, S, V, d, seed, hit_frac=0.2, logq=True, unique=True):
     rng = np.random.default_rng(seed)
     W = (rng.random((V, d), dtype=np.float32) - 0.5)
     bb = (rng.random(V, dtype=np.float32) - 0.5) * 0.2
     h = (rng.random((B, d), dtype=np.float32) - 0.5)
     labels = workloads.zipf_ids(rng, V, 1.0, B)
-    s, Tn, les, ley = oracle.sample(V, S, True, seed, 0, 0, labels)
+    s, Tn, les, ley = oracle.sample(V, S, unique, seed, 0, 0, labels)
     nh = int(B * hit_frac)
     labels[:nh] = rng.choice(s, nh)
     les = les.astype(np.float32)
-    ley = oracle.sample(V, S, True, seed, 0, 0, labels)[3].astype(np.float32)
+    ley = oracle.sample(V, S, unique, seed, 0, 0, labels)[3].astype(np.float32)
     return dict(h=h, labels=labels, w_true=W[labels], b_true=bb[labels], le_t=ley, s=s,
-                w_s=W[s], b_s=bb[s], le_s=les)
+                w_s=W[s], b_s=bb[s], le_s=les, V=V)
 
 
-def _run_ssm(c, dtype, grad_scale):
+def _run_ssm(c, dtype, grad_scale, use_map=True, ws=None):
+    """use_map: pass the vocabulary bound (candidate map in the workspace head) or 0."""
     out = ops.sampled_softmax(T(c["h"]), T(c["labels"]), T(c["w_true"]), T(c["b_true"]),
                               T(c["le_t"]), T(c["s"]), T(c["w_s"]), T(c["b_s"]), T(c["le_s"]),
-                              grad_scale=grad_scale, operand_dtype=dtype)
+                              grad_scale=grad_scale, operand_dtype=dtype,
+                              vocab=c["V"] if use_map else 0, ws=ws)
     return {k: v.cpu().numpy() for k, v in out.items()}
 
 
@@ -212,12 +214,13 @@ def test_ssm_fp32_parity(B, S, d):
     assert abs(got["loss_sum"][0] - gs * ref["loss"].sum()) <= 1e-5 * abs(gs * ref["loss"].sum())
 
 
+@pytest.mark.parametrize("use_map", [True, False])
 @pytest.mark.parametrize("B,S,d", [(256, 512, 512), (130, 300, 128), (2560, 512, 512),
                                    (300, 1000, 64)])
-def test_ssm_bf16_parity(B, S, d):
+def test_ssm_bf16_parity(B, S, d, use_map):
     c = _ssm_case(B, S, 40000, d, seed=3 * B + S)
     gs = 1.0 / B
-    got = _run_ssm(c, TFS_BF16, gs)
+    got = _run_ssm(c, TFS_BF16, gs, use_map)
     ref = _oracle_ssm(c, gs, False)       # accuracy: fp64, unrounded operands
     emu = _oracle_ssm(c, gs, True)        # rounding points: bf16-emulating oracle
     for k in KEYS:
@@ -225,6 +228,35 @@ def test_ssm_bf16_parity(B, S, d):
         assert rel(got[k], emu[k]) <= 2e-3, (k, rel(got[k], emu[k]))
     for k in ("loss", "lse"):
         assert rel_elem(got[k], ref[k]) <= 2e-2, (k, rel_elem(got[k], ref[k]))
+
+
+@pytest.mark.parametrize("use_map", [True, False])
+@pytest.mark.parametrize("B,S,d,V", [(700, 2000, 128, 3000), (300, 4096, 64, 500)])
+def test_ssm_bf16_duplicate_candidates(B, S, d, V, use_map):
+    """Sampling with replacement from a small vocabulary: ids repeat among the candidates, so a
+    label's columns span a range with other ids inside it (the epilogue's slow exclusion path)."""
+    c = _ssm_case(B, S, V, d, seed=B + 7, hit_frac=0.6, unique=False)
+    assert len(np.unique(c["s"])) < S
+    gs = 1.0 / B
+    got = _run_ssm(c, TFS_BF16, gs, use_map)
+    emu = _oracle_ssm(c, gs, True)
+    for k in KEYS:
+        assert rel(got[k], emu[k]) <= 2e-3, (k, rel(got[k], emu[k]))
+
+
+def test_ssm_candidate_map_left_zero():
+    """The candidate map in the workspace head is zero again after every call, so one
+    workspace serves calls with different candidate sets."""
+    c1 = _ssm_case(256, 512, 3000, 64, seed=11, hit_frac=0.5)
+    c2 = _ssm_case(256, 512, 3000, 64, seed=12, hit_frac=0.5)
+    ws = ops.ssm_workspace(256, 512, 64, TFS_BF16, DEV, 3000)
+    _run_ssm(c1, TFS_BF16, 0.01, ws=ws)
+    torch.cuda.synchronize()
+    assert int(ws[:3000 * 8].count_nonzero()) == 0
+    got = _run_ssm(c2, TFS_BF16, 0.01, ws=ws)
+    emu = _oracle_ssm(c2, 0.01, True)
+    for k in KEYS:
+        assert rel(got[k], emu[k]) <= 2e-3, (k, rel(got[k], emu[k]))
 
 
 def test_ssm_deterministic():
