@@ -267,6 +267,21 @@ using namespace tfs;
 
 // ================================================================================================
 // Part
+// One shard: the stable partition is the identity (local = id, position = i, count = n); only
+// the id range check remains.
+__global__ void partition_one_kernel(const int64_t* ids, int64_t n, int64_t vocab,
+                                     int64_t* local, int64_t* positions, int64_t* counts,
+                                     tfs_device_error* err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = ids[i];
+    if (id < 0 || id >= vocab) report_error(err, TFS_ERR_OUT_OF_RANGE, i);
+    local[i] = id;
+    positions[i] = i;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = n;
+}
+
 extern "C" size_t tfs_partition_workspace_bytes(int64_t n, int32_t num_shards) {
   (void)num_shards;
   return (size_t)kMaxBuckets * cdiv(n, kSortTile) * sizeof(uint32_t) + 256;
@@ -284,6 +299,14 @@ extern "C" int32_t tfs_partition(const int64_t* ids, int64_t n, int64_t vocab, i
   cudaStream_t st = as_stream(stream);
   if (n == 0) {
     TFS_CUDA_TRY(cudaMemsetAsync(out_counts, 0, sizeof(int64_t) * num_shards, st));
+    return TFS_OK;
+  }
+  if (num_shards == 1 && assignments == nullptr) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4ll * num_sms()));
+    partition_one_kernel<<<grid, 256, 0, st>>>(ids, n, vocab, out_local, out_positions,
+                                               out_counts, err);
+    launched();
+    TFS_LAUNCH_CHECK();
     return TFS_OK;
   }
   if (ws_bytes < tfs_partition_workspace_bytes(n, num_shards)) return TFS_ERR_WORKSPACE_TOO_SMALL;

@@ -152,9 +152,6 @@ class ShardedStep:
                              "db_s": self.db[B:]})
         self.ws_ssm = ops.ssm_workspace(B, S, d, cfg.operand_dtype, dev, V)
         if R == 1:
-            self.rows_e = torch.empty((B, d), **f32)
-            self.rows_w = torch.empty((B + S, d), **f32)
-            self.rows_b = torch.empty((B + S, 1), **f32)
             self.ws_sgd_e = ops._ws(L.tfs_scatter_add_sgd_workspace_bytes(B, d), dev)
             self.ws_sgd_w = ops._ws(L.tfs_scatter_add_sgd_workspace_bytes(B + S, d), dev)
         else:
@@ -205,19 +202,14 @@ class ShardedStep:
         main = torch.cuda.current_stream()
         side = self.side_stream
         side.wait_stream(main)
+        # With one shard Part is the identity (every id local, positions 0..n-1) and so is
+        # Stitch: each Gather writes its rows straight to their final place.
         with torch.cuda.stream(side):                      # E path
-            xl, xpos, _ = ops.partition(self.x, V, 1, err=self.err, out=self.part_x,
-                                        ws=self.ws_part_x)
-            ops.gather(self.E, xl, out=self.rows_e, err=self.err)
-            ops.stitch(xpos, self.rows_e, out=self.h)
+            ops.gather(self.E, self.x, out=self.h, err=self.err)
         self.qw[:B].copy_(self.y)                          # W path
         self._sample(step)
-        wl, wpos, _ = ops.partition(self.qw, V, 1, err=self.err, out=self.part_w,
-                                    ws=self.ws_part)
-        ops.gather(self.W, wl, out=self.rows_w, err=self.err)
-        ops.gather(self.b, wl, out=self.rows_b, err=self.err)
-        ops.stitch(wpos, self.rows_w, out=self.w_rows)
-        ops.stitch(wpos, self.rows_b.view(-1), out=self.b_rows)
+        ops.gather(self.W, self.qw, out=self.w_rows, err=self.err)
+        ops.gather(self.b, self.qw, out=self.b_rows.view(-1, 1), err=self.err)
         main.wait_stream(side)
         self._softmax()
         side.wait_stream(main)
@@ -234,19 +226,10 @@ class ShardedStep:
         with self._ph("sample"):
             self.qw[:B].copy_(self.y)
             self._sample(step)
-        with self._ph("partition"):
-            xl, xpos, _ = ops.partition(self.x, V, 1, err=self.err, out=self.part_x,
-                                        ws=self.ws_part_x)
-            wl, wpos, _ = ops.partition(self.qw, V, 1, err=self.err, out=self.part_w,
-                                        ws=self.ws_part)
-        with self._ph("gather"):
-            ops.gather(self.E, xl, out=self.rows_e, err=self.err)
-            ops.gather(self.W, wl, out=self.rows_w, err=self.err)
-            ops.gather(self.b, wl, out=self.rows_b, err=self.err)
-        with self._ph("stitch"):
-            ops.stitch(xpos, self.rows_e, out=self.h)
-            ops.stitch(wpos, self.rows_w, out=self.w_rows)
-            ops.stitch(wpos, self.rows_b.view(-1), out=self.b_rows)
+        with self._ph("gather"):  # one shard: Part / Stitch are the identity (see _local_step)
+            ops.gather(self.E, self.x, out=self.h, err=self.err)
+            ops.gather(self.W, self.qw, out=self.w_rows, err=self.err)
+            ops.gather(self.b, self.qw, out=self.b_rows.view(-1, 1), err=self.err)
         with self._ph("sampled_softmax"):
             self._softmax()
         with self._ph("scatter_sgd"):
