@@ -219,6 +219,27 @@ int32_t tfs_scatter_add_sgd(float* table, int64_t rows, int32_t dim, const int64
                             const float* grad2, void* ws, size_t ws_bytes,
                             tfs_device_error* err, void* stream);
 
+/* ==== Planned ScatterAdd + SGD ==================================================================
+ * tfs_scatter_add_sgd split in two.  The PLAN -- ids stably sorted, their segments found -- is a
+ * function of the ids alone, so a training step can build it as soon as the ids are known
+ * (before the gradient exists, overlapping the dense work); the APPLY step then sums each
+ * segment's gradient rows in the same fixed order and updates the table exactly as
+ * tfs_scatter_add_sgd does (identical results).
+ * tfs_scatter_plan: plan (device, caller-owned, tfs_scatter_plan_bytes(n) bytes) for ids[0..n)
+ * against a table of `rows` rows; ids outside [0, rows) -> TFS_ERR_OUT_OF_RANGE in err at the
+ * smallest such i (they are skipped by the apply).
+ * tfs_scatter_add_sgd_planned: apply with a plan built for the same ids, n and rows (not
+ * checked); grad_rows / grad2 indexed like those ids; ws of
+ * tfs_scatter_apply_workspace_bytes(n, dim) bytes.  The plan is not modified. */
+size_t tfs_scatter_plan_bytes(int64_t n);
+int32_t tfs_scatter_plan(const int64_t* ids, int64_t n, int64_t rows, void* plan,
+                         size_t plan_bytes, tfs_device_error* err, void* stream);
+size_t tfs_scatter_apply_workspace_bytes(int64_t n, int32_t dim);
+int32_t tfs_scatter_add_sgd_planned(float* table, int64_t rows, int32_t dim, const void* plan,
+                                    size_t plan_bytes, int64_t n, const float* grad_rows,
+                                    float lr, float* table2, const float* grad2, void* ws,
+                                    size_t ws_bytes, void* stream);
+
 /* ==== Diagnostics ===============================================================================
  * C[M x N] (fp32, row-major) = sum_k A(m, k) B(n, k) on the tcgen05 path with bf16 operands,
  * K split `ksplit` ways and the splits reduced by a finalize pass in split order

@@ -77,6 +77,10 @@ _SIGNATURES = {
     "tfs_sort_reduce": ([P, I64, I64, I32, P, I32, P, P, P, P, P, P, P, SZ, P, P], I32),
     "tfs_scatter_add_sgd_workspace_bytes": ([I64, I32], SZ),
     "tfs_scatter_add_sgd": ([P, I64, I32, P, P, I64, F32, P, P, P, SZ, P, P], I32),
+    "tfs_scatter_plan_bytes": ([I64], SZ),
+    "tfs_scatter_plan": ([P, I64, I64, P, SZ, P, P], I32),
+    "tfs_scatter_apply_workspace_bytes": ([I64, I32], SZ),
+    "tfs_scatter_add_sgd_planned": ([P, I64, I32, P, SZ, I64, P, F32, P, P, P, SZ, P], I32),
     "tfs_debug_gemm_workspace_bytes": ([I32, I32, I32, I32], SZ),
     "tfs_debug_gemm_bf16": ([P, I64, I32, P, I64, I32, I32, I32, I32, I32, P, P, SZ, P], I32),
     "tfs_debug_launch_count": ([], I64),

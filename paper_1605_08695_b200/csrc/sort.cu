@@ -774,21 +774,23 @@ __global__ void owner_counts_kernel(const uint32_t* keys, const uint32_t* seg_st
   counts[o] = first_ge(o + 1) - first_ge(o);
 }
 
+// Scratch of a segmented reduction, in two parts: the PLAN (sorted keys, permutation, segment
+// structure -- a function of the ids only, so it can be built before the rows exist) and the
+// APPLY scratch (partial sums of the segments that cross chunk boundaries).
 struct SegScratch {
+  // plan
   uint32_t *k0, *v0, *k1, *v1, *seg_start, *seg_of, *tile_cnt;
-  double *part, *part2;
-  float *sums, *sums2;
-  uint32_t *cross_list, *cross_count;
   int64_t* num_unique;
   void* sort_ws;
   size_t sort_ws_bytes;
+  // apply
+  double *part, *part2;
+  float *sums, *sums2;
+  uint32_t *cross_list, *cross_count;
 };
 
-static size_t seg_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws, size_t cap) {
-  Carver c(ws, cap);
+static void carve_plan(Carver& c, int64_t n, SegScratch& x) {
   const int64_t ntiles = cdiv(n, kSortTile);
-  const int64_t nchunks = cdiv(n, kChunk);
-  SegScratch x;
   x.k0 = c.take<uint32_t>(n);
   x.v0 = c.take<uint32_t>(n);
   x.k1 = c.take<uint32_t>(n);
@@ -796,15 +798,45 @@ static size_t seg_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws,
   x.seg_start = c.take<uint32_t>(n + 1);
   x.seg_of = c.take<uint32_t>(n);
   x.tile_cnt = c.take<uint32_t>(ntiles + 1);
+  x.num_unique = c.take<int64_t>(1);
+  x.sort_ws_bytes = radix_sort_ws_bytes(n);
+  x.sort_ws = c.take<char>(x.sort_ws_bytes);
+}
+
+static void carve_apply(Carver& c, int64_t n, int32_t dim, SegScratch& x) {
+  const int64_t nchunks = cdiv(n, kChunk);
   x.part = c.take<double>((size_t)2 * nchunks * dim);
   x.part2 = c.take<double>((size_t)2 * nchunks);
   x.sums = c.take<float>((size_t)n * dim);
   x.sums2 = c.take<float>((size_t)n);
   x.cross_list = c.take<uint32_t>((size_t)nchunks + 1);
   x.cross_count = c.take<uint32_t>(1);
-  x.num_unique = c.take<int64_t>(1);
-  x.sort_ws_bytes = radix_sort_ws_bytes(n);
-  x.sort_ws = c.take<char>(x.sort_ws_bytes);
+}
+
+static size_t plan_scratch_bytes(int64_t n, SegScratch* s, void* ws, size_t cap) {
+  Carver c(ws, cap);
+  SegScratch x{};
+  carve_plan(c, n, x);
+  if (s) *s = x;
+  return c.used + 256;
+}
+
+static size_t apply_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws, size_t cap) {
+  Carver c(ws, cap);
+  SegScratch x{};
+  carve_apply(c, n, dim, x);
+  if (s) {
+    s->part = x.part; s->part2 = x.part2; s->sums = x.sums; s->sums2 = x.sums2;
+    s->cross_list = x.cross_list; s->cross_count = x.cross_count;
+  }
+  return c.used + 256;
+}
+
+static size_t seg_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws, size_t cap) {
+  Carver c(ws, cap);
+  SegScratch x{};
+  carve_plan(c, n, x);
+  carve_apply(c, n, dim, x);
   if (s) *s = x;
   return c.used + 256;
 }
@@ -1072,6 +1104,52 @@ extern "C" int32_t tfs_scatter_add_sgd(float* table, int64_t rows, int32_t dim, 
   j.lr = lr;
   j.nloc = rows + 1;
   return run_segments(j, n, st);
+}
+
+// ---- planned ScatterAdd-SGD: the id sort (plan) split from the row reduction (apply) ---------
+extern "C" size_t tfs_scatter_plan_bytes(int64_t n) { return plan_scratch_bytes(n, nullptr, nullptr, 0); }
+
+extern "C" int32_t tfs_scatter_plan(const int64_t* ids, int64_t n, int64_t rows, void* plan,
+                                    size_t plan_bytes, tfs_device_error* err, void* stream) {
+  TFS_REQUIRE(n >= 0 && rows >= 0 && rows < (1ll << 31) - 1 && n < (1ll << 31));
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(ids && plan);
+  TFS_SUPPORTED();
+  SegScratch s;
+  if (plan_bytes < plan_scratch_bytes(n, &s, plan, plan_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+  return sort_and_segment(ids, n, rows, 1, rows + 1, 0, (uint32_t)rows, s, err, as_stream(stream));
+}
+
+extern "C" size_t tfs_scatter_apply_workspace_bytes(int64_t n, int32_t dim) {
+  return apply_scratch_bytes(n, dim, nullptr, nullptr, 0);
+}
+
+extern "C" int32_t tfs_scatter_add_sgd_planned(float* table, int64_t rows, int32_t dim,
+                                               const void* plan, size_t plan_bytes, int64_t n,
+                                               const float* grad_rows, float lr, float* table2,
+                                               const float* grad2, void* ws, size_t ws_bytes,
+                                               void* stream) {
+  TFS_REQUIRE(n >= 0 && dim >= 1 && rows >= 0 && rows < (1ll << 31) - 1 && n < (1ll << 31));
+  TFS_REQUIRE((table2 == nullptr) == (grad2 == nullptr));
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(table && plan && grad_rows);
+  TFS_REQUIRE(dim % 4 != 0 || ((uintptr_t)table & 15) == 0);
+  TFS_SUPPORTED();
+  SegScratch s;
+  if (plan_bytes < plan_scratch_bytes(n, &s, const_cast<void*>(plan), plan_bytes))
+    return TFS_ERR_WORKSPACE_TOO_SMALL;
+  if (ws_bytes < apply_scratch_bytes(n, dim, &s, ws, ws_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+  SegJob j{};
+  bind(j, s, n);
+  j.rows = grad_rows;
+  j.rows2 = grad2;
+  j.dim = dim;
+  j.invalid_key = (uint32_t)rows;
+  j.table = table;
+  j.table2 = table2;
+  j.lr = lr;
+  j.nloc = rows + 1;
+  return run_segments(j, n, as_stream(stream));
 }
 
 extern "C" size_t tfs_sort_reduce_workspace_bytes(int64_t n, int32_t dim) {

@@ -208,6 +208,32 @@ def scatter_add_sgd(table, ids, grad, lr: float, table2=None, grad2=None, err: E
     return table
 
 
+class ScatterPlan:
+    """Planned ScatterAdd-SGD: the id sort / segmentation (``build``, ids only) split from the
+    row reduction + table update (``apply``); identical results to scatter_add_sgd."""
+
+    def __init__(self, n: int, rows: int, dim: int, device):
+        L = _lib.lib()
+        self.n, self.rows, self.dim = int(n), int(rows), int(dim)
+        self.plan = _ws(L.tfs_scatter_plan_bytes(n), device)
+        self.ws = _ws(L.tfs_scatter_apply_workspace_bytes(n, dim), device)
+
+    def build(self, ids, err: ErrorSlot = None):
+        assert ids.numel() == self.n
+        check(_lib.lib().tfs_scatter_plan(_p(ids), self.n, self.rows, _p(self.plan),
+                                          self.plan.numel(), _err(err), _stream()),
+              "tfs_scatter_plan")
+        return self
+
+    def apply(self, table, grad, lr: float, table2=None, grad2=None):
+        assert table.shape[0] == self.rows
+        check(_lib.lib().tfs_scatter_add_sgd_planned(
+            _p(table), self.rows, self.dim, _p(self.plan), self.plan.numel(), self.n, _p(grad),
+            float(lr), _p(table2), _p(grad2), _p(self.ws), self.ws.numel(), _stream()),
+            "tfs_scatter_add_sgd_planned")
+        return table
+
+
 def debug_gemm_bf16(A, B, ksplit: int = 1, a_mn: bool = False, b_mn: bool = False):
     """C[ks] = sum_k A(m, k) B(n, k) on the tcgen05 path (diagnostics).  A is [M, K] (K-major)
     or, with a_mn, [K, M] (MN-major); likewise B is [N, K] or [K, N]."""

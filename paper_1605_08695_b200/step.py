@@ -16,7 +16,9 @@ Per step on rank r:
 
 With R = 1 the routes are the identity and the whole step is free of host synchronisation,
 so it is captured once into a CUDA graph and replayed (the sampler reads its step counter from
-device memory, advanced inside the graph).  With R > 1 each route needs its counts on the host
+device memory, advanced inside the graph).  Part and Stitch are identity maps then (Gather
+writes rows in place), and the SGD is split into a plan (id sort, tfs_scatter_plan) built on a
+side stream while the softmax runs, and its apply (tfs_scatter_add_sgd_planned).  With R > 1 each route needs its counts on the host
 (an all-to-all of R counts, then one device->host read).
 """
 from __future__ import annotations
@@ -152,8 +154,9 @@ class ShardedStep:
                              "db_s": self.db[B:]})
         self.ws_ssm = ops.ssm_workspace(B, S, d, cfg.operand_dtype, dev, V)
         if R == 1:
-            self.ws_sgd_e = ops._ws(L.tfs_scatter_add_sgd_workspace_bytes(B, d), dev)
-            self.ws_sgd_w = ops._ws(L.tfs_scatter_add_sgd_workspace_bytes(B + S, d), dev)
+            self.plan_e = ops.ScatterPlan(B, E.shape[0], d, dev)
+            self.plan_w = ops.ScatterPlan(B + S, W.shape[0], d, dev)
+            self.ev = {k: torch.cuda.Event() for k in ("h", "q", "plan_w", "ssm")}
         else:
             self.ws_sr_e = ops._ws(L.tfs_sort_reduce_workspace_bytes(B, d), dev)
             self.ws_sr_w = ops._ws(L.tfs_sort_reduce_workspace_bytes(B + S, d), dev)
@@ -203,21 +206,31 @@ class ShardedStep:
         side = self.side_stream
         side.wait_stream(main)
         # With one shard Part is the identity (every id local, positions 0..n-1) and so is
-        # Stitch: each Gather writes its rows straight to their final place.
+        # Stitch: each Gather writes its rows straight to their final place.  The ScatterAdd
+        # plans (id sorts) depend only on the ids, so they are built on the side stream while
+        # the main stream samples, gathers and runs the sampled softmax.
+        ev = self.ev
         with torch.cuda.stream(side):                      # E path
+            self.plan_e.build(self.x, err=self.err)
             ops.gather(self.E, self.x, out=self.h, err=self.err)
+            ev["h"].record(side)
         self.qw[:B].copy_(self.y)                          # W path
         self._sample(step)
+        ev["q"].record(main)
+        with torch.cuda.stream(side):
+            side.wait_event(ev["q"])
+            self.plan_w.build(self.qw, err=self.err)
+            ev["plan_w"].record(side)
         ops.gather(self.W, self.qw, out=self.w_rows, err=self.err)
         ops.gather(self.b, self.qw, out=self.b_rows.view(-1, 1), err=self.err)
-        main.wait_stream(side)
+        main.wait_event(ev["h"])
         self._softmax()
-        side.wait_stream(main)
+        ev["ssm"].record(main)
         with torch.cuda.stream(side):
-            ops.scatter_add_sgd(self.E, self.x, self.ssm_out["dh"], self.cfg.lr, err=self.err,
-                                ws=self.ws_sgd_e)
-        ops.scatter_add_sgd(self.W, self.qw, self.dw, self.cfg.lr, table2=self.b,
-                            grad2=self.db, err=self.err, ws=self.ws_sgd_w)
+            side.wait_event(ev["ssm"])
+            self.plan_e.apply(self.E, self.ssm_out["dh"], self.cfg.lr)
+        main.wait_event(ev["plan_w"])
+        self.plan_w.apply(self.W, self.dw, self.cfg.lr, table2=self.b, grad2=self.db)
         main.wait_stream(side)
 
     def _local_step_serial(self, step: int | None):
@@ -232,11 +245,12 @@ class ShardedStep:
             ops.gather(self.b, self.qw, out=self.b_rows.view(-1, 1), err=self.err)
         with self._ph("sampled_softmax"):
             self._softmax()
+        with self._ph("scatter_plan"):
+            self.plan_e.build(self.x, err=self.err)
+            self.plan_w.build(self.qw, err=self.err)
         with self._ph("scatter_sgd"):
-            ops.scatter_add_sgd(self.E, self.x, self.ssm_out["dh"], self.cfg.lr, err=self.err,
-                                ws=self.ws_sgd_e)
-            ops.scatter_add_sgd(self.W, self.qw, self.dw, self.cfg.lr, table2=self.b,
-                                grad2=self.db, err=self.err, ws=self.ws_sgd_w)
+            self.plan_e.apply(self.E, self.ssm_out["dh"], self.cfg.lr)
+            self.plan_w.apply(self.W, self.dw, self.cfg.lr, table2=self.b, grad2=self.db)
 
     def _dist_step(self, step: int | None):
         """R > 1: Part -> route -> Gather -> route back -> Stitch -> softmax -> sort-reduce ->

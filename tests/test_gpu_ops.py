@@ -347,3 +347,25 @@ def test_heavy_hitter_segments(dim):
     dt2 = T(table)
     ops.scatter_add_sgd(dt2, T(ids), T(g), 0.5)
     assert torch.equal(dt.cpu(), dt2.cpu())
+
+
+@pytest.mark.parametrize("n,dim,zipf", [(2560, 512, 1.0), (10752, 64, 1.2), (777, 6, 1.0)])
+def test_planned_scatter_matches_unplanned(n, dim, zipf):
+    """tfs_scatter_plan + tfs_scatter_add_sgd_planned == tfs_scatter_add_sgd, bit for bit, and
+    one plan serves repeated applies with fresh gradients."""
+    rng = np.random.default_rng(n + dim)
+    V = 5000
+    ids = workloads.zipf_ids(rng, V, zipf, n)
+    g1 = rng.standard_normal((n, dim)).astype(np.float32)
+    g2 = rng.standard_normal((n, dim)).astype(np.float32)
+    gb = rng.standard_normal(n).astype(np.float32)
+    t0 = rng.standard_normal((V, dim)).astype(np.float32)
+    b0 = rng.standard_normal(V).astype(np.float32)
+    a, ab = T(t0), T(b0)
+    ops.scatter_add_sgd(a, T(ids), T(g1), 0.1, table2=ab, grad2=T(gb))
+    ops.scatter_add_sgd(a, T(ids), T(g2), 0.1)
+    b, bb = T(t0), T(b0)
+    plan = ops.ScatterPlan(n, V, dim, DEV).build(T(ids))
+    plan.apply(b, T(g1), 0.1, table2=bb, grad2=T(gb))
+    plan.apply(b, T(g2), 0.1)
+    assert torch.equal(a, b) and torch.equal(ab, bb)
