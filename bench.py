@@ -181,6 +181,8 @@ def graph_kernel_nodes(graph):
     try:
         from cuda.bindings import runtime as rt
         g = graph.raw_cuda_graph()
+        if isinstance(g, int):
+            g = rt.cudaGraph_t(init_value=g)
         err, _, n = rt.cudaGraphGetNodes(g, 0)
         err, nodes, n = rt.cudaGraphGetNodes(g, n)
         k = 0
@@ -234,7 +236,7 @@ def main():
     xs_d = [t.to(dev) for t in xs_h]
     ys_d = [t.to(dev) for t in ys_h]
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    use_graph = (R == 1) and not args.no_graph
+    use_graph = not args.no_graph
     L = _lib.lib()
 
     def barrier():
@@ -249,6 +251,12 @@ def main():
     launches_per_step = L.tfs_debug_launch_count() - c0
     st.err.check("bench step")
     step_no = 1
+    if R > 1:  # size the fixed-capacity route slots from the observed distinct-id counts
+        caps = st.calibrate_routes()
+        st.run(xs_d[1], ys_d[1], step_no)
+        step_no += 1
+        torch.cuda.synchronize()
+        st.err.check("bench step after route calibration")
 
     if use_graph:
         st.x.copy_(xs_d[0])
@@ -394,7 +402,10 @@ def main():
                        "zipf_s": w.zipf_s, "parallelism": f"vocab-sharded x{R} (ids mod R), "
                        f"data-parallel x{R}", "l2": "flushed before every timed step "
                        "(256 MiB write outside the timed interval)",
-                       "cuda_graph": use_graph, "batches": N_BATCHES},
+                       "cuda_graph": use_graph, "batches": N_BATCHES,
+                       "route_slots": ({"cap_e": st.cap_e, "cap_w": st.cap_w,
+                                        "calibrated_from": "distinct ids per owner of one "
+                                        "eager step x1.25 + 64"} if R > 1 else None)},
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * B * 8,
                     "d2h_bytes_per_step": 4},
@@ -410,6 +421,8 @@ def main():
             line["graph_kernel_nodes"] = kernel_nodes
         print(json.dumps(line), flush=True)
     if world > 1:
+        st.graph = None  # release the captured NCCL work before the communicator goes away
+        torch.cuda.synchronize()
         dist.barrier()
         dist.destroy_process_group()
 

@@ -45,7 +45,8 @@ typedef enum {
   TFS_ERR_WORKSPACE_TOO_SMALL = 4,
   TFS_ERR_CUDA = 5,
   TFS_ERR_UNSUPPORTED = 7,
-  TFS_ERR_SAMPLER_EXHAUSTED = 8
+  TFS_ERR_SAMPLER_EXHAUSTED = 8,
+  TFS_ERR_CAPACITY = 9  /* a fixed-capacity route slot overflowed (tfs_route_plan) */
 } tfs_status;
 
 typedef enum { TFS_F32 = 0, TFS_BF16 = 1 } tfs_dtype;
@@ -86,8 +87,9 @@ int32_t tfs_partition(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_
  * "Gather, which extracts a sparse set of rows from a tensor", colocated with the variable.
  * out[j, :] = table[ids[j], :] for j < n; duplicates allowed; table is row-major [rows x dim].
  * table_dtype must be TFS_F32.  out_dtype TFS_F32 copies bits; TFS_BF16 rounds to nearest
- * even.  ids outside [0, rows) -> TFS_ERR_OUT_OF_RANGE at the smallest j.  dim >= 1; rows are
- * read with 16-byte vectors when dim % 4 == 0 and the pointers are 16-byte aligned. */
+ * even.  ids outside [0, rows) -> TFS_ERR_OUT_OF_RANGE at the smallest j, except id -1, which
+ * marks padding (its output row is left unwritten, no error).  dim >= 1; rows are read with
+ * 16-byte vectors when dim % 4 == 0 and the pointers are 16-byte aligned. */
 int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int32_t table_dtype,
                    const int64_t* ids, int64_t n, void* out, int32_t out_dtype,
                    tfs_device_error* err, void* stream);
@@ -227,7 +229,8 @@ int32_t tfs_scatter_add_sgd(float* table, int64_t rows, int32_t dim, const int64
  * tfs_scatter_add_sgd does (identical results).
  * tfs_scatter_plan: plan (device, caller-owned, tfs_scatter_plan_bytes(n) bytes) for ids[0..n)
  * against a table of `rows` rows; ids outside [0, rows) -> TFS_ERR_OUT_OF_RANGE in err at the
- * smallest such i (they are skipped by the apply).
+ * smallest such i (they are skipped by the apply); id -1 is padding: skipped, no error (also
+ * in tfs_scatter_add_sgd and tfs_sort_reduce).
  * tfs_scatter_add_sgd_planned: apply with a plan built for the same ids, n and rows (not
  * checked); grad_rows / grad2 indexed like those ids; ws of
  * tfs_scatter_apply_workspace_bytes(n, dim) bytes.  The plan is not modified. */
@@ -239,6 +242,58 @@ int32_t tfs_scatter_add_sgd_planned(float* table, int64_t rows, int32_t dim, con
                                     size_t plan_bytes, int64_t n, const float* grad_rows,
                                     float lr, float* table2, const float* grad2, void* ws,
                                     size_t ws_bytes, void* stream);
+
+/* ==== Fixed-capacity routing between R shards (R > 1; DESIGN.md §2 O3-O12) ======================
+ * The requester-side halves of Part / route / Stitch and of sort-reduce / route, in a SLOT
+ * layout that needs no host-visible counts (so a whole multi-GPU step can be a CUDA graph):
+ * the payload for owner o occupies slots [0, cap) of region o of a send buffer, region o at
+ * element offset o * stride; unused slots carry id -1.  Only DISTINCT ids travel (forward
+ * dedup): slot s of region o holds the s-th distinct id owned by o in ascending local order.
+ * tfs_route_plan: stable composite-key (owner = id mod R, local = id div R) sort plan of
+ * ids[0..n) (caller-owned, tfs_route_plan_bytes(n, R) bytes), the send ids (local ids, int64)
+ * and, if out_counts != NULL, the distinct ids per owner (device int64 [R]).  More than cap
+ * distinct ids for one owner -> TFS_ERR_CAPACITY in err (index = owner; the excess is dropped);
+ * ids outside [0, vocab) -> TFS_ERR_OUT_OF_RANGE.
+ * tfs_route_unpack: out[t, :] = slot row of ids[t] in the received rows (`slots`, region
+ * stride `slots_stride` floats, rows of dim floats): the Stitch of the routed Gather.
+ * tfs_route_reduce: the gradient rows of equal ids summed in increasing t (fixed order, fp64
+ * accumulation) and written to the slot of that id (rows2 / out_slots2: optional width-1
+ * companion, e.g. the bias gradient).  Plans are not modified. */
+size_t tfs_route_plan_bytes(int64_t n, int32_t num_shards);
+int32_t tfs_route_plan(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
+                       int64_t cap, void* plan, size_t plan_bytes, int64_t* out_send_local,
+                       int64_t send_stride, int64_t* out_counts, tfs_device_error* err,
+                       void* stream);
+int32_t tfs_route_unpack(const void* plan, size_t plan_bytes, int64_t n, int64_t vocab,
+                         int32_t num_shards, int64_t cap, const float* slots,
+                         int64_t slots_stride, int32_t dim, float* out, void* stream);
+size_t tfs_route_reduce_workspace_bytes(int64_t n, int32_t dim);
+int32_t tfs_route_reduce(const void* plan, size_t plan_bytes, int64_t n, int64_t vocab,
+                         int32_t num_shards, int64_t cap, const float* rows, int32_t dim,
+                         const float* rows2, float* out_slots, int64_t out_stride,
+                         float* out_slots2, int64_t out2_stride, void* ws, size_t ws_bytes,
+                         void* stream);
+/* Owner side.  tfs_gather_slots: for each slot (o, s) of num_slots regions x cap, the row of id
+ * ids[o * ids_stride + s] of the local shard to out + o * out_stride + s * dim (fp32; -1 ids
+ * are padding, rows left unwritten).  tfs_scatter_plan_slots / tfs_scatter_add_sgd_planned_slots:
+ * the planned ScatterAdd-SGD over the R x cap received slots (entry i = slot (i / cap, i % cap),
+ * so equal ids from different requesters are summed in requester order), gradient rows at
+ * grad + o * grad_stride + s * dim (grad2 + o * grad2_stride + s).  sorted_runs != 0 promises
+ * that every region holds strictly ascending ids followed by -1 padding (what tfs_route_plan
+ * sends): the plan is then a merge of the R runs instead of a radix sort; a violated promise is
+ * reported as TFS_ERR_INVALID_ARGUMENT in err. */
+int32_t tfs_gather_slots(const float* table, int64_t rows, int32_t dim, const int64_t* ids,
+                         int64_t ids_stride, int32_t num_slots, int64_t cap, float* out,
+                         int64_t out_stride, tfs_device_error* err, void* stream);
+int32_t tfs_scatter_plan_slots(const int64_t* ids, int64_t ids_stride, int32_t num_slots,
+                               int64_t cap, int64_t rows, int32_t sorted_runs, void* plan,
+                               size_t plan_bytes, tfs_device_error* err, void* stream);
+int32_t tfs_scatter_add_sgd_planned_slots(float* table, int64_t rows, int32_t dim,
+                                          const void* plan, size_t plan_bytes,
+                                          int32_t num_slots, int64_t cap, const float* grad,
+                                          int64_t grad_stride, float lr, float* table2,
+                                          const float* grad2, int64_t grad2_stride, void* ws,
+                                          size_t ws_bytes, void* stream);
 
 /* ==== Diagnostics ===============================================================================
  * C[M x N] (fp32, row-major) = sum_k A(m, k) B(n, k) on the tcgen05 path with bf16 operands,

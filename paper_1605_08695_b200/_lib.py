@@ -21,6 +21,7 @@ TFS_ERR_WORKSPACE_TOO_SMALL = 4
 TFS_ERR_CUDA = 5
 TFS_ERR_UNSUPPORTED = 7
 TFS_ERR_SAMPLER_EXHAUSTED = 8
+TFS_ERR_CAPACITY = 9
 TFS_F32, TFS_BF16 = 0, 1
 TFS_SUBTRACT_LOG_Q, TFS_REMOVE_ACCIDENTAL_HITS = 1, 2
 
@@ -81,6 +82,15 @@ _SIGNATURES = {
     "tfs_scatter_plan": ([P, I64, I64, P, SZ, P, P], I32),
     "tfs_scatter_apply_workspace_bytes": ([I64, I32], SZ),
     "tfs_scatter_add_sgd_planned": ([P, I64, I32, P, SZ, I64, P, F32, P, P, P, SZ, P], I32),
+    "tfs_route_plan_bytes": ([I64, I32], SZ),
+    "tfs_route_plan": ([P, I64, I64, I32, I64, P, SZ, P, I64, P, P, P], I32),
+    "tfs_route_unpack": ([P, SZ, I64, I64, I32, I64, P, I64, I32, P, P], I32),
+    "tfs_route_reduce_workspace_bytes": ([I64, I32], SZ),
+    "tfs_route_reduce": ([P, SZ, I64, I64, I32, I64, P, I32, P, P, I64, P, I64, P, SZ, P], I32),
+    "tfs_gather_slots": ([P, I64, I32, P, I64, I32, I64, P, I64, P, P], I32),
+    "tfs_scatter_plan_slots": ([P, I64, I32, I64, I64, I32, P, SZ, P, P], I32),
+    "tfs_scatter_add_sgd_planned_slots": ([P, I64, I32, P, SZ, I32, I64, P, I64, F32, P, P, I64,
+                                           P, SZ, P], I32),
     "tfs_debug_gemm_workspace_bytes": ([I32, I32, I32, I32], SZ),
     "tfs_debug_gemm_bf16": ([P, I64, I32, P, I64, I32, I32, I32, I32, I32, P, P, SZ, P], I32),
     "tfs_debug_launch_count": ([], I64),

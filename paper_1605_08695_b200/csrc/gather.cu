@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) gather_vec4_kernel(const float* __restric
       const int64_t j = j0 + u;
       id[u] = j < n ? __ldg(ids + j) : 0;
       ok[u] = j < n && id[u] >= 0 && id[u] < rows;
-      if (j < n && !ok[u] && lane == 0) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
+      if (j < n && !ok[u] && id[u] != -1 && lane == 0) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
     }
     for (int c0 = 0; c0 < n4; c0 += 128) {  // 4 float4 per lane per row per sweep
       float4 v[2][4];
@@ -121,7 +121,7 @@ __global__ void gather_scalar_kernel(const float* __restrict__ table, int64_t ro
     const int c = (int)(e - j * dim);
     const int64_t id = ids[j];
     if (id < 0 || id >= rows) {
-      if (c == 0) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
+      if (c == 0 && id != -1) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
       continue;
     }
     const float v = table[id * dim + c];
@@ -221,6 +221,7 @@ extern "C" const char* tfs_status_string(int32_t s) {
     case TFS_ERR_CUDA: return "CUDA error";
     case TFS_ERR_UNSUPPORTED: return "unsupported device (libtfs needs sm_100a)";
     case TFS_ERR_SAMPLER_EXHAUSTED: return "sampler draw budget exhausted";
+    case TFS_ERR_CAPACITY: return "route slot capacity exceeded";
     default: return "unknown status";
   }
 }
@@ -265,6 +266,62 @@ extern "C" int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int3
     else
       gather_scalar_kernel<false><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
   }
+  ::tfs::launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+// Gather in slot layout (owner side of a fixed-capacity route): entry (o, s), o < R, s < cap,
+// reads id ids[o * ids_stride + s] and writes its row to out + o * out_stride + s * dim.
+// Padding ids (-1) leave their row unwritten.  fp32 only.
+template <bool VEC>
+__global__ void __launch_bounds__(256) gather_slots_kernel(const float* __restrict__ table,
+                                                           int64_t rows, int32_t dim,
+                                                           const int64_t* __restrict__ ids,
+                                                           int64_t ids_stride, int64_t cap,
+                                                           int64_t n, float* __restrict__ out,
+                                                           int64_t out_stride,
+                                                           tfs_device_error* err) {
+  const int cols = VEC ? dim >> 2 : dim;
+  const int64_t total = n * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols;
+    const int c = (int)(e - i * cols);
+    const int64_t o = i / cap, sl = i - o * cap;
+    const int64_t id = __ldg(ids + o * ids_stride + sl);
+    if (id < 0 || id >= rows) {
+      if (c == 0 && id != -1) report_error(err, TFS_ERR_OUT_OF_RANGE, i);
+      continue;
+    }
+    float* dst = out + o * out_stride + sl * dim;
+    if (VEC)
+      reinterpret_cast<float4*>(dst)[c] = __ldg(reinterpret_cast<const float4*>(table + id * dim) + c);
+    else
+      dst[c] = __ldg(table + id * dim + c);
+  }
+}
+
+extern "C" int32_t tfs_gather_slots(const float* table, int64_t rows, int32_t dim,
+                                    const int64_t* ids, int64_t ids_stride, int32_t num_slots,
+                                    int64_t cap, float* out, int64_t out_stride,
+                                    tfs_device_error* err, void* stream) {
+  TFS_REQUIRE(dim >= 1 && rows >= 0 && num_slots >= 1 && cap >= 1 && ids_stride >= cap &&
+              out_stride >= cap * dim);
+  TFS_REQUIRE(table && ids && out);
+  TFS_SUPPORTED();
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = (int64_t)num_slots * cap;
+  const bool vec = dim % 4 == 0 && out_stride % 4 == 0 && ((uintptr_t)table % 16 == 0) &&
+                   ((uintptr_t)out % 16 == 0);
+  const int64_t total = n * (vec ? dim / 4 : dim);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 8ll * num_sms()));
+  if (vec)
+    gather_slots_kernel<true><<<grid, 256, 0, st>>>(table, rows, dim, ids, ids_stride, cap, n, out,
+                                                   out_stride, err);
+  else
+    gather_slots_kernel<false><<<grid, 256, 0, st>>>(table, rows, dim, ids, ids_stride, cap, n,
+                                                    out, out_stride, err);
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;

@@ -333,17 +333,29 @@ static int bits_for(uint64_t max_value) {
   return b;
 }
 
+// Ids read densely (cap == 0) or from a slot layout: id i = slot (i / cap, i % cap) at
+// p[o * stride + s].
+struct IdsView {
+  const int64_t* p;
+  int64_t cap, stride;
+};
+__device__ __forceinline__ int64_t load_id(const IdsView& v, int64_t i) {
+  if (v.cap == 0) return v.p[i];
+  const int64_t o = i / v.cap;
+  return v.p[o * v.stride + (i - o * v.cap)];
+}
+
 // keys for ScatterAdd: key = id (invalid -> sentinel `limit`); for sort_reduce: key =
 // owner * nloc + local (invalid -> R * nloc).  Invalid keys sort last and are skipped.
-__global__ void make_keys_kernel(const int64_t* ids, int64_t n, int64_t limit, int32_t R,
+__global__ void make_keys_kernel(IdsView ids, int64_t n, int64_t limit, int32_t R,
                                  int64_t nloc, int composite, uint32_t* keys, uint32_t* vals,
                                  tfs_device_error* err) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t id = ids[i];
+    const int64_t id = load_id(ids, i);
     uint32_t key;
     if (id < 0 || id >= limit) {
-      report_error(err, TFS_ERR_OUT_OF_RANGE, i);
+      if (id != -1) report_error(err, TFS_ERR_OUT_OF_RANGE, i);  // -1: padding, skipped
       key = composite ? (uint32_t)(R * nloc) : (uint32_t)limit;
     } else {
       key = composite ? (uint32_t)((id % R) * nloc + id / R) : (uint32_t)id;
@@ -428,10 +440,17 @@ struct SegJob {
   float* table;
   float* table2;
   float lr;
-  // write mode (sort_reduce): out_local[u], out_rows[u]
+  // write mode (sort_reduce): out_local[u], out_rows[u]; with slot_base (route_reduce) the row
+  // of segment u (owner o = key / nloc) goes to slot o * cap + (u - slot_base[o]) instead
   int64_t* out_local;
   float* out_rows;
   float* out_rows2;
+  const int64_t* slot_base;
+  int64_t cap;
+  int64_t out_stride, out2_stride;  // per-owner slot region strides of out_rows / out_rows2
+  // input rows in slot layout (row_cap > 0): row i = slot (i / row_cap, i % row_cap) at
+  // rows + o * row_stride + s * dim (rows2 + o * row2_stride + s)
+  int64_t row_cap, row_stride, row2_stride;
   int64_t nloc;
   // apply mode: sums of the segments that lie inside one chunk, [U x dim] (+ [U])
   float* sums;
@@ -449,6 +468,30 @@ struct SegJob {
 struct D4 {
   double x, y, z, w;
 };
+
+// Where segment u's results go in write mode: float offset of its row in out_rows, offset in
+// out_rows2, index in out_local.  row < 0: dropped (slot capacity exceeded).
+struct OutPos {
+  int64_t row, r2, local;
+};
+__device__ __forceinline__ OutPos seg_out_pos(const SegJob& j, int64_t u, uint32_t key) {
+  if (j.slot_base == nullptr) return OutPos{u * j.dim, u, u};
+  const int64_t o = key / (uint32_t)j.nloc;
+  const int64_t s = u - j.slot_base[o];
+  if (s >= j.cap) return OutPos{-1, -1, -1};
+  return OutPos{o * j.out_stride + s * j.dim, o * j.out2_stride + s, -1};
+}
+// Float offset of input row i (and of its rows2 value).
+__device__ __forceinline__ int64_t row_off(const SegJob& j, uint32_t i) {
+  if (j.row_cap == 0) return (int64_t)i * j.dim;
+  const int64_t o = i / j.row_cap;
+  return o * j.row_stride + ((int64_t)i - o * j.row_cap) * j.dim;
+}
+__device__ __forceinline__ int64_t row2_off(const SegJob& j, uint32_t i) {
+  if (j.row_cap == 0) return i;
+  const int64_t o = i / j.row_cap;
+  return o * j.row2_stride + ((int64_t)i - o * j.row_cap);
+}
 
 __device__ __forceinline__ void add4(D4& a, const float4& v) {
   a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
@@ -491,7 +534,7 @@ __global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j, int nslic
     perm_l = j.perm[base + lane];
     seg_l = j.seg_of[base + lane];
     key_l = j.keys[base + lane];
-    if (j.rows2 && slice == 0) r2_l = j.rows2[perm_l];
+    if (j.rows2 && slice == 0) r2_l = j.rows2[row2_off(j, perm_l)];
   }
   // Does the first segment start before this chunk / the last one continue after it?
   uint32_t edge = 0;
@@ -515,7 +558,7 @@ __global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j, int nslic
   for (int r = 0; r < kChunk; ++r) {  // every row of the chunk in flight at once
     const uint32_t pr = __shfl_sync(0xffffffffu, perm_l, r);
     const uint32_t kr = __shfl_sync(0xffffffffu, key_l, r);
-    x[r] = (r < cnt && col_ok) ? __ldg((const float4*)(j.rows + (int64_t)pr * j.dim) + c4)
+    x[r] = (r < cnt && col_ok) ? __ldg((const float4*)(j.rows + row_off(j, pr)) + c4)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
     t[r] = (!write_mode && ((WE >> r) & 1) && col_ok)
                ? *((const float4*)(j.table + (int64_t)kr * j.dim) + c4)
@@ -544,10 +587,13 @@ __global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j, int nslic
     const bool ends_after = r == cnt - 1 && last_after;
     if (!starts_before && !ends_after) {  // whole segment: apply / write now
       if (write_mode) {
-        if (col_ok) reinterpret_cast<float4*>(j.out_rows + (int64_t)sg * j.dim)[c4] = to_f4(acc);
-        if (lane == 0 && slice == 0) {
-          if (j.out_local) j.out_local[sg] = (int64_t)(kr % (uint32_t)j.nloc);
-          if (j.rows2) j.out_rows2[sg] = (float)acc2;
+        const OutPos op = seg_out_pos(j, sg, kr);
+        if (op.row >= 0) {
+          if (col_ok) reinterpret_cast<float4*>(j.out_rows + op.row)[c4] = to_f4(acc);
+          if (lane == 0 && slice == 0) {
+            if (j.out_local) j.out_local[op.local] = (int64_t)(kr % (uint32_t)j.nloc);
+            if (j.rows2) j.out_rows2[op.r2] = (float)acc2;
+          }
         }
       } else {
         if (col_ok) {
@@ -592,8 +638,10 @@ __global__ void __launch_bounds__(256) seg_cross_vec4_kernel(SegJob j) {
 #pragma unroll 16
     for (int64_t ch = c0 + 1; ch <= c1; ++ch)
       add4(acc, reinterpret_cast<const D4*>(j.part + (2 * ch) * j.dim)[c]);
+    const OutPos op = write_mode ? seg_out_pos(j, s, key) : OutPos{0, 0, 0};
+    if (op.row < 0) continue;
     if (write_mode) {
-      reinterpret_cast<float4*>(j.out_rows + (int64_t)s * j.dim)[c] = to_f4(acc);
+      reinterpret_cast<float4*>(j.out_rows + op.row)[c] = to_f4(acc);
     } else {
       float4* tp = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c;
       float4 w = *tp;
@@ -605,12 +653,12 @@ __global__ void __launch_bounds__(256) seg_cross_vec4_kernel(SegJob j) {
       *tp = w;
     }
     if (c == 0) {
-      if (write_mode && j.out_local) j.out_local[s] = (int64_t)(key % (uint32_t)j.nloc);
+      if (write_mode && j.out_local) j.out_local[op.local] = (int64_t)(key % (uint32_t)j.nloc);
       if (j.rows2) {
         double acc2 = j.part2[2 * c0 + 1];
         for (int64_t ch = c0 + 1; ch <= c1; ++ch) acc2 += j.part2[2 * ch];
         if (write_mode)
-          j.out_rows2[s] = (float)acc2;
+          j.out_rows2[op.r2] = (float)acc2;
         else if (j.table2)
           j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * acc2);
       }
@@ -631,7 +679,7 @@ __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
     perm_l = j.perm[base + lane];
     seg_l = j.seg_of[base + lane];
     key_l = j.keys[base + lane];
-    if (j.rows2) r2_l = j.rows2[perm_l];
+    if (j.rows2) r2_l = j.rows2[row2_off(j, perm_l)];
   }
   uint32_t edge = 0;
   if (lane == 0 && base > 0) edge = j.keys[base - 1] == j.keys[base];
@@ -650,9 +698,12 @@ __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
       const PieceDst dst = piece_dst(r_start == 0 && first_before, r_end == cnt && last_after,
                                      chunk);
       if (dst.kind == 0) {
+        const OutPos op = write_mode ? seg_out_pos(j, cur, cur_key)
+                                     : OutPos{(int64_t)cur * j.dim, (int64_t)cur, (int64_t)cur};
+        if (op.row < 0) return;
         float* o = write_mode ? j.out_rows : j.sums;
-        if (c < j.dim) o[(int64_t)cur * j.dim + c] = (float)acc;
-        if (j.rows2 && lane == 0 && c0 == 0) (write_mode ? j.out_rows2 : j.sums2)[cur] = (float)acc2;
+        if (c < j.dim) o[op.row + c] = (float)acc;
+        if (j.rows2 && lane == 0 && c0 == 0) (write_mode ? j.out_rows2 : j.sums2)[op.r2] = (float)acc2;
       } else {
         if (c < j.dim) j.part[dst.slot * j.dim + c] = acc;
         if (j.rows2 && lane == 0 && c0 == 0) j.part2[dst.slot] = acc2;
@@ -663,7 +714,7 @@ __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
       const uint32_t s = __shfl_sync(0xffffffffu, seg_l, r);
       const uint32_t k = __shfl_sync(0xffffffffu, key_l, r);
       const float r2 = __shfl_sync(0xffffffffu, r2_l, r);
-      const float xv = c < j.dim ? j.rows[(int64_t)pr * j.dim + c] : 0.f;
+      const float xv = c < j.dim ? j.rows[row_off(j, pr) + c] : 0.f;
       if (s != cur) {
         flush(r);
         cur = s;
@@ -695,7 +746,9 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
     const uint32_t a = j.seg_start[u], b = j.seg_start[u + 1];
     const uint32_t key = j.keys[a];
     if (key >= j.invalid_key) continue;
-    if (write_mode && c == 0 && j.out_local) j.out_local[u] = (int64_t)(key % (uint32_t)j.nloc);
+    const OutPos op = write_mode ? seg_out_pos(j, u, key) : OutPos{u * j.dim, u, u};
+    if (op.row < 0) continue;
+    if (write_mode && c == 0 && j.out_local) j.out_local[op.local] = (int64_t)(key % (uint32_t)j.nloc);
     const int64_t c0 = a / kChunk, c1 = (b - 1) / kChunk;
     const bool cross = c0 != c1;
     if (write_mode && !cross) continue;  // the chunk kernel already wrote it
@@ -711,7 +764,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
         acc = D4{s.x, s.y, s.z, s.w};
       }
       if (write_mode) {
-        reinterpret_cast<float4*>(j.out_rows + u * j.dim)[c] = to_f4(acc);
+        reinterpret_cast<float4*>(j.out_rows + op.row)[c] = to_f4(acc);
       } else {
         float4* t = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c;
         float4 w = *t;
@@ -732,7 +785,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
         acc = j.sums[u * j.dim + c];
       }
       if (write_mode) {
-        j.out_rows[u * j.dim + c] = (float)acc;
+        j.out_rows[op.row + c] = (float)acc;
       } else {
         float* t = j.table + (int64_t)key * j.dim + c;
         *t = (float)((double)*t - (double)j.lr * acc);
@@ -747,7 +800,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
         acc2 = write_mode ? 0.0 : j.sums2[u];
       }
       if (write_mode) {
-        j.out_rows2[u] = (float)acc2;
+        j.out_rows2[op.r2] = (float)acc2;
       } else if (j.table2) {
         j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * acc2);
       }
@@ -880,7 +933,7 @@ __device__ __forceinline__ uint32_t cta1024_exclusive_scan(uint32_t v, uint32_t*
 }
 
 __global__ void __launch_bounds__(kSmallThreads, 1) sort_segment_small_kernel(
-    const int64_t* ids, int n, int64_t limit, int32_t R, int64_t nloc, int composite, int passes,
+    IdsView ids, int n, int64_t limit, int32_t R, int64_t nloc, int composite, int passes,
     uint32_t* keys_out, uint32_t* perm_out, uint32_t* seg_start, uint32_t* seg_of,
     int64_t* num_unique, tfs_device_error* err) {
   extern __shared__ uint32_t sm[];
@@ -896,10 +949,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) sort_segment_small_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   for (int i = tid; i < n; i += kSmallThreads) {
-    const int64_t id = ids[i];
+    const int64_t id = load_id(ids, i);
     uint32_t key;
     if (id < 0 || id >= limit) {
-      report_error(err, TFS_ERR_OUT_OF_RANGE, i);
+      if (id != -1) report_error(err, TFS_ERR_OUT_OF_RANGE, i);  // -1: padding, skipped
       key = composite ? (uint32_t)(R * nloc) : (uint32_t)limit;
     } else {
       key = composite ? (uint32_t)((id % R) * nloc + id / R) : (uint32_t)id;
@@ -991,7 +1044,7 @@ static size_t small_sort_smem(int64_t n) {
   return (size_t)(kCntWords * 4 + cap * 4 * 2 + cap * 2 * 2);
 }
 
-static int32_t sort_and_segment(const int64_t* ids, int64_t n, int64_t limit, int32_t R,
+static int32_t sort_and_segment(IdsView ids, int64_t n, int64_t limit, int32_t R,
                                 int64_t nloc, int composite, uint32_t key_max, SegScratch& s,
                                 tfs_device_error* err, cudaStream_t st) {
   if (n <= kSmallMax) {
@@ -1091,7 +1144,7 @@ extern "C" int32_t tfs_scatter_add_sgd(float* table, int64_t rows, int32_t dim, 
   SegScratch s;
   if (ws_bytes < seg_scratch_bytes(n, dim, &s, ws, ws_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
   cudaStream_t st = as_stream(stream);
-  int32_t rc = sort_and_segment(ids, n, rows, 1, rows + 1, 0, (uint32_t)rows, s, err, st);
+  int32_t rc = sort_and_segment(IdsView{ids, 0, 0}, n, rows, 1, rows + 1, 0, (uint32_t)rows, s, err, st);
   if (rc != TFS_OK) return rc;
   SegJob j{};
   bind(j, s, n);
@@ -1117,7 +1170,7 @@ extern "C" int32_t tfs_scatter_plan(const int64_t* ids, int64_t n, int64_t rows,
   TFS_SUPPORTED();
   SegScratch s;
   if (plan_bytes < plan_scratch_bytes(n, &s, plan, plan_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
-  return sort_and_segment(ids, n, rows, 1, rows + 1, 0, (uint32_t)rows, s, err, as_stream(stream));
+  return sort_and_segment(IdsView{ids, 0, 0}, n, rows, 1, rows + 1, 0, (uint32_t)rows, s, err, as_stream(stream));
 }
 
 extern "C" size_t tfs_scatter_apply_workspace_bytes(int64_t n, int32_t dim) {
@@ -1152,6 +1205,317 @@ extern "C" int32_t tfs_scatter_add_sgd_planned(float* table, int64_t rows, int32
   return run_segments(j, n, as_stream(stream));
 }
 
+// ---- fixed-capacity routing (R > 1): plan, unpack, reduce -----------------------------------
+// A route plan is the composite-key (owner, local) sort plan of the requester's ids plus the
+// per-owner segment bases: segment u of owner o travels in slot o * cap + (u - base[o]).  Only
+// distinct ids travel (forward dedup); the reduced gradient rows use the same slots.
+namespace tfs {
+
+static size_t route_plan_bytes(int64_t n, int32_t R, SegScratch* s, int64_t** base, void* ws,
+                               size_t cap) {
+  Carver c(ws, cap);
+  SegScratch x{};
+  carve_plan(c, n, x);
+  int64_t* b = c.take<int64_t>((size_t)R + 1);
+  if (s) *s = x;
+  if (base) *base = b;
+  return c.used + 256;
+}
+
+// base[o] = first segment whose owner >= o (owner of an invalid key: R), o = 0..R: every
+// segment u writes the bases of the owners in (owner(u-1), owner(u)], the last one those after
+// it.  Fully parallel (no per-owner binary search).
+__device__ __forceinline__ int64_t seg_owner(const uint32_t* keys, const uint32_t* seg_start,
+                                             int64_t u, int32_t R, int64_t nloc,
+                                             uint32_t invalid_key) {
+  const uint32_t k = keys[seg_start[u]];
+  return k >= invalid_key ? R : (int64_t)(k / (uint32_t)nloc);
+}
+__global__ void route_bases_kernel(const uint32_t* keys, const uint32_t* seg_start,
+                                   const int64_t* num_unique, int64_t n, int32_t R, int64_t nloc,
+                                   uint32_t invalid_key, int64_t* base) {
+  const int64_t U = *num_unique;
+  if (U == 0) {
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o <= R;
+         o += (int64_t)gridDim.x * blockDim.x)
+      base[o] = 0;
+    return;
+  }
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < U;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ou = seg_owner(keys, seg_start, u, R, nloc, invalid_key);
+    const int64_t op = u == 0 ? -1 : seg_owner(keys, seg_start, u - 1, R, nloc, invalid_key);
+    for (int64_t o = op + 1; o <= ou; ++o) base[o] = u;
+    if (u == U - 1)
+      for (int64_t o = ou + 1; o <= R; ++o) base[o] = U;
+  }
+}
+
+__global__ void route_fill_kernel(const uint32_t* keys, const uint32_t* seg_start,
+                                  const int64_t* base, int32_t R, int64_t cap, int64_t nloc,
+                                  int64_t* send_local, int64_t stride, int64_t* counts,
+                                  tfs_device_error* err) {
+  const int64_t total = (int64_t)R * cap;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = e / cap, jx = e - o * cap;
+    if (jx == 0) {
+      const int64_t c = base[o + 1] - base[o];
+      if (counts) counts[o] = c;
+      if (c > cap) report_error(err, TFS_ERR_CAPACITY, o);
+    }
+    const int64_t u = base[o] + jx;
+    send_local[o * stride + jx] =
+        u < base[o + 1] ? (int64_t)(keys[seg_start[u]] % (uint32_t)nloc) : -1;
+  }
+}
+
+// out[t] = slots[o * cap + (u - base[o])] for every original position t (sorted position k:
+// t = perm[k], u = seg_of[k], o = owner of keys[k]).
+template <bool VEC>
+__global__ void route_unpack_kernel(const uint32_t* keys, const uint32_t* perm,
+                                    const uint32_t* seg_of, const int64_t* base, int64_t n,
+                                    int32_t dim, int64_t cap, int64_t nloc, uint32_t invalid_key,
+                                    const float* slots, int64_t stride, float* out) {
+  const int cols = VEC ? dim >> 2 : dim;
+  const int64_t total = n * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / cols;
+    const int c = (int)(e - k * cols);
+    const uint32_t key = keys[k];
+    if (key >= invalid_key) continue;
+    const int64_t o = key / (uint32_t)nloc;
+    const int64_t jx = (int64_t)seg_of[k] - base[o];
+    if (jx >= cap) continue;
+    const int64_t src = o * stride + jx * dim, dst = perm[k];  // float offset of the slot row
+    if (VEC)
+      reinterpret_cast<float4*>(out)[dst * cols + c] =
+          __ldg(reinterpret_cast<const float4*>(slots + src) + c);
+    else
+      out[dst * dim + c] = __ldg(slots + src + c);
+  }
+}
+
+}  // namespace tfs
+
+extern "C" size_t tfs_route_plan_bytes(int64_t n, int32_t num_shards) {
+  return route_plan_bytes(n, num_shards, nullptr, nullptr, nullptr, 0);
+}
+
+extern "C" int32_t tfs_route_plan(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
+                                  int64_t cap, void* plan, size_t plan_bytes,
+                                  int64_t* out_send_local, int64_t send_stride,
+                                  int64_t* out_counts, tfs_device_error* err, void* stream) {
+  TFS_REQUIRE(n >= 1 && vocab >= 1 && num_shards >= 1 && num_shards <= 1024 && cap >= 1);
+  TFS_REQUIRE(send_stride >= cap);
+  TFS_REQUIRE(n < (1ll << 31) && vocab + num_shards < (1ll << 32) - 1);
+  TFS_REQUIRE(ids && plan && out_send_local);
+  TFS_SUPPORTED();
+  SegScratch s;
+  int64_t* base;
+  if (plan_bytes < route_plan_bytes(n, num_shards, &s, &base, plan, plan_bytes))
+    return TFS_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = as_stream(stream);
+  const int64_t nloc = cdiv(vocab, num_shards);
+  const uint32_t invalid = (uint32_t)(num_shards * nloc);
+  int32_t rc = sort_and_segment(IdsView{ids, 0, 0}, n, vocab, num_shards, nloc, 1, invalid, s, err, st);
+  if (rc != TFS_OK) return rc;
+  const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4ll * num_sms()));
+  route_bases_kernel<<<bgrid, 256, 0, st>>>(s.k1, s.seg_start, s.num_unique, n, num_shards, nloc,
+                                            invalid, base);
+  launched();
+  const int64_t total = (int64_t)num_shards * cap;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 4ll * num_sms()));
+  route_fill_kernel<<<grid, 256, 0, st>>>(s.k1, s.seg_start, base, num_shards, cap, nloc,
+                                          out_send_local, send_stride, out_counts, err);
+  launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+extern "C" int32_t tfs_route_unpack(const void* plan, size_t plan_bytes, int64_t n, int64_t vocab,
+                                    int32_t num_shards, int64_t cap, const float* slots,
+                                    int64_t slots_stride, int32_t dim, float* out, void* stream) {
+  TFS_REQUIRE(n >= 1 && vocab >= 1 && num_shards >= 1 && num_shards <= 1024 && cap >= 1 &&
+              dim >= 1 && slots_stride >= cap * dim);
+  TFS_REQUIRE(plan && slots && out);
+  TFS_SUPPORTED();
+  SegScratch s;
+  int64_t* base;
+  if (plan_bytes < route_plan_bytes(n, num_shards, &s, &base, const_cast<void*>(plan), plan_bytes))
+    return TFS_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = as_stream(stream);
+  const int64_t nloc = cdiv(vocab, num_shards);
+  const uint32_t invalid = (uint32_t)(num_shards * nloc);
+  const bool vec = dim % 4 == 0 && slots_stride % 4 == 0 && ((uintptr_t)slots & 15) == 0 &&
+                   ((uintptr_t)out & 15) == 0;
+  const int64_t total = n * (vec ? dim / 4 : dim);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 8ll * num_sms()));
+  if (vec)
+    route_unpack_kernel<true><<<grid, 256, 0, st>>>(s.k1, s.v1, s.seg_of, base, n, dim, cap, nloc,
+                                                    invalid, slots, slots_stride, out);
+  else
+    route_unpack_kernel<false><<<grid, 256, 0, st>>>(s.k1, s.v1, s.seg_of, base, n, dim, cap,
+                                                     nloc, invalid, slots, slots_stride, out);
+  launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+extern "C" size_t tfs_route_reduce_workspace_bytes(int64_t n, int32_t dim) {
+  return apply_scratch_bytes(n, dim, nullptr, nullptr, 0);
+}
+
+extern "C" int32_t tfs_route_reduce(const void* plan, size_t plan_bytes, int64_t n, int64_t vocab,
+                                    int32_t num_shards, int64_t cap, const float* rows,
+                                    int32_t dim, const float* rows2, float* out_slots,
+                                    int64_t out_stride, float* out_slots2, int64_t out2_stride,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  TFS_REQUIRE(n >= 1 && vocab >= 1 && num_shards >= 1 && num_shards <= 1024 && cap >= 1 &&
+              dim >= 1 && out_stride >= cap * dim);
+  TFS_REQUIRE(plan && rows && out_slots);
+  TFS_REQUIRE((rows2 == nullptr) == (out_slots2 == nullptr));
+  TFS_REQUIRE(rows2 == nullptr || out2_stride >= cap);
+  TFS_REQUIRE(dim % 4 != 0 || (((uintptr_t)out_slots & 15) == 0 && out_stride % 4 == 0));
+  TFS_SUPPORTED();
+  SegScratch s;
+  int64_t* base;
+  if (plan_bytes < route_plan_bytes(n, num_shards, &s, &base, const_cast<void*>(plan), plan_bytes))
+    return TFS_ERR_WORKSPACE_TOO_SMALL;
+  if (ws_bytes < apply_scratch_bytes(n, dim, &s, ws, ws_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+  const int64_t nloc = cdiv(vocab, num_shards);
+  SegJob j{};
+  bind(j, s, n);
+  j.rows = rows;
+  j.rows2 = rows2;
+  j.dim = dim;
+  j.invalid_key = (uint32_t)(num_shards * nloc);
+  j.out_rows = out_slots;
+  j.out_rows2 = out_slots2;
+  j.nloc = nloc;
+  j.slot_base = base;
+  j.cap = cap;
+  j.out_stride = out_stride;
+  j.out2_stride = out2_stride;
+  return run_segments(j, n, as_stream(stream));
+}
+
+// ---- merge of R ascending runs (owner side: every requester's distinct ids, ascending) -------
+// Entry i = slot (o, s) of R runs of cap slots; a run is strictly ascending valid ids followed
+// by -1 padding.  Sorted order = valid ids ascending, equal ids by run (requester) order, then
+// the padding in entry order -- exactly the stable sort by key of the entries.  Every entry
+// finds its place with R binary searches (one kernel instead of the radix passes).
+__device__ __forceinline__ uint32_t run_key(const IdsView& v, int64_t o, int64_t s,
+                                            int64_t limit) {
+  const int64_t id = v.p[o * v.stride + s];
+  return (id < 0 || id >= limit) ? 0xFFFFFFFFu : (uint32_t)id;
+}
+// number of entries of run o with key < x (strict) or <= x
+__device__ __forceinline__ int64_t run_rank(const IdsView& v, int64_t o, int64_t cap,
+                                            uint32_t x, bool inclusive, int64_t limit) {
+  int64_t lo = 0, hi = cap;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const uint32_t k = run_key(v, o, mid, limit);
+    if (inclusive ? k <= x : k < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__global__ void merge_runs_kernel(IdsView ids, int32_t R, int64_t cap, int64_t limit,
+                                  uint32_t* keys_out, uint32_t* perm_out,
+                                  tfs_device_error* err) {
+  const int64_t n = (int64_t)R * cap;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i / cap, s = i - o * cap;
+    const int64_t id = ids.p[o * ids.stride + s];
+    const uint32_t k = run_key(ids, o, s, limit);
+    if (id != -1 && k == 0xFFFFFFFFu) report_error(err, TFS_ERR_OUT_OF_RANGE, i);
+    if (s + 1 < cap) {  // the promised layout: strictly ascending, padding only at the end
+      const uint32_t kn = run_key(ids, o, s + 1, limit);
+      if (kn != 0xFFFFFFFFu && kn <= k) report_error(err, TFS_ERR_INVALID_ARGUMENT, i);
+    }
+    int64_t pos;
+    if (k != 0xFFFFFFFFu) {
+      pos = s;
+      for (int64_t q = 0; q < R; ++q)
+        if (q != o) pos += run_rank(ids, q, cap, k, q < o, limit);
+    } else {
+      int64_t valid = 0, before = 0;
+      for (int64_t q = 0; q < R; ++q) {
+        const int64_t c = run_rank(ids, q, cap, 0xFFFFFFFEu, true, limit);
+        valid += c;
+        if (q < o) before += cap - c;
+        else if (q == o) before += s - c;
+      }
+      pos = valid + before;
+    }
+    keys_out[pos] = k == 0xFFFFFFFFu ? (uint32_t)limit : k;
+    perm_out[pos] = (uint32_t)i;
+  }
+}
+
+// ---- planned ScatterAdd-SGD over ids / gradients received in slot layout (R x cap) ----------
+extern "C" int32_t tfs_scatter_plan_slots(const int64_t* ids, int64_t ids_stride, int32_t R,
+                                          int64_t cap, int64_t rows, int32_t sorted_runs,
+                                          void* plan, size_t plan_bytes, tfs_device_error* err,
+                                          void* stream) {
+  TFS_REQUIRE(R >= 1 && cap >= 1 && ids_stride >= cap && rows >= 0 && rows < (1ll << 31) - 1);
+  const int64_t n = (int64_t)R * cap;
+  TFS_REQUIRE(n < (1ll << 31) && ids && plan);
+  TFS_SUPPORTED();
+  SegScratch s;
+  if (plan_bytes < plan_scratch_bytes(n, &s, plan, plan_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = as_stream(stream);
+  if (!sorted_runs)
+    return sort_and_segment(IdsView{ids, cap, ids_stride}, n, rows, 1, rows + 1, 0,
+                            (uint32_t)rows, s, err, st);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8ll * num_sms()));
+  merge_runs_kernel<<<grid, 256, 0, st>>>(IdsView{ids, cap, ids_stride}, R, cap, rows, s.k1, s.v1,
+                                          err);
+  launched();
+  const int ntiles = (int)cdiv(n, kSortTile);
+  heads_count_kernel<<<ntiles, kSortThreads, 0, st>>>(s.k1, n, s.tile_cnt);
+  launched();
+  heads_write_kernel<<<ntiles, kSortThreads, 0, st>>>(s.k1, n, s.tile_cnt, ntiles, s.seg_start,
+                                                      s.seg_of, s.num_unique);
+  launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+extern "C" int32_t tfs_scatter_add_sgd_planned_slots(
+    float* table, int64_t rows, int32_t dim, const void* plan, size_t plan_bytes, int32_t R,
+    int64_t cap, const float* grad, int64_t grad_stride, float lr, float* table2,
+    const float* grad2, int64_t grad2_stride, void* ws, size_t ws_bytes, void* stream) {
+  TFS_REQUIRE(R >= 1 && cap >= 1 && dim >= 1 && rows >= 0 && rows < (1ll << 31) - 1);
+  TFS_REQUIRE(grad_stride >= cap * dim && (grad2 == nullptr || grad2_stride >= cap));
+  TFS_REQUIRE((table2 == nullptr) == (grad2 == nullptr));
+  const int64_t n = (int64_t)R * cap;
+  TFS_REQUIRE(table && plan && grad && n < (1ll << 31));
+  TFS_REQUIRE(dim % 4 != 0 || (((uintptr_t)table & 15) == 0 && grad_stride % 4 == 0));
+  TFS_SUPPORTED();
+  SegScratch s;
+  if (plan_bytes < plan_scratch_bytes(n, &s, const_cast<void*>(plan), plan_bytes))
+    return TFS_ERR_WORKSPACE_TOO_SMALL;
+  if (ws_bytes < apply_scratch_bytes(n, dim, &s, ws, ws_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+  SegJob j{};
+  bind(j, s, n);
+  j.rows = grad;
+  j.rows2 = grad2;
+  j.dim = dim;
+  j.invalid_key = (uint32_t)rows;
+  j.table = table;
+  j.table2 = table2;
+  j.lr = lr;
+  j.nloc = rows + 1;
+  j.row_cap = cap;
+  j.row_stride = grad_stride;
+  j.row2_stride = grad2_stride;
+  return run_segments(j, n, as_stream(stream));
+}
+
 extern "C" size_t tfs_sort_reduce_workspace_bytes(int64_t n, int32_t dim) {
   return seg_scratch_bytes(n, dim, nullptr, nullptr, 0);
 }
@@ -1179,7 +1543,7 @@ extern "C" int32_t tfs_sort_reduce(const int64_t* ids, int64_t n, int64_t vocab,
   if (ws_bytes < seg_scratch_bytes(n, dim, &s, ws, ws_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
   const int64_t nloc = cdiv(vocab, num_shards);
   const uint32_t invalid = (uint32_t)(num_shards * nloc);
-  int32_t rc = sort_and_segment(ids, n, vocab, num_shards, nloc, 1, invalid, s, err, st);
+  int32_t rc = sort_and_segment(IdsView{ids, 0, 0}, n, vocab, num_shards, nloc, 1, invalid, s, err, st);
   if (rc != TFS_OK) return rc;
   SegJob j{};
   bind(j, s, n);

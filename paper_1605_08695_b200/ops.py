@@ -234,6 +234,80 @@ class ScatterPlan:
         return table
 
 
+class RoutePlan:
+    """Requester side of a fixed-capacity route between R shards (tfs_route_*): the plan of
+    ``n`` ids (built from ids only), its send ids in slot layout, the Stitch of received rows
+    and the reduction of gradient rows into slots.  Slot regions are ``stride`` elements
+    apart; each holds ``cap`` slots."""
+
+    def __init__(self, n: int, vocab: int, R: int, cap: int, dim: int, device):
+        L = _lib.lib()
+        self.n, self.vocab, self.R, self.cap = int(n), int(vocab), int(R), int(cap)
+        self.plan = _ws(L.tfs_route_plan_bytes(n, R), device)
+        self.ws = _ws(L.tfs_route_reduce_workspace_bytes(n, dim), device)
+
+    def build(self, ids, send, send_stride: int, counts=None, err: ErrorSlot = None):
+        assert ids.numel() == self.n
+        check(_lib.lib().tfs_route_plan(_p(ids), self.n, self.vocab, self.R, self.cap,
+                                        _p(self.plan), self.plan.numel(), _p(send),
+                                        int(send_stride), _p(counts), _err(err), _stream()),
+              "tfs_route_plan")
+        return self
+
+    def unpack(self, slots, slots_stride: int, dim: int, out):
+        check(_lib.lib().tfs_route_unpack(_p(self.plan), self.plan.numel(), self.n, self.vocab,
+                                          self.R, self.cap, _p(slots), int(slots_stride),
+                                          int(dim), _p(out), _stream()), "tfs_route_unpack")
+        return out
+
+    def reduce(self, rows, dim: int, out, out_stride: int, rows2=None, out2=None,
+               out2_stride: int = 0):
+        check(_lib.lib().tfs_route_reduce(_p(self.plan), self.plan.numel(), self.n, self.vocab,
+                                          self.R, self.cap, _p(rows), int(dim), _p(rows2),
+                                          _p(out), int(out_stride), _p(out2), int(out2_stride),
+                                          _p(self.ws), self.ws.numel(), _stream()),
+              "tfs_route_reduce")
+        return out
+
+
+def gather_slots(table, ids, ids_stride: int, num_slots: int, cap: int, out, out_stride: int,
+                 err: ErrorSlot = None):
+    """Owner side: rows of the received slot ids (-1 = padding) into slot layout."""
+    rows = table.shape[0]
+    dim = 1 if table.dim() == 1 else table.shape[1]
+    check(_lib.lib().tfs_gather_slots(_p(table), rows, dim, _p(ids), int(ids_stride),
+                                      int(num_slots), int(cap), _p(out), int(out_stride),
+                                      _err(err), _stream()), "tfs_gather_slots")
+    return out
+
+
+class SlotScatterPlan:
+    """Owner side: planned ScatterAdd-SGD over R x cap received slots (tfs_scatter_*_slots)."""
+
+    def __init__(self, R: int, cap: int, rows: int, dim: int, device):
+        L = _lib.lib()
+        self.R, self.cap, self.rows, self.dim = int(R), int(cap), int(rows), int(dim)
+        n = self.R * self.cap
+        self.plan = _ws(L.tfs_scatter_plan_bytes(n), device)
+        self.ws = _ws(L.tfs_scatter_apply_workspace_bytes(n, dim), device)
+
+    def build(self, ids, ids_stride: int, sorted_runs: bool = True, err: ErrorSlot = None):
+        """sorted_runs: every region is ascending ids + trailing -1 (as tfs_route_plan sends)."""
+        check(_lib.lib().tfs_scatter_plan_slots(_p(ids), int(ids_stride), self.R, self.cap,
+                                                self.rows, int(sorted_runs), _p(self.plan),
+                                                self.plan.numel(), _err(err), _stream()),
+              "tfs_scatter_plan_slots")
+        return self
+
+    def apply(self, table, grad, grad_stride: int, lr: float, table2=None, grad2=None,
+              grad2_stride: int = 0):
+        check(_lib.lib().tfs_scatter_add_sgd_planned_slots(
+            _p(table), self.rows, self.dim, _p(self.plan), self.plan.numel(), self.R, self.cap,
+            _p(grad), int(grad_stride), float(lr), _p(table2), _p(grad2), int(grad2_stride),
+            _p(self.ws), self.ws.numel(), _stream()), "tfs_scatter_add_sgd_planned_slots")
+        return table
+
+
 def debug_gemm_bf16(A, B, ksplit: int = 1, a_mn: bool = False, b_mn: bool = False):
     """C[ks] = sum_k A(m, k) B(n, k) on the tcgen05 path (diagnostics).  A is [M, K] (K-major)
     or, with a_mn, [K, M] (MN-major); likewise B is [N, K] or [K, N]."""

@@ -44,6 +44,11 @@ class StepConfig:
     flags: int = TFS_SUBTRACT_LOG_Q | TFS_REMOVE_ACCIDENTAL_HITS
     operand_dtype: int = TFS_BF16
     full_softmax: bool = False  # candidates = all V classes (config F; R must be 1)
+    # R > 1 fixed-capacity routes: distinct ids per (requester, owner) pair are expected near
+    # n / R (ids mod R); slots per owner = min(n, ceil(route_slack * n / R) + route_pad).
+    # An overflow is reported as TFS_ERR_CAPACITY (never silent).
+    route_slack: float = 1.25
+    route_pad: int = 64
 
 
 class Router:
@@ -69,6 +74,11 @@ class Router:
         send = [[both[0][o][j] for o in range(self.R)] for j in range(k)]
         rcv = [[both[1][o][j] for o in range(self.R)] for j in range(k)]
         return send, rcv
+
+    def a2a(self, out: torch.Tensor, inp: torch.Tensor):
+        """Equal-split all-to-all of [R, ...] buffers (fixed size: no host counts, capturable)."""
+        self.dist.all_to_all_single(out, inp, group=self.group)
+        return out
 
     def route(self, payload: torch.Tensor, send_counts, recv_counts) -> torch.Tensor:
         n_send = sum(send_counts)
@@ -138,10 +148,6 @@ class ShardedStep:
             self.flags = cfg.flags
         R = self.R
         L = ops._lib.lib()
-        self.part_x = (torch.empty(B, **i64), torch.empty(B, **i64), torch.empty(R, **i64))
-        self.part_w = (torch.empty(B + S, **i64), torch.empty(B + S, **i64), torch.empty(R, **i64))
-        self.ws_part = ops._ws(L.tfs_partition_workspace_bytes(B + S, R), dev)
-        self.ws_part_x = ops._ws(L.tfs_partition_workspace_bytes(B, R), dev)
         self.side_stream = torch.cuda.Stream(device=dev)
         self.h = torch.empty((B, d), **f32)
         self.w_rows = torch.empty((B + S, d), **f32)
@@ -158,14 +164,50 @@ class ShardedStep:
             self.plan_w = ops.ScatterPlan(B + S, W.shape[0], d, dev)
             self.ev = {k: torch.cuda.Event() for k in ("h", "q", "plan_w", "ssm")}
         else:
-            self.ws_sr_e = ops._ws(L.tfs_sort_reduce_workspace_bytes(B, d), dev)
-            self.ws_sr_w = ops._ws(L.tfs_sort_reduce_workspace_bytes(B + S, d), dev)
-            self.sr_e = (torch.empty(B, **i64), torch.empty((B, d), **f32), None,
-                         torch.empty(R, **i64), torch.empty(1, **i64))
-            self.sr_w = (torch.empty(B + S, **i64), torch.empty((B + S, d), **f32),
-                         torch.empty(B + S, **f32), torch.empty(R, **i64), torch.empty(1, **i64))
+            # Slot layout of the three exchanges (ids forward, rows forward, gradients back):
+            # region o of each buffer goes to / comes from rank o.
+            #   ids   int64 [R, cap_e + cap_w]          E ids | W ids
+            #   rows  f32   [R, rstride]                 E rows | W rows | b   (rows of d)
+            #   grads f32   [R, rstride]                 dE rows | dW rows | db
+            def cap_for(n):
+                return int(min(n, -(-cfg.route_slack * n // R) + cfg.route_pad))
+            self.set_route_caps(cap_for(B), cap_for(B + S))
+            self.ev = {k: torch.cuda.Event() for k in ("route_e", "ids", "own")}
         self.graph = None
         self.phase_events = None  # list of (phase, start, end) when instrumented
+
+    def set_route_caps(self, cap_e: int, cap_w: int):
+        """(Re)allocate the R > 1 slot buffers for cap_e / cap_w distinct ids per owner."""
+        R, B, S, d, V, dev = self.R, self.B, self.S, self.d, self.cfg.vocab, self.device
+        f32 = dict(dtype=torch.float32, device=dev)
+        i64 = dict(dtype=torch.int64, device=dev)
+        ce, cw = int(min(cap_e, B)), int(min(cap_w, B + S))
+        self.cap_e, self.cap_w = ce, cw
+        self.istride = ce + cw
+        self.off_w, self.off_b = ce * d, (ce + cw) * d
+        self.rstride = -(-((ce + cw) * d + cw) // 4) * 4  # 16-byte aligned regions
+        self.send_ids = torch.empty((R, self.istride), **i64)
+        self.recv_ids = torch.empty((R, self.istride), **i64)
+        self.send_rows = torch.empty((R, self.rstride), **f32)
+        self.recv_rows = torch.empty((R, self.rstride), **f32)
+        self.send_grads = torch.empty((R, self.rstride), **f32)
+        self.recv_grads = torch.empty((R, self.rstride), **f32)
+        self.route_e = ops.RoutePlan(B, V, R, ce, d, dev)
+        self.route_w = ops.RoutePlan(B + S, V, R, cw, d, dev)
+        self.own_e = ops.SlotScatterPlan(R, ce, self.E.shape[0], d, dev)
+        self.own_w = ops.SlotScatterPlan(R, cw, self.W.shape[0], d, dev)
+        self.counts = torch.zeros((2, R), **i64)  # distinct ids per owner of the last step
+        self.graph = None
+
+    def calibrate_routes(self, margin: float = 1.25, pad: int = 64):
+        """Shrink the slot capacities to margin x the largest per-owner distinct-id count of
+        the last eager step (max over ranks) + pad: the fixed-size exchanges then move little
+        padding.  Overflow in a later step is still reported (TFS_ERR_CAPACITY)."""
+        c = self.counts.max(dim=1).values.clone()
+        self.router.dist.all_reduce(c, op=self.router.dist.ReduceOp.MAX, group=self.router.group)
+        ce, cw = (int(v * margin) + pad for v in c.tolist())
+        self.set_route_caps(ce, cw)
+        return ce, cw
 
     # ------------------------------------------------------------------------------------------
     def _sample(self, step: int | None):
@@ -253,43 +295,57 @@ class ShardedStep:
             self.plan_w.apply(self.W, self.dw, self.cfg.lr, table2=self.b, grad2=self.db)
 
     def _dist_step(self, step: int | None):
-        """R > 1: Part -> route -> Gather -> route back -> Stitch -> softmax -> sort-reduce ->
-        route -> ScatterAdd-SGD on the owner."""
+        """R > 1, host-synchronisation free (capturable): plans -> ids a2a -> owner Gather ->
+        rows a2a -> Stitch -> softmax -> per-id gradient sums -> gradients a2a -> owner SGD.
+
+        Only distinct ids travel; every exchange is an equal-split all-to-all of slot regions
+        (tfs_route_*), so no count ever reaches the host.  The E route plan is built on the
+        side stream while the main stream samples; the owner-side ScatterAdd plans (a function
+        of the received ids only) are built on the side stream while the softmax runs."""
         V, B, R, d = self.cfg.vocab, self.B, self.R, self.d
-        rt = self.router
+        rt, ev = self.router, self.ev
+        main, side = torch.cuda.current_stream(), self.side_stream
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self.route_e.build(self.x, self.send_ids, self.istride, counts=self.counts[0],
+                               err=self.err)
+            ev["route_e"].record(side)
         self.qw[:B].copy_(self.y)
         self._sample(step)
-        xl, xpos, xcnt = ops.partition(self.x, V, R, err=self.err, out=self.part_x,
-                                       ws=self.ws_part_x)
-        wl, wpos, wcnt = ops.partition(self.qw, V, R, err=self.err, out=self.part_w, ws=self.ws_part)
-        (sx, sw), (rx, rw) = rt.exchange_counts(torch.stack([xcnt, wcnt], dim=1))
-        ids_x = rt.route(xl, sx, rx)
-        ids_w = rt.route(wl, sw, rw)
-        # Gather on the owner (colocated with the shard, P:688-691), send the rows back.
-        rows_e = ops.gather(self.E, ids_x, err=self.err)
-        rows_w = ops.gather(self.W, ids_w, err=self.err)
-        rows_b = ops.gather(self.b, ids_w, err=self.err)
-        back_e = rt.route(rows_e, rx, sx)
-        back_w = rt.route(rows_w, rw, sw)
-        back_b = rt.route(rows_b, rw, sw)
-        ops.stitch(xpos, back_e, out=self.h)
-        ops.stitch(wpos, back_w, out=self.w_rows)
-        ops.stitch(wpos, back_b.view(-1), out=self.b_rows)
+        self.route_w.build(self.qw, self.send_ids[:, self.cap_e:], self.istride,
+                           counts=self.counts[1], err=self.err)
+        main.wait_event(ev["route_e"])
+        rt.a2a(self.recv_ids, self.send_ids)                        # ids -> owners
+        ev["ids"].record(main)
+        with torch.cuda.stream(side):                               # owner plans (backward)
+            side.wait_event(ev["ids"])
+            self.own_e.build(self.recv_ids, self.istride, err=self.err)
+            self.own_w.build(self.recv_ids[:, self.cap_e:], self.istride, err=self.err)
+            ev["own"].record(side)
+        ce, cw, rs = self.cap_e, self.cap_w, self.rstride
+        rows = self.send_rows
+        ops.gather_slots(self.E, self.recv_ids, self.istride, R, ce, rows, rs, err=self.err)
+        ops.gather_slots(self.W, self.recv_ids[:, ce:], self.istride, R, cw, rows[:, self.off_w:],
+                         rs, err=self.err)
+        ops.gather_slots(self.b, self.recv_ids[:, ce:], self.istride, R, cw, rows[:, self.off_b:],
+                         rs, err=self.err)
+        rt.a2a(self.recv_rows, self.send_rows)                      # rows -> requesters
+        got = self.recv_rows
+        self.route_e.unpack(got, rs, d, self.h)
+        self.route_w.unpack(got[:, self.off_w:], rs, d, self.w_rows)
+        self.route_w.unpack(got[:, self.off_b:], rs, 1, self.b_rows)
         self._softmax()
-        # Sparse gradients: sum per id locally, route to the owners, apply there.
-        le, ge, _, ce, _ = ops.sort_reduce(self.x, V, R, self.ssm_out["dh"], err=self.err,
-                                           out=self.sr_e, ws=self.ws_sr_e)
-        lw, gw, gb, cw, _ = ops.sort_reduce(self.qw, V, R, self.dw, rows2=self.db, err=self.err,
-                                            out=self.sr_w, ws=self.ws_sr_w)
-        (se, sw2), (re, rw2) = rt.exchange_counts(torch.stack([ce, cw], dim=1))
-        r_ids_e = rt.route(le, se, re)
-        r_g_e = rt.route(ge, se, re)
-        r_ids_w = rt.route(lw, sw2, rw2)
-        r_g_w = rt.route(gw, sw2, rw2)
-        r_g_b = rt.route(gb, sw2, rw2)
-        ops.scatter_add_sgd(self.E, r_ids_e, r_g_e, self.cfg.lr, err=self.err)
-        ops.scatter_add_sgd(self.W, r_ids_w, r_g_w, self.cfg.lr, table2=self.b, grad2=r_g_b,
-                            err=self.err)
+        g = self.send_grads
+        self.route_e.reduce(self.ssm_out["dh"], d, g, rs)
+        self.route_w.reduce(self.dw, d, g[:, self.off_w:], rs, rows2=self.db,
+                            out2=g[:, self.off_b:], out2_stride=rs)
+        rt.a2a(self.recv_grads, self.send_grads)                    # gradients -> owners
+        main.wait_event(ev["own"])
+        gr = self.recv_grads
+        self.own_e.apply(self.E, gr, rs, self.cfg.lr)
+        self.own_w.apply(self.W, gr[:, self.off_w:], rs, self.cfg.lr, table2=self.b,
+                         grad2=gr[:, self.off_b:], grad2_stride=rs)
+        main.wait_stream(side)
 
     # ------------------------------------------------------------------------------------------
     def run(self, x: torch.Tensor, y: torch.Tensor, step: int):
@@ -303,15 +359,16 @@ class ShardedStep:
         return self.ssm_out["loss_sum"]
 
     def capture(self, first_step: int = 0):
-        """R = 1 only: capture the whole step (inputs read from self.x / self.y, step counter
-        from self.step_dev, advanced by one inside the graph) into a CUDA graph."""
-        assert self.R == 1
+        """Capture the whole step (inputs read from self.x / self.y, step counter from
+        self.step_dev, advanced by one inside the graph) into a CUDA graph.  Any R: the R > 1
+        step has no host synchronisation (fixed-capacity all-to-alls over NCCL)."""
         saved = (self.E.clone(), self.W.clone(), self.b.clone())
         self.step_dev.fill_(first_step)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
+        step_fn = self._local_step if self.R == 1 else self._dist_step
         with torch.cuda.stream(s):
-            self._local_step(None)       # warm-up (lazy init of kernels / attributes)
+            step_fn(None)                # warm-up (lazy init of kernels / attributes)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         for dst, src in zip((self.E, self.W, self.b), saved):  # undo the warm-up update
@@ -319,10 +376,11 @@ class ShardedStep:
         del saved
         self.step_dev.fill_(first_step)
         torch.cuda.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
+        self.graph = torch.cuda.CUDAGraph(keep_graph=True)  # raw graph kept for inspection
         with torch.cuda.graph(self.graph):
-            self._local_step(None)
+            step_fn(None)
             self.step_dev.add_(1)
+        self.graph.instantiate()
         torch.cuda.synchronize()
         return self.graph
 

@@ -369,3 +369,70 @@ def test_planned_scatter_matches_unplanned(n, dim, zipf):
     plan.apply(b, T(g1), 0.1, table2=bb, grad2=T(gb))
     plan.apply(b, T(g2), 0.1)
     assert torch.equal(a, b) and torch.equal(ab, bb)
+
+
+@pytest.mark.parametrize("R,n,dim,cap", [(3, 700, 64, 400), (2, 2560, 512, 1500), (4, 999, 6, 300)])
+def test_fixed_capacity_route_round_trip(R, n, dim, cap):
+    """tfs_route_plan / tfs_gather_slots / tfs_route_unpack / tfs_route_reduce /
+    tfs_scatter_*_slots with R requesters simulated on one GPU (the all-to-all is a tensor
+    transpose of slot regions): the stitched rows equal table[ids] bit for bit, and the owner
+    updates equal per-requester fixed-order sums added in requester order; the merge plan
+    (sorted runs) equals the radix plan bit for bit."""
+    rng = np.random.default_rng(R * n + dim)
+    V, lr = 5000, 0.5
+    table = rng.standard_normal((V, dim)).astype(np.float32)
+    ids = [workloads.zipf_ids(rng, V, 1.1, n) for _ in range(R)]
+    grads = [rng.standard_normal((n, dim)).astype(np.float32) for _ in range(R)]
+    stride = cap + 5                     # regions wider than the slots
+    rstride = (cap * dim + 8) // 4 * 4
+    plans, send = [], torch.full((R, R, stride), -9, dtype=torch.int64, device=DEV)
+    counts = torch.zeros((R, R), dtype=torch.int64, device=DEV)
+    for r in range(R):
+        plans.append(ops.RoutePlan(n, V, R, cap, dim, DEV).build(T(ids[r]), send[r], stride,
+                                                                 counts=counts[r]))
+    recv = send.transpose(0, 1).contiguous()               # recv[o][src] = send[src][o]
+    for r in range(R):
+        want = [len(np.unique(ids[r][ids[r] % R == o])) for o in range(R)]
+        assert counts[r].tolist() == want
+    rows = torch.zeros((R, R, rstride), dtype=torch.float32, device=DEV)
+    for o in range(R):
+        ops.gather_slots(T(np.ascontiguousarray(table[o::R])), recv[o], stride, R, cap, rows[o],
+                         rstride)
+    back = rows.transpose(0, 1).contiguous()               # back[r][o] = rows[o][r]
+    for r in range(R):
+        h = torch.empty((n, dim), dtype=torch.float32, device=DEV)
+        plans[r].unpack(back[r], rstride, dim, h)
+        assert np.array_equal(h.cpu().numpy(), table[ids[r]])
+    gs = torch.zeros((R, R, rstride), dtype=torch.float32, device=DEV)
+    for r in range(R):
+        plans[r].reduce(T(grads[r]), dim, gs[r], rstride)
+    gr = gs.transpose(0, 1).contiguous()
+    for o in range(R):
+        shard = table[o::R]
+        res = []
+        for sorted_runs in (True, False):
+            t = T(np.ascontiguousarray(shard))
+            p = ops.SlotScatterPlan(R, cap, shard.shape[0], dim, DEV)
+            p.build(recv[o], stride, sorted_runs=sorted_runs)
+            p.apply(t, gr[o], rstride, lr)
+            res.append(t.cpu().numpy())
+        assert np.array_equal(res[0], res[1])
+        ref = shard.astype(np.float64)
+        for r in range(R):                                  # requester order
+            acc = {}
+            for i in range(n):
+                if ids[r][i] % R == o:
+                    acc.setdefault(ids[r][i] // R, []).append(grads[r][i].astype(np.float64))
+            for loc, rows_ in acc.items():
+                ref[loc] -= lr * np.sum(rows_, axis=0)
+        touched = np.unique(np.concatenate([ids[r][ids[r] % R == o] // R for r in range(R)]))
+        assert rel(res[0][touched], ref[touched].astype(np.float32)) <= 1e-5
+
+
+def test_route_plan_capacity_overflow_is_reported():
+    V, R, n = 1000, 2, 500
+    ids = np.arange(n, dtype=np.int64) * 2            # every id owned by shard 0
+    send = torch.empty((R, 100), dtype=torch.int64, device=DEV)
+    err = ops.ErrorSlot(DEV)
+    ops.RoutePlan(n, V, R, 100, 8, DEV).build(T(ids), send, 100, err=err)
+    assert err.read() == (9, 0)

@@ -86,3 +86,44 @@ def test_router_gloo_matches_oracle_routing(world):
         assert ok_g, f"rank {rank}: routed sparse update differs from the unsharded update"
     w = workloads.WORKLOADS["T"]
     assert sum(r[4] for r in res) == world * w.tokens_per_replica(world)
+
+
+def _slot_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1605_08695_b200.step import Router
+        rt = Router()
+        R, cap = world, 6
+        # requester r sends to owner o the distinct local ids it needs, padded with -1
+        need = [[np.unique(np.arange(o + r, 40, R) // R)[:cap] for o in range(R)]
+                for r in range(R)]
+        send = np.full((R, cap + 3), -7, np.int64)   # 3 trailing elements outside the slots
+        for o in range(R):
+            send[o, :cap] = -1
+            send[o, :need[rank][o].size] = need[rank][o]
+        recv = torch.empty((R, cap + 3), dtype=torch.int64)
+        rt.a2a(recv, torch.from_numpy(send))
+        ok = all(np.array_equal(recv.numpy()[src, :need[src][rank].size], need[src][rank])
+                 and np.all(recv.numpy()[src, need[src][rank].size:cap] == -1)
+                 for src in range(R))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fixed_capacity_slot_exchange_gloo():
+    """Router.a2a: region o of the send buffer lands in region `rank` of owner o's receive
+    buffer, in source-rank order (the R > 1 step's slot exchanges)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slot_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: True, 1: True}
