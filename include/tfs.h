@@ -153,7 +153,8 @@ int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int32_t num_sam
  * operand_dtype TFS_F32: fp32 products, fp32 accumulation (parity mode, max rel err 1e-5).
  * operand_dtype TFS_BF16: h, w_true, w_s rounded to bf16 (RNE) and G rounded to bf16 before
  * the dh / dw_s / db_s reductions; tensor-core (tcgen05) GEMMs with fp32 accumulation; all
- * other math fp32 (R-18).  Requires dim % 64 == 0 for the tensor-core path.
+ * other math fp32 (R-18).  The tensor-core path requires dim % 64 == 0, lse != NULL and
+ * 16-byte aligned h, w_true, dh, dw_true, dw_s.
  * loss, lse, loss_sum may be NULL; the five gradient outputs are required.
  * vocab > 0 promises labels and sampled lie in [0, vocab) and lets the bf16 path find
  * accidental hits through a candidate map of 8 * vocab bytes at the START of the workspace

@@ -64,6 +64,7 @@ struct Carver {
 };
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__device__ __forceinline__ int64_t cdiv_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 inline cudaStream_t as_stream(void* s) { return (cudaStream_t)s; }
 

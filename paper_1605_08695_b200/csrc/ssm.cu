@@ -357,61 +357,71 @@ __global__ void to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
 }
 
 // db_s[j] = sum_t G[t, j] over the bf16 G [B x ldG]: block = 32 columns (4 x 16-byte chunks)
-// x 64 row groups; each thread sums its rows in order, then the 64 partials are added in
-// row-group order (fixed summation order, no atomics).
+// x 64 row groups; each thread sums its rows in order (8 loads in flight), then the 64 partials
+// are added in row-group order (fixed summation order, no atomics).  Also returns the candidate
+// map to all-zero (the GRAD pass was its last reader), and one extra block forms
+// loss_sum = c * sum_t loss_t (fixed-order tree) when loss_sum != nullptr.
 constexpr int kColsumChunks = 4, kColsumGroups = 64;
-// Also returns the candidate map to all-zero (the GRAD pass was its last reader).
 __global__ void __launch_bounds__(256) g_colsum_kernel(const uint16_t* G, int64_t B, int64_t S,
                                                        int64_t ldG, float* db_s,
                                                        const int64_t* sampled, int2* cmap,
-                                                       int64_t vocab) {
+                                                       int64_t vocab, const float* loss, float c,
+                                                       float* loss_sum) {
+  __shared__ float red[kColsumGroups][kColsumChunks * 8 + 1];
+  const int64_t ncol_blocks = cdiv_dev(S, kColsumChunks * 8);
+  if (blockIdx.x >= ncol_blocks) {  // the loss-sum block
+    float acc = 0.f;
+    for (int64_t t = threadIdx.x; t < B; t += 256) acc += loss[t];
+    float* r = &red[0][0];
+    r[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) r[threadIdx.x] += r[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) *loss_sum = c * r[0];
+    return;
+  }
   if (cmap != nullptr) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < S;
-         j += (int64_t)gridDim.x * blockDim.x) {
+         j += ncol_blocks * blockDim.x) {
       const int64_t k = sampled[j];
       if (k >= 0 && k < vocab) cmap[k] = make_int2(0, 0);
     }
   }
-  __shared__ float red[kColsumGroups][kColsumChunks * 8 + 1];
   const int chunk = threadIdx.x % kColsumChunks, rg = threadIdx.x / kColsumChunks;
   const int64_t c0 = (int64_t)blockIdx.x * (kColsumChunks * 8) + chunk * 8;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  auto add8 = [&](const uint4& x) {
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      acc[2 * k] += __uint_as_float(w[k] << 16);
+      acc[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
+    }
+  };
   if (c0 < S) {
+    constexpr int U = 8;
     const uint16_t* p = G + c0;
     int64_t r = rg;
-    for (; r + 3 * kColsumGroups < B; r += 4 * kColsumGroups) {
-      uint4 x[4];
+    for (; r + (U - 1) * kColsumGroups < B; r += U * kColsumGroups) {
+      uint4 x[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u)
         x[u] = __ldg(reinterpret_cast<const uint4*>(p + (r + u * kColsumGroups) * ldG));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          acc[2 * k] += __uint_as_float(w[k] << 16);
-          acc[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
-        }
-      }
+      for (int u = 0; u < U; ++u) add8(x[u]);
     }
-    for (; r < B; r += kColsumGroups) {
-      const uint4 x = __ldg(reinterpret_cast<const uint4*>(p + r * ldG));
-      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        acc[2 * k] += __uint_as_float(w[k] << 16);
-        acc[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
-      }
-    }
+    for (; r < B; r += kColsumGroups) add8(__ldg(reinterpret_cast<const uint4*>(p + r * ldG)));
   }
 #pragma unroll
   for (int k = 0; k < 8; ++k) red[rg][chunk * 8 + k] = acc[k];
   __syncthreads();
   if (threadIdx.x < kColsumChunks * 8) {
-    const int64_t c = (int64_t)blockIdx.x * (kColsumChunks * 8) + threadIdx.x;
-    float s = 0.f;
-    for (int g = 0; g < kColsumGroups; ++g) s += red[g][threadIdx.x];
-    if (c < S) db_s[c] = s;
+    const int64_t col = (int64_t)blockIdx.x * (kColsumChunks * 8) + threadIdx.x;
+    float sum = 0.f;
+    for (int g = 0; g < kColsumGroups; ++g) sum += red[g][threadIdx.x];
+    if (col < S) db_s[col] = sum;
   }
 }
 
@@ -482,26 +492,51 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
   if (t >= B) return;
   const float* ht = h + t * d;
   const float* wt = w_true + t * d;
+  // d % 64 == 0 on this path: 16-byte vectors, all of a lane's loads issued together
+  const float4* h4 = reinterpret_cast<const float4*>(ht);
+  const float4* w4 = reinterpret_cast<const float4*>(wt);
+  const int n4 = d >> 2;
   float part = 0.f;
-  for (int k = lane; k < d; k += 32) part = fmaf(bf16_round(ht[k]), bf16_round(wt[k]), part);
+  for (int k0 = lane; k0 < n4; k0 += 128) {
+    float4 a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 32 * u;
+      a[u] = k < n4 ? __ldg(h4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      b[u] = k < n4 ? __ldg(w4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      part = fmaf(bf16_round(a[u].x), bf16_round(b[u].x), part);
+      part = fmaf(bf16_round(a[u].y), bf16_round(b[u].y), part);
+      part = fmaf(bf16_round(a[u].z), bf16_round(b[u].z), part);
+      part = fmaf(bf16_round(a[u].w), bf16_round(b[u].w), part);
+    }
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   const float z = part + b_true[t] - (le_true ? le_true[t] : 0.f);
   const float z2 = z * umma::kLog2e;
   float m = z2;
-  for (int p = lane; p < nparts; p += 32) m = fmaxf(m, stats[(int64_t)p * B + t].x);
+  const float2* st_t = stats + t * nparts;  // this token's partials, contiguous
+  for (int p = lane; p < nparts; p += 32) m = fmaxf(m, st_t[p].x);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   float s = lane == 0 ? exp2f(z2 - m) : 0.f;
   for (int p = lane; p < nparts; p += 32) {
-    const float2 st = stats[(int64_t)p * B + t];
+    const float2 st = st_t[p];
     if (st.y > 0.f) s += st.y * exp2f(st.x - m);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   const float lse = (m + log2f(s)) * 0.6931471805599453f;
   const float g = c * (expf(z - lse) - 1.f);
-  for (int k = lane; k < d; k += 32) dw_true[t * d + k] = g * bf16_round(ht[k]);
+  float4* dw4 = reinterpret_cast<float4*>(dw_true + t * d);
+  for (int k = lane; k < n4; k += 32) {
+    const float4 a = __ldg(h4 + k);
+    dw4[k] = make_float4(g * bf16_round(a.x), g * bf16_round(a.y), g * bf16_round(a.z),
+                         g * bf16_round(a.w));
+  }
   if (lane == 0) {
     if (loss) loss[t] = lse - z;
     lse_out[t] = lse;
@@ -675,6 +710,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
   if (S > 0) {  // pass 1: per-row (max, sum 2^x) of each half tile, log2 domain
     ep.stats = w.stats;
+    ep.nparts = 2 * num_n;
     rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, ep, nullptr, 0, st);
     if (rc != TFS_OK) return rc;
   }
@@ -696,8 +732,8 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, ep, w.G, w.Sp, st);
   if (rc != TFS_OK) return rc;
   // db_s = column sums of G
-  g_colsum_kernel<<<(unsigned)cdiv(S, kColsumChunks * 8), 256, 0, st>>>(w.G, B, S, w.Sp, a->db_s,
-                                                                       a->sampled, cmap, V);
+  g_colsum_kernel<<<(unsigned)(cdiv(S, kColsumChunks * 8) + (a->loss_sum ? 1 : 0)), 256, 0, st>>>(
+      w.G, B, S, w.Sp, a->db_s, a->sampled, cmap, V, a->loss, a->grad_scale, a->loss_sum);
   launched();
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
   // (A = G K-major, B = W_s MN-major) in one persistent launch; split partials are reduced in
@@ -759,6 +795,7 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
   if (a->operand_dtype == TFS_BF16) {
     TFS_REQUIRE(a->dim % 64 == 0 && a->lse != nullptr);
     TFS_REQUIRE(((uintptr_t)a->h & 15) == 0 && ((uintptr_t)a->dh & 15) == 0);
+    TFS_REQUIRE(((uintptr_t)a->w_true & 15) == 0 && ((uintptr_t)a->dw_true & 15) == 0);
     TFS_REQUIRE(((uintptr_t)a->dw_s & 15) == 0 || a->S == 0);
   }
   TFS_SUPPORTED();
@@ -766,10 +803,11 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
     return TFS_ERR_WORKSPACE_TOO_SMALL;
   TFS_REQUIRE(((uintptr_t)ws & 255) == 0);
   cudaStream_t st = as_stream(stream);
+  TFS_REQUIRE(a->loss_sum == nullptr || a->loss != nullptr);
   int32_t rc = a->operand_dtype == TFS_BF16 ? ssm_bf16(a, ws, st) : ssm_f32(a, ws, st);
   if (rc != TFS_OK) return rc;
-  if (a->loss_sum) {
-    TFS_REQUIRE(a->loss != nullptr);
+  const bool fused_sum = a->operand_dtype == TFS_BF16 && a->S > 0;  // done by g_colsum_kernel
+  if (a->loss_sum && !fused_sum) {
     loss_sum_kernel<<<1, 256, 0, st>>>(a->loss, a->B, a->grad_scale, a->loss_sum); ::tfs::launched();
     TFS_LAUNCH_CHECK();
   }

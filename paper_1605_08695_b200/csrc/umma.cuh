@@ -88,7 +88,8 @@ struct EpiParams {
   const int2* cmap;
   int64_t vocab;
   int S_pad;
-  float2* stats;       // STATS: [(2*num_n) x M] (max, sum of 2^(v - max)) per half tile
+  float2* stats;       // STATS: [M x nparts] (max, sum of 2^(v - max)) per half tile
+  int nparts;          // 2 * number of n-tiles
   const float* lse;    // GRAD: natural-log lse per row
   float c;             // GRAD: gradient scale
 };
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(tempty + acc);  // the leader's barrier
       if (MODE == kStats && row_ok)
-        ep.stats[(int64_t)(t.nt * 2 + half) * M + row] = make_float2(run_m, run_s);
+        ep.stats[(int64_t)row * ep.nparts + t.nt * 2 + half] = make_float2(run_m, run_s);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
