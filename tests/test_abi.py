@@ -55,6 +55,7 @@ def test_built_for_sm100a_with_tensor_core_path(lib):
     assert "UTCHMMA" in sass          # tcgen05.mma
     assert "UTMALDG" in sass          # TMA tensor loads
     assert "LDTM" in sass             # tcgen05.ld (TMEM -> registers)
+    assert "UTMASTG" in sass          # TMA tensor stores (GEMM epilogues)
 
 
 def test_host_validation_without_gpu(lib):
