@@ -274,6 +274,29 @@ int32_t tfs_route_reduce(const void* plan, size_t plan_bytes, int64_t n, int64_t
                          const float* rows2, float* out_slots, int64_t out_stride,
                          float* out_slots2, int64_t out2_stride, void* ws, size_t ws_bytes,
                          void* stream);
+/* One-sided NVLink variants (R > 1 with peer-mapped memory, e.g. symmetric allocations): the
+ * payload goes straight into the owner's memory instead of a local send buffer.
+ * tfs_route_plan_push: as tfs_route_plan, but the send ids of owner o are stored at
+ * dst_tab[o] + dst_off (dst_tab: device array of R peer pointers to the owners' inboxes).
+ * tfs_route_reduce_push: as tfs_route_reduce, rows of owner o to out_tab[o] + out_off + s * dim
+ * (out_off % 4 == 0 when dim % 4 == 0), companions to out2_tab[o] + out2_off + s.
+ * tfs_gather_peers: out[t, :] = row (id div R) of shard (id mod R) read through shards[id mod R]
+ * (device array of R peer pointers to equally shaped shards of shard_rows rows): Part, both
+ * routes, the owner Gather and Stitch in one kernel (pull).  ids outside [0, vocab) ->
+ * TFS_ERR_OUT_OF_RANGE (-1: padding, row unwritten).  The caller orders these with device
+ * barriers across the GPUs (tables stable during pulls, inboxes complete before use). */
+int32_t tfs_route_plan_push(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
+                            int64_t cap, void* plan, size_t plan_bytes, int64_t* const* dst_tab,
+                            int64_t dst_off, int64_t* out_counts, tfs_device_error* err,
+                            void* stream);
+int32_t tfs_route_reduce_push(const void* plan, size_t plan_bytes, int64_t n, int64_t vocab,
+                              int32_t num_shards, int64_t cap, const float* rows, int32_t dim,
+                              const float* rows2, float* const* out_tab, int64_t out_off,
+                              float* const* out2_tab, int64_t out2_off, void* ws,
+                              size_t ws_bytes, void* stream);
+int32_t tfs_gather_peers(const float* const* shards, int64_t shard_rows, int32_t dim,
+                         const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
+                         float* out, tfs_device_error* err, void* stream);
 /* Owner side.  tfs_gather_slots: for each slot (o, s) of num_slots regions x cap, the row of id
  * ids[o * ids_stride + s] of the local shard to out + o * out_stride + s * dim (fp32; -1 ids
  * are padding, rows left unwritten).  tfs_scatter_plan_slots / tfs_scatter_add_sgd_planned_slots:

@@ -88,6 +88,10 @@ _SIGNATURES = {
     "tfs_route_reduce_workspace_bytes": ([I64, I32], SZ),
     "tfs_route_reduce": ([P, SZ, I64, I64, I32, I64, P, I32, P, P, I64, P, I64, P, SZ, P], I32),
     "tfs_gather_slots": ([P, I64, I32, P, I64, I32, I64, P, I64, P, P], I32),
+    "tfs_route_plan_push": ([P, I64, I64, I32, I64, P, SZ, P, I64, P, P, P], I32),
+    "tfs_route_reduce_push": ([P, SZ, I64, I64, I32, I64, P, I32, P, P, I64, P, I64, P, SZ, P],
+                              I32),
+    "tfs_gather_peers": ([P, I64, I32, P, I64, I64, I32, P, P, P], I32),
     "tfs_scatter_plan_slots": ([P, I64, I32, I64, I64, I32, P, SZ, P, P], I32),
     "tfs_scatter_add_sgd_planned_slots": ([P, I64, I32, P, SZ, I32, I64, P, I64, F32, P, P, I64,
                                            P, SZ, P], I32),

@@ -327,6 +327,60 @@ extern "C" int32_t tfs_gather_slots(const float* table, int64_t rows, int32_t di
   return TFS_OK;
 }
 
+// One-sided routed Gather (R > 1 over NVLink): out[t] = row (id div R) of the shard of owner
+// id mod R, read through that owner's table pointer (peer memory).  Part, the id route, the
+// owner Gather, the row route and Stitch in one kernel.
+template <bool VEC>
+__global__ void __launch_bounds__(256) gather_peers_kernel(const float* const* __restrict__ shards,
+                                                           int64_t shard_rows, int32_t dim,
+                                                           const int64_t* __restrict__ ids,
+                                                           int64_t n, int64_t vocab, int32_t R,
+                                                           float* __restrict__ out,
+                                                           tfs_device_error* err) {
+  const int cols = VEC ? dim >> 2 : dim;
+  const int64_t total = n * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / cols;
+    const int c = (int)(e - t * cols);
+    const int64_t id = __ldg(ids + t);
+    if (id < 0 || id >= vocab) {
+      if (c == 0 && id != -1) report_error(err, TFS_ERR_OUT_OF_RANGE, t);
+      continue;
+    }
+    const int64_t o = id % R, local = id / R;
+    if (local >= shard_rows) continue;
+    const float* src = shards[o] + local * dim;
+    if (VEC)
+      reinterpret_cast<float4*>(out + t * dim)[c] = reinterpret_cast<const float4*>(src)[c];
+    else
+      out[t * dim + c] = src[c];
+  }
+}
+
+extern "C" int32_t tfs_gather_peers(const float* const* shards, int64_t shard_rows, int32_t dim,
+                                    const int64_t* ids, int64_t n, int64_t vocab,
+                                    int32_t num_shards, float* out, tfs_device_error* err,
+                                    void* stream) {
+  TFS_REQUIRE(n >= 0 && dim >= 1 && shard_rows >= 0 && vocab >= 1 && num_shards >= 1);
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(shards && ids && out);
+  TFS_SUPPORTED();
+  cudaStream_t st = as_stream(stream);
+  const bool vec = dim % 4 == 0 && ((uintptr_t)out % 16 == 0);
+  const int64_t total = n * (vec ? dim / 4 : dim);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
+  if (vec)
+    gather_peers_kernel<true><<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab,
+                                                    num_shards, out, err);
+  else
+    gather_peers_kernel<false><<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab,
+                                                     num_shards, out, err);
+  ::tfs::launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
 extern "C" size_t tfs_stitch_workspace_bytes(int64_t n) {
   return (size_t)std::max<int64_t>(n, 1) * sizeof(unsigned long long) + 256;
 }

@@ -448,6 +448,9 @@ struct SegJob {
   const int64_t* slot_base;
   int64_t cap;
   int64_t out_stride, out2_stride;  // per-owner slot region strides of out_rows / out_rows2
+  float* const* out_tab;            // or per-owner region bases (+ out_off / out2_off)
+  float* const* out2_tab;
+  int64_t out_off, out2_off;
   // input rows in slot layout (row_cap > 0): row i = slot (i / row_cap, i % row_cap) at
   // rows + o * row_stride + s * dim (rows2 + o * row2_stride + s)
   int64_t row_cap, row_stride, row2_stride;
@@ -472,14 +475,21 @@ struct D4 {
 // Where segment u's results go in write mode: float offset of its row in out_rows, offset in
 // out_rows2, index in out_local.  row < 0: dropped (slot capacity exceeded).
 struct OutPos {
-  int64_t row, r2, local;
+  float* row;     // nullptr: dropped
+  float* r2;      // nullptr when there is no companion stream
+  int64_t local;  // index into out_local
 };
 __device__ __forceinline__ OutPos seg_out_pos(const SegJob& j, int64_t u, uint32_t key) {
-  if (j.slot_base == nullptr) return OutPos{u * j.dim, u, u};
+  if (j.slot_base == nullptr)
+    return OutPos{j.out_rows + u * j.dim, j.out_rows2 ? j.out_rows2 + u : nullptr, u};
   const int64_t o = key / (uint32_t)j.nloc;
   const int64_t s = u - j.slot_base[o];
-  if (s >= j.cap) return OutPos{-1, -1, -1};
-  return OutPos{o * j.out_stride + s * j.dim, o * j.out2_stride + s, -1};
+  if (s >= j.cap) return OutPos{nullptr, nullptr, -1};
+  if (j.out_tab != nullptr)  // owner o's inbox, written over NVLink
+    return OutPos{j.out_tab[o] + j.out_off + s * j.dim,
+                  j.out2_tab ? j.out2_tab[o] + j.out2_off + s : nullptr, -1};
+  return OutPos{j.out_rows + o * j.out_stride + s * j.dim,
+                j.out_rows2 ? j.out_rows2 + o * j.out2_stride + s : nullptr, -1};
 }
 // Float offset of input row i (and of its rows2 value).
 __device__ __forceinline__ int64_t row_off(const SegJob& j, uint32_t i) {
@@ -588,11 +598,11 @@ __global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j, int nslic
     if (!starts_before && !ends_after) {  // whole segment: apply / write now
       if (write_mode) {
         const OutPos op = seg_out_pos(j, sg, kr);
-        if (op.row >= 0) {
-          if (col_ok) reinterpret_cast<float4*>(j.out_rows + op.row)[c4] = to_f4(acc);
+        if (op.row != nullptr) {
+          if (col_ok) reinterpret_cast<float4*>(op.row)[c4] = to_f4(acc);
           if (lane == 0 && slice == 0) {
             if (j.out_local) j.out_local[op.local] = (int64_t)(kr % (uint32_t)j.nloc);
-            if (j.rows2) j.out_rows2[op.r2] = (float)acc2;
+            if (op.r2) *op.r2 = (float)acc2;
           }
         }
       } else {
@@ -638,10 +648,10 @@ __global__ void __launch_bounds__(256) seg_cross_vec4_kernel(SegJob j) {
 #pragma unroll 16
     for (int64_t ch = c0 + 1; ch <= c1; ++ch)
       add4(acc, reinterpret_cast<const D4*>(j.part + (2 * ch) * j.dim)[c]);
-    const OutPos op = write_mode ? seg_out_pos(j, s, key) : OutPos{0, 0, 0};
-    if (op.row < 0) continue;
+    const OutPos op = write_mode ? seg_out_pos(j, s, key) : OutPos{j.table, nullptr, 0};
+    if (op.row == nullptr) continue;
     if (write_mode) {
-      reinterpret_cast<float4*>(j.out_rows + op.row)[c] = to_f4(acc);
+      reinterpret_cast<float4*>(op.row)[c] = to_f4(acc);
     } else {
       float4* tp = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c;
       float4 w = *tp;
@@ -657,8 +667,9 @@ __global__ void __launch_bounds__(256) seg_cross_vec4_kernel(SegJob j) {
       if (j.rows2) {
         double acc2 = j.part2[2 * c0 + 1];
         for (int64_t ch = c0 + 1; ch <= c1; ++ch) acc2 += j.part2[2 * ch];
-        if (write_mode)
-          j.out_rows2[op.r2] = (float)acc2;
+        if (write_mode) {
+          if (op.r2) *op.r2 = (float)acc2;
+        }
         else if (j.table2)
           j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * acc2);
       }
@@ -699,11 +710,11 @@ __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
                                      chunk);
       if (dst.kind == 0) {
         const OutPos op = write_mode ? seg_out_pos(j, cur, cur_key)
-                                     : OutPos{(int64_t)cur * j.dim, (int64_t)cur, (int64_t)cur};
-        if (op.row < 0) return;
-        float* o = write_mode ? j.out_rows : j.sums;
-        if (c < j.dim) o[op.row + c] = (float)acc;
-        if (j.rows2 && lane == 0 && c0 == 0) (write_mode ? j.out_rows2 : j.sums2)[op.r2] = (float)acc2;
+                                     : OutPos{j.sums + (int64_t)cur * j.dim,
+                                              j.sums2 + cur, (int64_t)cur};
+        if (op.row == nullptr) return;
+        if (c < j.dim) op.row[c] = (float)acc;
+        if (j.rows2 && op.r2 && lane == 0 && c0 == 0) *op.r2 = (float)acc2;
       } else {
         if (c < j.dim) j.part[dst.slot * j.dim + c] = acc;
         if (j.rows2 && lane == 0 && c0 == 0) j.part2[dst.slot] = acc2;
@@ -746,8 +757,8 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
     const uint32_t a = j.seg_start[u], b = j.seg_start[u + 1];
     const uint32_t key = j.keys[a];
     if (key >= j.invalid_key) continue;
-    const OutPos op = write_mode ? seg_out_pos(j, u, key) : OutPos{u * j.dim, u, u};
-    if (op.row < 0) continue;
+    const OutPos op = write_mode ? seg_out_pos(j, u, key) : OutPos{j.table, nullptr, u};
+    if (op.row == nullptr) continue;
     if (write_mode && c == 0 && j.out_local) j.out_local[op.local] = (int64_t)(key % (uint32_t)j.nloc);
     const int64_t c0 = a / kChunk, c1 = (b - 1) / kChunk;
     const bool cross = c0 != c1;
@@ -764,7 +775,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
         acc = D4{s.x, s.y, s.z, s.w};
       }
       if (write_mode) {
-        reinterpret_cast<float4*>(j.out_rows + op.row)[c] = to_f4(acc);
+        reinterpret_cast<float4*>(op.row)[c] = to_f4(acc);
       } else {
         float4* t = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c;
         float4 w = *t;
@@ -785,7 +796,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
         acc = j.sums[u * j.dim + c];
       }
       if (write_mode) {
-        j.out_rows[op.row + c] = (float)acc;
+        op.row[c] = (float)acc;
       } else {
         float* t = j.table + (int64_t)key * j.dim + c;
         *t = (float)((double)*t - (double)j.lr * acc);
@@ -800,7 +811,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
         acc2 = write_mode ? 0.0 : j.sums2[u];
       }
       if (write_mode) {
-        j.out_rows2[op.r2] = (float)acc2;
+        if (op.r2) *op.r2 = (float)acc2;
       } else if (j.table2) {
         j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * acc2);
       }
@@ -1100,8 +1111,11 @@ static void bind(SegJob& j, const SegScratch& s, int64_t n) {
 static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
   const int64_t nchunks = cdiv(n, kChunk);
   const int grid = (int)std::max<int64_t>(1, cdiv(nchunks, 8));
+  // (inbox regions of out_tab are 16-byte aligned by construction: aligned bases, out_off % 4 == 0)
   const bool vec = (j.dim & 3) == 0 && ((uintptr_t)j.rows & 15) == 0 &&
-                   (j.table ? ((uintptr_t)j.table & 15) == 0 : ((uintptr_t)j.out_rows & 15) == 0);
+                   (j.row_cap == 0 || j.row_stride % 4 == 0) &&
+                   (j.table ? ((uintptr_t)j.table & 15) == 0
+                            : (j.out_tab != nullptr || ((uintptr_t)j.out_rows & 15) == 0));
   if (vec) {
     TFS_CUDA_TRY(cudaMemsetAsync(j.cross_count, 0, sizeof(uint32_t), st));
     const int nslices = (int)cdiv(j.dim >> 2, 32);
@@ -1251,9 +1265,12 @@ __global__ void route_bases_kernel(const uint32_t* keys, const uint32_t* seg_sta
   }
 }
 
+// Send ids go to send_local + o * stride (this GPU) or, with a pointer table, straight into
+// owner o's inbox: dst_tab[o] + dst_off (one-sided NVLink stores).
 __global__ void route_fill_kernel(const uint32_t* keys, const uint32_t* seg_start,
                                   const int64_t* base, int32_t R, int64_t cap, int64_t nloc,
-                                  int64_t* send_local, int64_t stride, int64_t* counts,
+                                  int64_t* send_local, int64_t stride,
+                                  int64_t* const* dst_tab, int64_t dst_off, int64_t* counts,
                                   tfs_device_error* err) {
   const int64_t total = (int64_t)R * cap;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -1265,8 +1282,8 @@ __global__ void route_fill_kernel(const uint32_t* keys, const uint32_t* seg_star
       if (c > cap) report_error(err, TFS_ERR_CAPACITY, o);
     }
     const int64_t u = base[o] + jx;
-    send_local[o * stride + jx] =
-        u < base[o + 1] ? (int64_t)(keys[seg_start[u]] % (uint32_t)nloc) : -1;
+    int64_t* dst = dst_tab ? dst_tab[o] + dst_off : send_local + o * stride;
+    dst[jx] = u < base[o + 1] ? (int64_t)(keys[seg_start[u]] % (uint32_t)nloc) : -1;
   }
 }
 
@@ -1303,14 +1320,14 @@ extern "C" size_t tfs_route_plan_bytes(int64_t n, int32_t num_shards) {
   return route_plan_bytes(n, num_shards, nullptr, nullptr, nullptr, 0);
 }
 
-extern "C" int32_t tfs_route_plan(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
-                                  int64_t cap, void* plan, size_t plan_bytes,
-                                  int64_t* out_send_local, int64_t send_stride,
-                                  int64_t* out_counts, tfs_device_error* err, void* stream) {
+static int32_t route_plan_impl(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
+                               int64_t cap, void* plan, size_t plan_bytes, int64_t* out_send_local,
+                               int64_t send_stride, int64_t* const* dst_tab, int64_t dst_off,
+                               int64_t* out_counts, tfs_device_error* err, void* stream) {
   TFS_REQUIRE(n >= 1 && vocab >= 1 && num_shards >= 1 && num_shards <= 1024 && cap >= 1);
-  TFS_REQUIRE(send_stride >= cap);
+  TFS_REQUIRE(dst_tab != nullptr || send_stride >= cap);
   TFS_REQUIRE(n < (1ll << 31) && vocab + num_shards < (1ll << 32) - 1);
-  TFS_REQUIRE(ids && plan && out_send_local);
+  TFS_REQUIRE(ids && plan && (out_send_local || dst_tab));
   TFS_SUPPORTED();
   SegScratch s;
   int64_t* base;
@@ -1328,10 +1345,29 @@ extern "C" int32_t tfs_route_plan(const int64_t* ids, int64_t n, int64_t vocab, 
   const int64_t total = (int64_t)num_shards * cap;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 4ll * num_sms()));
   route_fill_kernel<<<grid, 256, 0, st>>>(s.k1, s.seg_start, base, num_shards, cap, nloc,
-                                          out_send_local, send_stride, out_counts, err);
+                                          out_send_local, send_stride, dst_tab, dst_off,
+                                          out_counts, err);
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
+}
+
+extern "C" int32_t tfs_route_plan(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
+                                  int64_t cap, void* plan, size_t plan_bytes,
+                                  int64_t* out_send_local, int64_t send_stride,
+                                  int64_t* out_counts, tfs_device_error* err, void* stream) {
+  return route_plan_impl(ids, n, vocab, num_shards, cap, plan, plan_bytes, out_send_local,
+                         send_stride, nullptr, 0, out_counts, err, stream);
+}
+
+extern "C" int32_t tfs_route_plan_push(const int64_t* ids, int64_t n, int64_t vocab,
+                                       int32_t num_shards, int64_t cap, void* plan,
+                                       size_t plan_bytes, int64_t* const* dst_tab,
+                                       int64_t dst_off, int64_t* out_counts,
+                                       tfs_device_error* err, void* stream) {
+  TFS_REQUIRE(dst_tab != nullptr && dst_off >= 0);
+  return route_plan_impl(ids, n, vocab, num_shards, cap, plan, plan_bytes, nullptr, 0, dst_tab,
+                         dst_off, out_counts, err, stream);
 }
 
 extern "C" int32_t tfs_route_unpack(const void* plan, size_t plan_bytes, int64_t n, int64_t vocab,
@@ -1454,6 +1490,40 @@ __global__ void merge_runs_kernel(IdsView ids, int32_t R, int64_t cap, int64_t l
     keys_out[pos] = k == 0xFFFFFFFFu ? (uint32_t)limit : k;
     perm_out[pos] = (uint32_t)i;
   }
+}
+
+extern "C" int32_t tfs_route_reduce_push(const void* plan, size_t plan_bytes, int64_t n,
+                                         int64_t vocab, int32_t num_shards, int64_t cap,
+                                         const float* rows, int32_t dim, const float* rows2,
+                                         float* const* out_tab, int64_t out_off,
+                                         float* const* out2_tab, int64_t out2_off, void* ws,
+                                         size_t ws_bytes, void* stream) {
+  TFS_REQUIRE(n >= 1 && vocab >= 1 && num_shards >= 1 && num_shards <= 1024 && cap >= 1 &&
+              dim >= 1 && out_off >= 0 && out2_off >= 0);
+  TFS_REQUIRE(plan && rows && out_tab);
+  TFS_REQUIRE((rows2 == nullptr) == (out2_tab == nullptr));
+  TFS_REQUIRE(dim % 4 != 0 || out_off % 4 == 0);
+  TFS_SUPPORTED();
+  SegScratch s;
+  int64_t* base;
+  if (plan_bytes < route_plan_bytes(n, num_shards, &s, &base, const_cast<void*>(plan), plan_bytes))
+    return TFS_ERR_WORKSPACE_TOO_SMALL;
+  if (ws_bytes < apply_scratch_bytes(n, dim, &s, ws, ws_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+  const int64_t nloc = cdiv(vocab, num_shards);
+  SegJob j{};
+  bind(j, s, n);
+  j.rows = rows;
+  j.rows2 = rows2;
+  j.dim = dim;
+  j.invalid_key = (uint32_t)(num_shards * nloc);
+  j.nloc = nloc;
+  j.slot_base = base;
+  j.cap = cap;
+  j.out_tab = out_tab;
+  j.out2_tab = out2_tab;
+  j.out_off = out_off;
+  j.out2_off = out2_off;
+  return run_segments(j, n, as_stream(stream));
 }
 
 // ---- planned ScatterAdd-SGD over ids / gradients received in slot layout (R x cap) ----------

@@ -254,6 +254,25 @@ class RoutePlan:
               "tfs_route_plan")
         return self
 
+    def build_push(self, ids, dst_tab, dst_off: int, counts=None, err: ErrorSlot = None):
+        """Plan + send ids stored straight into the owners' inboxes (dst_tab: int64 tensor of R
+        peer pointers) at element offset dst_off."""
+        assert ids.numel() == self.n
+        check(_lib.lib().tfs_route_plan_push(_p(ids), self.n, self.vocab, self.R, self.cap,
+                                             _p(self.plan), self.plan.numel(), _p(dst_tab),
+                                             int(dst_off), _p(counts), _err(err), _stream()),
+              "tfs_route_plan_push")
+        return self
+
+    def reduce_push(self, rows, dim: int, out_tab, out_off: int, rows2=None, out2_tab=None,
+                    out2_off: int = 0):
+        check(_lib.lib().tfs_route_reduce_push(_p(self.plan), self.plan.numel(), self.n,
+                                               self.vocab, self.R, self.cap, _p(rows), int(dim),
+                                               _p(rows2), _p(out_tab), int(out_off),
+                                               _p(out2_tab), int(out2_off), _p(self.ws),
+                                               self.ws.numel(), _stream()),
+              "tfs_route_reduce_push")
+
     def unpack(self, slots, slots_stride: int, dim: int, out):
         check(_lib.lib().tfs_route_unpack(_p(self.plan), self.plan.numel(), self.n, self.vocab,
                                           self.R, self.cap, _p(slots), int(slots_stride),
@@ -268,6 +287,15 @@ class RoutePlan:
                                           _p(self.ws), self.ws.numel(), _stream()),
               "tfs_route_reduce")
         return out
+
+
+def gather_peers(shard_tab, shard_rows: int, dim: int, ids, vocab: int, R: int, out,
+                 err: ErrorSlot = None):
+    """One-sided routed Gather: out[t] = row id//R of shard id%R through peer pointers."""
+    check(_lib.lib().tfs_gather_peers(_p(shard_tab), int(shard_rows), int(dim), _p(ids),
+                                      ids.numel(), int(vocab), int(R), _p(out), _err(err),
+                                      _stream()), "tfs_gather_peers")
+    return out
 
 
 def gather_slots(table, ids, ids_stride: int, num_slots: int, cap: int, out, out_stride: int,

@@ -49,6 +49,10 @@ class StepConfig:
     # An overflow is reported as TFS_ERR_CAPACITY (never silent).
     route_slack: float = 1.25
     route_pad: int = 64
+    # R > 1 transport: "p2p" = one-sided NVLink (peer loads of the owners' rows, id / gradient
+    # stores into the owners' inboxes, device barriers; tables and inboxes in symmetric memory)
+    # or "nccl" = equal-split all-to-alls of slot regions.
+    route: str = "p2p"
 
 
 class Router:
@@ -63,6 +67,7 @@ class Router:
         self.group = group
         self.R = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.group_name = (group if group is not None else dist.group.WORLD).group_name
 
     def exchange_counts(self, send_counts: torch.Tensor):
         """send_counts int64 [R, k]: row o = counts of k payload kinds destined to rank o.
@@ -169,12 +174,41 @@ class ShardedStep:
             #   ids   int64 [R, cap_e + cap_w]          E ids | W ids
             #   rows  f32   [R, rstride]                 E rows | W rows | b   (rows of d)
             #   grads f32   [R, rstride]                 dE rows | dW rows | db
+            if cfg.route not in ("p2p", "nccl"):
+                raise ValueError(f"unknown route transport {cfg.route!r}")
+            if cfg.route == "p2p":
+                self._symm_tables()
+
             def cap_for(n):
                 return int(min(n, -(-cfg.route_slack * n // R) + cfg.route_pad))
             self.set_route_caps(cap_for(B), cap_for(B + S))
-            self.ev = {k: torch.cuda.Event() for k in ("route_e", "ids", "own")}
+            self.ev = {k: torch.cuda.Event() for k in ("route_e", "ids", "own", "h", "q")}
         self.graph = None
         self.phase_events = None  # list of (phase, start, end) when instrumented
+
+    def _symm(self, shape, dtype):
+        """A symmetric-memory tensor of this shape on every rank and the int64 tensor of the R
+        peer base pointers (device); the handle also provides the device barriers."""
+        import torch.distributed._symmetric_memory as symm_mem
+        t = symm_mem.empty(shape, dtype=dtype, device=self.device)
+        h = symm_mem.rendezvous(t, self.router.group_name)
+        ptrs = torch.tensor(list(h.buffer_ptrs), dtype=torch.int64, device=self.device)
+        return t, h, ptrs
+
+    def _symm_tables(self):
+        """Move this rank's shards of E, W, b into symmetric memory (equal shapes on every rank:
+        ceil(V / R) rows) so that peers can read them over NVLink."""
+        V, R, d = self.cfg.vocab, self.R, self.d
+        rows = -(-V // R)
+        self.shard_rows = rows
+        for name in ("E", "W", "b"):
+            src = getattr(self, name)
+            shape = (rows, d) if src.dim() == 2 else (rows,)
+            t, h, ptrs = self._symm(shape, src.dtype)
+            t[:src.shape[0]].copy_(src)
+            setattr(self, name, t[:src.shape[0]])
+            setattr(self, "tab_" + name, ptrs)
+            setattr(self, "hdl_" + name, h)
 
     def set_route_caps(self, cap_e: int, cap_w: int):
         """(Re)allocate the R > 1 slot buffers for cap_e / cap_w distinct ids per owner."""
@@ -186,12 +220,17 @@ class ShardedStep:
         self.istride = ce + cw
         self.off_w, self.off_b = ce * d, (ce + cw) * d
         self.rstride = -(-((ce + cw) * d + cw) // 4) * 4  # 16-byte aligned regions
-        self.send_ids = torch.empty((R, self.istride), **i64)
-        self.recv_ids = torch.empty((R, self.istride), **i64)
-        self.send_rows = torch.empty((R, self.rstride), **f32)
-        self.recv_rows = torch.empty((R, self.rstride), **f32)
-        self.send_grads = torch.empty((R, self.rstride), **f32)
-        self.recv_grads = torch.empty((R, self.rstride), **f32)
+        if self.cfg.route == "p2p":
+            # inboxes: region r of owner o's inbox is written by requester r over NVLink
+            self.recv_ids, self.hdl_ids, self.tab_ids = self._symm((R, self.istride), torch.int64)
+            self.recv_grads, _, self.tab_grads = self._symm((R, self.rstride), torch.float32)
+        else:
+            self.send_ids = torch.empty((R, self.istride), **i64)
+            self.recv_ids = torch.empty((R, self.istride), **i64)
+            self.send_rows = torch.empty((R, self.rstride), **f32)
+            self.recv_rows = torch.empty((R, self.rstride), **f32)
+            self.send_grads = torch.empty((R, self.rstride), **f32)
+            self.recv_grads = torch.empty((R, self.rstride), **f32)
         self.route_e = ops.RoutePlan(B, V, R, ce, d, dev)
         self.route_w = ops.RoutePlan(B + S, V, R, cw, d, dev)
         self.own_e = ops.SlotScatterPlan(R, ce, self.E.shape[0], d, dev)
@@ -294,7 +333,61 @@ class ShardedStep:
             self.plan_e.apply(self.E, self.ssm_out["dh"], self.cfg.lr)
             self.plan_w.apply(self.W, self.dw, self.cfg.lr, table2=self.b, grad2=self.db)
 
+    def _dist_step_p2p(self, step: int | None):
+        """R > 1 over NVLink, one-sided: three device barriers, no collectives, no host sync.
+
+        B0 (start): every owner finished the previous update, so its table is stable and its
+        inbox free.  The requester pulls its h / W / b rows straight from the owners' tables
+        (tfs_gather_peers) and stores its distinct ids into the owners' inboxes (route plan,
+        push).  B1: all ids have arrived; each owner builds the plan of its inbox (merge of R
+        ascending runs) on the side stream while the softmax runs.  The requester stores its
+        per-id gradient sums into the same inbox slots (reduce, push).  B2: all gradients have
+        arrived; each owner applies its planned ScatterAdd-SGD."""
+        V, B, R, d = self.cfg.vocab, self.B, self.R, self.d
+        ev, rank = self.ev, self.rank
+        main, side = torch.cuda.current_stream(), self.side_stream
+        self.hdl_ids.barrier(channel=0)                             # B0
+        side.wait_stream(main)
+        io = rank * self.istride
+        with torch.cuda.stream(side):                               # E path
+            self.route_e.build_push(self.x, self.tab_ids, io, counts=self.counts[0],
+                                    err=self.err)
+            ops.gather_peers(self.tab_E, self.shard_rows, d, self.x, V, R, self.h, err=self.err)
+            ev["h"].record(side)
+        self.qw[:B].copy_(self.y)                                   # W path
+        self._sample(step)
+        self.route_w.build_push(self.qw, self.tab_ids, io + self.cap_e, counts=self.counts[1],
+                                err=self.err)
+        ev["q"].record(main)
+        with torch.cuda.stream(side):                               # owner plans
+            side.wait_event(ev["q"])
+            self.hdl_ids.barrier(channel=1)                         # B1
+            self.own_e.build(self.recv_ids, self.istride, err=self.err)
+            self.own_w.build(self.recv_ids[:, self.cap_e:], self.istride, err=self.err)
+            ev["own"].record(side)
+        ops.gather_peers(self.tab_W, self.shard_rows, d, self.qw, V, R, self.w_rows, err=self.err)
+        ops.gather_peers(self.tab_b, self.shard_rows, 1, self.qw, V, R, self.b_rows, err=self.err)
+        main.wait_event(ev["h"])
+        self._softmax()
+        ro = rank * self.rstride
+        self.route_e.reduce_push(self.ssm_out["dh"], d, self.tab_grads, ro)
+        self.route_w.reduce_push(self.dw, d, self.tab_grads, ro + self.off_w, rows2=self.db,
+                                 out2_tab=self.tab_grads, out2_off=ro + self.off_b)
+        self.hdl_ids.barrier(channel=2)                             # B2
+        main.wait_event(ev["own"])
+        gr, rs = self.recv_grads, self.rstride
+        self.own_e.apply(self.E, gr, rs, self.cfg.lr)
+        self.own_w.apply(self.W, gr[:, self.off_w:], rs, self.cfg.lr, table2=self.b,
+                         grad2=gr[:, self.off_b:], grad2_stride=rs)
+        main.wait_stream(side)
+
     def _dist_step(self, step: int | None):
+        if self.cfg.route == "p2p":
+            self._dist_step_p2p(step)
+        else:
+            self._dist_step_nccl(step)
+
+    def _dist_step_nccl(self, step: int | None):
         """R > 1, host-synchronisation free (capturable): plans -> ids a2a -> owner Gather ->
         rows a2a -> Stitch -> softmax -> per-id gradient sums -> gradients a2a -> owner SGD.
 

@@ -23,7 +23,7 @@ def rel(g, o):
     return float(np.max(np.abs(g - o)) / max(np.max(np.abs(o)), 1e-300)) if o.size else 0.0
 
 
-def _worker(rank, world, port, name, dtype, q):
+def _worker(rank, world, port, name, dtype, route, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     import oracle  # noqa: F401
@@ -39,7 +39,8 @@ def _worker(rank, world, port, name, dtype, q):
         E, W, b = workloads.tables(V, w.dim)
         xs, ys = zip(*[workloads.batch(w, R, r) for r in range(R)])
         cfg = gstep.StepConfig(vocab=V, dim=w.dim, tokens=xs[0].size, num_sampled=w.num_sampled,
-                               lr=1.0, seed=workloads.SAMPLER_SEED, operand_dtype=dtype)
+                               lr=1.0, seed=workloads.SAMPLER_SEED, operand_dtype=dtype,
+                               route=route)
         st = gstep.ShardedStep(cfg, torch.from_numpy(E[rank::R].copy()).to(dev),
                                torch.from_numpy(W[rank::R].copy()).to(dev),
                                torch.from_numpy(b[rank::R].copy()).to(dev), gstep.Router())
@@ -65,13 +66,15 @@ def _worker(rank, world, port, name, dtype, q):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("route", ["p2p", "nccl"])
 @pytest.mark.parametrize("name,dtype,tol", [("T", 0, 1e-5), ("L", 1, 2e-3)])
-def test_dist_step_matches_oracle(name, dtype, tol):
+def test_dist_step_matches_oracle(name, dtype, tol, route):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, dtype, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, dtype, route, q))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(2)]
