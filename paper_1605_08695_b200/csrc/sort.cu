@@ -1526,6 +1526,62 @@ extern "C" int32_t tfs_route_reduce_push(const void* plan, size_t plan_bytes, in
   return run_segments(j, n, as_stream(stream));
 }
 
+// Same merge with every run staged in shared memory as 32-bit keys (R x cap x 4 bytes): the
+// R binary searches per entry then cost shared-memory latency instead of L2 latency.
+__device__ __forceinline__ int64_t smem_rank(const uint32_t* run, int64_t cap, uint32_t x,
+                                             bool inclusive) {
+  int64_t lo = 0, hi = cap;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const uint32_t k = run[mid];
+    if (inclusive ? k <= x : k < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__global__ void __launch_bounds__(512) merge_runs_smem_kernel(IdsView ids, int32_t R, int64_t cap,
+                                                              int64_t limit, uint32_t* keys_out,
+                                                              uint32_t* perm_out,
+                                                              tfs_device_error* err) {
+  extern __shared__ uint32_t runs[];  // [R][cap]
+  const int64_t n = (int64_t)R * cap;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t o = i / cap, s = i - o * cap;
+    runs[i] = run_key(ids, o, s, limit);
+  }
+  __syncthreads();
+  __shared__ int64_t valid_cnt[1024 + 1];  // R <= 1024: per-run valid counts, then the total
+  for (int q = threadIdx.x; q < R; q += blockDim.x)
+    valid_cnt[q] = smem_rank(runs + (int64_t)q * cap, cap, 0xFFFFFFFEu, true);
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i / cap, s = i - o * cap;
+    const uint32_t k = runs[i];
+    const int64_t id = ids.p[o * ids.stride + s];
+    if (id != -1 && k == 0xFFFFFFFFu) report_error(err, TFS_ERR_OUT_OF_RANGE, i);
+    if (s + 1 < cap && runs[i + 1] != 0xFFFFFFFFu && runs[i + 1] <= k)
+      report_error(err, TFS_ERR_INVALID_ARGUMENT, i);
+    int64_t pos;
+    if (k != 0xFFFFFFFFu) {
+      pos = s;
+      for (int64_t q = 0; q < R; ++q)
+        if (q != o) pos += smem_rank(runs + q * cap, cap, k, q < o);
+    } else {
+      int64_t valid = 0, before = 0;
+      for (int64_t q = 0; q < R; ++q) {
+        const int64_t c = valid_cnt[q];
+        valid += c;
+        if (q < o) before += cap - c;
+        else if (q == o) before += s - c;
+      }
+      pos = valid + before;
+    }
+    keys_out[pos] = k == 0xFFFFFFFFu ? (uint32_t)limit : k;
+    perm_out[pos] = (uint32_t)i;
+  }
+}
+constexpr size_t kMergeSmemMax = 200 * 1024;
+
 // ---- planned ScatterAdd-SGD over ids / gradients received in slot layout (R x cap) ----------
 extern "C" int32_t tfs_scatter_plan_slots(const int64_t* ids, int64_t ids_stride, int32_t R,
                                           int64_t cap, int64_t rows, int32_t sorted_runs,
@@ -1541,9 +1597,24 @@ extern "C" int32_t tfs_scatter_plan_slots(const int64_t* ids, int64_t ids_stride
   if (!sorted_runs)
     return sort_and_segment(IdsView{ids, cap, ids_stride}, n, rows, 1, rows + 1, 0,
                             (uint32_t)rows, s, err, st);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8ll * num_sms()));
-  merge_runs_kernel<<<grid, 256, 0, st>>>(IdsView{ids, cap, ids_stride}, R, cap, rows, s.k1, s.v1,
-                                          err);
+  const size_t smem = (size_t)n * sizeof(uint32_t);
+  if (smem <= kMergeSmemMax && R <= 1024) {
+    static bool attr = false;
+    if (!attr) {
+      TFS_CUDA_TRY(cudaFuncSetAttribute(merge_runs_smem_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kMergeSmemMax));
+      attr = true;
+    }
+    // every CTA stages all runs; few CTAs suffice (n ~ 1e4 entries)
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 512), num_sms()));
+    merge_runs_smem_kernel<<<grid, 512, smem, st>>>(IdsView{ids, cap, ids_stride}, R, cap, rows,
+                                                    s.k1, s.v1, err);
+  } else {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8ll * num_sms()));
+    merge_runs_kernel<<<grid, 256, 0, st>>>(IdsView{ids, cap, ids_stride}, R, cap, rows, s.k1,
+                                            s.v1, err);
+  }
   launched();
   const int ntiles = (int)cdiv(n, kSortTile);
   heads_count_kernel<<<ntiles, kSortThreads, 0, st>>>(s.k1, n, s.tile_cnt);

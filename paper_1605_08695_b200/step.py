@@ -182,7 +182,8 @@ class ShardedStep:
             def cap_for(n):
                 return int(min(n, -(-cfg.route_slack * n // R) + cfg.route_pad))
             self.set_route_caps(cap_for(B), cap_for(B + S))
-            self.ev = {k: torch.cuda.Event() for k in ("route_e", "ids", "own", "h", "q")}
+            self.ev = {k: torch.cuda.Event()
+                       for k in ("route_e", "ids", "own", "h", "q", "ssm", "red_e", "b2")}
         self.graph = None
         self.phase_events = None  # list of (phase, start, end) when instrumented
 
@@ -356,11 +357,11 @@ class ShardedStep:
             ev["h"].record(side)
         self.qw[:B].copy_(self.y)                                   # W path
         self._sample(step)
-        self.route_w.build_push(self.qw, self.tab_ids, io + self.cap_e, counts=self.counts[1],
-                                err=self.err)
         ev["q"].record(main)
-        with torch.cuda.stream(side):                               # owner plans
+        with torch.cuda.stream(side):     # W route plan + id push, then the owner plans
             side.wait_event(ev["q"])
+            self.route_w.build_push(self.qw, self.tab_ids, io + self.cap_e,
+                                    counts=self.counts[1], err=self.err)
             self.hdl_ids.barrier(channel=1)                         # B1
             self.own_e.build(self.recv_ids, self.istride, err=self.err)
             self.own_w.build(self.recv_ids[:, self.cap_e:], self.istride, err=self.err)
@@ -369,14 +370,22 @@ class ShardedStep:
         ops.gather_peers(self.tab_b, self.shard_rows, 1, self.qw, V, R, self.b_rows, err=self.err)
         main.wait_event(ev["h"])
         self._softmax()
+        ev["ssm"].record(main)
         ro = rank * self.rstride
-        self.route_e.reduce_push(self.ssm_out["dh"], d, self.tab_grads, ro)
+        with torch.cuda.stream(side):                               # E gradients, in parallel
+            side.wait_event(ev["ssm"])
+            self.route_e.reduce_push(self.ssm_out["dh"], d, self.tab_grads, ro)
+            ev["red_e"].record(side)
         self.route_w.reduce_push(self.dw, d, self.tab_grads, ro + self.off_w, rows2=self.db,
                                  out2_tab=self.tab_grads, out2_off=ro + self.off_b)
+        main.wait_event(ev["red_e"])
         self.hdl_ids.barrier(channel=2)                             # B2
-        main.wait_event(ev["own"])
+        ev["b2"].record(main)
         gr, rs = self.recv_grads, self.rstride
-        self.own_e.apply(self.E, gr, rs, self.cfg.lr)
+        with torch.cuda.stream(side):                               # E update, in parallel
+            side.wait_event(ev["b2"])
+            self.own_e.apply(self.E, gr, rs, self.cfg.lr)
+        main.wait_event(ev["own"])
         self.own_w.apply(self.W, gr[:, self.off_w:], rs, self.cfg.lr, table2=self.b,
                          grad2=gr[:, self.off_b:], grad2_stride=rs)
         main.wait_stream(side)

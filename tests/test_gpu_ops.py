@@ -371,7 +371,8 @@ def test_planned_scatter_matches_unplanned(n, dim, zipf):
     assert torch.equal(a, b) and torch.equal(ab, bb)
 
 
-@pytest.mark.parametrize("R,n,dim,cap", [(3, 700, 64, 400), (2, 2560, 512, 1500), (4, 999, 6, 300)])
+@pytest.mark.parametrize("R,n,dim,cap", [(3, 700, 64, 400), (2, 2560, 512, 1500), (4, 999, 6, 300),
+                                         (8, 600, 8, 7000)])  # last: merge beyond shared memory
 def test_fixed_capacity_route_round_trip(R, n, dim, cap):
     """tfs_route_plan / tfs_gather_slots / tfs_route_unpack / tfs_route_reduce /
     tfs_scatter_*_slots with R requesters simulated on one GPU (the all-to-all is a tensor
