@@ -27,6 +27,9 @@ constexpr int kSortItems = 4;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 1024 items per CTA
 constexpr int kMaxBuckets = 256;
 constexpr int kChunk = 8;  // sorted rows per warp in the segmented sums
+#ifndef TFS_SEG_MINB
+#define TFS_SEG_MINB 3  // 3 CTAs / SM (<= 85 registers): measured 24 -> 14 us on 10k Zipf rows
+#endif
 
 struct DigitSrc {
   int mode;
@@ -529,7 +532,7 @@ __device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_afte
 // inside the chunk -- are loaded at once; each segment's rows are added in sorted order in
 // fp64 and the segment is applied (T = fl32(T - lr * g)) or written directly.  Pieces of
 // segments that cross a chunk boundary go to partial slots and the segment to cross_list.
-__global__ void __launch_bounds__(256) seg_chunk_vec4_kernel(SegJob j, int nslices) {
+__global__ void __launch_bounds__(256, TFS_SEG_MINB) seg_chunk_vec4_kernel(SegJob j, int nslices) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t chunk = gw / nslices;
