@@ -161,7 +161,11 @@ int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int32_t num_sam
  * (tfs_ssm_workspace_bytes includes it): that region must be zero before the first call on a
  * workspace (e.g. zero-filled at allocation) and every call leaves it zero again.  vocab == 0:
  * no map, the hit test compares every (token, candidate) id pair (same result, slower). */
-enum { TFS_SUBTRACT_LOG_Q = 1u, TFS_REMOVE_ACCIDENTAL_HITS = 2u };
+/* TFS_BF16_OPERANDS (operand_dtype TFS_BF16 only): h, w_true and w_s point to bf16 arrays
+ * (uint16 bits, same shapes) that are already the RNE roundings of the fp32 values -- e.g.
+ * produced by tfs_gather with out_dtype TFS_BF16 -- so the call skips its conversion pass;
+ * results are identical to passing the fp32 arrays. */
+enum { TFS_SUBTRACT_LOG_Q = 1u, TFS_REMOVE_ACCIDENTAL_HITS = 2u, TFS_BF16_OPERANDS = 4u };
 typedef struct {
   int64_t B, S;
   int32_t dim;
@@ -282,7 +286,8 @@ int32_t tfs_route_reduce(const void* plan, size_t plan_bytes, int64_t n, int64_t
  * (out_off % 4 == 0 when dim % 4 == 0), companions to out2_tab[o] + out2_off + s.
  * tfs_gather_peers: out[t, :] = row (id div R) of shard (id mod R) read through shards[id mod R]
  * (device array of R peer pointers to equally shaped shards of shard_rows rows): Part, both
- * routes, the owner Gather and Stitch in one kernel (pull).  ids outside [0, vocab) ->
+ * routes, the owner Gather and Stitch in one kernel (pull); out_dtype TFS_F32 copies, TFS_BF16
+ * rounds to nearest even (as tfs_gather).  ids outside [0, vocab) ->
  * TFS_ERR_OUT_OF_RANGE (-1: padding, row unwritten).  The caller orders these with device
  * barriers across the GPUs (tables stable during pulls, inboxes complete before use). */
 int32_t tfs_route_plan_push(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
@@ -296,7 +301,7 @@ int32_t tfs_route_reduce_push(const void* plan, size_t plan_bytes, int64_t n, in
                               size_t ws_bytes, void* stream);
 int32_t tfs_gather_peers(const float* const* shards, int64_t shard_rows, int32_t dim,
                          const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
-                         float* out, tfs_device_error* err, void* stream);
+                         void* out, int32_t out_dtype, tfs_device_error* err, void* stream);
 /* Owner side.  tfs_gather_slots: for each slot (o, s) of num_slots regions x cap, the row of id
  * ids[o * ids_stride + s] of the local shard to out + o * out_stride + s * dim (fp32; -1 ids
  * are padding, rows left unwritten).  tfs_scatter_plan_slots / tfs_scatter_add_sgd_planned_slots:

@@ -22,6 +22,7 @@ TFS_ERR_CUDA = 5
 TFS_ERR_UNSUPPORTED = 7
 TFS_ERR_SAMPLER_EXHAUSTED = 8
 TFS_ERR_CAPACITY = 9
+TFS_BF16_OPERANDS = 4
 TFS_F32, TFS_BF16 = 0, 1
 TFS_SUBTRACT_LOG_Q, TFS_REMOVE_ACCIDENTAL_HITS = 1, 2
 
@@ -91,7 +92,7 @@ _SIGNATURES = {
     "tfs_route_plan_push": ([P, I64, I64, I32, I64, P, SZ, P, I64, P, P, P], I32),
     "tfs_route_reduce_push": ([P, SZ, I64, I64, I32, I64, P, I32, P, P, I64, P, I64, P, SZ, P],
                               I32),
-    "tfs_gather_peers": ([P, I64, I32, P, I64, I64, I32, P, P, P], I32),
+    "tfs_gather_peers": ([P, I64, I32, P, I64, I64, I32, P, I32, P, P], I32),
     "tfs_scatter_plan_slots": ([P, I64, I32, I64, I64, I32, P, SZ, P, P], I32),
     "tfs_scatter_add_sgd_planned_slots": ([P, I64, I32, P, SZ, I32, I64, P, I64, F32, P, P, I64,
                                            P, SZ, P], I32),

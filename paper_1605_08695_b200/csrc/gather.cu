@@ -330,12 +330,12 @@ extern "C" int32_t tfs_gather_slots(const float* table, int64_t rows, int32_t di
 // One-sided routed Gather (R > 1 over NVLink): out[t] = row (id div R) of the shard of owner
 // id mod R, read through that owner's table pointer (peer memory).  Part, the id route, the
 // owner Gather, the row route and Stitch in one kernel.
-template <bool VEC>
+template <bool VEC, bool BF16OUT>
 __global__ void __launch_bounds__(256) gather_peers_kernel(const float* const* __restrict__ shards,
                                                            int64_t shard_rows, int32_t dim,
                                                            const int64_t* __restrict__ ids,
                                                            int64_t n, int64_t vocab, int32_t R,
-                                                           float* __restrict__ out,
+                                                           void* __restrict__ out,
                                                            tfs_device_error* err) {
   const int cols = VEC ? dim >> 2 : dim;
   const int64_t total = n * cols;
@@ -351,31 +351,39 @@ __global__ void __launch_bounds__(256) gather_peers_kernel(const float* const* _
     const int64_t o = id % R, local = id / R;
     if (local >= shard_rows) continue;
     const float* src = shards[o] + local * dim;
-    if (VEC)
-      reinterpret_cast<float4*>(out + t * dim)[c] = reinterpret_cast<const float4*>(src)[c];
-    else
-      out[t * dim + c] = src[c];
+    if (VEC) {
+      const float4 v = reinterpret_cast<const float4*>(src)[c];
+      if (BF16OUT)
+        reinterpret_cast<uint2*>(out)[t * cols + c] =
+            make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+      else
+        reinterpret_cast<float4*>(out)[t * cols + c] = v;
+    } else {
+      if (BF16OUT)
+        reinterpret_cast<uint16_t*>(out)[t * dim + c] = f32_to_bf16_bits(src[c]);
+      else
+        reinterpret_cast<float*>(out)[t * dim + c] = src[c];
+    }
   }
 }
 
 extern "C" int32_t tfs_gather_peers(const float* const* shards, int64_t shard_rows, int32_t dim,
                                     const int64_t* ids, int64_t n, int64_t vocab,
-                                    int32_t num_shards, float* out, tfs_device_error* err,
-                                    void* stream) {
+                                    int32_t num_shards, void* out, int32_t out_dtype,
+                                    tfs_device_error* err, void* stream) {
   TFS_REQUIRE(n >= 0 && dim >= 1 && shard_rows >= 0 && vocab >= 1 && num_shards >= 1);
+  TFS_REQUIRE(out_dtype == TFS_F32 || out_dtype == TFS_BF16);
   if (n == 0) return TFS_OK;
   TFS_REQUIRE(shards && ids && out);
   TFS_SUPPORTED();
   cudaStream_t st = as_stream(stream);
-  const bool vec = dim % 4 == 0 && ((uintptr_t)out % 16 == 0);
+  const bool bf = out_dtype == TFS_BF16;
+  const bool vec = dim % 4 == 0 && ((uintptr_t)out % (bf ? 8 : 16) == 0);
   const int64_t total = n * (vec ? dim / 4 : dim);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
-  if (vec)
-    gather_peers_kernel<true><<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab,
-                                                    num_shards, out, err);
-  else
-    gather_peers_kernel<false><<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab,
-                                                     num_shards, out, err);
+  auto k = vec ? (bf ? gather_peers_kernel<true, true> : gather_peers_kernel<true, false>)
+               : (bf ? gather_peers_kernel<false, true> : gather_peers_kernel<false, false>);
+  k<<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab, num_shards, out, err);
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;

@@ -180,6 +180,7 @@ int32_t launch_store(const Gemm* g, int count, cudaStream_t st) {
     p.g = g[i].g;
     p.wt = g[i].wt;
     p.ldw = g[i].ldw;
+    p.wt_bf16 = g[i].wt_bf16;
     P.total_units += p.units;
   }
   return launch_params<kStore>(P, st);
@@ -481,36 +482,47 @@ __global__ void __launch_bounds__(256) prep_kernel(const float* h, int64_t nh4, 
   }
 }
 
+// Four consecutive operand values as bf16-rounded floats: from fp32 (rounded here, RNE) or
+// from bf16 bits (TFS_BF16_OPERANDS).  Element index i4 counts groups of four.
+template <bool BIN>
+__device__ __forceinline__ float4 ld4_bf(const void* p, int64_t i4) {
+  if (BIN) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p) + i4);
+    return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                       __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
+  }
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p) + i4);
+  return make_float4(bf16_round(v.x), bf16_round(v.y), bf16_round(v.z), bf16_round(v.w));
+}
+
 // Warp per token: true logit on bf16-rounded operands, combine the per-half-tile (max, sum)
 // partials (log2 domain) in tile order, then loss / g / dW_true / db_true.
+template <bool BIN>
 __global__ void __launch_bounds__(256) bf16_combine_kernel(
-    int64_t B, int32_t d, const float* h, const float* w_true, const float* b_true,
+    int64_t B, int32_t d, const void* h, const void* w_true, const float* b_true,
     const float* le_true, const float2* stats, int nparts, float c, float* loss, float* lse_out,
     float* dw_true, float* db_true) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= B) return;
-  const float* ht = h + t * d;
-  const float* wt = w_true + t * d;
-  // d % 64 == 0 on this path: 16-byte vectors, all of a lane's loads issued together
-  const float4* h4 = reinterpret_cast<const float4*>(ht);
-  const float4* w4 = reinterpret_cast<const float4*>(wt);
+  // d % 64 == 0 on this path: vector loads, all of a lane's loads issued together
   const int n4 = d >> 2;
+  const int64_t r4 = t * n4;  // this token's first group of four
   float part = 0.f;
   for (int k0 = lane; k0 < n4; k0 += 128) {
     float4 a[4], b[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int k = k0 + 32 * u;
-      a[u] = k < n4 ? __ldg(h4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-      b[u] = k < n4 ? __ldg(w4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      a[u] = k < n4 ? ld4_bf<BIN>(h, r4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      b[u] = k < n4 ? ld4_bf<BIN>(w_true, r4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      part = fmaf(bf16_round(a[u].x), bf16_round(b[u].x), part);
-      part = fmaf(bf16_round(a[u].y), bf16_round(b[u].y), part);
-      part = fmaf(bf16_round(a[u].z), bf16_round(b[u].z), part);
-      part = fmaf(bf16_round(a[u].w), bf16_round(b[u].w), part);
+      part = fmaf(a[u].x, b[u].x, part);
+      part = fmaf(a[u].y, b[u].y, part);
+      part = fmaf(a[u].z, b[u].z, part);
+      part = fmaf(a[u].w, b[u].w, part);
     }
   }
 #pragma unroll
@@ -533,9 +545,8 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
   const float g = c * (expf(z - lse) - 1.f);
   float4* dw4 = reinterpret_cast<float4*>(dw_true + t * d);
   for (int k = lane; k < n4; k += 32) {
-    const float4 a = __ldg(h4 + k);
-    dw4[k] = make_float4(g * bf16_round(a.x), g * bf16_round(a.y), g * bf16_round(a.z),
-                         g * bf16_round(a.w));
+    const float4 a = ld4_bf<BIN>(h, r4 + k);
+    dw4[k] = make_float4(g * a.x, g * a.y, g * a.z, g * a.w);
   }
   if (lane == 0) {
     if (loss) loss[t] = lse - z;
@@ -544,15 +555,16 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
   }
 }
 
-// out = sum_s part[s] (split order) [+ g[row] * bf16(wt)] (float4 columns; N % 4 == 0).
+// out = sum_s part[s] (split order) [+ g[row] * bf16(wt)] (float4 columns; N % 4 == 0); wt is
+// fp32 (rounded here) or bf16 bits (BIN).
+template <bool BIN>
 __global__ void split_finalize_kernel(const float* part, int nsplit, int64_t M, int32_t N,
-                                      const float* g, const float* wt, float* out) {
+                                      const float* g, const void* wt, float* out) {
   const int n4 = N / 4;
   const int64_t total = M * n4;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = e / n4;
-    const int c = 4 * (int)(e - row * n4);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < nsplit; ++s) {
       const float4 x = reinterpret_cast<const float4*>(part)[s * total + e];
@@ -560,13 +572,13 @@ __global__ void split_finalize_kernel(const float* part, int nsplit, int64_t M, 
     }
     if (g != nullptr) {
       const float gr = g[row];
-      const float4 w = *reinterpret_cast<const float4*>(wt + row * N + c);
-      acc.x += gr * bf16_round(w.x);
-      acc.y += gr * bf16_round(w.y);
-      acc.z += gr * bf16_round(w.z);
-      acc.w += gr * bf16_round(w.w);
+      const float4 w = ld4_bf<BIN>(wt, e);
+      acc.x += gr * w.x;
+      acc.y += gr * w.y;
+      acc.z += gr * w.z;
+      acc.w += gr * w.w;
     }
-    *reinterpret_cast<float4*>(out + row * N + c) = acc;
+    reinterpret_cast<float4*>(out)[e] = acc;
   }
 }
 
@@ -687,14 +699,20 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
   const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
   const int num_n = (int)cdiv(S, umma::BN);
+  const bool bin = (a->flags & TFS_BF16_OPERANDS) != 0;  // h, w_true, w_s given in bf16
 
   // Operands in bf16 (row-major; every GEMM reads them K- or MN-major as it needs), column
   // parameters and the candidate map: one launch.
   const int64_t V = hits ? a->vocab : 0;
   int2* cmap = V > 0 ? reinterpret_cast<int2*>(ws) : nullptr;
-  prep_kernel<<<grid1d(((B + S) * d / 4 + w.Spad) / 4), 256, 0, st>>>(
-      a->h, B * d / 4, a->w_s, S * d / 4, w.hb, w.wsb, a->b_s, le_s, a->sampled, S, w.Spad, cmap,
-      V, w.cb, w.sid);
+  if (bin) {  // already rounded by the producer (e.g. a bf16 Gather): no conversion pass
+    w.hb = static_cast<uint16_t*>(const_cast<void*>(static_cast<const void*>(a->h)));
+    w.wsb = static_cast<uint16_t*>(const_cast<void*>(static_cast<const void*>(a->w_s)));
+  }
+  const int64_t nconv = bin ? 0 : (B + S) * d / 4;
+  prep_kernel<<<grid1d((nconv + w.Spad) / 4), 256, 0, st>>>(
+      a->h, bin ? 0 : B * d / 4, a->w_s, bin ? 0 : S * d / 4, w.hb, w.wsb, a->b_s, le_s,
+      a->sampled, S, w.Spad, cmap, V, w.cb, w.sid);
   launched();
   TFS_LAUNCH_CHECK();
 
@@ -714,14 +732,15 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, ep, nullptr, 0, st);
     if (rc != TFS_OK) return rc;
   }
-  bf16_combine_kernel<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(
-      B, d, a->h, a->w_true, a->b_true, le_t, w.stats, 2 * num_n, a->grad_scale, a->loss,
-      a->lse, a->dw_true, a->db_true);
+  auto combine = bin ? bf16_combine_kernel<true> : bf16_combine_kernel<false>;
+  combine<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(B, d, a->h, a->w_true, a->b_true, le_t, w.stats,
+                                                2 * num_n, a->grad_scale, a->loss, a->lse,
+                                                a->dw_true, a->db_true);
   launched();
   TFS_LAUNCH_CHECK();
   if (S == 0) {  // no candidates: dh = g * bf16(w_true)
-    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true,
-                                                             a->w_true, a->dh);
+    auto fin = bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
+    fin<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true, a->w_true, a->dh);
     launched();
     TFS_LAUNCH_CHECK();
     return TFS_OK;
@@ -741,22 +760,23 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   umma::Gemm g[2];
   const bool dws_split = w.ks_dws > 1, dh_split = w.ks_dh > 1;
   g[0] = umma::Gemm{Operand{w.G, w.Sp, true}, Operand{w.hb, w.ldh, true}, (int)S, d, (int)B,
-                    w.ks_dws, a->dw_s, d, w.part_dws, nullptr, nullptr, 0};
+                    w.ks_dws, a->dw_s, d, w.part_dws, nullptr, nullptr, 0, 0};
   g[1] = umma::Gemm{Operand{w.G, w.Sp, false}, Operand{w.wsb, d, true}, (int)B, d, (int)S,
                     w.ks_dh, a->dh, d, w.part_dh, dh_split ? nullptr : a->db_true,
-                    dh_split ? nullptr : a->w_true, d};
+                    dh_split ? nullptr : static_cast<const void*>(a->w_true), d, bin ? 1 : 0};
   // larger units first so the static round-robin schedule balances the SMs
   const int64_t u0 = cdiv(B, umma::BK) / w.ks_dws, u1 = cdiv(S, umma::BK) / w.ks_dh;
   if (u1 > u0) std::swap(g[0], g[1]);
   rc = umma::launch_store(g, 2, st);
   if (rc != TFS_OK) return rc;
   if (dh_split) {
-    split_finalize_kernel<<<grid1d(B * d / 4), 256, 0, st>>>(
-        w.part_dh, w.ks_dh, B, d, a->db_true, a->w_true, a->dh);
+    auto fin = bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
+    fin<<<grid1d(B * d / 4), 256, 0, st>>>(w.part_dh, w.ks_dh, B, d, a->db_true, a->w_true,
+                                           a->dh);
     launched();
   }
   if (dws_split) {
-    split_finalize_kernel<<<grid1d(S * d / 4), 256, 0, st>>>(
+    split_finalize_kernel<false><<<grid1d(S * d / 4), 256, 0, st>>>(
         w.part_dws, w.ks_dws, S, d, nullptr, nullptr, a->dw_s);
     launched();
   }
@@ -792,6 +812,7 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
   TFS_REQUIRE(a->h && a->labels && a->w_true && a->b_true && a->dh && a->dw_true && a->db_true);
   TFS_REQUIRE(!(a->flags & TFS_SUBTRACT_LOG_Q) || (a->log_ec_true && (a->S == 0 || a->log_ec_s)));
   TFS_REQUIRE(a->S == 0 || (a->sampled && a->w_s && a->b_s && a->dw_s && a->db_s));
+  TFS_REQUIRE(!(a->flags & TFS_BF16_OPERANDS) || a->operand_dtype == TFS_BF16);
   if (a->operand_dtype == TFS_BF16) {
     TFS_REQUIRE(a->dim % 64 == 0 && a->lse != nullptr);
     TFS_REQUIRE(((uintptr_t)a->h & 15) == 0 && ((uintptr_t)a->dh & 15) == 0);
@@ -835,10 +856,10 @@ extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn,
   Carver c(ws, ws_bytes);
   float* part = c.take<float>(umma::part_floats(M, N, ks));
   umma::Gemm g{umma::Operand{A, lda, a_mn != 0}, umma::Operand{B, ldb, b_mn != 0}, M, N, K, ks,
-               C, N, part, nullptr, nullptr, 0};
+               C, N, part, nullptr, nullptr, 0, 0};
   int32_t rc = umma::launch_store(&g, 1, st);
   if (rc != TFS_OK || ks == 1) return rc;
-  split_finalize_kernel<<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, nullptr,
+  split_finalize_kernel<false><<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, nullptr,
                                                                     nullptr, C);
   launched();
   TFS_LAUNCH_CHECK();

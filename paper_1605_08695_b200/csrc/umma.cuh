@@ -105,8 +105,9 @@ struct Problem {
   int num_m, num_n, ksplit, kb_per_split, kb_total, units;
   int a_mn, b_mn;
   const float* g;   // optional row scale of the extra term (ksplit == 1 only)
-  const float* wt;  // optional [M x ldw] fp32 matrix of the extra term (bf16-rounded)
-  int64_t ldw;
+  const void* wt;   // optional [M x ldw] matrix of the extra term: fp32 (bf16-rounded here)
+  int64_t ldw;      //   or bf16 bits (wt_bf16)
+  int wt_bf16;
 };
 
 struct Params {
@@ -595,11 +596,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         } else {
           if (q.g != nullptr && row_ok) {
             const float gr = q.g[row];
-            const float* w = q.wt + (int64_t)row * q.ldw + col0;
+            const int64_t w0 = (int64_t)row * q.ldw + col0;
             const int N = q.N;
+            if (q.wt_bf16) {
+              const uint16_t* w = static_cast<const uint16_t*>(q.wt) + w0;
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < N) v[i] += gr * bf16_round(w[i]);
+              for (int i = 0; i < 32; ++i)
+                if (col0 + i < N) v[i] += gr * __uint_as_float((uint32_t)w[i] << 16);
+            } else {
+              const float* w = static_cast<const float*>(q.wt) + w0;
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (col0 + i < N) v[i] += gr * bf16_round(w[i]);
+            }
           }
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
@@ -664,8 +673,9 @@ struct Gemm {
   int64_t ldo;
   float* part;
   const float* g;
-  const float* wt;
+  const void* wt;
   int64_t ldw;
+  int wt_bf16;
 };
 
 // Scratch size (floats) of the split partials of a GEMM.

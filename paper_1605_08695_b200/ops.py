@@ -12,8 +12,8 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (TFS_BF16, TFS_F32, TFS_REMOVE_ACCIDENTAL_HITS, TFS_SUBTRACT_LOG_Q, SsmArgs,
-                   TfsError, check)
+from ._lib import (TFS_BF16, TFS_BF16_OPERANDS, TFS_F32, TFS_REMOVE_ACCIDENTAL_HITS,
+                   TFS_SUBTRACT_LOG_Q, SsmArgs, TfsError, check)
 
 INT64_MAX = (1 << 63) - 1
 
@@ -152,6 +152,10 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
     B, d = h.shape
     S = sampled.numel()
     dev = h.device
+    if h.dtype == torch.bfloat16:  # operands already rounded (e.g. by a bf16 Gather)
+        assert w_true.dtype == torch.bfloat16 and w_s.dtype == torch.bfloat16
+        assert operand_dtype == TFS_BF16
+        flags |= TFS_BF16_OPERANDS
     if out is None:
         f = lambda *s: torch.empty(*s, dtype=torch.float32, device=dev)
         out = {"loss": f(B), "lse": f(B), "loss_sum": f(1), "dh": f(B, d), "dw_true": f(B, d),
@@ -292,8 +296,9 @@ class RoutePlan:
 def gather_peers(shard_tab, shard_rows: int, dim: int, ids, vocab: int, R: int, out,
                  err: ErrorSlot = None):
     """One-sided routed Gather: out[t] = row id//R of shard id%R through peer pointers."""
+    od = TFS_BF16 if out.dtype == torch.bfloat16 else TFS_F32
     check(_lib.lib().tfs_gather_peers(_p(shard_tab), int(shard_rows), int(dim), _p(ids),
-                                      ids.numel(), int(vocab), int(R), _p(out), _err(err),
+                                      ids.numel(), int(vocab), int(R), _p(out), od, _err(err),
                                       _stream()), "tfs_gather_peers")
     return out
 

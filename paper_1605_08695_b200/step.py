@@ -154,8 +154,12 @@ class ShardedStep:
         R = self.R
         L = ops._lib.lib()
         self.side_stream = torch.cuda.Stream(device=dev)
-        self.h = torch.empty((B, d), **f32)
-        self.w_rows = torch.empty((B + S, d), **f32)
+        # bf16 operand mode: the Gathers round h / W rows to bf16 on the way (the only values
+        # the bf16 softmax consumes), halving their writes and skipping its conversion pass.
+        bf16_rows = cfg.operand_dtype == TFS_BF16 and (self.R == 1 or cfg.route == "p2p")
+        rdt = dict(dtype=torch.bfloat16 if bf16_rows else torch.float32, device=dev)
+        self.h = torch.empty((B, d), **rdt)
+        self.w_rows = torch.empty((B + S, d), **rdt)
         self.b_rows = torch.empty(B + S, **f32)
         self.ssm_out = {"loss": torch.empty(B, **f32), "lse": torch.empty(B, **f32),
                         "loss_sum": torch.zeros(1, **f32), "dh": torch.empty((B, d), **f32)}

@@ -437,3 +437,17 @@ def test_route_plan_capacity_overflow_is_reported():
     err = ops.ErrorSlot(DEV)
     ops.RoutePlan(n, V, R, 100, 8, DEV).build(T(ids), send, 100, err=err)
     assert err.read() == (9, 0)
+
+
+@pytest.mark.parametrize("B,S,d", [(2560, 512, 512), (300, 1000, 64)])
+def test_ssm_bf16_operand_inputs_identical(B, S, d):
+    """TFS_BF16_OPERANDS: h / w_true / w_s handed over already rounded (a bf16 Gather) give
+    bit-identical outputs to the fp32 inputs rounded inside the call."""
+    c = _ssm_case(B, S, 40000, d, seed=B + 2 * S)
+    ref = _run_ssm(c, TFS_BF16, 1.0 / B)
+    bf = lambda a: T(a).to(torch.bfloat16)
+    out = ops.sampled_softmax(bf(c["h"]), T(c["labels"]), bf(c["w_true"]), T(c["b_true"]),
+                              T(c["le_t"]), T(c["s"]), bf(c["w_s"]), T(c["b_s"]), T(c["le_s"]),
+                              grad_scale=1.0 / B, operand_dtype=TFS_BF16, vocab=c["V"])
+    for k in KEYS + ("loss_sum",):
+        assert np.array_equal(out[k].cpu().numpy(), ref[k]), k
