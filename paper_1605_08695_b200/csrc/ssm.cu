@@ -90,17 +90,20 @@ size_t part_floats(int M, int N, int ksplit) {
   return ksplit > 1 ? (size_t)ksplit * M * N : 0;
 }
 
-static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int K, int ksplit) {
-  if (M <= 0 || N <= 0 || K <= 0) return TFS_ERR_INVALID_ARGUMENT;
+static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int K, int ksplit,
+                            int bn = BN) {
+  if (M <= 0 || N <= 0 || K <= 0 || bn < 32 || bn > BN || bn % 32 != 0)
+    return TFS_ERR_INVALID_ARGUMENT;
   int32_t rc = make_tmap(&p.ta, A, (uint64_t)M, (uint64_t)K, BM);
   if (rc != TFS_OK) return rc;
-  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, BNC);
+  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, (uint32_t)(bn / kCta));
   if (rc != TFS_OK) return rc;
   p.M = M;
   p.N = N;
   p.K = K;
+  p.bn = bn;
   p.num_m = (int)cdiv(M, PM);
-  p.num_n = (int)cdiv(N, BN);
+  p.num_n = (int)cdiv(N, bn);
   p.kb_total = (int)cdiv(K, BK);
   ksplit = std::max(1, std::min(ksplit, p.kb_total));
   p.kb_per_split = (int)cdiv(p.kb_total, ksplit);
@@ -140,11 +143,26 @@ static int32_t launch_params(const Params& P, cudaStream_t st) {
   return TFS_OK;
 }
 
-int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K,
+int pick_bn(int M, int N) {
+  const int64_t groups = num_sms() / kCta;
+  int best = BN;
+  int64_t best_cost = -1;
+  for (int bn = BN; bn >= 128; bn -= 32) {
+    const int64_t tiles = cdiv(M, PM) * cdiv(N, bn);
+    const int64_t cost = cdiv(tiles, groups) * bn;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn,
                              EpiParams ep, uint16_t* G, int64_t ldG, cudaStream_t st) {
   if (A.mn || B.mn) return TFS_ERR_INVALID_ARGUMENT;
   Params P{};
-  int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1);
+  int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1, bn);
   if (rc != TFS_OK) return rc;
   P.nprob = 1;
   P.total_units = P.p[0].units;
@@ -627,8 +645,9 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, int64_t 
     return c.used + 256;
   }
   const int64_t Sp = (S + 7) / 8 * 8;
-  const int64_t Spad = std::max<int64_t>(cdiv(S, umma::BN), 1) * umma::BN;
-  const int num_n = (int)cdiv(S, umma::BN);
+  // sized for any STATS / GRAD tile width in [128, 256] (chosen at launch, pick_bn)
+  const int num_n = (int)cdiv(S, 128);
+  const int64_t Spad = std::max<int64_t>(num_n, 1) * 128 + 256;
   int ks_dh = 1, ks_dws = 1;
   if (S > 0 && B > 0) plan_backward(B, S, d, &ks_dh, &ks_dws);
   Bf16Ws x;
@@ -698,7 +717,8 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const int hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) ? 1 : 0;
   const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
   const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
-  const int num_n = (int)cdiv(S, umma::BN);
+  const int bn = S > 0 ? umma::pick_bn((int)B, (int)S) : umma::BN;  // STATS / GRAD tile width
+  const int num_n = (int)cdiv(S, bn);
   const bool bin = (a->flags & TFS_BF16_OPERANDS) != 0;  // h, w_true, w_s given in bf16
 
   // Operands in bf16 (row-major; every GEMM reads them K- or MN-major as it needs), column
@@ -729,7 +749,8 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   if (S > 0) {  // pass 1: per-row (max, sum 2^x) of each half tile, log2 domain
     ep.stats = w.stats;
     ep.nparts = 2 * num_n;
-    rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, ep, nullptr, 0, st);
+    rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, bn, ep, nullptr, 0,
+                                    st);
     if (rc != TFS_OK) return rc;
   }
   auto combine = bin ? bf16_combine_kernel<true> : bf16_combine_kernel<false>;
@@ -748,7 +769,8 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   // pass 2: G = c exp(Z - lse) -> bf16 G
   ep.lse = a->lse;
   ep.c = a->grad_scale;
-  rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, ep, w.G, w.Sp, st);
+  rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, bn, ep, w.G, w.Sp,
+                                  st);
   if (rc != TFS_OK) return rc;
   // db_s = column sums of G
   g_colsum_kernel<<<(unsigned)(cdiv(S, kColsumChunks * 8) + (a->loss_sum ? 1 : 0)), 256, 0, st>>>(

@@ -102,6 +102,7 @@ struct Problem {
   CUtensorMap ta, tb;
   CUtensorMap to;   // STORE: fp32 out [M x ldo] (2D) or part [ksplit x M x N] (3D), box 16x32
   int M, N, K;
+  int bn;  // tile width along N: a multiple of 32, <= BN (STATS / GRAD pick it to balance SMs)
   int num_m, num_n, ksplit, kb_per_split, kb_total, units;
   int a_mn, b_mn;
   const float* g;   // optional row scale of the extra term (ksplit == 1 only)
@@ -307,7 +308,7 @@ __device__ __forceinline__ Unit decode_unit(const Params& P, int u) {
   r.kb0 = r.ks * q.kb_per_split;
   r.kb1 = min(q.kb_total, r.kb0 + q.kb_per_split);
   // whole 32-column chunks, so every epilogue chunk lies inside the MMA width
-  r.nw = min(BN, (q.N - r.nt * BN + 31) & ~31);
+  r.nw = min(q.bn, (q.N - r.nt * q.bn + 31) & ~31);
   return r;
 }
 
@@ -376,9 +377,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const Problem& q = P.p[t.pi];
         const int nh = t.nw / kCta;  // B rows this CTA holds
         const int bboxes = q.b_mn ? (nh + kMNBox - 1) / kMNBox : 0;
-        const uint32_t bbytes = q.b_mn ? (uint32_t)(bboxes * kMNBoxBytes) : (uint32_t)B_BYTES;
+        const uint32_t bbytes = q.b_mn ? (uint32_t)(bboxes * kMNBoxBytes)
+                                       : (uint32_t)((q.bn / kCta) * BK * 2);  // box: bn/kCta rows
         const int arow = t.mt * PM + (int)rank * BM;
-        const int bcol = t.nt * BN + (int)rank * nh;
+        const int bcol = t.nt * q.bn + (int)rank * nh;
         for (int kb = t.kb0; kb < t.kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           // the leader's barrier (peer bit cleared)
@@ -472,7 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         // this half tile's 128 column offsets -> smem (each warp of the half loads 32); the
         // buffer of this accumulator was last read two tiles ago, before the previous barrier
 #ifndef TFS_EXP_CB_GLOBAL
-        cbh[quarter * 32 + lane] = __ldg(ep.cb + t.nt * BN + half * 128 + quarter * 32 + lane);
+        cbh[quarter * 32 + lane] =
+            __ldg(ep.cb + t.nt * q.bn + half * 128 + quarter * 32 + lane);
 #endif
         if (row_ok) {
           if (ep.labels != nullptr) {
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int c = 0; c < 4; ++c) {
         const int ct = half * 128 + c * 32;  // column within the tile
         if (ct >= nw) break;                 // beyond a narrow tile's MMA width
-        const int col0 = t.nt * BN + ct;
+        const int col0 = t.nt * q.bn + ct;
         const bool next = c + 1 < 4 && ct + 32 < nw;
         tmem_wait_ld();
         float v[32];
@@ -684,8 +687,12 @@ int tiles_of(int M, int N);
 int effective_split(int K, int ksplit);
 
 // STATS / GRAD launch; for GRAD, G (bf16 [M x ldG], ldG % 8 == 0) receives the gradient.
-int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K,
+// bn: tile width along N (pick_bn); cb / sid must be readable up to num_n * bn + 256 columns.
+int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn,
                              EpiParams ep, uint16_t* G, int64_t ldG, cudaStream_t st);
+// Tile width for an M x N output of single-pass tiles: the multiple of 32 in [128, 256] that
+// minimises the makespan (rounds of tiles over the CTA groups x tile width).
+int pick_bn(int M, int N);
 int32_t launch_store(const Gemm* g, int count, cudaStream_t st);
 
 }  // namespace umma
