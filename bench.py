@@ -374,13 +374,18 @@ def main():
                     "ms": phases["sampled_softmax"]}
     hbm = None
     if "gather" in phases and "scatter_sgd" in phases:
-        # algorithmic bytes: gather reads n ids + n rows and writes n rows (fp32, d floats);
-        # scatter-SGD reads grad rows + table rows and writes table rows of the unique ids.
-        row = 4 * d
-        n_g = 2 * B + S
-        g_bytes = n_g * 8 + 2 * n_g * row + 2 * (B + S) * 4
+        # algorithmic bytes of the gather phase: ids read, the DISTINCT rows read
+        # (repeats are L2 hits), every requested row written (bf16 operand rows in bf16 mode;
+        # the bias in fp32).
+        row_in = 4 * d
+        row_out = (2 if args.dtype == "bf16" else 4) * d
+        u_e = int(torch.unique(st.x).numel())
+        u_w = int(torch.unique(st.qw).numel())
+        n_e, n_w = B, B + S
+        g_bytes = (8 * (n_e + n_w) + (u_e + u_w) * row_in + (n_e + n_w) * row_out
+                   + u_w * 4 + n_w * 4)
         t_g = phases["gather"] / 1e3
-        hbm = {"gather_GBps": g_bytes / t_g / 1e9,
+        hbm = {"gather_GBps": g_bytes / t_g / 1e9, "distinct_rows": [u_e, u_w],
                "gather_frac": g_bytes / t_g / 1e9 / peaks.get("hbm_gbs", 6538.6),
                "peak": peaks.get("hbm_gbs", 6538.6), "unit": "GB/s"}
 

@@ -266,10 +266,18 @@ int orc_sampled_softmax(const orc_ssm_io* io) {
     return acc;
   };
 
-  // O10: lse_t = mu + ln(e^{z-mu} + sum_j e^{Z_tj - mu}) for every token.
+  // O10: lse_t = mu + ln(e^{z-mu} + sum_j e^{Z_tj - mu}) for every token that an output needs:
+  // all tokens when any dW_s / db_s column is asked for (they sum over t), else only the
+  // requested tokens (same formula; the others are simply not evaluated).
   std::vector<double> lse((size_t)B), zt((size_t)B);
   std::vector<double> Zrow((size_t)S);
+  std::vector<char> need((size_t)B, 0);
+  const bool all_tokens = !io->tok_idx || !io->col_idx || io->n_col > 0;
+  if (!all_tokens)
+    for (int64_t r = 0; r < io->n_tok; ++r)
+      if (io->tok_idx[r] >= 0 && io->tok_idx[r] < B) need[io->tok_idx[r]] = 1;
   for (int64_t t = 0; t < B; ++t) {
+    if (!all_tokens && !need[t]) continue;
     zt[t] = z_true(t);
     double mu = zt[t];
     for (int64_t j = 0; j < S; ++j) {
