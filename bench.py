@@ -338,40 +338,70 @@ def main():
     # ---- instrumented eager steps: per-phase device time (roofline of the dominant op)
     phases = {}
     n_ph = max(1, min(args.phase_steps, args.steps))
+    kern_ms = {}
     if R == 1:
         st.phase_events = []
+        ssm_ev = []
         for i in range(n_ph):
             flush.zero_()
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+            for e in evs:
+                e.record()  # creates the CUDA events; the library re-records them in the call
+            st.ssm_events = evs
             st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], step_no)
+            ssm_ev.append(evs)
             step_no += 1
         torch.cuda.synchronize()
+        st.ssm_events = None
         for name, s_, e_ in st.phase_events:
             phases.setdefault(name, []).append(s_.elapsed_time(e_))
         st.phase_events = None
         phases = {k: sum(v) / len(v) for k, v in phases.items()}
+        if dtype == TFS_BF16 and S > 0:  # per-GEMM-launch durations, CUDA events on its stream
+            for name, (i0, i1) in (("gemm_stats", (1, 2)), ("gemm_grad", (3, 4)),
+                                   ("gemm_store", (5, 6))):
+                kern_ms[name] = sum(ev[i0].elapsed_time(ev[i1]) for ev in ssm_ev) / len(ssm_ev)
     st.err.check("bench instrumented steps")
 
     peaks, peak_src = load_peaks()
     roofline = None
-    if "sampled_softmax" in phases:
-        flop = 6.0 * B * S * d
-        t = phases["sampled_softmax"] / 1e3
-        achieved = flop / t / 1e12
-        peak = peaks.get("bf16_tflops_sustained", 1407.0)
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "traffic_ssm.json")
-        if os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get(args.workload)
-            except Exception:
-                traffic = None
-        roofline = {"kernel": "tfs_sampled_softmax_fwd_bwd (4 tcgen05 GEMM passes + epilogues)",
-                    "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": traffic,
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_ssm.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.workload)
+        except Exception:
+            traffic = None
+    peak = peaks.get("bf16_tflops_sustained", 1407.0)
+    if kern_ms:
+        # The dominant kernel of the step: the grouped backward GEMM (dh = G W_s and
+        # dW_s = G^T h in one persistent tcgen05 launch), 2 x 2 B S d algorithmic flops.
+        flops = {"gemm_stats": 2.0 * B * S * d, "gemm_grad": 2.0 * B * S * d,
+                 "gemm_store": 4.0 * B * S * d}
+        per = {k: {"ms": v, "tflops": flops[k] / (v / 1e3) / 1e12,
+                   "frac": flops[k] / (v / 1e3) / 1e12 / peak} for k, v in kern_ms.items()}
+        top = per["gemm_store"]
+        roofline = {"kernel": "umma::gemm_kernel<STORE> (dh = G W_s and dW_s = G^T h, one "
+                              "persistent tcgen05 launch)",
+                    "bound": "tensor", "achieved": top["tflops"], "peak": peak,
+                    "unit": "TFLOP/s", "frac": top["frac"],
+                    "traffic": (traffic or {}).get("gemm_store"),
                     "peak_source": f"{peak_src} bf16 sustained",
-                    "algorithmic": "6*B*S*d flops per launch (3 GEMMs; the logits recompute "
-                                   "is overhead)",
-                    "ms": phases["sampled_softmax"]}
+                    "algorithmic": "4*B*S*d flops per launch (two GEMMs); achieved = that / the "
+                                   "launch's CUDA-event duration in instrumented eager steps",
+                    "ms": top["ms"], "kernels": per}
+    if "sampled_softmax" in phases:
+        t = phases["sampled_softmax"] / 1e3
+        ssm = {"kernel": "tfs_sampled_softmax_fwd_bwd (whole call: 7 launches)", "bound": "tensor",
+               "achieved": 6.0 * B * S * d / t / 1e12, "peak": peak, "unit": "TFLOP/s",
+               "frac": 6.0 * B * S * d / t / 1e12 / peak,
+               "traffic": (traffic or {}).get("ssm_total"),
+               "algorithmic": "6*B*S*d flops per call (3 GEMMs; the logits recompute is overhead)",
+               "ms": phases["sampled_softmax"]}
+        if roofline is None:
+            roofline = ssm
+        else:
+            roofline["sampled_softmax_call"] = ssm
     hbm = None
     if "gather" in phases and "scatter_sgd" in phases:
         # algorithmic bytes of the gather phase: ids read, the DISTINCT rows read

@@ -190,6 +190,11 @@ typedef struct {
   float* dw_s;
   float* db_s;
   int64_t vocab;
+  /* Optional instrumentation (bf16 path): NULL, or an array of 8 cudaEvent_t (any entry NULL)
+   * recorded on the stream at: 0 start, 1 after the prep pass, 2 after the logits GEMM (STATS),
+   * 3 after the combine, 4 after the gradient GEMM (GRAD), 5 after the column sums, 6 after
+   * the grouped dh / dW_s GEMM, 7 end.  Lets a caller time each GEMM launch live. */
+  void* const* timing_events;
 } tfs_ssm_args;
 size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype,
                                int64_t vocab);

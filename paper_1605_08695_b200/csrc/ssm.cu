@@ -717,6 +717,11 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const int hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) ? 1 : 0;
   const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
   const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
+  auto mark = [&](int i) {  // optional instrumentation events (tfs_ssm_args::timing_events)
+    if (a->timing_events != nullptr && a->timing_events[i] != nullptr)
+      cudaEventRecord(static_cast<cudaEvent_t>(a->timing_events[i]), st);
+  };
+  mark(0);
   const int bn = S > 0 ? umma::pick_bn((int)B, (int)S) : umma::BN;  // STATS / GRAD tile width
   const int num_n = (int)cdiv(S, bn);
   const bool bin = (a->flags & TFS_BF16_OPERANDS) != 0;  // h, w_true, w_s given in bf16
@@ -735,6 +740,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
       a->sampled, S, w.Spad, cmap, V, w.cb, w.sid);
   launched();
   TFS_LAUNCH_CHECK();
+  mark(1);
 
   using umma::Operand;
   umma::EpiParams ep{};
@@ -753,12 +759,14 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
                                     st);
     if (rc != TFS_OK) return rc;
   }
+  mark(2);
   auto combine = bin ? bf16_combine_kernel<true> : bf16_combine_kernel<false>;
   combine<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(B, d, a->h, a->w_true, a->b_true, le_t, w.stats,
                                                 2 * num_n, a->grad_scale, a->loss, a->lse,
                                                 a->dw_true, a->db_true);
   launched();
   TFS_LAUNCH_CHECK();
+  mark(3);
   if (S == 0) {  // no candidates: dh = g * bf16(w_true)
     auto fin = bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
     fin<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true, a->w_true, a->dh);
@@ -772,10 +780,12 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, bn, ep, w.G, w.Sp,
                                   st);
   if (rc != TFS_OK) return rc;
+  mark(4);
   // db_s = column sums of G
   g_colsum_kernel<<<(unsigned)(cdiv(S, kColsumChunks * 8) + (a->loss_sum ? 1 : 0)), 256, 0, st>>>(
       w.G, B, S, w.Sp, a->db_s, a->sampled, cmap, V, a->loss, a->grad_scale, a->loss_sum);
   launched();
+  mark(5);
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
   // (A = G K-major, B = W_s MN-major) in one persistent launch; split partials are reduced in
   // split order by the finalize pass, which also adds the true-class term of dh.
@@ -791,6 +801,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   if (u1 > u0) std::swap(g[0], g[1]);
   rc = umma::launch_store(g, 2, st);
   if (rc != TFS_OK) return rc;
+  mark(6);
   if (dh_split) {
     auto fin = bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
     fin<<<grid1d(B * d / 4), 256, 0, st>>>(w.part_dh, w.ks_dh, B, d, a->db_true, a->w_true,
@@ -803,6 +814,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     launched();
   }
   TFS_LAUNCH_CHECK();
+  mark(7);
   return TFS_OK;
 }
 

@@ -190,6 +190,7 @@ class ShardedStep:
                        for k in ("route_e", "ids", "own", "h", "q", "ssm", "red_e", "b2")}
         self.graph = None
         self.phase_events = None  # list of (phase, start, end) when instrumented
+        self.ssm_events = None    # 8 timing events recorded inside the softmax call (bench)
 
     def _symm(self, shape, dtype):
         """A symmetric-memory tensor of this shape on every rank and the int64 tensor of the R
@@ -268,7 +269,7 @@ class ShardedStep:
                             self.qw[B:], self.w_rows[B:], self.b_rows[B:], self.les,
                             flags=self.flags, grad_scale=self.c,
                             operand_dtype=self.cfg.operand_dtype, vocab=self.cfg.vocab,
-                            out=self.ssm_out, ws=self.ws_ssm)
+                            out=self.ssm_out, ws=self.ws_ssm, events=self.ssm_events)
 
     def _ph(self, name: str):
         """Phase marker: with ``self.phase_events`` set (bench instrumentation, eager only) the
