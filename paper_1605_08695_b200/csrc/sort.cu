@@ -466,7 +466,14 @@ struct SegJob {
   // chunk c and continues after it.
   double* part;   // [2 * nchunks x dim]
   double* part2;  // [2 * nchunks]
-  // segments that cross a chunk boundary (appended by the chunk kernel; order is irrelevant)
+  // Second level for segments that cross chunk boundaries: chunk_info[c] = (segment of the
+  // piece in slot 2c, segment of the piece in slot 2c+1), -1 where absent.  Blocks of kBlk
+  // chunks: blk[2b] = the block's piece of the segment that started before the block,
+  // blk[2b+1] = the piece of the segment that starts in the block and continues after it;
+  // those segments are appended to cross_list (order irrelevant).
+  int2* chunk_info;
+  double* blk;    // [2 * nblocks x dim]
+  double* blk2;   // [2 * nblocks]
   uint32_t* cross_list;
   uint32_t* cross_count;
 };
@@ -624,59 +631,123 @@ __global__ void __launch_bounds__(256, TFS_SEG_MINB) seg_chunk_vec4_kernel(SegJo
     } else {
       const int64_t slot = starts_before ? 2 * chunk : 2 * chunk + 1;
       if (col_ok) reinterpret_cast<D4*>(j.part + slot * j.dim)[c4] = acc;
-      if (lane == 0 && slice == 0) {
-        if (j.rows2) j.part2[slot] = acc2;
-        if (!starts_before) j.cross_list[atomicAdd(j.cross_count, 1u)] = sg;
-      }
+      if (lane == 0 && slice == 0 && j.rows2) j.part2[slot] = acc2;
+    }
+  }
+  {  // which segments own this chunk's two partial slots
+    const uint32_t s_first = __shfl_sync(0xffffffffu, seg_l, 0);
+    const uint32_t k_first = __shfl_sync(0xffffffffu, key_l, 0);
+    const uint32_t s_last = __shfl_sync(0xffffffffu, seg_l, cnt - 1);
+    const uint32_t k_last = __shfl_sync(0xffffffffu, key_l, cnt - 1);
+    if (lane == 0 && slice == 0) {
+      const int head = (first_before && k_first < j.invalid_key) ? (int)s_first : -1;
+      const int tail = (last_after && k_last < j.invalid_key && (int)s_last != head)
+                           ? (int)s_last : -1;
+      j.chunk_info[chunk] = make_int2(head, tail);
     }
   }
 }
 
-// One thread per (crossing segment, float4 column): chunk partials added in chunk order,
-// then applied / written.
-__global__ void __launch_bounds__(256) seg_cross_vec4_kernel(SegJob j) {
+// A segment whose pieces are all summed: T[key] = fl32(T - lr * g) (apply) or written out.
+__device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int c4, const D4& acc,
+                                                bool col0, double acc2) {
+  const uint32_t key = j.keys[j.seg_start[s]];
+  if (key >= j.invalid_key) return;
+  if (j.table == nullptr) {
+    const OutPos op = seg_out_pos(j, s, key);
+    if (op.row == nullptr) return;
+    reinterpret_cast<float4*>(op.row)[c4] = to_f4(acc);
+    if (col0) {
+      if (j.out_local) j.out_local[op.local] = (int64_t)(key % (uint32_t)j.nloc);
+      if (op.r2) *op.r2 = (float)acc2;
+    }
+  } else {
+    float4* tp = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c4;
+    float4 w = *tp;
+    const double lr = (double)j.lr;
+    w.x = (float)((double)w.x - lr * acc.x);
+    w.y = (float)((double)w.y - lr * acc.y);
+    w.z = (float)((double)w.z - lr * acc.z);
+    w.w = (float)((double)w.w - lr * acc.w);
+    *tp = w;
+    if (col0 && j.table2) j.table2[key] = (float)((double)j.table2[key] - lr * acc2);
+  }
+}
+
+constexpr int kBlk = 32;  // chunks per block of the second reduction level
+
+// Level A, one thread per (block of kBlk chunks, float4 column): walks the block's partial
+// slots in chunk order, summing each segment's run of pieces in order; a segment lying inside
+// the block is finished here, the runs of segments that enter or leave the block go to the
+// block slots.  Heavy ids (thousands of rows) thus become ~n / (8 kBlk) sums of <= 2 kBlk.
+__global__ void __launch_bounds__(256) seg_cross_a_vec4_kernel(SegJob j, int64_t nchunks) {
+  const int n4 = j.dim >> 2;
+  const int64_t nblk = (nchunks + kBlk - 1) / kBlk;
+  const int64_t total = nblk * n4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / n4;
+    const int c4 = (int)(e - b * n4);
+    const bool col0 = c4 == 0;
+    const int64_t cb = b * kBlk, ce = min(nchunks, cb + kBlk);
+    int64_t cur = -1;
+    D4 acc = D4{0.0, 0.0, 0.0, 0.0};
+    double acc2 = 0.0;
+    auto flush = [&]() {
+      if (cur < 0) return;
+      const int64_t c0 = j.seg_start[cur] / kChunk, c1 = (j.seg_start[cur + 1] - 1) / kChunk;
+      if (c0 >= cb && c1 < ce) {
+        seg_finish_vec4(j, (uint32_t)cur, c4, acc, col0, acc2);
+      } else {
+        const int64_t slot = c0 < cb ? 2 * b : 2 * b + 1;
+        reinterpret_cast<D4*>(j.blk + slot * j.dim)[c4] = acc;
+        if (col0) {
+          if (j.rows2) j.blk2[slot] = acc2;
+          if (c0 >= cb) j.cross_list[atomicAdd(j.cross_count, 1u)] = (uint32_t)cur;
+        }
+      }
+    };
+    for (int64_t c = cb; c < ce; ++c) {
+      const int2 info = j.chunk_info[c];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int sg = h ? info.y : info.x;
+        if (sg < 0) continue;
+        if (sg != cur) {
+          flush();
+          cur = sg;
+          acc = D4{0.0, 0.0, 0.0, 0.0};
+          acc2 = 0.0;
+        }
+        const int64_t slot = 2 * c + h;
+        add4(acc, reinterpret_cast<const D4*>(j.part + slot * j.dim)[c4]);
+        if (j.rows2) acc2 += j.part2[slot];
+      }
+    }
+    flush();
+  }
+}
+
+// Level B, one thread per (segment spanning several blocks, float4 column): its block pieces
+// added in block order, then finished.
+__global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
   const uint32_t ncross = *j.cross_count;
   const int n4 = j.dim >> 2;
   const int64_t total = (int64_t)ncross * n4;
-  const bool write_mode = j.table == nullptr;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = e / n4;
-    const int c = (int)(e - q * n4);
+    const int c4 = (int)(e - q * n4);
     const uint32_t s = j.cross_list[q];
-    const uint32_t a = j.seg_start[s], b = j.seg_start[s + 1];
-    const uint32_t key = j.keys[a];
-    const int64_t c0 = a / kChunk, c1 = (b - 1) / kChunk;
-    D4 acc = reinterpret_cast<const D4*>(j.part + (2 * c0 + 1) * j.dim)[c];
-#pragma unroll 16
-    for (int64_t ch = c0 + 1; ch <= c1; ++ch)
-      add4(acc, reinterpret_cast<const D4*>(j.part + (2 * ch) * j.dim)[c]);
-    const OutPos op = write_mode ? seg_out_pos(j, s, key) : OutPos{j.table, nullptr, 0};
-    if (op.row == nullptr) continue;
-    if (write_mode) {
-      reinterpret_cast<float4*>(op.row)[c] = to_f4(acc);
-    } else {
-      float4* tp = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c;
-      float4 w = *tp;
-      const double lr = (double)j.lr;
-      w.x = (float)((double)w.x - lr * acc.x);
-      w.y = (float)((double)w.y - lr * acc.y);
-      w.z = (float)((double)w.z - lr * acc.z);
-      w.w = (float)((double)w.w - lr * acc.w);
-      *tp = w;
+    const int64_t b0 = (j.seg_start[s] / kChunk) / kBlk;
+    const int64_t b1 = ((j.seg_start[s + 1] - 1) / kChunk) / kBlk;
+    D4 acc = reinterpret_cast<const D4*>(j.blk + (2 * b0 + 1) * j.dim)[c4];
+    double acc2 = (c4 == 0 && j.rows2) ? j.blk2[2 * b0 + 1] : 0.0;
+    for (int64_t bb = b0 + 1; bb <= b1; ++bb) {
+      add4(acc, reinterpret_cast<const D4*>(j.blk + (2 * bb) * j.dim)[c4]);
+      if (c4 == 0 && j.rows2) acc2 += j.blk2[2 * bb];
     }
-    if (c == 0) {
-      if (write_mode && j.out_local) j.out_local[op.local] = (int64_t)(key % (uint32_t)j.nloc);
-      if (j.rows2) {
-        double acc2 = j.part2[2 * c0 + 1];
-        for (int64_t ch = c0 + 1; ch <= c1; ++ch) acc2 += j.part2[2 * ch];
-        if (write_mode) {
-          if (op.r2) *op.r2 = (float)acc2;
-        }
-        else if (j.table2)
-          j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * acc2);
-      }
-    }
+    seg_finish_vec4(j, s, c4, acc, c4 == 0, acc2);
   }
 }
 
@@ -854,6 +925,8 @@ struct SegScratch {
   double *part, *part2;
   float *sums, *sums2;
   uint32_t *cross_list, *cross_count;
+  int2* chunk_info;
+  double *blk, *blk2;
 };
 
 static void carve_plan(Carver& c, int64_t n, SegScratch& x) {
@@ -878,6 +951,10 @@ static void carve_apply(Carver& c, int64_t n, int32_t dim, SegScratch& x) {
   x.sums2 = c.take<float>((size_t)n);
   x.cross_list = c.take<uint32_t>((size_t)nchunks + 1);
   x.cross_count = c.take<uint32_t>(1);
+  const int64_t nblk = cdiv(nchunks, kBlk);
+  x.chunk_info = c.take<int2>((size_t)nchunks);
+  x.blk = c.take<double>((size_t)2 * nblk * dim);
+  x.blk2 = c.take<double>((size_t)2 * nblk);
 }
 
 static size_t plan_scratch_bytes(int64_t n, SegScratch* s, void* ws, size_t cap) {
@@ -895,6 +972,7 @@ static size_t apply_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* w
   if (s) {
     s->part = x.part; s->part2 = x.part2; s->sums = x.sums; s->sums2 = x.sums2;
     s->cross_list = x.cross_list; s->cross_count = x.cross_count;
+    s->chunk_info = x.chunk_info; s->blk = x.blk; s->blk2 = x.blk2;
   }
   return c.used + 256;
 }
@@ -1109,6 +1187,9 @@ static void bind(SegJob& j, const SegScratch& s, int64_t n) {
   j.sums2 = s.sums2;
   j.cross_list = s.cross_list;
   j.cross_count = s.cross_count;
+  j.chunk_info = s.chunk_info;
+  j.blk = s.blk;
+  j.blk2 = s.blk2;
 }
 
 static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
@@ -1125,9 +1206,14 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
     const int vgrid = (int)std::max<int64_t>(1, cdiv(nchunks * nslices, 8));
     seg_chunk_vec4_kernel<<<vgrid, 256, 0, st>>>(j, nslices);
     launched();
-    const int64_t work = (nchunks + 1) * (j.dim >> 2);  // crossing segments <= nchunks
-    const int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, 256), 4 * num_sms()));
-    seg_cross_vec4_kernel<<<cgrid, 256, 0, st>>>(j);
+    const int64_t n4 = j.dim >> 2;
+    const int64_t awork = cdiv(nchunks, kBlk) * n4;
+    const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(awork, 256), 8 * num_sms()));
+    seg_cross_a_vec4_kernel<<<agrid, 256, 0, st>>>(j, nchunks);
+    launched();
+    const int64_t bwork = (cdiv(nchunks, kBlk) + 1) * n4;  // block-crossing segments <= blocks
+    const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(bwork, 256), 4 * num_sms()));
+    seg_cross_b_vec4_kernel<<<bgrid, 256, 0, st>>>(j);
     launched();
   } else {
     seg_chunk_scalar_kernel<<<grid, 256, 0, st>>>(j);
