@@ -467,13 +467,9 @@ struct SegJob {
   double* part;   // [2 * nchunks x dim]
   double* part2;  // [2 * nchunks]
   // Second level for segments that cross chunk boundaries: chunk_info[c] = (segment of the
-  // piece in slot 2c, segment of the piece in slot 2c+1), -1 where absent.  Blocks of kBlk
-  // chunks: blk[2b] = the block's piece of the segment that started before the block,
-  // blk[2b+1] = the piece of the segment that starts in the block and continues after it;
-  // those segments are appended to cross_list (order irrelevant).
+  // piece in slot 2c, segment of the piece in slot 2c+1), -1 where absent; the crossing
+  // segments are listed in cross_list (order irrelevant).
   int2* chunk_info;
-  double* blk;    // [2 * nblocks x dim]
-  double* blk2;   // [2 * nblocks]
   uint32_t* cross_list;
   uint32_t* cross_count;
 };
@@ -631,7 +627,10 @@ __global__ void __launch_bounds__(256, TFS_SEG_MINB) seg_chunk_vec4_kernel(SegJo
     } else {
       const int64_t slot = starts_before ? 2 * chunk : 2 * chunk + 1;
       if (col_ok) reinterpret_cast<D4*>(j.part + slot * j.dim)[c4] = acc;
-      if (lane == 0 && slice == 0 && j.rows2) j.part2[slot] = acc2;
+      if (lane == 0 && slice == 0) {
+        if (j.rows2) j.part2[slot] = acc2;
+        if (!starts_before) j.cross_list[atomicAdd(j.cross_count, 1u)] = sg;  // its first piece
+      }
     }
   }
   {  // which segments own this chunk's two partial slots
@@ -674,12 +673,13 @@ __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int
   }
 }
 
-constexpr int kBlk = 32;  // chunks per block of the second reduction level
+constexpr int kBlk = 16;  // chunks per block of the second reduction level
 
-// Level A, one thread per (block of kBlk chunks, float4 column): walks the block's partial
-// slots in chunk order, summing each segment's run of pieces in order; a segment lying inside
-// the block is finished here, the runs of segments that enter or leave the block go to the
-// block slots.  Heavy ids (thousands of rows) thus become ~n / (8 kBlk) sums of <= 2 kBlk.
+// Level A, one thread per (block of kBlk chunks, float4 column): the block's partial slots are
+// read in chunk order and every RUN of consecutive slots owned by the same segment is summed in
+// that order into the run's first slot (in place; the thread owns its block's slots of its
+// column).  A crossing segment then has one run per block it touches, starting at slot
+// 2 c0 + 1 (c0 = its first chunk) and at slot 2 kBlk b for every later block b.
 __global__ void __launch_bounds__(256) seg_cross_a_vec4_kernel(SegJob j, int64_t nchunks) {
   const int n4 = j.dim >> 2;
   const int64_t nblk = (nchunks + kBlk - 1) / kBlk;
@@ -688,48 +688,57 @@ __global__ void __launch_bounds__(256) seg_cross_a_vec4_kernel(SegJob j, int64_t
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = e / n4;
     const int c4 = (int)(e - b * n4);
-    const bool col0 = c4 == 0;
+    const bool col0 = c4 == 0 && j.rows2 != nullptr;
     const int64_t cb = b * kBlk, ce = min(nchunks, cb + kBlk);
-    int64_t cur = -1;
+    int2 info[kBlk];
+#pragma unroll
+    for (int u = 0; u < kBlk; ++u)
+      info[u] = cb + u < ce ? __ldg(j.chunk_info + cb + u) : make_int2(-1, -1);
+    int cur = -1;
+    int64_t run_slot = -1;
     D4 acc = D4{0.0, 0.0, 0.0, 0.0};
     double acc2 = 0.0;
-    auto flush = [&]() {
-      if (cur < 0) return;
-      const int64_t c0 = j.seg_start[cur] / kChunk, c1 = (j.seg_start[cur + 1] - 1) / kChunk;
-      if (c0 >= cb && c1 < ce) {
-        seg_finish_vec4(j, (uint32_t)cur, c4, acc, col0, acc2);
-      } else {
-        const int64_t slot = c0 < cb ? 2 * b : 2 * b + 1;
-        reinterpret_cast<D4*>(j.blk + slot * j.dim)[c4] = acc;
-        if (col0) {
-          if (j.rows2) j.blk2[slot] = acc2;
-          if (c0 >= cb) j.cross_list[atomicAdd(j.cross_count, 1u)] = (uint32_t)cur;
-        }
-      }
-    };
-    for (int64_t c = cb; c < ce; ++c) {
-      const int2 info = j.chunk_info[c];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int sg = h ? info.y : info.x;
+    for (int u0 = 0; u0 < kBlk; u0 += 4) {  // 8 slots' loads issued before their additions
+      D4 pc[8];
+      double p2[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int u = u0 + (q >> 1);
+        const int sg = (q & 1) ? info[u].y : info[u].x;
+        const int64_t slot = 2 * (cb + u) + (q & 1);
+        pc[q] = sg >= 0 ? reinterpret_cast<const D4*>(j.part + slot * j.dim)[c4]
+                        : D4{0.0, 0.0, 0.0, 0.0};
+        p2[q] = (sg >= 0 && col0) ? j.part2[slot] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int u = u0 + (q >> 1);
+        const int sg = (q & 1) ? info[u].y : info[u].x;
         if (sg < 0) continue;
         if (sg != cur) {
-          flush();
+          if (cur >= 0) {
+            reinterpret_cast<D4*>(j.part + run_slot * j.dim)[c4] = acc;
+            if (col0) j.part2[run_slot] = acc2;
+          }
           cur = sg;
+          run_slot = 2 * (cb + u) + (q & 1);
           acc = D4{0.0, 0.0, 0.0, 0.0};
           acc2 = 0.0;
         }
-        const int64_t slot = 2 * c + h;
-        add4(acc, reinterpret_cast<const D4*>(j.part + slot * j.dim)[c4]);
-        if (j.rows2) acc2 += j.part2[slot];
+        add4(acc, pc[q]);
+        acc2 += p2[q];
       }
     }
-    flush();
+    if (cur >= 0) {
+      reinterpret_cast<D4*>(j.part + run_slot * j.dim)[c4] = acc;
+      if (col0) j.part2[run_slot] = acc2;
+    }
   }
 }
 
-// Level B, one thread per (segment spanning several blocks, float4 column): its block pieces
-// added in block order, then finished.
+// Level B, one thread per (segment crossing a chunk boundary, float4 column): its run sums
+// added in block order, then T[key] = fl32(T - lr * sum) (apply) or written out.
 __global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
   const uint32_t ncross = *j.cross_count;
   const int n4 = j.dim >> 2;
@@ -739,13 +748,16 @@ __global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
     const int64_t q = e / n4;
     const int c4 = (int)(e - q * n4);
     const uint32_t s = j.cross_list[q];
-    const int64_t b0 = (j.seg_start[s] / kChunk) / kBlk;
-    const int64_t b1 = ((j.seg_start[s + 1] - 1) / kChunk) / kBlk;
-    D4 acc = reinterpret_cast<const D4*>(j.blk + (2 * b0 + 1) * j.dim)[c4];
-    double acc2 = (c4 == 0 && j.rows2) ? j.blk2[2 * b0 + 1] : 0.0;
+    const int64_t c0 = j.seg_start[s] / kChunk, c1 = (j.seg_start[s + 1] - 1) / kChunk;
+    const int64_t b0 = c0 / kBlk, b1 = c1 / kBlk;
+    const bool col0 = c4 == 0 && j.rows2 != nullptr;
+    D4 acc = reinterpret_cast<const D4*>(j.part + (2 * c0 + 1) * j.dim)[c4];
+    double acc2 = col0 ? j.part2[2 * c0 + 1] : 0.0;
+#pragma unroll 8
     for (int64_t bb = b0 + 1; bb <= b1; ++bb) {
-      add4(acc, reinterpret_cast<const D4*>(j.blk + (2 * bb) * j.dim)[c4]);
-      if (c4 == 0 && j.rows2) acc2 += j.blk2[2 * bb];
+      const int64_t slot = 2 * bb * kBlk;
+      add4(acc, reinterpret_cast<const D4*>(j.part + slot * j.dim)[c4]);
+      if (col0) acc2 += j.part2[slot];
     }
     seg_finish_vec4(j, s, c4, acc, c4 == 0, acc2);
   }
@@ -926,7 +938,6 @@ struct SegScratch {
   float *sums, *sums2;
   uint32_t *cross_list, *cross_count;
   int2* chunk_info;
-  double *blk, *blk2;
 };
 
 static void carve_plan(Carver& c, int64_t n, SegScratch& x) {
@@ -951,10 +962,7 @@ static void carve_apply(Carver& c, int64_t n, int32_t dim, SegScratch& x) {
   x.sums2 = c.take<float>((size_t)n);
   x.cross_list = c.take<uint32_t>((size_t)nchunks + 1);
   x.cross_count = c.take<uint32_t>(1);
-  const int64_t nblk = cdiv(nchunks, kBlk);
   x.chunk_info = c.take<int2>((size_t)nchunks);
-  x.blk = c.take<double>((size_t)2 * nblk * dim);
-  x.blk2 = c.take<double>((size_t)2 * nblk);
 }
 
 static size_t plan_scratch_bytes(int64_t n, SegScratch* s, void* ws, size_t cap) {
@@ -972,7 +980,7 @@ static size_t apply_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* w
   if (s) {
     s->part = x.part; s->part2 = x.part2; s->sums = x.sums; s->sums2 = x.sums2;
     s->cross_list = x.cross_list; s->cross_count = x.cross_count;
-    s->chunk_info = x.chunk_info; s->blk = x.blk; s->blk2 = x.blk2;
+    s->chunk_info = x.chunk_info;
   }
   return c.used + 256;
 }
@@ -1188,8 +1196,6 @@ static void bind(SegJob& j, const SegScratch& s, int64_t n) {
   j.cross_list = s.cross_list;
   j.cross_count = s.cross_count;
   j.chunk_info = s.chunk_info;
-  j.blk = s.blk;
-  j.blk2 = s.blk2;
 }
 
 static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
@@ -1211,7 +1217,7 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
     const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(awork, 256), 8 * num_sms()));
     seg_cross_a_vec4_kernel<<<agrid, 256, 0, st>>>(j, nchunks);
     launched();
-    const int64_t bwork = (cdiv(nchunks, kBlk) + 1) * n4;  // block-crossing segments <= blocks
+    const int64_t bwork = (nchunks + 1) * n4;  // crossing segments <= chunks
     const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(bwork, 256), 4 * num_sms()));
     seg_cross_b_vec4_kernel<<<bgrid, 256, 0, st>>>(j);
     launched();
