@@ -10,6 +10,7 @@
 // Every reduction has a fixed order (split-K partials are summed in split order), so outputs
 // are run-to-run bit-identical.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 
@@ -140,6 +141,14 @@ static int32_t launch_params(const Params& P, cudaStream_t st) {
   TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE>, P));
   launched();
   TFS_LAUNCH_CHECK();
+  if (std::getenv("TFS_DEBUG_SYNC") != nullptr) {  // diagnostics: attribute faults to a mode
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      static const char* names[] = {"gemm_kernel<STATS>", "gemm_kernel<GRAD>", "gemm_kernel<STORE>"};
+      set_last_error(names[MODE], e);
+      return TFS_ERR_CUDA;
+    }
+  }
   return TFS_OK;
 }
 

@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (ct >= nw) break;                 // beyond a narrow tile's MMA width
         const int col0 = t.nt * q.bn + ct;
         const bool next = c + 1 < 4 && ct + 32 < nw;
+        __syncwarp();  // tcgen05.ld / wait are .sync.aligned: the warp must be converged here
         tmem_wait_ld();
         float v[32];
         if (c & 1) {
