@@ -87,9 +87,12 @@ def _declare(L):
     L.orc_log_uniform_sample.argtypes = [I64, I32, I32, U64, U64, U32, P, I64, I64, P, P, P, P]
     L.orc_sampled_softmax.argtypes = [ctypes.POINTER(_SsmIO)]
     L.orc_scatter_add_sgd.argtypes = [P, I64, I32, P, P, I64, ctypes.c_double, P]
+    L.orc_scatter_opt.argtypes = [ctypes.c_int, P, P, I64, I32, P, P, I64, ctypes.c_double,
+                                  ctypes.c_double, P]
     L.orc_sort_reduce.argtypes = [P, I64, I32, P, I32, P, P, P, P]
     for f in (L.orc_partition, L.orc_gather, L.orc_stitch, L.orc_log_uniform_sample,
-              L.orc_sampled_softmax, L.orc_scatter_add_sgd, L.orc_sort_reduce):
+              L.orc_sampled_softmax, L.orc_scatter_add_sgd, L.orc_sort_reduce,
+              L.orc_scatter_opt):
         f.restype = ctypes.c_int
 
 
@@ -220,6 +223,24 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
                 _ptr(out["dw_true"]), _ptr(out["db_true"]), _ptr(out["dw_s"]), _ptr(out["db_s"]))
     _check(lib().orc_sampled_softmax(ctypes.byref(io)))
     return out
+
+
+def scatter_opt(kind, table, slot, ids, grad, lr, mu=0.0, inplace=False):
+    """Sparse Momentum ("momentum") / Adagrad ("adagrad") on distinct-id sums (R-29).
+    Returns (table, slot) (copies unless inplace)."""
+    k = {"momentum": 1, "adagrad": 2}[kind]
+    if not inplace:
+        table = np.array(table, dtype=np.float32, copy=True)
+        slot = np.array(slot, dtype=np.float32, copy=True)
+    rows = table.shape[0]
+    dim = 1 if table.ndim == 1 else table.shape[1]
+    ids = _c(ids, np.int64)
+    grad = _c(grad, np.float64).reshape(ids.size, dim)
+    bad = I64(-1)
+    st = lib().orc_scatter_opt(k, _ptr(table), _ptr(slot), rows, dim, _ptr(ids), _ptr(grad),
+                               ids.size, float(lr), float(mu), ctypes.byref(bad))
+    _check(st, bad)
+    return table, slot
 
 
 def scatter_add_sgd(table, ids, grad, lr, inplace=False):

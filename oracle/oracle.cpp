@@ -361,6 +361,45 @@ int orc_scatter_add_sgd(float* table, int64_t rows, int32_t dim, const int64_t* 
   return kOk;
 }
 
+// Sparse Momentum / Adagrad ("Momentum, Adagrad, ... as user-level code" on the same
+// sparse update path; reading R-29).  Per distinct id r, with g the fp64 sum of
+// its gradient rows in increasing i (as orc_scatter_add_sgd):
+//   momentum: m_r = fl32(mu * m_r + g);        T_r = fl32(T_r - lr * m_r)
+//   adagrad:  a_r = fl32(a_r + g * g);         T_r = fl32(T_r - lr * g / sqrt(a_r))
+// (elementwise; the slot tables m / a are fp32 like T; the rounded slot value is the one used).
+int orc_scatter_opt(int kind, float* table, float* slot, int64_t rows, int32_t dim,
+                    const int64_t* ids, const double* grad, int64_t n, double lr, double mu,
+                    int64_t* bad) {
+  if (n < 0 || dim < 1 || (kind != 1 && kind != 2)) return kInvalid;
+  for (int64_t i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= rows) {
+      if (bad) *bad = i;
+      return kOutOfRange;
+    }
+  }
+  std::map<int64_t, std::vector<double>> acc;
+  for (int64_t i = 0; i < n; ++i) {
+    auto& g = acc[ids[i]];
+    if (g.empty()) g.assign((size_t)dim, 0.0);
+    for (int32_t k = 0; k < dim; ++k) g[k] += grad[i * dim + k];
+  }
+  for (auto& kv : acc) {
+    float* row = table + kv.first * (int64_t)dim;
+    float* sl = slot + kv.first * (int64_t)dim;
+    for (int32_t k = 0; k < dim; ++k) {
+      const double g = kv.second[k];
+      if (kind == 1) {
+        sl[k] = (float)(mu * (double)sl[k] + g);
+        row[k] = (float)((double)row[k] - lr * (double)sl[k]);
+      } else {
+        sl[k] = (float)((double)sl[k] + g * g);
+        row[k] = (float)((double)row[k] - lr * g / std::sqrt((double)sl[k]));
+      }
+    }
+  }
+  return kOk;
+}
+
 int orc_sort_reduce(const int64_t* ids, int64_t n, int32_t num_shards, const double* rows,
                     int32_t dim, int64_t* out_local, double* out_rows, int64_t* out_counts,
                     int64_t* out_num_unique) {

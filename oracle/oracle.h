@@ -89,6 +89,12 @@ int orc_sampled_softmax(const orc_ssm_io* io);
  * table[r] = fl32(table[r] - lr * G[r]).  Duplicates accumulate; untouched rows unchanged. */
 int orc_scatter_add_sgd(float* table, int64_t rows, int32_t dim, const int64_t* ids,
                         const double* grad, int64_t n, double lr, int64_t* bad);
+/* Sparse Momentum (kind 1) / Adagrad (kind 2) on the same distinct-id sums (reading R-29):
+ * momentum m = fl32(mu m + g), T = fl32(T - lr m); adagrad a = fl32(a + g^2),
+ * T = fl32(T - lr g / sqrt(a)).  slot: the fp32 m or a table, same shape as table. */
+int orc_scatter_opt(int kind, float* table, float* slot, int64_t rows, int32_t dim,
+                    const int64_t* ids, const double* grad, int64_t n, double lr, double mu,
+                    int64_t* bad);
 
 /* ---- Sort-reduce of a sparse gradient before routing (R-16): unique ids in
  * ascending (owner, local) order, owner = id mod R, local = id div R, fp64 sums. */

@@ -523,3 +523,60 @@ def test_step_r1_is_sequential_sgd():
     refW = (W - 1.0 * dW).astype(np.float32)
     np.testing.assert_array_max_ulp(W2, refW, maxulp=1)
     np.testing.assert_array_max_ulp(b2, (b - db).astype(np.float32), maxulp=1)
+
+
+# ------------------------------------------------- sparse Momentum / Adagrad (R-29)
+def test_momentum_closed_form_constant_gradient():
+    """k updates of one row with a constant gradient g: m_k = g (1 - mu^k) / (1 - mu) and
+    w_k = w_0 - lr g sum_{i<=k} (1 - mu^i) / (1 - mu) (geometric series)."""
+    mu, lr, g, k = 0.9, 0.05, np.array([0.3, -1.25, 2.0]), 12
+    w = np.array([[1.0, -2.0, 0.5]], np.float32)
+    m = np.zeros((1, 3), np.float32)
+    for _ in range(k):
+        w, m = oracle.scatter_opt("momentum", w, m, [0], g.reshape(1, 3), lr, mu)
+    m_k = g * (1 - mu ** k) / (1 - mu)
+    series = (k - mu * (1 - mu ** k) / (1 - mu)) / (1 - mu)
+    assert np.allclose(m[0], m_k, rtol=1e-5)
+    assert np.allclose(w[0], np.array([1.0, -2.0, 0.5]) - lr * g * series, rtol=1e-5, atol=1e-6)
+
+
+def test_momentum_zero_is_sgd_and_duplicates_summed_once():
+    rng = np.random.default_rng(3)
+    T0 = rng.standard_normal((20, 4)).astype(np.float32)
+    ids = np.array([3, 7, 3, 3, 19, 7])
+    g = rng.standard_normal((6, 4))
+    w_m, m = oracle.scatter_opt("momentum", T0, np.zeros_like(T0), ids, g, 0.1, 0.0)
+    w_s = oracle.scatter_add_sgd(T0, ids, g, 0.1)
+    assert np.array_equal(w_m, w_s)                       # mu = 0 is plain SGD
+    # one call with duplicates == one occurrence per id carrying the sum
+    uniq = np.array([3, 7, 19])
+    gs = np.stack([g[ids == u].sum(axis=0) for u in uniq])
+    w_u, m_u = oracle.scatter_opt("momentum", T0, np.zeros_like(T0), uniq, gs, 0.1, 0.0)
+    assert np.allclose(w_m, w_u, rtol=0, atol=1e-7) and np.allclose(m, m_u, rtol=0, atol=1e-7)
+    untouched = np.setdiff1d(np.arange(20), ids)
+    assert np.array_equal(w_m[untouched], T0[untouched]) and not m[untouched].any()
+
+
+def test_adagrad_closed_form_constant_gradient():
+    """k updates with a constant gradient g and accumulator start a0:
+    w_k = w_0 - lr g sum_{i<=k} 1 / sqrt(a0 + i g^2)."""
+    lr, a0, k = 0.1, 0.1, 9
+    g = np.array([0.5, -3.0, 0.01])
+    w = np.array([[0.25, 1.0, -1.0]], np.float32)
+    a = np.full((1, 3), a0, np.float32)
+    for _ in range(k):
+        w, a = oracle.scatter_opt("adagrad", w, a, [0], g.reshape(1, 3), lr)
+    i = np.arange(1, k + 1)[:, None]
+    want = np.array([0.25, 1.0, -1.0]) - lr * g * (1.0 / np.sqrt(a0 + i * g ** 2)).sum(axis=0)
+    assert np.allclose(a[0], a0 + k * g ** 2, rtol=1e-5)
+    assert np.allclose(w[0], want, rtol=1e-5, atol=1e-6)
+
+
+def test_adagrad_step_bounded_by_lr():
+    """|delta w| = lr |g| / sqrt(a + g^2) <= lr for a >= 0 (the update is scale-free)."""
+    rng = np.random.default_rng(4)
+    T0 = rng.standard_normal((50, 8)).astype(np.float32)
+    ids = rng.integers(0, 50, 200)
+    g = rng.standard_normal((200, 8)) * 100.0
+    w, a = oracle.scatter_opt("adagrad", T0, np.zeros_like(T0), ids, g, 0.01)
+    assert np.all(np.abs(w.astype(np.float64) - T0) <= 0.01 * (1 + 1e-6))
