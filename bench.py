@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--phase-steps", type=int, default=20, help="instrumented eager steps")
+    p.add_argument("--optimizer", default="sgd", choices=["sgd", "momentum", "adagrad"],
+                   help="sparse optimizer of the ScatterAdd step (1 GPU; the paper uses SGD)")
     p.add_argument("--route", default="p2p", choices=["p2p", "nccl"],
                    help="R > 1 transport: one-sided NVLink (symmetric memory) or NCCL a2a")
     return p.parse_args()
@@ -226,7 +228,7 @@ def main():
     dtype = TFS_BF16 if args.dtype == "bf16" else TFS_F32
     cfg = gstep.StepConfig(vocab=w.vocab, dim=d, tokens=B, num_sampled=S, lr=0.1,
                            seed=workloads.SAMPLER_SEED, operand_dtype=dtype,
-                           full_softmax=(S == 0), route=args.route)
+                           full_softmax=(S == 0), route=args.route, optimizer=args.optimizer)
     E, W, b = workloads.tables_device(w.vocab, d, R, rank, dev)
     st = gstep.ShardedStep(cfg, E, W, b, router)
     # 16 distinct pre-generated batches per rank, resident in HBM and in pinned host memory.
@@ -440,6 +442,7 @@ def main():
                        f"data-parallel x{R}", "l2": "flushed before every timed step "
                        "(256 MiB write outside the timed interval)",
                        "cuda_graph": use_graph, "batches": N_BATCHES,
+                       "optimizer": args.optimizer,
                        "route_slots": ({"transport": args.route,
                                         "cap_e": st.cap_e, "cap_w": st.cap_w,
                                         "calibrated_from": "distinct ids per owner of one "

@@ -253,6 +253,27 @@ int32_t tfs_scatter_add_sgd_planned(float* table, int64_t rows, int32_t dim, con
                                     float lr, float* table2, const float* grad2, void* ws,
                                     size_t ws_bytes, void* stream);
 
+/* ==== Sparse Momentum / Adagrad on the planned ScatterAdd path =====
+ * The paper's optimizers "as user-level code" on the same sparse update: per distinct id r,
+ * with g the sum of its gradient rows in the plan's fixed order (fp64), elementwise:
+ *   kind 0 SGD:      T = fl32(T - lr g)                         (= tfs_scatter_add_sgd_planned)
+ *   kind 1 Momentum: m = fl32(mu m + g);   T = fl32(T - lr m)
+ *   kind 2 Adagrad:  a = fl32(a + g g);    T = fl32(T - lr g / sqrt(a))
+ * slot: the fp32 m / a table, same shape as table (required for kinds 1, 2); slot2 likewise for
+ * the width-1 companion table2 (e.g. the bias).  Duplicates are summed before the single step
+ * (reading R-29: the synchronous step applies the combined sparse gradient once). */
+typedef struct {
+  int32_t kind;
+  float lr;
+  float mu;
+  float* slot;
+  float* slot2;
+} tfs_sparse_opt;
+int32_t tfs_scatter_opt_planned(float* table, int64_t rows, int32_t dim, const void* plan,
+                                size_t plan_bytes, int64_t n, const float* grad_rows,
+                                float* table2, const float* grad2, const tfs_sparse_opt* opt,
+                                void* ws, size_t ws_bytes, void* stream);
+
 /* ==== Fixed-capacity routing between R shards (R > 1; DESIGN.md §2 O3-O12) ======================
  * The requester-side halves of Part / route / Stitch and of sort-reduce / route, in a SLOT
  * layout that needs no host-visible counts (so a whole multi-GPU step can be a CUDA graph):

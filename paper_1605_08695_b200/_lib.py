@@ -47,6 +47,10 @@ class TfsError(RuntimeError):
         super().__init__(msg)
 
 
+class SparseOpt(ctypes.Structure):
+    _fields_ = [("kind", I32), ("lr", F32), ("mu", F32), ("slot", P), ("slot2", P)]
+
+
 class SsmArgs(ctypes.Structure):
     _fields_ = [
         ("B", I64), ("S", I64), ("dim", I32), ("operand_dtype", I32), ("flags", U32),
@@ -83,6 +87,8 @@ _SIGNATURES = {
     "tfs_scatter_plan": ([P, I64, I64, P, SZ, P, P], I32),
     "tfs_scatter_apply_workspace_bytes": ([I64, I32], SZ),
     "tfs_scatter_add_sgd_planned": ([P, I64, I32, P, SZ, I64, P, F32, P, P, P, SZ, P], I32),
+    "tfs_scatter_opt_planned": ([P, I64, I32, P, SZ, I64, P, P, P, ctypes.POINTER(SparseOpt), P,
+                                 SZ, P], I32),
     "tfs_route_plan_bytes": ([I64, I32], SZ),
     "tfs_route_plan": ([P, I64, I64, I32, I64, P, SZ, P, I64, P, P, P], I32),
     "tfs_route_unpack": ([P, SZ, I64, I64, I32, I64, P, I64, I32, P, P], I32),

@@ -439,10 +439,15 @@ struct SegJob {
   const float* rows2;         // optional [n] companion values
   int32_t dim;
   uint32_t invalid_key;       // keys >= invalid_key are skipped (bad ids)
-  // apply mode (ScatterAdd-SGD): table[key] -= lr * sum
+  // apply mode (ScatterAdd-SGD): table[key] -= lr * sum; or sparse Momentum / Adagrad with the
+  // fp32 slot tables slot / slot2 (opt 1 / 2, reading R-29)
   float* table;
   float* table2;
   float lr;
+  int opt;
+  double mu;
+  float* slot;
+  float* slot2;
   // write mode (sort_reduce): out_local[u], out_rows[u]; with slot_base (route_reduce) the row
   // of segment u (owner o = key / nloc) goes to slot o * cap + (u - slot_base[o]) instead
   int64_t* out_local;
@@ -519,6 +524,45 @@ __device__ __forceinline__ float4 to_f4(const D4& v) {
   return make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w);
 }
 
+// One optimizer step of an fp32 element given the fp64 sum g of its gradients (R-29); s is the
+// element's slot value (updated; unused for SGD).
+template <int OPT>
+__device__ __forceinline__ float opt_step(const SegJob& j, float w, double g, float& s) {
+  const double lr = (double)j.lr;
+  if (OPT == 1) {
+    s = (float)(j.mu * (double)s + g);
+    return (float)((double)w - lr * (double)s);
+  }
+  if (OPT == 2) {
+    s = (float)((double)s + g * g);
+    return (float)((double)w - lr * g / sqrt((double)s));
+  }
+  return (float)((double)w - lr * g);
+}
+// The step on four columns of row `key` (slot row at the same offset as the table row).
+template <int OPT>
+__device__ __forceinline__ float4 opt_step4(const SegJob& j, float4 w, const D4& g, int64_t key,
+                                            int c4) {
+  if (OPT == 0) {
+    float dummy = 0.f;
+    return make_float4(opt_step<0>(j, w.x, g.x, dummy), opt_step<0>(j, w.y, g.y, dummy),
+                       opt_step<0>(j, w.z, g.z, dummy), opt_step<0>(j, w.w, g.w, dummy));
+  }
+  float4* sp = reinterpret_cast<float4*>(j.slot + key * j.dim) + c4;
+  float4 sv = *sp;
+  w = make_float4(opt_step<OPT>(j, w.x, g.x, sv.x), opt_step<OPT>(j, w.y, g.y, sv.y),
+                  opt_step<OPT>(j, w.z, g.z, sv.z), opt_step<OPT>(j, w.w, g.w, sv.w));
+  *sp = sv;
+  return w;
+}
+// The companion (width-1) table's step with its slot2.
+template <int OPT>
+__device__ __forceinline__ void opt_step2(const SegJob& j, int64_t key, double g2) {
+  float s = OPT ? j.slot2[key] : 0.f;
+  j.table2[key] = opt_step<OPT>(j, j.table2[key], g2, s);
+  if (OPT) j.slot2[key] = s;
+}
+
 // Where a finished piece of one segment goes (warp-uniform decision).
 struct PieceDst {
   int kind;  // 0 whole segment, 1 head slot (started before the chunk), 2 tail slot
@@ -535,6 +579,7 @@ __device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_afte
 // inside the chunk -- are loaded at once; each segment's rows are added in sorted order in
 // fp64 and the segment is applied (T = fl32(T - lr * g)) or written directly.  Pieces of
 // segments that cross a chunk boundary go to partial slots and the segment to cross_list.
+template <int OPT>
 __global__ void __launch_bounds__(256, TFS_SEG_MINB) seg_chunk_vec4_kernel(SegJob j, int nslices) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -612,17 +657,9 @@ __global__ void __launch_bounds__(256, TFS_SEG_MINB) seg_chunk_vec4_kernel(SegJo
           }
         }
       } else {
-        if (col_ok) {
-          const double lr = (double)j.lr;
-          float4 w = t[r];
-          w.x = (float)((double)w.x - lr * acc.x);
-          w.y = (float)((double)w.y - lr * acc.y);
-          w.z = (float)((double)w.z - lr * acc.z);
-          w.w = (float)((double)w.w - lr * acc.w);
-          *((float4*)(j.table + (int64_t)kr * j.dim) + c4) = w;
-        }
-        if (j.table2 && lane == 0 && slice == 0)
-          j.table2[kr] = (float)((double)j.table2[kr] - (double)j.lr * acc2);
+        if (col_ok)
+          *((float4*)(j.table + (int64_t)kr * j.dim) + c4) = opt_step4<OPT>(j, t[r], acc, kr, c4);
+        if (j.table2 && lane == 0 && slice == 0) opt_step2<OPT>(j, kr, acc2);
       }
     } else {
       const int64_t slot = starts_before ? 2 * chunk : 2 * chunk + 1;
@@ -648,6 +685,7 @@ __global__ void __launch_bounds__(256, TFS_SEG_MINB) seg_chunk_vec4_kernel(SegJo
 }
 
 // A segment whose pieces are all summed: T[key] = fl32(T - lr * g) (apply) or written out.
+template <int OPT>
 __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int c4, const D4& acc,
                                                 bool col0, double acc2) {
   const uint32_t key = j.keys[j.seg_start[s]];
@@ -662,14 +700,8 @@ __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int
     }
   } else {
     float4* tp = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c4;
-    float4 w = *tp;
-    const double lr = (double)j.lr;
-    w.x = (float)((double)w.x - lr * acc.x);
-    w.y = (float)((double)w.y - lr * acc.y);
-    w.z = (float)((double)w.z - lr * acc.z);
-    w.w = (float)((double)w.w - lr * acc.w);
-    *tp = w;
-    if (col0 && j.table2) j.table2[key] = (float)((double)j.table2[key] - lr * acc2);
+    *tp = opt_step4<OPT>(j, *tp, acc, key, c4);
+    if (col0 && j.table2) opt_step2<OPT>(j, key, acc2);
   }
 }
 
@@ -739,6 +771,7 @@ __global__ void __launch_bounds__(256) seg_cross_a_vec4_kernel(SegJob j, int64_t
 
 // Level B, one thread per (segment crossing a chunk boundary, float4 column): its run sums
 // added in block order, then T[key] = fl32(T - lr * sum) (apply) or written out.
+template <int OPT>
 __global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
   const uint32_t ncross = *j.cross_count;
   const int n4 = j.dim >> 2;
@@ -759,7 +792,7 @@ __global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
       add4(acc, reinterpret_cast<const D4*>(j.part + slot * j.dim)[c4]);
       if (col0) acc2 += j.part2[slot];
     }
-    seg_finish_vec4(j, s, c4, acc, c4 == 0, acc2);
+    seg_finish_vec4<OPT>(j, s, c4, acc, c4 == 0, acc2);
   }
 }
 
@@ -830,7 +863,7 @@ __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
 // One thread per (segment, column group): finish segments that cross chunk boundaries (their
 // chunk partials added in chunk order) and, in apply mode, T[key] = fl32(T - lr * sum) for
 // every segment; in write mode, out_local for every segment.  Fully parallel, coalesced.
-template <bool VEC>
+template <bool VEC, int OPT>
 __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
   const int64_t U = *j.num_unique;
   const int cols = VEC ? (j.dim >> 2) : j.dim;
@@ -864,13 +897,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
         reinterpret_cast<float4*>(op.row)[c] = to_f4(acc);
       } else {
         float4* t = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c;
-        float4 w = *t;
-        const double lr = (double)j.lr;
-        w.x = (float)((double)w.x - lr * acc.x);
-        w.y = (float)((double)w.y - lr * acc.y);
-        w.z = (float)((double)w.z - lr * acc.z);
-        w.w = (float)((double)w.w - lr * acc.w);
-        *t = w;
+        *t = opt_step4<OPT>(j, *t, acc, key, c);
       }
     } else {
       double acc;
@@ -885,7 +912,9 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
         op.row[c] = (float)acc;
       } else {
         float* t = j.table + (int64_t)key * j.dim + c;
-        *t = (float)((double)*t - (double)j.lr * acc);
+        float sv = OPT ? j.slot[(int64_t)key * j.dim + c] : 0.f;
+        *t = opt_step<OPT>(j, *t, acc, sv);
+        if (OPT) j.slot[(int64_t)key * j.dim + c] = sv;
       }
     }
     if (c == 0 && j.rows2) {
@@ -899,7 +928,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
       if (write_mode) {
         if (op.r2) *op.r2 = (float)acc2;
       } else if (j.table2) {
-        j.table2[key] = (float)((double)j.table2[key] - (double)j.lr * acc2);
+        opt_step2<OPT>(j, key, acc2);
       }
     }
   }
@@ -1210,7 +1239,9 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
     TFS_CUDA_TRY(cudaMemsetAsync(j.cross_count, 0, sizeof(uint32_t), st));
     const int nslices = (int)cdiv(j.dim >> 2, 32);
     const int vgrid = (int)std::max<int64_t>(1, cdiv(nchunks * nslices, 8));
-    seg_chunk_vec4_kernel<<<vgrid, 256, 0, st>>>(j, nslices);
+    auto chunk_k = j.opt == 1 ? seg_chunk_vec4_kernel<1>
+                              : (j.opt == 2 ? seg_chunk_vec4_kernel<2> : seg_chunk_vec4_kernel<0>);
+    chunk_k<<<vgrid, 256, 0, st>>>(j, nslices);
     launched();
     const int64_t n4 = j.dim >> 2;
     const int64_t awork = cdiv(nchunks, kBlk) * n4;
@@ -1219,14 +1250,18 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
     launched();
     const int64_t bwork = (nchunks + 1) * n4;  // crossing segments <= chunks
     const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(bwork, 256), 4 * num_sms()));
-    seg_cross_b_vec4_kernel<<<bgrid, 256, 0, st>>>(j);
+    auto cross_k = j.opt == 1 ? seg_cross_b_vec4_kernel<1>
+                              : (j.opt == 2 ? seg_cross_b_vec4_kernel<2> : seg_cross_b_vec4_kernel<0>);
+    cross_k<<<bgrid, 256, 0, st>>>(j);
     launched();
   } else {
     seg_chunk_scalar_kernel<<<grid, 256, 0, st>>>(j);
     launched();
     const int64_t work = n * j.dim;  // U <= n
     const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, 256), 16 * num_sms()));
-    seg_apply_kernel<false><<<agrid, 256, 0, st>>>(j);
+    auto apply_k = j.opt == 1 ? seg_apply_kernel<false, 1>
+                              : (j.opt == 2 ? seg_apply_kernel<false, 2> : seg_apply_kernel<false, 0>);
+    apply_k<<<agrid, 256, 0, st>>>(j);
     launched();
   }
   TFS_LAUNCH_CHECK();
@@ -1749,6 +1784,42 @@ extern "C" int32_t tfs_scatter_add_sgd_planned_slots(
   j.row_cap = cap;
   j.row_stride = grad_stride;
   j.row2_stride = grad2_stride;
+  return run_segments(j, n, as_stream(stream));
+}
+
+extern "C" int32_t tfs_scatter_opt_planned(float* table, int64_t rows, int32_t dim,
+                                           const void* plan, size_t plan_bytes, int64_t n,
+                                           const float* grad_rows, float* table2,
+                                           const float* grad2, const tfs_sparse_opt* opt,
+                                           void* ws, size_t ws_bytes, void* stream) {
+  TFS_REQUIRE(opt != nullptr && opt->kind >= 0 && opt->kind <= 2);
+  TFS_REQUIRE(n >= 0 && dim >= 1 && rows >= 0 && rows < (1ll << 31) - 1 && n < (1ll << 31));
+  TFS_REQUIRE((table2 == nullptr) == (grad2 == nullptr));
+  TFS_REQUIRE(opt->kind == 0 || opt->slot != nullptr);
+  TFS_REQUIRE(opt->kind == 0 || table2 == nullptr || opt->slot2 != nullptr);
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(table && plan && grad_rows);
+  TFS_REQUIRE(dim % 4 != 0 || (((uintptr_t)table & 15) == 0 &&
+                               (opt->kind == 0 || ((uintptr_t)opt->slot & 15) == 0)));
+  TFS_SUPPORTED();
+  SegScratch s;
+  if (plan_bytes < plan_scratch_bytes(n, &s, const_cast<void*>(plan), plan_bytes))
+    return TFS_ERR_WORKSPACE_TOO_SMALL;
+  if (ws_bytes < apply_scratch_bytes(n, dim, &s, ws, ws_bytes)) return TFS_ERR_WORKSPACE_TOO_SMALL;
+  SegJob j{};
+  bind(j, s, n);
+  j.rows = grad_rows;
+  j.rows2 = grad2;
+  j.dim = dim;
+  j.invalid_key = (uint32_t)rows;
+  j.table = table;
+  j.table2 = table2;
+  j.lr = opt->lr;
+  j.opt = opt->kind;
+  j.mu = (double)opt->mu;
+  j.slot = opt->slot;
+  j.slot2 = opt->slot2;
+  j.nloc = rows + 1;
   return run_segments(j, n, as_stream(stream));
 }
 

@@ -232,6 +232,19 @@ class ScatterPlan:
               "tfs_scatter_plan")
         return self
 
+    def apply_opt(self, kind: str, table, grad, lr: float, slot, mu: float = 0.0, table2=None,
+                  grad2=None, slot2=None):
+        """Sparse Momentum ("momentum") / Adagrad ("adagrad") / "sgd" with the fp32 slot
+        tables (tfs_scatter_opt_planned)."""
+        from ._lib import SparseOpt
+        k = {"sgd": 0, "momentum": 1, "adagrad": 2}[kind]
+        o = SparseOpt(k, float(lr), float(mu), _p(slot), _p(slot2))
+        check(_lib.lib().tfs_scatter_opt_planned(
+            _p(table), self.rows, self.dim, _p(self.plan), self.plan.numel(), self.n, _p(grad),
+            _p(table2), _p(grad2), ctypes.byref(o), _p(self.ws), self.ws.numel(), _stream()),
+            "tfs_scatter_opt_planned")
+        return table
+
     def apply(self, table, grad, lr: float, table2=None, grad2=None):
         assert table.shape[0] == self.rows
         check(_lib.lib().tfs_scatter_add_sgd_planned(

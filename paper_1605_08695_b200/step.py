@@ -53,6 +53,11 @@ class StepConfig:
     # stores into the owners' inboxes, device barriers; tables and inboxes in symmetric memory)
     # or "nccl" = equal-split all-to-alls of slot regions.
     route: str = "p2p"
+    # sparse optimizer of the ScatterAdd step: "sgd" (the paper's
+    # experiments), "momentum" (mu) or "adagrad" (accumulators start at adagrad_init); R = 1
+    optimizer: str = "sgd"
+    momentum: float = 0.9
+    adagrad_init: float = 0.1
 
 
 class Router:
@@ -168,6 +173,14 @@ class ShardedStep:
         self.ssm_out.update({"dw_true": self.dw[:B], "db_true": self.db[:B], "dw_s": self.dw[B:],
                              "db_s": self.db[B:]})
         self.ws_ssm = ops.ssm_workspace(B, S, d, cfg.operand_dtype, dev, V)
+        if cfg.optimizer not in ("sgd", "momentum", "adagrad"):
+            raise ValueError(f"unknown optimizer {cfg.optimizer!r}")
+        if cfg.optimizer != "sgd" and R != 1:
+            raise ValueError("sparse Momentum / Adagrad are wired into the R = 1 step")
+        self.slots = None
+        if cfg.optimizer != "sgd":  # fp32 slot tables shaped like E, W, b
+            init = 0.0 if cfg.optimizer == "momentum" else cfg.adagrad_init
+            self.slots = tuple(torch.full_like(t, init) for t in (E, W, b))
         if R == 1:
             self.plan_e = ops.ScatterPlan(B, E.shape[0], d, dev)
             self.plan_w = ops.ScatterPlan(B + S, W.shape[0], d, dev)
@@ -271,6 +284,23 @@ class ShardedStep:
                             operand_dtype=self.cfg.operand_dtype, vocab=self.cfg.vocab,
                             out=self.ssm_out, ws=self.ws_ssm, events=self.ssm_events)
 
+    def _apply_e(self):
+        cfg = self.cfg
+        if self.slots is None:
+            self.plan_e.apply(self.E, self.ssm_out["dh"], cfg.lr)
+        else:
+            self.plan_e.apply_opt(cfg.optimizer, self.E, self.ssm_out["dh"], cfg.lr, self.slots[0],
+                                  cfg.momentum)
+
+    def _apply_w(self):
+        cfg = self.cfg
+        if self.slots is None:
+            self.plan_w.apply(self.W, self.dw, cfg.lr, table2=self.b, grad2=self.db)
+        else:
+            self.plan_w.apply_opt(cfg.optimizer, self.W, self.dw, cfg.lr, self.slots[1],
+                                  cfg.momentum, table2=self.b, grad2=self.db,
+                                  slot2=self.slots[2])
+
     def _ph(self, name: str):
         """Phase marker: with ``self.phase_events`` set (bench instrumentation, eager only) the
         phase is bracketed by CUDA events on the current stream, preceded by a short device
@@ -315,9 +345,9 @@ class ShardedStep:
         ev["ssm"].record(main)
         with torch.cuda.stream(side):
             side.wait_event(ev["ssm"])
-            self.plan_e.apply(self.E, self.ssm_out["dh"], self.cfg.lr)
+            self._apply_e()
         main.wait_event(ev["plan_w"])
-        self.plan_w.apply(self.W, self.dw, self.cfg.lr, table2=self.b, grad2=self.db)
+        self._apply_w()
         main.wait_stream(side)
 
     def _local_step_serial(self, step: int | None):
@@ -336,8 +366,8 @@ class ShardedStep:
             self.plan_e.build(self.x, err=self.err)
             self.plan_w.build(self.qw, err=self.err)
         with self._ph("scatter_sgd"):
-            self.plan_e.apply(self.E, self.ssm_out["dh"], self.cfg.lr)
-            self.plan_w.apply(self.W, self.dw, self.cfg.lr, table2=self.b, grad2=self.db)
+            self._apply_e()
+            self._apply_w()
 
     def _dist_step_p2p(self, step: int | None):
         """R > 1 over NVLink, one-sided: three device barriers, no collectives, no host sync.
@@ -470,6 +500,7 @@ class ShardedStep:
         self.step_dev, advanced by one inside the graph) into a CUDA graph.  Any R: the R > 1
         step has no host synchronisation (fixed-capacity all-to-alls over NCCL)."""
         saved = (self.E.clone(), self.W.clone(), self.b.clone())
+        saved_slots = None if self.slots is None else tuple(t.clone() for t in self.slots)
         self.step_dev.fill_(first_step)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
@@ -480,7 +511,10 @@ class ShardedStep:
         torch.cuda.synchronize()
         for dst, src in zip((self.E, self.W, self.b), saved):  # undo the warm-up update
             dst.copy_(src)
-        del saved
+        if saved_slots is not None:
+            for dst, src in zip(self.slots, saved_slots):
+                dst.copy_(src)
+        del saved, saved_slots
         self.step_dev.fill_(first_step)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph(keep_graph=True)  # raw graph kept for inspection

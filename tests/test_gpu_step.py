@@ -159,3 +159,46 @@ def test_step_config_X_sampled_outputs(name):
         assert rel(Wg - W[s[cols]], -lr * o["dw_s"]) <= 2e-3
         bg = st.b[torch.from_numpy(s[cols]).to(DEV)].cpu().numpy()
         assert rel(bg - b[s[cols]], -lr * o["db_s"]) <= 2e-3
+
+
+@pytest.mark.parametrize("kind", ["momentum", "adagrad"])
+def test_step_sparse_optimizer(kind):
+    """The R = 1 step with sparse Momentum / Adagrad: the oracle step's
+    gradients (config L, fp32 operands) fed to the oracle's optimizer give the GPU tables and
+    slots; two steps so the slots carry state."""
+    E, W, b, x, y, cfg, st = _setup("L", TFS_F32, lr=0.5)
+    cfg2 = gstep.StepConfig(**{**cfg.__dict__, "optimizer": kind})
+    st = gstep.ShardedStep(cfg2, torch.from_numpy(E).to(DEV), torch.from_numpy(W).to(DEV),
+                           torch.from_numpy(b).to(DEV))
+    init = 0.0 if kind == "momentum" else cfg2.adagrad_init
+    Eo, Wo, bo = E.copy(), W.copy(), b.copy()
+    sE, sW, sb = (np.full_like(t, init) for t in (E, W, b))
+    for step in range(2):
+        ocfg = ostep.StepConfig(vocab=cfg.vocab, dim=cfg.dim, num_sampled=cfg.num_sampled,
+                                num_shards=1, lr=cfg.lr, seed=cfg.seed, step=step, bf16=False)
+        _, _, _, tr = ostep.step(Eo, Wo, bo, [x], [y], ocfg)   # gradients at this state
+        t = tr[0]
+        qw = np.concatenate([y, t.sampled])
+        Eo, sE = oracle.scatter_opt(kind, Eo, sE, x, t.ssm["dh"], cfg.lr, cfg2.momentum)
+        Wo, sW = oracle.scatter_opt(kind, Wo, sW, qw,
+                                    np.concatenate([t.ssm["dw_true"], t.ssm["dw_s"]]),
+                                    cfg.lr, cfg2.momentum)
+        bo, sb = oracle.scatter_opt(kind, bo, sb, qw,
+                                    np.concatenate([t.ssm["db_true"], t.ssm["db_s"]]),
+                                    cfg.lr, cfg2.momentum)
+        st.run(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), step)
+        torch.cuda.synchronize()
+        st.err.check("step")
+    for name, T0, Tg, To in (("E", E, st.E, Eo), ("W", W, st.W, Wo), ("b", b, st.b, bo),
+                             ("slotE", np.full_like(E, init), st.slots[0], sE),
+                             ("slotW", np.full_like(W, init), st.slots[1], sW)):
+        g = Tg.cpu().numpy()
+        touched = np.nonzero(np.any((To != T0).reshape(T0.shape[0], -1), axis=1))[0]
+        if name.startswith("slot") and init != 0.0:
+            # Adagrad accumulators move by g^2 << a0: compare the values (their deltas are
+            # within a few fp32 ulps of a0, where the relative difference is meaningless)
+            assert rel(g[touched], To[touched]) <= 1e-6, name
+        else:
+            assert rel(g[touched] - T0[touched], To[touched] - T0[touched]) <= 1e-5, name
+        untouched = np.setdiff1d(np.arange(T0.shape[0]), touched)
+        assert np.array_equal(g[untouched], T0[untouched]), name
