@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--phase-steps", type=int, default=20, help="instrumented eager steps")
+    p.add_argument("--null-step", action="store_true",
+                   help="SURVEY 8f #4 / P:1048-1055: step time of 32 random lookups per worker "
+                        "from a 1 GB and a 16 GB embedding sharded over the GPUs")
     p.add_argument("--optimizer", default="sgd", choices=["sgd", "momentum", "adagrad"],
                    help="sparse optimizer of the ScatterAdd step (1 GPU; the paper uses SGD)")
     p.add_argument("--route", default="p2p", choices=["p2p", "nccl"],
@@ -199,6 +202,72 @@ def graph_kernel_nodes(graph):
         return None
 
 
+def run_null_step(args, world, rank, dev, router):
+    """The paper's sparse null step: "Each worker reads 32 randomly selected
+    entries from a large embedding matrix containing 1 GB or 16 GB of data ... step times do
+    not vary with the size of the embedding ... 5 to 20 ms".  Here: fp32 rows of 512, the
+    matrix sharded by id mod R over the GPUs; one step = 32 fresh random ids per worker and
+    their rows gathered (R = 1: tfs_gather; R > 1: tfs_gather_peers, one-sided NVLink pulls
+    from symmetric-memory shards behind a device barrier).  Reported: median step time."""
+    import torch
+    from paper_1605_08695_b200 import ops
+    d, n_ids, steps = 512, 32, max(args.steps, 50)
+    out = {}
+    for gb in (1, 16):
+        V = gb * (1 << 30) // (4 * d)
+        rows = -(-V // world)
+        if world > 1:
+            import torch.distributed._symmetric_memory as symm_mem
+            shard = symm_mem.empty((rows, d), dtype=torch.float32, device=dev)
+            hdl = symm_mem.rendezvous(shard, router.group_name)
+            tab = torch.tensor(list(hdl.buffer_ptrs), dtype=torch.int64, device=dev)
+        else:
+            shard = torch.empty((rows, d), dtype=torch.float32, device=dev)
+        shard.uniform_(-0.5, 0.5)
+        gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+        ids = torch.empty(n_ids, dtype=torch.int64, device=dev)
+        res = torch.empty((n_ids, d), dtype=torch.float32, device=dev)
+        err = ops.ErrorSlot(dev)
+        times = []
+        for i in range(args.warmup + steps):
+            ids.random_(0, V, generator=gen)
+            torch.cuda.synchronize()
+            if world > 1:
+                hdl.barrier(channel=0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if world > 1:
+                ops.gather_peers(tab, rows, d, ids, V, world, res, err=err)
+                hdl.barrier(channel=1)
+            else:
+                ops.gather(shard, ids, out=res, err=err)
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                times.append(e0.elapsed_time(e1))
+        err.check("null step")
+        med = torch.tensor([float(np.median(times))], device=dev, dtype=torch.float64)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(med, op=dist.ReduceOp.MAX)
+        out[f"{gb}GB"] = {"median_ms": float(med.item()), "rows": V,
+                          "p10_ms": float(np.percentile(times, 10)),
+                          "p90_ms": float(np.percentile(times, 90))}
+        del shard
+        torch.cuda.empty_cache()
+    if rank == 0:
+        print(json.dumps({"metric": "sparse null step time (32 random embedding lookups per "
+                                    "worker, P:1048-1055)", "unit": "ms", "n_gpus": world,
+                          "higher_is_better": False, "steps": steps, "warmup": args.warmup,
+                          "data": "synthetic", "config": {"workload": "null-step", "dim": d,
+                          "lookups_per_worker": n_ids, "transport": "p2p" if world > 1
+                          else "local"}, "paper_ms": [5, 20], "results": out}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -220,6 +289,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         router = gstep.Router()
+    if args.null_step:
+        run_null_step(args, world, rank, dev, router)
+        return
     w = workloads.WORKLOADS[args.workload]
     R = world
     B = w.tokens_per_replica(R)
