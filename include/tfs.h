@@ -165,7 +165,15 @@ int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int32_t num_sam
  * (uint16 bits, same shapes) that are already the RNE roundings of the fp32 values -- e.g.
  * produced by tfs_gather with out_dtype TFS_BF16 -- so the call skips its conversion pass;
  * results are identical to passing the fp32 arrays. */
-enum { TFS_SUBTRACT_LOG_Q = 1u, TFS_REMOVE_ACCIDENTAL_HITS = 2u, TFS_BF16_OPERANDS = 4u };
+/* TFS_LABEL_IN_CANDIDATES (tfs_ssm_partial_stats / tfs_ssm_backward_from_lse only; excludes
+ * TFS_REMOVE_ACCIDENTAL_HITS): the candidates are a slice of the full vocabulary, and a token
+ * whose label is among them keeps that logit -- see the sharded full softmax below. */
+enum {
+  TFS_SUBTRACT_LOG_Q = 1u,
+  TFS_REMOVE_ACCIDENTAL_HITS = 2u,
+  TFS_BF16_OPERANDS = 4u,
+  TFS_LABEL_IN_CANDIDATES = 8u
+};
 typedef struct {
   int64_t B, S;
   int32_t dim;
@@ -200,6 +208,53 @@ size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operan
                                int64_t vocab);
 int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, size_t ws_bytes,
                                     void* stream);
+
+/* ==== Vocabulary-sharded full softmax: the two local halves =========
+ * "the weights are sharded across several tasks, and the multiplication and gradient
+ * calculation are colocated with the shards".  Shard r of R holds the classes
+ * v = j R + r (j < S) as candidates w_s / b_s / sampled; the B rows of h are the tokens of ALL
+ * replicas (an all-gather).  Per shard, over its candidates only (no true-class term):
+ *   tfs_ssm_partial_stats:  row_stats[t] = (m_t, s_t) with m_t = max_j Z_tj log2(e) and
+ *     s_t = sum_j 2^(Z_tj log2(e) - m_t)  (log2 domain; float pairs [B x 2], 8-byte aligned;
+ *     m = -inf, s = 0 when every logit is excluded).  The caller combines the R shards' pairs
+ *     into lse_t = ln 2 (M + log2 sum_r s_r 2^(m_r - M)), M = max_r m_r (tfs_lse_combine_peers).
+ *   tfs_ssm_backward_from_lse (a->lse = that global lse, input):
+ *     G_tj = c (e^{Z_tj - lse_t} - [s_j == y_t]);  dh = G W_s (this shard's PARTIAL of dh,
+ *     summed over shards by the caller); dw_s = G^T h;  db_s = column sums of G;
+ *     z_label[t] = Z_t,j* (natural units) for the tokens whose label s_j* is a candidate here
+ *     (other entries untouched).
+ * With TFS_LABEL_IN_CANDIDATES (labels[B], vocab > 0 required) a label among the candidates
+ * is part of the softmax (the full-softmax gradient p - onehot); without it, no label is used.
+ * Both calls take the same args and workspace (tfs_ssm_workspace_bytes(B, S, dim, TFS_BF16,
+ * vocab), candidate map zero before partial_stats) and must be paired in stream order: the
+ * backward reads the operand copies and the map the stats call left in the workspace and
+ * leaves the map zero.  Tensor-core path only: operand_dtype TFS_BF16, dim % 64 == 0, B, S >= 1;
+ * loss and loss_sum must be NULL; w_true / b_true / dw_true / db_true are not used. */
+int32_t tfs_ssm_partial_stats(const tfs_ssm_args* a, float* row_stats, void* ws,
+                              size_t ws_bytes, void* stream);
+int32_t tfs_ssm_backward_from_lse(const tfs_ssm_args* a, float* z_label, void* ws,
+                                  size_t ws_bytes, void* stream);
+/* Cross-shard pieces of the sharded full softmax, over peer memory (P2P loads of every
+ * shard's buffer -- pointers from a symmetric allocation; R >= 1; deterministic: shards are
+ * combined in rank order 0..R-1).
+ * tfs_lse_combine_peers: lse[t] = ln 2 (M + log2 sum_r s_r 2^(m_r - M)) over
+ *   stats_tab[r][t] = (m_r, s_r) float pairs, t < n.
+ * tfs_reduce_peers: out[i] = sum_r src_tab[r][offset + i], i < n (the reduce-scatter of dh:
+ *   each rank pulls its own tokens' partials).  16-byte aligned when n % 4 == 0 for speed.
+ * tfs_label_loss_sum: out[0] = c sum over t < n with labels[t] mod R == shard of
+ *   (lse[t] - z_label[t]), in increasing t (one block). */
+int32_t tfs_lse_combine_peers(const float* const* stats_tab, int32_t R, int64_t n, float* lse,
+                              void* stream);
+int32_t tfs_reduce_peers(const float* const* src_tab, int32_t R, int64_t offset, int64_t n,
+                         float* out, void* stream);
+int32_t tfs_label_loss_sum(const float* lse, const float* z_label, const int64_t* labels,
+                           int64_t n, int32_t R, int32_t shard, float c, float* out,
+                           void* stream);
+/* Dense SGD with a bf16 shadow: table[i] -= lr * grad[i] (fp32, i < n) and, if shadow is not
+ * NULL, shadow[i] = bf16(table[i]) (RNE) -- the updated rows' operand copy for the next
+ * step's tensor-core GEMMs.  n % 4 == 0, 16-byte aligned pointers (8 for the shadow). */
+int32_t tfs_dense_sgd(float* table, const float* grad, int64_t n, float lr, void* shadow,
+                      void* stream);
 
 /* ==== Sort-reduce of a sparse gradient (R-16) =======================================
  * The gradient of Gather is a sparse (ids, rows) pair; before it is routed to the owner

@@ -23,6 +23,7 @@ TFS_ERR_UNSUPPORTED = 7
 TFS_ERR_SAMPLER_EXHAUSTED = 8
 TFS_ERR_CAPACITY = 9
 TFS_BF16_OPERANDS = 4
+TFS_LABEL_IN_CANDIDATES = 8
 TFS_F32, TFS_BF16 = 0, 1
 TFS_SUBTRACT_LOG_Q, TFS_REMOVE_ACCIDENTAL_HITS = 1, 2
 
@@ -79,6 +80,12 @@ _SIGNATURES = {
                                 SZ, P, P], I32),
     "tfs_ssm_workspace_bytes": ([I64, I64, I32, I32, I64], SZ),
     "tfs_sampled_softmax_fwd_bwd": ([ctypes.POINTER(SsmArgs), P, SZ, P], I32),
+    "tfs_ssm_partial_stats": ([ctypes.POINTER(SsmArgs), P, P, SZ, P], I32),
+    "tfs_ssm_backward_from_lse": ([ctypes.POINTER(SsmArgs), P, P, SZ, P], I32),
+    "tfs_lse_combine_peers": ([P, I32, I64, P, P], I32),
+    "tfs_reduce_peers": ([P, I32, I64, I64, P, P], I32),
+    "tfs_label_loss_sum": ([P, P, P, I64, I32, I32, F32, P, P], I32),
+    "tfs_dense_sgd": ([P, P, I64, F32, P, P], I32),
     "tfs_sort_reduce_workspace_bytes": ([I64, I32], SZ),
     "tfs_sort_reduce": ([P, I64, I64, I32, P, I32, P, P, P, P, P, P, P, SZ, P, P], I32),
     "tfs_scatter_add_sgd_workspace_bytes": ([I64, I32], SZ),

@@ -718,83 +718,90 @@ static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   return TFS_OK;
 }
 
-static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
+// Optional instrumentation events (tfs_ssm_args::timing_events).
+static void mark(const tfs_ssm_args* a, int i, cudaStream_t st) {
+  if (a->timing_events != nullptr && a->timing_events[i] != nullptr)
+    cudaEventRecord(static_cast<cudaEvent_t>(a->timing_events[i]), st);
+}
+
+// Everything the phases of the tensor-core path share: workspace slices, epilogue parameters,
+// the STATS / GRAD tile width.
+struct Bf16Plan {
   Bf16Ws w;
-  ws_layout(a->B, a->S, a->dim, TFS_BF16, a->vocab, nullptr, &w, ws);
-  const int64_t B = a->B, S = a->S;
-  const int32_t d = a->dim;
-  const int hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) ? 1 : 0;
-  const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
-  const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
-  auto mark = [&](int i) {  // optional instrumentation events (tfs_ssm_args::timing_events)
-    if (a->timing_events != nullptr && a->timing_events[i] != nullptr)
-      cudaEventRecord(static_cast<cudaEvent_t>(a->timing_events[i]), st);
-  };
-  mark(0);
-  const int bn = S > 0 ? umma::pick_bn((int)B, (int)S) : umma::BN;  // STATS / GRAD tile width
-  const int num_n = (int)cdiv(S, bn);
-  const bool bin = (a->flags & TFS_BF16_OPERANDS) != 0;  // h, w_true, w_s given in bf16
+  umma::EpiParams ep;
+  int bn, num_n;
+  bool bin;
+};
 
-  // Operands in bf16 (row-major; every GEMM reads them K- or MN-major as it needs), column
-  // parameters and the candidate map: one launch.
-  const int64_t V = hits ? a->vocab : 0;
-  int2* cmap = V > 0 ? reinterpret_cast<int2*>(ws) : nullptr;
-  if (bin) {  // already rounded by the producer (e.g. a bf16 Gather): no conversion pass
-    w.hb = static_cast<uint16_t*>(const_cast<void*>(static_cast<const void*>(a->h)));
-    w.wsb = static_cast<uint16_t*>(const_cast<void*>(static_cast<const void*>(a->w_s)));
+static void bf16_plan(const tfs_ssm_args* a, void* ws, Bf16Plan* p) {
+  ws_layout(a->B, a->S, a->dim, TFS_BF16, a->vocab, nullptr, &p->w, ws);
+  const bool hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) != 0;
+  const bool label_in = (a->flags & TFS_LABEL_IN_CANDIDATES) != 0;
+  p->bn = a->S > 0 ? umma::pick_bn((int)a->B, (int)a->S) : umma::BN;
+  p->num_n = (int)cdiv(a->S, p->bn);
+  p->bin = (a->flags & TFS_BF16_OPERANDS) != 0;  // h, w_true, w_s given in bf16
+  if (p->bin) {  // already rounded by the producer (e.g. a bf16 Gather): no conversion pass
+    p->w.hb = static_cast<uint16_t*>(const_cast<void*>(static_cast<const void*>(a->h)));
+    p->w.wsb = static_cast<uint16_t*>(const_cast<void*>(static_cast<const void*>(a->w_s)));
   }
-  const int64_t nconv = bin ? 0 : (B + S) * d / 4;
-  prep_kernel<<<grid1d((nconv + w.Spad) / 4), 256, 0, st>>>(
-      a->h, bin ? 0 : B * d / 4, a->w_s, bin ? 0 : S * d / 4, w.hb, w.wsb, a->b_s, le_s,
-      a->sampled, S, w.Spad, cmap, V, w.cb, w.sid);
-  launched();
-  TFS_LAUNCH_CHECK();
-  mark(1);
-
-  using umma::Operand;
-  umma::EpiParams ep{};
-  ep.cb = w.cb;
-  ep.sid = w.sid;
-  ep.labels = hits ? a->labels : nullptr;
-  ep.cmap = cmap;
+  const int64_t V = (hits || label_in) ? a->vocab : 0;
+  umma::EpiParams& ep = p->ep;
+  ep = umma::EpiParams{};
+  ep.cb = p->w.cb;
+  ep.sid = p->w.sid;
+  ep.labels = (hits || label_in) ? a->labels : nullptr;
+  ep.cmap = V > 0 ? reinterpret_cast<int2*>(ws) : nullptr;
   ep.vocab = V;
-  ep.S_pad = (int)w.Spad;
-  int32_t rc;
-  const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
-  if (S > 0) {  // pass 1: per-row (max, sum 2^x) of each half tile, log2 domain
-    ep.stats = w.stats;
-    ep.nparts = 2 * num_n;
-    rc = umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)B, (int)S, d, bn, ep, nullptr, 0,
-                                    st);
-    if (rc != TFS_OK) return rc;
-  }
-  mark(2);
-  auto combine = bin ? bf16_combine_kernel<true> : bf16_combine_kernel<false>;
-  combine<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(B, d, a->h, a->w_true, a->b_true, le_t, w.stats,
-                                                2 * num_n, a->grad_scale, a->loss, a->lse,
-                                                a->dw_true, a->db_true);
-  launched();
-  TFS_LAUNCH_CHECK();
-  mark(3);
-  if (S == 0) {  // no candidates: dh = g * bf16(w_true)
-    auto fin = bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
-    fin<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true, a->w_true, a->dh);
-    launched();
-    TFS_LAUNCH_CHECK();
-    return TFS_OK;
-  }
-  // pass 2: G = c exp(Z - lse) -> bf16 G
+  ep.S_pad = (int)p->w.Spad;
+  ep.stats = p->w.stats;
+  ep.nparts = 2 * p->num_n;
   ep.lse = a->lse;
   ep.c = a->grad_scale;
-  rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, bn, ep, w.G, w.Sp,
-                                  st);
-  if (rc != TFS_OK) return rc;
-  mark(4);
-  // db_s = column sums of G
-  g_colsum_kernel<<<(unsigned)(cdiv(S, kColsumChunks * 8) + (a->loss_sum ? 1 : 0)), 256, 0, st>>>(
-      w.G, B, S, w.Sp, a->db_s, a->sampled, cmap, V, a->loss, a->grad_scale, a->loss_sum);
+  ep.label_in = label_in ? 1 : 0;
+}
+
+// Operands in bf16 (row-major; every GEMM reads them K- or MN-major as it needs), column
+// parameters and the candidate map: one launch.
+static int32_t bf16_prep(const tfs_ssm_args* a, const Bf16Plan& p, cudaStream_t st) {
+  const int64_t B = a->B, S = a->S;
+  const int32_t d = a->dim;
+  const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
+  const int64_t nconv = p.bin ? 0 : (B + S) * d / 4;
+  prep_kernel<<<grid1d((nconv + p.w.Spad) / 4), 256, 0, st>>>(
+      a->h, p.bin ? 0 : B * d / 4, a->w_s, p.bin ? 0 : S * d / 4, p.w.hb, p.w.wsb, a->b_s, le_s,
+      a->sampled, S, p.w.Spad, const_cast<int2*>(p.ep.cmap), p.ep.vocab, p.w.cb, p.w.sid);
   launched();
-  mark(5);
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+// Pass 1: per-row (max, sum 2^x) of each half tile, log2 domain.
+static int32_t bf16_stats(const tfs_ssm_args* a, const Bf16Plan& p, cudaStream_t st) {
+  const umma::Operand hK{p.w.hb, p.w.ldh, false}, wsK{p.w.wsb, a->dim, false};
+  return umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)a->B, (int)a->S, a->dim, p.bn,
+                                    p.ep, nullptr, 0, st);
+}
+
+// Pass 2 onwards (S > 0): G = c exp(Z - lse) -> bf16 G; db_s = column sums of G (+ loss sum);
+// dW_s = G^T h and dh = G W_s [+ g * bf16(w_true)] in one persistent launch.
+static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const float* g_true,
+                             const void* w_true, float* zlab, cudaStream_t st) {
+  const int64_t B = a->B, S = a->S;
+  const int32_t d = a->dim;
+  const Bf16Ws& w = p.w;
+  umma::EpiParams ep = p.ep;
+  ep.zlab = zlab;
+  using umma::Operand;
+  const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
+  int32_t rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, p.bn, ep, w.G,
+                                          w.Sp, st);
+  if (rc != TFS_OK) return rc;
+  mark(a, 4, st);
+  g_colsum_kernel<<<(unsigned)(cdiv(S, kColsumChunks * 8) + (a->loss_sum ? 1 : 0)), 256, 0, st>>>(
+      w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab, a->loss,
+      a->grad_scale, a->loss_sum);
+  launched();
+  mark(a, 5, st);
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
   // (A = G K-major, B = W_s MN-major) in one persistent launch; split partials are reduced in
   // split order by the finalize pass, which also adds the true-class term of dh.
@@ -803,18 +810,17 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   g[0] = umma::Gemm{Operand{w.G, w.Sp, true}, Operand{w.hb, w.ldh, true}, (int)S, d, (int)B,
                     w.ks_dws, a->dw_s, d, w.part_dws, nullptr, nullptr, 0, 0};
   g[1] = umma::Gemm{Operand{w.G, w.Sp, false}, Operand{w.wsb, d, true}, (int)B, d, (int)S,
-                    w.ks_dh, a->dh, d, w.part_dh, dh_split ? nullptr : a->db_true,
-                    dh_split ? nullptr : static_cast<const void*>(a->w_true), d, bin ? 1 : 0};
+                    w.ks_dh, a->dh, d, w.part_dh, dh_split ? nullptr : g_true,
+                    dh_split ? nullptr : w_true, d, p.bin ? 1 : 0};
   // larger units first so the static round-robin schedule balances the SMs
   const int64_t u0 = cdiv(B, umma::BK) / w.ks_dws, u1 = cdiv(S, umma::BK) / w.ks_dh;
   if (u1 > u0) std::swap(g[0], g[1]);
   rc = umma::launch_store(g, 2, st);
   if (rc != TFS_OK) return rc;
-  mark(6);
+  mark(a, 6, st);
   if (dh_split) {
-    auto fin = bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
-    fin<<<grid1d(B * d / 4), 256, 0, st>>>(w.part_dh, w.ks_dh, B, d, a->db_true, a->w_true,
-                                           a->dh);
+    auto fin = p.bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
+    fin<<<grid1d(B * d / 4), 256, 0, st>>>(w.part_dh, w.ks_dh, B, d, g_true, w_true, a->dh);
     launched();
   }
   if (dws_split) {
@@ -823,8 +829,63 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     launched();
   }
   TFS_LAUNCH_CHECK();
-  mark(7);
+  mark(a, 7, st);
   return TFS_OK;
+}
+
+static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
+  const int64_t B = a->B, S = a->S;
+  const int32_t d = a->dim;
+  const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
+  mark(a, 0, st);
+  Bf16Plan p;
+  bf16_plan(a, ws, &p);
+  int32_t rc = bf16_prep(a, p, st);
+  if (rc != TFS_OK) return rc;
+  mark(a, 1, st);
+  if (S > 0) {
+    rc = bf16_stats(a, p, st);
+    if (rc != TFS_OK) return rc;
+  }
+  mark(a, 2, st);
+  auto combine = p.bin ? bf16_combine_kernel<true> : bf16_combine_kernel<false>;
+  combine<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(B, d, a->h, a->w_true, a->b_true, le_t,
+                                                p.w.stats, 2 * p.num_n, a->grad_scale, a->loss,
+                                                a->lse, a->dw_true, a->db_true);
+  launched();
+  TFS_LAUNCH_CHECK();
+  mark(a, 3, st);
+  if (S == 0) {  // no candidates: dh = g * bf16(w_true)
+    auto fin = p.bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
+    fin<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true, a->w_true, a->dh);
+    launched();
+    TFS_LAUNCH_CHECK();
+    return TFS_OK;
+  }
+  return bf16_backward(a, p, a->db_true, a->w_true, nullptr, st);
+}
+
+// Warp per row: (max, sum) over all of the row's half-tile partials, log2 domain, combined in a
+// fixed order (lane-strided, then a butterfly).
+__global__ void __launch_bounds__(256) row_stats_kernel(const float2* stats, int nparts,
+                                                        int64_t B, float2* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= B) return;
+  const float2* st_t = stats + t * nparts;
+  float m = -INFINITY;
+  for (int q = lane; q < nparts; q += 32) m = fmaxf(m, st_t[q].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float s = 0.f;
+  if (m > -INFINITY)
+    for (int q = lane; q < nparts; q += 32) {
+      const float2 x = st_t[q];
+      if (x.y > 0.f) s += x.y * exp2f(x.x - m);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[t] = make_float2(m, s);
 }
 
 }  // namespace tfs
@@ -856,6 +917,7 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
   TFS_REQUIRE(!(a->flags & TFS_SUBTRACT_LOG_Q) || (a->log_ec_true && (a->S == 0 || a->log_ec_s)));
   TFS_REQUIRE(a->S == 0 || (a->sampled && a->w_s && a->b_s && a->dw_s && a->db_s));
   TFS_REQUIRE(!(a->flags & TFS_BF16_OPERANDS) || a->operand_dtype == TFS_BF16);
+  TFS_REQUIRE(!(a->flags & TFS_LABEL_IN_CANDIDATES));  // the split calls' mode only
   if (a->operand_dtype == TFS_BF16) {
     TFS_REQUIRE(a->dim % 64 == 0 && a->lse != nullptr);
     TFS_REQUIRE(((uintptr_t)a->h & 15) == 0 && ((uintptr_t)a->dh & 15) == 0);
@@ -876,6 +938,57 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
     TFS_LAUNCH_CHECK();
   }
   return TFS_OK;
+}
+
+// ---- the two halves of a vocabulary-sharded full softmax ------------------------------------
+static int32_t check_split_args(const tfs_ssm_args* a, void* ws, size_t ws_bytes) {
+  TFS_REQUIRE(a != nullptr);
+  TFS_REQUIRE(a->operand_dtype == TFS_BF16 && a->B >= 1 && a->S >= 1 && a->B < (1ll << 31) &&
+              a->S < (1ll << 31) && a->dim >= 64 && a->dim % 64 == 0);
+  TFS_REQUIRE(a->h && a->sampled && a->w_s && a->b_s);
+  TFS_REQUIRE(((uintptr_t)a->h & 15) == 0 && ((uintptr_t)a->w_s & 15) == 0);
+  TFS_REQUIRE(!(a->flags & TFS_SUBTRACT_LOG_Q) || a->log_ec_s);
+  const bool hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) != 0;
+  const bool label_in = (a->flags & TFS_LABEL_IN_CANDIDATES) != 0;
+  TFS_REQUIRE(!(hits && label_in));
+  TFS_REQUIRE(!(hits || label_in) || a->labels);
+  TFS_SUPPORTED();
+  if (ws_bytes < tfs_ssm_workspace_bytes(a->B, a->S, a->dim, TFS_BF16, a->vocab))
+    return TFS_ERR_WORKSPACE_TOO_SMALL;
+  TFS_REQUIRE(((uintptr_t)ws & 255) == 0);
+  return TFS_OK;
+}
+
+extern "C" int32_t tfs_ssm_partial_stats(const tfs_ssm_args* a, float* row_stats, void* ws,
+                                         size_t ws_bytes, void* stream) {
+  int32_t rc = check_split_args(a, ws, ws_bytes);
+  if (rc != TFS_OK) return rc;
+  TFS_REQUIRE(row_stats != nullptr && ((uintptr_t)row_stats & 7) == 0);
+  cudaStream_t st = as_stream(stream);
+  Bf16Plan p;
+  bf16_plan(a, ws, &p);
+  if ((rc = bf16_prep(a, p, st)) != TFS_OK) return rc;
+  if ((rc = bf16_stats(a, p, st)) != TFS_OK) return rc;
+  row_stats_kernel<<<(unsigned)cdiv(a->B, 8), 256, 0, st>>>(p.w.stats, 2 * p.num_n, a->B,
+                                                            reinterpret_cast<float2*>(row_stats));
+  launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+extern "C" int32_t tfs_ssm_backward_from_lse(const tfs_ssm_args* a, float* z_label, void* ws,
+                                             size_t ws_bytes, void* stream) {
+  int32_t rc = check_split_args(a, ws, ws_bytes);
+  if (rc != TFS_OK) return rc;
+  TFS_REQUIRE(a->lse && a->dh && a->dw_s && a->db_s);
+  TFS_REQUIRE(((uintptr_t)a->dh & 15) == 0 && ((uintptr_t)a->dw_s & 15) == 0);
+  TFS_REQUIRE(a->loss == nullptr && a->loss_sum == nullptr);
+  const bool label_in = (a->flags & TFS_LABEL_IN_CANDIDATES) != 0;
+  TFS_REQUIRE(!label_in || z_label != nullptr);
+  cudaStream_t st = as_stream(stream);
+  Bf16Plan p;
+  bf16_plan(a, ws, &p);
+  return bf16_backward(a, p, nullptr, nullptr, label_in ? z_label : nullptr, st);
 }
 
 // Diagnostics: C[ks][M x N] (fp32) = A[M x K] . B[N x K]^T with bf16 operands on the tcgen05

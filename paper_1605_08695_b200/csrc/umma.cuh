@@ -50,6 +50,7 @@ constexpr int kMNBox = 64;                      // MN-major TMA box: 64 elements
 constexpr int kMNBoxBytes = kMNBox * BK * 2;    // 8 KB
 constexpr int kTmemCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
 // Epilogue staging: two 2 KB buffers per epilogue warp (32 rows x 64 B, 64-byte swizzle), the
 // source of the TMA stores; and the column offsets cb of each (accumulator, half tile).
 constexpr int kStageBytes = 2048;
@@ -92,6 +93,11 @@ struct EpiParams {
   int nparts;          // 2 * number of n-tiles
   const float* lse;    // GRAD: natural-log lse per row
   float c;             // GRAD: gradient scale
+  // label_in != 0 (full softmax over a vocabulary slice): the label's column is NOT excluded;
+  // STATS keeps it in the sums and GRAD writes c (p - 1) there instead of c p, and stores the
+  // label's logit (natural units, bias included) to zlab[m].
+  int label_in;
+  float* zlab;
 };
 
 // One GEMM of a launch (a launch may carry two: the softmax backward runs dh and dW_s together
@@ -524,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         __syncwarp();  // tcgen05.ld / wait are .sync.aligned: the warp must be converged here
         tmem_wait_ld();
         float v[32];
+        uint32_t labmask = 0;  // label_in: columns holding the row's label
         if (c & 1) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(buf1[i]);
@@ -554,8 +561,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             if (mine) {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                if (col0 + i >= hlo && col0 + i <= hhi && __ldg(ep.sid + col0 + i) == y)
-                  v[i] = -INFINITY;
+                if (col0 + i >= hlo && col0 + i <= hhi && __ldg(ep.sid + col0 + i) == y) {
+                  if (ep.label_in) {
+                    labmask |= 1u << i;
+                    if (MODE == kGrad) ep.zlab[row] = v[i] * kLn2;
+                  } else {
+                    v[i] = -INFINITY;
+                  }
+                }
             }
           }
 #endif
@@ -576,14 +589,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             run_m = nm;
           }
         } else if (MODE == kGrad) {
+          float e[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) e[i] = fast_exp2(v[i] - goff);
+          if (labmask != 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if ((labmask >> i) & 1u) e[i] -= ep.c;
+          }
           uint4 x[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             uint32_t p[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              p[j] = pack_bf16x2(fast_exp2(v[8 * k + 2 * j] - goff),
-                                 fast_exp2(v[8 * k + 2 * j + 1] - goff));
+            for (int j = 0; j < 4; ++j) p[j] = pack_bf16x2(e[8 * k + 2 * j], e[8 * k + 2 * j + 1]);
             x[k] = make_uint4(p[0], p[1], p[2], p[3]);
           }
           uint8_t* sb = stg + (nst & 1) * kStageBytes;

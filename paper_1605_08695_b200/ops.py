@@ -12,8 +12,8 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (TFS_BF16, TFS_BF16_OPERANDS, TFS_F32, TFS_REMOVE_ACCIDENTAL_HITS,
-                   TFS_SUBTRACT_LOG_Q, SsmArgs, TfsError, check)
+from ._lib import (TFS_BF16, TFS_BF16_OPERANDS, TFS_F32, TFS_LABEL_IN_CANDIDATES,
+                   TFS_REMOVE_ACCIDENTAL_HITS, TFS_SUBTRACT_LOG_Q, SsmArgs, TfsError, check)
 
 INT64_MAX = (1 << 63) - 1
 
@@ -173,6 +173,76 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
     check(_lib.lib().tfs_sampled_softmax_fwd_bwd(ctypes.byref(a), _p(ws), ws.numel(), _stream()),
           "tfs_sampled_softmax_fwd_bwd")
     return out
+
+
+def _slice_args(h, labels, sampled, w_s, b_s, flags, grad_scale, vocab, lse=None, dh=None,
+                dw_s=None, db_s=None):
+    B, d = h.shape
+    if h.dtype == torch.bfloat16:
+        assert w_s.dtype == torch.bfloat16
+        flags |= TFS_BF16_OPERANDS
+    return SsmArgs(B, sampled.numel(), d, TFS_BF16, flags, float(grad_scale), _p(h), _p(labels),
+                   None, None, None, _p(sampled), _p(w_s), _p(b_s), None, None, _p(lse), None,
+                   _p(dh), None, None, _p(dw_s), _p(db_s), int(vocab), None)
+
+
+def ssm_partial_stats(h, labels, sampled, w_s, b_s, *, flags=TFS_LABEL_IN_CANDIDATES,
+                      vocab: int = 0, ws=None, out=None):
+    """First half of a vocabulary-sharded full softmax on one shard: per token the
+    (max, sum 2^x) pair, log2 domain, over this shard's candidate logits.  Returns fp32
+    [B, 2].  ws (from ssm_workspace(B, S, d, TFS_BF16, vocab)) must be passed on to
+    ssm_backward_from_lse."""
+    B = h.shape[0]
+    out = torch.empty(B, 2, dtype=torch.float32, device=h.device) if out is None else out
+    a = _slice_args(h, labels, sampled, w_s, b_s, flags, 1.0, vocab)
+    check(_lib.lib().tfs_ssm_partial_stats(ctypes.byref(a), _p(out), _p(ws), ws.numel(),
+                                           _stream()), "tfs_ssm_partial_stats")
+    return out
+
+
+def ssm_backward_from_lse(h, labels, sampled, w_s, b_s, lse, *, grad_scale, ws,
+                          flags=TFS_LABEL_IN_CANDIDATES, vocab: int = 0, out=None):
+    """Second half: with the global lse, this shard's G = c (p - onehot), its dh partial
+    (G W_s), dw_s = G^T h, db_s, and the label logits z_label of the labels it holds."""
+    B, d = h.shape
+    S = sampled.numel()
+    if out is None:
+        f = lambda *s: torch.empty(*s, dtype=torch.float32, device=h.device)
+        out = {"dh": f(B, d), "dw_s": f(S, d), "db_s": f(S), "z_label": f(B)}
+    a = _slice_args(h, labels, sampled, w_s, b_s, flags, grad_scale, vocab, lse, out["dh"],
+                    out["dw_s"], out["db_s"])
+    check(_lib.lib().tfs_ssm_backward_from_lse(ctypes.byref(a), _p(out["z_label"]), _p(ws),
+                                               ws.numel(), _stream()),
+          "tfs_ssm_backward_from_lse")
+    return out
+
+
+def lse_combine_peers(stats_tab, R: int, n: int, lse):
+    """lse[t] from every shard's (m, s) pair (peer pointers, rank order)."""
+    check(_lib.lib().tfs_lse_combine_peers(_p(stats_tab), int(R), int(n), _p(lse), _stream()),
+          "tfs_lse_combine_peers")
+    return lse
+
+
+def reduce_peers(src_tab, R: int, offset: int, n: int, out):
+    """out[i] = sum_r src_tab[r][offset + i] (peer pointers, rank order)."""
+    check(_lib.lib().tfs_reduce_peers(_p(src_tab), int(R), int(offset), int(n), _p(out),
+                                      _stream()), "tfs_reduce_peers")
+    return out
+
+
+def label_loss_sum(lse, z_label, labels, R: int, shard: int, c: float, out):
+    check(_lib.lib().tfs_label_loss_sum(_p(lse), _p(z_label), _p(labels), labels.numel(), int(R),
+                                        int(shard), float(c), _p(out), _stream()),
+          "tfs_label_loss_sum")
+    return out
+
+
+def dense_sgd(table, grad, lr: float, shadow=None):
+    """table -= lr * grad; shadow (bf16, same shape) = bf16(table) when given."""
+    check(_lib.lib().tfs_dense_sgd(_p(table), _p(grad), table.numel(), float(lr), _p(shadow),
+                                   _stream()), "tfs_dense_sgd")
+    return table
 
 
 def sort_reduce(ids, vocab: int, num_shards: int, rows, rows2=None, err: ErrorSlot = None,

@@ -486,3 +486,73 @@ def test_sparse_momentum_adagrad_match_oracle(kind, n, dim, zipf):
     plan.apply_opt("sgd", a, T(gs[0]), lr, None)
     plan.apply(c, T(gs[0]), lr)
     assert torch.equal(a, c)
+
+
+# ------------------------------------------------------- vocabulary-sharded full softmax (halves)
+def _full_softmax_oracle(h, labels, W, bb, c, bf16=False):
+    """Full softmax via the oracle (all V classes as candidates, hits removed, no log-Q -- pinned
+    to the brute-force definition in test_oracle), folded into per-class gradients."""
+    V = W.shape[0]
+    z = np.zeros(len(labels))
+    ref = oracle.sampled_softmax(h, labels, W[labels], bb[labels], z, np.arange(V), W, bb,
+                                 np.zeros(V), flags=oracle.REMOVE_ACCIDENTAL_HITS, grad_scale=c,
+                                 bf16=bf16)
+    dW = ref["dw_s"].copy()
+    db = ref["db_s"].copy()
+    np.add.at(dW, labels, ref["dw_true"])
+    np.add.at(db, labels, ref["db_true"])
+    return ref, dW, db
+
+
+def _sharded_full_softmax(h, labels, W, bb, c, R):
+    """R vocabulary shards (class v on shard v mod R) simulated on one GPU through the C ABI."""
+    M, d = h.shape
+    V = W.shape[0]
+    th, ty = T(h), T(labels)
+    shards = []
+    for r in range(R):
+        ids = np.arange(r, V, R)
+        ws = ops.ssm_workspace(M, ids.size, d, TFS_BF16, DEV, V)
+        args = (th, ty, T(ids), T(W[ids]), T(bb[ids]))
+        st = ops.ssm_partial_stats(*args, vocab=V, ws=ws)
+        shards.append((ids, ws, args, st))
+    tab = lambda ts: torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=DEV)
+    lse = torch.empty(M, device=DEV)
+    ops.lse_combine_peers(tab([s[3] for s in shards]), R, M, lse)
+    outs = [ops.ssm_backward_from_lse(*args, lse, grad_scale=c, ws=ws, vocab=V)
+            for ids, ws, args, st in shards]
+    dh = torch.empty(M, d, device=DEV)
+    ops.reduce_peers(tab([o["dh"] for o in outs]), R, 0, M * d, dh)
+    loss = torch.zeros(R, device=DEV)
+    for r in range(R):
+        ops.label_loss_sum(lse, outs[r]["z_label"], ty, R, r, c, loss[r:])
+    dW = np.zeros_like(W, dtype=np.float64)
+    db = np.zeros(V)
+    for r, o in enumerate(outs):
+        dW[shards[r][0]] = o["dw_s"].cpu().numpy()
+        db[shards[r][0]] = o["db_s"].cpu().numpy()
+    maps_zero = all(int(s[1][:8 * V].count_nonzero()) == 0 for s in shards)
+    return lse.cpu().numpy(), dh.cpu().numpy(), dW, db, float(loss.sum()), maps_zero
+
+
+@pytest.mark.parametrize("M,V,d,R", [(77, 500, 64, 1), (256, 1000, 64, 3), (300, 2000, 128, 2),
+                                     (1024, 4000, 512, 4)])
+def test_sharded_full_softmax_halves(M, V, d, R):
+    """logits and gradients computed on each vocabulary shard, combined through
+    (max, sum) pairs, equal the full softmax (loss, dh, dW, db)."""
+    rng = np.random.default_rng(M + V + R)
+    W = (rng.random((V, d), dtype=np.float32) - 0.5)
+    bb = (rng.random(V, dtype=np.float32) - 0.5) * 0.2
+    h = (rng.random((M, d), dtype=np.float32) - 0.5)
+    labels = workloads.zipf_ids(rng, V, 1.0, M)
+    c = 1.0 / M
+    lse, dh, dW, db, loss_sum, maps_zero = _sharded_full_softmax(h, labels, W, bb, c, R)
+    ref, rdW, rdb = _full_softmax_oracle(h, labels, W, bb, c)
+    emu, edW, edb = _full_softmax_oracle(h, labels, W, bb, c, bf16=True)
+    assert rel_elem(lse, ref["lse"]) <= 2e-2
+    for g, o, e in ((dh, ref["dh"], emu["dh"]), (dW, rdW, edW), (db, rdb, edb)):
+        assert rel(g, o) <= 2e-2, rel(g, o)
+        assert rel(g, e) <= 5e-3, rel(g, e)
+    want = c * ref["loss"].sum()
+    assert abs(loss_sum - want) <= 2e-2 * abs(want)
+    assert maps_zero
