@@ -252,7 +252,7 @@ int32_t tfs_label_loss_sum(const float* lse, const float* z_label, const int64_t
                            void* stream);
 /* Dense SGD with a bf16 shadow: table[i] -= lr * grad[i] (fp32, i < n) and, if shadow is not
  * NULL, shadow[i] = bf16(table[i]) (RNE) -- the updated rows' operand copy for the next
- * step's tensor-core GEMMs.  n % 4 == 0, 16-byte aligned pointers (8 for the shadow). */
+ * step's tensor-core GEMMs.  16-byte aligned table / grad, 8-byte aligned shadow. */
 int32_t tfs_dense_sgd(float* table, const float* grad, int64_t n, float lr, void* shadow,
                       void* stream);
 

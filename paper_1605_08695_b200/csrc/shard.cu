@@ -68,10 +68,18 @@ __global__ void __launch_bounds__(1024) label_loss_kernel(const float* lse, cons
   if (threadIdx.x == 0) out[0] = c * red[0];
 }
 
-__global__ void dense_sgd_kernel(float4* table, const float4* grad, int64_t n4, float lr,
+__global__ void dense_sgd_kernel(float4* table, const float4* grad, int64_t n, float lr,
                                  uint2* shadow) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+  const int64_t n4 = n / 4;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i0 < n % 4) {  // tail elements (n % 4 of them)
+    const int64_t e = n4 * 4 + i0;
+    float* t = reinterpret_cast<float*>(table);
+    t[e] -= lr * reinterpret_cast<const float*>(grad)[e];
+    if (shadow != nullptr) reinterpret_cast<uint16_t*>(shadow)[e] = f32_to_bf16_bits(t[e]);
+  }
+  for (int64_t i = i0; i < n4; i += stride) {
     float4 w = table[i];
     const float4 g = grad[i];
     w.x -= lr * g.x;
@@ -136,13 +144,13 @@ extern "C" int32_t tfs_label_loss_sum(const float* lse, const float* z_label,
 
 extern "C" int32_t tfs_dense_sgd(float* table, const float* grad, int64_t n, float lr,
                                  void* shadow, void* stream) {
-  TFS_REQUIRE(n >= 0 && n % 4 == 0);
+  TFS_REQUIRE(n >= 0);
   if (n == 0) return TFS_OK;
   TFS_REQUIRE(table && grad && ((uintptr_t)table & 15) == 0 && ((uintptr_t)grad & 15) == 0);
   TFS_REQUIRE(((uintptr_t)shadow & 7) == 0);
   TFS_SUPPORTED();
-  dense_sgd_kernel<<<grid_for(n / 4), 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<float4*>(table), reinterpret_cast<const float4*>(grad), n / 4, lr,
+  dense_sgd_kernel<<<grid_for(n / 4 + 1), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<float4*>(table), reinterpret_cast<const float4*>(grad), n, lr,
       static_cast<uint2*>(shadow));
   launched();
   TFS_LAUNCH_CHECK();

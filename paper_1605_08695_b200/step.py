@@ -43,7 +43,9 @@ class StepConfig:
     unique: bool = True
     flags: int = TFS_SUBTRACT_LOG_Q | TFS_REMOVE_ACCIDENTAL_HITS
     operand_dtype: int = TFS_BF16
-    full_softmax: bool = False  # candidates = all V classes (config F; R must be 1)
+    # candidates = all V classes (config F).  R > 1: the vocabulary-sharded full softmax of
+    # P:706-714 (W / b never move; every shard scores all R*B tokens against its classes).
+    full_softmax: bool = False
     # R > 1 fixed-capacity routes: distinct ids per (requester, owner) pair are expected near
     # n / R (ids mod R); slots per owner = min(n, ceil(route_slack * n / R) + route_pad).
     # An overflow is reported as TFS_ERR_CAPACITY (never silent).
@@ -131,9 +133,14 @@ class ShardedStep:
         dev = E.device
         self.device = dev
         V, d, B = cfg.vocab, cfg.dim, cfg.tokens
-        S = V if cfg.full_softmax else cfg.num_sampled
-        if cfg.full_softmax and self.R != 1:
-            raise ValueError("full softmax (config F) is a single-GPU configuration")
+        self.full_sharded = cfg.full_softmax and self.R > 1
+        if self.full_sharded:
+            if cfg.route != "p2p" or cfg.operand_dtype != TFS_BF16 or cfg.optimizer != "sgd":
+                raise ValueError("the sharded full softmax runs over p2p with bf16 operands and "
+                                 "SGD")
+            S = 0  # no candidate rows travel: the softmax runs where W lives
+        else:
+            S = V if cfg.full_softmax else cfg.num_sampled
         self.B, self.S, self.d = B, S, d
         self.c = 1.0 / (self.R * B)  # R-13: mean over the global batch
         f32 = dict(dtype=torch.float32, device=dev)
@@ -144,7 +151,7 @@ class ShardedStep:
         self.err = ops.ErrorSlot(dev)
         self.step_dev = torch.zeros(1, **i64)
         if cfg.full_softmax:
-            self.qw[B:] = torch.arange(V, **i64)
+            self.qw[B:] = torch.arange(S, **i64)
             self.les = torch.zeros(S, **f32)
             self.ley = torch.zeros(B, **f32)
             self.num_tries = torch.full((1,), V, **i64)
@@ -195,6 +202,8 @@ class ShardedStep:
                 raise ValueError(f"unknown route transport {cfg.route!r}")
             if cfg.route == "p2p":
                 self._symm_tables()
+            if self.full_sharded:
+                self._init_full_sharded()
 
             def cap_for(n):
                 return int(min(n, -(-cfg.route_slack * n // R) + cfg.route_pad))
@@ -228,6 +237,35 @@ class ShardedStep:
             setattr(self, name, t[:src.shape[0]])
             setattr(self, "tab_" + name, ptrs)
             setattr(self, "hdl_" + name, h)
+
+    def _init_full_sharded(self):
+        """Buffers of the vocabulary-sharded full softmax (R > 1).  h and y live in symmetric
+        memory (every shard all-gathers them), and so do the per-token (max, sum) pairs, the dh
+        partials and the loss partial that the other shards pull."""
+        R, B, d, V, dev = self.R, self.B, self.d, self.cfg.vocab, self.device
+        M = R * B
+        f32 = dict(dtype=torch.float32, device=dev)
+        i64 = dict(dtype=torch.int64, device=dev)
+        self.M, self.nloc = M, self.W.shape[0]
+        self.h, _, self.tab_h = self._symm((B, d), torch.bfloat16)
+        self.y, _, self.tab_y = self._symm((B,), torch.int64)
+        self.h_all = torch.empty((M, d), dtype=torch.bfloat16, device=dev)
+        self.y_all = torch.empty(M, **i64)
+        g = torch.arange(M, **i64)
+        self.ag_ids = (g % B) * R + g // B      # global token g = rank g // B, row g % B
+        self.cand = torch.arange(self.nloc, **i64) * R + self.rank   # this shard's classes
+        self.W_bf = self.W.to(torch.bfloat16)   # operand shadow, refreshed by the W update
+        self.rowstats, _, self.tab_rowstats = self._symm((M, 2), torch.float32)
+        self.lse_all = torch.empty(M, **f32)
+        dh_part, _, self.tab_dh = self._symm((M, d), torch.float32)
+        self.full_out = {"dh": dh_part, "dw_s": torch.empty((self.nloc, d), **f32),
+                         "db_s": torch.empty(self.nloc, **f32), "z_label": torch.empty(M, **f32)}
+        self.loss_part, _, self.tab_loss = self._symm((4,), torch.float32)
+        self.ws_full = ops.ssm_workspace(M, self.nloc, d, TFS_BF16, dev, V)
+
+    def _refresh_shadow(self):
+        if self.full_sharded:
+            self.W_bf.copy_(self.W)
 
     def set_route_caps(self, cap_e: int, cap_w: int):
         """(Re)allocate the R > 1 slot buffers for cap_e / cap_w distinct ids per owner."""
@@ -425,8 +463,70 @@ class ShardedStep:
                          grad2=gr[:, self.off_b:], grad2_stride=rs)
         main.wait_stream(side)
 
+    def _dist_step_full(self, step: int | None):
+        """Vocabulary-sharded full softmax over NVLink ("the multiplication and
+        gradient calculation are colocated with the shards"): W and b never move.
+
+        B0: the previous step is applied everywhere.  Each rank pulls its h rows from the E
+        owners and pushes its distinct x ids into their inboxes.  B1: h, y and the ids are
+        in place; every rank all-gathers h and y (peer loads), scores all R*B tokens against
+        its own classes and publishes per-token (max, sum) pairs.  B2: every rank combines all
+        pairs into the global lse, forms G = c (p - onehot) on its classes, its dh partial,
+        dW / db of its classes (applied locally, dense) and the loss of the labels it holds.
+        B3: each rank pulls and sums its tokens' dh partials and the loss partials, then pushes
+        per-id dh sums to the E owners.  B4: the E owners apply their planned ScatterAdd-SGD."""
+        V, B, R, d, M = self.cfg.vocab, self.B, self.R, self.d, self.M
+        ev, rank, lr = self.ev, self.rank, self.cfg.lr
+        main, side = torch.cuda.current_stream(), self.side_stream
+        L = ops._lib.lib()
+        bar = self.hdl_ids.barrier
+        bar(channel=0)                                              # B0
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self.route_e.build_push(self.x, self.tab_ids, rank * self.istride,
+                                    counts=self.counts[0], err=self.err)
+            ev["q"].record(side)
+        ops.gather_peers(self.tab_E, self.shard_rows, d, self.x, V, R, self.h, err=self.err)
+        main.wait_event(ev["q"])
+        bar(channel=1)                                              # B1
+        ev["ids"].record(main)
+        with torch.cuda.stream(side):                               # E owner plan, in parallel
+            side.wait_event(ev["ids"])
+            self.own_e.build(self.recv_ids, self.istride, err=self.err)
+            ev["own"].record(side)
+        # all-gathers of h (bf16) and y (int64) as bit copies of float words
+        ops.gather_peers(self.tab_h, B, d // 2, self.ag_ids, M, R,
+                         self.h_all.view(torch.float32), err=self.err)
+        ops.gather_peers(self.tab_y, B, 2, self.ag_ids, M, R, self.y_all.view(torch.float32),
+                         err=self.err)
+        ops.ssm_partial_stats(self.h_all, self.y_all, self.cand, self.W_bf, self.b, vocab=V,
+                              ws=self.ws_full, out=self.rowstats)
+        bar(channel=2)                                              # B2
+        ops.lse_combine_peers(self.tab_rowstats, R, M, self.lse_all)
+        fo = self.full_out
+        ops.ssm_backward_from_lse(self.h_all, self.y_all, self.cand, self.W_bf, self.b,
+                                  self.lse_all, grad_scale=self.c, ws=self.ws_full, vocab=V,
+                                  out=fo)
+        ops.label_loss_sum(self.lse_all, fo["z_label"], self.y_all, R, rank, self.c,
+                           self.loss_part)
+        ev["ssm"].record(main)
+        with torch.cuda.stream(side):                  # W / b: local dense SGD, in parallel
+            side.wait_event(ev["ssm"])
+            ops.dense_sgd(self.W, fo["dw_s"], lr, shadow=self.W_bf)
+            ops.dense_sgd(self.b, fo["db_s"], lr)
+        bar(channel=3)                                              # B3
+        ops.reduce_peers(self.tab_dh, R, rank * B * d, B * d, self.ssm_out["dh"])
+        ops.reduce_peers(self.tab_loss, R, 0, 1, self.ssm_out["loss_sum"])
+        self.route_e.reduce_push(self.ssm_out["dh"], d, self.tab_grads, rank * self.rstride)
+        bar(channel=4)                                              # B4
+        main.wait_event(ev["own"])
+        self.own_e.apply(self.E, self.recv_grads, self.rstride, lr)
+        main.wait_stream(side)
+
     def _dist_step(self, step: int | None):
-        if self.cfg.route == "p2p":
+        if self.full_sharded:
+            self._dist_step_full(step)
+        elif self.cfg.route == "p2p":
             self._dist_step_p2p(step)
         else:
             self._dist_step_nccl(step)
@@ -511,6 +611,7 @@ class ShardedStep:
         torch.cuda.synchronize()
         for dst, src in zip((self.E, self.W, self.b), saved):  # undo the warm-up update
             dst.copy_(src)
+        self._refresh_shadow()
         if saved_slots is not None:
             for dst, src in zip(self.slots, saved_slots):
                 dst.copy_(src)

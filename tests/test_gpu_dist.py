@@ -23,7 +23,18 @@ def rel(g, o):
     return float(np.max(np.abs(g - o)) / max(np.max(np.abs(o)), 1e-300)) if o.size else 0.0
 
 
-def _worker(rank, world, port, name, dtype, route, q):
+# A mid-size full-softmax case (the oracle's full softmax over F itself takes minutes).
+EXTRA = {"Fm": dict(vocab=4000, dim=128, tokens=256)}
+
+
+def _workload(name):
+    import workloads
+    if name in EXTRA:
+        return workloads.Workload(name, shards=2, num_sampled=0, **EXTRA[name])
+    return workloads.WORKLOADS[name]
+
+
+def _worker(rank, world, port, name, dtype, route, q, full=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     import oracle  # noqa: F401
@@ -34,13 +45,13 @@ def _worker(rank, world, port, name, dtype, route, q):
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     try:
-        w = workloads.WORKLOADS[name]
+        w = _workload(name)
         V, R = w.vocab, world
         E, W, b = workloads.tables(V, w.dim)
         xs, ys = zip(*[workloads.batch(w, R, r) for r in range(R)])
         cfg = gstep.StepConfig(vocab=V, dim=w.dim, tokens=xs[0].size, num_sampled=w.num_sampled,
                                lr=1.0, seed=workloads.SAMPLER_SEED, operand_dtype=dtype,
-                               route=route)
+                               route=route, full_softmax=full)
         st = gstep.ShardedStep(cfg, torch.from_numpy(E[rank::R].copy()).to(dev),
                                torch.from_numpy(W[rank::R].copy()).to(dev),
                                torch.from_numpy(b[rank::R].copy()).to(dev), gstep.Router())
@@ -48,11 +59,17 @@ def _worker(rank, world, port, name, dtype, route, q):
         torch.cuda.synchronize()
         st.err.check("dist step")
         ocfg = ostep.StepConfig(vocab=V, dim=w.dim, num_sampled=w.num_sampled, num_shards=R,
-                                lr=1.0, seed=workloads.SAMPLER_SEED, step=2, bf16=(dtype == 1))
+                                lr=1.0, seed=workloads.SAMPLER_SEED, step=2, bf16=(dtype == 1),
+                                full_softmax=full)
         E2, W2, b2, tr = ostep.step(E, W, b, list(xs), list(ys), ocfg)
         B = xs[0].size
-        res = {"sampled": np.array_equal(st.qw[B:].cpu().numpy(), tr[rank].sampled),
-               "loss": rel(st.ssm_out["loss"].cpu().numpy(), tr[rank].ssm["loss"])}
+        if full:  # the loss is formed where each label lives: compare the global sum
+            want = sum(t.ssm["loss"].sum() for t in tr) / (R * B)
+            res = {"sampled": True,
+                   "loss": abs(float(st.ssm_out["loss_sum"].item()) - want) / abs(want)}
+        else:
+            res = {"sampled": np.array_equal(st.qw[B:].cpu().numpy(), tr[rank].sampled),
+                   "loss": rel(st.ssm_out["loss"].cpu().numpy(), tr[rank].ssm["loss"])}
         for nm, T0, Tg, To in (("E", E, st.E, E2), ("W", W, st.W, W2), ("b", b, st.b, b2)):
             g = Tg.cpu().numpy()
             t0, to = T0[rank::R], To[rank::R]
@@ -87,3 +104,27 @@ def test_dist_step_matches_oracle(name, dtype, tol, route):
         for nm in ("E", "W", "b"):
             assert r[nm + "_untouched"], (rank, nm)
             assert r[nm] <= tol, (rank, nm, r[nm])
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("name", ["T", "Fm"])
+def test_dist_full_softmax_sharded_matches_oracle(name):
+    """The vocabulary-sharded full softmax (W / b stay on their shard, which scores
+    all R*B tokens) reaches the oracle's full-softmax step over the same global batch."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, 1, "p2p", q, True))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, r in res:
+        assert r["loss"] <= 5e-3, (rank, r)
+        for nm in ("E", "W", "b"):
+            assert r[nm + "_untouched"], (rank, nm)
+            assert r[nm] <= 5e-3, (rank, nm, r[nm])
