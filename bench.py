@@ -431,10 +431,23 @@ def main():
             phases.setdefault(name, []).append(s_.elapsed_time(e_))
         st.phase_events = None
         phases = {k: sum(v) / len(v) for k, v in phases.items()}
-        if dtype == TFS_BF16 and S > 0:  # per-GEMM-launch durations, CUDA events on its stream
+        if dtype == TFS_BF16:  # per-GEMM-launch durations, CUDA events on its stream
             for name, (i0, i1) in (("gemm_stats", (1, 2)), ("gemm_grad", (3, 4)),
                                    ("gemm_store", (5, 6))):
                 kern_ms[name] = sum(ev[i0].elapsed_time(ev[i1]) for ev in ssm_ev) / len(ssm_ev)
+    elif st.full_sharded:  # the two softmax halves on each shard, CUDA events on their stream
+        half_ev = []
+        for i in range(n_ph):
+            flush.zero_()
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            st.ssm_events = evs
+            st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], step_no)
+            half_ev.append(evs)
+            step_no += 1
+        torch.cuda.synchronize()
+        st.ssm_events = None
+        kern_ms["partial_stats"] = sum(e[0].elapsed_time(e[1]) for e in half_ev) / n_ph
+        kern_ms["backward_from_lse"] = sum(e[2].elapsed_time(e[3]) for e in half_ev) / n_ph
     st.err.check("bench instrumented steps")
 
     peaks, peak_src = load_peaks()
@@ -447,11 +460,27 @@ def main():
         except Exception:
             traffic = None
     peak = peaks.get("bf16_tflops_sustained", 1407.0)
-    if kern_ms:
+    S_eff = S if S > 0 else w.vocab  # candidates per replica (full softmax: all V classes)
+    if kern_ms and st.full_sharded:
+        # per shard: M = R*B tokens x its V/R classes; STATS 2 M n d, GRAD + STORE 6 M n d flops
+        M_, n_ = R * B, st.nloc
+        fl = {"partial_stats": 2.0 * M_ * n_ * d, "backward_from_lse": 6.0 * M_ * n_ * d}
+        per = {k: {"ms": v, "tflops": fl[k] / (v / 1e3) / 1e12,
+                   "frac": fl[k] / (v / 1e3) / 1e12 / peak} for k, v in kern_ms.items()}
+        top = per["backward_from_lse"]
+        roofline = {"kernel": "tfs_ssm_backward_from_lse (GRAD + column sums + grouped "
+                              "dh / dW GEMM on this shard's classes)",
+                    "bound": "tensor", "achieved": top["tflops"], "peak": peak,
+                    "unit": "TFLOP/s", "frac": top["frac"], "traffic": None,
+                    "peak_source": f"{peak_src} bf16 sustained",
+                    "algorithmic": "6*M*n*d flops per call (M = R*B tokens, n = V/R classes); "
+                                   "achieved = that / the call's CUDA-event duration",
+                    "ms": top["ms"], "kernels": per}
+    elif kern_ms:
         # The dominant kernel of the step: the grouped backward GEMM (dh = G W_s and
         # dW_s = G^T h in one persistent tcgen05 launch), 2 x 2 B S d algorithmic flops.
-        flops = {"gemm_stats": 2.0 * B * S * d, "gemm_grad": 2.0 * B * S * d,
-                 "gemm_store": 4.0 * B * S * d}
+        flops = {"gemm_stats": 2.0 * B * S_eff * d, "gemm_grad": 2.0 * B * S_eff * d,
+                 "gemm_store": 4.0 * B * S_eff * d}
         per = {k: {"ms": v, "tflops": flops[k] / (v / 1e3) / 1e12,
                    "frac": flops[k] / (v / 1e3) / 1e12 / peak} for k, v in kern_ms.items()}
         top = per["gemm_store"]
@@ -467,8 +496,8 @@ def main():
     if "sampled_softmax" in phases:
         t = phases["sampled_softmax"] / 1e3
         ssm = {"kernel": "tfs_sampled_softmax_fwd_bwd (whole call: 7 launches)", "bound": "tensor",
-               "achieved": 6.0 * B * S * d / t / 1e12, "peak": peak, "unit": "TFLOP/s",
-               "frac": 6.0 * B * S * d / t / 1e12 / peak,
+               "achieved": 6.0 * B * S_eff * d / t / 1e12, "peak": peak, "unit": "TFLOP/s",
+               "frac": 6.0 * B * S_eff * d / t / 1e12 / peak,
                "traffic": (traffic or {}).get("ssm_total"),
                "algorithmic": "6*B*S*d flops per call (3 GEMMs; the logits recompute is overhead)",
                "ms": phases["sampled_softmax"]}
@@ -510,7 +539,11 @@ def main():
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": args.workload, "vocab": w.vocab, "dim": d,
                        "tokens_per_gpu": B, "global_batch": R * B, "num_sampled": S,
-                       "zipf_s": w.zipf_s, "parallelism": f"vocab-sharded x{R} (ids mod R), "
+                       "zipf_s": w.zipf_s,
+                       "softmax": ("sampled" if S > 0 else "full" if R == 1 else
+                                   "full, vocabulary-sharded: each GPU scores all R*B tokens "
+                                   "against its V/R classes (P:706-714)"),
+                       "parallelism": f"vocab-sharded x{R} (ids mod R), "
                        f"data-parallel x{R}", "l2": "flushed before every timed step "
                        "(256 MiB write outside the timed interval)",
                        "cuda_graph": use_graph, "batches": N_BATCHES,

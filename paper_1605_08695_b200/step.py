@@ -499,14 +499,23 @@ class ShardedStep:
                          self.h_all.view(torch.float32), err=self.err)
         ops.gather_peers(self.tab_y, B, 2, self.ag_ids, M, R, self.y_all.view(torch.float32),
                          err=self.err)
+        tev = self.ssm_events  # optional timing: 4 events around the two softmax halves
+        if tev is not None:
+            tev[0].record()
         ops.ssm_partial_stats(self.h_all, self.y_all, self.cand, self.W_bf, self.b, vocab=V,
                               ws=self.ws_full, out=self.rowstats)
+        if tev is not None:
+            tev[1].record()
         bar(channel=2)                                              # B2
         ops.lse_combine_peers(self.tab_rowstats, R, M, self.lse_all)
         fo = self.full_out
+        if tev is not None:
+            tev[2].record()
         ops.ssm_backward_from_lse(self.h_all, self.y_all, self.cand, self.W_bf, self.b,
                                   self.lse_all, grad_scale=self.c, ws=self.ws_full, vocab=V,
                                   out=fo)
+        if tev is not None:
+            tev[3].record()
         ops.label_loss_sum(self.lse_all, fo["z_label"], self.y_all, R, rank, self.c,
                            self.loss_part)
         ev["ssm"].record(main)
