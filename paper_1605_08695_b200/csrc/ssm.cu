@@ -115,11 +115,11 @@ static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int 
   return TFS_OK;
 }
 
-template <int MODE>
+template <int MODE, bool LAB = false>
 static int32_t launch_params(const Params& P, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE>,
+    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, LAB>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmemBytes));
     attr_done = true;
@@ -138,7 +138,7 @@ static int32_t launch_params(const Params& P, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = kCta > 1 ? 1 : 0;  // plain launch for single-CTA tiles
-  TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE>, P));
+  TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, LAB>, P));
   launched();
   TFS_LAUNCH_CHECK();
   if (std::getenv("TFS_DEBUG_SYNC") != nullptr) {  // diagnostics: attribute faults to a mode
@@ -181,6 +181,8 @@ int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K
     if (rc != TFS_OK) return rc;
   }
   P.ep = ep;
+  if (ep.label_in)
+    return mode == kStats ? launch_params<kStats, true>(P, st) : launch_params<kGrad, true>(P, st);
   return mode == kStats ? launch_params<kStats>(P, st) : launch_params<kGrad>(P, st);
 }
 

@@ -327,7 +327,9 @@ __device__ __forceinline__ void stage_row64(uint8_t* buf, int lane, const uint4 
     *reinterpret_cast<uint4*>(buf + lane * 64 + ((k ^ sw) << 4)) = x[k];
 }
 
-template <int MODE>
+// LAB: the label-in-candidates epilogue (EpiParams::label_in), a separate instantiation so the
+// sampled-softmax kernels compile exactly as without it.
+template <int MODE, bool LAB = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
@@ -562,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
               for (int i = 0; i < 32; ++i)
                 if (col0 + i >= hlo && col0 + i <= hhi && __ldg(ep.sid + col0 + i) == y) {
-                  if (ep.label_in) {
+                  if (LAB) {
                     labmask |= 1u << i;
                     if (MODE == kGrad) ep.zlab[row] = v[i] * kLn2;
                   } else {
@@ -589,21 +591,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             run_m = nm;
           }
         } else if (MODE == kGrad) {
-          float e[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) e[i] = fast_exp2(v[i] - goff);
-          if (labmask != 0) {
+          uint4 x[4];
+          if (LAB) {  // G = c (p - 1) at the label's column
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if ((labmask >> i) & 1u) e[i] -= ep.c;
-          }
-          uint4 x[4];
+              v[i] = fast_exp2(v[i] - goff) - (((labmask >> i) & 1u) ? ep.c : 0.f);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint32_t p[4];
+            for (int k = 0; k < 4; ++k) {
+              uint32_t p[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) p[j] = pack_bf16x2(e[8 * k + 2 * j], e[8 * k + 2 * j + 1]);
-            x[k] = make_uint4(p[0], p[1], p[2], p[3]);
+              for (int j = 0; j < 4; ++j)
+                p[j] = pack_bf16x2(v[8 * k + 2 * j], v[8 * k + 2 * j + 1]);
+              x[k] = make_uint4(p[0], p[1], p[2], p[3]);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              uint32_t p[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                p[j] = pack_bf16x2(fast_exp2(v[8 * k + 2 * j] - goff),
+                                   fast_exp2(v[8 * k + 2 * j + 1] - goff));
+              x[k] = make_uint4(p[0], p[1], p[2], p[3]);
+            }
           }
           uint8_t* sb = stg + (nst & 1) * kStageBytes;
           if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
