@@ -115,8 +115,19 @@ static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int 
   return TFS_OK;
 }
 
+// As many pipeline stages as the widest B tile of the launch leaves room for (Params).
+template <int MODE>
+static void stage_plan(Params& P) {
+  int bmax = 0;
+  for (int i = 0; i < P.nprob; ++i) bmax = std::max(bmax, P.p[i].bn / kCta * BK * 2);
+  P.b_stride = (bmax + 1023) / 1024 * 1024;
+  const int fixed = (MODE == kStats ? 0 : kEpiSmem) + kCbSmem + kBarBytes;
+  P.stages = std::min<int>(kMaxStages, ((int)kSmemBytes - fixed) / (A_BYTES + P.b_stride));
+}
+
 template <int MODE, bool LAB = false>
-static int32_t launch_params(const Params& P, cudaStream_t st) {
+static int32_t launch_params(Params P, cudaStream_t st) {
+  stage_plan<MODE>(P);
   static bool attr_done = false;
   if (!attr_done) {
     TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, LAB>,

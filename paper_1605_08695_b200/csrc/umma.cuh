@@ -39,7 +39,8 @@ namespace umma {
 constexpr int kCta = TFS_UMMA_CTAS;  // 1: one CTA per tile; 2: CTA pairs (cta_group::2)
 static_assert(kCta == 1 || kCta == 2, "kCta");
 constexpr int BM = 128, BN = 256, BK = 64;      // BM: rows per CTA; BN: tile N
-constexpr int STAGES = kCta == 2 ? 6 : 4;
+constexpr int STAGES = kCta == 2 ? 6 : 4;       // stages at the widest tile (BN); a launch with
+constexpr int kMaxStages = 8;                   // narrower tiles / no staging fits more (Params)
 constexpr int PM = kCta * BM;                   // rows per tile
 constexpr int BNC = BN / kCta;                  // B rows per CTA
 constexpr int kEpiWarps = 8;
@@ -56,8 +57,8 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kStageBytes = 2048;
 constexpr int kEpiSmem = kEpiWarps * 2 * kStageBytes;  // 32 KB
 constexpr int kCbSmem = 2 * 2 * 128 * 4;               // 2 KB
-constexpr int kBarBytes = 256;  // (2 STAGES + 4) mbarriers + the TMEM address slot
-static_assert((2 * STAGES + 4) * 8 + 4 <= kBarBytes, "barrier area too small");
+constexpr int kBarBytes = 256;  // (2 kMaxStages + 4) mbarriers + the TMEM address slot
+static_assert((2 * kMaxStages + 4) * 8 + 4 <= kBarBytes, "barrier area too small");
 constexpr size_t kSmemBytes =
     (size_t)STAGES * (A_BYTES + B_BYTES) + kEpiSmem + kCbSmem + kBarBytes;  // 231680 B
 static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
@@ -117,10 +118,15 @@ struct Problem {
   int wt_bf16;
 };
 
+// Shared-memory pipeline of a launch: `stages` ring slots of A (A_BYTES) and B (b_stride bytes:
+// the widest B tile of the launch's problems, 1 KB aligned) -- as many as fit beside the
+// epilogue staging (none for STATS), the column offsets and the barriers (stage_plan, host).
 struct Params {
   Problem p[2];
   int nprob;
   int total_units;
+  int stages;
+  int b_stride;
   EpiParams ep;
 };
 
@@ -332,13 +338,15 @@ __device__ __forceinline__ void stage_row64(uint8_t* buf, int lane, const uint4 
 template <int MODE, bool LAB = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  const int STAGES = P.stages;
+  const int B_BYTES = P.b_stride;
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint8_t* sE = sB + STAGES * B_BYTES;                 // epilogue staging
-  float* sCb = reinterpret_cast<float*>(sE + kEpiSmem);  // [acc][half][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sE + kEpiSmem + kCbSmem);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sE = sB + STAGES * B_BYTES;                 // epilogue staging (not for STATS)
+  float* sCb = reinterpret_cast<float*>(sE + (MODE == kStats ? 0 : kEpiSmem));  // [acc][half][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCb) + kCbSmem);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   const EpiParams& ep = P.ep;
