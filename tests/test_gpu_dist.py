@@ -34,7 +34,20 @@ def _workload(name):
     return workloads.WORKLOADS[name]
 
 
-def _worker(rank, world, port, name, dtype, route, q, full=False):
+def _worker(rank, world, port, name, dtype, route, *rest):
+    """Runs one rank; any exception is reported through the queue (so the parent fails fast
+    with the traceback instead of waiting for a result that never comes)."""
+    import traceback
+    *flag, q = rest
+    full = bool(flag and flag[0])
+    try:
+        _worker_body(rank, world, port, name, dtype, route, q, full)
+    except BaseException:
+        q.put((rank, {"error": traceback.format_exc()}))
+        raise
+
+
+def _worker_body(rank, world, port, name, dtype, route, q, full):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     import oracle  # noqa: F401
@@ -82,22 +95,39 @@ def _worker(rank, world, port, name, dtype, route, q, full=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("route", ["p2p", "nccl"])
-@pytest.mark.parametrize("name,dtype,tol", [("T", 0, 1e-5), ("L", 1, 2e-3)])
-def test_dist_step_matches_oracle(name, dtype, tol, route):
+def _run_ranks(args_of_rank):
+    """Spawn one process per rank, collect (rank, result) pairs; a rank that raised fails the
+    test with its traceback, and no rank is left running (a peer of a failed rank may be
+    blocked in a device barrier)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, dtype, route, q))
-             for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, len(args_of_rank), port, *a, q))
+             for r, a in enumerate(args_of_rank)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(2)]
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    try:
+        res = []
+        for _ in procs:
+            rank, r = q.get(timeout=600)
+            assert "error" not in r, f"rank {rank}:\n{r['error']}"
+            res.append((rank, r))
+        for p in procs:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+        return res
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("route", ["p2p", "nccl"])
+@pytest.mark.parametrize("name,dtype,tol", [("T", 0, 1e-5), ("L", 1, 2e-3)])
+def test_dist_step_matches_oracle(name, dtype, tol, route):
+    res = _run_ranks([(name, dtype, route)] * 2)
     for rank, r in res:
         assert r["sampled"], rank
         assert r["loss"] <= tol, (rank, r)
@@ -111,18 +141,7 @@ def test_dist_step_matches_oracle(name, dtype, tol, route):
 def test_dist_full_softmax_sharded_matches_oracle(name):
     """The vocabulary-sharded full softmax (W / b stay on their shard, which scores
     all R*B tokens) reaches the oracle's full-softmax step over the same global batch."""
-    import torch.multiprocessing as mp
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, 1, "p2p", q, True))
-             for r in range(2)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=600) for _ in range(2)]
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    res = _run_ranks([(name, 1, "p2p", True)] * 2)
     for rank, r in res:
         assert r["loss"] <= 5e-3, (rank, r)
         for nm in ("E", "W", "b"):
