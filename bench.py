@@ -413,8 +413,10 @@ def main():
     phases = {}
     n_ph = max(1, min(args.phase_steps, args.steps))
     kern_ms = {}
-    if R == 1:
-        st.phase_events = []
+    call_ms = None
+    if not st.full_sharded:
+        if R == 1:  # the R = 1 step also brackets its phases (the R > 1 step runs overlapped)
+            st.phase_events = []
         ssm_ev = []
         for i in range(n_ph):
             flush.zero_()
@@ -427,7 +429,7 @@ def main():
             step_no += 1
         torch.cuda.synchronize()
         st.ssm_events = None
-        for name, s_, e_ in st.phase_events:
+        for name, s_, e_ in st.phase_events or []:
             phases.setdefault(name, []).append(s_.elapsed_time(e_))
         st.phase_events = None
         phases = {k: sum(v) / len(v) for k, v in phases.items()}
@@ -435,6 +437,7 @@ def main():
             for name, (i0, i1) in (("gemm_stats", (1, 2)), ("gemm_grad", (3, 4)),
                                    ("gemm_store", (5, 6))):
                 kern_ms[name] = sum(ev[i0].elapsed_time(ev[i1]) for ev in ssm_ev) / len(ssm_ev)
+            call_ms = sum(ev[0].elapsed_time(ev[7]) for ev in ssm_ev) / len(ssm_ev)
     elif st.full_sharded:  # the two softmax halves on each shard, CUDA events on their stream
         half_ev = []
         for i in range(n_ph):
@@ -493,14 +496,18 @@ def main():
                     "algorithmic": "4*B*S*d flops per launch (two GEMMs); achieved = that / the "
                                    "launch's CUDA-event duration in instrumented eager steps",
                     "ms": top["ms"], "kernels": per}
-    if "sampled_softmax" in phases:
-        t = phases["sampled_softmax"] / 1e3
+    if "sampled_softmax" not in phases and call_ms is not None:
+        phases_call = call_ms  # R > 1: the call bracketed by its own first / last event
+    else:
+        phases_call = phases.get("sampled_softmax")
+    if phases_call is not None:
+        t = phases_call / 1e3
         ssm = {"kernel": "tfs_sampled_softmax_fwd_bwd (whole call: 7 launches)", "bound": "tensor",
                "achieved": 6.0 * B * S_eff * d / t / 1e12, "peak": peak, "unit": "TFLOP/s",
                "frac": 6.0 * B * S_eff * d / t / 1e12 / peak,
                "traffic": (traffic or {}).get("ssm_total"),
                "algorithmic": "6*B*S*d flops per call (3 GEMMs; the logits recompute is overhead)",
-               "ms": phases["sampled_softmax"]}
+               "ms": phases_call}
         if roofline is None:
             roofline = ssm
         else:
