@@ -26,7 +26,10 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = 4;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 1024 items per CTA
 constexpr int kMaxBuckets = 256;
-constexpr int kChunk = 8;  // sorted rows per warp in the segmented sums
+#ifndef TFS_SEG_CHUNK
+#define TFS_SEG_CHUNK 8
+#endif
+constexpr int kChunk = TFS_SEG_CHUNK;  // sorted rows per warp in the segmented sums
 #ifndef TFS_SEG_MINB
 #define TFS_SEG_MINB 3  // 3 CTAs / SM (<= 85 registers): measured 24 -> 14 us on 10k Zipf rows
 #endif
