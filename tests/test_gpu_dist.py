@@ -24,7 +24,8 @@ def rel(g, o):
 
 
 # A mid-size full-softmax case (the oracle's full softmax over F itself takes minutes).
-EXTRA = {"Fm": dict(vocab=4000, dim=128, tokens=256)}
+EXTRA = {"Fm": dict(vocab=4000, dim=128, tokens=256),
+         "Fo": dict(vocab=4003, dim=64, tokens=96)}   # V not a multiple of R (ragged shards)
 
 
 def _workload(name):
@@ -147,3 +148,19 @@ def test_dist_full_softmax_sharded_matches_oracle(name):
         for nm in ("E", "W", "b"):
             assert r[nm + "_untouched"], (rank, nm)
             assert r[nm] <= 5e-3, (rank, nm, r[nm])
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("name,dtype,route,full,tol", [
+    ("T", 0, "p2p", False, 1e-5), ("T", 1, "nccl", False, 2e-3), ("Fo", 1, "p2p", True, 5e-3)])
+def test_dist4_matches_oracle(name, dtype, route, full, tol):
+    """R = 4 ranks (the bench's 4-GPU configuration): sampled step over both transports, and the
+    sharded full softmax with V = 4003 (shards of 1001 / 1001 / 1001 / 1000 classes)."""
+    res = _run_ranks([(name, dtype, route, full)] * 4)
+    assert len(res) == 4
+    for rank, r in res:
+        assert r["sampled"], rank
+        assert r["loss"] <= tol, (rank, r)
+        for nm in ("E", "W", "b"):
+            assert r[nm + "_untouched"], (rank, nm)
+            assert r[nm] <= tol, (rank, nm, r[nm])
