@@ -93,6 +93,12 @@ int32_t tfs_partition(const int64_t* ids, int64_t n, int64_t vocab, int32_t num_
 int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int32_t table_dtype,
                    const int64_t* ids, int64_t n, void* out, int32_t out_dtype,
                    tfs_device_error* err, void* stream);
+/* tfs_gather2: the same Gather of a row table plus its width-1 companion in one pass (the
+ * softmax rows W with their bias b, R-11): out as tfs_gather; out2[j] = table2[ids[j]] (fp32,
+ * [n]); table2 has the same `rows`.  Same error and padding behaviour. */
+int32_t tfs_gather2(const float* table, int64_t rows, int32_t dim, const float* table2,
+                    const int64_t* ids, int64_t n, void* out, int32_t out_dtype, float* out2,
+                    tfs_device_error* err, void* stream);
 
 /* ==== Stitch =======================================================================
  * The "dynamic static" (read: dynamic stitch, R-3) op "reassembles the partial results from
@@ -383,6 +389,12 @@ int32_t tfs_route_reduce_push(const void* plan, size_t plan_bytes, int64_t n, in
 int32_t tfs_gather_peers(const float* const* shards, int64_t shard_rows, int32_t dim,
                          const int64_t* ids, int64_t n, int64_t vocab, int32_t num_shards,
                          void* out, int32_t out_dtype, tfs_device_error* err, void* stream);
+/* tfs_gather_peers2: tfs_gather_peers plus a width-1 companion table sharded the same way
+ * (shards2[o] = owner o's [shard_rows] fp32 array): out2[t] = shards2[id % R][id / R]. */
+int32_t tfs_gather_peers2(const float* const* shards, int64_t shard_rows, int32_t dim,
+                          const float* const* shards2, const int64_t* ids, int64_t n,
+                          int64_t vocab, int32_t num_shards, void* out, int32_t out_dtype,
+                          float* out2, tfs_device_error* err, void* stream);
 /* Owner side.  tfs_gather_slots: for each slot (o, s) of num_slots regions x cap, the row of id
  * ids[o * ids_stride + s] of the local shard to out + o * out_stride + s * dim (fp32; -1 ids
  * are padding, rows left unwritten).  tfs_scatter_plan_slots / tfs_scatter_add_sgd_planned_slots:

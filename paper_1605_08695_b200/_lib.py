@@ -106,6 +106,8 @@ _SIGNATURES = {
     "tfs_route_reduce_push": ([P, SZ, I64, I64, I32, I64, P, I32, P, P, I64, P, I64, P, SZ, P],
                               I32),
     "tfs_gather_peers": ([P, I64, I32, P, I64, I64, I32, P, I32, P, P], I32),
+    "tfs_gather_peers2": ([P, I64, I32, P, P, I64, I64, I32, P, I32, P, P, P], I32),
+    "tfs_gather2": ([P, I64, I32, P, P, I64, P, I32, P, P, P], I32),
     "tfs_scatter_plan_slots": ([P, I64, I32, I64, I64, I32, P, SZ, P, P], I32),
     "tfs_scatter_add_sgd_planned_slots": ([P, I64, I32, P, SZ, I32, I64, P, I64, F32, P, P, I64,
                                            P, SZ, P], I32),

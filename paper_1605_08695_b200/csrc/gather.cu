@@ -58,11 +58,14 @@ int num_sms() {
 }
 
 // ------------------------------------------------------------------------------------------------
+// table2 / out2 (nullable): a width-1 companion gathered with the same ids (e.g. b with W).
 template <bool BF16OUT>
 __global__ void __launch_bounds__(256) gather_vec4_kernel(const float* __restrict__ table,
                                                           int64_t rows, int32_t dim,
                                                           const int64_t* __restrict__ ids,
                                                           int64_t n, void* __restrict__ out,
+                                                          const float* __restrict__ table2,
+                                                          float* __restrict__ out2,
                                                           tfs_device_error* err) {
   const int lane = threadIdx.x & 31;
   const int n4 = dim >> 2;
@@ -76,6 +79,10 @@ __global__ void __launch_bounds__(256) gather_vec4_kernel(const float* __restric
       id[u] = j < n ? __ldg(ids + j) : 0;
       ok[u] = j < n && id[u] >= 0 && id[u] < rows;
       if (j < n && !ok[u] && id[u] != -1 && lane == 0) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
+    }
+    if (table2 != nullptr && lane < 2) {  // lanes 0 / 1: the companion values of the two rows
+      const bool okl = lane == 0 ? ok[0] : ok[1];
+      if (okl) out2[j0 + lane] = __ldg(table2 + (lane == 0 ? id[0] : id[1]));
     }
     for (int c0 = 0; c0 < n4; c0 += 128) {  // 4 float4 per lane per row per sweep
       float4 v[2][4];
@@ -256,9 +263,11 @@ extern "C" int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int3
   if (vec) {
     const int grid = grid_for_rows(n, 2);
     if (bf)
-      gather_vec4_kernel<true><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
+      gather_vec4_kernel<true><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out,
+                                                     nullptr, nullptr, err);
     else
-      gather_vec4_kernel<false><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
+      gather_vec4_kernel<false><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out,
+                                                      nullptr, nullptr, err);
   } else {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * dim, 256), 8ll * num_sms()));
     if (bf)
@@ -336,6 +345,8 @@ __global__ void __launch_bounds__(256) gather_peers_kernel(const float* const* _
                                                            const int64_t* __restrict__ ids,
                                                            int64_t n, int64_t vocab, int32_t R,
                                                            void* __restrict__ out,
+                                                           const float* const* __restrict__ shards2,
+                                                           float* __restrict__ out2,
                                                            tfs_device_error* err) {
   const int cols = VEC ? dim >> 2 : dim;
   const int64_t total = n * cols;
@@ -351,6 +362,7 @@ __global__ void __launch_bounds__(256) gather_peers_kernel(const float* const* _
     const int64_t o = id % R, local = id / R;
     if (local >= shard_rows) continue;
     const float* src = shards[o] + local * dim;
+    if (shards2 != nullptr && c == 0) out2[t] = shards2[o][local];
     if (VEC) {
       const float4 v = reinterpret_cast<const float4*>(src)[c];
       if (BF16OUT)
@@ -383,7 +395,61 @@ extern "C" int32_t tfs_gather_peers(const float* const* shards, int64_t shard_ro
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
   auto k = vec ? (bf ? gather_peers_kernel<true, true> : gather_peers_kernel<true, false>)
                : (bf ? gather_peers_kernel<false, true> : gather_peers_kernel<false, false>);
-  k<<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab, num_shards, out, err);
+  k<<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab, num_shards, out, nullptr,
+                          nullptr, err);
+  ::tfs::launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+extern "C" int32_t tfs_gather_peers2(const float* const* shards, int64_t shard_rows, int32_t dim,
+                                     const float* const* shards2, const int64_t* ids, int64_t n,
+                                     int64_t vocab, int32_t num_shards, void* out,
+                                     int32_t out_dtype, float* out2, tfs_device_error* err,
+                                     void* stream) {
+  TFS_REQUIRE(n >= 0 && dim >= 1 && shard_rows >= 0 && vocab >= 1 && num_shards >= 1);
+  TFS_REQUIRE(out_dtype == TFS_F32 || out_dtype == TFS_BF16);
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(shards && shards2 && ids && out && out2);
+  TFS_SUPPORTED();
+  cudaStream_t st = as_stream(stream);
+  const bool bf = out_dtype == TFS_BF16;
+  const bool vec = dim % 4 == 0 && ((uintptr_t)out % (bf ? 8 : 16) == 0);
+  const int64_t total = n * (vec ? dim / 4 : dim);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
+  auto k = vec ? (bf ? gather_peers_kernel<true, true> : gather_peers_kernel<true, false>)
+               : (bf ? gather_peers_kernel<false, true> : gather_peers_kernel<false, false>);
+  k<<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab, num_shards, out, shards2, out2,
+                          err);
+  ::tfs::launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+extern "C" int32_t tfs_gather2(const float* table, int64_t rows, int32_t dim, const float* table2,
+                               const int64_t* ids, int64_t n, void* out, int32_t out_dtype,
+                               float* out2, tfs_device_error* err, void* stream) {
+  TFS_REQUIRE(n >= 0 && dim >= 1 && rows >= 0);
+  TFS_REQUIRE(out_dtype == TFS_F32 || out_dtype == TFS_BF16);
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(table && table2 && ids && out && out2);
+  TFS_SUPPORTED();
+  cudaStream_t st = as_stream(stream);
+  const bool bf = out_dtype == TFS_BF16;
+  const bool vec = (dim % 4 == 0) && ((uintptr_t)table % 16 == 0) &&
+                   ((uintptr_t)out % (bf ? 8 : 16) == 0);
+  if (!vec) {  // unaligned / odd widths: the two plain gathers
+    int32_t rc = tfs_gather(table, rows, dim, TFS_F32, ids, n, out, out_dtype, err, stream);
+    if (rc != TFS_OK) return rc;
+    return tfs_gather(table2, rows, 1, TFS_F32, ids, n, out2, TFS_F32, err, stream);
+  }
+  const int grid = grid_for_rows(n, 2);
+  if (bf)
+    gather_vec4_kernel<true><<<grid, 256, 0, st>>>(table, rows, dim, ids, n, out, table2, out2,
+                                                   err);
+  else
+    gather_vec4_kernel<false><<<grid, 256, 0, st>>>(table, rows, dim, ids, n, out, table2, out2,
+                                                    err);
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;

@@ -91,6 +91,16 @@ def gather(table, ids, out_dtype=torch.float32, err: ErrorSlot = None, out=None)
     return out
 
 
+def gather2(table, table2, ids, out, out2, err: ErrorSlot = None):
+    """Gather of a row table and its width-1 companion in one pass: out[j] = table[ids[j]]
+    (fp32 or bf16 per out.dtype), out2[j] = table2[ids[j]]."""
+    od = TFS_BF16 if out.dtype == torch.bfloat16 else TFS_F32
+    check(_lib.lib().tfs_gather2(_p(table), table.shape[0], table.shape[1], _p(table2), _p(ids),
+                                 ids.numel(), _p(out), od, _p(out2), _err(err), _stream()),
+          "tfs_gather2")
+    return out, out2
+
+
 def stitch(positions, rows, err: ErrorSlot = None, out=None):
     """Stitch (P:693-695): out[positions[j]] = rows[j]."""
     n = positions.numel()
@@ -387,6 +397,16 @@ def gather_peers(shard_tab, shard_rows: int, dim: int, ids, vocab: int, R: int, 
                                       ids.numel(), int(vocab), int(R), _p(out), od, _err(err),
                                       _stream()), "tfs_gather_peers")
     return out
+
+
+def gather_peers2(shard_tab, shard_tab2, shard_rows: int, dim: int, ids, vocab: int, R: int,
+                  out, out2, err: ErrorSlot = None):
+    """tfs_gather_peers plus the width-1 companion shards (e.g. b with W) in one pass."""
+    od = TFS_BF16 if out.dtype == torch.bfloat16 else TFS_F32
+    check(_lib.lib().tfs_gather_peers2(_p(shard_tab), int(shard_rows), int(dim), _p(shard_tab2),
+                                       _p(ids), ids.numel(), int(vocab), int(R), _p(out), od,
+                                       _p(out2), _err(err), _stream()), "tfs_gather_peers2")
+    return out, out2
 
 
 def gather_slots(table, ids, ids_stride: int, num_slots: int, cap: int, out, out_stride: int,

@@ -376,8 +376,7 @@ class ShardedStep:
             side.wait_event(ev["q"])
             self.plan_w.build(self.qw, err=self.err)
             ev["plan_w"].record(side)
-        ops.gather(self.W, self.qw, out=self.w_rows, err=self.err)
-        ops.gather(self.b, self.qw, out=self.b_rows.view(-1, 1), err=self.err)
+        ops.gather2(self.W, self.b, self.qw, self.w_rows, self.b_rows, err=self.err)
         main.wait_event(ev["h"])
         self._softmax()
         ev["ssm"].record(main)
@@ -396,8 +395,7 @@ class ShardedStep:
             self._sample(step)
         with self._ph("gather"):  # one shard: Part / Stitch are the identity (see _local_step)
             ops.gather(self.E, self.x, out=self.h, err=self.err)
-            ops.gather(self.W, self.qw, out=self.w_rows, err=self.err)
-            ops.gather(self.b, self.qw, out=self.b_rows.view(-1, 1), err=self.err)
+            ops.gather2(self.W, self.b, self.qw, self.w_rows, self.b_rows, err=self.err)
         with self._ph("sampled_softmax"):
             self._softmax()
         with self._ph("scatter_plan"):
@@ -439,8 +437,8 @@ class ShardedStep:
             self.own_e.build(self.recv_ids, self.istride, err=self.err)
             self.own_w.build(self.recv_ids[:, self.cap_e:], self.istride, err=self.err)
             ev["own"].record(side)
-        ops.gather_peers(self.tab_W, self.shard_rows, d, self.qw, V, R, self.w_rows, err=self.err)
-        ops.gather_peers(self.tab_b, self.shard_rows, 1, self.qw, V, R, self.b_rows, err=self.err)
+        ops.gather_peers2(self.tab_W, self.tab_b, self.shard_rows, d, self.qw, V, R, self.w_rows,
+                          self.b_rows, err=self.err)
         main.wait_event(ev["h"])
         self._softmax()
         ev["ssm"].record(main)

@@ -113,6 +113,63 @@ def test_gather_bit_exact(dim, bf16):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("dim", [512, 64, 3])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_gather2_rows_and_companion_bit_exact(dim, bf16):
+    """W rows and their bias in one pass == two oracle Gathers; padding ids leave both unwritten,
+    a bad id is reported at its position."""
+    rng = np.random.default_rng(dim + 1)
+    table = rng.standard_normal((5000, dim)).astype(np.float32)
+    bias = rng.standard_normal(5000).astype(np.float32)
+    ids = rng.integers(0, 5000, 3001)
+    ids[:100] = 7
+    ids[200] = -1
+    od = torch.bfloat16 if bf16 else torch.float32
+    out = torch.full((ids.size, dim), 3.0, dtype=od, device=DEV)
+    out2 = torch.full((ids.size,), 5.0, device=DEV)
+    err = ops.ErrorSlot(DEV)
+    ops.gather2(T(table), T(bias), T(ids), out, out2, err=err)
+    assert err.read()[0] == 0
+    keep = ids != -1
+    ref = oracle.gather(table, ids[keep], bf16=bf16)
+    got = out.cpu().view(torch.int16).numpy().view(np.uint16) if bf16 else out.cpu().numpy()
+    assert np.array_equal(got[keep], ref)
+    assert np.array_equal(out2.cpu().numpy()[keep], oracle.gather(bias.reshape(-1, 1), ids[keep])[:, 0])
+    assert float(out2[200]) == 5.0 and float(out[200, 0].float()) == 3.0
+    ids[2500] = 5000
+    ops.gather2(T(table), T(bias), T(ids), out, out2, err=err)
+    assert err.read() == (2, 2500)
+
+
+@pytest.mark.parametrize("R", [1, 3, 4])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_gather_peers2_simulated_shards(R, bf16):
+    """The one-sided routed Gather (shard id % R, row id // R) through a pointer table, with the
+    bias companion; R shards simulated on one GPU; == the oracle's Gather of the logical table."""
+    rng = np.random.default_rng(R)
+    V, d = 3001, 64
+    W = rng.standard_normal((V, d)).astype(np.float32)
+    b = rng.standard_normal(V).astype(np.float32)
+    rows = -(-V // R)
+    sh = [torch.zeros((rows, d), device=DEV) for _ in range(R)]
+    sb = [torch.zeros(rows, device=DEV) for _ in range(R)]
+    for r in range(R):
+        n_r = W[r::R].shape[0]
+        sh[r][:n_r] = T(W[r::R])
+        sb[r][:n_r] = T(b[r::R])
+    tab = torch.tensor([t.data_ptr() for t in sh], dtype=torch.int64, device=DEV)
+    tab2 = torch.tensor([t.data_ptr() for t in sb], dtype=torch.int64, device=DEV)
+    ids = workloads.zipf_ids(rng, V, 1.0, 2000)
+    od = torch.bfloat16 if bf16 else torch.float32
+    out = torch.empty((ids.size, d), dtype=od, device=DEV)
+    out2 = torch.empty(ids.size, device=DEV)
+    ops.gather_peers2(tab, tab2, rows, d, T(ids), V, R, out, out2)
+    ref = oracle.gather(W, ids, bf16=bf16)
+    got = out.cpu().view(torch.int16).numpy().view(np.uint16) if bf16 else out.cpu().numpy()
+    assert np.array_equal(got, ref)
+    assert np.array_equal(out2.cpu().numpy(), b[ids])
+
+
 def test_gather_out_of_range():
     err = ops.ErrorSlot(DEV)
     table = T(np.zeros((10, 8), np.float32))
