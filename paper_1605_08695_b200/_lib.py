@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libtfs.so")
+SO_PATH = os.environ.get("TFS_LIB") or os.path.join(HERE, "libtfs.so")  # TFS_LIB: a variant build
 HEADER = os.path.join(os.path.dirname(HERE), "include", "tfs.h")
 
 TFS_OK = 0

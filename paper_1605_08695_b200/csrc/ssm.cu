@@ -122,7 +122,8 @@ static void stage_plan(Params& P) {
   for (int i = 0; i < P.nprob; ++i) bmax = std::max(bmax, P.p[i].bn / kCta * BK * 2);
   P.b_stride = (bmax + 1023) / 1024 * 1024;
   const int fixed = (MODE == kStats ? 0 : kEpiSmem) + kCbSmem + kBarBytes;
-  P.stages = std::min<int>(kMaxStages, ((int)kSmemBytes - fixed) / (A_BYTES + P.b_stride));
+  P.stages =
+      std::min<int>(kMaxStages, ((int)kSmemBytes - fixed) / (KSUB * (A_BYTES + P.b_stride)));
 }
 
 template <int MODE, bool LAB = false>

@@ -41,6 +41,10 @@ static_assert(kCta == 1 || kCta == 2, "kCta");
 constexpr int BM = 128, BN = 256, BK = 64;      // BM: rows per CTA; BN: tile N
 constexpr int STAGES = kCta == 2 ? 6 : 4;       // stages at the widest tile (BN); a launch with
 constexpr int kMaxStages = 8;                   // narrower tiles / no staging fits more (Params)
+#ifndef TFS_KSUB
+#define TFS_KSUB 2
+#endif
+constexpr int KSUB = TFS_KSUB;                  // k-blocks per pipeline stage (one barrier each)
 constexpr int PM = kCta * BM;                   // rows per tile
 constexpr int BNC = BN / kCta;                  // B rows per CTA
 constexpr int kEpiWarps = 8;
@@ -341,8 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const int STAGES = P.stages;
   const int B_BYTES = P.b_stride;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint8_t* sE = sB + STAGES * B_BYTES;                 // epilogue staging (not for STATS)
+  uint8_t* sB = smem + STAGES * KSUB * A_BYTES;
+  uint8_t* sE = sB + STAGES * KSUB * B_BYTES;          // epilogue staging (not for STATS)
   float* sCb = reinterpret_cast<float*>(sE + (MODE == kStats ? 0 : kEpiSmem));  // [acc][half][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCb) + kCbSmem);
   uint64_t* empty = full + kMaxStages;
@@ -397,7 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                                        : (uint32_t)((q.bn / kCta) * BK * 2);  // box: bn/kCta rows
         const int arow = t.mt * PM + (int)rank * BM;
         const int bcol = t.nt * q.bn + (int)rank * nh;
-        for (int kb = t.kb0; kb < t.kb1; ++kb) {
+        for (int kb0 = t.kb0; kb0 < t.kb1; kb0 += KSUB) {
+          const int ns = min(KSUB, t.kb1 - kb0);
           mbar_wait(empty + stage, phase ^ 1);
           // the leader's barrier (peer bit cleared)
           const uint32_t fb = smem_u32(full + stage) & (kCta == 2 ? 0xFEFFFFFFu : 0xFFFFFFFFu);
@@ -406,21 +411,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
 #endif
-          if (leader) mbar_expect_tx(full + stage, kCta * (A_BYTES + bbytes));
-          uint8_t* a = sA + stage * A_BYTES;
-          uint8_t* b = sB + stage * B_BYTES;
-          if (q.a_mn) {
+          if (leader) mbar_expect_tx(full + stage, kCta * ns * (A_BYTES + bbytes));
+          for (int sb = 0; sb < ns; ++sb) {
+            const int kb = kb0 + sb;
+            uint8_t* a = sA + (stage * KSUB + sb) * A_BYTES;
+            uint8_t* b = sB + (stage * KSUB + sb) * B_BYTES;
+            if (q.a_mn) {
 #pragma unroll
-            for (int i = 0; i < BM / kMNBox; ++i)
-              tma_load_2d_pair(a + i * kMNBoxBytes, &q.ta, arow + i * kMNBox, kb * BK, fb);
-          } else {
-            tma_load_2d_pair(a, &q.ta, kb * BK, arow, fb);
-          }
-          if (q.b_mn) {
-            for (int i = 0; i < bboxes; ++i)
-              tma_load_2d_pair(b + i * kMNBoxBytes, &q.tb, bcol + i * kMNBox, kb * BK, fb);
-          } else {
-            tma_load_2d_pair(b, &q.tb, kb * BK, bcol, fb);
+              for (int i = 0; i < BM / kMNBox; ++i)
+                tma_load_2d_pair(a + i * kMNBoxBytes, &q.ta, arow + i * kMNBox, kb * BK, fb);
+            } else {
+              tma_load_2d_pair(a, &q.ta, kb * BK, arow, fb);
+            }
+            if (q.b_mn) {
+              for (int i = 0; i < bboxes; ++i)
+                tma_load_2d_pair(b + i * kMNBoxBytes, &q.tb, bcol + i * kMNBox, kb * BK, fb);
+            } else {
+              tma_load_2d_pair(b, &q.tb, kb * BK, bcol, fb);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -441,19 +449,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = t.kb0; kb < t.kb1; ++kb) {
+        for (int kb0 = t.kb0; kb0 < t.kb1; kb0 += KSUB) {
+          const int ns = min(KSUB, t.kb1 - kb0);
           mbar_wait(full + stage, phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+          for (int sb = 0; sb < ns; ++sb) {
+            const int kb = kb0 + sb;
+            const uint32_t a0 = smem_u32(sA + (stage * KSUB + sb) * A_BYTES);
+            const uint32_t b0 = smem_u32(sB + (stage * KSUB + sb) * B_BYTES);
 #ifndef TFS_EXP_NO_MMA
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
-                      (kb > t.kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
+                        (kb > t.kb0 || k > 0) ? 1u : 0u);
 #else
-          (void)a0; (void)b0; (void)d_tmem;
+            (void)a0; (void)b0; (void)d_tmem; (void)kb;
 #endif
+          }
           umma_commit_pair(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
