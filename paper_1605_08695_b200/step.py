@@ -365,10 +365,10 @@ class ShardedStep:
         # plans (id sorts) depend only on the ids, so they are built on the side stream while
         # the main stream samples, gathers and runs the sampled softmax.
         ev = self.ev
-        with torch.cuda.stream(side):                      # E path
+        with torch.cuda.stream(side):                      # E path: h first (the softmax
+            ops.gather(self.E, self.x, out=self.h, err=self.err)   # waits for it), then the
+            ev["h"].record(side)                           # plan of the E update
             self.plan_e.build(self.x, err=self.err)
-            ops.gather(self.E, self.x, out=self.h, err=self.err)
-            ev["h"].record(side)
         self.qw[:B].copy_(self.y)                          # W path
         self._sample(step)
         ev["q"].record(main)
@@ -421,11 +421,11 @@ class ShardedStep:
         self.hdl_ids.barrier(channel=0)                             # B0
         side.wait_stream(main)
         io = rank * self.istride
-        with torch.cuda.stream(side):                               # E path
-            self.route_e.build_push(self.x, self.tab_ids, io, counts=self.counts[0],
-                                    err=self.err)
+        with torch.cuda.stream(side):                               # E path: h first
             ops.gather_peers(self.tab_E, self.shard_rows, d, self.x, V, R, self.h, err=self.err)
             ev["h"].record(side)
+            self.route_e.build_push(self.x, self.tab_ids, io, counts=self.counts[0],
+                                    err=self.err)
         self.qw[:B].copy_(self.y)                                   # W path
         self._sample(step)
         ev["q"].record(main)
