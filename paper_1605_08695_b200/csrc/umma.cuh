@@ -647,20 +647,48 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
           ++nst;
         } else {
-          if (q.g != nullptr && row_ok) {
+          if (q.g != nullptr && row_ok) {  // + g[row] * bf16(wt[row, col0 .. col0 + 31])
             const float gr = q.g[row];
             const int64_t w0 = (int64_t)row * q.ldw + col0;
             const int N = q.N;
             if (q.wt_bf16) {
               const uint16_t* w = static_cast<const uint16_t*>(q.wt) + w0;
+              if (col0 + 32 <= N && (q.ldw & 7) == 0) {  // this row's 64 bytes: 4 vector loads
+                uint4 u[4];
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (col0 + i < N) v[i] += gr * __uint_as_float((uint32_t)w[i] << 16);
+                for (int k = 0; k < 4; ++k) u[k] = __ldg(reinterpret_cast<const uint4*>(w) + k);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint32_t p[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    v[8 * k + 2 * j] += gr * __uint_as_float(p[j] << 16);
+                    v[8 * k + 2 * j + 1] += gr * __uint_as_float(p[j] & 0xffff0000u);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < N) v[i] += gr * __uint_as_float((uint32_t)w[i] << 16);
+              }
             } else {
               const float* w = static_cast<const float*>(q.wt) + w0;
+              if (col0 + 32 <= N && (q.ldw & 3) == 0) {  // 128 bytes: 8 vector loads
+                float4 f[8];
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (col0 + i < N) v[i] += gr * bf16_round(w[i]);
+                for (int k = 0; k < 8; ++k) f[k] = __ldg(reinterpret_cast<const float4*>(w) + k);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  v[4 * k] += gr * bf16_round(f[k].x);
+                  v[4 * k + 1] += gr * bf16_round(f[k].y);
+                  v[4 * k + 2] += gr * bf16_round(f[k].z);
+                  v[4 * k + 3] += gr * bf16_round(f[k].w);
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < N) v[i] += gr * bf16_round(w[i]);
+              }
             }
           }
 #pragma unroll
