@@ -403,21 +403,23 @@ __global__ void to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
 // are added in row-group order (fixed summation order, no atomics).  Also returns the candidate
 // map to all-zero (the GRAD pass was its last reader), and one extra block forms
 // loss_sum = c * sum_t loss_t (fixed-order tree) when loss_sum != nullptr.
-constexpr int kColsumChunks = 4, kColsumGroups = 64;
-__global__ void __launch_bounds__(256) g_colsum_kernel(const uint16_t* G, int64_t B, int64_t S,
-                                                       int64_t ldG, float* db_s,
-                                                       const int64_t* sampled, int2* cmap,
-                                                       int64_t vocab, const float* loss, float c,
-                                                       float* loss_sum) {
+// GROUPS row groups per block (4 GROUPS threads): 64 when there are enough 32-column blocks to
+// fill the GPU, 256 for narrow G (few column blocks: more rows in flight per block).
+constexpr int kColsumChunks = 4;
+template <int GROUPS>
+__global__ void __launch_bounds__(kColsumChunks * GROUPS) g_colsum_kernel(
+    const uint16_t* G, int64_t B, int64_t S, int64_t ldG, float* db_s, const int64_t* sampled,
+    int2* cmap, int64_t vocab, const float* loss, float c, float* loss_sum) {
+  constexpr int kColsumGroups = GROUPS, kColsumThreads = kColsumChunks * GROUPS;
   __shared__ float red[kColsumGroups][kColsumChunks * 8 + 1];
   const int64_t ncol_blocks = cdiv_dev(S, kColsumChunks * 8);
   if (blockIdx.x >= ncol_blocks) {  // the loss-sum block
     float acc = 0.f;
-    for (int64_t t = threadIdx.x; t < B; t += 256) acc += loss[t];
+    for (int64_t t = threadIdx.x; t < B; t += kColsumThreads) acc += loss[t];
     float* r = &red[0][0];
     r[threadIdx.x] = acc;
     __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
+    for (int s = kColsumThreads / 2; s > 0; s >>= 1) {
       if (threadIdx.x < s) r[threadIdx.x] += r[threadIdx.x + s];
       __syncthreads();
     }
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(256) g_colsum_kernel(const uint16_t* G, int64_
     }
   };
   if (c0 < S) {
-    constexpr int U = 8;
+    constexpr int U = GROUPS >= 256 ? 4 : 8;  // independent row loads in flight per thread
     const uint16_t* p = G + c0;
     int64_t r = rg;
     for (; r + (U - 1) * kColsumGroups < B; r += U * kColsumGroups) {
@@ -459,10 +461,22 @@ __global__ void __launch_bounds__(256) g_colsum_kernel(const uint16_t* G, int64_
 #pragma unroll
   for (int k = 0; k < 8; ++k) red[rg][chunk * 8 + k] = acc[k];
   __syncthreads();
-  if (threadIdx.x < kColsumChunks * 8) {
-    const int64_t col = (int64_t)blockIdx.x * (kColsumChunks * 8) + threadIdx.x;
+  // fixed-order tree over the row groups: 8 parts of 32 groups, then the 8 part sums
+  constexpr int kCols = kColsumChunks * 8, kParts = 8;
+  __shared__ float part[kParts][kCols];
+  if (threadIdx.x < kParts * kCols) {
+    const int col = threadIdx.x % kCols, pt = threadIdx.x / kCols;
     float sum = 0.f;
-    for (int g = 0; g < kColsumGroups; ++g) sum += red[g][threadIdx.x];
+    for (int g = pt * (kColsumGroups / kParts); g < (pt + 1) * (kColsumGroups / kParts); ++g)
+      sum += red[g][col];
+    part[pt][col] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x < kCols) {
+    const int64_t col = (int64_t)blockIdx.x * kCols + threadIdx.x;
+    float sum = 0.f;
+#pragma unroll
+    for (int pt = 0; pt < kParts; ++pt) sum += part[pt][threadIdx.x];
     if (col < S) db_s[col] = sum;
   }
 }
@@ -811,9 +825,14 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
                                           w.Sp, st);
   if (rc != TFS_OK) return rc;
   mark(a, 4, st);
-  g_colsum_kernel<<<(unsigned)(cdiv(S, kColsumChunks * 8) + (a->loss_sum ? 1 : 0)), 256, 0, st>>>(
-      w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab, a->loss,
-      a->grad_scale, a->loss_sum);
+  {
+    const int64_t ncb = cdiv(S, kColsumChunks * 8);
+    const bool narrow = ncb < num_sms();
+    auto colsum = narrow ? g_colsum_kernel<256> : g_colsum_kernel<64>;
+    colsum<<<(unsigned)(ncb + (a->loss_sum ? 1 : 0)), kColsumChunks * (narrow ? 256 : 64), 0,
+             st>>>(w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
+                   a->loss, a->grad_scale, a->loss_sum);
+  }
   launched();
   mark(a, 5, st);
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
