@@ -708,13 +708,18 @@ __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int
   }
 }
 
-constexpr int kBlk = 16;  // chunks per block of the second reduction level
+// Chunks per block of the second reduction level: 8 for short inputs (level A then reads its
+// slots in two rounds instead of four), 16 for long ones (level B walks fewer blocks of a
+// heavy segment).
+constexpr int kBlkLong = 16, kBlkShort = 8;
+constexpr int64_t kBlkShortMaxChunks = 2048;
 
 // Level A, one thread per (block of kBlk chunks, float4 column): the block's partial slots are
 // read in chunk order and every RUN of consecutive slots owned by the same segment is summed in
 // that order into the run's first slot (in place; the thread owns its block's slots of its
 // column).  A crossing segment then has one run per block it touches, starting at slot
 // 2 c0 + 1 (c0 = its first chunk) and at slot 2 kBlk b for every later block b.
+template <int kBlk>
 __global__ void __launch_bounds__(256) seg_cross_a_vec4_kernel(SegJob j, int64_t nchunks) {
   const int n4 = j.dim >> 2;
   const int64_t nblk = (nchunks + kBlk - 1) / kBlk;
@@ -774,7 +779,7 @@ __global__ void __launch_bounds__(256) seg_cross_a_vec4_kernel(SegJob j, int64_t
 
 // Level B, one thread per (segment crossing a chunk boundary, float4 column): its run sums
 // added in block order, then T[key] = fl32(T - lr * sum) (apply) or written out.
-template <int OPT>
+template <int OPT, int kBlk>
 __global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
   const uint32_t ncross = *j.cross_count;
   const int n4 = j.dim >> 2;
@@ -1247,14 +1252,22 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
     chunk_k<<<vgrid, 256, 0, st>>>(j, nslices);
     launched();
     const int64_t n4 = j.dim >> 2;
-    const int64_t awork = cdiv(nchunks, kBlk) * n4;
+    const bool shortn = nchunks <= kBlkShortMaxChunks;
+    const int kb = shortn ? kBlkShort : kBlkLong;
+    const int64_t awork = cdiv(nchunks, kb) * n4;
     const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(awork, 256), 8 * num_sms()));
-    seg_cross_a_vec4_kernel<<<agrid, 256, 0, st>>>(j, nchunks);
+    auto cross_a = shortn ? seg_cross_a_vec4_kernel<kBlkShort> : seg_cross_a_vec4_kernel<kBlkLong>;
+    cross_a<<<agrid, 256, 0, st>>>(j, nchunks);
     launched();
     const int64_t bwork = (nchunks + 1) * n4;  // crossing segments <= chunks
     const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(bwork, 256), 4 * num_sms()));
-    auto cross_k = j.opt == 1 ? seg_cross_b_vec4_kernel<1>
-                              : (j.opt == 2 ? seg_cross_b_vec4_kernel<2> : seg_cross_b_vec4_kernel<0>);
+    auto cross_k =
+        shortn ? (j.opt == 1 ? seg_cross_b_vec4_kernel<1, kBlkShort>
+                             : (j.opt == 2 ? seg_cross_b_vec4_kernel<2, kBlkShort>
+                                           : seg_cross_b_vec4_kernel<0, kBlkShort>))
+               : (j.opt == 1 ? seg_cross_b_vec4_kernel<1, kBlkLong>
+                             : (j.opt == 2 ? seg_cross_b_vec4_kernel<2, kBlkLong>
+                                           : seg_cross_b_vec4_kernel<0, kBlkLong>));
     cross_k<<<bgrid, 256, 0, st>>>(j);
     launched();
   } else {
