@@ -560,17 +560,24 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= B) return;
-  // d % 64 == 0 on this path: vector loads, all of a lane's loads issued together
+  // d % 64 == 0 on this path: vector loads.  Every load of the token -- h and w_true (kept in
+  // registers for dw_true = g h when d <= 512), its bias and the stats partials (when at most
+  // 128) -- is issued before any result is needed: one memory round trip.
   const int n4 = d >> 2;
   const int64_t r4 = t * n4;  // this token's first group of four
+  const float2* st_t = stats + t * nparts;  // this token's partials, contiguous
+  const bool regs = n4 <= 128 && nparts <= 128;
+  float4 a[4], b[4];
+  float2 sp[4];
   float part = 0.f;
-  for (int k0 = lane; k0 < n4; k0 += 128) {
-    float4 a[4], b[4];
+  const float bt = b_true[t], lt = le_true ? le_true[t] : 0.f;
+  if (regs) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int k = k0 + 32 * u;
+      const int k = lane + 32 * u;
       a[u] = k < n4 ? ld4_bf<BIN>(h, r4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
       b[u] = k < n4 ? ld4_bf<BIN>(w_true, r4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      sp[u] = k < nparts ? st_t[k] : make_float2(-INFINITY, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -579,29 +586,63 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
       part = fmaf(a[u].z, b[u].z, part);
       part = fmaf(a[u].w, b[u].w, part);
     }
+  } else {
+    for (int k0 = lane; k0 < n4; k0 += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + 32 * u;
+        a[u] = k < n4 ? ld4_bf<BIN>(h, r4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        b[u] = k < n4 ? ld4_bf<BIN>(w_true, r4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        part = fmaf(a[u].x, b[u].x, part);
+        part = fmaf(a[u].y, b[u].y, part);
+        part = fmaf(a[u].z, b[u].z, part);
+        part = fmaf(a[u].w, b[u].w, part);
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-  const float z = part + b_true[t] - (le_true ? le_true[t] : 0.f);
+  const float z = part + bt - lt;
   const float z2 = z * umma::kLog2e;
   float m = z2;
-  const float2* st_t = stats + t * nparts;  // this token's partials, contiguous
-  for (int p = lane; p < nparts; p += 32) m = fmaxf(m, st_t[p].x);
+  if (regs) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m = fmaxf(m, sp[u].x);
+  } else {
+    for (int p = lane; p < nparts; p += 32) m = fmaxf(m, st_t[p].x);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   float s = lane == 0 ? exp2f(z2 - m) : 0.f;
-  for (int p = lane; p < nparts; p += 32) {
-    const float2 st = st_t[p];
-    if (st.y > 0.f) s += st.y * exp2f(st.x - m);
+  if (regs) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (sp[u].y > 0.f) s += sp[u].y * exp2f(sp[u].x - m);
+  } else {
+    for (int p = lane; p < nparts; p += 32) {
+      const float2 st = st_t[p];
+      if (st.y > 0.f) s += st.y * exp2f(st.x - m);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   const float lse = (m + log2f(s)) * 0.6931471805599453f;
   const float g = c * (expf(z - lse) - 1.f);
   float4* dw4 = reinterpret_cast<float4*>(dw_true + t * d);
-  for (int k = lane; k < n4; k += 32) {
-    const float4 a = ld4_bf<BIN>(h, r4 + k);
-    dw4[k] = make_float4(g * a.x, g * a.y, g * a.z, g * a.w);
+  if (regs) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = lane + 32 * u;
+      if (k < n4) dw4[k] = make_float4(g * a[u].x, g * a[u].y, g * a[u].z, g * a[u].w);
+    }
+  } else {
+    for (int k = lane; k < n4; k += 32) {
+      const float4 x = ld4_bf<BIN>(h, r4 + k);
+      dw4[k] = make_float4(g * x.x, g * x.y, g * x.z, g * x.w);
+    }
   }
   if (lane == 0) {
     if (loss) loss[t] = lse - z;
