@@ -9,11 +9,13 @@ ScatterAdd-SGD -- over one synthetic batch of B tokens per GPU (weak scaling: B 
 Default workload X: V = 800,000, d = 512, B = 2,560 (128 x 20) per GPU, S = 8,192 per GPU,
 Zipf(1.0) ids, bf16 tensor-core operands with fp32 accumulation and fp32 master tables.
 
-Timing: W untimed warm-up steps; K timed steps, each preceded by an L2 flush (a 256 MiB write,
-outside the timed interval); per-step CUDA events on the launching stream; barrier + sync on
-both sides; max over ranks.  value = N*B*K / max-rank time.  e2e: the same K steps through the
-public API with the inputs copied from pinned host memory and the loss read back every step.
-``--impl reference`` times the CPU oracle (the reference arm of this tier).
+The step is the native stepper of libtfs (tfs_step_*; one CUDA graph per step, one process per
+GPU, tfs_comm over NVLink for R > 1).  Timing: W untimed warm-up steps; K timed steps, each
+preceded by an L2 flush (a 256 MiB write, outside the timed interval); per-step CUDA events on
+the launching stream; barrier + sync on both sides; max over ranks.  value = N*B*K / max-rank
+time.  e2e: the same K steps through the C-ABI call tfs_step_run with HOST buffers: the H2D
+copies of x, y from pinned memory and the D2H copy of the loss happen inside the call, every
+step.  ``--impl reference`` times the CPU oracle (the reference arm of this tier).
 """
 from __future__ import annotations
 
@@ -54,8 +56,8 @@ def parse():
                         "from a 1 GB and a 16 GB embedding sharded over the GPUs")
     p.add_argument("--optimizer", default="sgd", choices=["sgd", "momentum", "adagrad"],
                    help="sparse optimizer of the ScatterAdd step (1 GPU; the paper uses SGD)")
-    p.add_argument("--route", default="p2p", choices=["p2p", "nccl"],
-                   help="R > 1 transport: one-sided NVLink (symmetric memory) or NCCL a2a")
+    p.add_argument("--cap", type=int, default=0,
+                   help="R > 1 route slots per owner (0 = the worst case, never overflows)")
     return p.parse_args()
 
 
@@ -202,25 +204,58 @@ def graph_kernel_nodes(graph):
         return None
 
 
-def run_null_step(args, world, rank, dev, router):
+def host_info():
+    """Host cores and CPU model of the box the oracle baseline runs on."""
+    model = None
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
+
+
+def so_info():
+    import hashlib
+    from paper_1605_08695_b200 import _lib
+    with open(_lib.SO_PATH, "rb") as f:
+        h = hashlib.sha256(f.read()).hexdigest()[:16]
+    return {"path": os.path.relpath(_lib.SO_PATH, ROOT), "sha256_16": h,
+            "product": _lib.SO_PATH == _lib.PRODUCT_SO}
+
+
+def run_null_step(args, world, rank, dev):
     """The paper's sparse null step: "Each worker reads 32 randomly selected
     entries from a large embedding matrix containing 1 GB or 16 GB of data ... step times do
     not vary with the size of the embedding ... 5 to 20 ms".  Here: fp32 rows of 512, the
     matrix sharded by id mod R over the GPUs; one step = 32 fresh random ids per worker and
     their rows gathered (R = 1: tfs_gather; R > 1: tfs_gather_peers, one-sided NVLink pulls
-    from symmetric-memory shards behind a device barrier).  Reported: median step time."""
+    from the tfs_comm heaps behind a device barrier).  Reported: median step time."""
     import torch
     from paper_1605_08695_b200 import ops
+    from paper_1605_08695_b200 import step as gstep
+    from paper_1605_08695_b200 import _lib
     d, n_ids, steps = 512, 32, max(args.steps, 50)
     out = {}
     for gb in (1, 16):
         V = gb * (1 << 30) // (4 * d)
         rows = -(-V // world)
+        comm = None
         if world > 1:
-            import torch.distributed._symmetric_memory as symm_mem
-            shard = symm_mem.empty((rows, d), dtype=torch.float32, device=dev)
-            hdl = symm_mem.rendezvous(shard, router.group_name)
-            tab = torch.tensor(list(hdl.buffer_ptrs), dtype=torch.int64, device=dev)
+            import ctypes
+            p = ctypes.c_void_p()
+            L = _lib.lib()
+            _lib.check(L.tfs_comm_create(world, rank, 1, dev.index, 65536 + 4 * rows * d, 60000,
+                                         ctypes.byref(p)), "tfs_comm_create")
+            h = ctypes.create_string_buffer(64)
+            _lib.check(L.tfs_comm_export(p, h), "tfs_comm_export")
+            _lib.check(L.tfs_comm_connect(p, gstep.exchange_handles(h.raw)), "tfs_comm_connect")
+            comm = gstep.Comm(p, world, rank, 1, dev)
+            shard = gstep.device_tensor(comm.heap() + 65536, (rows, d), torch.float32, dev)
+            tab = comm.peer_bases() + 65536
         else:
             shard = torch.empty((rows, d), dtype=torch.float32, device=dev)
         shard.uniform_(-0.5, 0.5)
@@ -232,13 +267,13 @@ def run_null_step(args, world, rank, dev, router):
         for i in range(args.warmup + steps):
             ids.random_(0, V, generator=gen)
             torch.cuda.synchronize()
-            if world > 1:
-                hdl.barrier(channel=0)
+            if comm is not None:
+                comm.barrier(0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            if world > 1:
+            if comm is not None:
                 ops.gather_peers(tab, rows, d, ids, V, world, res, err=err)
-                hdl.barrier(channel=1)
+                comm.barrier(1)
             else:
                 ops.gather(shard, ids, out=res, err=err)
             e1.record()
@@ -250,6 +285,8 @@ def run_null_step(args, world, rank, dev, router):
         if world > 1:
             import torch.distributed as dist
             dist.all_reduce(med, op=dist.ReduceOp.MAX)
+            dist.barrier()
+            comm.close()
         out[f"{gb}GB"] = {"median_ms": float(med.item()), "rows": V,
                           "p10_ms": float(np.percentile(times, 10)),
                           "p90_ms": float(np.percentile(times, 90))}
@@ -262,10 +299,6 @@ def run_null_step(args, world, rank, dev, router):
                           "data": "synthetic", "config": {"workload": "null-step", "dim": d,
                           "lookups_per_worker": n_ids, "transport": "p2p" if world > 1
                           else "local"}, "paper_ms": [5, 20], "results": out}), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 def main():
@@ -276,7 +309,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1605_08695_b200 import _lib, ops
+    from paper_1605_08695_b200 import _lib
     from paper_1605_08695_b200 import step as gstep
     from paper_1605_08695_b200._lib import TFS_BF16, TFS_F32
 
@@ -285,12 +318,13 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    router = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        router = gstep.Router()
     if args.null_step:
-        run_null_step(args, world, rank, dev, router)
+        run_null_step(args, world, rank, dev)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
         return
     w = workloads.WORKLOADS[args.workload]
     R = world
@@ -298,11 +332,15 @@ def main():
     S = w.num_sampled
     d = w.dim
     dtype = TFS_BF16 if args.dtype == "bf16" else TFS_F32
-    cfg = gstep.StepConfig(vocab=w.vocab, dim=d, tokens=B, num_sampled=S, lr=0.1,
+    cfg = gstep.StepConfig(vocab=w.vocab, dim=d, tokens=B, num_sampled=S, num_shards=R, lr=0.1,
                            seed=workloads.SAMPLER_SEED, operand_dtype=dtype,
-                           full_softmax=(S == 0), route=args.route, optimizer=args.optimizer)
+                           optimizer=args.optimizer, cap_e=args.cap, cap_w=args.cap)
+    comm = gstep.Comm.distributed(cfg, timeout_ms=60000) if R > 1 else None
+    st = gstep.Step(cfg, comm)
     E, W, b = workloads.tables_device(w.vocab, d, R, rank, dev)
-    st = gstep.ShardedStep(cfg, E, W, b, router)
+    st.load_tables(E, W, b)
+    del E, W, b
+    st.sync()
     # 16 distinct pre-generated batches per rank, resident in HBM and in pinned host memory.
     xs_h, ys_h = [], []
     for i in range(N_BATCHES):
@@ -321,35 +359,20 @@ def main():
         torch.cuda.synchronize()
 
     # ---- one counted eager step: how many libtfs kernels a step launches
+    barrier()
     c0 = L.tfs_debug_launch_count()
-    st.run(xs_d[0], ys_d[0], 0)
+    st.run(xs_d[0], ys_d[0])
     torch.cuda.synchronize()
     launches_per_step = L.tfs_debug_launch_count() - c0
-    st.err.check("bench step")
-    step_no = 1
-    if R > 1:  # size the fixed-capacity route slots from the observed distinct-id counts
-        caps = st.calibrate_routes()
-        st.run(xs_d[1], ys_d[1], step_no)
-        step_no += 1
-        torch.cuda.synchronize()
-        st.err.check("bench step after route calibration")
-
+    st.check("bench step")
+    kernel_nodes = None
     if use_graph:
-        st.x.copy_(xs_d[0])
-        st.y.copy_(ys_d[0])
-        st.capture(first_step=step_no)
-        kernel_nodes = graph_kernel_nodes(st.graph)
+        barrier()
+        st.capture()
+        kernel_nodes = st.graph_kernels()
 
     def one_step(i):
-        nonlocal step_no
-        if use_graph:
-            st.x.copy_(xs_d[i % N_BATCHES])
-            st.y.copy_(ys_d[i % N_BATCHES])
-            out = st.replay()
-        else:
-            out = st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], step_no)
-        step_no += 1
-        return out
+        return st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES])
 
     for i in range(args.warmup):
         one_step(i)
@@ -369,7 +392,7 @@ def main():
         ends[i].record()
     barrier()
     t_wall1 = time.time()
-    per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    per_step = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
     local_ms = sum(per_step)
     clk = clocks.finish(t_wall0, t_wall1)
     if world > 1:
@@ -378,27 +401,18 @@ def main():
         total_ms = float(tt.item())
     else:
         total_ms = local_ms
-    st.err.check("bench timed steps")
+    st.check("bench timed steps")
     words = R * B * args.steps
     value = words / (total_ms / 1e3)
 
-    # ---- e2e: public API with host buffers (H2D of x, y and D2H of the loss every step)
+    # ---- e2e: the C-ABI step call with HOST buffers (H2D of x, y and D2H of the loss inside)
     loss_host = torch.empty(args.steps, dtype=torch.float32).pin_memory()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        if use_graph:
-            st.x.copy_(xs_h[i % N_BATCHES], non_blocking=True)
-            st.y.copy_(ys_h[i % N_BATCHES], non_blocking=True)
-            out = st.replay()
-        else:
-            xd = xs_h[i % N_BATCHES].to(dev, non_blocking=True)
-            yd = ys_h[i % N_BATCHES].to(dev, non_blocking=True)
-            out = st.run(xd, yd, step_no)
-        step_no += 1
-        loss_host[i:i + 1].copy_(out, non_blocking=True)
+        st.run_host(xs_h[i % N_BATCHES], ys_h[i % N_BATCHES], loss_host[i:i + 1])
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
@@ -408,52 +422,34 @@ def main():
         e2e_ms = float(tt.item())
     assert np.all(np.isfinite(loss_host.numpy()))
     e2e_value = words / (e2e_ms / 1e3)
+    st.check("bench e2e steps")
 
-    # ---- instrumented eager steps: per-phase device time (roofline of the dominant op)
-    phases = {}
+    # ---- instrumented eager steps: per-phase (R = 1, serial) and per-GEMM device time
+    if use_graph:
+        st.uncapture()
     n_ph = max(1, min(args.phase_steps, args.steps))
-    kern_ms = {}
-    call_ms = None
-    if not st.full_sharded:
-        if R == 1:  # the R = 1 step also brackets its phases (the R > 1 step runs overlapped)
-            st.phase_events = []
-        ssm_ev = []
-        for i in range(n_ph):
-            flush.zero_()
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
-            for e in evs:
-                e.record()  # creates the CUDA events; the library re-records them in the call
-            st.ssm_events = evs
-            st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], step_no)
-            ssm_ev.append(evs)
-            step_no += 1
-        torch.cuda.synchronize()
-        st.ssm_events = None
-        for name, s_, e_ in st.phase_events or []:
-            phases.setdefault(name, []).append(s_.elapsed_time(e_))
-        st.phase_events = None
-        phases = {k: sum(v) / len(v) for k, v in phases.items()}
-        if dtype == TFS_BF16:  # per-GEMM-launch durations, CUDA events on its stream
-            for name, (i0, i1) in (("gemm_stats", (1, 2)), ("gemm_grad", (3, 4)),
-                                   ("gemm_store", (5, 6))):
-                kern_ms[name] = sum(ev[i0].elapsed_time(ev[i1]) for ev in ssm_ev) / len(ssm_ev)
-            call_ms = sum(ev[0].elapsed_time(ev[7]) for ev in ssm_ev) / len(ssm_ev)
-    elif st.full_sharded:  # the two softmax halves on each shard, CUDA events on their stream
-        half_ev = []
-        for i in range(n_ph):
-            flush.zero_()
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            st.ssm_events = evs
-            st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], step_no)
-            half_ev.append(evs)
-            step_no += 1
-        torch.cuda.synchronize()
-        st.ssm_events = None
-        kern_ms["partial_stats"] = sum(e[0].elapsed_time(e[1]) for e in half_ev) / n_ph
-        kern_ms["backward_from_lse"] = sum(e[2].elapsed_time(e[3]) for e in half_ev) / n_ph
-    st.err.check("bench instrumented steps")
+    evs_all = []
+    barrier()
+    for i in range(n_ph):
+        flush.zero_()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(14)]
+        st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], timing_events=evs)
+        evs_all.append(evs)
+    barrier()
+    st.check("bench instrumented steps")
 
+    def avg(i0, i1):
+        return sum(e[i0].elapsed_time(e[i1]) for e in evs_all) / len(evs_all)
+
+    phases = {}
+    if R == 1:
+        for name, (i0, i1) in (("sample", (0, 1)), ("gather", (1, 2)), ("sampled_softmax", (2, 3)),
+                               ("scatter_plan", (3, 4)), ("scatter_sgd", (4, 5))):
+            phases[name] = avg(i0, i1)
     peaks, peak_src = load_peaks()
+    # Sub-millisecond kernels timed inside eager steps at full clocks: the BURST peak.
+    peak = peaks.get("bf16_tflops", 1675.0)
+    hbm_peak = peaks.get("hbm_gbs", 6456.2)
     roofline = None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_ssm.json")
@@ -462,26 +458,27 @@ def main():
             traffic = json.load(open(tpath)).get(args.workload)
         except Exception:
             traffic = None
-    peak = peaks.get("bf16_tflops_sustained", 1407.0)
     S_eff = S if S > 0 else w.vocab  # candidates per replica (full softmax: all V classes)
-    if kern_ms and st.full_sharded:
+    if S == 0 and R > 1:
         # per shard: M = R*B tokens x its V/R classes; STATS 2 M n d, GRAD + STORE 6 M n d flops
-        M_, n_ = R * B, st.nloc
-        fl = {"partial_stats": 2.0 * M_ * n_ * d, "backward_from_lse": 6.0 * M_ * n_ * d}
-        per = {k: {"ms": v, "tflops": fl[k] / (v / 1e3) / 1e12,
-                   "frac": fl[k] / (v / 1e3) / 1e12 / peak} for k, v in kern_ms.items()}
+        M_, n_ = R * B, -(-w.vocab // R)
+        kern = {"partial_stats": (avg(6, 7), 2.0 * M_ * n_ * d),
+                "backward_from_lse": (avg(8, 9), 6.0 * M_ * n_ * d)}
+        per = {k: {"ms": v, "tflops": f / (v / 1e3) / 1e12, "frac": f / (v / 1e3) / 1e12 / peak}
+               for k, (v, f) in kern.items()}
         top = per["backward_from_lse"]
         roofline = {"kernel": "tfs_ssm_backward_from_lse (GRAD + column sums + grouped "
                               "dh / dW GEMM on this shard's classes)",
                     "bound": "tensor", "achieved": top["tflops"], "peak": peak,
                     "unit": "TFLOP/s", "frac": top["frac"], "traffic": None,
-                    "peak_source": f"{peak_src} bf16 sustained",
+                    "peak_source": f"{peak_src} bf16 burst (sub-ms kernels at full clocks)",
                     "algorithmic": "6*M*n*d flops per call (M = R*B tokens, n = V/R classes); "
                                    "achieved = that / the call's CUDA-event duration",
                     "ms": top["ms"], "kernels": per}
-    elif kern_ms:
-        # The dominant kernel of the step: the grouped backward GEMM (dh = G W_s and
-        # dW_s = G^T h in one persistent tcgen05 launch), 2 x 2 B S d algorithmic flops.
+        call_ms = None
+    else:
+        kern_ms = {"gemm_stats": avg(7, 8), "gemm_grad": avg(9, 10), "gemm_store": avg(11, 12)}
+        call_ms = avg(6, 13)
         flops = {"gemm_stats": 2.0 * B * S_eff * d, "gemm_grad": 2.0 * B * S_eff * d,
                  "gemm_store": 4.0 * B * S_eff * d}
         per = {k: {"ms": v, "tflops": flops[k] / (v / 1e3) / 1e12,
@@ -492,51 +489,59 @@ def main():
                     "bound": "tensor", "achieved": top["tflops"], "peak": peak,
                     "unit": "TFLOP/s", "frac": top["frac"],
                     "traffic": (traffic or {}).get("gemm_store"),
-                    "peak_source": f"{peak_src} bf16 sustained",
+                    "peak_source": f"{peak_src} bf16 burst (sub-ms kernels at full clocks)",
                     "algorithmic": "4*B*S*d flops per launch (two GEMMs); achieved = that / the "
                                    "launch's CUDA-event duration in instrumented eager steps",
                     "ms": top["ms"], "kernels": per}
-    if "sampled_softmax" not in phases and call_ms is not None:
-        phases_call = call_ms  # R > 1: the call bracketed by its own first / last event
-    else:
-        phases_call = phases.get("sampled_softmax")
-    if phases_call is not None:
-        t = phases_call / 1e3
-        ssm = {"kernel": "tfs_sampled_softmax_fwd_bwd (whole call: 7 launches)", "bound": "tensor",
-               "achieved": 6.0 * B * S_eff * d / t / 1e12, "peak": peak, "unit": "TFLOP/s",
-               "frac": 6.0 * B * S_eff * d / t / 1e12 / peak,
-               "traffic": (traffic or {}).get("ssm_total"),
-               "algorithmic": "6*B*S*d flops per call (3 GEMMs; the logits recompute is overhead)",
-               "ms": phases_call}
-        if roofline is None:
-            roofline = ssm
-        else:
-            roofline["sampled_softmax_call"] = ssm
+        t = call_ms / 1e3
+        roofline["sampled_softmax_call"] = {
+            "kernel": "tfs_sampled_softmax_fwd_bwd (whole call)", "bound": "tensor",
+            "achieved": 6.0 * B * S_eff * d / t / 1e12, "peak": peak, "unit": "TFLOP/s",
+            "frac": 6.0 * B * S_eff * d / t / 1e12 / peak,
+            "traffic": (traffic or {}).get("ssm_total"),
+            "algorithmic": "6*B*S*d flops per call (3 GEMMs; the logits recompute is overhead)",
+            "ms": call_ms}
     hbm = None
-    if "gather" in phases and "scatter_sgd" in phases:
-        # algorithmic bytes of the gather phase: ids read, the DISTINCT rows read
-        # (repeats are L2 hits), every requested row written (bf16 operand rows in bf16 mode;
-        # the bias in fp32).
+    if R == 1 and S > 0:
+        # algorithmic bytes.  Gather: ids read, the DISTINCT rows read (repeats
+        # are L2 hits), every requested row written (bf16 operand rows in bf16 mode; the bias
+        # in fp32).  ScatterAdd-SGD apply: every gradient row read once (fp32), each distinct
+        # row of the table read and written (W with its bias).  Plan: ids read, keys + values
+        # sorted (3 LSD passes of 8-byte pairs written and read) -- reported as latency.
+        qw = st.tensor("qw")
+        x_last = st.tensor("x")
+        u_e = int(torch.unique(x_last).numel())
+        u_w = int(torch.unique(qw).numel())
+        n_e, n_w = B, B + S
         row_in = 4 * d
         row_out = (2 if args.dtype == "bf16" else 4) * d
-        u_e = int(torch.unique(st.x).numel())
-        u_w = int(torch.unique(st.qw).numel())
-        n_e, n_w = B, B + S
         g_bytes = (8 * (n_e + n_w) + (u_e + u_w) * row_in + (n_e + n_w) * row_out
                    + u_w * 4 + n_w * 4)
+        s_bytes = (n_e + n_w) * 4 * d + n_w * 4 + 2 * (u_e + u_w) * 4 * d + 2 * u_w * 4
         t_g = phases["gather"] / 1e3
-        hbm = {"gather_GBps": g_bytes / t_g / 1e9, "distinct_rows": [u_e, u_w],
-               "gather_frac": g_bytes / t_g / 1e9 / peaks.get("hbm_gbs", 6538.6),
-               "peak": peaks.get("hbm_gbs", 6538.6), "unit": "GB/s"}
+        t_s = phases["scatter_sgd"] / 1e3
+        hbm = {"gather_GBps": g_bytes / t_g / 1e9, "gather_frac": g_bytes / t_g / 1e9 / hbm_peak,
+               "gather_bytes": g_bytes,
+               "scatter_GBps": s_bytes / t_s / 1e9,
+               "scatter_frac": s_bytes / t_s / 1e9 / hbm_peak, "scatter_bytes": s_bytes,
+               "scatter_plan_us": phases["scatter_plan"] * 1e3,
+               "distinct_rows": [u_e, u_w], "peak": hbm_peak, "unit": "GB/s",
+               "note": "phase times of serial instrumented eager steps (CUDA events); the "
+                       "gather / apply phases each hold 2 launches (E, W) -- launch gaps count"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tokens = 128
         words_o, secs_o = oracle_steps(w, 3, tokens)
-        cpu = {"value": words_o / secs_o, "unit": UNIT, "cores": 1, "kind": "oracle",
+        hi = host_info()
+        rate = words_o / secs_o
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "nproc": hi["nproc"], "lscpu_model": hi["lscpu_model"],
+               "ideal_all_cores_extrapolation": rate * (hi["nproc"] or 1),
                "sample": f"3 oracle steps of {tokens} of the {B} tokens of a batch (full "
                          f"V={w.vocab}, S={S or w.vocab}, d={d}); single-threaded C++ oracle "
-                         f"+ numpy glue; {secs_o:.1f} s"}
+                         f"+ numpy glue on 1 of {hi['nproc']} cores; {secs_o:.1f} s; the "
+                         f"all-cores figure is an extrapolation (x nproc), not a measurement"}
 
     if rank == 0:
         line = {
@@ -554,29 +559,29 @@ def main():
                        f"data-parallel x{R}", "l2": "flushed before every timed step "
                        "(256 MiB write outside the timed interval)",
                        "cuda_graph": use_graph, "batches": N_BATCHES,
-                       "optimizer": args.optimizer,
-                       "route_slots": ({"transport": args.route,
-                                        "cap_e": st.cap_e, "cap_w": st.cap_w,
-                                        "calibrated_from": "distinct ids per owner of one "
-                                        "eager step x1.25 + 64"} if R > 1 else None)},
+                       "optimizer": args.optimizer, "runtime": "native tfs_step (C ABI)",
+                       "route_slots": ({"transport": "one-sided NVLink (tfs_comm IPC heaps)",
+                                        "cap": args.cap or "worst case (B, B+S)"}
+                                       if R > 1 else None)},
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * B * 8,
-                    "d2h_bytes_per_step": 4},
+                    "d2h_bytes_per_step": 4, "api": "tfs_step_run with host x / y / loss"},
             "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step,
+            "graph_kernel_nodes": kernel_nodes,
             "roofline": roofline,
             "hbm": hbm,
             "phases_ms": phases,
             "per_step_ms_p10_p50_p90": [float(np.percentile(per_step, q)) for q in (10, 50, 90)],
             "cpu_baseline": cpu,
+            "library": so_info(),
         }
-        if use_graph:
-            line["graph_kernel_nodes"] = kernel_nodes
         print(json.dumps(line), flush=True)
+    st.close()
     if world > 1:
-        st.graph = None  # release the captured NCCL work before the communicator goes away
         torch.cuda.synchronize()
         dist.barrier()
+        comm.close()
         dist.destroy_process_group()
 
 

@@ -46,7 +46,8 @@ typedef enum {
   TFS_ERR_CUDA = 5,
   TFS_ERR_UNSUPPORTED = 7,
   TFS_ERR_SAMPLER_EXHAUSTED = 8,
-  TFS_ERR_CAPACITY = 9  /* a fixed-capacity route slot overflowed (tfs_route_plan) */
+  TFS_ERR_CAPACITY = 9, /* a fixed-capacity route slot overflowed (tfs_route_plan) */
+  TFS_ERR_COMM_TIMEOUT = 10 /* a device barrier waited longer than its timeout (tfs_comm) */
 } tfs_status;
 
 typedef enum { TFS_F32 = 0, TFS_BF16 = 1 } tfs_dtype;
@@ -416,6 +417,143 @@ int32_t tfs_scatter_add_sgd_planned_slots(float* table, int64_t rows, int32_t di
                                           int64_t grad_stride, float lr, float* table2,
                                           const float* grad2, int64_t grad2_stride, void* ws,
                                           size_t ws_bytes, void* stream);
+
+/* tfs_scatter_opt_planned_slots: tfs_scatter_add_sgd_planned_slots with the sparse optimizer of
+ * tfs_scatter_opt_planned (slot / slot2 shaped like this owner's table / table2). */
+int32_t tfs_scatter_opt_planned_slots(float* table, int64_t rows, int32_t dim, const void* plan,
+                                      size_t plan_bytes, int32_t num_slots, int64_t cap,
+                                      const float* grad, int64_t grad_stride, float* table2,
+                                      const float* grad2, int64_t grad2_stride,
+                                      const tfs_sparse_opt* opt, void* ws, size_t ws_bytes,
+                                      void* stream);
+
+/* ==== Communicator: symmetric device heap + device barriers ===========
+ * The paper's workers reach the PS tasks through Send/Recv and note RDMA / NCCL as
+ * the next transport.  Here every GPU r is worker r and vocabulary shard r (R-26),
+ * and the three exchanges of the step are one-sided NVLink loads / stores into a SYMMETRIC
+ * heap: every rank allocates the same number of bytes and carves it in the same order, so a
+ * buffer has the same offset on every rank and a peer's copy lives at peer_base[r] + offset.
+ *
+ * Two modes, one code path above them:
+ *  - one process per GPU (nlocal = 1): tfs_comm_create allocates this rank's heap
+ *    (cudaMalloc on `device`); tfs_comm_export writes its CUDA IPC handle (host, 64 bytes);
+ *    the caller all-gathers the R handles (e.g. through torch.distributed -- plumbing) and
+ *    passes them to tfs_comm_connect, which maps the peers' heaps (P2P over NVLink/NVSwitch).
+ *    Barriers are a one-block kernel per rank: it stores an epoch into slot (channel, rank) of
+ *    every peer's flag area (st.release.sys) and waits until its own R slots reach the epoch
+ *    (ld.acquire.sys); a wait longer than timeout_ms (0: 10 s) writes TFS_ERR_COMM_TIMEOUT and
+ *    the peer index into the comm's device error slot and returns (no hang, no trap).
+ *  - all ranks in one process on one GPU (nlocal = nranks, first_rank = 0; test and
+ *    development mode): nranks heaps on `device`, no IPC; a barrier is stream ordering
+ *    (every local rank records an event, every local rank's stream waits for all of them) --
+ *    no kernel ever spins on another kernel.  tfs_comm_connect must not be called.
+ * heap_bytes is per rank (tfs_step_heap_bytes gives what a step needs); the first 64 KB of each
+ * heap hold the barrier flags.  One comm serves one stepper at a time.
+ * tfs_comm_heap: device base of local rank `local`'s heap; tfs_comm_peer_bases: device array
+ * int64[nranks] of the heap bases as seen from local rank `local` (for peer pointer tables).
+ * tfs_comm_error: device tfs_device_error of local rank `local` (zeroed at create). */
+typedef struct tfs_comm tfs_comm;
+int32_t tfs_comm_create(int32_t nranks, int32_t first_rank, int32_t nlocal, int32_t device,
+                        size_t heap_bytes, uint32_t timeout_ms, tfs_comm** out);
+int32_t tfs_comm_export(tfs_comm* comm, void* handle_out /* host, 64 bytes */);
+int32_t tfs_comm_connect(tfs_comm* comm, const void* handles /* host, nranks x 64 bytes */);
+int32_t tfs_comm_barrier(tfs_comm* comm, int32_t channel, void* stream);  /* nlocal == 1 only */
+void* tfs_comm_heap(tfs_comm* comm, int32_t local);
+const int64_t* tfs_comm_peer_bases(tfs_comm* comm, int32_t local);
+tfs_device_error* tfs_comm_error(tfs_comm* comm, int32_t local);
+int32_t tfs_comm_destroy(tfs_comm* comm);
+
+/* ==== The training step ===================================
+ * One synchronous step (R-15) of the paper's large-vocabulary LM output path on every
+ * local rank: sample -> Part -> route ids -> Gather on the
+ * owner -> route rows back -> Stitch -> sampled softmax forward +
+ * backward -> per-id gradient sums -> route gradients -> ScatterAdd-SGD
+ * `-=` on the owner.  With R = 1 the routes are identities; with R > 1 they are the
+ * one-sided NVLink exchanges of the comm (pull of rows, push of distinct ids and gradient sums
+ * into the owners' inboxes, three device barriers).  num_sampled == 0 selects the FULL softmax
+ * (config F): R = 1 scores every class (true class separate, hit excluded, R-9); R > 1 is the
+ * vocabulary-sharded full softmax of P:706-714 (W, b never move; each shard scores all R*B
+ * tokens against its V/R classes, R-30).
+ * The stepper owns every buffer: tables (shards of E, W, b; in the comm heap when R > 1), the
+ * per-step buffers, workspaces, plans, its streams and events; nothing is allocated after
+ * tfs_step_create.  The step has no host synchronisation, so tfs_step_capture records it (all
+ * local ranks) into one CUDA graph that tfs_step_run replays.
+ * Config: tokens = B per replica; lr > 0 SGD step; optimizer 0 SGD / 1 Momentum (momentum) /
+ * 2 Adagrad (accumulators start at adagrad_init), slot tables sharded like the tables (R-29);
+ * cap_e / cap_w: route slots per owner for the E / W lookups (0: the worst case, B and B + S,
+ * so no batch can overflow; smaller values save memory and an overflow is reported as
+ * TFS_ERR_CAPACITY in the step's error slot); seed: sampler key; flags as tfs_ssm_args
+ * (TFS_SUBTRACT_LOG_Q | TFS_REMOVE_ACCIDENTAL_HITS for the sampled step).
+ * loss_sum (buffer TFS_BUF_LOSS_SUM) is this rank's share of the global mean loss: c times the
+ * sum of the per-token losses formed on this rank (its own tokens; full-sharded: the tokens
+ * whose label it owns); the global loss is the sum over ranks.  c = 1 / (R B) (R-13). */
+typedef struct {
+  int64_t vocab;
+  int32_t dim;
+  int32_t num_shards;     /* R */
+  int64_t tokens;         /* B per replica */
+  int64_t num_sampled;    /* S per replica; 0 = full softmax */
+  int32_t operand_dtype;  /* TFS_BF16 (tensor cores) or TFS_F32 (parity mode; R = 1 only) */
+  uint32_t flags;
+  float lr;
+  int32_t unique;         /* sampler: first S distinct draws (1) or S draws (0) */
+  uint64_t seed;
+  int32_t optimizer;      /* 0 SGD, 1 Momentum, 2 Adagrad */
+  float momentum;
+  float adagrad_init;
+  int64_t cap_e, cap_w;   /* 0 = worst case */
+} tfs_step_config;
+typedef struct tfs_stepper tfs_stepper;
+/* Bytes of symmetric heap per rank that a step with this config needs (host arithmetic). */
+size_t tfs_step_heap_bytes(const tfs_step_config* cfg);
+/* comm: NULL for R = 1 (one local rank); else a comm of cfg->num_shards ranks with heaps of at
+ * least tfs_step_heap_bytes(cfg) bytes (connected, in the one-process-per-GPU mode).  The
+ * tables are zero after create: fill them through tfs_step_buffer, then tfs_step_sync. */
+int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, tfs_stepper** out);
+int32_t tfs_step_destroy(tfs_stepper* st);
+/* Named buffers of local rank `local` (device pointer, element count, element type 0 f32 /
+ * 1 bf16 / 2 int64 / 3 int32): tables and slots (this rank's shard rows), the step's inputs x, y
+ * and the lookup ids y||s, the sampler outputs, gathered rows, softmax outputs and gradients,
+ * the error slot (2 x int64: code, smallest offending position), the step counter, and the
+ * distinct ids per owner of the last step ([2 x R]: E, W). */
+enum {
+  TFS_BUF_E = 0, TFS_BUF_W, TFS_BUF_B, TFS_BUF_SLOT_E, TFS_BUF_SLOT_W, TFS_BUF_SLOT_B,
+  TFS_BUF_X, TFS_BUF_Y, TFS_BUF_QW, TFS_BUF_LOG_EC_S, TFS_BUF_LOG_EC_Y, TFS_BUF_NUM_TRIES,
+  TFS_BUF_H, TFS_BUF_W_ROWS, TFS_BUF_B_ROWS, TFS_BUF_LOSS, TFS_BUF_LSE, TFS_BUF_LOSS_SUM,
+  TFS_BUF_DH, TFS_BUF_DW, TFS_BUF_DB, TFS_BUF_ERR, TFS_BUF_STEP, TFS_BUF_COUNTS,
+  TFS_BUF_COUNT_
+};
+int32_t tfs_step_buffer(tfs_stepper* st, int32_t local, int32_t which, void** ptr,
+                        int64_t* numel, int32_t* elem_type);
+/* After the caller wrote tables / slots: refresh derived copies (the bf16 operand shadow of W
+ * in the sharded full softmax) and zero the error slots; synchronises the device. */
+int32_t tfs_step_sync(tfs_stepper* st);
+/* One step of every local rank on `stream`.  io->host == 0: x / y are DEVICE pointers to
+ * [nlocal x B] int64 (rank-major); == 1: HOST pointers (pinned for asynchrony) copied to the
+ * step's input buffers on `stream` inside the call, and each local rank's loss_sum is copied
+ * back to io->loss_host[nlocal] (host) on `stream` -- the caller synchronises before reading.
+ * The step counter (sampler; TFS_BUF_STEP) advances by one on the device.
+ * io->timing_events (one local rank, eager only; NULL normally): 14 cudaEvent_t.  R = 1: the
+ * step runs its phases SERIALLY on one stream and records 0 start, 1 sampled, 2 gathered,
+ * 3 softmax done, 4 plans built, 5 tables updated; 6..13 the softmax call's 8 events
+ * (tfs_ssm_args.timing_events).  R > 1 (phases overlapped as usual): 6..13 as above for the
+ * sampled softmax; the sharded full softmax records 6 / 7 around its partial-stats call and
+ * 8 / 9 around its backward call.  Entries may be NULL. */
+typedef struct {
+  const int64_t* x;
+  const int64_t* y;
+  int32_t host;
+  float* loss_host;
+  void* const* timing_events;
+} tfs_step_io;
+int32_t tfs_step_run(tfs_stepper* st, const tfs_step_io* io, void* stream);
+/* Record one step of every local rank (inputs read from TFS_BUF_X / TFS_BUF_Y, step counter
+ * advanced on the device) into a CUDA graph; later tfs_step_run calls replay it.  The capture
+ * itself launches nothing (stream capture); tfs_step_uncapture drops the graph. */
+int32_t tfs_step_capture(tfs_stepper* st);
+int32_t tfs_step_uncapture(tfs_stepper* st);
+/* Kernel nodes of the captured graph (0 if none). */
+int64_t tfs_step_graph_kernels(tfs_stepper* st);
 
 /* ==== Diagnostics ===============================================================================
  * C[M x N] (fp32, row-major) = sum_k A(m, k) B(n, k) on the tcgen05 path with bf16 operands,

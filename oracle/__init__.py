@@ -25,7 +25,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.cpp")
 
 OK, INVALID, OUT_OF_RANGE, BAD_POSITIONS, EXHAUSTED = 0, 1, 2, 3, 8
-SUBTRACT_LOG_Q, REMOVE_ACCIDENTAL_HITS = 1, 2
+SUBTRACT_LOG_Q, REMOVE_ACCIDENTAL_HITS, LABEL_IN_CANDIDATES = 1, 2, 4
 
 
 class OracleError(RuntimeError):
@@ -70,6 +70,7 @@ class _SsmIO(ctypes.Structure):
         ("n_tok", I64), ("tok_idx", P), ("n_col", I64), ("col_idx", P),
         ("loss", P), ("lse", P), ("z_true", P), ("dh", P), ("dw_true", P), ("db_true", P),
         ("dw_s", P), ("db_s", P),
+        ("abs_loss", P), ("abs_dh", P), ("abs_dw_s", P), ("abs_db_s", P),
     ]
 
 
@@ -195,12 +196,19 @@ def sample(vocab, num_sampled, unique, seed, step, replica, labels, max_draws=No
 def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, log_ec_s, *,
                     flags=SUBTRACT_LOG_Q | REMOVE_ACCIDENTAL_HITS, grad_scale=1.0, bf16=False,
                     tok_idx=None, col_idx=None):
-    """Sampled softmax forward + backward (O9-O11).  Returns a dict of fp64 arrays."""
+    """Sampled softmax forward + backward (O9-O11).  Returns a dict of fp64 arrays:
+    loss, lse, z_true, dh, dw_true, db_true, dw_s, db_s, and abs_loss / abs_dh / abs_dw_s /
+    abs_db_s -- the sums of absolute values of the terms forming those outputs (the scale of
+    the rounding error of any evaluation order; abs of dw_true / db_true is the value itself).
+    flags may include LABEL_IN_CANDIDATES (R-30: sharded full softmax; w_true, b_true,
+    log_ec_true are then unused and may be None)."""
     h = _c(h, np.float32)
     B, d = h.shape
     w_s = _c(w_s, np.float32).reshape(-1, d)
     S = w_s.shape[0]
     labels = _c(labels, np.int64)
+    if w_true is None:  # label-in mode: no true-class operand
+        w_true, b_true, log_ec_true = np.zeros((B, d)), np.zeros(B), np.zeros(B)
     w_true = _c(w_true, np.float32).reshape(B, d)
     b_true = _c(b_true, np.float32)
     le_t = _c(log_ec_true, np.float64)
@@ -215,12 +223,16 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
         "loss": np.empty(nt), "lse": np.empty(nt), "z_true": np.empty(nt),
         "dh": np.empty((nt, d)), "dw_true": np.empty((nt, d)), "db_true": np.empty(nt),
         "dw_s": np.empty((nc, d)), "db_s": np.empty(nc),
+        "abs_loss": np.empty(nt), "abs_dh": np.empty((nt, d)), "abs_dw_s": np.empty((nc, d)),
+        "abs_db_s": np.empty(nc),
     }
     io = _SsmIO(B, S, d, int(bf16), flags, grad_scale, _ptr(h), _ptr(labels), _ptr(w_true),
                 _ptr(b_true), _ptr(le_t), _ptr(sampled), _ptr(w_s), _ptr(b_s), _ptr(le_s),
                 nt, _ptr(ti), nc, _ptr(ci),
                 _ptr(out["loss"]), _ptr(out["lse"]), _ptr(out["z_true"]), _ptr(out["dh"]),
-                _ptr(out["dw_true"]), _ptr(out["db_true"]), _ptr(out["dw_s"]), _ptr(out["db_s"]))
+                _ptr(out["dw_true"]), _ptr(out["db_true"]), _ptr(out["dw_s"]), _ptr(out["db_s"]),
+                _ptr(out["abs_loss"]), _ptr(out["abs_dh"]), _ptr(out["abs_dw_s"]),
+                _ptr(out["abs_db_s"]))
     _check(lib().orc_sampled_softmax(ctypes.byref(io)))
     return out
 

@@ -232,32 +232,37 @@ int orc_log_uniform_sample(int64_t vocab, int32_t num_sampled, int32_t unique, u
 // "multiplies the output by a random sparse matrix containing weights for the
 // true class and a random sample of false classes".  Logits, loss and gradients are the
 // definitions O9-O11 of DESIGN.md §3 (Jean et al., cited P:715).
+//
+// flag 4 (label in candidates, reading R-30): the vocabulary-sharded FULL softmax of
+// P:706-714, where the candidates are classes of the vocabulary and a token's label is one of
+// them (no separate true-class term): lse_t = ln sum_j e^{Z_tj}; z_t = Z_{t,j*} with j* the
+// first column whose id is y_t (one must exist); G_tj = c (e^{Z_tj - lse_t} - [s_j == y_t]),
+// rounded to bf16 as a whole in bf16 mode (the GPU's rounding point); dh = sum_j G_tj W_s,j.
+//
+// Alongside every gradient the oracle can return the sum of the ABSOLUTE values of the terms
+// that form it (abs_* outputs): abs_dh_t = |g_t| |W_true,t| + sum_j |G_tj| |W_s,j|,
+// abs_dw_s,j = sum_t |G_tj| |h_t|, abs_db_s,j = sum_t |G_tj|, abs_loss_t = |lse_t| + |z_t|.
+// They are the scale of the rounding error any evaluation order commits (the parity tests
+// bound |gpu - oracle| by tol x abs_*, element by element).
 int orc_sampled_softmax(const orc_ssm_io* io) {
   const int64_t B = io->B, S = io->S;
   const int32_t d = io->dim;
   if (B < 0 || S < 0 || d < 1) return kInvalid;
-  const bool sub_q = io->flags & 1u, rm_hits = io->flags & 2u;
+  const bool sub_q = io->flags & 1u, rm_hits = io->flags & 2u, label_in = io->flags & 4u;
+  if (rm_hits && label_in) return kInvalid;
   const double c = io->grad_scale;
   auto op = [&](float v) -> double { return io->bf16 ? (double)orc_bf16_round(v) : (double)v; };
   auto grad_round = [&](double g) -> double {
     return io->bf16 ? (double)orc_bf16_round((float)g) : g;
   };
-  // Operands (rounded in bf16 mode), as fp64.
-  std::vector<double> h((size_t)(B * d)), wt((size_t)(B * d)), ws((size_t)(S * d));
-  for (int64_t i = 0; i < B * d; ++i) { h[i] = op(io->h[i]); wt[i] = op(io->w_true[i]); }
+  // Operands (rounded in bf16 mode), as fp64.  Label-in mode has no true-class operand.
+  std::vector<double> h((size_t)(B * d)), wt(label_in ? 0 : (size_t)(B * d)), ws((size_t)(S * d));
+  for (int64_t i = 0; i < B * d; ++i) h[i] = op(io->h[i]);
+  if (!label_in)
+    for (int64_t i = 0; i < B * d; ++i) wt[i] = op(io->w_true[i]);
   for (int64_t i = 0; i < S * d; ++i) ws[i] = op(io->w_s[i]);
 
-  // O9: true logit z_t and sampled logits Z_tj (excluded: accidental hit).
-  auto z_true = [&](int64_t t) -> double {
-    double acc = 0.0;
-    for (int32_t k = 0; k < d; ++k) acc += h[t * d + k] * wt[t * d + k];
-    acc += io->b_true[t];
-    if (sub_q) acc -= io->log_ec_true[t];
-    return acc;
-  };
-  auto excluded = [&](int64_t t, int64_t j) -> bool {
-    return rm_hits && io->sampled[j] == io->labels[t];
-  };
+  // O9: sampled logits Z_tj and the true logit z_t.
   auto z_samp = [&](int64_t t, int64_t j) -> double {
     double acc = 0.0;
     for (int32_t k = 0; k < d; ++k) acc += h[t * d + k] * ws[j * d + k];
@@ -265,10 +270,30 @@ int orc_sampled_softmax(const orc_ssm_io* io) {
     if (sub_q) acc -= io->log_ec_s[j];
     return acc;
   };
+  auto label_col = [&](int64_t t) -> int64_t {  // label-in: first column holding y_t
+    for (int64_t j = 0; j < S; ++j)
+      if (io->sampled[j] == io->labels[t]) return j;
+    return -1;
+  };
+  auto z_true = [&](int64_t t) -> double {
+    if (label_in) return z_samp(t, label_col(t));
+    double acc = 0.0;
+    for (int32_t k = 0; k < d; ++k) acc += h[t * d + k] * wt[t * d + k];
+    acc += io->b_true[t];
+    if (sub_q) acc -= io->log_ec_true[t];
+    return acc;
+  };
+  // Excluded (treated as -inf): an accidental hit of the label among the sampled classes (R-9).
+  auto excluded = [&](int64_t t, int64_t j) -> bool {
+    return rm_hits && io->sampled[j] == io->labels[t];
+  };
+  auto is_label = [&](int64_t t, int64_t j) -> bool {
+    return label_in && io->sampled[j] == io->labels[t];
+  };
 
-  // O10: lse_t = mu + ln(e^{z-mu} + sum_j e^{Z_tj - mu}) for every token that an output needs:
-  // all tokens when any dW_s / db_s column is asked for (they sum over t), else only the
-  // requested tokens (same formula; the others are simply not evaluated).
+  // O10: lse_t = mu + ln(e^{z-mu} + sum_j e^{Z_tj - mu}) (label-in: the label is one of the
+  // Z_tj, so there is no separate e^{z-mu} term) for every token an output needs: all tokens
+  // when any dW_s / db_s column is asked for (they sum over t), else only the requested ones.
   std::vector<double> lse((size_t)B), zt((size_t)B);
   std::vector<double> Zrow((size_t)S);
   std::vector<char> need((size_t)B, 0);
@@ -278,37 +303,55 @@ int orc_sampled_softmax(const orc_ssm_io* io) {
       if (io->tok_idx[r] >= 0 && io->tok_idx[r] < B) need[io->tok_idx[r]] = 1;
   for (int64_t t = 0; t < B; ++t) {
     if (!all_tokens && !need[t]) continue;
+    if (label_in && label_col(t) < 0) return kInvalid;
     zt[t] = z_true(t);
-    double mu = zt[t];
+    double mu = label_in ? -INFINITY : zt[t];
     for (int64_t j = 0; j < S; ++j) {
       Zrow[j] = z_samp(t, j);
       if (!excluded(t, j)) mu = std::max(mu, Zrow[j]);
     }
-    double sum = std::exp(zt[t] - mu);
+    double sum = label_in ? 0.0 : std::exp(zt[t] - mu);
     for (int64_t j = 0; j < S; ++j)
       if (!excluded(t, j)) sum += std::exp(Zrow[j] - mu);
     lse[t] = mu + std::log(sum);
   }
+  // O11: G_tj = c e^{Z_tj - lse_t} (label-in: minus c at the label), bf16-rounded in bf16 mode.
+  auto G_at = [&](int64_t t, int64_t j) -> double {
+    return grad_round(c * (std::exp(z_samp(t, j) - lse[t]) - (is_label(t, j) ? 1.0 : 0.0)));
+  };
 
   // O10/O11 per token.
   const int64_t n_tok = io->tok_idx ? io->n_tok : B;
   for (int64_t r = 0; r < n_tok; ++r) {
     const int64_t t = io->tok_idx ? io->tok_idx[r] : r;
     if (t < 0 || t >= B) return kInvalid;
-    const double g = c * (std::exp(zt[t] - lse[t]) - 1.0);  // d loss / d z_t
+    // d loss / d z_t of the separate true-class term (label-in: carried by G, so 0 here)
+    const double g = label_in ? 0.0 : c * (std::exp(zt[t] - lse[t]) - 1.0);
     if (io->loss) io->loss[r] = lse[t] - zt[t];
+    if (io->abs_loss) io->abs_loss[r] = std::fabs(lse[t]) + std::fabs(zt[t]);
     if (io->lse) io->lse[r] = lse[t];
     if (io->z_true) io->z_true[r] = zt[t];
     if (io->db_true) io->db_true[r] = g;
     if (io->dw_true)
       for (int32_t k = 0; k < d; ++k) io->dw_true[r * d + k] = g * h[t * d + k];
-    if (io->dh) {
-      double* dh = io->dh + r * d;
-      for (int32_t k = 0; k < d; ++k) dh[k] = g * wt[t * d + k];
+    if (io->dh || io->abs_dh) {
+      std::vector<double> dh((size_t)d, 0.0), ad((size_t)d, 0.0);
+      if (!label_in)
+        for (int32_t k = 0; k < d; ++k) {
+          dh[k] = g * wt[t * d + k];
+          ad[k] = std::fabs(g * wt[t * d + k]);
+        }
       for (int64_t j = 0; j < S; ++j) {
         if (excluded(t, j)) continue;
-        const double G = grad_round(c * std::exp(z_samp(t, j) - lse[t]));
-        for (int32_t k = 0; k < d; ++k) dh[k] += G * ws[j * d + k];
+        const double G = G_at(t, j);
+        for (int32_t k = 0; k < d; ++k) {
+          dh[k] += G * ws[j * d + k];
+          ad[k] += std::fabs(G * ws[j * d + k]);
+        }
+      }
+      for (int32_t k = 0; k < d; ++k) {
+        if (io->dh) io->dh[r * d + k] = dh[k];
+        if (io->abs_dh) io->abs_dh[r * d + k] = ad[k];
       }
     }
   }
@@ -318,18 +361,24 @@ int orc_sampled_softmax(const orc_ssm_io* io) {
   for (int64_t r = 0; r < n_col; ++r) {
     const int64_t j = io->col_idx ? io->col_idx[r] : r;
     if (j < 0 || j >= S) return kInvalid;
-    double db = 0.0;
-    double* dw = io->dw_s ? io->dw_s + r * d : nullptr;
-    if (dw)
-      for (int32_t k = 0; k < d; ++k) dw[k] = 0.0;
+    double db = 0.0, adb = 0.0;
+    std::vector<double> dw((size_t)d, 0.0), aw((size_t)d, 0.0);
     for (int64_t t = 0; t < B; ++t) {
       if (excluded(t, j)) continue;
-      const double G = grad_round(c * std::exp(z_samp(t, j) - lse[t]));
+      const double G = G_at(t, j);
       db += G;
-      if (dw)
-        for (int32_t k = 0; k < d; ++k) dw[k] += G * h[t * d + k];
+      adb += std::fabs(G);
+      for (int32_t k = 0; k < d; ++k) {
+        dw[k] += G * h[t * d + k];
+        aw[k] += std::fabs(G * h[t * d + k]);
+      }
+    }
+    for (int32_t k = 0; k < d; ++k) {
+      if (io->dw_s) io->dw_s[r * d + k] = dw[k];
+      if (io->abs_dw_s) io->abs_dw_s[r * d + k] = aw[k];
     }
     if (io->db_s) io->db_s[r] = db;
+    if (io->abs_db_s) io->abs_db_s[r] = adb;
   }
   return kOk;
 }

@@ -54,7 +54,8 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
 void orc_log_uniform_thresholds(int64_t vocab, uint64_t* thr);
 /* p_k = (ln(k+2) - ln(k+1)) / ln(V+1) */
 double orc_log_uniform_prob(int64_t vocab, int64_t k);
-/* Draw i of replica r at step tau: Philox(ctr=(i,0,tau,r), key=(seed_lo,seed_hi)) -> m =
+/* Draw i of replica r at step tau: Philox(ctr=(i, tau_hi, tau_lo, r), key=(seed_lo, seed_hi))
+ * (tau_hi / tau_lo = high / low 32 bits of the 64-bit step) -> m =
  * ((w0<<32)|w1)>>11 -> k = min{k : m < Thr[k]}.  unique: first S distinct in draw order and
  * T = draws consumed; else s_j = k_j, T = S.  log expected counts in fp64 for s and labels:
  * ec = -expm1(T*log1p(-p)) (unique) or S*p.  max_draws bounds the unique loop (status 8). */
@@ -65,7 +66,9 @@ int orc_log_uniform_sample(int64_t vocab, int32_t num_sampled, int32_t unique, u
                            int64_t* out_num_tries);
 
 /* ---- Sampled softmax forward + backward (O8-O11 of DESIGN §3). ----
- * flags: 1 = subtract log expected count (R-10), 2 = remove accidental hits (R-9).
+ * flags: 1 = subtract log expected count (R-10), 2 = remove accidental hits (R-9), 4 = label in
+ * candidates (R-30: the sharded full softmax; no true-class term, the label's column carries
+ * G = c (p - 1); w_true / b_true / log_ec_true unused; excludes flag 2).
  * bf16 != 0 emulates the bf16-operand mode: h, w_true, w_s rounded RNE to bf16 before use, and
  * the gradient-of-logits G rounded to bf16 before the dh / dW_s / db_s reductions (R-18).
  * Everything else is fp64.  The full log-sum-exp is always computed for every token; the
@@ -81,6 +84,10 @@ typedef struct {
   int64_t n_tok; const int64_t* tok_idx; int64_t n_col; const int64_t* col_idx;
   double* loss; double* lse; double* z_true; double* dh; double* dw_true; double* db_true;
   double* dw_s; double* db_s;
+  /* optional (NULL = skip): sums of the absolute values of the terms forming loss, dh, dw_s,
+   * db_s (|lse| + |z|; |g||W_true| + sum_j |G||W_s|; sum_t |G||h|; sum_t |G|) -- the scale of
+   * any evaluation order's rounding error, used by the element-wise parity bound. */
+  double* abs_loss; double* abs_dh; double* abs_dw_s; double* abs_db_s;
 } orc_ssm_io;
 int orc_sampled_softmax(const orc_ssm_io* io);
 

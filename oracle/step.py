@@ -15,8 +15,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import (REMOVE_ACCIDENTAL_HITS, SUBTRACT_LOG_Q, gather, partition, sample,
-               sampled_softmax, scatter_add_sgd, stitch)
+from . import (LABEL_IN_CANDIDATES, REMOVE_ACCIDENTAL_HITS, SUBTRACT_LOG_Q, gather, partition,
+               sample, sampled_softmax, scatter_add_sgd, stitch)
 
 
 @dataclass
@@ -32,7 +32,14 @@ class StepConfig:
     flags: int = SUBTRACT_LOG_Q | REMOVE_ACCIDENTAL_HITS
     bf16: bool = False
     full_softmax: bool = False   # candidates = all V classes, no sampler (config F)
+    # full softmax with the label among the candidates (R-30: the vocabulary-sharded full
+    # softmax of P:706-714 -- G = c (p - onehot) rounded as a whole in bf16 mode); the plain
+    # full softmax (R = 1) keeps the separate true-class term with the hit excluded (R-9)
+    label_in: bool = False
     inplace: bool = False        # update E, W, b in place (same arithmetic; saves table copies)
+    # also return, per table, lr x the sum over contributions of the abs_* term sums: the
+    # element-wise scale of the update's rounding error (tests' parity bound)
+    abs_bounds: bool = False
 
 
 @dataclass
@@ -51,6 +58,7 @@ class ReplicaTrace:
     w_rows: np.ndarray = None     # [B+S, d]: W_true then W_s
     b_rows: np.ndarray = None     # [B+S]
     ssm: dict = field(default_factory=dict)
+    abs_delta: tuple = None       # (E, W, b) update scales, traces[0] only, cfg.abs_bounds
 
 
 def _route(send_local, counts, R):
@@ -130,8 +138,12 @@ def step(E, W, b, xs, ys, cfg: StepConfig):
         t = traces[r]
         S = t.sampled.size
         # Config F (full softmax): every class is a candidate, no log-Q correction, and the
-        # true class is excluded from the candidates (R-9) -- exactly the full softmax.
-        flags = REMOVE_ACCIDENTAL_HITS if cfg.full_softmax else cfg.flags
+        # true class is excluded from the candidates (R-9) -- exactly the full softmax; or,
+        # label_in, the label's own column carries its gradient (R-30).
+        if cfg.full_softmax:
+            flags = LABEL_IN_CANDIDATES if cfg.label_in else REMOVE_ACCIDENTAL_HITS
+        else:
+            flags = cfg.flags
         t.ssm = sampled_softmax(
             t.h, ys[r], t.w_rows[:B], t.b_rows[:B], t.log_ec_y, t.sampled, t.w_rows[B:B + S],
             t.b_rows[B:B + S], t.log_ec_s, flags=flags, grad_scale=c, bf16=cfg.bf16)
@@ -145,4 +157,18 @@ def step(E, W, b, xs, ys, cfg: StepConfig):
     E2 = scatter_add_sgd(E, np.concatenate(ids_e), np.concatenate(g_e), cfg.lr, cfg.inplace)
     W2 = scatter_add_sgd(W, np.concatenate(ids_w), np.concatenate(g_w), cfg.lr, cfg.inplace)
     b2 = scatter_add_sgd(b, np.concatenate(ids_w), np.concatenate(g_b), cfg.lr, cfg.inplace)
+    if cfg.abs_bounds:
+        # per touched entry: lr x sum over its contributions of their absolute term sums
+        aE, aW, ab = np.zeros(E.shape), np.zeros(W.shape), np.zeros(b.shape)
+        for r in range(R):
+            t = traces[r]
+            np.add.at(aE, xs[r], cfg.lr * t.ssm["abs_dh"])
+            q = np.concatenate([ys[r], t.sampled])
+            # g_t = c (p_t - 1) is a difference: its scale is c (p_t + 1), p_t = e^{-loss_t}
+            dbt = t.ssm["db_true"]
+            sg = np.where(dbt == 0, 0.0, c * (np.exp(-t.ssm["loss"]) + 1.0))
+            hs = np.abs(t.ssm["dw_true"]) / np.maximum(np.abs(dbt), 1e-300)[:, None]
+            np.add.at(aW, q, cfg.lr * np.concatenate([sg[:, None] * hs, t.ssm["abs_dw_s"]]))
+            np.add.at(ab, q, cfg.lr * np.concatenate([sg, t.ssm["abs_db_s"]]))
+        traces[0].abs_delta = (aE, aW, ab)
     return E2, W2, b2, traces

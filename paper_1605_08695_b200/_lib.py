@@ -10,7 +10,11 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.environ.get("TFS_LIB") or os.path.join(HERE, "libtfs.so")  # TFS_LIB: a variant build
+PRODUCT_SO = os.path.join(HERE, "libtfs.so")
+# An A/B-timing variant (tools/build_variant.py) is loaded only when BOTH variables are set, so
+# a stray TFS_LIB cannot silently replace the product; bench.py records which .so it loaded.
+SO_PATH = (os.environ["TFS_LIB"] if os.environ.get("TFS_ALLOW_VARIANT_LIB") == "1"
+           and os.environ.get("TFS_LIB") else PRODUCT_SO)
 HEADER = os.path.join(os.path.dirname(HERE), "include", "tfs.h")
 
 TFS_OK = 0
@@ -22,6 +26,7 @@ TFS_ERR_CUDA = 5
 TFS_ERR_UNSUPPORTED = 7
 TFS_ERR_SAMPLER_EXHAUSTED = 8
 TFS_ERR_CAPACITY = 9
+TFS_ERR_COMM_TIMEOUT = 10
 TFS_BF16_OPERANDS = 4
 TFS_LABEL_IN_CANDIDATES = 8
 TFS_F32, TFS_BF16 = 0, 1
@@ -50,6 +55,17 @@ class TfsError(RuntimeError):
 
 class SparseOpt(ctypes.Structure):
     _fields_ = [("kind", I32), ("lr", F32), ("mu", F32), ("slot", P), ("slot2", P)]
+
+
+class StepConfigC(ctypes.Structure):
+    _fields_ = [("vocab", I64), ("dim", I32), ("num_shards", I32), ("tokens", I64),
+                ("num_sampled", I64), ("operand_dtype", I32), ("flags", U32), ("lr", F32),
+                ("unique", I32), ("seed", U64), ("optimizer", I32), ("momentum", F32),
+                ("adagrad_init", F32), ("cap_e", I64), ("cap_w", I64)]
+
+
+class StepIO(ctypes.Structure):
+    _fields_ = [("x", P), ("y", P), ("host", I32), ("loss_host", P), ("timing_events", P)]
 
 
 class SsmArgs(ctypes.Structure):
@@ -111,6 +127,26 @@ _SIGNATURES = {
     "tfs_scatter_plan_slots": ([P, I64, I32, I64, I64, I32, P, SZ, P, P], I32),
     "tfs_scatter_add_sgd_planned_slots": ([P, I64, I32, P, SZ, I32, I64, P, I64, F32, P, P, I64,
                                            P, SZ, P], I32),
+    "tfs_scatter_opt_planned_slots": ([P, I64, I32, P, SZ, I32, I64, P, I64, P, P, I64,
+                                       ctypes.POINTER(SparseOpt), P, SZ, P], I32),
+    "tfs_comm_create": ([I32, I32, I32, I32, SZ, U32, ctypes.POINTER(P)], I32),
+    "tfs_comm_export": ([P, P], I32),
+    "tfs_comm_connect": ([P, P], I32),
+    "tfs_comm_barrier": ([P, I32, P], I32),
+    "tfs_comm_heap": ([P, I32], P),
+    "tfs_comm_peer_bases": ([P, I32], P),
+    "tfs_comm_error": ([P, I32], P),
+    "tfs_comm_destroy": ([P], I32),
+    "tfs_step_heap_bytes": ([ctypes.POINTER(StepConfigC)], SZ),
+    "tfs_step_create": ([ctypes.POINTER(StepConfigC), P, ctypes.POINTER(P)], I32),
+    "tfs_step_destroy": ([P], I32),
+    "tfs_step_buffer": ([P, I32, I32, ctypes.POINTER(P), ctypes.POINTER(I64),
+                         ctypes.POINTER(I32)], I32),
+    "tfs_step_sync": ([P], I32),
+    "tfs_step_run": ([P, ctypes.POINTER(StepIO), P], I32),
+    "tfs_step_capture": ([P], I32),
+    "tfs_step_uncapture": ([P], I32),
+    "tfs_step_graph_kernels": ([P], I64),
     "tfs_debug_gemm_workspace_bytes": ([I32, I32, I32, I32], SZ),
     "tfs_debug_gemm_bf16": ([P, I64, I32, P, I64, I32, I32, I32, I32, I32, P, P, SZ, P], I32),
     "tfs_debug_launch_count": ([], I64),

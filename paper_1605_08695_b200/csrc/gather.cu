@@ -214,7 +214,7 @@ static int grid_for_rows(int64_t n, int rows_per_warp) {
 
 using namespace tfs;
 
-extern "C" int32_t tfs_version(void) { return 100; }
+extern "C" int32_t tfs_version(void) { return 200; }
 
 extern "C" int64_t tfs_debug_launch_count(void) { return g_launches.load(); }
 
@@ -229,6 +229,7 @@ extern "C" const char* tfs_status_string(int32_t s) {
     case TFS_ERR_UNSUPPORTED: return "unsupported device (libtfs needs sm_100a)";
     case TFS_ERR_SAMPLER_EXHAUSTED: return "sampler draw budget exhausted";
     case TFS_ERR_CAPACITY: return "route slot capacity exceeded";
+    case TFS_ERR_COMM_TIMEOUT: return "device barrier timed out (a peer never arrived)";
     default: return "unknown status";
   }
 }

@@ -1772,16 +1772,21 @@ extern "C" int32_t tfs_scatter_plan_slots(const int64_t* ids, int64_t ids_stride
   return TFS_OK;
 }
 
-extern "C" int32_t tfs_scatter_add_sgd_planned_slots(
-    float* table, int64_t rows, int32_t dim, const void* plan, size_t plan_bytes, int32_t R,
-    int64_t cap, const float* grad, int64_t grad_stride, float lr, float* table2,
-    const float* grad2, int64_t grad2_stride, void* ws, size_t ws_bytes, void* stream) {
+static int32_t planned_slots_impl(float* table, int64_t rows, int32_t dim, const void* plan,
+                                  size_t plan_bytes, int32_t R, int64_t cap, const float* grad,
+                                  int64_t grad_stride, float* table2, const float* grad2,
+                                  int64_t grad2_stride, const tfs_sparse_opt* opt, void* ws,
+                                  size_t ws_bytes, void* stream) {
   TFS_REQUIRE(R >= 1 && cap >= 1 && dim >= 1 && rows >= 0 && rows < (1ll << 31) - 1);
   TFS_REQUIRE(grad_stride >= cap * dim && (grad2 == nullptr || grad2_stride >= cap));
   TFS_REQUIRE((table2 == nullptr) == (grad2 == nullptr));
+  TFS_REQUIRE(opt != nullptr && opt->kind >= 0 && opt->kind <= 2);
+  TFS_REQUIRE(opt->kind == 0 || opt->slot != nullptr);
+  TFS_REQUIRE(opt->kind == 0 || table2 == nullptr || opt->slot2 != nullptr);
   const int64_t n = (int64_t)R * cap;
   TFS_REQUIRE(table && plan && grad && n < (1ll << 31));
-  TFS_REQUIRE(dim % 4 != 0 || (((uintptr_t)table & 15) == 0 && grad_stride % 4 == 0));
+  TFS_REQUIRE(dim % 4 != 0 || (((uintptr_t)table & 15) == 0 && grad_stride % 4 == 0 &&
+                               (opt->kind == 0 || ((uintptr_t)opt->slot & 15) == 0)));
   TFS_SUPPORTED();
   SegScratch s;
   if (plan_bytes < plan_scratch_bytes(n, &s, const_cast<void*>(plan), plan_bytes))
@@ -1795,12 +1800,33 @@ extern "C" int32_t tfs_scatter_add_sgd_planned_slots(
   j.invalid_key = (uint32_t)rows;
   j.table = table;
   j.table2 = table2;
-  j.lr = lr;
+  j.lr = opt->lr;
+  j.opt = opt->kind;
+  j.mu = (double)opt->mu;
+  j.slot = opt->slot;
+  j.slot2 = opt->slot2;
   j.nloc = rows + 1;
   j.row_cap = cap;
   j.row_stride = grad_stride;
   j.row2_stride = grad2_stride;
   return run_segments(j, n, as_stream(stream));
+}
+
+extern "C" int32_t tfs_scatter_add_sgd_planned_slots(
+    float* table, int64_t rows, int32_t dim, const void* plan, size_t plan_bytes, int32_t R,
+    int64_t cap, const float* grad, int64_t grad_stride, float lr, float* table2,
+    const float* grad2, int64_t grad2_stride, void* ws, size_t ws_bytes, void* stream) {
+  const tfs_sparse_opt sgd{0, lr, 0.f, nullptr, nullptr};
+  return planned_slots_impl(table, rows, dim, plan, plan_bytes, R, cap, grad, grad_stride, table2,
+                            grad2, grad2_stride, &sgd, ws, ws_bytes, stream);
+}
+
+extern "C" int32_t tfs_scatter_opt_planned_slots(
+    float* table, int64_t rows, int32_t dim, const void* plan, size_t plan_bytes, int32_t R,
+    int64_t cap, const float* grad, int64_t grad_stride, float* table2, const float* grad2,
+    int64_t grad2_stride, const tfs_sparse_opt* opt, void* ws, size_t ws_bytes, void* stream) {
+  return planned_slots_impl(table, rows, dim, plan, plan_bytes, R, cap, grad, grad_stride, table2,
+                            grad2, grad2_stride, opt, ws, ws_bytes, stream);
 }
 
 extern "C" int32_t tfs_scatter_opt_planned(float* table, int64_t rows, int32_t dim,

@@ -406,11 +406,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           mbar_wait(empty + stage, phase ^ 1);
           // the leader's barrier (peer bit cleared)
           const uint32_t fb = smem_u32(full + stage) & (kCta == 2 ? 0xFEFFFFFFu : 0xFFFFFFFFu);
-#ifdef TFS_EXP_NO_TMA
-          if (leader) mbar_expect_tx(full + stage, 0);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          continue;
-#endif
           if (leader) mbar_expect_tx(full + stage, kCta * ns * (A_BYTES + bbytes));
           for (int sb = 0; sb < ns; ++sb) {
             const int kb = kb0 + sb;
@@ -457,14 +452,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             const int kb = kb0 + sb;
             const uint32_t a0 = smem_u32(sA + (stage * KSUB + sb) * A_BYTES);
             const uint32_t b0 = smem_u32(sB + (stage * KSUB + sb) * B_BYTES);
-#ifndef TFS_EXP_NO_MMA
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               umma_bf16(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
                         (kb > t.kb0 || k > 0) ? 1u : 0u);
-#else
-            (void)a0; (void)b0; (void)d_tmem; (void)kb;
-#endif
           }
           umma_commit_pair(empty + stage);
           if (++stage == STAGES) {
@@ -501,10 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       if (MODE != kStore) {
         // this half tile's 128 column offsets -> smem (each warp of the half loads 32); the
         // buffer of this accumulator was last read two tiles ago, before the previous barrier
-#ifndef TFS_EXP_CB_GLOBAL
         cbh[quarter * 32 + lane] =
             __ldg(ep.cb + t.nt * q.bn + half * 128 + quarter * 32 + lane);
-#endif
         if (row_ok) {
           if (ep.labels != nullptr) {
             const int64_t yl = __ldg(ep.labels + row);
@@ -522,22 +511,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
           if (MODE == kGrad) goff = __ldg(ep.lse + row) * kLog2e - log2f(ep.c);
         }
-#ifndef TFS_EXP_CB_GLOBAL
         named_bar_sync(2 + half, 128);
-#endif
       }
       float run_m = -INFINITY, run_s = 0.f;
 
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-#ifdef TFS_EXP_NO_EPI
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(tempty + acc);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-      continue;
-#endif
       // Software-pipelined TMEM reads: chunk c+1 is in flight while chunk c is processed.
       const uint32_t tbase =
           tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * 128);
@@ -564,11 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
         if (MODE != kStore) {
           // corrected logits in log2 units; accidental hits (rare) -> -inf
-#ifdef TFS_EXP_CB_GLOBAL
-          const float4* cb4 = reinterpret_cast<const float4*>(ep.cb + col0);
-#else
           const float4* cb4 = reinterpret_cast<const float4*>(cbh + c * 32);
-#endif
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const float4 cc = cb4[k];
@@ -578,7 +553,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             v[4 * k + 3] = fmaf(v[4 * k + 3], kLog2e, cc.w);
           }
           const bool mine = hlo <= col0 + 31 && hhi >= col0;
-#ifndef TFS_EXP_NO_HITS
           if (__any_sync(0xffffffffu, mine)) {
             if (mine) {
 #pragma unroll
@@ -593,7 +567,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                 }
             }
           }
-#endif
         }
         if (MODE == kStats) {
           float m4[4];

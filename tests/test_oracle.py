@@ -580,3 +580,111 @@ def test_adagrad_step_bounded_by_lr():
     g = rng.standard_normal((200, 8)) * 100.0
     w, a = oracle.scatter_opt("adagrad", T0, np.zeros_like(T0), ids, g, 0.01)
     assert np.all(np.abs(w.astype(np.float64) - T0) <= 0.01 * (1 + 1e-6))
+
+
+# ------------------------------------------------------- round 2 pins (VERDICT r1 "What's weak" 1)
+def test_log_uniform_closed_form_values():
+    """SURVEY c.4 prints p(k) for V = 1000, 40000, 800000 (k = 0, 1, V-1); the oracle's p_k
+    must agree to half a unit in the last printed digit."""
+    from decimal import Decimal
+    g = _golden("log_uniform_closed_form.json")
+    for v in g["values"]:
+        printed = Decimal(v["p"])
+        half_unit = Decimal(1).scaleb(printed.as_tuple().exponent) / 2
+        got = oracle.log_uniform_prob(v["V"], v["k"])
+        assert abs(Decimal(got) - printed) <= half_unit, (v, got)
+    # k = 0 special case: p(0) = ln 2 / ln(V + 1) (the telescoping sum's first term)
+    for V in (1000, 40000, 800000):
+        assert abs(oracle.log_uniform_prob(V, 0) - math.log(2) / math.log(V + 1)) < 1e-16
+
+
+def test_log_q_shift_invariance_pins_true_logit_correction():
+    """R-10: ln ec is subtracted from the TRUE logit and from every sampled logit.  With the
+    same value k for every label and every class, the correction shifts all logits of a token
+    by -k, which the softmax cannot see: loss and every gradient equal the uncorrected ones.
+    (Dropping the correction on either side breaks the equality.)"""
+    rng = np.random.default_rng(21)
+    B, S, V, d = 9, 13, 200, 5
+    h, labels, W, b, _, sampled = _ssm_inputs(rng, B, S, V, d, hit_frac=0.3)
+    plain = oracle.sampled_softmax(h, labels, W[labels], b[labels], np.zeros(B), sampled,
+                                   W[sampled], b[sampled], np.zeros(S),
+                                   flags=oracle.REMOVE_ACCIDENTAL_HITS, grad_scale=0.2)
+    for k in (-3.0, 0.75, 11.0):
+        cor = oracle.sampled_softmax(h, labels, W[labels], b[labels], np.full(B, k), sampled,
+                                     W[sampled], b[sampled], np.full(S, k), grad_scale=0.2)
+        np.testing.assert_allclose(cor["loss"], plain["loss"], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(cor["lse"], plain["lse"] - k, rtol=1e-12, atol=1e-11)
+        for key in ("dh", "dw_true", "db_true", "dw_s", "db_s"):
+            np.testing.assert_allclose(cor[key], plain[key], rtol=1e-10, atol=1e-15)
+    # the true-logit correction alone: raising ln ec(y_t) lowers z_t, so every loss rises
+    up = oracle.sampled_softmax(h, labels, W[labels], b[labels], np.full(B, 1.0), sampled,
+                                W[sampled], b[sampled], np.zeros(S), grad_scale=0.2)
+    assert np.all(up["loss"] > plain["loss"])
+
+
+def test_label_in_candidates_equals_textbook_full_softmax():
+    """R-30 (the sharded full softmax): all V classes as candidates with the label
+    among them (flag 4, no true-class term) == the textbook dense softmax cross-entropy, loss
+    and every gradient; and == the excluded-hit form with a separate true logit (R-9)."""
+    rng = np.random.default_rng(22)
+    B, V, d = 11, 29, 7
+    h, labels, W, b, _, _ = _ssm_inputs(rng, B, V, V, d)
+    c = 1.0 / B
+    o = oracle.sampled_softmax(h, labels, None, None, None, np.arange(V), W, b, np.zeros(V),
+                               flags=oracle.LABEL_IN_CANDIDATES, grad_scale=c)
+    loss, lse, dh, dW, db = _numpy_full_softmax(h, labels, W, b, c)
+    np.testing.assert_allclose(o["loss"], loss, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(o["lse"], lse, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(o["dh"], dh, rtol=1e-10, atol=1e-13)
+    np.testing.assert_allclose(o["dw_s"], dW, rtol=1e-10, atol=1e-13)
+    np.testing.assert_allclose(o["db_s"], db, rtol=1e-10, atol=1e-13)
+    assert np.all(o["dw_true"] == 0) and np.all(o["db_true"] == 0)
+    # a token whose label is missing from the candidates is an error in label-in mode
+    keep = np.setdiff1d(np.arange(V), [labels[0]])
+    with pytest.raises(oracle.OracleError):
+        oracle.sampled_softmax(h, labels, None, None, None, keep, W[keep], b[keep],
+                               np.zeros(keep.size), flags=oracle.LABEL_IN_CANDIDATES,
+                               grad_scale=c)
+
+
+def test_label_in_bf16_rounding_point():
+    """bf16 emulation of the sharded full softmax (R-18 + R-30): operands rounded RNE, and
+    G = c (p - onehot) rounded to bf16 AS A WHOLE at the label column (the GPU's epilogue
+    forms c p - c in fp32, then rounds), recomputed with numpy + torch casts."""
+    rng = np.random.default_rng(23)
+    B, V, d = 10, 40, 16
+    h, labels, W, b, _, _ = _ssm_inputs(rng, B, V, V, d)
+    c = 0.05
+    o = oracle.sampled_softmax(h, labels, None, None, None, np.arange(V), W, b, np.zeros(V),
+                               flags=oracle.LABEL_IN_CANDIDATES, grad_scale=c, bf16=True)
+    r = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).double().numpy()
+    hb, wb = r(h), r(W)
+    Z = hb @ wb.T + b
+    m = Z.max(1)
+    lse = m + np.log(np.exp(Z - m[:, None]).sum(1))
+    onehot = np.zeros_like(Z)
+    onehot[np.arange(B), labels] = 1.0
+    Gr = r((c * (np.exp(Z - lse[:, None]) - onehot)).astype(np.float32))
+    np.testing.assert_allclose(o["lse"], lse, rtol=1e-13)
+    np.testing.assert_allclose(o["loss"], lse - Z[np.arange(B), labels], rtol=1e-12)
+    np.testing.assert_allclose(o["dh"], Gr @ wb, rtol=1e-11, atol=1e-14)
+    np.testing.assert_allclose(o["dw_s"], Gr.T @ hb, rtol=1e-11, atol=1e-14)
+    np.testing.assert_allclose(o["db_s"], Gr.sum(0), rtol=1e-12, atol=1e-15)
+
+
+def test_abs_term_sums_bound_the_outputs():
+    """abs_* (the element-wise parity scale) are >= |output|, and equal it where every term is
+    non-negative: G >= 0 in sampled mode, so with h >= 0, abs_dw_s == dw_s and
+    abs_db_s == db_s; abs_loss = |lse| + |z|."""
+    rng = np.random.default_rng(24)
+    B, S, V, d = 12, 17, 300, 6
+    h, labels, W, b, le, sampled = _ssm_inputs(rng, B, S, V, d)
+    h = np.abs(h)
+    o = oracle.sampled_softmax(h, labels, W[labels], b[labels], le[labels], sampled, W[sampled],
+                               b[sampled], le[sampled], grad_scale=0.1)
+    for k in ("dh", "dw_s", "db_s"):
+        assert np.all(o["abs_" + k] >= np.abs(o[k]) * (1 - 1e-15))
+    np.testing.assert_allclose(o["abs_dw_s"], o["dw_s"], rtol=1e-14)
+    np.testing.assert_allclose(o["abs_db_s"], o["db_s"], rtol=1e-14)
+    np.testing.assert_allclose(o["abs_loss"], np.abs(o["lse"]) + np.abs(o["z_true"]), rtol=1e-15)
+    assert np.any(o["abs_dh"] > np.abs(o["dh"]) * 1.01)   # dh does cancel (g_t < 0 <= G)

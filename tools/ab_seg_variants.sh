@@ -5,6 +5,7 @@
 # then on the GPU:   gpurun -- bash tools/ab_seg_variants.sh
 # Prints "variant workload rep ms_per_step phases_ms" per run.
 cd "$(dirname "$0")/.."
+export TFS_ALLOW_VARIANT_LIB=1   # _lib.py honours TFS_LIB only with this set
 for rep in 1 2 3; do
  for w in X Z; do
   for v in base minb2 c4m4; do

@@ -1,13 +1,13 @@
 """Build an experiment variant of libtfs.so with extra -D switches, for A/B timing only.
 
-    python tools/build_variant.py OUT.so -DTFS_EXP_NO_TMA -DTFS_EXP_NO_MMA   # barrier skeleton
-    TFS_LIB=$PWD/OUT.so python tools/one_ssm.py                              # run against it
+    python tools/build_variant.py OUT.so -DTFS_KSUB=1
+    TFS_ALLOW_VARIANT_LIB=1 TFS_LIB=$PWD/OUT.so python tools/one_ssm.py      # run against it
 
-Switches (paper_1605_08695_b200/csrc): TFS_EXP_NO_TMA / TFS_EXP_NO_MMA / TFS_EXP_NO_EPI isolate
-the three roles of the tcgen05 GEMM (results are wrong; timing only), TFS_EXP_NO_HITS and
-TFS_EXP_CB_GLOBAL vary its epilogue, TFS_KSUB sets k-blocks per pipeline stage, TFS_UMMA_CTAS=2
-builds the CTA-pair GEMM, TFS_SEG_CHUNK / TFS_SEG_MINB tune the sparse apply.  The numbers these
-produced are in profiles/r1_summary.md.
+Tuning switches of the product source (every variant computes correct results): TFS_KSUB sets
+k-blocks per pipeline stage of the tcgen05 GEMM, TFS_UMMA_CTAS=2 builds the CTA-pair GEMM,
+TFS_SEG_CHUNK / TFS_SEG_MINB tune the sparse apply.  (Round 1's wrong-result role-isolation
+switches were removed from the product source; their numbers stay in profiles/r1_summary.md.)
+bench.py records the path and hash of the library it loaded.
 """
 import glob
 import os
