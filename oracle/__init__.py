@@ -71,6 +71,7 @@ class _SsmIO(ctypes.Structure):
         ("loss", P), ("lse", P), ("z_true", P), ("dh", P), ("dw_true", P), ("db_true", P),
         ("dw_s", P), ("db_s", P),
         ("abs_loss", P), ("abs_dh", P), ("abs_dw_s", P), ("abs_db_s", P),
+        ("amb_dh", P), ("amb_dw_s", P), ("amb_db_s", P),
     ]
 
 
@@ -199,7 +200,9 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
     """Sampled softmax forward + backward (O9-O11).  Returns a dict of fp64 arrays:
     loss, lse, z_true, dh, dw_true, db_true, dw_s, db_s, and abs_loss / abs_dh / abs_dw_s /
     abs_db_s -- the sums of absolute values of the terms forming those outputs (the scale of
-    the rounding error of any evaluation order; abs of dw_true / db_true is the value itself).
+    the rounding error of any evaluation order; abs of dw_true / db_true is the value itself)
+    -- and, in bf16 mode, amb_dh / amb_dw_s / amb_db_s: one bf16 unit (2^-8) of the terms whose
+    G rounding is a tie within 2^-14 (R-34: either neighbour is a correct rounding).
     flags may include LABEL_IN_CANDIDATES (R-30: sharded full softmax; w_true, b_true,
     log_ec_true are then unused and may be None)."""
     h = _c(h, np.float32)
@@ -225,6 +228,7 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
         "dw_s": np.empty((nc, d)), "db_s": np.empty(nc),
         "abs_loss": np.empty(nt), "abs_dh": np.empty((nt, d)), "abs_dw_s": np.empty((nc, d)),
         "abs_db_s": np.empty(nc),
+        "amb_dh": np.zeros((nt, d)), "amb_dw_s": np.zeros((nc, d)), "amb_db_s": np.zeros(nc),
     }
     io = _SsmIO(B, S, d, int(bf16), flags, grad_scale, _ptr(h), _ptr(labels), _ptr(w_true),
                 _ptr(b_true), _ptr(le_t), _ptr(sampled), _ptr(w_s), _ptr(b_s), _ptr(le_s),
@@ -232,7 +236,8 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
                 _ptr(out["loss"]), _ptr(out["lse"]), _ptr(out["z_true"]), _ptr(out["dh"]),
                 _ptr(out["dw_true"]), _ptr(out["db_true"]), _ptr(out["dw_s"]), _ptr(out["db_s"]),
                 _ptr(out["abs_loss"]), _ptr(out["abs_dh"]), _ptr(out["abs_dw_s"]),
-                _ptr(out["abs_db_s"]))
+                _ptr(out["abs_db_s"]), _ptr(out["amb_dh"]), _ptr(out["amb_dw_s"]),
+                _ptr(out["amb_db_s"]))
     _check(lib().orc_sampled_softmax(ctypes.byref(io)))
     return out
 

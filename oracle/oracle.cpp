@@ -316,9 +316,29 @@ int orc_sampled_softmax(const orc_ssm_io* io) {
     lse[t] = mu + std::log(sum);
   }
   // O11: G_tj = c e^{Z_tj - lse_t} (label-in: minus c at the label), bf16-rounded in bf16 mode.
-  auto G_at = [&](int64_t t, int64_t j) -> double {
-    return grad_round(c * (std::exp(z_samp(t, j) - lse[t]) - (is_label(t, j) ? 1.0 : 0.0)));
+  auto G_pre = [&](int64_t t, int64_t j) -> double {
+    return c * (std::exp(z_samp(t, j) - lse[t]) - (is_label(t, j) ? 1.0 : 0.0));
   };
+  // bf16 mode: is the rounding of this G a tie within evaluation error?  Any implementation
+  // forms G from logits that carry rounding error (the GPU: fp32 accumulation, fp32 exp2); when
+  // the exact value lies within kAmbiguity (relative) of the midpoint between two bf16 values,
+  // either neighbour is a correct rounding (reading R-34), and the element-wise bound admits
+  // one bf16 unit (2^-8 relative) of that term: the amb_* outputs.
+  constexpr double kAmbiguity = 1.0 / 16384.0;  // 2^-14
+  auto ambiguous = [&](double g) -> bool {
+    if (!io->bf16 || g == 0.0) return false;
+    const float f = (float)g;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    const uint32_t lo_b = u & 0xffff0000u, hi_b = lo_b + 0x10000u;
+    float lo, hi;
+    std::memcpy(&lo, &lo_b, 4);
+    std::memcpy(&hi, &hi_b, 4);
+    const double mid = 0.5 * ((double)lo + (double)hi);
+    return std::fabs(g - mid) <= kAmbiguity * std::fabs(g);
+  };
+  constexpr double kBf16Unit = 1.0 / 256.0;  // 2^-8: one bf16 unit, relative
+  auto G_at = [&](int64_t t, int64_t j) -> double { return grad_round(G_pre(t, j)); };
 
   // O10/O11 per token.
   const int64_t n_tok = io->tok_idx ? io->n_tok : B;
@@ -341,17 +361,21 @@ int orc_sampled_softmax(const orc_ssm_io* io) {
           dh[k] = g * wt[t * d + k];
           ad[k] = std::fabs(g * wt[t * d + k]);
         }
+      std::vector<double> am((size_t)d, 0.0);
       for (int64_t j = 0; j < S; ++j) {
         if (excluded(t, j)) continue;
-        const double G = G_at(t, j);
+        const double Gp = G_pre(t, j), G = grad_round(Gp);
+        const bool amb = ambiguous(Gp);
         for (int32_t k = 0; k < d; ++k) {
           dh[k] += G * ws[j * d + k];
           ad[k] += std::fabs(G * ws[j * d + k]);
+          if (amb) am[k] += kBf16Unit * std::fabs(G * ws[j * d + k]);
         }
       }
       for (int32_t k = 0; k < d; ++k) {
         if (io->dh) io->dh[r * d + k] = dh[k];
         if (io->abs_dh) io->abs_dh[r * d + k] = ad[k];
+        if (io->amb_dh) io->amb_dh[r * d + k] = am[k];
       }
     }
   }
@@ -361,24 +385,29 @@ int orc_sampled_softmax(const orc_ssm_io* io) {
   for (int64_t r = 0; r < n_col; ++r) {
     const int64_t j = io->col_idx ? io->col_idx[r] : r;
     if (j < 0 || j >= S) return kInvalid;
-    double db = 0.0, adb = 0.0;
-    std::vector<double> dw((size_t)d, 0.0), aw((size_t)d, 0.0);
+    double db = 0.0, adb = 0.0, amb_b = 0.0;
+    std::vector<double> dw((size_t)d, 0.0), aw((size_t)d, 0.0), am((size_t)d, 0.0);
     for (int64_t t = 0; t < B; ++t) {
       if (excluded(t, j)) continue;
-      const double G = G_at(t, j);
+      const double Gp = G_pre(t, j), G = grad_round(Gp);
+      const bool amb = ambiguous(Gp);
       db += G;
       adb += std::fabs(G);
+      if (amb) amb_b += kBf16Unit * std::fabs(G);
       for (int32_t k = 0; k < d; ++k) {
         dw[k] += G * h[t * d + k];
         aw[k] += std::fabs(G * h[t * d + k]);
+        if (amb) am[k] += kBf16Unit * std::fabs(G * h[t * d + k]);
       }
     }
     for (int32_t k = 0; k < d; ++k) {
       if (io->dw_s) io->dw_s[r * d + k] = dw[k];
       if (io->abs_dw_s) io->abs_dw_s[r * d + k] = aw[k];
+      if (io->amb_dw_s) io->amb_dw_s[r * d + k] = am[k];
     }
     if (io->db_s) io->db_s[r] = db;
     if (io->abs_db_s) io->abs_db_s[r] = adb;
+    if (io->amb_db_s) io->amb_db_s[r] = amb_b;
   }
   return kOk;
 }

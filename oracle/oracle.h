@@ -88,6 +88,9 @@ typedef struct {
    * db_s (|lse| + |z|; |g||W_true| + sum_j |G||W_s|; sum_t |G||h|; sum_t |G|) -- the scale of
    * any evaluation order's rounding error, used by the element-wise parity bound. */
   double* abs_loss; double* abs_dh; double* abs_dw_s; double* abs_db_s;
+  /* optional, bf16 mode: 2^-8 x the sum of |terms| whose G rounding is a tie within 2^-14
+   * relative (either bf16 neighbour is a correct rounding, reading R-34); 0 elsewhere. */
+  double* amb_dh; double* amb_dw_s; double* amb_db_s;
 } orc_ssm_io;
 int orc_sampled_softmax(const orc_ssm_io* io);
 

@@ -59,6 +59,7 @@ class ReplicaTrace:
     b_rows: np.ndarray = None     # [B+S]
     ssm: dict = field(default_factory=dict)
     abs_delta: tuple = None       # (E, W, b) update scales, traces[0] only, cfg.abs_bounds
+    amb_delta: tuple = None       # (E, W, b) bf16 rounding-tie allowances (R-34), likewise
 
 
 def _route(send_local, counts, R):
@@ -171,4 +172,15 @@ def step(E, W, b, xs, ys, cfg: StepConfig):
             np.add.at(aW, q, cfg.lr * np.concatenate([sg[:, None] * hs, t.ssm["abs_dw_s"]]))
             np.add.at(ab, q, cfg.lr * np.concatenate([sg, t.ssm["abs_db_s"]]))
         traces[0].abs_delta = (aE, aW, ab)
+        # bf16 rounding ties (R-34): lr x the amb_* allowances of the contributions
+        mE, mW, mb = np.zeros(E.shape), np.zeros(W.shape), np.zeros(b.shape)
+        for r in range(R):
+            t = traces[r]
+            np.add.at(mE, xs[r], cfg.lr * t.ssm["amb_dh"])
+            q = np.concatenate([ys[r], t.sampled])
+            np.add.at(mW, q, cfg.lr * np.concatenate([np.zeros_like(t.ssm["dw_true"]),
+                                                     t.ssm["amb_dw_s"]]))
+            np.add.at(mb, q, cfg.lr * np.concatenate([np.zeros_like(t.ssm["db_true"]),
+                                                     t.ssm["amb_db_s"]]))
+        traces[0].amb_delta = (mE, mW, mb)
     return E2, W2, b2, traces

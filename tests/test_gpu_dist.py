@@ -95,15 +95,26 @@ def _worker_body(rank, world, port, name, dtype, route, q, full):
                 res["sampled"] &= bool(np.array_equal(st.tensor("qw")[B:].cpu().numpy(),
                                                       tr[rank].sampled))
             aE, aW, ab = tr[0].abs_delta
-            for nm, T0, To, A in (("E", E, E2, aE), ("W", W, W2, aW), ("b", b, b2, ab)):
+            mE, mW, mb = tr[0].amb_delta
+            nxt = []
+            for nm, T0, To, A, Mb in (("E", E, E2, aE, mE), ("W", W, W2, aW, mW),
+                                      ("b", b, b2, ab, mb)):
                 g = st.tensor(nm).cpu().numpy()
-                t0, to, a = T0[rank::R], To[rank::R], A[rank::R]
+                t0, to, a, m = T0[rank::R], To[rank::R], A[rank::R], Mb[rank::R]
                 touched = np.nonzero(np.any((a != 0).reshape(t0.shape[0], -1), axis=1))[0]
                 untouched = np.setdiff1d(np.arange(t0.shape[0]), touched)
                 res[nm + "_untouched"] = res.get(nm + "_untouched", True) and bool(
                     np.array_equal(g[untouched], t0[untouched]))
-                res[nm] = max(res.get(nm, 0.0), update_err(g[touched], to[touched], a[touched]))
-            E, W, b = E2, W2, b2
+                res[nm] = max(res.get(nm, 0.0), update_err(g[touched], to[touched], a[touched],
+                                                           allow=m[touched]))
+                # the next step starts from the GPUs' own state (identical inputs, c.5)
+                parts = [None] * R
+                dist.all_gather_object(parts, g)
+                full = np.empty_like(T0)
+                for r in range(R):
+                    full[r::R] = parts[r]
+                nxt.append(full)
+            E, W, b = nxt
         q.put((rank, res))
         st.close()
         comm.close()

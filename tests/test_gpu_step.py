@@ -18,7 +18,8 @@ import torch
 import oracle
 from oracle import step as ostep
 import workloads
-from parity import TOL_BF16_ACC, TOL_BF16_EMU, TOL_F32, elem_err, ssm_scales, update_err
+from parity import (TOL_BF16_ACC, TOL_BF16_EMU, TOL_F32, elem_err, ssm_allow, ssm_scales,
+                    update_err)
 
 pytestmark = pytest.mark.gpu
 
@@ -103,16 +104,31 @@ def _check_step(st, E, W, b, xs, ys, cfg, emu, tol, step, E2=None):
     scale = sum(t.ssm["abs_loss"].sum() for t in tr) / (R * B)
     assert abs(got - want) <= tol * scale, (got, want)
     aE, aW, ab = tr[0].abs_delta
-    for name, T0, To, A in (("E", E, E2, aE), ("W", W, W2, aW), ("b", b, b2, ab)):
+    mE, mW, mb = tr[0].amb_delta
+    for name, T0, To, A, M in (("E", E, E2, aE, mE), ("W", W, W2, aW, mW), ("b", b, b2, ab, mb)):
         for r in range(st.nlocal):
             g = st.tensor(name, r).cpu().numpy()
-            t0, to, a = T0[r::R], To[r::R], A[r::R]
+            t0, to, a, m = T0[r::R], To[r::R], A[r::R], M[r::R]
             touched = np.nonzero(np.any((a != 0).reshape(t0.shape[0], -1), axis=1))[0]
             untouched = np.setdiff1d(np.arange(t0.shape[0]), touched)
             assert np.array_equal(g[untouched], t0[untouched]), (name, r)
-            e = update_err(g[touched], to[touched], a[touched])
+            e = update_err(g[touched], to[touched], a[touched], allow=m[touched])
             assert e <= tol, (name, r, e)
     return E2, W2, b2, tr
+
+
+def gpu_tables(st, V):
+    """The logical tables E, W, b assembled from every local rank's shard (row i of shard
+    i mod R at local row i div R) -- the state the next step starts from."""
+    R = st.R
+    out = []
+    for name in ("E", "W", "b"):
+        parts = [st.tensor(name, r).cpu().numpy() for r in range(st.nlocal)]
+        full = np.empty((V,) + parts[0].shape[1:], np.float32)
+        for r in range(R):
+            full[r::R] = parts[r]
+        out.append(full)
+    return out
 
 
 # ------------------------------------------------------------------------------------- R = 1
@@ -220,26 +236,29 @@ def test_step_config_X_full_outputs():
     o = oracle.sampled_softmax(E[x], y, W[y], b[y], ley.astype(np.float32).astype(np.float64), s,
                                W[s], b[s], les.astype(np.float32).astype(np.float64),
                                grad_scale=c, bf16=True)
-    sc = ssm_scales(o, c)
+    sc, al = ssm_scales(o, c), ssm_allow(o)
     dw, db = st.tensor("dw").cpu().numpy(), st.tensor("db").cpu().numpy()
     got = {"loss": st.tensor("loss").cpu().numpy(), "lse": st.tensor("lse").cpu().numpy(),
            "dh": st.tensor("dh").cpu().numpy(), "dw_true": dw[:B], "db_true": db[:B],
            "dw_s": dw[B:], "db_s": db[B:]}
     for k, v in got.items():
-        e = elem_err(v, o[k], sc[k])
+        e = elem_err(v, o[k], sc[k], al[k])
         assert e <= TOL_BF16_EMU, (k, e)
     # table updates of the touched rows (sub-tables indexed by the distinct ids)
-    for name, T0, ids, grads, scale in (
-            ("E", E, x, o["dh"], o["abs_dh"]),
+    for name, T0, ids, grads, scale, amb in (
+            ("E", E, x, o["dh"], o["abs_dh"], o["amb_dh"]),
             ("W", W, np.concatenate([y, s]), np.concatenate([o["dw_true"], o["dw_s"]]),
-             np.concatenate([sc["dw_true"], o["abs_dw_s"]])),
+             np.concatenate([sc["dw_true"], o["abs_dw_s"]]),
+             np.concatenate([np.zeros_like(o["dw_true"]), o["amb_dw_s"]])),
             ("b", b, np.concatenate([y, s]), np.concatenate([o["db_true"], o["db_s"]]),
-             np.concatenate([sc["db_true"], o["abs_db_s"]]))):
+             np.concatenate([sc["db_true"], o["abs_db_s"]]),
+             np.concatenate([np.zeros_like(o["db_true"]), o["amb_db_s"]]))):
         u, inv = np.unique(ids, return_inverse=True)
         ref = oracle.scatter_add_sgd(T0[u], inv, grads, cfg.lr)
         _, a, _ = oracle.sort_reduce(inv, 1, scale)
+        _, m, _ = oracle.sort_reduce(inv, 1, amb)
         g = st.tensor(name)[torch.from_numpy(u).to(DEV)].cpu().numpy()
-        e = update_err(g, ref, cfg.lr * a)
+        e = update_err(g, ref, cfg.lr * a, allow=cfg.lr * m)
         assert e <= TOL_BF16_EMU, (name, e)
 
 
@@ -265,7 +284,8 @@ def test_step_config_Z_sampled_tokens():
                                grad_scale=1.0 / B, bf16=True, tok_idx=tok, col_idx=np.zeros(0, np.int64))
     assert elem_err(st.tensor("loss").cpu().numpy()[tok], o["loss"], o["abs_loss"]) <= TOL_BF16_EMU
     assert elem_err(st.tensor("lse").cpu().numpy()[tok], o["lse"], o["abs_loss"]) <= TOL_BF16_EMU
-    assert elem_err(st.tensor("dh").cpu().numpy()[tok], o["dh"], o["abs_dh"]) <= TOL_BF16_EMU
+    assert elem_err(st.tensor("dh").cpu().numpy()[tok], o["dh"], o["abs_dh"],
+                    o["amb_dh"]) <= TOL_BF16_EMU
 
 
 @pytest.mark.parametrize("kind", ["momentum", "adagrad"])
@@ -353,7 +373,8 @@ def test_sim_sharded_steps_graph_replay(R):
     st.capture()
     for k in range(3):
         xs, ys = _batches(w, R, step=k)
-        E, W, b, _ = _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, k)
+        E, W, b = gpu_tables(st, w.vocab)        # identical inputs: the GPU's state (c.5)
+        _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, k)
 
 
 @pytest.mark.parametrize("R,vocab,tokens", [(2, 1000, 32), (3, 4003, 96), (4, 4003, 64)])
@@ -366,8 +387,9 @@ def test_sim_sharded_full_softmax(R, vocab, tokens):
     cfg = _cfg(w, R, TFS_BF16)
     xs, ys = _batches(w, R)
     st = make_step(cfg, E, W, b)
-    E, W, b, _ = _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, 0)
+    _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, 0)
     xs, ys = _batches(w, R, step=1)              # second step: updated W / its bf16 shadow
+    E, W, b = gpu_tables(st, vocab)              # from the GPU's own state (identical inputs)
     _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, 1)
 
 

@@ -688,3 +688,29 @@ def test_abs_term_sums_bound_the_outputs():
     np.testing.assert_allclose(o["abs_db_s"], o["db_s"], rtol=1e-14)
     np.testing.assert_allclose(o["abs_loss"], np.abs(o["lse"]) + np.abs(o["z_true"]), rtol=1e-15)
     assert np.any(o["abs_dh"] > np.abs(o["dh"]) * 1.01)   # dh does cancel (g_t < 0 <= G)
+
+
+def test_bf16_rounding_ties_are_flagged():
+    """R-34: a G whose exact value is a bf16 rounding tie (within 2^-14) is flagged, and its
+    term enters amb_* at one bf16 unit.  h = 0, equal biases, no log-Q: G_tj = c / (1 + S) for
+    tokens without hits; with c = (1 + S)(1 + 2^-8), G = 1 + 2^-8 is exactly the midpoint of the
+    bf16 neighbours 1 and 1 + 2^-7 (ties to even -> 1).  fp32 mode flags nothing."""
+    rng = np.random.default_rng(25)
+    B, S, V, d = 6, 9, 400, 4
+    _, labels, W, _, _, sampled = _ssm_inputs(rng, B, S, V, d, hit_frac=0.0)
+    labels = np.setdiff1d(np.arange(V), sampled)[:B]           # no accidental hits
+    h = np.zeros((B, d), np.float32)
+    bb = np.full(V, 0.5, np.float32)
+    c = (1 + S) * (1 + 2.0 ** -8)
+    args = (h, labels, W[labels], bb[labels], np.zeros(B), sampled, W[sampled], bb[sampled],
+            np.zeros(S))
+    o = oracle.sampled_softmax(*args, flags=oracle.REMOVE_ACCIDENTAL_HITS, grad_scale=c, bf16=True)
+    np.testing.assert_array_equal(o["db_s"], np.full(S, B * 1.0))          # ties to even: 1.0
+    np.testing.assert_allclose(o["amb_db_s"], np.full(S, B * 2.0 ** -8), rtol=1e-15)
+    assert np.all(o["amb_dh"] <= o["abs_dh"] * 2.0 ** -8 * (1 + 1e-12))
+    f = oracle.sampled_softmax(*args, flags=oracle.REMOVE_ACCIDENTAL_HITS, grad_scale=c)
+    assert not f["amb_db_s"].any() and not f["amb_dh"].any() and not f["amb_dw_s"].any()
+    # away from a tie nothing is flagged
+    g = oracle.sampled_softmax(*args, flags=oracle.REMOVE_ACCIDENTAL_HITS, grad_scale=c * 1.001,
+                               bf16=True)
+    assert not g["amb_db_s"].any()
