@@ -145,6 +145,18 @@ int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int32_t num_sam
                                float* out_log_ec_labels, int64_t* out_num_tries, void* ws,
                                size_t ws_bytes, tfs_device_error* err, void* stream);
 
+/* tfs_sample_commit: the step draws each step's candidates one step AHEAD (the draws depend on
+ * (seed, step, replica) only, not on the batch), off the critical path; at the step it commits
+ * them: out_sampled / out_log_ec_sampled / out_num_tries = copies of a tfs_log_uniform_sample
+ * result (drawn with n_labels = 0), and out_log_ec_labels[t] = log ec(labels[t]) with that T --
+ * identical to one tfs_log_uniform_sample call with the labels.  Bad labels as there. */
+int32_t tfs_sample_commit(int64_t vocab, int32_t num_sampled, int32_t unique,
+                          const int64_t* sampled, const float* log_ec_sampled,
+                          const int64_t* num_tries, const int64_t* labels, int64_t n_labels,
+                          int64_t* out_sampled, float* out_log_ec_sampled,
+                          float* out_log_ec_labels, int64_t* out_num_tries,
+                          tfs_device_error* err, void* stream);
+
 /* ==== Sampled softmax forward + backward (DESIGN §3 O9-O11) ==========
  * "performs a sparse multiplication based on the true class for an example and a set of
  * randomly sampled false classes".  For tokens t < B and candidates j < S (R-7: one candidate
@@ -528,6 +540,11 @@ int32_t tfs_step_buffer(tfs_stepper* st, int32_t local, int32_t which, void** pt
 /* After the caller wrote tables / slots: refresh derived copies (the bf16 operand shadow of W
  * in the sharded full softmax) and zero the error slots; synchronises the device. */
 int32_t tfs_step_sync(tfs_stepper* st);
+/* Set every local rank's step counter (the sampler's step, R-17) and re-draw the sample the
+ * next step commits (each step draws the following step's candidates ahead of time).  The
+ * counter buffer TFS_BUF_STEP is read-only for callers: write it only through this call.
+ * Synchronises the device. */
+int32_t tfs_step_set_counter(tfs_stepper* st, int64_t value);
 /* One step of every local rank on `stream`.  io->host == 0: x / y are DEVICE pointers to
  * [nlocal x B] int64 (rank-major); == 1: HOST pointers (pinned for asynchrony) copied to the
  * step's input buffers on `stream` inside the call, and each local rank's loss_sum is copied

@@ -225,6 +225,34 @@ __global__ void sample_finish_kernel(const int32_t* draws, int32_t* firstpos, in
 
 __global__ void set_i64_kernel(int64_t* p, int64_t v) { *p = v; }
 
+// Commit of a sample drawn ahead of time: copy (s, log ec(s), T) into the step's buffers and
+// form the labels' log expected counts with that T.
+__global__ void sample_commit_kernel(int64_t V, double log_v1, int unique, int32_t S,
+                                     const int64_t* s_in, const float* les_in,
+                                     const int64_t* T_in, const int64_t* labels, int64_t n_labels,
+                                     int64_t* s_out, float* les_out, float* ley_out,
+                                     int64_t* T_out, tfs_device_error* err) {
+  const int64_t T = unique ? *T_in : (int64_t)S;
+  const int64_t total = (int64_t)S + n_labels;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e == 0) *T_out = *T_in;
+    if (e < S) {
+      s_out[e] = s_in[e];
+      les_out[e] = les_in[e];
+    } else {
+      const int64_t t = e - S;
+      const int64_t k = labels[t];
+      if (k < 0 || k >= V) {
+        report_error(err, TFS_ERR_OUT_OF_RANGE, t);
+        ley_out[t] = 0.f;
+      } else {
+        ley_out[t] = log_expected_count(k, V, log_v1, unique, T, S);
+      }
+    }
+  }
+}
+
 }  // namespace tfs
 
 using namespace tfs;
@@ -341,6 +369,28 @@ extern "C" int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int3
                                              out_num_tries, out_log_ec_sampled, out_log_ec_labels,
                                              err); ::tfs::launched();
   }
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
+extern "C" int32_t tfs_sample_commit(int64_t vocab, int32_t num_sampled, int32_t unique,
+                                     const int64_t* sampled, const float* log_ec_sampled,
+                                     const int64_t* num_tries, const int64_t* labels,
+                                     int64_t n_labels, int64_t* out_sampled,
+                                     float* out_log_ec_sampled, float* out_log_ec_labels,
+                                     int64_t* out_num_tries, tfs_device_error* err,
+                                     void* stream) {
+  TFS_REQUIRE(vocab >= 1 && num_sampled >= 0 && n_labels >= 0 && num_tries && out_num_tries);
+  TFS_REQUIRE(num_sampled == 0 || (sampled && log_ec_sampled && out_sampled && out_log_ec_sampled));
+  TFS_REQUIRE(n_labels == 0 || (labels && out_log_ec_labels));
+  TFS_SUPPORTED();
+  const int64_t total = std::max<int64_t>(1, (int64_t)num_sampled + n_labels);
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 4 * num_sms()));
+  sample_commit_kernel<<<g, 256, 0, as_stream(stream)>>>(
+      vocab, std::log((double)vocab + 1.0), unique, num_sampled, sampled, log_ec_sampled,
+      num_tries, labels, n_labels, out_sampled, out_log_ec_sampled, out_log_ec_labels,
+      out_num_tries, err);
+  ::tfs::launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }

@@ -71,6 +71,10 @@ __global__ void barrier_kernel(const int64_t* bases, int R, int rank, int ch, ui
 
 __global__ void add_i64_kernel(int64_t* p, int64_t v) { *p += v; }
 
+__global__ void next_counter_kernel(const int64_t* step, int64_t* next, int64_t add) {
+  *next = *step + add;
+}
+
 // Index maps of the steps, computed once at create (nothing of them is left to the caller):
 // mode 0: out[i] = i * mul + add (the candidate ids of a shard: j R + r; the full softmax's
 // candidates 0..V-1); mode 1: out[g] = (g mod B) R + g div B (the all-gather order of the
@@ -310,12 +314,14 @@ struct BufInfo {
   int32_t t = 0;
 };
 
-enum Ev { kFork, kH, kQ, kPlanW, kOwn, kSsm, kRedE, kB2, kSideDone, kMainDone, kBar, kNumEv };
+enum Ev { kFork, kH, kQ, kPlanW, kOwn, kSsm, kRedE, kB2, kSideDone, kMainDone, kBar, kCommit,
+          kSmp, kNumEv };
 
 struct Rank {
   int r = 0;           // global rank
   int64_t nloc = 0;    // rows of this shard
   cudaStream_t main = nullptr, side = nullptr;  // main: caller's stream (nlocal == 1) or own
+  cudaStream_t smp = nullptr;                    // draws the NEXT step's candidates
   bool own_main = false;
   cudaEvent_t ev[kNumEv] = {};
   BufInfo buf[TFS_BUF_COUNT_];
@@ -331,6 +337,8 @@ struct Rank {
   float *dh = nullptr, *dw = nullptr, *db = nullptr;
   tfs_device_error* err = nullptr;
   void *smp_state = nullptr, *smp_ws = nullptr;
+  int64_t *s_next = nullptr, *T_next = nullptr, *step_next = nullptr;  // drawn one step ahead
+  float* les_next = nullptr;
   size_t smp_ws_b = 0;
   int64_t max_draws = 0;
   void* ws_ssm = nullptr;
@@ -459,13 +467,40 @@ tfs_ssm_args slice_args(const tfs_stepper* st, const Rank& k, bool backward) {
   return a;
 }
 
-int32_t sample(tfs_stepper* st, Rank& k, cudaStream_t s) {
+// The candidates of a step depend on (seed, step, replica) only (R-7, R-17), so each step draws
+// the NEXT step's sample on its own stream, concurrently with its softmax, and commits the
+// ahead-drawn sample at its start (tfs_sample_commit: copies + the labels' log expected counts).
+// `add` = 1: draw for the step after the current counter (the pipelined case); 0: prime the
+// pipeline for the current counter (create / set_counter / sync).
+int32_t presample(tfs_stepper* st, Rank& k, cudaStream_t s, int64_t add) {
   const Dims& m = st->m;
   if (m.full) return TFS_OK;
+  next_counter_kernel<<<1, 1, 0, s>>>(k.step, k.step_next, add);
+  launched();
+  TFS_LAUNCH_CHECK();
   return tfs_log_uniform_sample(k.smp_state, m.V, (int32_t)m.S, st->cfg.unique, k.max_draws,
-                                st->cfg.seed, 0, (const uint64_t*)k.step, (uint32_t)k.r, k.y,
-                                m.B, k.qw + m.B, k.les, k.ley, k.num_tries, k.smp_ws, k.smp_ws_b,
-                                k.err, s);
+                                st->cfg.seed, 0, (const uint64_t*)k.step_next, (uint32_t)k.r,
+                                nullptr, 0, k.s_next, k.les_next, nullptr, k.T_next, k.smp_ws,
+                                k.smp_ws_b, k.err, s);
+}
+
+int32_t commit(tfs_stepper* st, Rank& k, cudaStream_t s) {
+  const Dims& m = st->m;
+  if (m.full) return TFS_OK;
+  return tfs_sample_commit(m.V, (int32_t)m.S, st->cfg.unique, k.s_next, k.les_next, k.T_next,
+                           k.y, m.B, k.qw + m.B, k.les, k.ley, k.num_tries, k.err, s);
+}
+
+// At the start of a step: commit this step's sample, then fork the next step's draw.
+void sample_phase(tfs_stepper* st, Rank& k, cudaStream_t mn) {
+  if (st->m.full) return;
+  STEP_CALL(st, commit(st, k, mn));
+  STEP_CALL(st, join(k.smp, mn, k.ev[kCommit]));
+  STEP_CALL(st, presample(st, k, k.smp, 1));
+  STEP_CALL(st, rec(k.ev[kSmp], k.smp));
+}
+void sample_join(tfs_stepper* st, Rank& k, cudaStream_t mn) {
+  if (!st->m.full) STEP_CALL(st, waitev(mn, k.ev[kSmp]));
 }
 
 int32_t apply_local(tfs_stepper* st, Rank& k, bool e_table, cudaStream_t s) {
@@ -519,7 +554,7 @@ void local_step(tfs_stepper* st, Rank& k, cudaStream_t mn) {
   STEP_CALL(st, tfs_scatter_plan(k.x, m.B, m.V, k.plan_e, k.plan_e_b, k.err, sd));
   if (cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) != cudaSuccess)
     st->status = st->status ? st->status : TFS_ERR_CUDA;
-  STEP_CALL(st, sample(st, k, mn));
+  sample_phase(st, k, mn);
   STEP_CALL(st, rec(k.ev[kQ], mn));
   STEP_CALL(st, waitev(sd, k.ev[kQ]));
   STEP_CALL(st, tfs_scatter_plan(k.qw, m.B + m.Seff, m.V, k.plan_w, k.plan_w_b, k.err, sd));
@@ -535,6 +570,7 @@ void local_step(tfs_stepper* st, Rank& k, cudaStream_t mn) {
   STEP_CALL(st, waitev(mn, k.ev[kPlanW]));
   STEP_CALL(st, apply_local(st, k, false, mn));
   STEP_CALL(st, join(mn, sd, k.ev[kSideDone]));
+  sample_join(st, k, mn);
 }
 
 // The same step on one stream, its phases bracketed by the caller's events (instrumentation).
@@ -547,7 +583,8 @@ void local_step_serial(tfs_stepper* st, Rank& k, cudaStream_t mn, void* const* e
   mark(0);
   if (cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) != cudaSuccess)
     st->status = st->status ? st->status : TFS_ERR_CUDA;
-  STEP_CALL(st, sample(st, k, mn));
+  STEP_CALL(st, commit(st, k, mn));       // this step's sample (drawn ahead) ...
+  STEP_CALL(st, presample(st, k, mn, 1)); // ... and the next step's draw, inline here
   mark(1);
   STEP_CALL(st, tfs_gather(k.E, m.V, m.d, TFS_F32, k.x, m.B, k.h, rdt, k.err, mn));
   STEP_CALL(st, tfs_gather2(k.W, m.V, m.d, k.b, k.qw, m.B + m.Seff, k.w_rows, rdt, k.b_rows,
@@ -604,7 +641,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       if (cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) !=
           cudaSuccess)
         st->status = st->status ? st->status : TFS_ERR_CUDA;
-      STEP_CALL(st, sample(st, k, mn));
+      sample_phase(st, k, mn);
       STEP_CALL(st, rec(k.ev[kQ], mn));
       STEP_CALL(st, waitev(sd, k.ev[kQ]));
       STEP_CALL(st, tfs_route_plan_push(k.qw, m.B + m.S, m.V, R, m.cap_w, k.rplan_w, k.rplan_w_b,
@@ -643,6 +680,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       STEP_CALL(st, waitev(mn, k.ev[kOwn]));
       STEP_CALL(st, apply_owner(st, k, false, mn));
       STEP_CALL(st, join(mn, sd, k.ev[kSideDone]));
+      sample_join(st, k, mn);
       break;
   }
 }
@@ -799,10 +837,24 @@ void free_rank(Rank& k) {
   for (int i = 0; i < kNumEv; ++i)
     if (k.ev[i]) cudaEventDestroy(k.ev[i]);
   if (k.side) cudaStreamDestroy(k.side);
+  if (k.smp) cudaStreamDestroy(k.smp);
   if (k.own_main && k.main) cudaStreamDestroy(k.main);
   if (k.block) cudaFree(k.block);
 }
 
+}  // namespace
+
+namespace {
+// Draw the sample of the CURRENT step counter into the ahead buffers (create, set_counter,
+// sync): the first step's commit then finds it there.
+int32_t prime(tfs_stepper* st) {
+  for (auto& k : st->ranks) {
+    int32_t r = presample(st, k, k.smp, 0);
+    if (r != TFS_OK) return r;
+  }
+  for (auto& k : st->ranks) TFS_CUDA_TRY(cudaStreamSynchronize(k.smp));
+  return TFS_OK;
+}
 }  // namespace
 
 extern "C" size_t tfs_step_heap_bytes(const tfs_step_config* cfg) {
@@ -855,7 +907,8 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
     Rank& k = st->ranks[l];
     k.r = (m.R == 1) ? 0 : comm->first + l;
     k.nloc = cdiv(V - k.r, R);
-    if (cudaStreamCreateWithFlags(&k.side, cudaStreamNonBlocking) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&k.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&k.smp, cudaStreamNonBlocking) != cudaSuccess)
       return bail(TFS_ERR_CUDA);
     if (nl > 1) {
       if (cudaStreamCreateWithFlags(&k.main, cudaStreamNonBlocking) != cudaSuccess)
@@ -891,6 +944,9 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
       cv.take<float>((B + m.Seff) * d);             // dw
       cv.take<float>(B + m.Seff);                   // db
       cv.take<char>(smp_state_b);
+      cv.take<int64_t>(std::max<int64_t>(m.S, 1));  // s_next
+      cv.take<float>(std::max<int64_t>(m.S, 1));    // les_next
+      cv.take<int64_t>(4);                          // T_next, step_next
     };
     plan_sizes(c, false);
     // the rest is carved after the sizes of plans / workspaces are known
@@ -960,6 +1016,10 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
     k.dw = cv.take<float>((B + m.Seff) * d);
     k.db = cv.take<float>(B + m.Seff);
     k.smp_state = smp_state_b ? (void*)cv.take<char>(smp_state_b) : nullptr;
+    k.s_next = cv.take<int64_t>(std::max<int64_t>(m.S, 1));
+    k.les_next = cv.take<float>(std::max<int64_t>(m.S, 1));
+    k.T_next = cv.take<int64_t>(4);
+    k.step_next = k.T_next + 1;
     if (m.R == 1) {
       k.plan_e = cv.take<char>(k.plan_e_b);
       k.plan_w = cv.take<char>(k.plan_w_b);
@@ -1086,6 +1146,8 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
     (void)nq;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(TFS_ERR_CUDA);
+  int32_t pr = prime(st);
+  if (pr != TFS_OK) return bail(pr);
   *out = st;
   return TFS_OK;
 }
@@ -1115,7 +1177,15 @@ extern "C" int32_t tfs_step_sync(tfs_stepper* st) {
     for (int l = 0; l < st->comm->nlocal; ++l)
       TFS_CUDA_TRY(cudaMemcpy(st->comm->d_err[l], &none, sizeof(none), cudaMemcpyHostToDevice));
   TFS_CUDA_TRY(cudaDeviceSynchronize());
-  return TFS_OK;
+  return prime(st);
+}
+
+extern "C" int32_t tfs_step_set_counter(tfs_stepper* st, int64_t value) {
+  TFS_REQUIRE(st && value >= 0);
+  TFS_CUDA_TRY(cudaDeviceSynchronize());
+  for (auto& k : st->ranks)
+    TFS_CUDA_TRY(cudaMemcpy(k.step, &value, sizeof(int64_t), cudaMemcpyHostToDevice));
+  return prime(st);
 }
 
 extern "C" int32_t tfs_step_run(tfs_stepper* st, const tfs_step_io* io, void* stream) {

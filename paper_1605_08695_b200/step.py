@@ -220,8 +220,8 @@ class Step:
         check(_lib.lib().tfs_step_sync(self.ptr), "tfs_step_sync")
 
     def set_step(self, value: int):
-        for l in range(self.nlocal):
-            self.tensor("step", l).fill_(int(value))
+        """Set the step counter of every local rank (re-draws the sample drawn ahead)."""
+        check(_lib.lib().tfs_step_set_counter(self.ptr, int(value)), "tfs_step_set_counter")
 
     # ---- running
     def run(self, x=None, y=None, timing_events=None):
