@@ -27,12 +27,10 @@ constexpr int kSortItems = 4;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 1024 items per CTA
 constexpr int kMaxBuckets = 256;
 #ifndef TFS_SEG_CHUNK
-#define TFS_SEG_CHUNK 8
+#define TFS_SEG_CHUNK 32
 #endif
 constexpr int kChunk = TFS_SEG_CHUNK;  // sorted rows per warp in the segmented sums
-#ifndef TFS_SEG_MINB
-#define TFS_SEG_MINB 3  // 3 CTAs / SM (<= 85 registers): measured 24 -> 14 us on 10k Zipf rows
-#endif
+
 
 struct DigitSrc {
   int mode;
@@ -577,112 +575,135 @@ __device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_afte
   return PieceDst{0, 0};
 }
 
-// One warp per (chunk of kChunk sorted rows, slice of 32 float4 columns), dim % 4 == 0.
-// All kChunk gradient rows -- and, in apply mode, the table row of every segment that lies
-// inside the chunk -- are loaded at once; each segment's rows are added in sorted order in
-// fp64 and the segment is applied (T = fl32(T - lr * g)) or written directly.  Pieces of
-// segments that cross a chunk boundary go to partial slots and the segment to cross_list.
+// One CTA per window of kChunk sorted rows, all columns (thread = one float4 column group,
+// looping when dim / 4 exceeds the CTA).  The window's segment structure (heads, ends, whole
+// segments, crossings) is computed once by warp 0 and is uniform across the CTA, so the column
+// threads run branch-uniform: every row of a batch of 8 -- and the table row of every whole
+// segment ending in the batch -- is loaded at once, each segment's rows are added in sorted
+// order in fp64, and a whole segment is applied (T = fl32(T - lr g), or Momentum / Adagrad) or
+// written; pieces of segments crossing the window's edges go to the partial slots (2c: the
+// piece of the segment that started before window c; 2c + 1: the piece of the segment that
+// starts in c and continues after it) and the segment to cross_list.
+constexpr int kWinBatch = 8;
+static_assert(kChunk == 32, "the window prologue maps row r of a window to lane r");
 template <int OPT>
-__global__ void __launch_bounds__(256, TFS_SEG_MINB) seg_chunk_vec4_kernel(SegJob j, int nslices) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int64_t chunk = gw / nslices;
-  const int slice = (int)(gw - chunk * nslices);
+__global__ void __launch_bounds__(128) seg_window_vec4_kernel(SegJob j) {
+  __shared__ uint32_t s_perm[kChunk], s_key[kChunk], s_seg[kChunk];
+  __shared__ float s_r2[kChunk];
+  __shared__ uint32_t s_mask[3];
+  __shared__ int s_edge[2];
+  const int64_t chunk = blockIdx.x;
   const int64_t base = chunk * kChunk;
-  if (base >= j.n) return;
   const int cnt = (int)min((int64_t)kChunk, j.n - base);
-  const bool write_mode = j.table == nullptr;
-  uint32_t perm_l = 0, seg_l = 0, key_l = 0;
-  float r2_l = 0.f;
-  if (lane < cnt) {
-    perm_l = j.perm[base + lane];
-    seg_l = j.seg_of[base + lane];
-    key_l = j.keys[base + lane];
-    if (j.rows2 && slice == 0) r2_l = j.rows2[row2_off(j, perm_l)];
-  }
-  // Does the first segment start before this chunk / the last one continue after it?
-  uint32_t edge = 0;
-  if (lane == 0 && base > 0) edge = j.keys[base - 1] == j.keys[base];
-  if (lane == 1 && base + cnt < j.n) edge = j.keys[base + cnt] == j.keys[base + cnt - 1];
-  const bool first_before = __shfl_sync(0xffffffffu, edge, 0) != 0;
-  const bool last_after = __shfl_sync(0xffffffffu, edge, 1) != 0;
-  // Segment structure of the chunk as bit masks over rows.
-  const uint32_t key_prev = __shfl_up_sync(0xffffffffu, key_l, 1);
-  const bool head_l = lane < cnt && (lane == 0 ? !first_before : key_l != key_prev);
-  const uint32_t H = __ballot_sync(0xffffffffu, head_l);                 // segment starts
-  const bool end_l = lane < cnt && (lane == cnt - 1 ? !last_after : ((H >> (lane + 1)) & 1));
-  const uint32_t E = __ballot_sync(0xffffffffu, end_l);                  // segment ends
-  const bool whole_l = end_l && (H & ((2u << lane) - 1u)) != 0 && key_l < j.invalid_key;
-  const uint32_t WE = __ballot_sync(0xffffffffu, whole_l);               // ends of whole segments
-  const int n4 = j.dim >> 2;
-  const int c4 = slice * 32 + lane;
-  const bool col_ok = c4 < n4;
-  float4 x[kChunk], t[kChunk];
-#pragma unroll
-  for (int r = 0; r < kChunk; ++r) {  // every row of the chunk in flight at once
-    const uint32_t pr = __shfl_sync(0xffffffffu, perm_l, r);
-    const uint32_t kr = __shfl_sync(0xffffffffu, key_l, r);
-    x[r] = (r < cnt && col_ok) ? __ldg((const float4*)(j.rows + row_off(j, pr)) + c4)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-    t[r] = (!write_mode && ((WE >> r) & 1) && col_ok)
-               ? *((const float4*)(j.table + (int64_t)kr * j.dim) + c4)
-               : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  D4 acc = D4{0.0, 0.0, 0.0, 0.0};
-  double acc2 = 0.0;
-  int r_start = 0;
-#pragma unroll
-  for (int r = 0; r < kChunk; ++r) {
-    if (r >= cnt) break;
-    const float r2 = __shfl_sync(0xffffffffu, r2_l, r);
-    if (r > 0 && ((H >> r) & 1)) {
-      acc = D4{0.0, 0.0, 0.0, 0.0};
-      acc2 = 0.0;
-      r_start = r;
-    }
-    add4(acc, x[r]);
-    acc2 += r2;
-    if (!(((E >> r) & 1) || r == cnt - 1)) continue;
-    // ---- the piece [r_start, r] is complete
-    const uint32_t sg = __shfl_sync(0xffffffffu, seg_l, r);
-    const uint32_t kr = __shfl_sync(0xffffffffu, key_l, r);
-    if (kr >= j.invalid_key) continue;
-    const bool starts_before = r_start == 0 && first_before;
-    const bool ends_after = r == cnt - 1 && last_after;
-    if (!starts_before && !ends_after) {  // whole segment: apply / write now
-      if (write_mode) {
-        const OutPos op = seg_out_pos(j, sg, kr);
-        if (op.row != nullptr) {
-          if (col_ok) reinterpret_cast<float4*>(op.row)[c4] = to_f4(acc);
-          if (lane == 0 && slice == 0) {
-            if (j.out_local) j.out_local[op.local] = (int64_t)(kr % (uint32_t)j.nloc);
-            if (op.r2) *op.r2 = (float)acc2;
-          }
-        }
-      } else {
-        if (col_ok)
-          *((float4*)(j.table + (int64_t)kr * j.dim) + c4) = opt_step4<OPT>(j, t[r], acc, kr, c4);
-        if (j.table2 && lane == 0 && slice == 0) opt_step2<OPT>(j, kr, acc2);
-      }
-    } else {
-      const int64_t slot = starts_before ? 2 * chunk : 2 * chunk + 1;
-      if (col_ok) reinterpret_cast<D4*>(j.part + slot * j.dim)[c4] = acc;
-      if (lane == 0 && slice == 0) {
-        if (j.rows2) j.part2[slot] = acc2;
-        if (!starts_before) j.cross_list[atomicAdd(j.cross_count, 1u)] = sg;  // its first piece
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    const int lane = tid;
+    uint32_t key_l = 0, seg_l = 0;
+    for (int r = lane; r < kChunk; r += 32) {
+      if (r < cnt) {
+        const uint32_t pr = j.perm[base + r];
+        s_perm[r] = pr;
+        key_l = j.keys[base + r];
+        seg_l = j.seg_of[base + r];
+        s_key[r] = key_l;
+        s_seg[r] = seg_l;
+        s_r2[r] = j.rows2 ? j.rows2[row2_off(j, pr)] : 0.f;
       }
     }
-  }
-  {  // which segments own this chunk's two partial slots
+    // (kChunk == 32: lane r holds row r's key)
+    uint32_t edge = 0;
+    if (lane == 0 && base > 0) edge = j.keys[base - 1] == j.keys[base];
+    if (lane == 1 && base + cnt < j.n) edge = j.keys[base + cnt] == j.keys[base + cnt - 1];
+    const bool first_before = __shfl_sync(0xffffffffu, edge, 0) != 0;
+    const bool last_after = __shfl_sync(0xffffffffu, edge, 1) != 0;
+    const uint32_t key_prev = __shfl_up_sync(0xffffffffu, key_l, 1);
+    const bool head_l = lane < cnt && (lane == 0 ? !first_before : key_l != key_prev);
+    const uint32_t H = __ballot_sync(0xffffffffu, head_l);
+    const bool end_l = lane < cnt && (lane == cnt - 1 ? !last_after : ((H >> (lane + 1)) & 1));
+    const uint32_t E = __ballot_sync(0xffffffffu, end_l);
+    const bool whole_l = end_l && (H & ((2u << lane) - 1u)) != 0 && key_l < j.invalid_key;
+    const uint32_t WE = __ballot_sync(0xffffffffu, whole_l);
+    if (lane == 0) {
+      s_mask[0] = H;
+      s_mask[1] = E;
+      s_mask[2] = WE;
+      s_edge[0] = first_before;
+      s_edge[1] = last_after;
+    }
+    // which segments own this window's two partial slots
     const uint32_t s_first = __shfl_sync(0xffffffffu, seg_l, 0);
     const uint32_t k_first = __shfl_sync(0xffffffffu, key_l, 0);
     const uint32_t s_last = __shfl_sync(0xffffffffu, seg_l, cnt - 1);
     const uint32_t k_last = __shfl_sync(0xffffffffu, key_l, cnt - 1);
-    if (lane == 0 && slice == 0) {
+    if (lane == 0) {
       const int head = (first_before && k_first < j.invalid_key) ? (int)s_first : -1;
       const int tail = (last_after && k_last < j.invalid_key && (int)s_last != head)
                            ? (int)s_last : -1;
       j.chunk_info[chunk] = make_int2(head, tail);
+    }
+  }
+  __syncthreads();
+  const uint32_t H = s_mask[0], E = s_mask[1], WE = s_mask[2];
+  const bool first_before = s_edge[0] != 0, last_after = s_edge[1] != 0;
+  const bool write_mode = j.table == nullptr;
+  const int n4 = j.dim >> 2;
+  for (int c4 = tid; c4 < n4; c4 += blockDim.x) {
+    const bool col0 = c4 == 0;
+    D4 acc = D4{0.0, 0.0, 0.0, 0.0};
+    double acc2 = 0.0;
+    int r_start = 0;
+    for (int b0 = 0; b0 < cnt; b0 += kWinBatch) {
+      float4 x[kWinBatch], t[kWinBatch];
+#pragma unroll
+      for (int q = 0; q < kWinBatch; ++q) {  // the batch's rows (and table rows) in flight
+        const int r = b0 + q;
+        x[q] = r < cnt ? __ldg((const float4*)(j.rows + row_off(j, s_perm[r])) + c4)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        t[q] = (!write_mode && r < cnt && ((WE >> r) & 1))
+                   ? *((const float4*)(j.table + (int64_t)s_key[r] * j.dim) + c4)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < kWinBatch; ++q) {
+        const int r = b0 + q;
+        if (r >= cnt) break;
+        if (r > 0 && ((H >> r) & 1)) {
+          acc = D4{0.0, 0.0, 0.0, 0.0};
+          acc2 = 0.0;
+          r_start = r;
+        }
+        add4(acc, x[q]);
+        acc2 += s_r2[r];
+        if (!(((E >> r) & 1) || r == cnt - 1)) continue;
+        // ---- the piece [r_start, r] is complete
+        const uint32_t kr = s_key[r];
+        if (kr >= j.invalid_key) continue;
+        const uint32_t sg = s_seg[r];
+        const bool starts_before = r_start == 0 && first_before;
+        const bool ends_after = r == cnt - 1 && last_after;
+        if (!starts_before && !ends_after) {  // whole segment: apply / write now
+          if (write_mode) {
+            const OutPos op = seg_out_pos(j, sg, kr);
+            if (op.row != nullptr) {
+              reinterpret_cast<float4*>(op.row)[c4] = to_f4(acc);
+              if (col0) {
+                if (j.out_local) j.out_local[op.local] = (int64_t)(kr % (uint32_t)j.nloc);
+                if (op.r2) *op.r2 = (float)acc2;
+              }
+            }
+          } else {
+            *((float4*)(j.table + (int64_t)kr * j.dim) + c4) = opt_step4<OPT>(j, t[q], acc, kr, c4);
+            if (j.table2 && col0) opt_step2<OPT>(j, kr, acc2);
+          }
+        } else {
+          const int64_t slot = starts_before ? 2 * chunk : 2 * chunk + 1;
+          reinterpret_cast<D4*>(j.part + slot * j.dim)[c4] = acc;
+          if (col0) {
+            if (j.rows2) j.part2[slot] = acc2;
+            if (!starts_before) j.cross_list[atomicAdd(j.cross_count, 1u)] = sg;  // first piece
+          }
+        }
+      }
     }
   }
 }
@@ -1031,14 +1052,14 @@ static size_t seg_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws,
   return c.used + 256;
 }
 
-// Single-CTA sort + segmentation for n <= kSmallMax (both lookups of the X workload): keys are
+// Single-CTA sort + segmentation for n <= kSmallMax (both plans of the X workload): keys are
 // built, radix-sorted (8-bit LSD passes, stable) and segmented entirely in shared memory by
 // one 1024-thread CTA -- one launch instead of nine.  Warp w owns the contiguous input range
 // [w * per, (w + 1) * per); its digit counts are private (no per-round CTA barriers), and one
 // CTA-wide exclusive scan over the (digit, warp) counters in digit-major order per pass makes
 // the scatter stable (equal digits keep warp order, and lane order inside a warp).
 constexpr int kSmallThreads = 1024;
-constexpr int kSmallMax = 4096;  // above this the multi-CTA passes are faster
+constexpr int kSmallMax = 16384;  // one CTA, keys + values + counters in 225 KB of smem
 constexpr int kCntWords = 32 * 257;
 
 __device__ __forceinline__ uint32_t cta1024_exclusive_scan(uint32_t v, uint32_t* wsum,
@@ -1245,13 +1266,12 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
                             : (j.out_tab != nullptr || ((uintptr_t)j.out_rows & 15) == 0));
   if (vec) {
     TFS_CUDA_TRY(cudaMemsetAsync(j.cross_count, 0, sizeof(uint32_t), st));
-    const int nslices = (int)cdiv(j.dim >> 2, 32);
-    const int vgrid = (int)std::max<int64_t>(1, cdiv(nchunks * nslices, 8));
-    auto chunk_k = j.opt == 1 ? seg_chunk_vec4_kernel<1>
-                              : (j.opt == 2 ? seg_chunk_vec4_kernel<2> : seg_chunk_vec4_kernel<0>);
-    chunk_k<<<vgrid, 256, 0, st>>>(j, nslices);
-    launched();
     const int64_t n4 = j.dim >> 2;
+    const int wthreads = (int)std::min<int64_t>(128, cdiv(n4, 32) * 32);
+    auto win_k = j.opt == 1 ? seg_window_vec4_kernel<1>
+                            : (j.opt == 2 ? seg_window_vec4_kernel<2> : seg_window_vec4_kernel<0>);
+    win_k<<<(unsigned)nchunks, wthreads, 0, st>>>(j);
+    launched();
     const bool shortn = nchunks <= kBlkShortMaxChunks;
     const int kb = shortn ? kBlkShort : kBlkLong;
     const int64_t awork = cdiv(nchunks, kb) * n4;

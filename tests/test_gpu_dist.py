@@ -110,10 +110,10 @@ def _worker_body(rank, world, port, name, dtype, route, q, full):
                 # the next step starts from the GPUs' own state (identical inputs, c.5)
                 parts = [None] * R
                 dist.all_gather_object(parts, g)
-                full = np.empty_like(T0)
+                table = np.empty_like(T0)
                 for r in range(R):
-                    full[r::R] = parts[r]
-                nxt.append(full)
+                    table[r::R] = parts[r]
+                nxt.append(table)
             E, W, b = nxt
         q.put((rank, res))
         st.close()
