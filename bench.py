@@ -432,7 +432,7 @@ def main():
     barrier()
     for i in range(n_ph):
         flush.zero_()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(14)]
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(17)]
         st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], timing_events=evs)
         evs_all.append(evs)
     barrier()
@@ -443,8 +443,9 @@ def main():
 
     phases = {}
     if R == 1:
-        for name, (i0, i1) in (("sample", (0, 1)), ("gather", (1, 2)), ("sampled_softmax", (2, 3)),
-                               ("scatter_plan", (3, 4)), ("scatter_sgd", (4, 5))):
+        for name, (i0, i1) in (("sample", (0, 1)), ("gather_E", (1, 2)), ("gather_W", (2, 3)),
+                               ("sampled_softmax", (3, 4)), ("plan_E", (4, 5)),
+                               ("plan_W", (5, 6)), ("apply_E", (6, 7)), ("apply_W", (7, 8))):
             phases[name] = avg(i0, i1)
     peaks, peak_src = load_peaks()
     # Sub-millisecond kernels timed inside eager steps at full clocks: the BURST peak.
@@ -462,8 +463,8 @@ def main():
     if S == 0 and R > 1:
         # per shard: M = R*B tokens x its V/R classes; STATS 2 M n d, GRAD + STORE 6 M n d flops
         M_, n_ = R * B, -(-w.vocab // R)
-        kern = {"partial_stats": (avg(6, 7), 2.0 * M_ * n_ * d),
-                "backward_from_lse": (avg(8, 9), 6.0 * M_ * n_ * d)}
+        kern = {"partial_stats": (avg(9, 10), 2.0 * M_ * n_ * d),
+                "backward_from_lse": (avg(11, 12), 6.0 * M_ * n_ * d)}
         per = {k: {"ms": v, "tflops": f / (v / 1e3) / 1e12, "frac": f / (v / 1e3) / 1e12 / peak}
                for k, (v, f) in kern.items()}
         top = per["backward_from_lse"]
@@ -477,8 +478,8 @@ def main():
                     "ms": top["ms"], "kernels": per}
         call_ms = None
     else:
-        kern_ms = {"gemm_stats": avg(7, 8), "gemm_grad": avg(9, 10), "gemm_store": avg(11, 12)}
-        call_ms = avg(6, 13)
+        kern_ms = {"gemm_stats": avg(10, 11), "gemm_grad": avg(12, 13), "gemm_store": avg(14, 15)}
+        call_ms = avg(9, 16)
         flops = {"gemm_stats": 2.0 * B * S_eff * d, "gemm_grad": 2.0 * B * S_eff * d,
                  "gemm_store": 4.0 * B * S_eff * d}
         per = {k: {"ms": v, "tflops": flops[k] / (v / 1e3) / 1e12,
@@ -503,11 +504,13 @@ def main():
             "ms": call_ms}
     hbm = None
     if R == 1 and S > 0:
-        # algorithmic bytes.  Gather: ids read, the DISTINCT rows read (repeats
-        # are L2 hits), every requested row written (bf16 operand rows in bf16 mode; the bias
-        # in fp32).  ScatterAdd-SGD apply: every gradient row read once (fp32), each distinct
-        # row of the table read and written (W with its bias).  Plan: ids read, keys + values
-        # sorted (3 LSD passes of 8-byte pairs written and read) -- reported as latency.
+        # Algorithmic bytes per call, each call timed alone by CUDA
+        # events on its stream in the serial instrumented steps.
+        #  Gather: the ids, the DISTINCT rows read once (repeats are L2 hits), every requested
+        #    row written (bf16 operand rows in bf16 mode; the bias in fp32).
+        #  ScatterAdd-SGD apply: every gradient row read once (fp32), each distinct row of the
+        #    table read and written (W with its bias).
+        #  Plan: ids read, sorted keys / permutation / segments written -- latency-bound (us).
         qw = st.tensor("qw")
         x_last = st.tensor("x")
         u_e = int(torch.unique(x_last).numel())
@@ -515,19 +518,37 @@ def main():
         n_e, n_w = B, B + S
         row_in = 4 * d
         row_out = (2 if args.dtype == "bf16" else 4) * d
-        g_bytes = (8 * (n_e + n_w) + (u_e + u_w) * row_in + (n_e + n_w) * row_out
-                   + u_w * 4 + n_w * 4)
-        s_bytes = (n_e + n_w) * 4 * d + n_w * 4 + 2 * (u_e + u_w) * 4 * d + 2 * u_w * 4
-        t_g = phases["gather"] / 1e3
-        t_s = phases["scatter_sgd"] / 1e3
+        calls = {
+            "gather_E": 8 * n_e + u_e * row_in + n_e * row_out,
+            "gather_W": 8 * n_w + u_w * (row_in + 4) + n_w * (row_out + 4),
+            "apply_E": n_e * row_in + 2 * u_e * row_in,
+            "apply_W": n_w * (row_in + 4) + 2 * u_w * (row_in + 4),
+        }
+        per = {}
+        for k, nbytes in calls.items():
+            t_ = phases[k] / 1e3
+            per[k] = {"bytes": nbytes, "us": phases[k] * 1e3, "GBps": nbytes / t_ / 1e9,
+                      "frac": nbytes / t_ / 1e9 / hbm_peak}
+        g_bytes = calls["gather_E"] + calls["gather_W"]
+        s_bytes = calls["apply_E"] + calls["apply_W"]
+        t_g = (phases["gather_E"] + phases["gather_W"]) / 1e3
+        t_s = (phases["apply_E"] + phases["apply_W"]) / 1e3
         hbm = {"gather_GBps": g_bytes / t_g / 1e9, "gather_frac": g_bytes / t_g / 1e9 / hbm_peak,
-               "gather_bytes": g_bytes,
                "scatter_GBps": s_bytes / t_s / 1e9,
-               "scatter_frac": s_bytes / t_s / 1e9 / hbm_peak, "scatter_bytes": s_bytes,
-               "scatter_plan_us": phases["scatter_plan"] * 1e3,
-               "distinct_rows": [u_e, u_w], "peak": hbm_peak, "unit": "GB/s",
-               "note": "phase times of serial instrumented eager steps (CUDA events); the "
-                       "gather / apply phases each hold 2 launches (E, W) -- launch gaps count"}
+               "scatter_frac": s_bytes / t_s / 1e9 / hbm_peak,
+               "scatter_plan_us": {"E": phases["plan_E"] * 1e3, "W": phases["plan_W"] * 1e3},
+               "calls": per, "distinct_rows": [u_e, u_w], "peak": hbm_peak, "unit": "GB/s",
+               "note": "per-call CUDA-event times of serial instrumented eager steps (L2 "
+                       "flushed before each step); bytes = algorithmic (DESIGN.md §6)"}
+        roofline["scatter"] = {"kernel": "ScatterAdd-SGD apply (seg_window + crossing "
+                                         "segments), E and W calls",
+                               "bound": "hbm", "achieved": hbm["scatter_GBps"],
+                               "peak": hbm_peak, "unit": "GB/s", "frac": hbm["scatter_frac"],
+                               "traffic": None, "algorithmic": "per distinct row: read its "
+                               "gradient rows + read and write the table row"}
+        roofline["gather"] = {"kernel": "Gather (gather_vec4, bf16 out), E and W calls",
+                              "bound": "hbm", "achieved": hbm["gather_GBps"], "peak": hbm_peak,
+                              "unit": "GB/s", "frac": hbm["gather_frac"], "traffic": None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

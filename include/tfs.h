@@ -550,12 +550,13 @@ int32_t tfs_step_set_counter(tfs_stepper* st, int64_t value);
  * step's input buffers on `stream` inside the call, and each local rank's loss_sum is copied
  * back to io->loss_host[nlocal] (host) on `stream` -- the caller synchronises before reading.
  * The step counter (sampler; TFS_BUF_STEP) advances by one on the device.
- * io->timing_events (one local rank, eager only; NULL normally): 14 cudaEvent_t.  R = 1: the
- * step runs its phases SERIALLY on one stream and records 0 start, 1 sampled, 2 gathered,
- * 3 softmax done, 4 plans built, 5 tables updated; 6..13 the softmax call's 8 events
- * (tfs_ssm_args.timing_events).  R > 1 (phases overlapped as usual): 6..13 as above for the
- * sampled softmax; the sharded full softmax records 6 / 7 around its partial-stats call and
- * 8 / 9 around its backward call.  Entries may be NULL. */
+ * io->timing_events (one local rank, eager only; NULL normally): 17 cudaEvent_t.  R = 1: the
+ * step runs its phases SERIALLY on one stream and records 0 start, 1 sample committed (and the
+ * next step's drawn), 2 E rows gathered, 3 W rows + b gathered, 4 softmax done, 5 E plan built,
+ * 6 W plan built, 7 E updated, 8 W + b updated; 9..16 the softmax call's 8 events
+ * (tfs_ssm_args.timing_events).  R > 1 (phases overlapped as usual): 9..16 as above for the
+ * sampled softmax; the sharded full softmax records 9 / 10 around its partial-stats call and
+ * 11 / 12 around its backward call.  Entries may be NULL. */
 typedef struct {
   const int64_t* x;
   const int64_t* y;

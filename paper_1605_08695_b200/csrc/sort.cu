@@ -643,6 +643,9 @@ __global__ void __launch_bounds__(128) seg_window_vec4_kernel(SegJob j) {
     }
   }
   __syncthreads();
+  // Sorted keys put skipped entries (padding slots, bad ids: key >= invalid_key) last, so a
+  // window whose first key is invalid has nothing to do, and no invalid row is ever loaded.
+  if (s_key[0] >= j.invalid_key) return;
   const uint32_t H = s_mask[0], E = s_mask[1], WE = s_mask[2];
   const bool first_before = s_edge[0] != 0, last_after = s_edge[1] != 0;
   const bool write_mode = j.table == nullptr;
@@ -657,8 +660,9 @@ __global__ void __launch_bounds__(128) seg_window_vec4_kernel(SegJob j) {
 #pragma unroll
       for (int q = 0; q < kWinBatch; ++q) {  // the batch's rows (and table rows) in flight
         const int r = b0 + q;
-        x[q] = r < cnt ? __ldg((const float4*)(j.rows + row_off(j, s_perm[r])) + c4)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[q] = (r < cnt && s_key[r] < j.invalid_key)
+                   ? __ldg((const float4*)(j.rows + row_off(j, s_perm[r])) + c4)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
         t[q] = (!write_mode && r < cnt && ((WE >> r) & 1))
                    ? *((const float4*)(j.table + (int64_t)s_key[r] * j.dim) + c4)
                    : make_float4(0.f, 0.f, 0.f, 0.f);

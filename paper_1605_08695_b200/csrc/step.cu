@@ -587,18 +587,21 @@ void local_step_serial(tfs_stepper* st, Rank& k, cudaStream_t mn, void* const* e
   STEP_CALL(st, presample(st, k, mn, 1)); // ... and the next step's draw, inline here
   mark(1);
   STEP_CALL(st, tfs_gather(k.E, m.V, m.d, TFS_F32, k.x, m.B, k.h, rdt, k.err, mn));
+  mark(2);
   STEP_CALL(st, tfs_gather2(k.W, m.V, m.d, k.b, k.qw, m.B + m.Seff, k.w_rows, rdt, k.b_rows,
                             k.err, mn));
-  mark(2);
-  tfs_ssm_args a = ssm_args(st, k, ev ? ev + 6 : nullptr);
-  STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
   mark(3);
-  STEP_CALL(st, tfs_scatter_plan(k.x, m.B, m.V, k.plan_e, k.plan_e_b, k.err, mn));
-  STEP_CALL(st, tfs_scatter_plan(k.qw, m.B + m.Seff, m.V, k.plan_w, k.plan_w_b, k.err, mn));
+  tfs_ssm_args a = ssm_args(st, k, ev ? ev + 9 : nullptr);
+  STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
   mark(4);
-  STEP_CALL(st, apply_local(st, k, true, mn));
-  STEP_CALL(st, apply_local(st, k, false, mn));
+  STEP_CALL(st, tfs_scatter_plan(k.x, m.B, m.V, k.plan_e, k.plan_e_b, k.err, mn));
   mark(5);
+  STEP_CALL(st, tfs_scatter_plan(k.qw, m.B + m.Seff, m.V, k.plan_w, k.plan_w_b, k.err, mn));
+  mark(6);
+  STEP_CALL(st, apply_local(st, k, true, mn));
+  mark(7);
+  STEP_CALL(st, apply_local(st, k, false, mn));
+  mark(8);
 }
 
 void mark(tfs_stepper* st, int i, cudaStream_t s) {
@@ -658,7 +661,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
                                       (const float* const*)k.tab_b, k.qw, m.B + m.S, m.V, R,
                                       k.w_rows, rdt, k.b_rows, k.err, mn));
       STEP_CALL(st, waitev(mn, k.ev[kH]));
-      tfs_ssm_args a = ssm_args(st, k, st->timing ? st->timing + 6 : nullptr);
+      tfs_ssm_args a = ssm_args(st, k, st->timing ? st->timing + 9 : nullptr);
       STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
       STEP_CALL(st, rec(k.ev[kSsm], mn));
       STEP_CALL(st, waitev(sd, k.ev[kSsm]));
@@ -731,18 +734,18 @@ void full_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       STEP_CALL(st, tfs_gather_peers((const float* const*)k.tab_y, m.B, 2, k.ag_ids, m.M, m.M, R,
                                      k.y_all, TFS_F32, k.err, mn));
       tfs_ssm_args a = slice_args(st, k, false);
-      mark(st, 6, mn);
+      mark(st, 9, mn);
       STEP_CALL(st, tfs_ssm_partial_stats(&a, k.rowstats, k.ws_full, k.ws_full_b, mn));
-      mark(st, 7, mn);
+      mark(st, 10, mn);
       break;
     }
     case 3: {
       STEP_CALL(st, tfs_lse_combine_peers((const float* const*)k.tab_rowstats, R, m.M, k.lse_all,
                                           mn));
       tfs_ssm_args a = slice_args(st, k, true);
-      mark(st, 8, mn);
+      mark(st, 11, mn);
       STEP_CALL(st, tfs_ssm_backward_from_lse(&a, k.z_label, k.ws_full, k.ws_full_b, mn));
-      mark(st, 9, mn);
+      mark(st, 12, mn);
       STEP_CALL(st, tfs_label_loss_sum(k.lse_all, k.z_label, k.y_all, m.M, R, rank,
                                        1.0f / (float)(R * m.B), k.loss_part, mn));
       STEP_CALL(st, rec(k.ev[kSsm], mn));
