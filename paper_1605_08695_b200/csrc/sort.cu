@@ -26,10 +26,13 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = 4;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 1024 items per CTA
 constexpr int kMaxBuckets = 256;
-#ifndef TFS_SEG_CHUNK
-#define TFS_SEG_CHUNK 32
+// Sorted rows per window of the segmented sums: 32 for long inputs, 8 for short ones (more
+// windows in flight); scratch is sized for the smallest.
+constexpr int kChunk = 32;
+constexpr int kChunkMin = 8;
+#ifndef TFS_SEG_SHORT_N
+#define TFS_SEG_SHORT_N 40000  // below this many rows: 8-row windows
 #endif
-constexpr int kChunk = TFS_SEG_CHUNK;  // sorted rows per warp in the segmented sums
 
 
 struct DigitSrc {
@@ -464,6 +467,7 @@ struct SegJob {
   // rows + o * row_stride + s * dim (rows2 + o * row2_stride + s)
   int64_t row_cap, row_stride, row2_stride;
   int64_t nloc;
+  int32_t chunk;  // rows per window (kChunk or kChunkMin)
   // apply mode: sums of the segments that lie inside one chunk, [U x dim] (+ [U])
   float* sums;
   float* sums2;
@@ -585,7 +589,7 @@ __device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_afte
 // piece of the segment that started before window c; 2c + 1: the piece of the segment that
 // starts in c and continues after it) and the segment to cross_list.
 constexpr int kWinBatch = 8;
-static_assert(kChunk == 32, "the window prologue maps row r of a window to lane r");
+static_assert(kChunk <= 32, "the window prologue maps row r of a window to lane r");
 template <int OPT>
 __global__ void __launch_bounds__(128) seg_window_vec4_kernel(SegJob j) {
   __shared__ uint32_t s_perm[kChunk], s_key[kChunk], s_seg[kChunk];
@@ -593,13 +597,13 @@ __global__ void __launch_bounds__(128) seg_window_vec4_kernel(SegJob j) {
   __shared__ uint32_t s_mask[3];
   __shared__ int s_edge[2];
   const int64_t chunk = blockIdx.x;
-  const int64_t base = chunk * kChunk;
-  const int cnt = (int)min((int64_t)kChunk, j.n - base);
+  const int64_t base = chunk * j.chunk;
+  const int cnt = (int)min((int64_t)j.chunk, j.n - base);
   const int tid = threadIdx.x;
   if (tid < 32) {
     const int lane = tid;
     uint32_t key_l = 0, seg_l = 0;
-    for (int r = lane; r < kChunk; r += 32) {
+    for (int r = lane; r < j.chunk; r += 32) {
       if (r < cnt) {
         const uint32_t pr = j.perm[base + r];
         s_perm[r] = pr;
@@ -814,7 +818,7 @@ __global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
     const int64_t q = e / n4;
     const int c4 = (int)(e - q * n4);
     const uint32_t s = j.cross_list[q];
-    const int64_t c0 = j.seg_start[s] / kChunk, c1 = (j.seg_start[s + 1] - 1) / kChunk;
+    const int64_t c0 = j.seg_start[s] / j.chunk, c1 = (j.seg_start[s + 1] - 1) / j.chunk;
     const int64_t b0 = c0 / kBlk, b1 = c1 / kBlk;
     const bool col0 = c4 == 0 && j.rows2 != nullptr;
     D4 acc = reinterpret_cast<const D4*>(j.part + (2 * c0 + 1) * j.dim)[c4];
@@ -833,9 +837,9 @@ __global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
 __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
   const int lane = threadIdx.x & 31;
   const int64_t chunk = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int64_t base = chunk * kChunk;
+  const int64_t base = chunk * j.chunk;
   if (base >= j.n) return;
-  const int cnt = (int)min((int64_t)kChunk, j.n - base);
+  const int cnt = (int)min((int64_t)j.chunk, j.n - base);
   uint32_t perm_l = 0, seg_l = 0, key_l = 0;
   float r2_l = 0.f;
   if (lane < cnt) {
@@ -912,7 +916,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
     const OutPos op = write_mode ? seg_out_pos(j, u, key) : OutPos{j.table, nullptr, u};
     if (op.row == nullptr) continue;
     if (write_mode && c == 0 && j.out_local) j.out_local[op.local] = (int64_t)(key % (uint32_t)j.nloc);
-    const int64_t c0 = a / kChunk, c1 = (b - 1) / kChunk;
+    const int64_t c0 = a / j.chunk, c1 = (b - 1) / j.chunk;
     const bool cross = c0 != c1;
     if (write_mode && !cross) continue;  // the chunk kernel already wrote it
     if (VEC) {
@@ -1017,7 +1021,7 @@ static void carve_plan(Carver& c, int64_t n, SegScratch& x) {
 }
 
 static void carve_apply(Carver& c, int64_t n, int32_t dim, SegScratch& x) {
-  const int64_t nchunks = cdiv(n, kChunk);
+  const int64_t nchunks = cdiv(n, kChunkMin);
   x.part = c.take<double>((size_t)2 * nchunks * dim);
   x.part2 = c.take<double>((size_t)2 * nchunks);
   x.sums = c.take<float>((size_t)n * dim);
@@ -1063,7 +1067,7 @@ static size_t seg_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* ws,
 // CTA-wide exclusive scan over the (digit, warp) counters in digit-major order per pass makes
 // the scatter stable (equal digits keep warp order, and lane order inside a warp).
 constexpr int kSmallThreads = 1024;
-constexpr int kSmallMax = 16384;  // one CTA, keys + values + counters in 225 KB of smem
+constexpr int kSmallMax = 4096;  // above this the multi-CTA passes are faster (measured)
 constexpr int kCntWords = 32 * 257;
 
 __device__ __forceinline__ uint32_t cta1024_exclusive_scan(uint32_t v, uint32_t* wsum,
@@ -1261,7 +1265,8 @@ static void bind(SegJob& j, const SegScratch& s, int64_t n) {
 }
 
 static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
-  const int64_t nchunks = cdiv(n, kChunk);
+  j.chunk = n >= TFS_SEG_SHORT_N ? kChunk : kChunkMin;
+  const int64_t nchunks = cdiv(n, j.chunk);
   const int grid = (int)std::max<int64_t>(1, cdiv(nchunks, 8));
   // (inbox regions of out_tab are 16-byte aligned by construction: aligned bases, out_off % 4 == 0)
   const bool vec = (j.dim & 3) == 0 && ((uintptr_t)j.rows & 15) == 0 &&

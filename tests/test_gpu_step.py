@@ -393,6 +393,22 @@ def test_sim_sharded_full_softmax(R, vocab, tokens):
     _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, 1)
 
 
+@pytest.mark.parametrize("R", [2, 3])
+def test_sim_sharded_full_softmax_graph_replay(R):
+    """The sharded full softmax captured once into a CUDA graph and replayed for three steps,
+    each step against the oracle from the GPU's own state."""
+    w = workloads.Workload("Fs", 1000, 64, 32, 0, R)
+    E, W, b = workloads.tables(1000, 64)
+    cfg = _cfg(w, R, TFS_BF16)
+    st = make_step(cfg, E, W, b)
+    st.set_step(0)
+    st.capture()
+    for k in range(3):
+        xs, ys = _batches(w, R, step=k)
+        E, W, b = gpu_tables(st, 1000)
+        _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, k)
+
+
 @pytest.mark.parametrize("R", [2, 4])
 def test_sim_sharded_X_integer_paths(R):
     """BASELINE's X shape (V = 800k, B = 2560 and S = 8192 per replica) with R shards: the
