@@ -65,7 +65,8 @@ def _worker_body(rank, world, port, name, dtype, route, q, full):
         V, R = w.vocab, world
         E, W, b = workloads.tables(V, w.dim)
         B = w.tokens_per_replica(R)
-        cfg = gstep.StepConfig(vocab=V, dim=w.dim, tokens=B, num_sampled=w.num_sampled,
+        S = 0 if full else w.num_sampled      # full: the vocabulary-sharded full softmax
+        cfg = gstep.StepConfig(vocab=V, dim=w.dim, tokens=B, num_sampled=S,
                                num_shards=R, lr=1.0, seed=workloads.SAMPLER_SEED,
                                operand_dtype=dtype)
         comm = gstep.Comm.distributed(cfg, timeout_ms=60000)
@@ -77,7 +78,7 @@ def _worker_body(rank, world, port, name, dtype, route, q, full):
         res = {"sampled": True, "loss": 0.0}
         for k in range(3):
             xs, ys = zip(*[workloads.batch(w, R, r, step=k) for r in range(R)])
-            ocfg = ostep.StepConfig(vocab=V, dim=w.dim, num_sampled=w.num_sampled, num_shards=R,
+            ocfg = ostep.StepConfig(vocab=V, dim=w.dim, num_sampled=S or V, num_shards=R,
                                     lr=1.0, seed=workloads.SAMPLER_SEED, step=k,
                                     bf16=(dtype == 1), full_softmax=full, label_in=full,
                                     abs_bounds=True)
