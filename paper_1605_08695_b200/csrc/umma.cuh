@@ -308,37 +308,6 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA / ALU pipes (no MUFU): x = n + f with n = round(x) (magic-number rounding),
-// f in [-1/2, 1/2]; 2^f by a degree-5 polynomial (max rel. error 8e-8, like ex2.approx's
-// 2^-22.5), n added to the exponent field.  x < -125 (including -inf) gives 0, as the ftz
-// MUFU does.  The softmax epilogues issue one exponential per logit, which saturates the MUFU
-// (XU) pipe ahead of the tensor pipe (ncu: xu ~100-120 % of peak in STATS / GRAD, round 2);
-// every kPolyEvery-th exponential takes this path instead.
-#ifndef TFS_POLY_EXP_EVERY
-#define TFS_POLY_EXP_EVERY 2
-#endif
-constexpr int kPolyEvery = TFS_POLY_EXP_EVERY;  // 0: MUFU only
-__device__ __forceinline__ float poly_exp2(float x) {
-  const float xc = fmaxf(x, -125.f);
-  const float t = xc + 12582912.f;  // 1.5 * 2^23: round(xc) in the low mantissa bits
-  const float n = t - 12582912.f;
-  const float f = xc - n;
-  float p = fmaf(0.0013266970636323094f, f, 0.009675459936261177f);
-  p = fmaf(p, f, 0.05550742521882057f);
-  p = fmaf(p, f, 0.24022121727466583f);
-  p = fmaf(p, f, 0.6931469440460205f);
-  p = fmaf(p, f, 1.0000001192092896f);
-  const int e = (__float_as_int(t) - 0x4B400000) << 23;
-  const float r = __int_as_float(__float_as_int(p) + e);
-  return x < -125.f ? 0.f : r;
-}
-// i: the element's index in a fully unrolled loop (the choice folds at compile time)
-__device__ __forceinline__ float mixed_exp2(int i, float x) {
-  if (kPolyEvery > 0 && i % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1)
-    return poly_exp2(x);
-  return fast_exp2(x);
-}
-
 struct Unit {
   int pi, mt, nt, ks, kb0, kb1, nw;  // nw: MMA N of this tile (last n-tile may be narrower)
 };
@@ -609,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             const float nm = fmaxf(run_m, cm);
             float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int i = 0; i < 32; ++i) s4[i & 3] += mixed_exp2(i, v[i] - nm);
+            for (int i = 0; i < 32; ++i) s4[i & 3] += fast_exp2(v[i] - nm);
             run_s = run_s * fast_exp2(run_m - nm) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
             run_m = nm;
           }
@@ -618,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           if (LAB) {  // G = c (p - 1) at the label's column
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              v[i] = mixed_exp2(i, v[i] - goff) - (((labmask >> i) & 1u) ? ep.c : 0.f);
+              v[i] = fast_exp2(v[i] - goff) - (((labmask >> i) & 1u) ? ep.c : 0.f);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               uint32_t p[4];
@@ -633,8 +602,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               uint32_t p[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j)
-                p[j] = pack_bf16x2(mixed_exp2(8 * k + 2 * j, v[8 * k + 2 * j] - goff),
-                                   mixed_exp2(8 * k + 2 * j + 1, v[8 * k + 2 * j + 1] - goff));
+                p[j] = pack_bf16x2(fast_exp2(v[8 * k + 2 * j] - goff),
+                                   fast_exp2(v[8 * k + 2 * j + 1] - goff));
               x[k] = make_uint4(p[0], p[1], p[2], p[3]);
             }
           }
