@@ -9,9 +9,12 @@
  * CONVENTIONS (every entry point)
  *  - Buffers are DEVICE pointers owned by the caller (e.g. torch CUDA tensors), unless a
  *    parameter says "host".  The library never allocates device memory and never synchronises
- *    the stream, except tfs_sampler_init (a one-off setup call).  Scratch comes from a
- *    caller-provided workspace `ws` of at least the bytes the matching *_workspace_bytes()
- *    query returns; ws must be 256-byte aligned.
+ *    the stream, except tfs_sampler_init and the stepper / communicator setup calls.  Scratch
+ *    comes from a caller-provided workspace `ws` of at least the bytes the matching
+ *    *_workspace_bytes() query returns; ws must be 256-byte aligned.  Workspaces of the calls
+ *    that sum gradient rows per id (tfs_sort_reduce, tfs_scatter_add_sgd*, tfs_scatter_opt_*,
+ *    tfs_route_reduce*) hold arrival counters: zero-fill them once before the first call
+ *    (every call leaves them zero).
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
  *    stream-ordered and asynchronous.
  *  - The returned tfs_status reports ARGUMENT errors only, detected on the host before any

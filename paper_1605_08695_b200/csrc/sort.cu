@@ -482,6 +482,11 @@ struct SegJob {
   int2* chunk_info;
   uint32_t* cross_list;
   uint32_t* cross_count;
+  // Fused crossing reduction (vec path): arrival counters, zero between calls (the last
+  // arriver resets them): per window (the level-1 run of a segment inside a block of
+  // kRunWin windows is keyed by its first window) and per segment (level 2).
+  uint32_t* win_cnt;
+  uint32_t* seg_cnt;
 };
 
 struct D4 {
@@ -589,9 +594,87 @@ __device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_afte
 // piece of the segment that started before window c; 2c + 1: the piece of the segment that
 // starts in c and continues after it) and the segment to cross_list.
 constexpr int kWinBatch = 8;
-static_assert(kChunk <= 32, "the window prologue maps row r of a window to lane r");
+constexpr int kRunWin = 16;  // windows per level-1 block of a crossing segment
+
 template <int OPT>
-__global__ void __launch_bounds__(128) seg_window_vec4_kernel(SegJob j) {
+__device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int c4, const D4& acc,
+                                                bool col0, double acc2);
+
+// One CTA arrives with its piece of crossing segment s (window `chunk`; its partial is already
+// in slot 2 chunk (head piece) or 2 chunk + 1 (the segment's first piece)).  Level 1: the pieces
+// of s inside one block of kRunWin windows are summed, in window order, by the block's last
+// arriver into the slot of the block's first piece.  Level 2: the last block to finish sums the
+// block partials in block order and finishes the segment (table update or written sum).  Fixed
+// order at both levels (R-16); arrival order only decides WHO adds, never the order.
+template <int OPT>
+__device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_t chunk,
+                                          bool head_piece) {
+  __shared__ int s_last;
+  const int64_t c0 = j.seg_start[s] / j.chunk, c1 = (j.seg_start[s + 1] - 1) / j.chunk;
+  const int64_t b = chunk / kRunWin;
+  const int64_t w0 = max(c0, b * kRunWin), w1 = min(c1, b * kRunWin + kRunWin - 1);
+  auto slot_of = [&](int64_t w) { return w == c0 ? 2 * w + 1 : 2 * w; };
+  (void)head_piece;
+  __syncthreads();  // this CTA's partial (all columns) is written
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t need = (uint32_t)(w1 - w0 + 1);
+    const uint32_t old = atomicAdd(j.win_cnt + w0, 1u);
+    s_last = old + 1 == need;
+    if (s_last) {
+      j.win_cnt[w0] = 0;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  const int n4 = j.dim >> 2;
+  const int64_t first = slot_of(w0);
+  for (int c4 = threadIdx.x; c4 < n4; c4 += blockDim.x) {  // level 1, window order
+    D4 acc = D4{0.0, 0.0, 0.0, 0.0};
+    double acc2 = 0.0;
+    for (int64_t w = w0; w <= w1; ++w) {
+      const int64_t sl = slot_of(w);
+      const double2* pp = reinterpret_cast<const double2*>(j.part + sl * j.dim) + 2 * c4;
+      const double2 v0 = __ldcg(pp), v1 = __ldcg(pp + 1);  // L2: written by other CTAs
+      add4(acc, D4{v0.x, v0.y, v1.x, v1.y});
+      if (c4 == 0 && j.rows2) acc2 += __ldcg(j.part2 + sl);
+    }
+    reinterpret_cast<D4*>(j.part + first * j.dim)[c4] = acc;
+    if (c4 == 0 && j.rows2) j.part2[first] = acc2;
+  }
+  __syncthreads();
+  const int64_t b0 = c0 / kRunWin, b1 = c1 / kRunWin;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t old = atomicAdd(j.seg_cnt + s, 1u);
+    s_last = old + 1 == (uint32_t)(b1 - b0 + 1);
+    if (s_last) {
+      j.seg_cnt[s] = 0;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  for (int c4 = threadIdx.x; c4 < n4; c4 += blockDim.x) {  // level 2, block order
+    D4 acc = D4{0.0, 0.0, 0.0, 0.0};
+    double acc2 = 0.0;
+    for (int64_t bb = b0; bb <= b1; ++bb) {
+      const int64_t sl = bb == b0 ? 2 * c0 + 1 : 2 * bb * kRunWin;
+      const double2* pp = reinterpret_cast<const double2*>(j.part + sl * j.dim) + 2 * c4;
+      const double2 v0 = __ldcg(pp), v1 = __ldcg(pp + 1);  // L2: written by other CTAs
+      add4(acc, D4{v0.x, v0.y, v1.x, v1.y});
+      if (c4 == 0 && j.rows2) acc2 += __ldcg(j.part2 + sl);
+    }
+    seg_finish_vec4<OPT>(j, s, c4, acc, c4 == 0, acc2);
+  }
+}
+static_assert(kChunk <= 32, "the window prologue maps row r of a window to lane r");
+#ifndef TFS_WIN_MINB
+#define TFS_WIN_MINB 4  // CTAs per SM the register budget must allow (128 regs at 4)
+#endif
+template <int OPT>
+__global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJob j) {
   __shared__ uint32_t s_perm[kChunk], s_key[kChunk], s_seg[kChunk];
   __shared__ float s_r2[kChunk];
   __shared__ uint32_t s_mask[3];
@@ -706,14 +789,17 @@ __global__ void __launch_bounds__(128) seg_window_vec4_kernel(SegJob j) {
         } else {
           const int64_t slot = starts_before ? 2 * chunk : 2 * chunk + 1;
           reinterpret_cast<D4*>(j.part + slot * j.dim)[c4] = acc;
-          if (col0) {
-            if (j.rows2) j.part2[slot] = acc2;
-            if (!starts_before) j.cross_list[atomicAdd(j.cross_count, 1u)] = sg;  // first piece
-          }
+          if (col0 && j.rows2) j.part2[slot] = acc2;
         }
       }
     }
   }
+  // Pieces of segments crossing this window's edges (at most two: the one that started before
+  // it and the one that continues after it): arrive, and the last arriver of a level sums it.
+  const uint32_t kf = s_key[0], kl = s_key[cnt - 1];
+  if (first_before && kf < j.invalid_key) cross_arrive<OPT>(j, s_seg[0], chunk, true);
+  if (last_after && kl < j.invalid_key && !(first_before && s_seg[cnt - 1] == s_seg[0]))
+    cross_arrive<OPT>(j, s_seg[cnt - 1], chunk, false);
 }
 
 // A segment whose pieces are all summed: T[key] = fl32(T - lr * g) (apply) or written out.
@@ -1004,6 +1090,7 @@ struct SegScratch {
   float *sums, *sums2;
   uint32_t *cross_list, *cross_count;
   int2* chunk_info;
+  uint32_t *win_cnt, *seg_cnt;
 };
 
 static void carve_plan(Carver& c, int64_t n, SegScratch& x) {
@@ -1029,6 +1116,8 @@ static void carve_apply(Carver& c, int64_t n, int32_t dim, SegScratch& x) {
   x.cross_list = c.take<uint32_t>((size_t)nchunks + 1);
   x.cross_count = c.take<uint32_t>(1);
   x.chunk_info = c.take<int2>((size_t)nchunks);
+  x.win_cnt = c.take<uint32_t>((size_t)nchunks);
+  x.seg_cnt = c.take<uint32_t>((size_t)n);
 }
 
 static size_t plan_scratch_bytes(int64_t n, SegScratch* s, void* ws, size_t cap) {
@@ -1047,6 +1136,7 @@ static size_t apply_scratch_bytes(int64_t n, int32_t dim, SegScratch* s, void* w
     s->part = x.part; s->part2 = x.part2; s->sums = x.sums; s->sums2 = x.sums2;
     s->cross_list = x.cross_list; s->cross_count = x.cross_count;
     s->chunk_info = x.chunk_info;
+    s->win_cnt = x.win_cnt; s->seg_cnt = x.seg_cnt;
   }
   return c.used + 256;
 }
@@ -1262,6 +1352,8 @@ static void bind(SegJob& j, const SegScratch& s, int64_t n) {
   j.cross_list = s.cross_list;
   j.cross_count = s.cross_count;
   j.chunk_info = s.chunk_info;
+  j.win_cnt = s.win_cnt;
+  j.seg_cnt = s.seg_cnt;
 }
 
 static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
@@ -1273,31 +1365,12 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
                    (j.row_cap == 0 || j.row_stride % 4 == 0) &&
                    (j.table ? ((uintptr_t)j.table & 15) == 0
                             : (j.out_tab != nullptr || ((uintptr_t)j.out_rows & 15) == 0));
-  if (vec) {
-    TFS_CUDA_TRY(cudaMemsetAsync(j.cross_count, 0, sizeof(uint32_t), st));
+  if (vec) {  // one launch: windows + the fused crossing reduction (cross_arrive)
     const int64_t n4 = j.dim >> 2;
     const int wthreads = (int)std::min<int64_t>(128, cdiv(n4, 32) * 32);
     auto win_k = j.opt == 1 ? seg_window_vec4_kernel<1>
                             : (j.opt == 2 ? seg_window_vec4_kernel<2> : seg_window_vec4_kernel<0>);
     win_k<<<(unsigned)nchunks, wthreads, 0, st>>>(j);
-    launched();
-    const bool shortn = nchunks <= kBlkShortMaxChunks;
-    const int kb = shortn ? kBlkShort : kBlkLong;
-    const int64_t awork = cdiv(nchunks, kb) * n4;
-    const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(awork, 256), 8 * num_sms()));
-    auto cross_a = shortn ? seg_cross_a_vec4_kernel<kBlkShort> : seg_cross_a_vec4_kernel<kBlkLong>;
-    cross_a<<<agrid, 256, 0, st>>>(j, nchunks);
-    launched();
-    const int64_t bwork = (nchunks + 1) * n4;  // crossing segments <= chunks
-    const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(bwork, 256), 4 * num_sms()));
-    auto cross_k =
-        shortn ? (j.opt == 1 ? seg_cross_b_vec4_kernel<1, kBlkShort>
-                             : (j.opt == 2 ? seg_cross_b_vec4_kernel<2, kBlkShort>
-                                           : seg_cross_b_vec4_kernel<0, kBlkShort>))
-               : (j.opt == 1 ? seg_cross_b_vec4_kernel<1, kBlkLong>
-                             : (j.opt == 2 ? seg_cross_b_vec4_kernel<2, kBlkLong>
-                                           : seg_cross_b_vec4_kernel<0, kBlkLong>));
-    cross_k<<<bgrid, 256, 0, st>>>(j);
     launched();
   } else {
     seg_chunk_scalar_kernel<<<grid, 256, 0, st>>>(j);

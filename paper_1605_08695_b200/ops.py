@@ -27,7 +27,9 @@ def _stream():
 
 
 def _ws(nbytes: int, device) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    """Zero-filled: the segmented-sum workspaces hold arrival counters that must start at zero
+    (every call leaves them zero again; include/tfs.h)."""
+    return torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
 class ErrorSlot:
