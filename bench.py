@@ -442,6 +442,13 @@ def main():
         return sum(e[i0].elapsed_time(e[i1]) for e in evs_all) / len(evs_all)
 
     phases = {}
+    if R > 1 and S > 0:  # main-stream phase boundaries of the one-sided step (include/tfs.h)
+        for name, (i0, i1) in (("barrier_B0", (0, 1)), ("commit", (1, 2)),
+                               ("pull_W_and_wait_B1_side", (2, 3)), ("softmax_call", (9, 16)),
+                               ("reduce_push_W", (16, 4)), ("barrier_B2", (4, 5)),
+                               ("apply_W", (5, 6)), ("join_E_apply", (6, 7)),
+                               ("total", (0, 7))):
+            phases[name] = avg(i0, i1)
     if R == 1:
         for name, (i0, i1) in (("sample", (0, 1)), ("gather_E", (1, 2)), ("gather_W", (2, 3)),
                                ("sampled_softmax", (3, 4)), ("plan_E", (4, 5)),

@@ -483,8 +483,8 @@ struct SegJob {
   uint32_t* cross_list;
   uint32_t* cross_count;
   // Fused crossing reduction (vec path): arrival counters, zero between calls (the last
-  // arriver resets them): per window (the level-1 run of a segment inside a block of
-  // kRunWin windows is keyed by its first window) and per segment (level 2).
+  // arriver resets them): per partial slot (the level-1 run of a segment inside a block of
+  // kRunWin windows is keyed by its first slot) and per segment (level 2).
   uint32_t* win_cnt;
   uint32_t* seg_cnt;
 };
@@ -618,11 +618,13 @@ __device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_
   __syncthreads();  // this CTA's partial (all columns) is written
   if (threadIdx.x == 0) {
     __threadfence();
+    // keyed by the run's first SLOT (a window can start one run and end another)
     const uint32_t need = (uint32_t)(w1 - w0 + 1);
-    const uint32_t old = atomicAdd(j.win_cnt + w0, 1u);
+    const int64_t key = slot_of(w0);
+    const uint32_t old = atomicAdd(j.win_cnt + key, 1u);
     s_last = old + 1 == need;
     if (s_last) {
-      j.win_cnt[w0] = 0;
+      j.win_cnt[key] = 0;
       __threadfence();
     }
   }
@@ -1116,7 +1118,7 @@ static void carve_apply(Carver& c, int64_t n, int32_t dim, SegScratch& x) {
   x.cross_list = c.take<uint32_t>((size_t)nchunks + 1);
   x.cross_count = c.take<uint32_t>(1);
   x.chunk_info = c.take<int2>((size_t)nchunks);
-  x.win_cnt = c.take<uint32_t>((size_t)nchunks);
+  x.win_cnt = c.take<uint32_t>((size_t)2 * nchunks);
   x.seg_cnt = c.take<uint32_t>((size_t)n);
 }
 

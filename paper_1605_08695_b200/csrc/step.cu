@@ -633,8 +633,10 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
   const int64_t io = rank * m.istride, ro = rank * m.rstride;
   switch (phase) {
     case 0:
+      mark(st, 0, mn);
       break;
     case 1:
+      mark(st, 1, mn);  // B0 passed
       STEP_CALL(st, join(sd, mn, k.ev[kFork]));
       STEP_CALL(st, tfs_gather_peers((const float* const*)k.tab_E, m.shard_rows, m.d, k.x, m.B,
                                      m.V, R, k.h, rdt, k.err, sd));
@@ -645,6 +647,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
           cudaSuccess)
         st->status = st->status ? st->status : TFS_ERR_CUDA;
       sample_phase(st, k, mn);
+      mark(st, 2, mn);  // sample committed
       STEP_CALL(st, rec(k.ev[kQ], mn));
       STEP_CALL(st, waitev(sd, k.ev[kQ]));
       STEP_CALL(st, tfs_route_plan_push(k.qw, m.B + m.S, m.V, R, m.cap_w, k.rplan_w, k.rplan_w_b,
@@ -660,6 +663,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       STEP_CALL(st, tfs_gather_peers2((const float* const*)k.tab_W, m.shard_rows, m.d,
                                       (const float* const*)k.tab_b, k.qw, m.B + m.S, m.V, R,
                                       k.w_rows, rdt, k.b_rows, k.err, mn));
+      mark(st, 3, mn);  // W rows pulled
       STEP_CALL(st, waitev(mn, k.ev[kH]));
       tfs_ssm_args a = ssm_args(st, k, st->timing ? st->timing + 9 : nullptr);
       STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
@@ -673,17 +677,21 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
                                           k.dw, m.d, k.db, (float* const*)k.tab_grads,
                                           ro + m.off_w, (float* const*)k.tab_grads, ro + m.off_b,
                                           k.rws_w, k.rws_w_b, mn));
+      mark(st, 4, mn);  // W gradients pushed
       STEP_CALL(st, waitev(mn, k.ev[kRedE]));
       break;
     }
     case 3:
+      mark(st, 5, mn);  // B2 passed
       STEP_CALL(st, rec(k.ev[kB2], mn));
       STEP_CALL(st, waitev(sd, k.ev[kB2]));
       STEP_CALL(st, apply_owner(st, k, true, sd));
       STEP_CALL(st, waitev(mn, k.ev[kOwn]));
       STEP_CALL(st, apply_owner(st, k, false, mn));
+      mark(st, 6, mn);  // W updated
       STEP_CALL(st, join(mn, sd, k.ev[kSideDone]));
       sample_join(st, k, mn);
+      mark(st, 7, mn);  // E updated too (side joined)
       break;
   }
 }
