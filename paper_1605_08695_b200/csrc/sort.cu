@@ -600,6 +600,34 @@ template <int OPT>
 __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int c4, const D4& acc,
                                                 bool col0, double acc2);
 
+// acc += the partial slots slot(0), slot(1), ..., slot(n - 1) of column group c4, added in
+// that order; loads are issued 8 at a time (the slots were written by other CTAs: L2 loads).
+template <class SlotFn>
+__device__ __forceinline__ void sum_slots(const SegJob& j, int c4, int64_t n, SlotFn slot,
+                                          D4& acc, double& acc2) {
+  for (int64_t q0 = 0; q0 < n; q0 += 8) {
+    double2 v[8][2];
+    double p2[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (q0 + u < n) {
+        const int64_t sl = slot(q0 + u);
+        const double2* pp = reinterpret_cast<const double2*>(j.part + sl * j.dim) + 2 * c4;
+        v[u][0] = __ldcg(pp);
+        v[u][1] = __ldcg(pp + 1);
+        p2[u] = (c4 == 0 && j.rows2) ? __ldcg(j.part2 + sl) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (q0 + u < n) {
+        add4(acc, D4{v[u][0].x, v[u][0].y, v[u][1].x, v[u][1].y});
+        acc2 += p2[u];
+      }
+    }
+  }
+}
+
 // One CTA arrives with its piece of crossing segment s (window `chunk`; its partial is already
 // in slot 2 chunk (head piece) or 2 chunk + 1 (the segment's first piece)).  Level 1: the pieces
 // of s inside one block of kRunWin windows are summed, in window order, by the block's last
@@ -635,13 +663,7 @@ __device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_
   for (int c4 = threadIdx.x; c4 < n4; c4 += blockDim.x) {  // level 1, window order
     D4 acc = D4{0.0, 0.0, 0.0, 0.0};
     double acc2 = 0.0;
-    for (int64_t w = w0; w <= w1; ++w) {
-      const int64_t sl = slot_of(w);
-      const double2* pp = reinterpret_cast<const double2*>(j.part + sl * j.dim) + 2 * c4;
-      const double2 v0 = __ldcg(pp), v1 = __ldcg(pp + 1);  // L2: written by other CTAs
-      add4(acc, D4{v0.x, v0.y, v1.x, v1.y});
-      if (c4 == 0 && j.rows2) acc2 += __ldcg(j.part2 + sl);
-    }
+    sum_slots(j, c4, w1 - w0 + 1, [&](int64_t q) { return slot_of(w0 + q); }, acc, acc2);
     reinterpret_cast<D4*>(j.part + first * j.dim)[c4] = acc;
     if (c4 == 0 && j.rows2) j.part2[first] = acc2;
   }
@@ -661,13 +683,8 @@ __device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_
   for (int c4 = threadIdx.x; c4 < n4; c4 += blockDim.x) {  // level 2, block order
     D4 acc = D4{0.0, 0.0, 0.0, 0.0};
     double acc2 = 0.0;
-    for (int64_t bb = b0; bb <= b1; ++bb) {
-      const int64_t sl = bb == b0 ? 2 * c0 + 1 : 2 * bb * kRunWin;
-      const double2* pp = reinterpret_cast<const double2*>(j.part + sl * j.dim) + 2 * c4;
-      const double2 v0 = __ldcg(pp), v1 = __ldcg(pp + 1);  // L2: written by other CTAs
-      add4(acc, D4{v0.x, v0.y, v1.x, v1.y});
-      if (c4 == 0 && j.rows2) acc2 += __ldcg(j.part2 + sl);
-    }
+    sum_slots(j, c4, b1 - b0 + 1,
+              [&](int64_t q) { return q == 0 ? 2 * c0 + 1 : 2 * (b0 + q) * kRunWin; }, acc, acc2);
     seg_finish_vec4<OPT>(j, s, c4, acc, c4 == 0, acc2);
   }
 }
@@ -678,7 +695,6 @@ static_assert(kChunk <= 32, "the window prologue maps row r of a window to lane 
 template <int OPT>
 __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJob j) {
   __shared__ uint32_t s_perm[kChunk], s_key[kChunk], s_seg[kChunk];
-  __shared__ float s_r2[kChunk];
   __shared__ uint32_t s_mask[3];
   __shared__ int s_edge[2];
   const int64_t chunk = blockIdx.x;
@@ -696,7 +712,6 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
         seg_l = j.seg_of[base + r];
         s_key[r] = key_l;
         s_seg[r] = seg_l;
-        s_r2[r] = j.rows2 ? j.rows2[row2_off(j, pr)] : 0.f;
       }
     }
     // (kChunk == 32: lane r holds row r's key)
@@ -746,12 +761,14 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
     int r_start = 0;
     for (int b0 = 0; b0 < cnt; b0 += kWinBatch) {
       float4 x[kWinBatch], t[kWinBatch];
+      float r2v[kWinBatch];
 #pragma unroll
       for (int q = 0; q < kWinBatch; ++q) {  // the batch's rows (and table rows) in flight
         const int r = b0 + q;
-        x[q] = (r < cnt && s_key[r] < j.invalid_key)
-                   ? __ldg((const float4*)(j.rows + row_off(j, s_perm[r])) + c4)
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool valid = r < cnt && s_key[r] < j.invalid_key;
+        x[q] = valid ? __ldg((const float4*)(j.rows + row_off(j, s_perm[r])) + c4)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        r2v[q] = (valid && col0 && j.rows2) ? __ldg(j.rows2 + row2_off(j, s_perm[r])) : 0.f;
         t[q] = (!write_mode && r < cnt && ((WE >> r) & 1))
                    ? *((const float4*)(j.table + (int64_t)s_key[r] * j.dim) + c4)
                    : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -766,7 +783,7 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
           r_start = r;
         }
         add4(acc, x[q]);
-        acc2 += s_r2[r];
+        acc2 += r2v[q];
         if (!(((E >> r) & 1) || r == cnt - 1)) continue;
         // ---- the piece [r_start, r] is complete
         const uint32_t kr = s_key[r];

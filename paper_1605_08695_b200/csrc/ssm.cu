@@ -112,6 +112,7 @@ static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int 
   p.units = p.num_m * p.num_n * p.ksplit;
   p.a_mn = A.mn;
   p.b_mn = B.mn;
+  p.n_fast = (int64_t)M * K * 2 > (48ll << 20) ? 1 : 0;  // A (bf16) beyond ~40% of L2
   return TFS_OK;
 }
 
