@@ -482,6 +482,60 @@ __global__ void __launch_bounds__(kColsumChunks * GROUPS) g_colsum_kernel(
   }
 }
 
+// db_s[j] = sum over the GRAD epilogue's 32-row slab partials colpart[q * ld + j], q = 0, 1, ...
+// (fixed order: 32 row groups of slabs summed in slab order, then the groups in group order);
+// also returns the candidate map to all-zero (the GRAD pass was its last reader), and one
+// extra block forms loss_sum = c * sum_t loss_t (fixed-order tree) when loss_sum != nullptr.
+constexpr int kDbGroups = 32, kDbCols = 32;
+__global__ void __launch_bounds__(kDbGroups * kDbCols) db_colpart_kernel(
+    const float* colpart, int64_t nslabs, int64_t ld, int64_t S, float* db_s,
+    const int64_t* sampled, int2* cmap, int64_t vocab, const float* loss, int64_t B, float c,
+    float* loss_sum) {
+  __shared__ float red[kDbGroups][kDbCols + 1];
+  const int64_t ncol_blocks = cdiv_dev(S, kDbCols);
+  const int tid = threadIdx.x;
+  if (blockIdx.x >= ncol_blocks) {  // the loss-sum block
+    float acc = 0.f;
+    for (int64_t t = tid; t < B; t += blockDim.x) acc += loss[t];
+    float* r = &red[0][0];
+    r[tid] = acc;
+    __syncthreads();
+    for (int s2 = (int)blockDim.x / 2; s2 > 0; s2 >>= 1) {
+      if (tid < s2) r[tid] += r[tid + s2];
+      __syncthreads();
+    }
+    if (tid == 0) *loss_sum = c * r[0];
+    return;
+  }
+  if (cmap != nullptr) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + tid; j < S; j += ncol_blocks * blockDim.x) {
+      const int64_t k = sampled[j];
+      if (k >= 0 && k < vocab) cmap[k] = make_int2(0, 0);
+    }
+  }
+  const int col = tid % kDbCols, g = tid / kDbCols;
+  const int64_t j = (int64_t)blockIdx.x * kDbCols + col;
+  float acc = 0.f;
+  if (j < S) {
+    int64_t q = g;
+    for (; q + 7 * kDbGroups < nslabs; q += 8 * kDbGroups) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(colpart + (q + u * kDbGroups) * ld + j);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; q < nslabs; q += kDbGroups) acc += __ldg(colpart + q * ld + j);
+  }
+  red[g][col] = acc;
+  __syncthreads();
+  if (g == 0) {
+    float sum = 0.f;
+    for (int k = 0; k < kDbGroups; ++k) sum += red[k][col];
+    if (j < S) db_s[j] = sum;
+  }
+}
+
 // ---- operand conversion + column parameters + candidate map, one launch ---------------------
 // h and W_s -> bf16 (RNE).  Per column (padded to a multiple of the 256-column tile):
 // cb[j] = (b_s[j] - [Q] log_ec_s[j]) * log2(e) (-inf beyond S), sid[j] = s_j (-1 beyond S).
@@ -686,9 +740,9 @@ struct F32Ws {
 struct Bf16Ws {
   uint16_t *hb, *wsb, *G;
   float2* stats;
-  float *cb, *part_dh, *part_dws;
+  float *cb, *part_dh, *part_dws, *colpart;
   int32_t* sid;
-  int64_t Sp, Spad, ldh;
+  int64_t Sp, Spad, ldh, nslabs;
   int ks_dh, ks_dws;
 };
 
@@ -739,6 +793,8 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, int64_t 
   x.part_dws = c.take<float>(umma::part_floats((int)S, d, ks_dws));
   x.cb = c.take<float>(Spad);
   x.sid = c.take<int32_t>(Spad);
+  x.nslabs = cdiv(std::max<int64_t>(B, 1), umma::PM) * umma::kCta * 4;
+  x.colpart = c.take<float>((size_t)x.nslabs * Spad);
   x.Sp = Sp;
   x.Spad = Spad;
   x.ks_dh = ks_dh;
@@ -861,12 +917,24 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   const Bf16Ws& w = p.w;
   umma::EpiParams ep = p.ep;
   ep.zlab = zlab;
+#ifdef TFS_GRAD_COLSUM
+  ep.colpart = w.colpart;
+  ep.colpart_ld = w.Spad;
+#endif
   using umma::Operand;
   const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
   int32_t rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, p.bn, ep, w.G,
                                           w.Sp, st);
   if (rc != TFS_OK) return rc;
   mark(a, 4, st);
+#ifdef TFS_GRAD_COLSUM
+  {
+    const int64_t ncb = cdiv(S, kDbCols);
+    db_colpart_kernel<<<(unsigned)(ncb + (a->loss_sum ? 1 : 0)), kDbGroups * kDbCols, 0, st>>>(
+        w.colpart, w.nslabs, w.Spad, S, a->db_s, a->sampled, const_cast<int2*>(ep.cmap),
+        ep.vocab, a->loss, B, a->grad_scale, a->loss_sum);
+  }
+#else
   {
     const int64_t ncb = cdiv(S, kColsumChunks * 8);
     const bool narrow = ncb < num_sms();
@@ -875,6 +943,7 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
              st>>>(w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
                    a->loss, a->grad_scale, a->loss_sum);
   }
+#endif
   launched();
   mark(a, 5, st);
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)

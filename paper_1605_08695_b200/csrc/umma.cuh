@@ -42,7 +42,7 @@ constexpr int BM = 128, BN = 256, BK = 64;      // BM: rows per CTA; BN: tile N
 constexpr int STAGES = kCta == 2 ? 6 : 4;       // stages at the widest tile (BN); a launch with
 constexpr int kMaxStages = 8;                   // narrower tiles / no staging fits more (Params)
 #ifndef TFS_KSUB
-#define TFS_KSUB 1
+#define TFS_KSUB 2
 #endif
 constexpr int KSUB = TFS_KSUB;                  // k-blocks per pipeline stage (one barrier each)
 constexpr int PM = kCta * BM;                   // rows per tile
@@ -103,6 +103,11 @@ struct EpiParams {
   // label's logit (natural units, bias included) to zlab[m].
   int label_in;
   float* zlab;
+  // GRAD: column sums of each warp's 32-row slab of the stored (bf16) G, one fp32 partial per
+  // (32-row slab, column): colpart[slab * colpart_ld + n] (slab = (m-tile * kCta + rank) * 4 +
+  // lane quarter); db_s = their fixed-order sum (a small finalize pass).  nullptr: no sums.
+  float* colpart;
+  int64_t colpart_ld;
 };
 
 // One GEMM of a launch (a launch may carry two: the softmax backward runs dh and dW_s together
@@ -626,6 +631,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           if (lane == 0) {
             tma_store_2d(&ep.tG, sb, col0, row0);
             bulk_commit();
+          }
+          if (ep.colpart != nullptr) {  // db_s partial: column `lane` of the staged slab
+            const int nrows = min(32, M - row0);
+            const int k16 = lane >> 3, e2 = (lane & 7) * 2;
+            float cs = 0.f;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const uint32_t gb =
+                  *reinterpret_cast<const uint16_t*>(sb + r * 64 + ((k16 ^ ((r >> 1) & 3)) << 4) + e2);
+              if (r < nrows) cs += __uint_as_float(gb << 16);
+            }
+            const int64_t slab = ((int64_t)t.mt * kCta + rank) * 4 + quarter;
+            ep.colpart[slab * ep.colpart_ld + col0 + lane] = cs;
           }
           ++nst;
         } else {

@@ -6,7 +6,7 @@
 # then:  gpurun -- bash tools/ab_variants.sh base variants/NAME.so ...
 cd "$(dirname "$0")/.."
 export TFS_ALLOW_VARIANT_LIB=1
-for rep in 1 2; do
+for rep in ${AB_REPS:-1 2}; do
  for w in X Z; do
   for v in "$@"; do
    if [ "$v" = base ]; then unset TFS_LIB; else export TFS_LIB=$PWD/$v; fi
