@@ -917,25 +917,26 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   const Bf16Ws& w = p.w;
   umma::EpiParams ep = p.ep;
   ep.zlab = zlab;
-#ifdef TFS_GRAD_COLSUM
-  ep.colpart = w.colpart;
-  ep.colpart_ld = w.Spad;
-#endif
+  // db_s = column sums of G.  When G is larger than L2 can keep (Z: 1 GB), the GRAD epilogue
+  // sums each 32-row slab it stages (+8 us on X's GRAD, but no 1 GB re-read: Z -4.5 %, A/B
+  // round 2, profiles/r2_ab_grad_colsum.log); otherwise a separate pass over G is cheaper.
+  const bool fused_colsum = B * S * 2 > (64ll << 20);
+  if (fused_colsum) {
+    ep.colpart = w.colpart;
+    ep.colpart_ld = w.Spad;
+  }
   using umma::Operand;
   const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
   int32_t rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, p.bn, ep, w.G,
                                           w.Sp, st);
   if (rc != TFS_OK) return rc;
   mark(a, 4, st);
-#ifdef TFS_GRAD_COLSUM
-  {
+  if (fused_colsum) {
     const int64_t ncb = cdiv(S, kDbCols);
     db_colpart_kernel<<<(unsigned)(ncb + (a->loss_sum ? 1 : 0)), kDbGroups * kDbCols, 0, st>>>(
         w.colpart, w.nslabs, w.Spad, S, a->db_s, a->sampled, const_cast<int2*>(ep.cmap),
         ep.vocab, a->loss, B, a->grad_scale, a->loss_sum);
-  }
-#else
-  {
+  } else {
     const int64_t ncb = cdiv(S, kColsumChunks * 8);
     const bool narrow = ncb < num_sms();
     auto colsum = narrow ? g_colsum_kernel<256> : g_colsum_kernel<64>;
@@ -943,7 +944,6 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
              st>>>(w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
                    a->loss, a->grad_scale, a->loss_sum);
   }
-#endif
   launched();
   mark(a, 5, st);
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
