@@ -491,33 +491,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     uint32_t nst = 0;              // TMA stores issued by this warp (staging buffer parity)
     int acc = 0;
     uint32_t acc_phase = 0;
-    // STATS / GRAD per-tile inputs (this lane's column offset, its row's label, the label's
-    // candidate-column range, GRAD's lse) are loaded ONE TILE AHEAD: the loads for unit u+1 are
-    // issued while tile u is processed (the candidate-map lookup, which depends on the label,
-    // mid-tile), so no tile starts with exposed global-load round trips.
-    const float log2c = MODE == kGrad ? log2f(ep.c) : 0.f;
-    auto row_of = [&](const Unit& tt) {
-      return tt.mt * PM + (int)rank * BM + quarter * 32 + lane;
-    };
-    float nx_cb = 0.f, nx_lse = 0.f;
-    int64_t nx_yl = -2;
-    int2 nx_m = make_int2(0, 0);
-    auto issue_tile_loads = [&](int uu) {  // first stage: cb, label, lse of unit uu
-      const Unit tt = decode_unit(P, uu);
-      const int rr = row_of(tt);
-      const bool ok = rr < P.p[0].M;
-      nx_cb = __ldg(ep.cb + tt.nt * P.p[0].bn + half * 128 + quarter * 32 + lane);
-      nx_yl = (ok && ep.labels != nullptr) ? __ldg(ep.labels + rr) : -2;
-      if (MODE == kGrad) nx_lse = ok ? __ldg(ep.lse + rr) : 0.f;
-    };
-    auto issue_map_load = [&]() {  // second stage: the label's candidate-column range
-      nx_m = (ep.cmap != nullptr && nx_yl >= 0 && nx_yl < ep.vocab) ? __ldg(ep.cmap + nx_yl)
-                                                                     : make_int2(0, 0);
-    };
-    if (MODE != kStore && pair < P.total_units) {
-      issue_tile_loads(pair);
-      issue_map_load();
-    }
     for (int u = pair; u < P.total_units; u += npairs) {
       const Unit t = decode_unit(P, u);
       const Problem& q = P.p[MODE == kStore ? t.pi : 0];
@@ -531,24 +504,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       float goff = 0.f;  // GRAD: G = c 2^(v - lse log2 e) = 2^(v - goff)
       float* cbh = sCb + (acc * 2 + half) * 128;
       if (MODE != kStore) {
-        // this half tile's 128 column offsets -> smem (each warp of the half holds 32); the
+        // this half tile's 128 column offsets -> smem (each warp of the half loads 32); the
         // buffer of this accumulator was last read two tiles ago, before the previous barrier
-        cbh[quarter * 32 + lane] = nx_cb;
-        if (row_ok && ep.labels != nullptr) {
-          y = (int32_t)nx_yl;
-          if (ep.cmap == nullptr) {
-            hlo = 0;
-            hhi = ep.S_pad;
-          } else if (nx_m.y > 0) {
-            hlo = (1 << 30) - nx_m.x;
-            hhi = nx_m.y - 1;
+        cbh[quarter * 32 + lane] =
+            __ldg(ep.cb + t.nt * q.bn + half * 128 + quarter * 32 + lane);
+        if (row_ok) {
+          if (ep.labels != nullptr) {
+            const int64_t yl = __ldg(ep.labels + row);
+            y = (int32_t)yl;
+            if (ep.cmap == nullptr) {
+              hlo = 0;
+              hhi = ep.S_pad;
+            } else if (yl >= 0 && yl < ep.vocab) {
+              const int2 m = __ldg(ep.cmap + yl);
+              if (m.y > 0) {
+                hlo = (1 << 30) - m.x;
+                hhi = m.y - 1;
+              }
+            }
           }
+          if (MODE == kGrad) goff = __ldg(ep.lse + row) * kLog2e - log2f(ep.c);
         }
-        if (MODE == kGrad && row_ok) goff = nx_lse * kLog2e - log2c;
         named_bar_sync(2 + half, 128);
-        if (u + npairs < P.total_units) issue_tile_loads(u + npairs);  // the next tile's
       }
-      bool map_issued = false;
       float run_m = -INFINITY, run_s = 0.f;
 
       mbar_wait(tfull + acc, acc_phase);
@@ -564,10 +542,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (ct >= nw) break;                 // beyond a narrow tile's MMA width
         const int col0 = t.nt * q.bn + ct;
         const bool next = c + 1 < 4 && ct + 32 < nw;
-        if (MODE != kStore && c == 1 && u + npairs < P.total_units) {
-          issue_map_load();
-          map_issued = true;
-        }
         __syncwarp();  // tcgen05.ld / wait are .sync.aligned: the warp must be converged here
         tmem_wait_ld();
         float v[32];
@@ -743,7 +717,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
       }
-      if (MODE != kStore && !map_issued && u + npairs < P.total_units) issue_map_load();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(tempty + acc);  // the leader's barrier
