@@ -374,8 +374,11 @@ def main():
     def one_step(i):
         return st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES])
 
+    check_every = int(os.environ.get("TFS_BENCH_CHECK_EVERY", "0"))  # debugging aid (off)
     for i in range(args.warmup):
         one_step(i)
+        if check_every and (i + 1) % check_every == 0:
+            st.check(f"warmup step {i}")
     barrier()
 
     # ---- timed region: K steps, L2 flushed before each (outside the events)
@@ -390,6 +393,8 @@ def main():
         starts[i].record()
         one_step(i)
         ends[i].record()
+        if check_every and (i + 1) % check_every == 0:
+            st.check(f"timed step {i}")
     barrier()
     t_wall1 = time.time()
     per_step = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
