@@ -653,6 +653,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       STEP_CALL(st, tfs_route_plan_push(k.qw, m.B + m.S, m.V, R, m.cap_w, k.rplan_w, k.rplan_w_b,
                                         (int64_t* const*)k.tab_ids, io + m.cap_e, k.counts + R,
                                         k.err, sd));
+      STEP_CALL(st, rec(k.ev[kPlanW], sd));  // main's W gradient push reads this plan
       break;
     case 2: {
       STEP_CALL(st, tfs_scatter_plan_slots(k.recv_ids, m.istride, R, m.cap_e, k.nloc, 1,
@@ -673,6 +674,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
                                           nullptr, (float* const*)k.tab_grads, ro, nullptr, 0,
                                           k.rws_e, k.rws_e_b, sd));
       STEP_CALL(st, rec(k.ev[kRedE], sd));
+      STEP_CALL(st, waitev(mn, k.ev[kPlanW]));  // the W route plan (side stream, phase 1)
       STEP_CALL(st, tfs_route_reduce_push(k.rplan_w, k.rplan_w_b, m.B + m.S, m.V, R, m.cap_w,
                                           k.dw, m.d, k.db, (float* const*)k.tab_grads,
                                           ro + m.off_w, (float* const*)k.tab_grads, ro + m.off_b,
