@@ -12,6 +12,7 @@
 // the barrier is stream ordering across the local ranks (events), then phase k + 1.  No kernel
 // ever spins on another kernel of the same GPU.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <vector>
@@ -73,6 +74,15 @@ __global__ void add_i64_kernel(int64_t* p, int64_t v) { *p += v; }
 
 __global__ void next_counter_kernel(const int64_t* step, int64_t* next, int64_t add) {
   *next = *step + add;
+}
+
+// Race detector (TFS_DEBUG_SIDE_DELAY_US, read at create; unset in production): a spin of that
+// many microseconds at the head of every side-stream phase, so a missing cross-stream wait
+// shows up as wrong results in the parity tests.  Results are unchanged -- only timing.
+__global__ void delay_kernel(uint64_t ns) {
+  const uint64_t t0 = global_ns();
+  while (global_ns() - t0 < ns) {
+  }
 }
 
 // Index maps of the steps, computed once at create (nothing of them is left to the caller):
@@ -378,6 +388,7 @@ struct tfs_stepper {
   int32_t status = TFS_OK;  // first failing call of the step being issued
   cudaEvent_t origin = nullptr;
   void* const* timing = nullptr;  // caller's instrumentation events of the step being issued
+  uint64_t side_delay_ns = 0;     // TFS_DEBUG_SIDE_DELAY_US (race detector)
 };
 
 namespace {
@@ -403,6 +414,8 @@ inline int32_t join(cudaStream_t s2, cudaStream_t s1, cudaEvent_t e) {
   if (x != TFS_OK) return x;
   return waitev(s2, e);
 }
+// Fork the side stream from main (+ the race detector's delay).
+void fork_side(tfs_stepper* st, Rank& k, cudaStream_t mn);
 
 void set_buf(Rank& k, int which, void* p, int64_t n, int32_t t) {
   k.buf[which].p = p;
@@ -538,6 +551,14 @@ int32_t apply_owner(tfs_stepper* st, Rank& k, bool e_table, cudaStream_t s) {
                                        s);
 }
 
+void fork_side(tfs_stepper* st, Rank& k, cudaStream_t mn) {
+  STEP_CALL(st, join(k.side, mn, k.ev[kFork]));
+  if (st->side_delay_ns) {
+    delay_kernel<<<1, 1, 0, k.side>>>(st->side_delay_ns);
+    launched();
+  }
+}
+
 // ---------------------------------------------------------------------------------- R = 1
 // The embedding lookup (E) and the softmax-row lookup (W, b) are independent until the
 // sampled softmax, and so are their updates afterwards: the E path runs on the side stream.
@@ -548,7 +569,7 @@ void local_step(tfs_stepper* st, Rank& k, cudaStream_t mn) {
   const Dims& m = st->m;
   cudaStream_t sd = k.side;
   const int32_t rdt = m.bf16 ? TFS_BF16 : TFS_F32;
-  STEP_CALL(st, join(sd, mn, k.ev[kFork]));
+  fork_side(st, k, mn);
   STEP_CALL(st, tfs_gather(k.E, m.V, m.d, TFS_F32, k.x, m.B, k.h, rdt, k.err, sd));
   STEP_CALL(st, rec(k.ev[kH], sd));
   STEP_CALL(st, tfs_scatter_plan(k.x, m.B, m.V, k.plan_e, k.plan_e_b, k.err, sd));
@@ -637,7 +658,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       break;
     case 1:
       mark(st, 1, mn);  // B0 passed
-      STEP_CALL(st, join(sd, mn, k.ev[kFork]));
+      fork_side(st, k, mn);
       STEP_CALL(st, tfs_gather_peers((const float* const*)k.tab_E, m.shard_rows, m.d, k.x, m.B,
                                      m.V, R, k.h, rdt, k.err, sd));
       STEP_CALL(st, rec(k.ev[kH], sd));
@@ -721,7 +742,7 @@ void full_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
     case 0:
       break;
     case 1:
-      STEP_CALL(st, join(sd, mn, k.ev[kFork]));
+      fork_side(st, k, mn);
       STEP_CALL(st, tfs_route_plan_push(k.x, m.B, m.V, R, m.cap_e, k.rplan_e, k.rplan_e_b,
                                         (int64_t* const*)k.tab_ids, rank * m.istride, k.counts,
                                         k.err, sd));
@@ -901,6 +922,8 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
   TFS_SUPPORTED();
   tfs_stepper* st = new tfs_stepper();
   st->cfg = *cfg;
+  if (const char* dly = std::getenv("TFS_DEBUG_SIDE_DELAY_US"))
+    st->side_delay_ns = (uint64_t)std::strtoull(dly, nullptr, 10) * 1000ull;
   st->m = m;
   st->comm = comm;
   const int nl = (m.R == 1) ? 1 : comm->nlocal;

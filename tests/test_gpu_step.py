@@ -450,3 +450,20 @@ def test_route_capacity_overflow_is_reported():
     st.run(_dev(xs), _dev(ys))
     torch.cuda.synchronize()
     assert any(st.error(r)[0] == 9 for r in range(2))
+
+
+@pytest.mark.parametrize("R,full", [(1, False), (2, False), (3, False), (2, True)])
+def test_step_with_delayed_side_stream(R, full, monkeypatch):
+    """Race detector: TFS_DEBUG_SIDE_DELAY_US makes every side-stream phase start 3 ms late, so
+    any work on the main stream that reads side-stream results without an event wait computes
+    on stale data and fails the oracle comparison (round 2 found one this way: the W gradient
+    push of the R > 1 step did not wait for the W route plan)."""
+    monkeypatch.setenv("TFS_DEBUG_SIDE_DELAY_US", "3000")
+    w = (workloads.Workload("Fs", 1000, 64, 32, 0, R) if full else workloads.WORKLOADS["T"])
+    E, W, b = workloads.tables(w.vocab, w.dim)
+    cfg = _cfg(w, R, TFS_BF16)
+    st = make_step(cfg, E, W, b)
+    for k in range(2):
+        xs, ys = _batches(w, R, step=k)
+        E, W, b = gpu_tables(st, w.vocab)
+        _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, k)
