@@ -454,6 +454,12 @@ def main():
                                ("apply_W", (5, 6)), ("join_E_apply", (6, 7)),
                                ("total", (0, 7))):
             phases[name] = avg(i0, i1)
+        allph = [None] * world  # every rank's phases (load balance across owners)
+        dist.all_gather_object(allph, phases)
+        phases = {"rank0": phases, "max_over_ranks": {k: max(p[k] for p in allph) for k in phases},
+                  "per_rank_total": [p["total"] for p in allph],
+                  "per_rank_barrier_B2": [p["barrier_B2"] for p in allph],
+                  "per_rank_apply_W": [p["apply_W"] for p in allph]}
     if R == 1:
         for name, (i0, i1) in (("sample", (0, 1)), ("gather_E", (1, 2)), ("gather_W", (2, 3)),
                                ("sampled_softmax", (3, 4)), ("plan_E", (4, 5)),

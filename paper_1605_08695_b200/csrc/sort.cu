@@ -660,6 +660,16 @@ __device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_
   if (!s_last) return;
   const int n4 = j.dim >> 2;
   const int64_t first = slot_of(w0);
+  const int64_t b0 = c0 / kRunWin, b1 = c1 / kRunWin;
+  if (b0 == b1) {  // the segment lies in one block: level 1 finishes it (no second arrival)
+    for (int c4 = threadIdx.x; c4 < n4; c4 += blockDim.x) {
+      D4 acc = D4{0.0, 0.0, 0.0, 0.0};
+      double acc2 = 0.0;
+      sum_slots(j, c4, w1 - w0 + 1, [&](int64_t q) { return slot_of(w0 + q); }, acc, acc2);
+      seg_finish_vec4<OPT>(j, s, c4, acc, c4 == 0, acc2);
+    }
+    return;
+  }
   for (int c4 = threadIdx.x; c4 < n4; c4 += blockDim.x) {  // level 1, window order
     D4 acc = D4{0.0, 0.0, 0.0, 0.0};
     double acc2 = 0.0;
@@ -668,7 +678,6 @@ __device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_
     if (c4 == 0 && j.rows2) j.part2[first] = acc2;
   }
   __syncthreads();
-  const int64_t b0 = c0 / kRunWin, b1 = c1 / kRunWin;
   if (threadIdx.x == 0) {
     __threadfence();
     const uint32_t old = atomicAdd(j.seg_cnt + s, 1u);
