@@ -437,7 +437,7 @@ def main():
     barrier()
     for i in range(n_ph):
         flush.zero_()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(17)]
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(21)]
         st.run(xs_d[i % N_BATCHES], ys_d[i % N_BATCHES], timing_events=evs)
         evs_all.append(evs)
     barrier()
@@ -452,7 +452,10 @@ def main():
                                ("pull_W_and_wait_B1_side", (2, 3)), ("softmax_call", (9, 16)),
                                ("reduce_push_W", (16, 4)), ("barrier_B2", (4, 5)),
                                ("apply_W", (5, 6)), ("join_E_apply", (6, 7)),
-                               ("total", (0, 7))):
+                               ("total", (0, 7)),
+                               ("side_phase1_from_B0", (1, 17)), ("side_B1_wait", (17, 18)),
+                               ("side_owner_plans", (18, 19)), ("side_until_E_pushed", (19, 20)),
+                               ("side_E_pushed_at", (0, 20)), ("main_W_pushed_at", (0, 4))):
             phases[name] = avg(i0, i1)
         allph = [None] * world  # every rank's phases (load balance across owners)
         dist.all_gather_object(allph, phases)

@@ -553,14 +553,15 @@ int32_t tfs_step_set_counter(tfs_stepper* st, int64_t value);
  * step's input buffers on `stream` inside the call, and each local rank's loss_sum is copied
  * back to io->loss_host[nlocal] (host) on `stream` -- the caller synchronises before reading.
  * The step counter (sampler; TFS_BUF_STEP) advances by one on the device.
- * io->timing_events (one local rank, eager only; NULL normally): 17 cudaEvent_t.  R = 1: the
+ * io->timing_events (one local rank, eager only; NULL normally): 21 cudaEvent_t.  R = 1: the
  * step runs its phases SERIALLY on one stream and records 0 start, 1 sample committed (and the
  * next step's drawn), 2 E rows gathered, 3 W rows + b gathered, 4 softmax done, 5 E plan built,
  * 6 W plan built, 7 E updated, 8 W + b updated; 9..16 the softmax call's 8 events
  * (tfs_ssm_args.timing_events).  R > 1 (phases overlapped as usual; events on the main
  * stream): the sampled step records 0 start, 1 B0 passed, 2 sample committed, 3 W rows
  * pulled, 4 W gradients pushed, 5 B2 passed, 6 W updated, 7 E updated (side joined), and
- * 9..16 as above for the softmax; the sharded full softmax records 9 / 10 around its
+ * 9..16 as above for the softmax; on the side stream 17 ids pushed (before B1), 18 B1 passed,
+ * 19 owner plans built, 20 E gradients pushed; the sharded full softmax records 9 / 10 around its
  * partial-stats call and 11 / 12 around its backward call.  Entries may be NULL. */
 typedef struct {
   const int64_t* x;

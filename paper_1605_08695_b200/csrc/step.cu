@@ -675,13 +675,16 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
                                         (int64_t* const*)k.tab_ids, io + m.cap_e, k.counts + R,
                                         k.err, sd));
       STEP_CALL(st, rec(k.ev[kPlanW], sd));  // main's W gradient push reads this plan
+      mark(st, 17, sd);  // side: pushes issued (before B1)
       break;
     case 2: {
+      mark(st, 18, sd);  // side: B1 passed
       STEP_CALL(st, tfs_scatter_plan_slots(k.recv_ids, m.istride, R, m.cap_e, k.nloc, 1,
                                            k.oplan_e, k.oplan_e_b, k.err, sd));
       STEP_CALL(st, tfs_scatter_plan_slots(k.recv_ids + m.cap_e, m.istride, R, m.cap_w, k.nloc,
                                            1, k.oplan_w, k.oplan_w_b, k.err, sd));
       STEP_CALL(st, rec(k.ev[kOwn], sd));
+      mark(st, 19, sd);  // side: owner plans built
       STEP_CALL(st, tfs_gather_peers2((const float* const*)k.tab_W, m.shard_rows, m.d,
                                       (const float* const*)k.tab_b, k.qw, m.B + m.S, m.V, R,
                                       k.w_rows, rdt, k.b_rows, k.err, mn));
@@ -695,6 +698,7 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
                                           nullptr, (float* const*)k.tab_grads, ro, nullptr, 0,
                                           k.rws_e, k.rws_e_b, sd));
       STEP_CALL(st, rec(k.ev[kRedE], sd));
+      mark(st, 20, sd);  // side: E gradients pushed
       STEP_CALL(st, waitev(mn, k.ev[kPlanW]));  // the W route plan (side stream, phase 1)
       STEP_CALL(st, tfs_route_reduce_push(k.rplan_w, k.rplan_w_b, m.B + m.S, m.V, R, m.cap_w,
                                           k.dw, m.d, k.db, (float* const*)k.tab_grads,

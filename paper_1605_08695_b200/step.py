@@ -240,7 +240,7 @@ class Step:
             for e in timing_events:  # torch creates its CUDA event lazily, at the first record
                 if e is not None and not e.cuda_event:
                     e.record()
-            arr = (ctypes.c_void_p * 17)(*[ctypes.c_void_p(e.cuda_event if e is not None else 0)
+            arr = (ctypes.c_void_p * 21)(*[ctypes.c_void_p(e.cuda_event if e is not None else 0)
                                           for e in timing_events])
             io.timing_events = ctypes.cast(arr, ctypes.c_void_p)
         check(_lib.lib().tfs_step_run(self.ptr, ctypes.byref(io), _stream()), "tfs_step_run")
