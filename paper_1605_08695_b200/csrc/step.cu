@@ -692,20 +692,19 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       STEP_CALL(st, waitev(mn, k.ev[kH]));
       tfs_ssm_args a = ssm_args(st, k, st->timing ? st->timing + 9 : nullptr);
       STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
-      STEP_CALL(st, rec(k.ev[kSsm], mn));
-      STEP_CALL(st, waitev(sd, k.ev[kSsm]));
-      STEP_CALL(st, tfs_route_reduce_push(k.rplan_e, k.rplan_e_b, m.B, m.V, R, m.cap_e, k.dh, m.d,
-                                          nullptr, (float* const*)k.tab_grads, ro, nullptr, 0,
-                                          k.rws_e, k.rws_e_b, sd));
-      STEP_CALL(st, rec(k.ev[kRedE], sd));
-      mark(st, 20, sd);  // side: E gradients pushed
-      STEP_CALL(st, waitev(mn, k.ev[kPlanW]));  // the W route plan (side stream, phase 1)
+      // Both gradient pushes on the main stream, right after the softmax: B2 then does not wait
+      // for the side stream's owner plans (which the persistent softmax GEMMs delay: they hold
+      // every SM), only the applies in phase 3 do.
+      STEP_CALL(st, waitev(mn, k.ev[kPlanW]));  // the E and W route plans (side, phase 1)
       STEP_CALL(st, tfs_route_reduce_push(k.rplan_w, k.rplan_w_b, m.B + m.S, m.V, R, m.cap_w,
                                           k.dw, m.d, k.db, (float* const*)k.tab_grads,
                                           ro + m.off_w, (float* const*)k.tab_grads, ro + m.off_b,
                                           k.rws_w, k.rws_w_b, mn));
       mark(st, 4, mn);  // W gradients pushed
-      STEP_CALL(st, waitev(mn, k.ev[kRedE]));
+      STEP_CALL(st, tfs_route_reduce_push(k.rplan_e, k.rplan_e_b, m.B, m.V, R, m.cap_e, k.dh, m.d,
+                                          nullptr, (float* const*)k.tab_grads, ro, nullptr, 0,
+                                          k.rws_e, k.rws_e_b, mn));
+      mark(st, 20, mn);  // E gradients pushed
       break;
     }
     case 3:
@@ -947,8 +946,13 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
     Rank& k = st->ranks[l];
     k.r = (m.R == 1) ? 0 : comm->first + l;
     k.nloc = cdiv(V - k.r, R);
-    if (cudaStreamCreateWithFlags(&k.side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&k.smp, cudaStreamNonBlocking) != cudaSuccess)
+    // The side streams (plans, pushes, owner plans, the E path; the sampler ahead) get the
+    // highest priority: the softmax's persistent GEMMs hold every SM while they run, so side
+    // work only runs at the main stream's kernel boundaries -- where it should go first.
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&k.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&k.smp, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
       return bail(TFS_ERR_CUDA);
     if (nl > 1) {
       if (cudaStreamCreateWithFlags(&k.main, cudaStreamNonBlocking) != cudaSuccess)
