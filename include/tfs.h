@@ -225,6 +225,9 @@ typedef struct {
    * 3 after the combine, 4 after the gradient GEMM (GRAD), 5 after the column sums, 6 after
    * the grouped dh / dW_s GEMM, 7 end.  Lets a caller time each GEMM launch live. */
   void* const* timing_events;
+  /* SMs the persistent tensor-core GEMMs of the call leave free (0: use every SM), so work on
+   * other streams (e.g. the training step's side streams) progresses while they run. */
+  int32_t sm_reserve;
 } tfs_ssm_args;
 size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype,
                                int64_t vocab);

@@ -75,7 +75,7 @@ class SsmArgs(ctypes.Structure):
         ("h", P), ("labels", P), ("w_true", P), ("b_true", P), ("log_ec_true", P),
         ("sampled", P), ("w_s", P), ("b_s", P), ("log_ec_s", P),
         ("loss", P), ("lse", P), ("loss_sum", P), ("dh", P), ("dw_true", P), ("db_true", P),
-        ("dw_s", P), ("db_s", P), ("vocab", I64), ("timing_events", P),
+        ("dw_s", P), ("db_s", P), ("vocab", I64), ("timing_events", P), ("sm_reserve", I32),
     ]
 
 

@@ -127,8 +127,14 @@ static void stage_plan(Params& P) {
       std::min<int>(kMaxStages, ((int)kSmemBytes - fixed) / (KSUB * (A_BYTES + P.b_stride)));
 }
 
+// groups: CTA groups (SMs / kCta) the persistent launch uses; <= 0: every SM.
+static int groups_or_all(int groups) {
+  const int all = num_sms() / kCta;
+  return groups > 0 ? std::min(groups, all) : all;
+}
+
 template <int MODE, bool LAB = false>
-static int32_t launch_params(Params P, cudaStream_t st) {
+static int32_t launch_params(Params P, int groups_req, cudaStream_t st) {
   stage_plan<MODE>(P);
   static bool attr_done = false;
   if (!attr_done) {
@@ -138,7 +144,7 @@ static int32_t launch_params(Params P, cudaStream_t st) {
     attr_done = true;
   }
   // persistent: one CTA (or CTA pair: a cluster of 2 on one TPC) per SM (or per two SMs)
-  const int groups = std::min(P.total_units, num_sms() / kCta);
+  const int groups = std::min(P.total_units, groups_or_all(groups_req));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(kCta * groups));
   cfg.blockDim = dim3(kThreads);
@@ -165,8 +171,8 @@ static int32_t launch_params(Params P, cudaStream_t st) {
   return TFS_OK;
 }
 
-int pick_bn(int M, int N) {
-  const int64_t groups = num_sms() / kCta;
+int pick_bn(int M, int N, int groups_req) {
+  const int64_t groups = groups_or_all(groups_req);
   int best = BN;
   int64_t best_cost = -1;
   for (int bn = BN; bn >= 128; bn -= 32) {
@@ -181,7 +187,8 @@ int pick_bn(int M, int N) {
 }
 
 int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn,
-                             EpiParams ep, uint16_t* G, int64_t ldG, cudaStream_t st) {
+                             int groups, EpiParams ep, uint16_t* G, int64_t ldG,
+                             cudaStream_t st) {
   if (A.mn || B.mn) return TFS_ERR_INVALID_ARGUMENT;
   Params P{};
   int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1, bn);
@@ -195,12 +202,13 @@ int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K
   }
   P.ep = ep;
   if (ep.label_in)
-    return mode == kStats ? launch_params<kStats, true>(P, st) : launch_params<kGrad, true>(P, st);
-  return mode == kStats ? launch_params<kStats>(P, st) : launch_params<kGrad>(P, st);
+    return mode == kStats ? launch_params<kStats, true>(P, groups, st)
+                          : launch_params<kGrad, true>(P, groups, st);
+  return mode == kStats ? launch_params<kStats>(P, groups, st) : launch_params<kGrad>(P, groups, st);
 }
 
 // Up to two STORE GEMMs in one persistent launch; the caller orders them by unit size.
-int32_t launch_store(const Gemm* g, int count, cudaStream_t st) {
+int32_t launch_store(const Gemm* g, int count, int groups, cudaStream_t st) {
   if (count < 1 || count > 2) return TFS_ERR_INVALID_ARGUMENT;
   Params P{};
   P.nprob = count;
@@ -225,7 +233,7 @@ int32_t launch_store(const Gemm* g, int count, cudaStream_t st) {
     p.wt_bf16 = g[i].wt_bf16;
     P.total_units += p.units;
   }
-  return launch_params<kStore>(P, st);
+  return launch_params<kStore>(P, groups, st);
 }
 
 }  // namespace umma
@@ -856,6 +864,7 @@ struct Bf16Plan {
   Bf16Ws w;
   umma::EpiParams ep;
   int bn, num_n;
+  int groups;  // CTA groups of the persistent GEMMs (0: every SM; tfs_ssm_args.sm_reserve)
   bool bin;
 };
 
@@ -863,7 +872,8 @@ static void bf16_plan(const tfs_ssm_args* a, void* ws, Bf16Plan* p) {
   ws_layout(a->B, a->S, a->dim, TFS_BF16, a->vocab, nullptr, &p->w, ws);
   const bool hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) != 0;
   const bool label_in = (a->flags & TFS_LABEL_IN_CANDIDATES) != 0;
-  p->bn = a->S > 0 ? umma::pick_bn((int)a->B, (int)a->S) : umma::BN;
+  p->groups = a->sm_reserve > 0 ? std::max(1, num_sms() / umma::kCta - a->sm_reserve) : 0;
+  p->bn = a->S > 0 ? umma::pick_bn((int)a->B, (int)a->S, p->groups) : umma::BN;
   p->num_n = (int)cdiv(a->S, p->bn);
   p->bin = (a->flags & TFS_BF16_OPERANDS) != 0;  // h, w_true, w_s given in bf16
   if (p->bin) {  // already rounded by the producer (e.g. a bf16 Gather): no conversion pass
@@ -905,6 +915,7 @@ static int32_t bf16_prep(const tfs_ssm_args* a, const Bf16Plan& p, cudaStream_t 
 static int32_t bf16_stats(const tfs_ssm_args* a, const Bf16Plan& p, cudaStream_t st) {
   const umma::Operand hK{p.w.hb, p.w.ldh, false}, wsK{p.w.wsb, a->dim, false};
   return umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)a->B, (int)a->S, a->dim, p.bn,
+                                    p.groups,
                                     p.ep, nullptr, 0, st);
 }
 
@@ -927,7 +938,8 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   }
   using umma::Operand;
   const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
-  int32_t rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, p.bn, ep, w.G,
+  int32_t rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, p.bn,
+                                          p.groups, ep, w.G,
                                           w.Sp, st);
   if (rc != TFS_OK) return rc;
   mark(a, 4, st);
@@ -959,7 +971,7 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   // larger units first so the static round-robin schedule balances the SMs
   const int64_t u0 = cdiv(B, umma::BK) / w.ks_dws, u1 = cdiv(S, umma::BK) / w.ks_dh;
   if (u1 > u0) std::swap(g[0], g[1]);
-  rc = umma::launch_store(g, 2, st);
+  rc = umma::launch_store(g, 2, p.groups, st);
   if (rc != TFS_OK) return rc;
   mark(a, 6, st);
   if (dh_split) {
@@ -1157,7 +1169,7 @@ extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn,
   float* part = c.take<float>(umma::part_floats(M, N, ks));
   umma::Gemm g{umma::Operand{A, lda, a_mn != 0}, umma::Operand{B, ldb, b_mn != 0}, M, N, K, ks,
                C, N, part, nullptr, nullptr, 0, 0};
-  int32_t rc = umma::launch_store(&g, 1, st);
+  int32_t rc = umma::launch_store(&g, 1, 0, st);
   if (rc != TFS_OK || ks == 1) return rc;
   split_finalize_kernel<false><<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, nullptr,
                                                                     nullptr, C);

@@ -23,6 +23,12 @@ namespace tfs {
 namespace {
 
 constexpr size_t kHeapHeader = 64 * 1024;  // barrier flags: [kChannels][kMaxRanks] uint32
+#ifndef TFS_STEP_SM_RESERVE_R
+#define TFS_STEP_SM_RESERVE_R 8  // SMs left free by the softmax GEMMs in the R > 1 step
+#endif
+#ifndef TFS_STEP_SM_RESERVE_1
+#define TFS_STEP_SM_RESERVE_1 0  // ... and in the R = 1 step
+#endif
 constexpr int kChannels = 16;
 constexpr int kMaxRanks = 64;
 
@@ -389,6 +395,7 @@ struct tfs_stepper {
   cudaEvent_t origin = nullptr;
   void* const* timing = nullptr;  // caller's instrumentation events of the step being issued
   uint64_t side_delay_ns = 0;     // TFS_DEBUG_SIDE_DELAY_US (race detector)
+  int32_t sm_reserve = 0;         // SMs the softmax GEMMs leave to the side streams
 };
 
 namespace {
@@ -453,6 +460,7 @@ tfs_ssm_args ssm_args(const tfs_stepper* st, const Rank& k, void* const* events)
   a.db_s = k.db + m.B;
   a.vocab = m.V;
   a.timing_events = events;
+  a.sm_reserve = st->sm_reserve;
   return a;
 }
 
@@ -471,6 +479,7 @@ tfs_ssm_args slice_args(const tfs_stepper* st, const Rank& k, bool backward) {
   a.w_s = (const float*)k.W_bf;
   a.b_s = k.b;
   a.vocab = m.V;
+  a.sm_reserve = st->sm_reserve;
   if (backward) {
     a.lse = k.lse_all;
     a.dh = k.dh_part;
@@ -925,6 +934,10 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
   TFS_SUPPORTED();
   tfs_stepper* st = new tfs_stepper();
   st->cfg = *cfg;
+  // The softmax's persistent GEMMs hold every SM they run on; leaving a few to the side
+  // streams lets the plans / pushes / owner plans progress during the GEMMs (R > 1, where the
+  // side work is on the critical path).  A tuning constant (A/B: profiles/r2_summary.md).
+  st->sm_reserve = m.R > 1 ? TFS_STEP_SM_RESERVE_R : TFS_STEP_SM_RESERVE_1;
   if (const char* dly = std::getenv("TFS_DEBUG_SIDE_DELAY_US"))
     st->side_delay_ns = (uint64_t)std::strtoull(dly, nullptr, 10) * 1000ull;
   st->m = m;

@@ -766,12 +766,12 @@ int effective_split(int K, int ksplit);
 
 // STATS / GRAD launch; for GRAD, G (bf16 [M x ldG], ldG % 8 == 0) receives the gradient.
 // bn: tile width along N (pick_bn); cb / sid must be readable up to num_n * bn + 256 columns.
-int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn,
+int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn, int groups,
                              EpiParams ep, uint16_t* G, int64_t ldG, cudaStream_t st);
 // Tile width for an M x N output of single-pass tiles: the multiple of 32 in [128, 256] that
 // minimises the makespan (rounds of tiles over the CTA groups x tile width).
-int pick_bn(int M, int N);
-int32_t launch_store(const Gemm* g, int count, cudaStream_t st);
+int pick_bn(int M, int N, int groups);
+int32_t launch_store(const Gemm* g, int count, int groups, cudaStream_t st);
 
 }  // namespace umma
 }  // namespace tfs

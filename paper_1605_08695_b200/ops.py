@@ -178,7 +178,7 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
                 _p(h), _p(labels), _p(w_true), _p(b_true), _p(log_ec_true), _p(sampled), _p(w_s),
                 _p(b_s), _p(log_ec_s), _p(out["loss"]), _p(out["lse"]), _p(out["loss_sum"]),
                 _p(out["dh"]), _p(out["dw_true"]), _p(out["db_true"]), _p(out["dw_s"]),
-                _p(out["db_s"]), int(vocab), None)
+                _p(out["db_s"]), int(vocab), None, 0)
     if events is not None:  # 8 torch.cuda.Event (timing), recorded inside the call
         arr = (ctypes.c_void_p * 8)(*[ctypes.c_void_p(e.cuda_event) for e in events])
         a.timing_events = ctypes.cast(arr, ctypes.c_void_p)
@@ -195,7 +195,7 @@ def _slice_args(h, labels, sampled, w_s, b_s, flags, grad_scale, vocab, lse=None
         flags |= TFS_BF16_OPERANDS
     return SsmArgs(B, sampled.numel(), d, TFS_BF16, flags, float(grad_scale), _p(h), _p(labels),
                    None, None, None, _p(sampled), _p(w_s), _p(b_s), None, None, _p(lse), None,
-                   _p(dh), None, None, _p(dw_s), _p(db_s), int(vocab), None)
+                   _p(dh), None, None, _p(dw_s), _p(db_s), int(vocab), None, 0)
 
 
 def ssm_partial_stats(h, labels, sampled, w_s, b_s, *, flags=TFS_LABEL_IN_CANDIDATES,
