@@ -1820,9 +1820,18 @@ __global__ void __launch_bounds__(512) merge_runs_smem_kernel(IdsView ids, int32
                                                               tfs_device_error* err) {
   extern __shared__ uint32_t runs[];  // [R][cap]
   const int64_t n = (int64_t)R * cap;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const int64_t o = i / cap, s = i - o * cap;
-    runs[i] = run_key(ids, o, s, limit);
+  for (int64_t i0 = threadIdx.x; i0 < n; i0 += 8 * (int64_t)blockDim.x) {  // 8 loads in flight
+    uint32_t kk[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + u * (int64_t)blockDim.x;
+      kk[u] = i < n ? run_key(ids, i / cap, i - (i / cap) * cap, limit) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + u * (int64_t)blockDim.x;
+      if (i < n) runs[i] = kk[u];
+    }
   }
   __syncthreads();
   __shared__ int64_t valid_cnt[1024 + 1];  // R <= 1024: per-run valid counts, then the total
@@ -1833,8 +1842,8 @@ __global__ void __launch_bounds__(512) merge_runs_smem_kernel(IdsView ids, int32
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = i / cap, s = i - o * cap;
     const uint32_t k = runs[i];
-    const int64_t id = ids.p[o * ids.stride + s];
-    if (id != -1 && k == 0xFFFFFFFFu) report_error(err, TFS_ERR_OUT_OF_RANGE, i);
+    if (k == 0xFFFFFFFFu && ids.p[o * ids.stride + s] != -1)  // not padding: a bad id
+      report_error(err, TFS_ERR_OUT_OF_RANGE, i);
     if (s + 1 < cap && runs[i + 1] != 0xFFFFFFFFu && runs[i + 1] <= k)
       report_error(err, TFS_ERR_INVALID_ARGUMENT, i);
     int64_t pos;
