@@ -768,31 +768,38 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
     D4 acc = D4{0.0, 0.0, 0.0, 0.0};
     double acc2 = 0.0;
     int r_start = 0;
-    for (int b0 = 0; b0 < cnt; b0 += kWinBatch) {
-      float4 x[kWinBatch], t[kWinBatch];
-      float r2v[kWinBatch];
+    // Rows in half-batches of kHalf, software-pipelined: the loads of half-batch h + 1 (its
+    // gradient rows and the table rows of the whole segments ending in it) are in flight while
+    // half-batch h is summed and applied.
+    constexpr int kHalf = kWinBatch / 2;
+    float4 x[2][kHalf], t[2][kHalf];
+    float r2v[2][kHalf];
+    auto load_half = [&](int hb, int buf) {
 #pragma unroll
-      for (int q = 0; q < kWinBatch; ++q) {  // the batch's rows (and table rows) in flight
-        const int r = b0 + q;
+      for (int q = 0; q < kHalf; ++q) {
+        const int r = hb * kHalf + q;
         const bool valid = r < cnt && s_key[r] < j.invalid_key;
-        x[q] = valid ? __ldg((const float4*)(j.rows + row_off(j, s_perm[r])) + c4)
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-        r2v[q] = (valid && col0 && j.rows2) ? __ldg(j.rows2 + row2_off(j, s_perm[r])) : 0.f;
-        t[q] = (!write_mode && r < cnt && ((WE >> r) & 1))
-                   ? *((const float4*)(j.table + (int64_t)s_key[r] * j.dim) + c4)
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[buf][q] = valid ? __ldg((const float4*)(j.rows + row_off(j, s_perm[r])) + c4)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        r2v[buf][q] =
+            (valid && col0 && j.rows2) ? __ldg(j.rows2 + row2_off(j, s_perm[r])) : 0.f;
+        t[buf][q] = (!write_mode && r < cnt && ((WE >> r) & 1))
+                        ? *((const float4*)(j.table + (int64_t)s_key[r] * j.dim) + c4)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+    };
+    auto proc_half = [&](int hb, int buf) {
 #pragma unroll
-      for (int q = 0; q < kWinBatch; ++q) {
-        const int r = b0 + q;
+      for (int q = 0; q < kHalf; ++q) {
+        const int r = hb * kHalf + q;
         if (r >= cnt) break;
         if (r > 0 && ((H >> r) & 1)) {
           acc = D4{0.0, 0.0, 0.0, 0.0};
           acc2 = 0.0;
           r_start = r;
         }
-        add4(acc, x[q]);
-        acc2 += r2v[q];
+        add4(acc, x[buf][q]);
+        acc2 += r2v[buf][q];
         if (!(((E >> r) & 1) || r == cnt - 1)) continue;
         // ---- the piece [r_start, r] is complete
         const uint32_t kr = s_key[r];
@@ -811,7 +818,8 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
               }
             }
           } else {
-            *((float4*)(j.table + (int64_t)kr * j.dim) + c4) = opt_step4<OPT>(j, t[q], acc, kr, c4);
+            *((float4*)(j.table + (int64_t)kr * j.dim) + c4) =
+                opt_step4<OPT>(j, t[buf][q], acc, kr, c4);
             if (j.table2 && col0) opt_step2<OPT>(j, kr, acc2);
           }
         } else {
@@ -820,6 +828,14 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
           if (col0 && j.rows2) j.part2[slot] = acc2;
         }
       }
+    };
+    const int nh = (cnt + kHalf - 1) / kHalf;
+    load_half(0, 0);
+    for (int hb = 0; hb < nh; hb += 2) {
+      if (hb + 1 < nh) load_half(hb + 1, 1);
+      proc_half(hb, 0);
+      if (hb + 2 < nh) load_half(hb + 2, 0);
+      if (hb + 1 < nh) proc_half(hb + 1, 1);
     }
   }
   // Pieces of segments crossing this window's edges (at most two: the one that started before
