@@ -555,6 +555,8 @@ int32_t tfs_step_set_counter(tfs_stepper* st, int64_t value);
  * [nlocal x B] int64 (rank-major); == 1: HOST pointers (pinned for asynchrony) copied to the
  * step's input buffers on `stream` inside the call, and each local rank's loss_sum is copied
  * back to io->loss_host[nlocal] (host) on `stream` -- the caller synchronises before reading.
+ * With one local rank and y == x + B (x || y adjacent in one buffer) the inputs move in ONE
+ * copy.
  * The step counter (sampler; TFS_BUF_STEP) advances by one on the device.
  * io->timing_events (one local rank, eager only; NULL normally): 21 cudaEvent_t.  R = 1: the
  * step runs its phases SERIALLY on one stream and records 0 start, 1 sample committed (and the

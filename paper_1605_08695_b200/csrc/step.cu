@@ -1256,10 +1256,15 @@ extern "C" int32_t tfs_step_run(tfs_stepper* st, const tfs_step_io* io, void* st
     const cudaMemcpyKind kind = io->host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     for (size_t l = 0; l < nl; ++l) {
       Rank& k = st->ranks[l];
-      if (io->x + l * m.B != k.x)
-        TFS_CUDA_TRY(cudaMemcpyAsync(k.x, io->x + l * m.B, sizeof(int64_t) * m.B, kind, s));
-      if (io->y + l * m.B != k.y)
-        TFS_CUDA_TRY(cudaMemcpyAsync(k.y, io->y + l * m.B, sizeof(int64_t) * m.B, kind, s));
+      const int64_t* xs = io->x + l * m.B;
+      const int64_t* ys = io->y + l * m.B;
+      if (nl == 1 && ys == xs + m.B && k.y == k.x + m.B) {  // adjacent: one copy of x || y
+        if (xs != k.x)
+          TFS_CUDA_TRY(cudaMemcpyAsync(k.x, xs, 2 * sizeof(int64_t) * m.B, kind, s));
+        continue;
+      }
+      if (xs != k.x) TFS_CUDA_TRY(cudaMemcpyAsync(k.x, xs, sizeof(int64_t) * m.B, kind, s));
+      if (ys != k.y) TFS_CUDA_TRY(cudaMemcpyAsync(k.y, ys, sizeof(int64_t) * m.B, kind, s));
     }
   }
   if (st->exec) {

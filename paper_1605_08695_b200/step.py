@@ -251,6 +251,7 @@ class Step:
         the step and the D2H copy of each local rank's loss_sum into loss_host (pinned float32
         [nlocal]) all happen inside the C call, on the current stream."""
         assert not x_host.is_cuda and x_host.dtype == torch.int64
+        assert x_host.is_contiguous() and y_host.is_contiguous()
         io = _lib.StepIO()
         io.x, io.y = x_host.data_ptr(), y_host.data_ptr()
         io.host = 1
