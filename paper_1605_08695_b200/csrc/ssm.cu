@@ -78,7 +78,7 @@ static int32_t make_store_map(CUtensorMap* map, CUtensorMapDataType dt, int esiz
   return r == CUDA_SUCCESS ? TFS_OK : TFS_ERR_INVALID_ARGUMENT;
 }
 
-int tiles_of(int M, int N) { return (int)(cdiv(M, PM) * cdiv(N, BN)); }
+int tiles_of(int M, int N, int ct) { return (int)(cdiv(M, ct * BM) * cdiv(N, BN)); }
 
 int effective_split(int K, int ksplit) {
   const int kb = (int)cdiv(K, BK);
@@ -91,19 +91,20 @@ size_t part_floats(int M, int N, int ksplit) {
   return ksplit > 1 ? (size_t)ksplit * M * N : 0;
 }
 
+// ct: CTAs per tile of the launch (kSoftmaxCta / kStoreCta); each CTA loads bn / ct B rows.
 static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int K, int ksplit,
-                            int bn = BN) {
+                            int ct, int bn = BN) {
   if (M <= 0 || N <= 0 || K <= 0 || bn < 32 || bn > BN || bn % 32 != 0)
     return TFS_ERR_INVALID_ARGUMENT;
   int32_t rc = make_tmap(&p.ta, A, (uint64_t)M, (uint64_t)K, BM);
   if (rc != TFS_OK) return rc;
-  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, (uint32_t)(bn / kCta));
+  rc = make_tmap(&p.tb, B, (uint64_t)N, (uint64_t)K, (uint32_t)(bn / ct));
   if (rc != TFS_OK) return rc;
   p.M = M;
   p.N = N;
   p.K = K;
   p.bn = bn;
-  p.num_m = (int)cdiv(M, PM);
+  p.num_m = (int)cdiv(M, ct * BM);
   p.num_n = (int)cdiv(N, bn);
   p.kb_total = (int)cdiv(K, BK);
   ksplit = std::max(1, std::min(ksplit, p.kb_total));
@@ -117,47 +118,48 @@ static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int 
 }
 
 // As many pipeline stages as the widest B tile of the launch leaves room for (Params).
-template <int MODE>
+template <int MODE, int CT>
 static void stage_plan(Params& P) {
   int bmax = 0;
-  for (int i = 0; i < P.nprob; ++i) bmax = std::max(bmax, P.p[i].bn / kCta * BK * 2);
+  for (int i = 0; i < P.nprob; ++i) bmax = std::max(bmax, P.p[i].bn / CT * BK * 2);
   P.b_stride = (bmax + 1023) / 1024 * 1024;
   const int fixed = (MODE == kStats ? 0 : kEpiSmem) + kCbSmem + kBarBytes;
   P.stages =
       std::min<int>(kMaxStages, ((int)kSmemBytes - fixed) / (KSUB * (A_BYTES + P.b_stride)));
 }
 
-// groups: CTA groups (SMs / kCta) the persistent launch uses; <= 0: every SM.
-static int groups_or_all(int groups) {
-  const int all = num_sms() / kCta;
-  return groups > 0 ? std::min(groups, all) : all;
+// sms: the SMs a persistent launch may use (<= 0: every SM) -> its CTA groups of ct CTAs.
+static int groups_or_all(int sms, int ct) {
+  const int all = num_sms() / ct;
+  return sms > 0 ? std::max(1, std::min(sms / ct, all)) : all;
 }
 
 template <int MODE, bool LAB = false>
-static int32_t launch_params(Params P, int groups_req, cudaStream_t st) {
-  stage_plan<MODE>(P);
+static int32_t launch_params(Params P, int sms, cudaStream_t st) {
+  constexpr int CT = MODE == kStore ? kStoreCta : kSoftmaxCta;
+  stage_plan<MODE, CT>(P);
   static bool attr_done = false;
   if (!attr_done) {
-    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, LAB>,
+    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, LAB, CT>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmemBytes));
     attr_done = true;
   }
   // persistent: one CTA (or CTA pair: a cluster of 2 on one TPC) per SM (or per two SMs)
-  const int groups = std::min(P.total_units, groups_or_all(groups_req));
+  const int groups = std::min(P.total_units, groups_or_all(sms, CT));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(kCta * groups));
+  cfg.gridDim = dim3((unsigned)(CT * groups));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.x = CT;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = kCta > 1 ? 1 : 0;  // plain launch for single-CTA tiles
-  TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, LAB>, P));
+  cfg.numAttrs = CT > 1 ? 1 : 0;  // plain launch for single-CTA tiles
+  TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, LAB, CT>, P));
   launched();
   TFS_LAUNCH_CHECK();
   if (std::getenv("TFS_DEBUG_SYNC") != nullptr) {  // diagnostics: attribute faults to a mode
@@ -171,12 +173,12 @@ static int32_t launch_params(Params P, int groups_req, cudaStream_t st) {
   return TFS_OK;
 }
 
-int pick_bn(int M, int N, int groups_req) {
-  const int64_t groups = groups_or_all(groups_req);
+int pick_bn(int M, int N, int sms) {
+  const int64_t groups = groups_or_all(sms, kSoftmaxCta);
   int best = BN;
   int64_t best_cost = -1;
   for (int bn = BN; bn >= 128; bn -= 32) {
-    const int64_t tiles = cdiv(M, PM) * cdiv(N, bn);
+    const int64_t tiles = cdiv(M, kSoftmaxCta * BM) * cdiv(N, bn);
     const int64_t cost = cdiv(tiles, groups) * bn;
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
@@ -191,7 +193,7 @@ int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K
                              cudaStream_t st) {
   if (A.mn || B.mn) return TFS_ERR_INVALID_ARGUMENT;
   Params P{};
-  int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1, bn);
+  int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1, kSoftmaxCta, bn);
   if (rc != TFS_OK) return rc;
   P.nprob = 1;
   P.total_units = P.p[0].units;
@@ -215,7 +217,7 @@ int32_t launch_store(const Gemm* g, int count, int groups, cudaStream_t st) {
   P.total_units = 0;
   for (int i = 0; i < count; ++i) {
     Problem& p = P.p[i];
-    int32_t rc = fill_problem(p, g[i].A, g[i].B, g[i].M, g[i].N, g[i].K, g[i].ksplit);
+    int32_t rc = fill_problem(p, g[i].A, g[i].B, g[i].M, g[i].N, g[i].K, g[i].ksplit, kStoreCta);
     if (rc != TFS_OK) return rc;
     if (p.ksplit > 1) {
       if (g[i].part == nullptr || g[i].g != nullptr) return TFS_ERR_INVALID_ARGUMENT;
@@ -759,10 +761,11 @@ struct Bf16Ws {
 // Split-K plan for the backward pair (dW_s: M=S, K=B; dh: M=B, K=S; both N=d) run in one
 // persistent launch: aim for ~2 units per CTA pair of roughly equal k-block count.
 static void plan_backward(int64_t B, int64_t S, int32_t d, int* ks_dh, int* ks_dws) {
-  const int64_t t_dh = umma::tiles_of((int)B, d), t_dws = umma::tiles_of((int)S, d);
+  constexpr int ct = umma::kStoreCta;
+  const int64_t t_dh = umma::tiles_of((int)B, d, ct), t_dws = umma::tiles_of((int)S, d, ct);
   const int64_t kb_dh = cdiv(S, umma::BK), kb_dws = cdiv(B, umma::BK);
   const int64_t work = t_dh * kb_dh + t_dws * kb_dws;
-  const int64_t target = std::max<int64_t>(16, cdiv(work, 2 * (num_sms() / umma::kCta)));
+  const int64_t target = std::max<int64_t>(16, cdiv(work, 2 * (num_sms() / ct)));
   auto split = [&](int64_t kb) {
     if (kb <= target + target / 4) return 1;
     return (int)std::min<int64_t>(16, cdiv(kb, target));
@@ -801,7 +804,7 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, int64_t 
   x.part_dws = c.take<float>(umma::part_floats((int)S, d, ks_dws));
   x.cb = c.take<float>(Spad);
   x.sid = c.take<int32_t>(Spad);
-  x.nslabs = cdiv(std::max<int64_t>(B, 1), umma::PM) * umma::kCta * 4;
+  x.nslabs = cdiv(std::max<int64_t>(B, 1), umma::BM) * 4;  // GRAD: one CTA per 128-row tile
   x.colpart = c.take<float>((size_t)x.nslabs * Spad);
   x.Sp = Sp;
   x.Spad = Spad;
@@ -864,7 +867,7 @@ struct Bf16Plan {
   Bf16Ws w;
   umma::EpiParams ep;
   int bn, num_n;
-  int groups;  // CTA groups of the persistent GEMMs (0: every SM; tfs_ssm_args.sm_reserve)
+  int groups;  // SMs the persistent GEMMs may use (0: every SM; tfs_ssm_args.sm_reserve)
   bool bin;
 };
 
@@ -872,7 +875,7 @@ static void bf16_plan(const tfs_ssm_args* a, void* ws, Bf16Plan* p) {
   ws_layout(a->B, a->S, a->dim, TFS_BF16, a->vocab, nullptr, &p->w, ws);
   const bool hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) != 0;
   const bool label_in = (a->flags & TFS_LABEL_IN_CANDIDATES) != 0;
-  p->groups = a->sm_reserve > 0 ? std::max(1, num_sms() / umma::kCta - a->sm_reserve) : 0;
+  p->groups = a->sm_reserve > 0 ? std::max(2, num_sms() - a->sm_reserve) : 0;  // SMs
   p->bn = a->S > 0 ? umma::pick_bn((int)a->B, (int)a->S, p->groups) : umma::BN;
   p->num_n = (int)cdiv(a->S, p->bn);
   p->bin = (a->flags & TFS_BF16_OPERANDS) != 0;  // h, w_true, w_s given in bf16

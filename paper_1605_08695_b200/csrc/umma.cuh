@@ -33,24 +33,26 @@
 namespace tfs {
 namespace umma {
 
-#ifndef TFS_UMMA_CTAS
-#define TFS_UMMA_CTAS 1
+// CTAs per tile, per launch kind (the kernel's CT template parameter): the logits / gradient
+// passes run one CTA per 128 x bn tile; the grouped STORE GEMM runs CTA pairs (cta_group::2,
+// 256 x 256 tiles, each CTA loading half of B) -- measured round 2: STORE 53.2 -> 49.4 us at
+// X and 1148 -> 963 us at Z with pairs, while pairs slow STATS / GRAD (31.2 -> 34.5 us at X).
+#ifndef TFS_STORE_CTA
+#define TFS_STORE_CTA 2
 #endif
-constexpr int kCta = TFS_UMMA_CTAS;  // 1: one CTA per tile; 2: CTA pairs (cta_group::2)
-static_assert(kCta == 1 || kCta == 2, "kCta");
+constexpr int kSoftmaxCta = 1, kStoreCta = TFS_STORE_CTA;
+static_assert(kStoreCta == 1 || kStoreCta == 2, "kStoreCta");
 constexpr int BM = 128, BN = 256, BK = 64;      // BM: rows per CTA; BN: tile N
-constexpr int STAGES = kCta == 2 ? 6 : 4;       // stages at the widest tile (BN); a launch with
+constexpr int STAGES = 4;                       // stages at the widest tile (BN); a launch with
 constexpr int kMaxStages = 8;                   // narrower tiles / no staging fits more (Params)
 #ifndef TFS_KSUB
 #define TFS_KSUB 2
 #endif
 constexpr int KSUB = TFS_KSUB;                  // k-blocks per pipeline stage (one barrier each)
-constexpr int PM = kCta * BM;                   // rows per tile
-constexpr int BNC = BN / kCta;                  // B rows per CTA
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + kEpiWarps * 32;  // 384
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
-constexpr int B_BYTES = BNC * BK * 2;           // 32 KB (16 KB per CTA of a pair)
+constexpr int B_BYTES = BN * BK * 2;            // 32 KB (the widest single-CTA B stage)
 constexpr int kMNBox = 64;                      // MN-major TMA box: 64 elements (128 B) x BK rows
 constexpr int kMNBoxBytes = kMNBox * BK * 2;    // 8 KB
 constexpr int kTmemCols = 512;
@@ -68,14 +70,14 @@ constexpr size_t kSmemBytes =
 static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 
 // Instruction descriptor of tcgen05.mma.kind::f16: bf16 x bf16 -> f32, M = 256 (pair), N = n.
-__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int n = BN) {
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int n, int m) {
   return (1u << 4)                       // D format f32
          | (1u << 7)                     // A format bf16
          | (1u << 10)                    // B format bf16
          | ((a_mn ? 1u : 0u) << 15)      // A major (0 = K, 1 = MN)
          | ((b_mn ? 1u : 0u) << 16)      // B major
          | ((uint32_t)(n >> 3) << 17)    // N (multiple of 16)
-         | ((uint32_t)(PM >> 4) << 24);  // M
+         | ((uint32_t)(m >> 4) << 24);   // M (128 per CTA, 256 per pair)
 }
 
 enum Mode : int { kStats = 0, kGrad = 1, kStore = 2 };
@@ -104,7 +106,7 @@ struct EpiParams {
   int label_in;
   float* zlab;
   // GRAD: column sums of each warp's 32-row slab of the stored (bf16) G, one fp32 partial per
-  // (32-row slab, column): colpart[slab * colpart_ld + n] (slab = (m-tile * kCta + rank) * 4 +
+  // (32-row slab, column): colpart[slab * colpart_ld + n] (slab = (m-tile * CT + rank) * 4 +
   // lane quarter); db_s = their fixed-order sum (a small finalize pass).  nullptr: no sums.
   float* colpart;
   int64_t colpart_ld;
@@ -177,9 +179,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 // Pair variant: the completion goes to the LEADER CTA's mbarrier (peer bit cleared).
+template <int CT>
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
                                                  uint32_t leader_bar) {
-  if constexpr (kCta == 2) {
+  if constexpr (CT == 2) {
     asm volatile(
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
@@ -193,22 +196,25 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
         : "memory");
   }
 }
+template <int CT>
 __device__ __forceinline__ uint32_t cluster_ctarank() {
-  if constexpr (kCta == 1) return 0;
+  if constexpr (CT == 1) return 0;
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
+template <int CT>
 __device__ __forceinline__ void cluster_sync_all() {  // both CTAs of a pair (else the CTA)
-  if constexpr (kCta == 2)
+  if constexpr (CT == 2)
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                      : "memory");
   else
     __syncthreads();
 }
 // Arrive on the mbarrier at the same smem offset in the leader CTA (rank 0) of the pair.
+template <int CT>
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
-  if constexpr (kCta == 2) {
+  if constexpr (CT == 2) {
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(0));
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
@@ -268,18 +274,20 @@ __device__ __forceinline__ uint64_t operand_desc(bool mn, uint32_t base, int k16
   return mn ? desc_sw128(base + (uint32_t)k16 * 2048u, kMNBoxBytes, 1024)
             : desc_sw128(base + (uint32_t)k16 * 32u, 16, 1024);
 }
+template <int CT>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
                                           uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::%5.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "n"(kCta));
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "n"(CT));
 }
 // Arrive (once MMAs issued so far complete) on the mbarrier at this offset (in both CTAs of a
 // pair).
+template <int CT>
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
-  if constexpr (kCta == 2) {
+  if constexpr (CT == 2) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
         " [%0], %1;" ::"r"(smem_u32(bar)),
@@ -353,8 +361,9 @@ __device__ __forceinline__ void stage_row64(uint8_t* buf, int lane, const uint4 
 
 // LAB: the label-in-candidates epilogue (EpiParams::label_in), a separate instantiation so the
 // sampled-softmax kernels compile exactly as without it.
-template <int MODE, bool LAB = false>
+template <int MODE, bool LAB = false, int CT = 1>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Params P) {
+  constexpr int PM = CT * BM;  // rows per tile
   extern __shared__ __align__(1024) uint8_t smem[];
   const int STAGES = P.stages;
   const int B_BYTES = P.b_stride;
@@ -370,9 +379,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const EpiParams& ep = P.ep;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMAs)
+  const uint32_t rank = cluster_ctarank<CT>();  // 0 = leader (issues the MMAs)
   const bool leader = rank == 0;
-  const int pair = blockIdx.x / kCta, npairs = gridDim.x / kCta;  // tile-owning CTA groups
+  const int pair = blockIdx.x / CT, npairs = gridDim.x / CT;  // tile-owning CTA groups
 
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem) & 1023u) != 0) __trap();  // swizzled tiles need 1 KB alignment
@@ -382,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, kCta * kEpiWarps);  // leader: epilogue warps of both CTAs
+      mbar_init(tempty + a, CT * kEpiWarps);  // leader: epilogue warps of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < P.nprob; ++i) {
@@ -393,11 +402,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::%2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(kTmemCols), "n"(kCta));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::%0.sync.aligned;" ::"n"(kCta));
+                 "r"(kTmemCols), "n"(CT));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::%0.sync.aligned;" ::"n"(CT));
   }
   tc_fence_before();
-  cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+  cluster_sync_all<CT>();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -409,18 +418,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int u = pair; u < P.total_units; u += npairs) {
         const Unit t = decode_unit(P, u);
         const Problem& q = P.p[t.pi];
-        const int nh = t.nw / kCta;  // B rows this CTA holds
+        const int nh = t.nw / CT;  // B rows this CTA holds
         const int bboxes = q.b_mn ? (nh + kMNBox - 1) / kMNBox : 0;
         const uint32_t bbytes = q.b_mn ? (uint32_t)(bboxes * kMNBoxBytes)
-                                       : (uint32_t)((q.bn / kCta) * BK * 2);  // box: bn/kCta rows
+                                       : (uint32_t)((q.bn / CT) * BK * 2);  // box: bn/CT rows
         const int arow = t.mt * PM + (int)rank * BM;
         const int bcol = t.nt * q.bn + (int)rank * nh;
         for (int kb0 = t.kb0; kb0 < t.kb1; kb0 += KSUB) {
           const int ns = min(KSUB, t.kb1 - kb0);
           mbar_wait(empty + stage, phase ^ 1);
           // the leader's barrier (peer bit cleared)
-          const uint32_t fb = smem_u32(full + stage) & (kCta == 2 ? 0xFEFFFFFFu : 0xFFFFFFFFu);
-          if (leader) mbar_expect_tx(full + stage, kCta * ns * (A_BYTES + bbytes));
+          const uint32_t fb = smem_u32(full + stage) & (CT == 2 ? 0xFEFFFFFFu : 0xFFFFFFFFu);
+          if (leader) mbar_expect_tx(full + stage, CT * ns * (A_BYTES + bbytes));
           for (int sb = 0; sb < ns; ++sb) {
             const int kb = kb0 + sb;
             uint8_t* a = sA + (stage * KSUB + sb) * A_BYTES;
@@ -428,15 +437,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             if (q.a_mn) {
 #pragma unroll
               for (int i = 0; i < BM / kMNBox; ++i)
-                tma_load_2d_pair(a + i * kMNBoxBytes, &q.ta, arow + i * kMNBox, kb * BK, fb);
+                tma_load_2d_pair<CT>(a + i * kMNBoxBytes, &q.ta, arow + i * kMNBox, kb * BK, fb);
             } else {
-              tma_load_2d_pair(a, &q.ta, kb * BK, arow, fb);
+              tma_load_2d_pair<CT>(a, &q.ta, kb * BK, arow, fb);
             }
             if (q.b_mn) {
               for (int i = 0; i < bboxes; ++i)
-                tma_load_2d_pair(b + i * kMNBoxBytes, &q.tb, bcol + i * kMNBox, kb * BK, fb);
+                tma_load_2d_pair<CT>(b + i * kMNBoxBytes, &q.tb, bcol + i * kMNBox, kb * BK, fb);
             } else {
-              tma_load_2d_pair(b, &q.tb, kb * BK, bcol, fb);
+              tma_load_2d_pair<CT>(b, &q.tb, kb * BK, bcol, fb);
             }
           }
           if (++stage == STAGES) {
@@ -454,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int u = pair; u < P.total_units; u += npairs) {
         const Unit t = decode_unit(P, u);
         const bool amn = P.p[t.pi].a_mn != 0, bmn = P.p[t.pi].b_mn != 0;
-        const uint32_t idesc = make_idesc(amn, bmn, t.nw);
+        const uint32_t idesc = make_idesc(amn, bmn, t.nw, PM);
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -468,16 +477,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             const uint32_t b0 = smem_u32(sB + (stage * KSUB + sb) * B_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              umma_bf16(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
+              umma_bf16<CT>(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
                         (kb > t.kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit_pair(empty + stage);
+          umma_commit_pair<CT>(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(tfull + acc);
+        umma_commit_pair<CT>(tfull + acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -642,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                   *reinterpret_cast<const uint16_t*>(sb + r * 64 + ((k16 ^ ((r >> 1) & 3)) << 4) + e2);
               if (r < nrows) cs += __uint_as_float(gb << 16);
             }
-            const int64_t slab = ((int64_t)t.mt * kCta + rank) * 4 + quarter;
+            const int64_t slab = ((int64_t)t.mt * CT + rank) * 4 + quarter;
             ep.colpart[slab * ep.colpart_ld + col0 + lane] = cs;
           }
           ++nst;
@@ -719,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_leader(tempty + acc);  // the leader's barrier
+      if (lane == 0) mbar_arrive_leader<CT>(tempty + acc);  // the leader's barrier
       if (MODE == kStats && row_ok)
         ep.stats[(int64_t)row * ep.nparts + t.nt * 2 + half] = make_float2(run_m, run_s);
       acc ^= 1;
@@ -729,11 +738,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
   // Neither CTA may leave (or free TMEM) while its peer can still reach its smem / TMEM.
   tc_fence_before();
-  cluster_sync_all();
+  cluster_sync_all<CT>();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::%2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols), "n"(kCta));
+                 "r"(kTmemCols), "n"(CT));
   }
 }
 
@@ -761,17 +770,17 @@ struct Gemm {
 
 // Scratch size (floats) of the split partials of a GEMM.
 size_t part_floats(int M, int N, int ksplit);
-int tiles_of(int M, int N);
+int tiles_of(int M, int N, int ct);
 int effective_split(int K, int ksplit);
 
 // STATS / GRAD launch; for GRAD, G (bf16 [M x ldG], ldG % 8 == 0) receives the gradient.
 // bn: tile width along N (pick_bn); cb / sid must be readable up to num_n * bn + 256 columns.
-int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn, int groups,
+int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn, int sms,
                              EpiParams ep, uint16_t* G, int64_t ldG, cudaStream_t st);
 // Tile width for an M x N output of single-pass tiles: the multiple of 32 in [128, 256] that
 // minimises the makespan (rounds of tiles over the CTA groups x tile width).
-int pick_bn(int M, int N, int groups);
-int32_t launch_store(const Gemm* g, int count, int groups, cudaStream_t st);
+int pick_bn(int M, int N, int sms);
+int32_t launch_store(const Gemm* g, int count, int sms, cudaStream_t st);
 
 }  // namespace umma
 }  // namespace tfs
