@@ -2,8 +2,9 @@
 // status/diagnostic entry points.
 //
 // Both movers are HBM-bound row copies: one warp per row, 16-byte vector
-// accesses (a 512-wide fp32 row is 128 float4 = 4 per lane), two rows in flight per warp, and
-// a grid of 8 CTAs x 8 warps per SM so ~64 KB of loads are outstanding per SM.
+// accesses (a 512-wide fp32 row is 128 float4 = 4 per lane), two rows in flight per warp.  A
+// shared-memory-staged bulk-TMA Gather (gather_bulk_kernel) is kept as a measured alternative
+// (TFS_GATHER_BULK=1 builds; slower on B200, see there).
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -205,9 +206,154 @@ __global__ void stitch_word_kernel(const int64_t* __restrict__ positions,
   }
 }
 
+#ifndef TFS_GRID_PER_SM
+#define TFS_GRID_PER_SM 8
+#endif
 static int grid_for_rows(int64_t n, int rows_per_warp) {
   const int64_t blocks = cdiv(cdiv(n, rows_per_warp), 8);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 8ll * num_sms()));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)TFS_GRID_PER_SM * num_sms()));
+}
+
+// ---- Gather through bulk TMA (an A/B alternative, OFF in the product build) -------------------
+// Measured round 2 (profiles/r2_ab_gather_bulk.log, r2_ncu_gather_bulk_Z.txt): 2x SLOWER than the
+// register-staged kernel at Z (gather E 50 vs 25 us) and no faster at X.  The copies complete
+// at ~9 B/clk per SM whatever the ring depth (2 / 4 / 6 slots per warp: 76 / 50 / 54 us), with
+// DRAM at 15-19 % busy: one 2 KB cp.async.bulk per row is bound by the copy engine's per-request
+// rate, not by bytes in flight.  The register kernel keeps 2 rows x 2 KB per warp in flight and
+// is bound by the L2 -> SM traffic of the duplicated (Zipf) rows.
+// Each warp owns a contiguous run of `per` output rows and a ring of kGDepth row slots in shared
+// memory.  Lane r of a 32-row group reads id r (coalesced) and validates it; lane 0 then keeps
+// kGDepth rows in flight as cp.async.bulk copies (table row -> slot, completion on the slot's
+// mbarrier); the warp converts each landed row (fp32 -> bf16 RNE, or fp32 as is) with 16-byte
+// shared loads and writes it with coalesced stores, then refills the slot with the row kGDepth
+// ahead.  A single persistent wave (CTAs per SM from the occupancy calculator): 3 CTAs x 8 warps
+// x 4 slots x 2 KB = 192 KB of row loads in flight per SM at d = 512, with ~40 registers a
+// thread, where the register-staged kernel above held 4 KB per warp in registers.
+#ifndef TFS_GATHER_BULK
+#define TFS_GATHER_BULK 0  // 1: A/B builds only (tools/build_variant.py)
+#endif
+constexpr int kGDepth = 4;
+constexpr int kGWarps = 8;
+constexpr int kGMaxRowBytes = 4096;
+
+__host__ __device__ inline uint32_t gslot_bytes(int32_t dim) {
+  return ((uint32_t)dim * 4u + 127u) & ~127u;
+}
+constexpr int kGBarBytes = (kGWarps * kGDepth * 8 + 127) / 128 * 128;  // the slots' mbarriers
+inline size_t gather_bulk_smem(int32_t dim) {
+  return kGBarBytes + (size_t)kGWarps * kGDepth * gslot_bytes(dim);
+}
+
+template <bool BF16OUT>
+__global__ void __launch_bounds__(kGWarps * 32) gather_bulk_kernel(
+    const float* __restrict__ table, int64_t rows, int32_t dim, const int64_t* __restrict__ ids,
+    int64_t n, int64_t per, void* __restrict__ out, const float* __restrict__ table2,
+    float* __restrict__ out2, tfs_device_error* err) {
+  extern __shared__ __align__(128) uint8_t gsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rb = (uint32_t)dim * 4u, sb = gslot_bytes(dim);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(gsm) + warp * kGDepth;
+  uint8_t* ring = gsm + kGBarBytes + (size_t)warp * kGDepth * sb;
+  if (lane < kGDepth) bulk::init(bar + lane, 1);
+  bulk::fence_init();
+  __syncwarp();
+  const int n4 = dim >> 2;
+  const int64_t j0 = ((int64_t)blockIdx.x * kGWarps + warp) * per;
+  const int64_t j1 = min(n, j0 + per);
+  uint32_t q0 = 0;  // rows this warp has put through its ring (slot = q % depth, phase = q / depth)
+  for (int64_t c0 = j0; c0 < j1; c0 += 32) {
+    const int cnt = (int)min((int64_t)32, j1 - c0);
+    int64_t id = -1;
+    bool ok = false;
+    if (lane < cnt) {
+      id = __ldg(ids + c0 + lane);
+      ok = id >= 0 && id < rows;
+      if (!ok && id != -1) report_error(err, TFS_ERR_OUT_OF_RANGE, c0 + lane);
+      if (ok && table2 != nullptr) out2[c0 + lane] = __ldg(table2 + id);
+    }
+    const uint32_t okm = __ballot_sync(0xffffffffu, ok);
+    const int nok = __popc(okm);
+    // lane k: the position (in this group) of the k-th valid row
+    const int kth = lane < nok ? (int)__fns(okm, 0, lane + 1) : 0;
+    auto issue = [&](int k) {  // all lanes call (shuffles); lane 0 issues row k's copy
+      const int r = __shfl_sync(0xffffffffu, kth, k);
+      const int64_t idr = __shfl_sync(0xffffffffu, id, r);
+      if (lane == 0) {
+        const uint32_t q = q0 + (uint32_t)k, s = q % kGDepth;
+        bulk::fence_proxy();
+        bulk::expect_tx(bar + s, rb);
+        bulk::g2s(ring + s * sb, table + idr * dim, rb, bar + s);
+      }
+    };
+    for (int k = 0; k < min(kGDepth, nok); ++k) issue(k);
+    for (int k = 0; k < nok; ++k) {
+      const uint32_t q = q0 + (uint32_t)k, s = q % kGDepth;
+      bulk::wait(bar + s, (q / kGDepth) & 1u);
+      const int64_t j = c0 + __shfl_sync(0xffffffffu, kth, k);
+      const float4* src = reinterpret_cast<const float4*>(ring + s * sb);
+      for (int c = lane; c < n4; c += 32) {
+        const float4 v = src[c];
+        if (BF16OUT) {
+          uint2 p;
+          p.x = pack_bf16x2(v.x, v.y);
+          p.y = pack_bf16x2(v.z, v.w);
+          reinterpret_cast<uint2*>(out)[j * n4 + c] = p;
+        } else {
+          reinterpret_cast<float4*>(out)[j * n4 + c] = v;
+        }
+      }
+      __syncwarp();  // every lane has read slot s
+      if (k + kGDepth < nok) issue(k + kGDepth);
+    }
+    q0 += (uint32_t)nok;
+  }
+}
+
+// Launch the bulk gather when the rows qualify (dim % 4 == 0, 16-byte-aligned table and out,
+// rows <= 4 KB); returns false (nothing launched) otherwise.
+static bool launch_gather_bulk(const float* table, int64_t rows, int32_t dim,
+                               const int64_t* ids, int64_t n, void* out, bool bf,
+                               const float* table2, float* out2, tfs_device_error* err,
+                               cudaStream_t st, int32_t* rc) {
+  *rc = TFS_OK;
+  if (!TFS_GATHER_BULK || dim % 4 != 0 || (size_t)dim * 4 > (size_t)kGMaxRowBytes || (uintptr_t)table % 16 != 0 ||
+      (uintptr_t)out % 16 != 0)
+    return false;
+  const size_t smem = gather_bulk_smem(dim);
+  auto kern = bf ? gather_bulk_kernel<true> : gather_bulk_kernel<false>;
+  // CTAs per SM by (device, dtype, dim / 4); the kernel's smem limit is set once per device to
+  // the widest row's footprint (the attribute is per kernel, not per launch)
+  static int per_sm[8][2][kGMaxRowBytes / 16 + 1];
+  static bool attr_set[8][2];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 8) return false;
+  if (!attr_set[dev][bf ? 1 : 0]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gather_bulk_smem(kGMaxRowBytes / 4)) != cudaSuccess) {
+      *rc = TFS_ERR_CUDA;
+      set_last_error("gather_bulk_kernel attributes", cudaGetLastError());
+      return true;
+    }
+    attr_set[dev][bf ? 1 : 0] = true;
+  }
+  int& cps = per_sm[dev][bf ? 1 : 0][dim / 4];
+  if (cps == 0) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kGWarps * 32, smem);
+    cps = std::max(1, b);
+  }
+  const int64_t warps_cap = (int64_t)num_sms() * cps * kGWarps;
+  const int64_t per = std::max<int64_t>(1, cdiv(n, warps_cap));
+  const int grid = (int)std::max<int64_t>(1, cdiv(cdiv(n, per), kGWarps));
+  kern<<<grid, kGWarps * 32, smem, st>>>(table, rows, dim, ids, n, per, out, table2, out2, err);
+  ::tfs::launched();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_error("gather_bulk_kernel launch", e);
+    *rc = TFS_ERR_CUDA;
+  }
+  return true;
 }
 
 }  // namespace tfs
@@ -261,6 +407,10 @@ extern "C" int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int3
   const bool bf = out_dtype == TFS_BF16;
   const bool vec = (dim % 4 == 0) && ((uintptr_t)table % 16 == 0) &&
                    ((uintptr_t)out % (bf ? 8 : 16) == 0);
+  int32_t brc = TFS_OK;
+  if (launch_gather_bulk((const float*)table, rows, dim, ids, n, out, bf, nullptr, nullptr, err,
+                         st, &brc))
+    return brc;
   if (vec) {
     const int grid = grid_for_rows(n, 2);
     if (bf)
@@ -444,6 +594,9 @@ extern "C" int32_t tfs_gather2(const float* table, int64_t rows, int32_t dim, co
     if (rc != TFS_OK) return rc;
     return tfs_gather(table2, rows, 1, TFS_F32, ids, n, out2, TFS_F32, err, stream);
   }
+  int32_t brc = TFS_OK;
+  if (launch_gather_bulk(table, rows, dim, ids, n, out, bf, table2, out2, err, st, &brc))
+    return brc;
   const int grid = grid_for_rows(n, 2);
   if (bf)
     gather_vec4_kernel<true><<<grid, 256, 0, st>>>(table, rows, dim, ids, n, out, table2, out2,

@@ -867,102 +867,6 @@ __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int
   }
 }
 
-// Chunks per block of the second reduction level: 8 for short inputs (level A then reads its
-// slots in two rounds instead of four), 16 for long ones (level B walks fewer blocks of a
-// heavy segment).
-constexpr int kBlkLong = 16, kBlkShort = 8;
-constexpr int64_t kBlkShortMaxChunks = 2048;
-
-// Level A, one thread per (block of kBlk chunks, float4 column): the block's partial slots are
-// read in chunk order and every RUN of consecutive slots owned by the same segment is summed in
-// that order into the run's first slot (in place; the thread owns its block's slots of its
-// column).  A crossing segment then has one run per block it touches, starting at slot
-// 2 c0 + 1 (c0 = its first chunk) and at slot 2 kBlk b for every later block b.
-template <int kBlk>
-__global__ void __launch_bounds__(256) seg_cross_a_vec4_kernel(SegJob j, int64_t nchunks) {
-  const int n4 = j.dim >> 2;
-  const int64_t nblk = (nchunks + kBlk - 1) / kBlk;
-  const int64_t total = nblk * n4;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = e / n4;
-    const int c4 = (int)(e - b * n4);
-    const bool col0 = c4 == 0 && j.rows2 != nullptr;
-    const int64_t cb = b * kBlk, ce = min(nchunks, cb + kBlk);
-    int2 info[kBlk];
-#pragma unroll
-    for (int u = 0; u < kBlk; ++u)
-      info[u] = cb + u < ce ? __ldg(j.chunk_info + cb + u) : make_int2(-1, -1);
-    int cur = -1;
-    int64_t run_slot = -1;
-    D4 acc = D4{0.0, 0.0, 0.0, 0.0};
-    double acc2 = 0.0;
-#pragma unroll
-    for (int u0 = 0; u0 < kBlk; u0 += 4) {  // 8 slots' loads issued before their additions
-      D4 pc[8];
-      double p2[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int u = u0 + (q >> 1);
-        const int sg = (q & 1) ? info[u].y : info[u].x;
-        const int64_t slot = 2 * (cb + u) + (q & 1);
-        pc[q] = sg >= 0 ? reinterpret_cast<const D4*>(j.part + slot * j.dim)[c4]
-                        : D4{0.0, 0.0, 0.0, 0.0};
-        p2[q] = (sg >= 0 && col0) ? j.part2[slot] : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int u = u0 + (q >> 1);
-        const int sg = (q & 1) ? info[u].y : info[u].x;
-        if (sg < 0) continue;
-        if (sg != cur) {
-          if (cur >= 0) {
-            reinterpret_cast<D4*>(j.part + run_slot * j.dim)[c4] = acc;
-            if (col0) j.part2[run_slot] = acc2;
-          }
-          cur = sg;
-          run_slot = 2 * (cb + u) + (q & 1);
-          acc = D4{0.0, 0.0, 0.0, 0.0};
-          acc2 = 0.0;
-        }
-        add4(acc, pc[q]);
-        acc2 += p2[q];
-      }
-    }
-    if (cur >= 0) {
-      reinterpret_cast<D4*>(j.part + run_slot * j.dim)[c4] = acc;
-      if (col0) j.part2[run_slot] = acc2;
-    }
-  }
-}
-
-// Level B, one thread per (segment crossing a chunk boundary, float4 column): its run sums
-// added in block order, then T[key] = fl32(T - lr * sum) (apply) or written out.
-template <int OPT, int kBlk>
-__global__ void __launch_bounds__(256) seg_cross_b_vec4_kernel(SegJob j) {
-  const uint32_t ncross = *j.cross_count;
-  const int n4 = j.dim >> 2;
-  const int64_t total = (int64_t)ncross * n4;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = e / n4;
-    const int c4 = (int)(e - q * n4);
-    const uint32_t s = j.cross_list[q];
-    const int64_t c0 = j.seg_start[s] / j.chunk, c1 = (j.seg_start[s + 1] - 1) / j.chunk;
-    const int64_t b0 = c0 / kBlk, b1 = c1 / kBlk;
-    const bool col0 = c4 == 0 && j.rows2 != nullptr;
-    D4 acc = reinterpret_cast<const D4*>(j.part + (2 * c0 + 1) * j.dim)[c4];
-    double acc2 = col0 ? j.part2[2 * c0 + 1] : 0.0;
-#pragma unroll 8
-    for (int64_t bb = b0 + 1; bb <= b1; ++bb) {
-      const int64_t slot = 2 * bb * kBlk;
-      add4(acc, reinterpret_cast<const D4*>(j.part + slot * j.dim)[c4]);
-      if (col0) acc2 += j.part2[slot];
-    }
-    seg_finish_vec4<OPT>(j, s, c4, acc, c4 == 0, acc2);
-  }
-}
-
 // Scalar columns (any dim): same structure, one column per lane per 32-column block.
 __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
   const int lane = threadIdx.x & 31;
