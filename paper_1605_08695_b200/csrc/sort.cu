@@ -29,7 +29,10 @@ constexpr int kMaxBuckets = 256;
 // Sorted rows per window of the segmented sums: 32 for long inputs, 8 for short ones (more
 // windows in flight); scratch is sized for the smallest.
 constexpr int kChunk = 32;
-constexpr int kChunkMin = 8;
+#ifndef TFS_SEG_CHUNK_MIN
+#define TFS_SEG_CHUNK_MIN 8
+#endif
+constexpr int kChunkMin = TFS_SEG_CHUNK_MIN;
 #ifndef TFS_SEG_SHORT_N
 #define TFS_SEG_SHORT_N 40000  // below this many rows: 8-row windows
 #endif
@@ -596,7 +599,7 @@ __device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_afte
 constexpr int kWinBatch = 8;
 constexpr int kRunWin = 16;  // windows per level-1 block of a crossing segment
 
-template <int OPT>
+template <int OPT, bool WR>
 __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int c4, const D4& acc,
                                                 bool col0, double acc2);
 
@@ -634,7 +637,7 @@ __device__ __forceinline__ void sum_slots(const SegJob& j, int c4, int64_t n, Sl
 // arriver into the slot of the block's first piece.  Level 2: the last block to finish sums the
 // block partials in block order and finishes the segment (table update or written sum).  Fixed
 // order at both levels (R-16); arrival order only decides WHO adds, never the order.
-template <int OPT>
+template <int OPT, bool WR>
 __device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_t chunk,
                                           bool head_piece) {
   __shared__ int s_last;
@@ -666,7 +669,7 @@ __device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_
       D4 acc = D4{0.0, 0.0, 0.0, 0.0};
       double acc2 = 0.0;
       sum_slots(j, c4, w1 - w0 + 1, [&](int64_t q) { return slot_of(w0 + q); }, acc, acc2);
-      seg_finish_vec4<OPT>(j, s, c4, acc, c4 == 0, acc2);
+      seg_finish_vec4<OPT, WR>(j, s, c4, acc, c4 == 0, acc2);
     }
     return;
   }
@@ -694,17 +697,23 @@ __device__ __forceinline__ void cross_arrive(const SegJob& j, uint32_t s, int64_
     double acc2 = 0.0;
     sum_slots(j, c4, b1 - b0 + 1,
               [&](int64_t q) { return q == 0 ? 2 * c0 + 1 : 2 * (b0 + q) * kRunWin; }, acc, acc2);
-    seg_finish_vec4<OPT>(j, s, c4, acc, c4 == 0, acc2);
+    seg_finish_vec4<OPT, WR>(j, s, c4, acc, c4 == 0, acc2);
   }
 }
 static_assert(kChunk <= 32, "the window prologue maps row r of a window to lane r");
 #ifndef TFS_WIN_MINB
 #define TFS_WIN_MINB 4  // CTAs per SM the register budget must allow (128 regs at 4)
 #endif
-template <int OPT>
+// WR: write mode (sort_reduce / route_reduce: sums written out, j.table == nullptr) or apply.
+template <int OPT, bool WR>
 __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJob j) {
-  __shared__ uint32_t s_perm[kChunk], s_key[kChunk], s_seg[kChunk];
-  __shared__ uint32_t s_mask[3];
+  // The window's row program, built once by warp 0 (lane r = row r) and read by every column
+  // thread as broadcast shared loads: the gradient row's float offset (-1: skipped row), its
+  // companion offset, the table row's float offset when a whole segment ends at r (apply mode),
+  // and the flags below.  The column loop then runs branch-uniform with no index arithmetic.
+  enum : uint32_t { kReset = 1, kPieceEnd = 2, kWhole = 4, kHeadSlot = 8 };
+  __shared__ int64_t s_off[kChunk], s_off2[kChunk], s_toff[kChunk];
+  __shared__ uint32_t s_key[kChunk], s_seg[kChunk], s_fl[kChunk];
   __shared__ int s_edge[2];
   const int64_t chunk = blockIdx.x;
   const int64_t base = chunk * j.chunk;
@@ -712,18 +721,12 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
   const int tid = threadIdx.x;
   if (tid < 32) {
     const int lane = tid;
-    uint32_t key_l = 0, seg_l = 0;
-    for (int r = lane; r < j.chunk; r += 32) {
-      if (r < cnt) {
-        const uint32_t pr = j.perm[base + r];
-        s_perm[r] = pr;
-        key_l = j.keys[base + r];
-        seg_l = j.seg_of[base + r];
-        s_key[r] = key_l;
-        s_seg[r] = seg_l;
-      }
+    uint32_t key_l = 0xffffffffu, seg_l = 0, perm_l = 0;
+    if (lane < cnt) {
+      perm_l = j.perm[base + lane];
+      key_l = j.keys[base + lane];
+      seg_l = j.seg_of[base + lane];
     }
-    // (kChunk == 32: lane r holds row r's key)
     uint32_t edge = 0;
     if (lane == 0 && base > 0) edge = j.keys[base - 1] == j.keys[base];
     if (lane == 1 && base + cnt < j.n) edge = j.keys[base + cnt] == j.keys[base + cnt - 1];
@@ -732,14 +735,23 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
     const uint32_t key_prev = __shfl_up_sync(0xffffffffu, key_l, 1);
     const bool head_l = lane < cnt && (lane == 0 ? !first_before : key_l != key_prev);
     const uint32_t H = __ballot_sync(0xffffffffu, head_l);
-    const bool end_l = lane < cnt && (lane == cnt - 1 ? !last_after : ((H >> (lane + 1)) & 1));
-    const uint32_t E = __ballot_sync(0xffffffffu, end_l);
-    const bool whole_l = end_l && (H & ((2u << lane) - 1u)) != 0 && key_l < j.invalid_key;
-    const uint32_t WE = __ballot_sync(0xffffffffu, whole_l);
+    const bool valid_l = lane < cnt && key_l < j.invalid_key;
+    // the piece holding row r starts at the last head <= r (row 0 if none: it started before)
+    const uint32_t upto = H & ((2u << lane) - 1u);
+    const bool starts_before = upto == 0;  // (implies first_before)
+    const bool piece_end = lane < cnt && (lane == cnt - 1 || ((H >> (lane + 1)) & 1));
+    const bool ends_after = lane == cnt - 1 && last_after;
+    const bool whole = piece_end && !starts_before && !ends_after;
+    uint32_t fl = 0;
+    if (lane > 0 && lane < cnt && ((H >> lane) & 1)) fl |= kReset;
+    if (valid_l && piece_end) fl |= kPieceEnd | (whole ? kWhole : 0) | (starts_before ? kHeadSlot : 0);
+    s_fl[lane] = fl;
+    s_key[lane] = key_l;
+    s_seg[lane] = seg_l;
+    s_off[lane] = valid_l ? row_off(j, perm_l) : -1;
+    s_off2[lane] = (valid_l && j.rows2) ? row2_off(j, perm_l) : -1;
+    s_toff[lane] = (!WR && valid_l && whole) ? (int64_t)key_l * j.dim : -1;
     if (lane == 0) {
-      s_mask[0] = H;
-      s_mask[1] = E;
-      s_mask[2] = WE;
       s_edge[0] = first_before;
       s_edge[1] = last_after;
     }
@@ -759,15 +771,13 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
   // Sorted keys put skipped entries (padding slots, bad ids: key >= invalid_key) last, so a
   // window whose first key is invalid has nothing to do, and no invalid row is ever loaded.
   if (s_key[0] >= j.invalid_key) return;
-  const uint32_t H = s_mask[0], E = s_mask[1], WE = s_mask[2];
   const bool first_before = s_edge[0] != 0, last_after = s_edge[1] != 0;
-  const bool write_mode = j.table == nullptr;
   const int n4 = j.dim >> 2;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int c4 = tid; c4 < n4; c4 += blockDim.x) {
     const bool col0 = c4 == 0;
     D4 acc = D4{0.0, 0.0, 0.0, 0.0};
     double acc2 = 0.0;
-    int r_start = 0;
     // Rows in half-batches of kHalf, software-pipelined: the loads of half-batch h + 1 (its
     // gradient rows and the table rows of the whole segments ending in it) are in flight while
     // half-batch h is summed and applied.
@@ -778,14 +788,17 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
 #pragma unroll
       for (int q = 0; q < kHalf; ++q) {
         const int r = hb * kHalf + q;
-        const bool valid = r < cnt && s_key[r] < j.invalid_key;
-        x[buf][q] = valid ? __ldg((const float4*)(j.rows + row_off(j, s_perm[r])) + c4)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-        r2v[buf][q] =
-            (valid && col0 && j.rows2) ? __ldg(j.rows2 + row2_off(j, s_perm[r])) : 0.f;
-        t[buf][q] = (!write_mode && r < cnt && ((WE >> r) & 1))
-                        ? *((const float4*)(j.table + (int64_t)s_key[r] * j.dim) + c4)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int64_t o = s_off[r];
+        x[buf][q] = o >= 0 ? __ldg(reinterpret_cast<const float4*>(j.rows + o) + c4) : z4;
+        r2v[buf][q] = 0.f;
+        if (col0) {
+          const int64_t o2 = s_off2[r];
+          if (o2 >= 0) r2v[buf][q] = __ldg(j.rows2 + o2);
+        }
+        if (!WR) {
+          const int64_t to = s_toff[r];
+          t[buf][q] = to >= 0 ? *(reinterpret_cast<const float4*>(j.table + to) + c4) : z4;
+        }
       }
     };
     auto proc_half = [&](int hb, int buf) {
@@ -793,23 +806,19 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
       for (int q = 0; q < kHalf; ++q) {
         const int r = hb * kHalf + q;
         if (r >= cnt) break;
-        if (r > 0 && ((H >> r) & 1)) {
+        const uint32_t f = s_fl[r];
+        if (f & kReset) {
           acc = D4{0.0, 0.0, 0.0, 0.0};
           acc2 = 0.0;
-          r_start = r;
         }
         add4(acc, x[buf][q]);
         acc2 += r2v[buf][q];
-        if (!(((E >> r) & 1) || r == cnt - 1)) continue;
-        // ---- the piece [r_start, r] is complete
-        const uint32_t kr = s_key[r];
-        if (kr >= j.invalid_key) continue;
-        const uint32_t sg = s_seg[r];
-        const bool starts_before = r_start == 0 && first_before;
-        const bool ends_after = r == cnt - 1 && last_after;
-        if (!starts_before && !ends_after) {  // whole segment: apply / write now
-          if (write_mode) {
-            const OutPos op = seg_out_pos(j, sg, kr);
+        if (!(f & kPieceEnd)) continue;
+        // ---- the piece ending at row r is complete
+        if (f & kWhole) {  // whole segment: apply / write now
+          const uint32_t kr = s_key[r];
+          if (WR) {
+            const OutPos op = seg_out_pos(j, s_seg[r], kr);
             if (op.row != nullptr) {
               reinterpret_cast<float4*>(op.row)[c4] = to_f4(acc);
               if (col0) {
@@ -818,12 +827,12 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
               }
             }
           } else {
-            *((float4*)(j.table + (int64_t)kr * j.dim) + c4) =
+            *(reinterpret_cast<float4*>(j.table + s_toff[r]) + c4) =
                 opt_step4<OPT>(j, t[buf][q], acc, kr, c4);
             if (j.table2 && col0) opt_step2<OPT>(j, kr, acc2);
           }
         } else {
-          const int64_t slot = starts_before ? 2 * chunk : 2 * chunk + 1;
+          const int64_t slot = (f & kHeadSlot) ? 2 * chunk : 2 * chunk + 1;
           reinterpret_cast<D4*>(j.part + slot * j.dim)[c4] = acc;
           if (col0 && j.rows2) j.part2[slot] = acc2;
         }
@@ -841,18 +850,18 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
   // Pieces of segments crossing this window's edges (at most two: the one that started before
   // it and the one that continues after it): arrive, and the last arriver of a level sums it.
   const uint32_t kf = s_key[0], kl = s_key[cnt - 1];
-  if (first_before && kf < j.invalid_key) cross_arrive<OPT>(j, s_seg[0], chunk, true);
+  if (first_before && kf < j.invalid_key) cross_arrive<OPT, WR>(j, s_seg[0], chunk, true);
   if (last_after && kl < j.invalid_key && !(first_before && s_seg[cnt - 1] == s_seg[0]))
-    cross_arrive<OPT>(j, s_seg[cnt - 1], chunk, false);
+    cross_arrive<OPT, WR>(j, s_seg[cnt - 1], chunk, false);
 }
 
 // A segment whose pieces are all summed: T[key] = fl32(T - lr * g) (apply) or written out.
-template <int OPT>
+template <int OPT, bool WR>
 __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int c4, const D4& acc,
                                                 bool col0, double acc2) {
   const uint32_t key = j.keys[j.seg_start[s]];
   if (key >= j.invalid_key) return;
-  if (j.table == nullptr) {
+  if (WR) {
     const OutPos op = seg_out_pos(j, s, key);
     if (op.row == nullptr) return;
     reinterpret_cast<float4*>(op.row)[c4] = to_f4(acc);
@@ -1316,8 +1325,11 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
   if (vec) {  // one launch: windows + the fused crossing reduction (cross_arrive)
     const int64_t n4 = j.dim >> 2;
     const int wthreads = (int)std::min<int64_t>(128, cdiv(n4, 32) * 32);
-    auto win_k = j.opt == 1 ? seg_window_vec4_kernel<1>
-                            : (j.opt == 2 ? seg_window_vec4_kernel<2> : seg_window_vec4_kernel<0>);
+    const bool wr = j.table == nullptr;
+    auto win_k = j.opt == 1   ? seg_window_vec4_kernel<1, false>
+                 : j.opt == 2 ? seg_window_vec4_kernel<2, false>
+                 : wr         ? seg_window_vec4_kernel<0, true>
+                              : seg_window_vec4_kernel<0, false>;
     win_k<<<(unsigned)nchunks, wthreads, 0, st>>>(j);
     launched();
   } else {
