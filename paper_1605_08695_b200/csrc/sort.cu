@@ -28,7 +28,10 @@ constexpr int kSortTile = kSortThreads * kSortItems;  // 1024 items per CTA
 constexpr int kMaxBuckets = 256;
 // Sorted rows per window of the segmented sums: 32 for long inputs, 8 for short ones (more
 // windows in flight); scratch is sized for the smallest.
-constexpr int kChunk = 32;
+#ifndef TFS_SEG_CHUNK
+#define TFS_SEG_CHUNK 32
+#endif
+constexpr int kChunk = TFS_SEG_CHUNK;
 #ifndef TFS_SEG_CHUNK_MIN
 #define TFS_SEG_CHUNK_MIN 8
 #endif
@@ -712,8 +715,8 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
   // companion offset, the table row's float offset when a whole segment ends at r (apply mode),
   // and the flags below.  The column loop then runs branch-uniform with no index arithmetic.
   enum : uint32_t { kReset = 1, kPieceEnd = 2, kWhole = 4, kHeadSlot = 8 };
-  __shared__ int64_t s_off[kChunk], s_off2[kChunk], s_toff[kChunk];
-  __shared__ uint32_t s_key[kChunk], s_seg[kChunk], s_fl[kChunk];
+  __shared__ int64_t s_off[32], s_off2[32], s_toff[32];  // one entry per lane of warp 0
+  __shared__ uint32_t s_key[32], s_seg[32], s_fl[32];
   __shared__ int s_edge[2];
   const int64_t chunk = blockIdx.x;
   const int64_t base = chunk * j.chunk;
