@@ -7,6 +7,8 @@
 #include <stdint.h>
 #include <stddef.h>
 
+#include <utility>
+
 #include "../../include/tfs.h"
 
 namespace tfs {
@@ -93,6 +95,39 @@ __device__ __forceinline__ float bf16_round(float x) {
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // one cvt.rn.bf16x2.f32; lo in bits 0-15
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ---- programmatic dependent launch (PDL) ---------------------------------------------------------
+// Every kernel of the library is launched with programmatic stream serialization and opens with
+// pdl_enter(), which waits (griddepcontrol.wait) until the PREVIOUS grid on the stream has
+// completed and its memory is visible before touching any data: results are those of plain
+// stream order, and the next grid's launch is processed while the previous one drains (inside
+// CUDA graphs too).  Measured round 2 (profiles/r2_ab_pdl.log): X step 192 -> 183 us, Z neutral.
+// An explicit early trigger (griddepcontrol.launch_dependents at kernel start, TFS_PDL_TRIGGER=1
+// builds) is SLOWER (X 215 us, Z +8 %): the early-scheduled CTAs sit on SMs while they wait and
+// crowd out the side streams' kernels.  TFS_PDL=0 in the environment turns PDL off.
+#ifndef TFS_PDL_TRIGGER
+#define TFS_PDL_TRIGGER 0
+#endif
+__device__ __forceinline__ void pdl_enter() {
+  if (TFS_PDL_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ---- bulk (non-tensor) TMA copies into shared memory, completed on an mbarrier -----------------

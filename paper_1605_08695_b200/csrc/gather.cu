@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -45,6 +46,14 @@ int32_t device_supported() {
   return cached[dev];
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TFS_PDL");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 int num_sms() {
   static int cached[64] = {0};
   int dev = 0;
@@ -68,6 +77,7 @@ __global__ void __launch_bounds__(256) gather_vec4_kernel(const float* __restric
                                                           const float* __restrict__ table2,
                                                           float* __restrict__ out2,
                                                           tfs_device_error* err) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int n4 = dim >> 2;
   const int64_t nwarps = (int64_t)gridDim.x * 8;
@@ -122,6 +132,7 @@ template <bool BF16OUT>
 __global__ void gather_scalar_kernel(const float* __restrict__ table, int64_t rows, int32_t dim,
                                      const int64_t* __restrict__ ids, int64_t n,
                                      void* __restrict__ out, tfs_device_error* err) {
+  pdl_enter();
   const int64_t total = n * dim;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -143,6 +154,7 @@ __global__ void gather_scalar_kernel(const float* __restrict__ table, int64_t ro
 // Stitch: out[positions[j]] = rows[j].  With validation, claim[p] = min j claiming p.
 __global__ void stitch_claim_kernel(const int64_t* positions, int64_t n,
                                     unsigned long long* claim, tfs_device_error* err) {
+  pdl_enter();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = positions[j];
@@ -159,6 +171,7 @@ __global__ void __launch_bounds__(256) stitch_vec4_kernel(const int64_t* __restr
                                                           uint4* __restrict__ out,
                                                           const unsigned long long* claim,
                                                           tfs_device_error* err) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * 8;
   for (int64_t j = blockIdx.x * 8 + (threadIdx.x >> 5); j < n; j += nwarps) {
@@ -191,6 +204,7 @@ __global__ void stitch_word_kernel(const int64_t* __restrict__ positions,
                                    const uint32_t* __restrict__ rows, int64_t n,
                                    int64_t row_words, uint32_t* __restrict__ out,
                                    const unsigned long long* claim, tfs_device_error* err) {
+  pdl_enter();
   const int64_t total = n * row_words;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -249,6 +263,7 @@ __global__ void __launch_bounds__(kGWarps * 32) gather_bulk_kernel(
     const float* __restrict__ table, int64_t rows, int32_t dim, const int64_t* __restrict__ ids,
     int64_t n, int64_t per, void* __restrict__ out, const float* __restrict__ table2,
     float* __restrict__ out2, tfs_device_error* err) {
+  pdl_enter();
   extern __shared__ __align__(128) uint8_t gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rb = (uint32_t)dim * 4u, sb = gslot_bytes(dim);
@@ -346,7 +361,7 @@ static bool launch_gather_bulk(const float* table, int64_t rows, int32_t dim,
   const int64_t warps_cap = (int64_t)num_sms() * cps * kGWarps;
   const int64_t per = std::max<int64_t>(1, cdiv(n, warps_cap));
   const int grid = (int)std::max<int64_t>(1, cdiv(cdiv(n, per), kGWarps));
-  kern<<<grid, kGWarps * 32, smem, st>>>(table, rows, dim, ids, n, per, out, table2, out2, err);
+  ::tfs::launch(kern, grid, kGWarps * 32, smem, st, table, rows, dim, ids, n, per, out, table2, out2, err);
   ::tfs::launched();
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -414,17 +429,17 @@ extern "C" int32_t tfs_gather(const void* table, int64_t rows, int32_t dim, int3
   if (vec) {
     const int grid = grid_for_rows(n, 2);
     if (bf)
-      gather_vec4_kernel<true><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out,
+      ::tfs::launch(gather_vec4_kernel<true>, grid, 256, 0, st, (const float*)table, rows, dim, ids, n, out,
                                                      nullptr, nullptr, err);
     else
-      gather_vec4_kernel<false><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out,
+      ::tfs::launch(gather_vec4_kernel<false>, grid, 256, 0, st, (const float*)table, rows, dim, ids, n, out,
                                                       nullptr, nullptr, err);
   } else {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * dim, 256), 8ll * num_sms()));
     if (bf)
-      gather_scalar_kernel<true><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
+      ::tfs::launch(gather_scalar_kernel<true>, grid, 256, 0, st, (const float*)table, rows, dim, ids, n, out, err);
     else
-      gather_scalar_kernel<false><<<grid, 256, 0, st>>>((const float*)table, rows, dim, ids, n, out, err);
+      ::tfs::launch(gather_scalar_kernel<false>, grid, 256, 0, st, (const float*)table, rows, dim, ids, n, out, err);
   }
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
@@ -442,6 +457,7 @@ __global__ void __launch_bounds__(256) gather_slots_kernel(const float* __restri
                                                            int64_t n, float* __restrict__ out,
                                                            int64_t out_stride,
                                                            tfs_device_error* err) {
+  pdl_enter();
   const int cols = VEC ? dim >> 2 : dim;
   const int64_t total = n * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -477,10 +493,10 @@ extern "C" int32_t tfs_gather_slots(const float* table, int64_t rows, int32_t di
   const int64_t total = n * (vec ? dim / 4 : dim);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 8ll * num_sms()));
   if (vec)
-    gather_slots_kernel<true><<<grid, 256, 0, st>>>(table, rows, dim, ids, ids_stride, cap, n, out,
+    ::tfs::launch(gather_slots_kernel<true>, grid, 256, 0, st, table, rows, dim, ids, ids_stride, cap, n, out,
                                                    out_stride, err);
   else
-    gather_slots_kernel<false><<<grid, 256, 0, st>>>(table, rows, dim, ids, ids_stride, cap, n,
+    ::tfs::launch(gather_slots_kernel<false>, grid, 256, 0, st, table, rows, dim, ids, ids_stride, cap, n,
                                                     out, out_stride, err);
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
@@ -499,6 +515,7 @@ __global__ void __launch_bounds__(256) gather_peers_kernel(const float* const* _
                                                            const float* const* __restrict__ shards2,
                                                            float* __restrict__ out2,
                                                            tfs_device_error* err) {
+  pdl_enter();
   const int cols = VEC ? dim >> 2 : dim;
   const int64_t total = n * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -546,7 +563,7 @@ extern "C" int32_t tfs_gather_peers(const float* const* shards, int64_t shard_ro
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
   auto k = vec ? (bf ? gather_peers_kernel<true, true> : gather_peers_kernel<true, false>)
                : (bf ? gather_peers_kernel<false, true> : gather_peers_kernel<false, false>);
-  k<<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab, num_shards, out, nullptr,
+  ::tfs::launch(k, grid, 256, 0, st, shards, shard_rows, dim, ids, n, vocab, num_shards, out, nullptr,
                           nullptr, err);
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
@@ -570,7 +587,7 @@ extern "C" int32_t tfs_gather_peers2(const float* const* shards, int64_t shard_r
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
   auto k = vec ? (bf ? gather_peers_kernel<true, true> : gather_peers_kernel<true, false>)
                : (bf ? gather_peers_kernel<false, true> : gather_peers_kernel<false, false>);
-  k<<<grid, 256, 0, st>>>(shards, shard_rows, dim, ids, n, vocab, num_shards, out, shards2, out2,
+  ::tfs::launch(k, grid, 256, 0, st, shards, shard_rows, dim, ids, n, vocab, num_shards, out, shards2, out2,
                           err);
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
@@ -599,10 +616,10 @@ extern "C" int32_t tfs_gather2(const float* table, int64_t rows, int32_t dim, co
     return brc;
   const int grid = grid_for_rows(n, 2);
   if (bf)
-    gather_vec4_kernel<true><<<grid, 256, 0, st>>>(table, rows, dim, ids, n, out, table2, out2,
+    ::tfs::launch(gather_vec4_kernel<true>, grid, 256, 0, st, table, rows, dim, ids, n, out, table2, out2,
                                                    err);
   else
-    gather_vec4_kernel<false><<<grid, 256, 0, st>>>(table, rows, dim, ids, n, out, table2, out2,
+    ::tfs::launch(gather_vec4_kernel<false>, grid, 256, 0, st, table, rows, dim, ids, n, out, table2, out2,
                                                     err);
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
@@ -627,16 +644,16 @@ extern "C" int32_t tfs_stitch(const int64_t* positions, const void* rows, int64_
     claim = (unsigned long long*)ws;
     TFS_CUDA_TRY(cudaMemsetAsync(claim, 0xff, sizeof(unsigned long long) * n, st));
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4ll * num_sms()));
-    stitch_claim_kernel<<<g, 256, 0, st>>>(positions, n, claim, err); ::tfs::launched();
+    ::tfs::launch(stitch_claim_kernel, g, 256, 0, st, positions, n, claim, err); ::tfs::launched();
   }
   const bool vec = row_bytes % 16 == 0 && ((uintptr_t)rows % 16 == 0) && ((uintptr_t)out % 16 == 0);
   if (vec) {
-    stitch_vec4_kernel<<<grid_for_rows(n, 1), 256, 0, st>>>(
+    ::tfs::launch(stitch_vec4_kernel, grid_for_rows(n, 1), 256, 0, st, 
         positions, (const uint4*)rows, n, row_bytes / 16, (uint4*)out, claim, err); ::tfs::launched();
   } else {
     const int64_t words = row_bytes / 4;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * words, 256), 8ll * num_sms()));
-    stitch_word_kernel<<<g, 256, 0, st>>>(positions, (const uint32_t*)rows, n, words,
+    ::tfs::launch(stitch_word_kernel, g, 256, 0, st, positions, (const uint32_t*)rows, n, words,
                                           (uint32_t*)out, claim, err); ::tfs::launched();
   }
   TFS_LAUNCH_CHECK();

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(256) sample_draw_kernel(const uint64_t* thr, i
                                                           uint32_t replica, int unique,
                                                           int32_t* draws, int32_t* firstpos,
                                                           int64_t* out_direct) {
+  pdl_enter();
   __shared__ int32_t hot[kHotIds];
   if (step_dev != nullptr) step = *step_dev;
   if (unique) {
@@ -125,6 +126,7 @@ __device__ __forceinline__ uint32_t cta_exclusive_scan(uint32_t v, uint32_t* tot
 __global__ void __launch_bounds__(kSelThreads) sample_count_kernel(const int32_t* draws,
                                                                    const int32_t* firstpos,
                                                                    int64_t N, uint32_t* blk_cnt) {
+  pdl_enter();
   const int64_t base = (int64_t)blockIdx.x * kSelTile + threadIdx.x * kSelItems;
   uint32_t c = 0;
 #pragma unroll
@@ -140,6 +142,7 @@ __global__ void __launch_bounds__(kSelThreads) sample_count_kernel(const int32_t
 __global__ void __launch_bounds__(kSelThreads) sample_select_kernel(
     const int32_t* draws, const int32_t* firstpos, int64_t N, const uint32_t* blk_cnt, int nblk,
     int32_t S, int64_t* out_sampled, int64_t* out_num_tries, tfs_device_error* err) {
+  pdl_enter();
   __shared__ uint32_t s_pre, s_all;
   if (threadIdx.x < 32) {
     uint32_t pre = 0, all = 0;
@@ -200,6 +203,7 @@ __global__ void sample_finish_kernel(const int32_t* draws, int32_t* firstpos, in
                                      const int64_t* out_sampled, const int64_t* labels,
                                      int64_t n_labels, const int64_t* num_tries, float* les,
                                      float* ley, tfs_device_error* err) {
+  pdl_enter();
   const int64_t T = unique ? *num_tries : (int64_t)S;
   const int64_t nl = (int64_t)S + n_labels;
   const int64_t total = (unique && N > nl) ? N : nl;
@@ -223,7 +227,8 @@ __global__ void sample_finish_kernel(const int32_t* draws, int32_t* firstpos, in
   }
 }
 
-__global__ void set_i64_kernel(int64_t* p, int64_t v) { *p = v; }
+__global__ void set_i64_kernel(int64_t* p, int64_t v) {
+  pdl_enter(); *p = v; }
 
 // Commit of a sample drawn ahead of time: copy (s, log ec(s), T) into the step's buffers and
 // form the labels' log expected counts with that T.
@@ -232,6 +237,7 @@ __global__ void sample_commit_kernel(int64_t V, double log_v1, int unique, int32
                                      const int64_t* T_in, const int64_t* labels, int64_t n_labels,
                                      int64_t* s_out, float* les_out, float* ley_out,
                                      int64_t* T_out, tfs_device_error* err) {
+  pdl_enter();
   const int64_t T = unique ? *T_in : (int64_t)S;
   const int64_t total = (int64_t)S + n_labels;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -333,12 +339,12 @@ extern "C" int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int3
   SamplerState s = carve_state((void*)state, vocab);
   const double log_v1 = std::log((double)vocab + 1.0);
   if (num_sampled == 0) {
-    set_i64_kernel<<<1, 1, 0, st>>>(out_num_tries, 0); ::tfs::launched();
+    ::tfs::launch(set_i64_kernel, 1, 1, 0, st, out_num_tries, 0); ::tfs::launched();
   } else if (!unique) {
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(num_sampled, 256), 4 * num_sms()));
-    sample_draw_kernel<<<g, 256, 0, st>>>(s.thr, vocab, log_v1, num_sampled, seed, step, step_dev, replica,
+    ::tfs::launch(sample_draw_kernel, g, 256, 0, st, s.thr, vocab, log_v1, num_sampled, seed, step, step_dev, replica,
                                           0, nullptr, nullptr, out_sampled); ::tfs::launched();
-    set_i64_kernel<<<1, 1, 0, st>>>(out_num_tries, num_sampled); ::tfs::launched();
+    ::tfs::launch(set_i64_kernel, 1, 1, 0, st, out_num_tries, num_sampled); ::tfs::launched();
   } else {
     if (ws_bytes < tfs_sampler_workspace_bytes(max_draws)) return TFS_ERR_WORKSPACE_TOO_SMALL;
     Carver c(ws, ws_bytes);
@@ -346,15 +352,15 @@ extern "C" int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int3
     const int nblk = (int)cdiv(max_draws, kSelTile);
     uint32_t* blk = c.take<uint32_t>(nblk + 1);
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(max_draws, 256), num_sms()));
-    sample_draw_kernel<<<g, 256, 0, st>>>(s.thr, vocab, log_v1, max_draws, seed, step, step_dev, replica,
+    ::tfs::launch(sample_draw_kernel, g, 256, 0, st, s.thr, vocab, log_v1, max_draws, seed, step, step_dev, replica,
                                           1, draws, s.firstpos, nullptr); ::tfs::launched();
-    sample_count_kernel<<<nblk, kSelThreads, 0, st>>>(draws, s.firstpos, max_draws, blk); ::tfs::launched();
-    sample_select_kernel<<<nblk, kSelThreads, 0, st>>>(draws, s.firstpos, max_draws, blk, nblk,
+    ::tfs::launch(sample_count_kernel, nblk, kSelThreads, 0, st, draws, s.firstpos, max_draws, blk); ::tfs::launched();
+    ::tfs::launch(sample_select_kernel, nblk, kSelThreads, 0, st, draws, s.firstpos, max_draws, blk, nblk,
                                                        num_sampled, out_sampled, out_num_tries, err); ::tfs::launched();
     TFS_LAUNCH_CHECK();
     const int64_t total = std::max<int64_t>(max_draws, num_sampled + n_labels);
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 4 * num_sms()));
-    sample_finish_kernel<<<g2, 256, 0, st>>>(draws, s.firstpos, max_draws, 1, vocab, log_v1,
+    ::tfs::launch(sample_finish_kernel, g2, 256, 0, st, draws, s.firstpos, max_draws, 1, vocab, log_v1,
                                              num_sampled, out_sampled, labels, n_labels,
                                              out_num_tries, out_log_ec_sampled, out_log_ec_labels,
                                              err); ::tfs::launched();
@@ -364,7 +370,7 @@ extern "C" int32_t tfs_log_uniform_sample(const void* state, int64_t vocab, int3
   const int64_t total = (int64_t)num_sampled + n_labels;
   if (total > 0) {
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 4 * num_sms()));
-    sample_finish_kernel<<<g2, 256, 0, st>>>(nullptr, nullptr, 0, unique, vocab, log_v1,
+    ::tfs::launch(sample_finish_kernel, g2, 256, 0, st, nullptr, nullptr, 0, unique, vocab, log_v1,
                                              num_sampled, out_sampled, labels, n_labels,
                                              out_num_tries, out_log_ec_sampled, out_log_ec_labels,
                                              err); ::tfs::launched();
@@ -386,7 +392,7 @@ extern "C" int32_t tfs_sample_commit(int64_t vocab, int32_t num_sampled, int32_t
   TFS_SUPPORTED();
   const int64_t total = std::max<int64_t>(1, (int64_t)num_sampled + n_labels);
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 4 * num_sms()));
-  sample_commit_kernel<<<g, 256, 0, as_stream(stream)>>>(
+  ::tfs::launch(sample_commit_kernel, g, 256, 0, as_stream(stream), 
       vocab, std::log((double)vocab + 1.0), unique, num_sampled, sampled, log_ec_sampled,
       num_tries, labels, n_labels, out_sampled, out_log_ec_sampled, out_log_ec_labels,
       out_num_tries, err);

@@ -13,6 +13,7 @@ constexpr float kLn2f = 0.6931471805599453f;
 
 // lse[t] from the R shards' (m, s) pairs, in rank order.
 __global__ void lse_combine_peers_kernel(const float* const* tab, int R, int64_t n, float* lse) {
+  pdl_enter();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n) return;
   float m = -INFINITY;
@@ -29,6 +30,7 @@ __global__ void lse_combine_peers_kernel(const float* const* tab, int R, int64_t
 template <bool VEC>
 __global__ void reduce_peers_kernel(const float* const* tab, int R, int64_t offset, int64_t n,
                                     float* out) {
+  pdl_enter();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (VEC) {
     const int64_t n4 = n / 4;
@@ -53,6 +55,7 @@ __global__ void reduce_peers_kernel(const float* const* tab, int R, int64_t offs
 __global__ void __launch_bounds__(1024) label_loss_kernel(const float* lse, const float* zl,
                                                           const int64_t* labels, int64_t n, int R,
                                                           int shard, float c, float* out) {
+  pdl_enter();
   __shared__ float red[1024];
   float acc = 0.f;
   for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
@@ -70,6 +73,7 @@ __global__ void __launch_bounds__(1024) label_loss_kernel(const float* lse, cons
 
 __global__ void dense_sgd_kernel(float4* table, const float4* grad, int64_t n, float lr,
                                  uint2* shadow) {
+  pdl_enter();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n4 = n / 4;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -106,7 +110,7 @@ extern "C" int32_t tfs_lse_combine_peers(const float* const* stats_tab, int32_t 
   if (n == 0) return TFS_OK;
   TFS_REQUIRE(stats_tab && lse);
   TFS_SUPPORTED();
-  lse_combine_peers_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(stats_tab, R, n,
+  ::tfs::launch(lse_combine_peers_kernel, (unsigned)cdiv(n, 256), 256, 0, as_stream(stream), stats_tab, R, n,
                                                                                  lse);
   launched();
   TFS_LAUNCH_CHECK();
@@ -122,9 +126,9 @@ extern "C" int32_t tfs_reduce_peers(const float* const* src_tab, int32_t R, int6
   cudaStream_t st = as_stream(stream);
   const bool vec = n % 4 == 0 && offset % 4 == 0 && ((uintptr_t)out & 15) == 0;
   if (vec)
-    reduce_peers_kernel<true><<<grid_for(n / 4), 256, 0, st>>>(src_tab, R, offset, n, out);
+    ::tfs::launch(reduce_peers_kernel<true>, grid_for(n / 4), 256, 0, st, src_tab, R, offset, n, out);
   else
-    reduce_peers_kernel<false><<<grid_for(n), 256, 0, st>>>(src_tab, R, offset, n, out);
+    ::tfs::launch(reduce_peers_kernel<false>, grid_for(n), 256, 0, st, src_tab, R, offset, n, out);
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
@@ -136,7 +140,7 @@ extern "C" int32_t tfs_label_loss_sum(const float* lse, const float* z_label,
   TFS_REQUIRE(R >= 1 && shard >= 0 && shard < R && n >= 0 && out);
   TFS_REQUIRE(n == 0 || (lse && z_label && labels));
   TFS_SUPPORTED();
-  label_loss_kernel<<<1, 1024, 0, as_stream(stream)>>>(lse, z_label, labels, n, R, shard, c, out);
+  ::tfs::launch(label_loss_kernel, 1, 1024, 0, as_stream(stream), lse, z_label, labels, n, R, shard, c, out);
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
@@ -149,7 +153,7 @@ extern "C" int32_t tfs_dense_sgd(float* table, const float* grad, int64_t n, flo
   TFS_REQUIRE(table && grad && ((uintptr_t)table & 15) == 0 && ((uintptr_t)grad & 15) == 0);
   TFS_REQUIRE(((uintptr_t)shadow & 7) == 0);
   TFS_SUPPORTED();
-  dense_sgd_kernel<<<grid_for(n / 4 + 1), 256, 0, as_stream(stream)>>>(
+  ::tfs::launch(dense_sgd_kernel, grid_for(n / 4 + 1), 256, 0, as_stream(stream), 
       reinterpret_cast<float4*>(table), reinterpret_cast<const float4*>(grad), n, lr,
       static_cast<uint2*>(shadow));
   launched();

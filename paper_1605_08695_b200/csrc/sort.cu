@@ -132,6 +132,7 @@ __device__ __forceinline__ uint32_t match_digit8(int dg, bool valid) {
 __global__ void __launch_bounds__(kSortThreads) digit_hist_kernel(DigitSrc src, int64_t n,
                                                                   uint32_t* hist, int ntiles,
                                                                   tfs_device_error* err) {
+  pdl_enter();
   __shared__ uint32_t cnt[kMaxBuckets];
   const int nb = src.nbuckets;
   for (int b = threadIdx.x; b < nb; b += kSortThreads) cnt[b] = 0;
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(kSortThreads) digit_scatter_kernel(DigitSrc sr
                                                                      const uint32_t* hist,
                                                                      int ntiles, Sink sink,
                                                                      int64_t* counts_out) {
+  pdl_enter();
   __shared__ uint32_t running[kMaxBuckets];
   __shared__ uint32_t wcnt[kSortWarps][kMaxBuckets];
   const int nb = src.nbuckets;
@@ -262,9 +264,9 @@ int32_t radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint3
     uint32_t* kd = to_out ? keys_out : tk;
     uint32_t* vd = to_out ? vals_out : tv;
     DigitSrc s{kDigitRadix, nullptr, nullptr, 0, 0, ksrc, vsrc, 8 * p, 256};
-    digit_hist_kernel<<<ntiles, kSortThreads, 0, st>>>(s, n, hist, ntiles, nullptr);
+    ::tfs::launch(digit_hist_kernel, ntiles, kSortThreads, 0, st, s, n, hist, ntiles, nullptr);
     launched();
-    digit_scatter_kernel<RadixSink><<<ntiles, kSortThreads, 0, st>>>(
+    ::tfs::launch(digit_scatter_kernel<RadixSink>, ntiles, kSortThreads, 0, st, 
         s, n, hist, ntiles, RadixSink{kd, vd}, nullptr);
     launched();
     TFS_LAUNCH_CHECK();
@@ -285,6 +287,7 @@ using namespace tfs;
 __global__ void partition_one_kernel(const int64_t* ids, int64_t n, int64_t vocab,
                                      int64_t* local, int64_t* positions, int64_t* counts,
                                      tfs_device_error* err) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t id = ids[i];
@@ -316,7 +319,7 @@ extern "C" int32_t tfs_partition(const int64_t* ids, int64_t n, int64_t vocab, i
   }
   if (num_shards == 1 && assignments == nullptr) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4ll * num_sms()));
-    partition_one_kernel<<<grid, 256, 0, st>>>(ids, n, vocab, out_local, out_positions,
+    ::tfs::launch(partition_one_kernel, grid, 256, 0, st, ids, n, vocab, out_local, out_positions,
                                                out_counts, err);
     launched();
     TFS_LAUNCH_CHECK();
@@ -327,9 +330,9 @@ extern "C" int32_t tfs_partition(const int64_t* ids, int64_t n, int64_t vocab, i
   uint32_t* hist = (uint32_t*)ws;
   DigitSrc s{assignments ? kDigitAssign : kDigitMod, ids, assignments, vocab, num_shards,
              nullptr, nullptr, 0, num_shards};
-  digit_hist_kernel<<<ntiles, kSortThreads, 0, st>>>(s, n, hist, ntiles, err);
+  ::tfs::launch(digit_hist_kernel, ntiles, kSortThreads, 0, st, s, n, hist, ntiles, err);
   launched();
-  digit_scatter_kernel<PartSink><<<ntiles, kSortThreads, 0, st>>>(
+  ::tfs::launch(digit_scatter_kernel<PartSink>, ntiles, kSortThreads, 0, st, 
       s, n, hist, ntiles, PartSink{out_local, out_positions}, out_counts);
   launched();
   TFS_LAUNCH_CHECK();
@@ -363,6 +366,7 @@ __device__ __forceinline__ int64_t load_id(const IdsView& v, int64_t i) {
 __global__ void make_keys_kernel(IdsView ids, int64_t n, int64_t limit, int32_t R,
                                  int64_t nloc, int composite, uint32_t* keys, uint32_t* vals,
                                  tfs_device_error* err) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t id = load_id(ids, i);
@@ -382,6 +386,7 @@ __global__ void make_keys_kernel(IdsView ids, int64_t n, int64_t limit, int32_t 
 // segment index of every sorted position.
 __global__ void __launch_bounds__(kSortThreads) heads_count_kernel(const uint32_t* k, int64_t n,
                                                                    uint32_t* tile_cnt) {
+  pdl_enter();
   const int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)threadIdx.x * kSortItems;
   uint32_t c = 0;
 #pragma unroll
@@ -397,6 +402,7 @@ __global__ void __launch_bounds__(kSortThreads) heads_count_kernel(const uint32_
 __global__ void __launch_bounds__(kSortThreads) heads_write_kernel(
     const uint32_t* k, int64_t n, const uint32_t* tile_cnt, int ntiles, uint32_t* seg_start,
     uint32_t* seg_of, int64_t* num_unique) {
+  pdl_enter();
   __shared__ uint32_t tile_base;
   if (threadIdx.x < 32) {
     uint32_t pre = 0, all = 0;
@@ -710,6 +716,7 @@ static_assert(kChunk <= 32, "the window prologue maps row r of a window to lane 
 // WR: write mode (sort_reduce / route_reduce: sums written out, j.table == nullptr) or apply.
 template <int OPT, bool WR>
 __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJob j) {
+  pdl_enter();
   // The window's row program, built once by warp 0 (lane r = row r) and read by every column
   // thread as broadcast shared loads: the gradient row's float offset (-1: skipped row), its
   // companion offset, the table row's float offset when a whole segment ends at r (apply mode),
@@ -881,6 +888,7 @@ __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int
 
 // Scalar columns (any dim): same structure, one column per lane per 32-column block.
 __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t chunk = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t base = chunk * j.chunk;
@@ -948,6 +956,7 @@ __global__ void __launch_bounds__(256) seg_chunk_scalar_kernel(SegJob j) {
 // every segment; in write mode, out_local for every segment.  Fully parallel, coalesced.
 template <bool VEC, int OPT>
 __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
+  pdl_enter();
   const int64_t U = *j.num_unique;
   const int cols = VEC ? (j.dim >> 2) : j.dim;
   const int64_t total = U * cols;
@@ -1020,6 +1029,7 @@ __global__ void __launch_bounds__(256) seg_apply_kernel(SegJob j) {
 __global__ void owner_counts_kernel(const uint32_t* keys, const uint32_t* seg_start,
                                     const int64_t* num_unique, int32_t R, int64_t nloc,
                                     uint32_t invalid_key, int64_t* counts) {
+  pdl_enter();
   const int o = threadIdx.x;
   if (o >= R) return;
   const int64_t U = *num_unique;
@@ -1152,6 +1162,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) sort_segment_small_kernel(
     IdsView ids, int n, int64_t limit, int32_t R, int64_t nloc, int composite, int passes,
     uint32_t* keys_out, uint32_t* perm_out, uint32_t* seg_start, uint32_t* seg_of,
     int64_t* num_unique, tfs_device_error* err) {
+  pdl_enter();
   extern __shared__ uint32_t sm[];
   __shared__ uint32_t wsum[33];
   const int cap = (n + 31) & ~31;
@@ -1274,7 +1285,7 @@ static int32_t sort_and_segment(IdsView ids, int64_t n, int64_t limit, int32_t R
     }
     const int bits = bits_for(key_max);
     const int passes = bits <= 8 ? 1 : (bits + 7) / 8;
-    sort_segment_small_kernel<<<1, kSmallThreads, smem, st>>>(
+    ::tfs::launch(sort_segment_small_kernel, 1, kSmallThreads, smem, st, 
         ids, (int)n, limit, R, nloc, composite, passes, s.k1, s.v1, s.seg_start, s.seg_of,
         s.num_unique, err);
     launched();
@@ -1282,16 +1293,16 @@ static int32_t sort_and_segment(IdsView ids, int64_t n, int64_t limit, int32_t R
     return TFS_OK;
   }
   const int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
-  make_keys_kernel<<<grid, 256, 0, st>>>(ids, n, limit, R, nloc, composite, s.k0, s.v0, err);
+  ::tfs::launch(make_keys_kernel, grid, 256, 0, st, ids, n, limit, R, nloc, composite, s.k0, s.v0, err);
   launched();
   TFS_LAUNCH_CHECK();
   int32_t rc = radix_sort_pairs(s.k0, s.v0, s.k1, s.v1, n, bits_for(key_max), s.sort_ws,
                                 s.sort_ws_bytes, st);
   if (rc != TFS_OK) return rc;
   const int ntiles = (int)cdiv(n, kSortTile);
-  heads_count_kernel<<<ntiles, kSortThreads, 0, st>>>(s.k1, n, s.tile_cnt);
+  ::tfs::launch(heads_count_kernel, ntiles, kSortThreads, 0, st, s.k1, n, s.tile_cnt);
   launched();
-  heads_write_kernel<<<ntiles, kSortThreads, 0, st>>>(s.k1, n, s.tile_cnt, ntiles, s.seg_start,
+  ::tfs::launch(heads_write_kernel, ntiles, kSortThreads, 0, st, s.k1, n, s.tile_cnt, ntiles, s.seg_start,
                                                       s.seg_of, s.num_unique);
   launched();
   TFS_LAUNCH_CHECK();
@@ -1333,16 +1344,16 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
                  : j.opt == 2 ? seg_window_vec4_kernel<2, false>
                  : wr         ? seg_window_vec4_kernel<0, true>
                               : seg_window_vec4_kernel<0, false>;
-    win_k<<<(unsigned)nchunks, wthreads, 0, st>>>(j);
+    ::tfs::launch(win_k, (unsigned)nchunks, wthreads, 0, st, j);
     launched();
   } else {
-    seg_chunk_scalar_kernel<<<grid, 256, 0, st>>>(j);
+    ::tfs::launch(seg_chunk_scalar_kernel, grid, 256, 0, st, j);
     launched();
     const int64_t work = n * j.dim;  // U <= n
     const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, 256), 16 * num_sms()));
     auto apply_k = j.opt == 1 ? seg_apply_kernel<false, 1>
                               : (j.opt == 2 ? seg_apply_kernel<false, 2> : seg_apply_kernel<false, 0>);
-    apply_k<<<agrid, 256, 0, st>>>(j);
+    ::tfs::launch(apply_k, agrid, 256, 0, st, j);
     launched();
   }
   TFS_LAUNCH_CHECK();
@@ -1459,6 +1470,7 @@ __device__ __forceinline__ int64_t seg_owner(const uint32_t* keys, const uint32_
 __global__ void route_bases_kernel(const uint32_t* keys, const uint32_t* seg_start,
                                    const int64_t* num_unique, int64_t n, int32_t R, int64_t nloc,
                                    uint32_t invalid_key, int64_t* base) {
+  pdl_enter();
   const int64_t U = *num_unique;
   if (U == 0) {
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o <= R;
@@ -1483,6 +1495,7 @@ __global__ void route_fill_kernel(const uint32_t* keys, const uint32_t* seg_star
                                   int64_t* send_local, int64_t stride,
                                   int64_t* const* dst_tab, int64_t dst_off, int64_t* counts,
                                   tfs_device_error* err) {
+  pdl_enter();
   const int64_t total = (int64_t)R * cap;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1505,6 +1518,7 @@ __global__ void route_unpack_kernel(const uint32_t* keys, const uint32_t* perm,
                                     const uint32_t* seg_of, const int64_t* base, int64_t n,
                                     int32_t dim, int64_t cap, int64_t nloc, uint32_t invalid_key,
                                     const float* slots, int64_t stride, float* out) {
+  pdl_enter();
   const int cols = VEC ? dim >> 2 : dim;
   const int64_t total = n * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -1550,12 +1564,12 @@ static int32_t route_plan_impl(const int64_t* ids, int64_t n, int64_t vocab, int
   int32_t rc = sort_and_segment(IdsView{ids, 0, 0}, n, vocab, num_shards, nloc, 1, invalid, s, err, st);
   if (rc != TFS_OK) return rc;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4ll * num_sms()));
-  route_bases_kernel<<<bgrid, 256, 0, st>>>(s.k1, s.seg_start, s.num_unique, n, num_shards, nloc,
+  ::tfs::launch(route_bases_kernel, bgrid, 256, 0, st, s.k1, s.seg_start, s.num_unique, n, num_shards, nloc,
                                             invalid, base);
   launched();
   const int64_t total = (int64_t)num_shards * cap;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 4ll * num_sms()));
-  route_fill_kernel<<<grid, 256, 0, st>>>(s.k1, s.seg_start, base, num_shards, cap, nloc,
+  ::tfs::launch(route_fill_kernel, grid, 256, 0, st, s.k1, s.seg_start, base, num_shards, cap, nloc,
                                           out_send_local, send_stride, dst_tab, dst_off,
                                           out_counts, err);
   launched();
@@ -1600,10 +1614,10 @@ extern "C" int32_t tfs_route_unpack(const void* plan, size_t plan_bytes, int64_t
   const int64_t total = n * (vec ? dim / 4 : dim);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 8ll * num_sms()));
   if (vec)
-    route_unpack_kernel<true><<<grid, 256, 0, st>>>(s.k1, s.v1, s.seg_of, base, n, dim, cap, nloc,
+    ::tfs::launch(route_unpack_kernel<true>, grid, 256, 0, st, s.k1, s.v1, s.seg_of, base, n, dim, cap, nloc,
                                                     invalid, slots, slots_stride, out);
   else
-    route_unpack_kernel<false><<<grid, 256, 0, st>>>(s.k1, s.v1, s.seg_of, base, n, dim, cap,
+    ::tfs::launch(route_unpack_kernel<false>, grid, 256, 0, st, s.k1, s.v1, s.seg_of, base, n, dim, cap,
                                                      nloc, invalid, slots, slots_stride, out);
   launched();
   TFS_LAUNCH_CHECK();
@@ -1672,6 +1686,7 @@ __device__ __forceinline__ int64_t run_rank(const IdsView& v, int64_t o, int64_t
 __global__ void merge_runs_kernel(IdsView ids, int32_t R, int64_t cap, int64_t limit,
                                   uint32_t* keys_out, uint32_t* perm_out,
                                   tfs_device_error* err) {
+  pdl_enter();
   const int64_t n = (int64_t)R * cap;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -1753,6 +1768,7 @@ __global__ void __launch_bounds__(512) merge_runs_smem_kernel(IdsView ids, int32
                                                               int64_t limit, uint32_t* keys_out,
                                                               uint32_t* perm_out,
                                                               tfs_device_error* err) {
+  pdl_enter();
   extern __shared__ uint32_t runs[];  // [R][cap]
   const int64_t n = (int64_t)R * cap;
   for (int64_t i0 = threadIdx.x; i0 < n; i0 += 8 * (int64_t)blockDim.x) {  // 8 loads in flight
@@ -1828,18 +1844,18 @@ extern "C" int32_t tfs_scatter_plan_slots(const int64_t* ids, int64_t ids_stride
     }
     // every CTA stages all runs; few CTAs suffice (n ~ 1e4 entries)
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 512), num_sms()));
-    merge_runs_smem_kernel<<<grid, 512, smem, st>>>(IdsView{ids, cap, ids_stride}, R, cap, rows,
+    ::tfs::launch(merge_runs_smem_kernel, grid, 512, smem, st, IdsView{ids, cap, ids_stride}, R, cap, rows,
                                                     s.k1, s.v1, err);
   } else {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8ll * num_sms()));
-    merge_runs_kernel<<<grid, 256, 0, st>>>(IdsView{ids, cap, ids_stride}, R, cap, rows, s.k1,
+    ::tfs::launch(merge_runs_kernel, grid, 256, 0, st, IdsView{ids, cap, ids_stride}, R, cap, rows, s.k1,
                                             s.v1, err);
   }
   launched();
   const int ntiles = (int)cdiv(n, kSortTile);
-  heads_count_kernel<<<ntiles, kSortThreads, 0, st>>>(s.k1, n, s.tile_cnt);
+  ::tfs::launch(heads_count_kernel, ntiles, kSortThreads, 0, st, s.k1, n, s.tile_cnt);
   launched();
-  heads_write_kernel<<<ntiles, kSortThreads, 0, st>>>(s.k1, n, s.tile_cnt, ntiles, s.seg_start,
+  ::tfs::launch(heads_write_kernel, ntiles, kSortThreads, 0, st, s.k1, n, s.tile_cnt, ntiles, s.seg_start,
                                                       s.seg_of, s.num_unique);
   launched();
   TFS_LAUNCH_CHECK();
@@ -1980,7 +1996,7 @@ extern "C" int32_t tfs_sort_reduce(const int64_t* ids, int64_t n, int64_t vocab,
   j.nloc = nloc;
   rc = run_segments(j, n, st);
   if (rc != TFS_OK) return rc;
-  owner_counts_kernel<<<1, 1024, 0, st>>>(s.k1, s.seg_start, s.num_unique, num_shards, nloc,
+  ::tfs::launch(owner_counts_kernel, 1, 1024, 0, st, s.k1, s.seg_start, s.num_unique, num_shards, nloc,
                                           invalid, out_counts);
   launched();
   TFS_LAUNCH_CHECK();

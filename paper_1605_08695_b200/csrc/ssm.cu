@@ -152,13 +152,20 @@ static int32_t launch_params(Params P, int sms, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CT;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {  // programmatic dependent launch (common.cuh)
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (CT > 1) {  // CTA pairs: a cluster of 2 (plain launch for single-CTA tiles)
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CT;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = CT > 1 ? 1 : 0;  // plain launch for single-CTA tiles
+  cfg.numAttrs = na;
   TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, LAB, CT>, P));
   launched();
   TFS_LAUNCH_CHECK();
@@ -269,6 +276,7 @@ __device__ __forceinline__ float block_max_256(float v, float* red) {
 
 __global__ void __launch_bounds__(256) loss_sum_kernel(const float* loss, int64_t B, float c,
                                                        float* out) {
+  pdl_enter();
   __shared__ float red[256];
   float acc = 0.f;
   for (int64_t t = threadIdx.x; t < B; t += 256) acc += loss[t];
@@ -296,6 +304,7 @@ template <int EPI>
 __global__ void __launch_bounds__(256) simt_gemm_kernel(int M, int N, int K, const float* A,
                                                         int64_t sam, int64_t sak, const float* B,
                                                         int64_t sbk, int64_t sbn, SimtParams p) {
+  pdl_enter();
   __shared__ float As[16][68];
   __shared__ float Bs[16][68];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -358,6 +367,7 @@ __global__ void __launch_bounds__(256) f32_row_kernel(
     int64_t S, int32_t d, const float* h, const float* w_true, const float* b_true,
     const float* le_true, float c, float* ZG, int64_t ldz, float* loss, float* lse_out,
     float* dw_true, float* db_true) {
+  pdl_enter();
   __shared__ float red[256];
   const int64_t t = blockIdx.x;
   const float* ht = h + t * d;
@@ -387,6 +397,7 @@ __global__ void __launch_bounds__(256) f32_row_kernel(
 
 // db_s[j] = sum_t G[t, j] in increasing t.
 __global__ void colsum_kernel(const float* G, int64_t B, int64_t S, int64_t ldg, float* out) {
+  pdl_enter();
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= S) return;
   float acc = 0.f;
@@ -398,6 +409,7 @@ __global__ void colsum_kernel(const float* G, int64_t B, int64_t S, int64_t ldg,
 // bf16 tensor-core path: small kernels around the GEMMs
 // fp32 -> bf16 (RNE), 4 elements per thread.
 __global__ void to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
+  pdl_enter();
   const int64_t n4 = n >> 2;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -421,6 +433,7 @@ template <int GROUPS>
 __global__ void __launch_bounds__(kColsumChunks * GROUPS) g_colsum_kernel(
     const uint16_t* G, int64_t B, int64_t S, int64_t ldG, float* db_s, const int64_t* sampled,
     int2* cmap, int64_t vocab, const float* loss, float c, float* loss_sum) {
+  pdl_enter();
   constexpr int kColsumGroups = GROUPS, kColsumThreads = kColsumChunks * GROUPS;
   __shared__ float red[kColsumGroups][kColsumChunks * 8 + 1];
   const int64_t ncol_blocks = cdiv_dev(S, kColsumChunks * 8);
@@ -501,6 +514,7 @@ __global__ void __launch_bounds__(kDbGroups * kDbCols) db_colpart_kernel(
     const float* colpart, int64_t nslabs, int64_t ld, int64_t S, float* db_s,
     const int64_t* sampled, int2* cmap, int64_t vocab, const float* loss, int64_t B, float c,
     float* loss_sum) {
+  pdl_enter();
   __shared__ float red[kDbGroups][kDbCols + 1];
   const int64_t ncol_blocks = cdiv_dev(S, kDbCols);
   const int tid = threadIdx.x;
@@ -561,6 +575,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const float* h, int64_t nh4, 
                                                    const int64_t* sampled, int64_t S,
                                                    int64_t S_pad, int2* cmap, int64_t vocab,
                                                    float* cb, int32_t* sid) {
+  pdl_enter();
   constexpr int U = 4;  // independent loads in flight per thread
   const int64_t total = nh4 + nw4 + S_pad;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -622,6 +637,7 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
     int64_t B, int32_t d, const void* h, const void* w_true, const float* b_true,
     const float* le_true, const float2* stats, int nparts, float c, float* loss, float* lse_out,
     float* dw_true, float* db_true) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= B) return;
@@ -721,6 +737,7 @@ __global__ void __launch_bounds__(256) bf16_combine_kernel(
 template <bool BIN>
 __global__ void split_finalize_kernel(const float* part, int nsplit, int64_t M, int32_t N,
                                       const float* g, const void* wt, float* out) {
+  pdl_enter();
   const int n4 = N / 4;
   const int64_t total = M * n4;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -829,26 +846,26 @@ static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   if (S > 0) {  // Z = h W_s^T + b_s - logQ (excluded -> -inf)
     SimtParams p{a->b_s, le_s, a->sampled, a->labels, hits, nullptr, nullptr, w.Z, S};
     dim3 grid((unsigned)cdiv(S, 64), (unsigned)cdiv(B, 64));
-    simt_gemm_kernel<kSimtLogits><<<grid, 256, 0, st>>>((int)B, (int)S, d, a->h, d, 1, a->w_s, 1,
+    ::tfs::launch(simt_gemm_kernel<kSimtLogits>, grid, 256, 0, st, (int)B, (int)S, d, a->h, d, 1, a->w_s, 1,
                                                          d, p);
     launched();
   }
-  f32_row_kernel<<<(unsigned)B, 256, 0, st>>>(S, d, a->h, a->w_true, a->b_true, le_t,
+  ::tfs::launch(f32_row_kernel, (unsigned)B, 256, 0, st, S, d, a->h, a->w_true, a->b_true, le_t,
                                               a->grad_scale, w.Z, S, a->loss, a->lse, a->dw_true,
                                               a->db_true);
   launched();
   {  // dh = G W_s + g * w_true
     SimtParams p{nullptr, nullptr, nullptr, nullptr, 0, a->db_true, a->w_true, a->dh, d};
     dim3 grid((unsigned)cdiv(d, 64), (unsigned)cdiv(B, 64));
-    simt_gemm_kernel<kSimtDh><<<grid, 256, 0, st>>>((int)B, d, (int)S, w.Z, S, 1, a->w_s, d, 1, p);
+    ::tfs::launch(simt_gemm_kernel<kSimtDh>, grid, 256, 0, st, (int)B, d, (int)S, w.Z, S, 1, a->w_s, d, 1, p);
     launched();
   }
   if (S > 0) {  // dW_s = G^T h ; db_s = column sums of G
     SimtParams p{nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, a->dw_s, d};
     dim3 grid((unsigned)cdiv(d, 64), (unsigned)cdiv(S, 64));
-    simt_gemm_kernel<kSimtStore><<<grid, 256, 0, st>>>((int)S, d, (int)B, w.Z, 1, S, a->h, d, 1, p);
+    ::tfs::launch(simt_gemm_kernel<kSimtStore>, grid, 256, 0, st, (int)S, d, (int)B, w.Z, 1, S, a->h, d, 1, p);
     launched();
-    colsum_kernel<<<(unsigned)cdiv(S, 256), 256, 0, st>>>(w.Z, B, S, S, a->db_s);
+    ::tfs::launch(colsum_kernel, (unsigned)cdiv(S, 256), 256, 0, st, w.Z, B, S, S, a->db_s);
     launched();
   }
   TFS_LAUNCH_CHECK();
@@ -906,7 +923,7 @@ static int32_t bf16_prep(const tfs_ssm_args* a, const Bf16Plan& p, cudaStream_t 
   const int32_t d = a->dim;
   const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
   const int64_t nconv = p.bin ? 0 : (B + S) * d / 4;
-  prep_kernel<<<grid1d((nconv + p.w.Spad) / 4), 256, 0, st>>>(
+  ::tfs::launch(prep_kernel, grid1d((nconv + p.w.Spad) / 4), 256, 0, st, 
       a->h, p.bin ? 0 : B * d / 4, a->w_s, p.bin ? 0 : S * d / 4, p.w.hb, p.w.wsb, a->b_s, le_s,
       a->sampled, S, p.w.Spad, const_cast<int2*>(p.ep.cmap), p.ep.vocab, p.w.cb, p.w.sid);
   launched();
@@ -948,15 +965,14 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   mark(a, 4, st);
   if (fused_colsum) {
     const int64_t ncb = cdiv(S, kDbCols);
-    db_colpart_kernel<<<(unsigned)(ncb + (a->loss_sum ? 1 : 0)), kDbGroups * kDbCols, 0, st>>>(
+    ::tfs::launch(db_colpart_kernel, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kDbGroups * kDbCols, 0, st, 
         w.colpart, w.nslabs, w.Spad, S, a->db_s, a->sampled, const_cast<int2*>(ep.cmap),
         ep.vocab, a->loss, B, a->grad_scale, a->loss_sum);
   } else {
     const int64_t ncb = cdiv(S, kColsumChunks * 8);
     const bool narrow = ncb < num_sms();
     auto colsum = narrow ? g_colsum_kernel<256> : g_colsum_kernel<64>;
-    colsum<<<(unsigned)(ncb + (a->loss_sum ? 1 : 0)), kColsumChunks * (narrow ? 256 : 64), 0,
-             st>>>(w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
+    ::tfs::launch(colsum, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kColsumChunks * (narrow ? 256 : 64), 0, st, w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
                    a->loss, a->grad_scale, a->loss_sum);
   }
   launched();
@@ -979,11 +995,11 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   mark(a, 6, st);
   if (dh_split) {
     auto fin = p.bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
-    fin<<<grid1d(B * d / 4), 256, 0, st>>>(w.part_dh, w.ks_dh, B, d, g_true, w_true, a->dh);
+    ::tfs::launch(fin, grid1d(B * d / 4), 256, 0, st, w.part_dh, w.ks_dh, B, d, g_true, w_true, a->dh);
     launched();
   }
   if (dws_split) {
-    split_finalize_kernel<false><<<grid1d(S * d / 4), 256, 0, st>>>(
+    ::tfs::launch(split_finalize_kernel<false>, grid1d(S * d / 4), 256, 0, st, 
         w.part_dws, w.ks_dws, S, d, nullptr, nullptr, a->dw_s);
     launched();
   }
@@ -1008,7 +1024,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   }
   mark(a, 2, st);
   auto combine = p.bin ? bf16_combine_kernel<true> : bf16_combine_kernel<false>;
-  combine<<<(unsigned)cdiv(B, 8), 256, 0, st>>>(B, d, a->h, a->w_true, a->b_true, le_t,
+  ::tfs::launch(combine, (unsigned)cdiv(B, 8), 256, 0, st, B, d, a->h, a->w_true, a->b_true, le_t,
                                                 p.w.stats, 2 * p.num_n, a->grad_scale, a->loss,
                                                 a->lse, a->dw_true, a->db_true);
   launched();
@@ -1016,7 +1032,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   mark(a, 3, st);
   if (S == 0) {  // no candidates: dh = g * bf16(w_true)
     auto fin = p.bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
-    fin<<<grid1d(B * d / 4), 256, 0, st>>>(nullptr, 0, B, d, a->db_true, a->w_true, a->dh);
+    ::tfs::launch(fin, grid1d(B * d / 4), 256, 0, st, nullptr, 0, B, d, a->db_true, a->w_true, a->dh);
     launched();
     TFS_LAUNCH_CHECK();
     return TFS_OK;
@@ -1028,6 +1044,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
 // fixed order (lane-strided, then a butterfly).
 __global__ void __launch_bounds__(256) row_stats_kernel(const float2* stats, int nparts,
                                                         int64_t B, float2* out) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= B) return;
@@ -1093,7 +1110,7 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
   if (rc != TFS_OK) return rc;
   const bool fused_sum = a->operand_dtype == TFS_BF16 && a->S > 0;  // done by g_colsum_kernel
   if (a->loss_sum && !fused_sum) {
-    loss_sum_kernel<<<1, 256, 0, st>>>(a->loss, a->B, a->grad_scale, a->loss_sum); ::tfs::launched();
+    ::tfs::launch(loss_sum_kernel, 1, 256, 0, st, a->loss, a->B, a->grad_scale, a->loss_sum); ::tfs::launched();
     TFS_LAUNCH_CHECK();
   }
   return TFS_OK;
@@ -1128,7 +1145,7 @@ extern "C" int32_t tfs_ssm_partial_stats(const tfs_ssm_args* a, float* row_stats
   bf16_plan(a, ws, &p);
   if ((rc = bf16_prep(a, p, st)) != TFS_OK) return rc;
   if ((rc = bf16_stats(a, p, st)) != TFS_OK) return rc;
-  row_stats_kernel<<<(unsigned)cdiv(a->B, 8), 256, 0, st>>>(p.w.stats, 2 * p.num_n, a->B,
+  ::tfs::launch(row_stats_kernel, (unsigned)cdiv(a->B, 8), 256, 0, st, p.w.stats, 2 * p.num_n, a->B,
                                                             reinterpret_cast<float2*>(row_stats));
   launched();
   TFS_LAUNCH_CHECK();
@@ -1174,7 +1191,7 @@ extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn,
                C, N, part, nullptr, nullptr, 0, 0};
   int32_t rc = umma::launch_store(&g, 1, 0, st);
   if (rc != TFS_OK || ks == 1) return rc;
-  split_finalize_kernel<false><<<grid1d((int64_t)M * N / 4), 256, 0, st>>>(part, ks, M, N, nullptr,
+  ::tfs::launch(split_finalize_kernel<false>, grid1d((int64_t)M * N / 4), 256, 0, st, part, ks, M, N, nullptr,
                                                                     nullptr, C);
   launched();
   TFS_LAUNCH_CHECK();

@@ -53,6 +53,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 // fence + release store publish it to the peers, the acquire load orders what follows.
 __global__ void barrier_kernel(const int64_t* bases, int R, int rank, int ch, uint32_t* epoch,
                                tfs_device_error* err, uint64_t timeout_ns) {
+  pdl_enter();
   __shared__ uint32_t e;
   if (threadIdx.x == 0) {
     e = epoch[ch] + 1u;
@@ -76,9 +77,11 @@ __global__ void barrier_kernel(const int64_t* bases, int R, int rank, int ch, ui
   __syncthreads();
 }
 
-__global__ void add_i64_kernel(int64_t* p, int64_t v) { *p += v; }
+__global__ void add_i64_kernel(int64_t* p, int64_t v) {
+  pdl_enter(); *p += v; }
 
 __global__ void next_counter_kernel(const int64_t* step, int64_t* next, int64_t add) {
+  pdl_enter();
   *next = *step + add;
 }
 
@@ -86,6 +89,7 @@ __global__ void next_counter_kernel(const int64_t* step, int64_t* next, int64_t 
 // many microseconds at the head of every side-stream phase, so a missing cross-stream wait
 // shows up as wrong results in the parity tests.  Results are unchanged -- only timing.
 __global__ void delay_kernel(uint64_t ns) {
+  pdl_enter();
   const uint64_t t0 = global_ns();
   while (global_ns() - t0 < ns) {
   }
@@ -98,17 +102,20 @@ __global__ void delay_kernel(uint64_t ns) {
 // id-mod-R layout so that tfs_gather_peers can fetch it).
 __global__ void index_map_kernel(int64_t* out, int64_t n, int mode, int64_t mul, int64_t add,
                                  int64_t B, int64_t R) {
+  pdl_enter();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   out[i] = mode == 0 ? i * mul + add : (i % B) * R + i / B;
 }
 
 __global__ void fill_i64_kernel(int64_t* p, int64_t n, int64_t v) {
+  pdl_enter();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
 
 __global__ void f32_to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
+  pdl_enter();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
     dst[i] = f32_to_bf16_bits(src[i]);
@@ -230,7 +237,7 @@ extern "C" int32_t tfs_comm_connect(tfs_comm* c, const void* handles) {
 
 extern "C" int32_t tfs_comm_barrier(tfs_comm* c, int32_t channel, void* stream) {
   TFS_REQUIRE(c && c->nlocal == 1 && c->connected && channel >= 0 && channel < kChannels);
-  barrier_kernel<<<1, 64, 0, as_stream(stream)>>>(c->d_bases[0], c->R, c->first, channel,
+  ::tfs::launch(barrier_kernel, 1, 64, 0, as_stream(stream), c->d_bases[0], c->R, c->first, channel,
                                                  c->d_epoch[0], c->d_err[0], c->timeout_ns);
   launched();
   TFS_LAUNCH_CHECK();
@@ -497,7 +504,7 @@ tfs_ssm_args slice_args(const tfs_stepper* st, const Rank& k, bool backward) {
 int32_t presample(tfs_stepper* st, Rank& k, cudaStream_t s, int64_t add) {
   const Dims& m = st->m;
   if (m.full) return TFS_OK;
-  next_counter_kernel<<<1, 1, 0, s>>>(k.step, k.step_next, add);
+  ::tfs::launch(next_counter_kernel, 1, 1, 0, s, k.step, k.step_next, add);
   launched();
   TFS_LAUNCH_CHECK();
   return tfs_log_uniform_sample(k.smp_state, m.V, (int32_t)m.S, st->cfg.unique, k.max_draws,
@@ -563,7 +570,7 @@ int32_t apply_owner(tfs_stepper* st, Rank& k, bool e_table, cudaStream_t s) {
 void fork_side(tfs_stepper* st, Rank& k, cudaStream_t mn) {
   STEP_CALL(st, join(k.side, mn, k.ev[kFork]));
   if (st->side_delay_ns) {
-    delay_kernel<<<1, 1, 0, k.side>>>(st->side_delay_ns);
+    ::tfs::launch(delay_kernel, 1, 1, 0, k.side, st->side_delay_ns);
     launched();
   }
 }
@@ -816,7 +823,7 @@ void full_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
 }
 
 int32_t bump_step(Rank& k, cudaStream_t mn) {
-  add_i64_kernel<<<1, 1, 0, mn>>>(k.step, 1);
+  ::tfs::launch(add_i64_kernel, 1, 1, 0, mn, k.step, 1);
   launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;
@@ -830,7 +837,7 @@ void barrier(tfs_stepper* st, int channel, int which_stream, std::vector<cudaStr
   auto stream_of = [&](size_t l) { return which_stream ? st->ranks[l].side : mains[l]; };
   if (c->nlocal == 1) {
     Rank& k = st->ranks[0];
-    barrier_kernel<<<1, 64, 0, stream_of(0)>>>(c->d_bases[0], c->R, k.r, channel, c->d_epoch[0],
+    ::tfs::launch(barrier_kernel, 1, 64, 0, stream_of(0), c->d_bases[0], c->R, k.r, channel, c->d_epoch[0],
                                                c->d_err[0], c->timeout_ns);
     launched();
     if (cudaGetLastError() != cudaSuccess && st->status == TFS_OK) st->status = TFS_ERR_CUDA;
@@ -1135,8 +1142,8 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
         k.dw_full = cv.take<float>(k.nloc * d);
         k.db_full = cv.take<float>(k.nloc);
         k.z_label = cv.take<float>(m.M);
-        index_map_kernel<<<grid1d(m.M), 256>>>(k.ag_ids, m.M, 1, 0, 0, B, R);
-        index_map_kernel<<<grid1d(k.nloc), 256>>>(k.cand, k.nloc, 0, R, k.r, B, R);
+        ::tfs::launch(index_map_kernel, grid1d(m.M), 256, 0, 0, k.ag_ids, m.M, 1, 0, 0, B, R);
+        ::tfs::launch(index_map_kernel, grid1d(k.nloc), 256, 0, 0, k.cand, k.nloc, 0, R, k.r, B, R);
         launched(2);
       }
     }
@@ -1158,8 +1165,8 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
       k.smp_ws_b = tfs_sampler_workspace_bytes(md);
       if (cudaMalloc(&k.smp_ws, k.smp_ws_b) != cudaSuccess) return bail(TFS_ERR_CUDA);
     } else if (m.R == 1) {  // candidates = all V classes, no correction (config F)
-      index_map_kernel<<<grid1d(V), 256>>>(k.qw + B, V, 0, 1, 0, B, R);
-      fill_i64_kernel<<<1, 1>>>(k.num_tries, 1, V);
+      ::tfs::launch(index_map_kernel, grid1d(V), 256, 0, 0, k.qw + B, V, 0, 1, 0, B, R);
+      ::tfs::launch(fill_i64_kernel, 1, 1, 0, 0, k.num_tries, 1, V);
       launched(2);
     }
     if (cfg->optimizer == 2) {
@@ -1225,7 +1232,7 @@ extern "C" int32_t tfs_step_sync(tfs_stepper* st) {
   const tfs_device_error none{0, 0, INT64_MAX};
   for (auto& k : st->ranks) {
     if (k.W_bf) {
-      f32_to_bf16_kernel<<<grid1d(k.nloc * st->m.d), 256>>>(k.W, k.nloc * st->m.d, k.W_bf);
+      ::tfs::launch(f32_to_bf16_kernel, grid1d(k.nloc * st->m.d), 256, 0, 0, k.W, k.nloc * st->m.d, k.W_bf);
       launched();
     }
     TFS_CUDA_TRY(cudaMemcpy(k.err, &none, sizeof(none), cudaMemcpyHostToDevice));

@@ -365,6 +365,9 @@ template <int MODE, bool LAB = false, int CT = 1>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Params P) {
   constexpr int PM = CT * BM;  // rows per tile
   extern __shared__ __align__(1024) uint8_t smem[];
+  // PDL (common.cuh): this grid's setup (barriers, TMEM, descriptor prefetch) may overlap the
+  // previous kernel's tail; its results are waited for below.
+  if (TFS_PDL_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int STAGES = P.stages;
   const int B_BYTES = P.b_stride;
   uint8_t* sA = smem;
@@ -409,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   cluster_sync_all<CT>();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid's outputs are visible
 
   if (warp == 0) {
     // ================================ TMA producer ================================
