@@ -777,12 +777,16 @@ struct Bf16Ws {
 
 // Split-K plan for the backward pair (dW_s: M=S, K=B; dh: M=B, K=S; both N=d) run in one
 // persistent launch: aim for ~2 units per CTA pair of roughly equal k-block count.
+#ifndef TFS_BWD_UNITS_PER_GROUP
+#define TFS_BWD_UNITS_PER_GROUP 2
+#endif
 static void plan_backward(int64_t B, int64_t S, int32_t d, int* ks_dh, int* ks_dws) {
   constexpr int ct = umma::kStoreCta;
   const int64_t t_dh = umma::tiles_of((int)B, d, ct), t_dws = umma::tiles_of((int)S, d, ct);
   const int64_t kb_dh = cdiv(S, umma::BK), kb_dws = cdiv(B, umma::BK);
   const int64_t work = t_dh * kb_dh + t_dws * kb_dws;
-  const int64_t target = std::max<int64_t>(16, cdiv(work, 2 * (num_sms() / ct)));
+  const int64_t target =
+      std::max<int64_t>(16, cdiv(work, TFS_BWD_UNITS_PER_GROUP * (num_sms() / ct)));
   auto split = [&](int64_t kb) {
     if (kb <= target + target / 4) return 1;
     return (int)std::min<int64_t>(16, cdiv(kb, target));
