@@ -500,6 +500,21 @@ def main():
                                    "achieved = that / the call's CUDA-event duration",
                     "ms": top["ms"], "kernels": per}
         call_ms = None
+    elif args.dtype == "f32":
+        # the fp32 parity path: SIMT FFMA GEMMs (no tensor cores); peak = SMs x 128 FP32 lanes
+        # x 2 flops x the max SM clock (B200_PROFILING.md unit counts), timed as the whole call
+        call_ms = avg(9, 16)
+        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        t = call_ms / 1e3
+        ach = 6.0 * B * S_eff * d / t / 1e12
+        roofline = {"kernel": "tfs_sampled_softmax_fwd_bwd, fp32 path (SIMT FFMA GEMMs)",
+                    "bound": "alu", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": ach / fp32_peak, "traffic": None,
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz",
+                    "algorithmic": "6*B*S*d flops per call; achieved = that / the call's "
+                                   "CUDA-event duration in instrumented eager steps",
+                    "ms": call_ms,
+                    "logits_gemm_ms": avg(9, 11)}
     else:
         kern_ms = {"gemm_stats": avg(10, 11), "gemm_grad": avg(12, 13), "gemm_store": avg(14, 15)}
         call_ms = avg(9, 16)

@@ -223,7 +223,8 @@ typedef struct {
   /* Optional instrumentation (bf16 path): NULL, or an array of 8 cudaEvent_t (any entry NULL)
    * recorded on the stream at: 0 start, 1 after the prep pass, 2 after the logits GEMM (STATS),
    * 3 after the combine, 4 after the gradient GEMM (GRAD), 5 after the column sums, 6 after
-   * the grouped dh / dW_s GEMM, 7 end.  Lets a caller time each GEMM launch live. */
+   * the grouped dh / dW_s GEMM, 7 end.  Lets a caller time each GEMM launch live.  The fp32
+   * path records 0, 2 (after its logits GEMM) and 7 only. */
   void* const* timing_events;
   /* SMs the persistent tensor-core GEMMs of the call leave free (0: use every SM), so work on
    * other streams (e.g. the training step's side streams) progresses while they run. */

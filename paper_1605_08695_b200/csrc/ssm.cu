@@ -839,6 +839,12 @@ static int grid1d(int64_t n, int threads = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, threads), 8ll * num_sms()));
 }
 
+// Optional instrumentation events (tfs_ssm_args::timing_events).
+static void mark(const tfs_ssm_args* a, int i, cudaStream_t st) {
+  if (a->timing_events != nullptr && a->timing_events[i] != nullptr)
+    cudaEventRecord(static_cast<cudaEvent_t>(a->timing_events[i]), st);
+}
+
 static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   F32Ws w;
   ws_layout(a->B, a->S, a->dim, TFS_F32, a->vocab, &w, nullptr, ws);
@@ -847,6 +853,7 @@ static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const int hits = (a->flags & TFS_REMOVE_ACCIDENTAL_HITS) ? 1 : 0;
   const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
   const float* le_t = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_true : nullptr;
+  mark(a, 0, st);  // fp32 path: events 0 (start), 2 (after the logits GEMM), 7 (end) only
   if (S > 0) {  // Z = h W_s^T + b_s - logQ (excluded -> -inf)
     SimtParams p{a->b_s, le_s, a->sampled, a->labels, hits, nullptr, nullptr, w.Z, S};
     dim3 grid((unsigned)cdiv(S, 64), (unsigned)cdiv(B, 64));
@@ -854,6 +861,7 @@ static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
                                                          d, p);
     launched();
   }
+  mark(a, 2, st);
   ::tfs::launch(f32_row_kernel, (unsigned)B, 256, 0, st, S, d, a->h, a->w_true, a->b_true, le_t,
                                               a->grad_scale, w.Z, S, a->loss, a->lse, a->dw_true,
                                               a->db_true);
@@ -872,15 +880,11 @@ static int32_t ssm_f32(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     ::tfs::launch(colsum_kernel, (unsigned)cdiv(S, 256), 256, 0, st, w.Z, B, S, S, a->db_s);
     launched();
   }
+  mark(a, 7, st);
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }
 
-// Optional instrumentation events (tfs_ssm_args::timing_events).
-static void mark(const tfs_ssm_args* a, int i, cudaStream_t st) {
-  if (a->timing_events != nullptr && a->timing_events[i] != nullptr)
-    cudaEventRecord(static_cast<cudaEvent_t>(a->timing_events[i]), st);
-}
 
 // Everything the phases of the tensor-core path share: workspace slices, epilogue parameters,
 // the STATS / GRAD tile width.

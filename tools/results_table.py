@@ -23,7 +23,9 @@ def row(path):
     gemm = f"{st['tflops']:.0f} ({st['frac']:.2f})" if st else "-"
     cpu = d.get("cpu_baseline")
     cpu_s = f"{cpu['value']:.0f} (1 of {cpu.get('nproc')} cores)" if cpu else "-"
-    return (f"| {c['workload']}{' f32' if d.get('dtype') == 'f32' else ''} | {d['n_gpus']} | "
+    opt = c.get("optimizer", "sgd")
+    tag = (" f32" if d.get("dtype") == "f32" else "") + (f" {opt}" if opt != "sgd" else "")
+    return (f"| {c['workload']}{tag} | {d['n_gpus']} | "
             f"{d['value'] / 1e6:.2f}M ({rng}) | {d['ms_per_step'] * 1e3:.1f} | {g} | {s} | {gemm} | "
             f"{cpu_s} | {d['e2e']['value'] / 1e6:.2f}M |")
 
