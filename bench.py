@@ -516,12 +516,22 @@ def main():
                     "ms": call_ms,
                     "logits_gemm_ms": avg(9, 11)}
     else:
-        kern_ms = {"gemm_stats": avg(10, 11), "gemm_grad": avg(12, 13), "gemm_store": avg(14, 15)}
+        zpass = int(_lib.lib().tfs_ssm_grad_from_logits()) == 1
+        kern_ms = {"gemm_stats": avg(10, 11), "gemm_store": avg(14, 15)}
+        flops = {"gemm_stats": 2.0 * B * S_eff * d, "gemm_store": 4.0 * B * S_eff * d}
+        if not zpass:
+            kern_ms["gemm_grad"] = avg(12, 13)
+            flops["gemm_grad"] = 2.0 * B * S_eff * d
         call_ms = avg(9, 16)
-        flops = {"gemm_stats": 2.0 * B * S_eff * d, "gemm_grad": 2.0 * B * S_eff * d,
-                 "gemm_store": 4.0 * B * S_eff * d}
         per = {k: {"ms": v, "tflops": flops[k] / (v / 1e3) / 1e12,
                    "frac": flops[k] / (v / 1e3) / 1e12 / peak} for k, v in kern_ms.items()}
+        if zpass:
+            # the elementwise gradient pass: reads the fp32 logits, writes bf16 G (+ slab sums)
+            gp_ms = avg(12, 13)
+            gp_bytes = B * S_eff * (4 + 2)
+            per["grad_pass"] = {"ms": gp_ms, "GBps": gp_bytes / (gp_ms / 1e3) / 1e9,
+                                "frac": gp_bytes / (gp_ms / 1e3) / 1e9 / hbm_peak,
+                                "bound": "hbm", "bytes": gp_bytes}
         top = per["gemm_store"]
         roofline = {"kernel": "umma::gemm_kernel<STORE> (dh = G W_s and dW_s = G^T h, one "
                               "persistent tcgen05 launch)",

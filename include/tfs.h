@@ -223,8 +223,10 @@ typedef struct {
   /* Optional instrumentation (bf16 path): NULL, or an array of 8 cudaEvent_t (any entry NULL)
    * recorded on the stream at: 0 start, 1 after the prep pass, 2 after the logits GEMM (STATS),
    * 3 after the combine, 4 after the gradient GEMM (GRAD), 5 after the column sums, 6 after
-   * the grouped dh / dW_s GEMM, 7 end.  Lets a caller time each GEMM launch live.  The fp32
-   * path records 0, 2 (after its logits GEMM) and 7 only. */
+   * the grouped dh / dW_s GEMM, 7 end.  Lets a caller time each GEMM launch live.  When
+   * tfs_ssm_grad_from_logits() is 1, 2 is after the logits GEMM that also stores the logits and
+   * 4 after the elementwise gradient pass that replaces GRAD.  The fp32 path records 0, 2
+   * (after its logits GEMM) and 7 only. */
   void* const* timing_events;
   /* SMs the persistent tensor-core GEMMs of the call leave free (0: use every SM), so work on
    * other streams (e.g. the training step's side streams) progresses while they run. */
@@ -234,6 +236,10 @@ size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operan
                                int64_t vocab);
 int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, size_t ws_bytes,
                                     void* stream);
+/* 1 if this build's bf16 path keeps the logits from the logits GEMM (fp32, B x S in the
+ * workspace) and forms G from them in an elementwise pass, 0 if it recomputes them on the
+ * tensor cores (the GRAD GEMM).  Results are identical; only the schedule differs. */
+int32_t tfs_ssm_grad_from_logits(void);
 
 /* ==== Vocabulary-sharded full softmax: the two local halves =========
  * "the weights are sharded across several tasks, and the multiplication and gradient

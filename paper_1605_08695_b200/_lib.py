@@ -81,6 +81,7 @@ class SsmArgs(ctypes.Structure):
 
 _SIGNATURES = {
     "tfs_version": ([], I32),
+    "tfs_ssm_grad_from_logits": ([], I32),
     "tfs_status_string": ([I32], ctypes.c_char_p),
     "tfs_last_error_detail": ([ctypes.c_char_p, SZ], I32),
     "tfs_device_check": ([I32], I32),

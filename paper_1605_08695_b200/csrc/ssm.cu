@@ -123,7 +123,7 @@ static void stage_plan(Params& P) {
   int bmax = 0;
   for (int i = 0; i < P.nprob; ++i) bmax = std::max(bmax, P.p[i].bn / CT * BK * 2);
   P.b_stride = (bmax + 1023) / 1024 * 1024;
-  const int fixed = (MODE == kStats ? 0 : kEpiSmem) + kCbSmem + kBarBytes;
+  const int fixed = (MODE == kStats && !TFS_SSM_ZPASS ? 0 : kEpiSmem) + kCbSmem + kBarBytes;
   P.stages =
       std::min<int>(kMaxStages, ((int)kSmemBytes - fixed) / (KSUB * (A_BYTES + P.b_stride)));
 }
@@ -196,7 +196,7 @@ int pick_bn(int M, int N, int sms) {
 }
 
 int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn,
-                             int groups, EpiParams ep, uint16_t* G, int64_t ldG,
+                             int groups, EpiParams ep, void* G, int64_t ldG,
                              cudaStream_t st) {
   if (A.mn || B.mn) return TFS_ERR_INVALID_ARGUMENT;
   Params P{};
@@ -206,6 +206,10 @@ int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K
   P.total_units = P.p[0].units;
   if (mode == kGrad) {
     rc = make_store_map(&ep.tG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, G, (uint64_t)N,
+                        (uint64_t)M, (uint64_t)ldG, 1, 0);
+    if (rc != TFS_OK) return rc;
+  } else if (ep.zstore) {  // STATS also writes the fp32 logits Z [M x ldG]
+    rc = make_store_map(&ep.tZ, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, G, (uint64_t)N,
                         (uint64_t)M, (uint64_t)ldG, 1, 0);
     if (rc != TFS_OK) return rc;
   }
@@ -768,10 +772,12 @@ struct Bf16Ws {
   uint16_t *hb, *wsb, *G;
   float2* stats;
   float *cb, *part_dh, *part_dws, *colpart;
+  float* Z;  // [B x Spad] fp32 logits (log2 units) from the STATS pass (TFS_SSM_ZPASS)
   int32_t* sid;
   int64_t Sp, Spad, ldh, nslabs;
   int ks_dh, ks_dws;
 };
+
 
 
 
@@ -827,6 +833,7 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, int64_t 
   x.sid = c.take<int32_t>(Spad);
   x.nslabs = cdiv(std::max<int64_t>(B, 1), umma::BM) * 4;  // GRAD: one CTA per 128-row tile
   x.colpart = c.take<float>((size_t)x.nslabs * Spad);
+  x.Z = TFS_SSM_ZPASS ? c.take<float>((size_t)std::max<int64_t>(B, 1) * Spad) : nullptr;
   x.Sp = Sp;
   x.Spad = Spad;
   x.ks_dh = ks_dh;
@@ -939,52 +946,93 @@ static int32_t bf16_prep(const tfs_ssm_args* a, const Bf16Plan& p, cudaStream_t 
   return TFS_OK;
 }
 
-// Pass 1: per-row (max, sum 2^x) of each half tile, log2 domain.
-static int32_t bf16_stats(const tfs_ssm_args* a, const Bf16Plan& p, cudaStream_t st) {
-  const umma::Operand hK{p.w.hb, p.w.ldh, false}, wsK{p.w.wsb, a->dim, false};
-  return umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)a->B, (int)a->S, a->dim, p.bn,
-                                    p.groups,
-                                    p.ep, nullptr, 0, st);
+// The gradient pass from the stored logits (TFS_SSM_ZPASS): G = c exp(Z - lse) = 2^(v - goff)
+// in bf16, with the label column (label_in) at c (p - 1) and the label's logit to zlab -- the
+// arithmetic of the GRAD epilogue (umma.cuh) on the same v, so G is bit-identical -- plus the
+// column sums of each 32-row slab of the bf16 G in row order (the colpart layout the GRAD
+// epilogue writes; db_colpart_kernel finishes db_s).  Block: 32 rows x 256 columns, lane =
+// column (32-column loads and 64-byte stores per row, coalesced), all 32 row loads in flight.
+template <bool LAB>
+__global__ void __launch_bounds__(256) g_from_z_kernel(
+    const float* __restrict__ Z, int64_t ldz, int64_t B, int64_t S, const float* __restrict__ lse,
+    float c, const int64_t* __restrict__ labels, const int2* __restrict__ cmap, int64_t vocab,
+    int S_pad, const int32_t* __restrict__ sid, uint16_t* __restrict__ G, int64_t ldG,
+    float* __restrict__ colpart, int64_t colpart_ld, float* __restrict__ zlab) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int64_t col = ((int64_t)blockIdx.y * 8 + warp) * 32 + lane;
+  const int nrows = (int)min((int64_t)32, B - r0);
+  // lane r: row r0 + r's constants (as the GRAD epilogue forms them)
+  const int64_t row_l = r0 + lane;
+  float goff_l = 0.f;
+  int32_t y_l = -2;
+  int hlo_l = 1 << 30, hhi_l = -1;
+  if (row_l < B) {
+    if (LAB && labels != nullptr) {
+      const int64_t yl = __ldg(labels + row_l);
+      y_l = (int32_t)yl;
+      if (cmap == nullptr) {
+        hlo_l = 0;
+        hhi_l = S_pad;
+      } else if (yl >= 0 && yl < vocab) {
+        const int2 m = __ldg(cmap + yl);
+        if (m.y > 0) {
+          hlo_l = (1 << 30) - m.x;
+          hhi_l = m.y - 1;
+        }
+      }
+    }
+    goff_l = __ldg(lse + row_l) * umma::kLog2e - log2f(c);
+  }
+  const bool col_ok = col < S;
+  const int32_t sid_c = (LAB && col_ok) ? __ldg(sid + col) : -1;
+  float v[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r)
+    v[r] = (r < nrows && col_ok) ? __ldg(Z + (r0 + r) * ldz + col) : -INFINITY;
+  float cs = 0.f;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const float goff = __shfl_sync(0xffffffffu, goff_l, r);
+    float g;
+    if (LAB) {
+      const int32_t y = __shfl_sync(0xffffffffu, y_l, r);
+      const int lo = __shfl_sync(0xffffffffu, hlo_l, r), hi = __shfl_sync(0xffffffffu, hhi_l, r);
+      const bool lab = col >= lo && col <= hi && sid_c == y;
+      if (lab && r < nrows) zlab[r0 + r] = v[r] * umma::kLn2;
+      g = umma::fast_exp2(v[r] - goff) - (lab ? c : 0.f);
+    } else {
+      g = umma::fast_exp2(v[r] - goff);
+    }
+    const uint16_t gb = f32_to_bf16_bits(g);
+    if (r < nrows && col_ok) {
+      G[(r0 + r) * ldG + col] = gb;
+      cs += __uint_as_float((uint32_t)gb << 16);
+    }
+  }
+  if (col_ok) colpart[(r0 >> 5) * colpart_ld + col] = cs;
 }
 
-// Pass 2 onwards (S > 0): G = c exp(Z - lse) -> bf16 G; db_s = column sums of G (+ loss sum);
-// dW_s = G^T h and dh = G W_s [+ g * bf16(w_true)] in one persistent launch.
-static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const float* g_true,
-                             const void* w_true, float* zlab, cudaStream_t st) {
+// Pass 1: per-row (max, sum 2^x) of each half tile, log2 domain.
+// zstore: also keep the logits (fp32 Z) for the gradient pass (the full fwd+bwd call).
+static int32_t bf16_stats(const tfs_ssm_args* a, const Bf16Plan& p, bool zstore,
+                          cudaStream_t st) {
+  const umma::Operand hK{p.w.hb, p.w.ldh, false}, wsK{p.w.wsb, a->dim, false};
+  umma::EpiParams ep = p.ep;
+  ep.zstore = (zstore && p.w.Z != nullptr) ? 1 : 0;
+  return umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)a->B, (int)a->S, a->dim, p.bn,
+                                    p.groups, ep, ep.zstore ? p.w.Z : nullptr, p.w.Spad, st);
+}
+
+// dW_s = G^T h and dh = G W_s [+ g * bf16(w_true)] from the bf16 G, in one persistent launch.
+static int32_t bf16_store(const tfs_ssm_args* a, const Bf16Plan& p, const float* g_true,
+                          const void* w_true, cudaStream_t st) {
   const int64_t B = a->B, S = a->S;
   const int32_t d = a->dim;
   const Bf16Ws& w = p.w;
-  umma::EpiParams ep = p.ep;
-  ep.zlab = zlab;
-  // db_s = column sums of G.  When G is larger than L2 can keep (Z: 1 GB), the GRAD epilogue
-  // sums each 32-row slab it stages (+8 us on X's GRAD, but no 1 GB re-read: Z -4.5 %, A/B
-  // round 2, profiles/r2_ab_grad_colsum.log); otherwise a separate pass over G is cheaper.
-  const bool fused_colsum = B * S * 2 > (64ll << 20);
-  if (fused_colsum) {
-    ep.colpart = w.colpart;
-    ep.colpart_ld = w.Spad;
-  }
   using umma::Operand;
-  const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
-  int32_t rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, p.bn,
-                                          p.groups, ep, w.G,
-                                          w.Sp, st);
-  if (rc != TFS_OK) return rc;
-  mark(a, 4, st);
-  if (fused_colsum) {
-    const int64_t ncb = cdiv(S, kDbCols);
-    ::tfs::launch(db_colpart_kernel, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kDbGroups * kDbCols, 0, st, 
-        w.colpart, w.nslabs, w.Spad, S, a->db_s, a->sampled, const_cast<int2*>(ep.cmap),
-        ep.vocab, a->loss, B, a->grad_scale, a->loss_sum);
-  } else {
-    const int64_t ncb = cdiv(S, kColsumChunks * 8);
-    const bool narrow = ncb < num_sms();
-    auto colsum = narrow ? g_colsum_kernel<256> : g_colsum_kernel<64>;
-    ::tfs::launch(colsum, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kColsumChunks * (narrow ? 256 : 64), 0, st, w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
-                   a->loss, a->grad_scale, a->loss_sum);
-  }
-  launched();
-  mark(a, 5, st);
+  int32_t rc = TFS_OK;
   // dW_s = G^T h (A = G MN-major, B = h MN-major) and dh = G W_s + g * bf16(w_true)
   // (A = G K-major, B = W_s MN-major) in one persistent launch; split partials are reduced in
   // split order by the finalize pass, which also adds the true-class term of dh.
@@ -1016,6 +1064,62 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   return TFS_OK;
 }
 
+// Pass 2 onwards (S > 0): G = c exp(Z - lse) -> bf16 G; db_s = column sums of G (+ loss sum);
+// dW_s = G^T h and dh = G W_s [+ g * bf16(w_true)] in one persistent launch.
+static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const float* g_true,
+                             const void* w_true, float* zlab, cudaStream_t st, bool z_stored = false) {
+  const int64_t B = a->B, S = a->S;
+  const int32_t d = a->dim;
+  const Bf16Ws& w = p.w;
+  umma::EpiParams ep = p.ep;
+  ep.zlab = zlab;
+  if (z_stored && w.Z != nullptr) {  // G (and the db_s slab partials) from the stored logits
+    const dim3 grid((unsigned)cdiv(B, 32), (unsigned)cdiv(S, 256));
+    auto gk = ep.label_in ? g_from_z_kernel<true> : g_from_z_kernel<false>;
+    ::tfs::launch(gk, grid, 256, 0, st, w.Z, w.Spad, B, S, a->lse, a->grad_scale, ep.labels,
+                  ep.cmap, ep.vocab, ep.S_pad, ep.sid, w.G, w.Sp, w.colpart, w.Spad, zlab);
+    launched();
+    mark(a, 4, st);
+    const int64_t ncb = cdiv(S, kDbCols);
+    ::tfs::launch(db_colpart_kernel, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kDbGroups * kDbCols,
+                  0, st, w.colpart, cdiv(B, 32), w.Spad, S, a->db_s, a->sampled,
+                  const_cast<int2*>(ep.cmap), ep.vocab, a->loss, B, a->grad_scale, a->loss_sum);
+    launched();
+    mark(a, 5, st);
+    return bf16_store(a, p, g_true, w_true, st);
+  }
+  // db_s = column sums of G.  When G is larger than L2 can keep (Z: 1 GB), the GRAD epilogue
+  // sums each 32-row slab it stages (+8 us on X's GRAD, but no 1 GB re-read: Z -4.5 %, A/B
+  // round 2, profiles/r2_ab_grad_colsum.log); otherwise a separate pass over G is cheaper.
+  const bool fused_colsum = B * S * 2 > (64ll << 20);
+  if (fused_colsum) {
+    ep.colpart = w.colpart;
+    ep.colpart_ld = w.Spad;
+  }
+  using umma::Operand;
+  const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
+  int32_t rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, p.bn,
+                                          p.groups, ep, w.G,
+                                          w.Sp, st);
+  if (rc != TFS_OK) return rc;
+  mark(a, 4, st);
+  if (fused_colsum) {
+    const int64_t ncb = cdiv(S, kDbCols);
+    ::tfs::launch(db_colpart_kernel, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kDbGroups * kDbCols, 0, st, 
+        w.colpart, w.nslabs, w.Spad, S, a->db_s, a->sampled, const_cast<int2*>(ep.cmap),
+        ep.vocab, a->loss, B, a->grad_scale, a->loss_sum);
+  } else {
+    const int64_t ncb = cdiv(S, kColsumChunks * 8);
+    const bool narrow = ncb < num_sms();
+    auto colsum = narrow ? g_colsum_kernel<256> : g_colsum_kernel<64>;
+    ::tfs::launch(colsum, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kColsumChunks * (narrow ? 256 : 64), 0, st, w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
+                   a->loss, a->grad_scale, a->loss_sum);
+  }
+  launched();
+  mark(a, 5, st);
+  return bf16_store(a, p, g_true, w_true, st);
+}
+
 static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   const int64_t B = a->B, S = a->S;
   const int32_t d = a->dim;
@@ -1027,7 +1131,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
   if (rc != TFS_OK) return rc;
   mark(a, 1, st);
   if (S > 0) {
-    rc = bf16_stats(a, p, st);
+    rc = bf16_stats(a, p, true, st);
     if (rc != TFS_OK) return rc;
   }
   mark(a, 2, st);
@@ -1045,7 +1149,7 @@ static int32_t ssm_bf16(const tfs_ssm_args* a, void* ws, cudaStream_t st) {
     TFS_LAUNCH_CHECK();
     return TFS_OK;
   }
-  return bf16_backward(a, p, a->db_true, a->w_true, nullptr, st);
+  return bf16_backward(a, p, a->db_true, a->w_true, nullptr, st, /*z_stored=*/true);
 }
 
 // Warp per row: (max, sum) over all of the row's half-tile partials, log2 domain, combined in a
@@ -1152,7 +1256,7 @@ extern "C" int32_t tfs_ssm_partial_stats(const tfs_ssm_args* a, float* row_stats
   Bf16Plan p;
   bf16_plan(a, ws, &p);
   if ((rc = bf16_prep(a, p, st)) != TFS_OK) return rc;
-  if ((rc = bf16_stats(a, p, st)) != TFS_OK) return rc;
+  if ((rc = bf16_stats(a, p, false, st)) != TFS_OK) return rc;
   ::tfs::launch(row_stats_kernel, (unsigned)cdiv(a->B, 8), 256, 0, st, p.w.stats, 2 * p.num_n, a->B,
                                                             reinterpret_cast<float2*>(row_stats));
   launched();
@@ -1205,3 +1309,5 @@ extern "C" int32_t tfs_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn,
   TFS_LAUNCH_CHECK();
   return TFS_OK;
 }
+
+extern "C" int32_t tfs_ssm_grad_from_logits(void) { return TFS_SSM_ZPASS ? 1 : 0; }

@@ -41,6 +41,16 @@ namespace umma {
 #define TFS_STORE_CTA 2
 #endif
 constexpr int kSoftmaxCta = 1, kStoreCta = TFS_STORE_CTA;
+
+// TFS_SSM_ZPASS=1 builds (A/B only): the logits GEMM also stores the logits (fp32 Z, B x Spad)
+// and G is formed from them in an elementwise pass instead of recomputing the logits on the
+// tensor cores (the GRAD GEMM).  Measured round 2 (profiles/r2_ab_zpass.log): SLOWER -- X 186.7
+// vs 184.9 us (STATS 33 -> 39 us with the store, the pass 39 us vs GRAD 36 us), Z 2691 vs 2454
+// us (STATS 549 -> 724 us writing 2.2 GB, the pass 845 vs GRAD 772 us).  On B200 the recompute
+// is cheaper than the logits' round trip through memory, so the product keeps it.
+#ifndef TFS_SSM_ZPASS
+#define TFS_SSM_ZPASS 0
+#endif
 static_assert(kStoreCta == 1 || kStoreCta == 2, "kStoreCta");
 constexpr int BM = 128, BN = 256, BK = 64;      // BM: rows per CTA; BN: tile N
 constexpr int STAGES = 4;                       // stages at the widest tile (BN); a launch with
@@ -90,6 +100,11 @@ struct EpiParams {
   // without a map (vocab == 0) the range is every column), and the per-element id compare runs
   // only for chunks that intersect that range.
   CUtensorMap tG;      // GRAD: store map of bf16 G [M x ldG], box {32, 32}, 64-byte swizzle
+  // STATS with zstore != 0: v (the corrected log2-unit logits, exclusions applied) is also
+  // written to fp32 Z [M x ldz] through tZ (box {16, 32}), so the gradient pass can form G from
+  // it instead of recomputing the logits GEMM (bit-identical G: same v, same arithmetic).
+  CUtensorMap tZ;
+  int zstore;
   const float* cb;
   const int32_t* sid;
   const int64_t* labels;
@@ -372,8 +387,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const int B_BYTES = P.b_stride;
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * KSUB * A_BYTES;
-  uint8_t* sE = sB + STAGES * KSUB * B_BYTES;          // epilogue staging (not for STATS)
-  float* sCb = reinterpret_cast<float*>(sE + (MODE == kStats ? 0 : kEpiSmem));  // [acc][half][128]
+  uint8_t* sE = sB + STAGES * KSUB * B_BYTES;  // epilogue staging (STATS: only to store Z)
+  float* sCb = reinterpret_cast<float*>(sE + (MODE == kStats && !TFS_SSM_ZPASS ? 0 : kEpiSmem));
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCb) + kCbSmem);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
@@ -610,6 +625,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             run_s = run_s * fast_exp2(run_m - nm) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
             run_m = nm;
           }
+          if (TFS_SSM_ZPASS && ep.zstore) {  // v -> Z (two 16-column halves via the slabs)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              uint4 x[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                x[k] = make_uint4(__float_as_uint(v[16 * h2 + 4 * k]),
+                                  __float_as_uint(v[16 * h2 + 4 * k + 1]),
+                                  __float_as_uint(v[16 * h2 + 4 * k + 2]),
+                                  __float_as_uint(v[16 * h2 + 4 * k + 3]));
+              uint8_t* sb = stg + (nst & 1) * kStageBytes;
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+              stage_row64(sb, lane, x);
+              fence_proxy_async();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&ep.tZ, sb, col0 + 16 * h2, row0);
+                bulk_commit();
+              }
+              ++nst;
+            }
+          }
         } else if (MODE == kGrad) {
           uint4 x[4];
           if (LAB) {  // G = c (p - 1) at the label's column
@@ -779,8 +817,9 @@ int effective_split(int K, int ksplit);
 
 // STATS / GRAD launch; for GRAD, G (bf16 [M x ldG], ldG % 8 == 0) receives the gradient.
 // bn: tile width along N (pick_bn); cb / sid must be readable up to num_n * bn + 256 columns.
+// STATS with ep.zstore: G / ldG are the fp32 logits buffer Z and its row stride instead.
 int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K, int bn, int sms,
-                             EpiParams ep, uint16_t* G, int64_t ldG, cudaStream_t st);
+                             EpiParams ep, void* G, int64_t ldG, cudaStream_t st);
 // Tile width for an M x N output of single-pass tiles: the multiple of 32 in [128, 256] that
 // minimises the makespan (rounds of tiles over the CTA groups x tile width).
 int pick_bn(int M, int N, int sms);
