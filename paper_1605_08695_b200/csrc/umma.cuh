@@ -4,22 +4,24 @@
 // MN-major (row-major [K x rows]: the transposed view), selected per launch, so the softmax
 // backward reads G, W_s and h in the layout they already have -- no transposed copies.
 //
-// CTA pairs (clusters of 2, tcgen05 cta_group::2): a pair owns a 256 x 256 output tile, CTA r
-// holding rows [128 r, +128) of it (A half) and B rows [r N/2, +N/2) of the operand; the
-// leader's single MMA thread multiplies across both CTAs' smem (per-CTA operand traffic per MMA
-// is 2/3 of a 1-CTA 128 x 256 tile).  Persistent over (problem, m-pair, n-tile, k-split) units.
-// CTA = 12 warps:
-//   warp 0      TMA producer (one lane, both CTAs): A 128x64 + B 128x64 per stage, 128-byte
-//               swizzle, 6-stage ring; both CTAs' loads complete on the leader's full barrier.
-//   warp 1      MMA issuer (one lane, leader only): 4 x tcgen05.mma.cta_group::2.kind::f16
-//               (M=256, N<=256, K=16) per stage into one of two 256-column TMEM accumulators;
-//               tcgen05.commit multicasts stage release / accumulator ready to both CTAs.
-//   warp 2      TMEM allocator (512 columns = both accumulators, cta_group::2).
+// Persistent over (problem, m-tile, n-tile, k-split) units, one CTA per SM (or one CTA pair per
+// two SMs).  CTAs per tile (CT) is a template parameter chosen per launch kind: the logits
+// (STATS) and gradient (GRAD) passes run one CTA per 128 x bn tile (cta_group::1); the grouped
+// STORE GEMM runs CTA pairs (clusters of 2, cta_group::2): a pair owns a 256 x 256 tile, CTA r
+// holding rows [128 r, +128) (its A half) and B rows [r N/2, +N/2), the leader's MMA thread
+// multiplying across both CTAs' smem.  CTA = 12 warps:
+//   warp 0      TMA producer (one lane): A 128 x 64 and B bn/CT x 64 tiles, 128-byte swizzle,
+//               two k-blocks per stage of an mbarrier ring (as many stages as the launch's smem
+//               allows); in pairs both CTAs' loads complete on the leader's full barrier.
+//   warp 1      MMA issuer (one lane; the pair's leader): tcgen05.mma.cta_group::CT.kind::f16
+//               (M = 128 CT, N <= 256, K = 16) into one of two 256-column TMEM accumulators;
+//               tcgen05.commit releases stages / publishes the accumulator (to both CTAs).
+//   warp 2      TMEM allocator (512 columns = both accumulators).
 //   warps 4-11  epilogue: warp w reads TMEM lanes 32*(w%4).. (its 32 rows), columns
-//               [128*((w-4)/4), +128) in 32-column tcgen05.ld chunks, applies the fused epilogue
-//               and frees the accumulator, so the epilogue of tile i overlaps the MMAs of i+1.
-//               Results leave through per-warp swizzled smem buffers and TMA bulk-tensor stores
-//               (full 64-byte row segments, bounds clipped by the tensor map).
+//               [128*((w-4)/4), +128) in 32-column tcgen05.ld chunks (double-buffered), applies
+//               the fused epilogue and frees the accumulator, so the epilogue of tile i overlaps
+//               the MMAs of tile i+1.  Results leave through per-warp swizzled smem slabs and
+//               TMA bulk-tensor stores (full 64-byte row segments, clipped by the tensor map).
 // Epilogue modes: STATS (row max / sum of 2^x of the corrected logits per half
 // tile, log2 domain), GRAD (G = c exp(Z - lse) -> bf16 G), STORE (fp32 product or split-K
 // partial, optional extra term g[m] * bf16(wt[m, n])).
