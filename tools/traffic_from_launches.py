@@ -11,7 +11,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SSM = ("prep_kernel", "gemm_kernel<0", "bf16_combine", "gemm_kernel<1", "g_colsum",
+SSM = ("prep_kernel", "gemm_kernel<0", "bf16_combine", "gemm_kernel<1", "g_colsum", "db_colpart",
        "gemm_kernel<2", "split_finalize")
 
 
