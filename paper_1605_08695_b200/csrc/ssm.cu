@@ -134,21 +134,22 @@ static int groups_or_all(int sms, int ct) {
   return sms > 0 ? std::max(1, std::min(sms / ct, all)) : all;
 }
 
-template <int MODE, bool LAB = false>
-static int32_t launch_params(Params P, int sms, cudaStream_t st) {
+template <int MODE, bool LAB, int MC>
+static int32_t launch_params_mc(Params P, int sms, cudaStream_t st) {
   constexpr int CT = MODE == kStore ? kStoreCta : kSoftmaxCta;
+  constexpr int CL = CT * MC;
   stage_plan<MODE, CT>(P);
   static bool attr_done = false;
   if (!attr_done) {
-    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, LAB, CT>,
+    TFS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, LAB, CT, MC>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmemBytes));
     attr_done = true;
   }
   // persistent: one CTA (or CTA pair: a cluster of 2 on one TPC) per SM (or per two SMs)
-  const int groups = std::min(P.total_units, groups_or_all(sms, CT));
+  const int groups = std::min(P.total_units, groups_or_all(sms, CL));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(CT * groups));
+  cfg.gridDim = dim3((unsigned)(CL * groups));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
@@ -158,15 +159,15 @@ static int32_t launch_params(Params P, int sms, cudaStream_t st) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na++].val.programmaticStreamSerializationAllowed = 1;
   }
-  if (CT > 1) {  // CTA pairs: a cluster of 2 (plain launch for single-CTA tiles)
+  if (CL > 1) {  // CTA pairs / multicast pairs: a cluster of 2 (else a plain launch)
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = CT;
+    attr[na].val.clusterDim.x = CL;
     attr[na].val.clusterDim.y = 1;
     attr[na++].val.clusterDim.z = 1;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, LAB, CT>, P));
+  TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, LAB, CT, MC>, P));
   launched();
   TFS_LAUNCH_CHECK();
   if (std::getenv("TFS_DEBUG_SYNC") != nullptr) {  // diagnostics: attribute faults to a mode
@@ -180,12 +181,32 @@ static int32_t launch_params(Params P, int sms, cudaStream_t st) {
   return TFS_OK;
 }
 
+// mc: 2 = the logits / gradient GEMM shares B tiles across a cluster of 2 (softmax_mc).
+template <int MODE, bool LAB = false>
+static int32_t launch_params(Params P, int sms, cudaStream_t st, int mc = 1) {
+  if constexpr (MODE == kStore) {
+    return launch_params_mc<MODE, LAB, 1>(P, sms, st);
+  } else {
+    return mc == 2 ? launch_params_mc<MODE, LAB, 2>(P, sms, st)
+                   : launch_params_mc<MODE, LAB, 1>(P, sms, st);
+  }
+}
+
+// Multicast B in the logits / gradient GEMMs (gemm_kernel's MC = 2) for tall problems: A/B
+// round 2 (profiles/r2_ab_mcast_b.log): Z STATS 539 -> 520 us, GRAD 807 -> 782 us; no gain at X
+// (B = 2,560 rows: 184.0 vs 185.6 us), so below TFS_MCAST_MIN_ROWS rows every CTA loads its B.
+#ifndef TFS_MCAST_MIN_ROWS
+#define TFS_MCAST_MIN_ROWS 16384
+#endif
+static int softmax_mc(int M) { return (TFS_MCAST_B && M >= TFS_MCAST_MIN_ROWS) ? 2 : 1; }
+
 int pick_bn(int M, int N, int sms) {
-  const int64_t groups = groups_or_all(sms, kSoftmaxCta);
+  const int mc = softmax_mc(M);
+  const int64_t groups = groups_or_all(sms, kSoftmaxCta * mc);
   int best = BN;
   int64_t best_cost = -1;
   for (int bn = BN; bn >= 128; bn -= 32) {
-    const int64_t tiles = cdiv(M, kSoftmaxCta * BM) * cdiv(N, bn);
+    const int64_t tiles = cdiv(M, kSoftmaxCta * mc * BM) * cdiv(N, bn);
     const int64_t cost = cdiv(tiles, groups) * bn;
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
@@ -200,7 +221,8 @@ int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K
                              cudaStream_t st) {
   if (A.mn || B.mn) return TFS_ERR_INVALID_ARGUMENT;
   Params P{};
-  int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1, kSoftmaxCta, bn);
+  const int mc = softmax_mc(M);
+  int32_t rc = fill_problem(P.p[0], A, B, M, N, K, 1, kSoftmaxCta * mc, bn);
   if (rc != TFS_OK) return rc;
   P.nprob = 1;
   P.total_units = P.p[0].units;
@@ -215,9 +237,10 @@ int32_t launch_stats_or_grad(int mode, Operand A, Operand B, int M, int N, int K
   }
   P.ep = ep;
   if (ep.label_in)
-    return mode == kStats ? launch_params<kStats, true>(P, groups, st)
-                          : launch_params<kGrad, true>(P, groups, st);
-  return mode == kStats ? launch_params<kStats>(P, groups, st) : launch_params<kGrad>(P, groups, st);
+    return mode == kStats ? launch_params<kStats, true>(P, groups, st, mc)
+                          : launch_params<kGrad, true>(P, groups, st, mc);
+  return mode == kStats ? launch_params<kStats>(P, groups, st, mc)
+                        : launch_params<kGrad>(P, groups, st, mc);
 }
 
 // Up to two STORE GEMMs in one persistent launch; the caller orders them by unit size.
@@ -831,7 +854,7 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, int64_t 
   x.part_dws = c.take<float>(umma::part_floats((int)S, d, ks_dws));
   x.cb = c.take<float>(Spad);
   x.sid = c.take<int32_t>(Spad);
-  x.nslabs = cdiv(std::max<int64_t>(B, 1), umma::BM) * 4;  // GRAD: one CTA per 128-row tile
+  x.nslabs = cdiv(std::max<int64_t>(B, 1), 2 * umma::BM) * 2 * 4;  // GRAD: 32-row slabs (MC <= 2)
   x.colpart = c.take<float>((size_t)x.nslabs * Spad);
   x.Z = TFS_SSM_ZPASS ? c.take<float>((size_t)std::max<int64_t>(B, 1) * Spad) : nullptr;
   x.Sp = Sp;

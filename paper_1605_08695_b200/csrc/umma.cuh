@@ -43,6 +43,11 @@ namespace umma {
 #define TFS_STORE_CTA 2
 #endif
 constexpr int kSoftmaxCta = 1, kStoreCta = TFS_STORE_CTA;
+// Logits / gradient passes may run clusters of 2 single-CTA tiles sharing each B tile by TMA
+// multicast (gemm_kernel's MC, chosen per launch by size in ssm.cu); 0: never.
+#ifndef TFS_MCAST_B
+#define TFS_MCAST_B 1
+#endif
 
 // TFS_SSM_ZPASS=1 builds (A/B only): the logits GEMM also stores the logits (fp32 Z, B x Spad)
 // and G is formed from them in an elementwise pass instead of recomputing the logits on the
@@ -213,6 +218,24 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
         : "memory");
   }
 }
+// Multicast load: the box lands at the same smem offset in every CTA of ctaMask and each
+// destination's mbarrier at offset `bar` receives the byte count.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1,
+                                               uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// Single-CTA MMAs' completion signalled on the mbarrier at this offset in every CTA of ctaMask.
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 template <int CT>
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   if constexpr (CT == 1) return 0;
@@ -378,9 +401,14 @@ __device__ __forceinline__ void stage_row64(uint8_t* buf, int lane, const uint4 
 
 // LAB: the label-in-candidates epilogue (EpiParams::label_in), a separate instantiation so the
 // sampled-softmax kernels compile exactly as without it.
-template <int MODE, bool LAB = false, int CT = 1>
+// MC = 2 (with CT = 1): clusters of two single-CTA tiles stacked along M share each B tile --
+// CTA r loads B rows [r bn/2, +bn/2) and multicasts them into both CTAs' stage, so each CTA
+// issues half of the B traffic; a stage is refilled once BOTH CTAs' MMAs have read it.
+template <int MODE, bool LAB = false, int CT = 1, int MC = 1>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Params P) {
-  constexpr int PM = CT * BM;  // rows per tile
+  static_assert(MC == 1 || CT == 1, "multicast B is for single-CTA tiles");
+  constexpr int CL = CT * MC;  // CTAs per cluster
+  constexpr int PM = CL * BM;  // rows per unit
   extern __shared__ __align__(1024) uint8_t smem[];
   // PDL (common.cuh): this grid's setup (barriers, TMEM, descriptor prefetch) may overlap the
   // previous kernel's tail; its results are waited for below.
@@ -399,15 +427,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const EpiParams& ep = P.ep;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank<CT>();  // 0 = leader (issues the MMAs)
-  const bool leader = rank == 0;
-  const int pair = blockIdx.x / CT, npairs = gridDim.x / CT;  // tile-owning CTA groups
+  const uint32_t rank = cluster_ctarank<CL>();  // CT = 2: 0 = leader (issues the MMAs)
+  const bool leader = CT == 1 || rank == 0;
+  const int pair = blockIdx.x / CL, npairs = gridDim.x / CL;  // tile-owning CTA groups
 
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem) & 1023u) != 0) __trap();  // swizzled tiles need 1 KB alignment
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);   // leader: its expect_tx arrival + both CTAs' TMA bytes
-      mbar_init(empty + s, 1);  // the leader's multicast commit
+      mbar_init(empty + s, MC);  // the leader's (multicast) commit; MC = 2: both CTAs' MMAs
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
@@ -426,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::%0.sync.aligned;" ::"n"(CT));
   }
   tc_fence_before();
-  cluster_sync_all<CT>();  // barriers of both CTAs initialised, TMEM allocated
+  cluster_sync_all<CL>();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid's outputs are visible
@@ -439,18 +467,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int u = pair; u < P.total_units; u += npairs) {
         const Unit t = decode_unit(P, u);
         const Problem& q = P.p[t.pi];
-        const int nh = t.nw / CT;  // B rows this CTA holds
+        const int nh = t.nw / CL;  // B rows this CTA loads (CT = 2: holds)
         const int bboxes = q.b_mn ? (nh + kMNBox - 1) / kMNBox : 0;
         const uint32_t bbytes = q.b_mn ? (uint32_t)(bboxes * kMNBoxBytes)
-                                       : (uint32_t)((q.bn / CT) * BK * 2);  // box: bn/CT rows
+                                       : (uint32_t)((q.bn / CL) * BK * 2);  // box: bn/CL rows
         const int arow = t.mt * PM + (int)rank * BM;
-        const int bcol = t.nt * q.bn + (int)rank * nh;
+        const int bcol = t.nt * q.bn + (int)rank * (MC == 2 ? q.bn / 2 : nh);
         for (int kb0 = t.kb0; kb0 < t.kb1; kb0 += KSUB) {
           const int ns = min(KSUB, t.kb1 - kb0);
           mbar_wait(empty + stage, phase ^ 1);
           // the leader's barrier (peer bit cleared)
           const uint32_t fb = smem_u32(full + stage) & (CT == 2 ? 0xFEFFFFFFu : 0xFFFFFFFFu);
-          if (leader) mbar_expect_tx(full + stage, CT * ns * (A_BYTES + bbytes));
+          if (leader) mbar_expect_tx(full + stage, ns * (CT * A_BYTES + CL * bbytes));
           for (int sb = 0; sb < ns; ++sb) {
             const int kb = kb0 + sb;
             uint8_t* a = sA + (stage * KSUB + sb) * A_BYTES;
@@ -462,7 +490,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             } else {
               tma_load_2d_pair<CT>(a, &q.ta, kb * BK, arow, fb);
             }
-            if (q.b_mn) {
+            if (MC == 2) {  // K-major B (STATS / GRAD): this CTA's half into both CTAs
+              tma_load_2d_mc(b + (size_t)rank * (q.bn / 2) * (BK * 2), &q.tb, kb * BK, bcol,
+                             full + stage, (uint16_t)3);
+            } else if (q.b_mn) {
               for (int i = 0; i < bboxes; ++i)
                 tma_load_2d_pair<CT>(b + i * kMNBoxBytes, &q.tb, bcol + i * kMNBox, kb * BK, fb);
             } else {
@@ -484,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int u = pair; u < P.total_units; u += npairs) {
         const Unit t = decode_unit(P, u);
         const bool amn = P.p[t.pi].a_mn != 0, bmn = P.p[t.pi].b_mn != 0;
-        const uint32_t idesc = make_idesc(amn, bmn, t.nw, PM);
+        const uint32_t idesc = make_idesc(amn, bmn, t.nw, CT * BM);
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -501,7 +532,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               umma_bf16<CT>(d_tmem, operand_desc(amn, a0, k), operand_desc(bmn, b0, k), idesc,
                         (kb > t.kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit_pair<CT>(empty + stage);
+          if (MC == 2)
+            umma_commit_mc(empty + stage, (uint16_t)3);  // both CTAs may refill their halves
+          else
+            umma_commit_pair<CT>(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -685,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             tma_store_2d(&ep.tG, sb, col0, row0);
             bulk_commit();
           }
-          if (ep.colpart != nullptr) {  // db_s partial: column `lane` of the staged slab
+          if (ep.colpart != nullptr && row0 < M) {  // db_s partial: column `lane` of the slab
             const int nrows = min(32, M - row0);
             const int k16 = lane >> 3, e2 = (lane & 7) * 2;
             float cs = 0.f;
@@ -695,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                   *reinterpret_cast<const uint16_t*>(sb + r * 64 + ((k16 ^ ((r >> 1) & 3)) << 4) + e2);
               if (r < nrows) cs += __uint_as_float(gb << 16);
             }
-            const int64_t slab = ((int64_t)t.mt * CT + rank) * 4 + quarter;
+            const int64_t slab = ((int64_t)t.mt * CL + rank) * 4 + quarter;
             ep.colpart[slab * ep.colpart_ld + col0 + lane] = cs;
           }
           ++nst;
@@ -782,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
   // Neither CTA may leave (or free TMEM) while its peer can still reach its smem / TMEM.
   tc_fence_before();
-  cluster_sync_all<CT>();
+  cluster_sync_all<CL>();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::%2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
