@@ -605,7 +605,10 @@ __device__ __forceinline__ PieceDst piece_dst(bool starts_before, bool ends_afte
 // written; pieces of segments crossing the window's edges go to the partial slots (2c: the
 // piece of the segment that started before window c; 2c + 1: the piece of the segment that
 // starts in c and continues after it) and the segment to cross_list.
-constexpr int kWinBatch = 8;
+#ifndef TFS_WIN_BATCH
+#define TFS_WIN_BATCH 8
+#endif
+constexpr int kWinBatch = TFS_WIN_BATCH;  // rows per two pipelined half-batches
 constexpr int kRunWin = 16;  // windows per level-1 block of a crossing segment
 
 template <int OPT, bool WR>
