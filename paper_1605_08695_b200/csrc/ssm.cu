@@ -110,6 +110,9 @@ static int32_t fill_problem(Problem& p, Operand A, Operand B, int M, int N, int 
   ksplit = std::max(1, std::min(ksplit, p.kb_total));
   p.kb_per_split = (int)cdiv(p.kb_total, ksplit);
   p.ksplit = (int)cdiv(p.kb_total, p.kb_per_split);
+  p.fd_ks = FastDiv::make((uint32_t)p.ksplit);
+  p.fd_m = FastDiv::make((uint32_t)p.num_m);
+  p.fd_n = FastDiv::make((uint32_t)p.num_n);
   p.units = p.num_m * p.num_n * p.ksplit;
   p.a_mn = A.mn;
   p.b_mn = B.mn;

@@ -134,6 +134,23 @@ struct EpiParams {
   int64_t colpart_ld;
 };
 
+// Division by a launch constant without the integer-divide sequence: the unit decode runs on
+// the single producer / MMA threads at every tile boundary, where a ~40-instruction dependent
+// divide chain showed as ~0.4 us per tile (role timeline, round 2).  q = (umulhi(n, mul) + n)
+// >> shift, exact for n < 2^31 and 1 <= d < 2^31 (mul, shift from FastDiv::make on the host).
+struct FastDiv {
+  uint32_t d, mul, shift;
+  static FastDiv make(uint32_t d) {
+    FastDiv f{d, 0, 0};
+    while ((1ull << f.shift) < d) ++f.shift;
+    f.mul = (uint32_t)(((1ull << 32) * ((1ull << f.shift) - d)) / d + 1);
+    return f;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(n, mul) + n) >> shift);
+  }
+};
+
 // One GEMM of a launch (a launch may carry two: the softmax backward runs dh and dW_s together
 // so their tiles share the 148 SMs).  STORE epilogue: out[m, n] = acc (+ g[m] * bf16(wt[m, n]))
 // when ksplit == 1; with K split `ksplit` ways each split writes its partial to
@@ -144,6 +161,7 @@ struct Problem {
   int M, N, K;
   int bn;  // tile width along N: a multiple of 32, <= BN (STATS / GRAD pick it to balance SMs)
   int num_m, num_n, ksplit, kb_per_split, kb_total, units;
+  FastDiv fd_ks, fd_m, fd_n;  // by ksplit, num_m, num_n
   int a_mn, b_mn;
   int n_fast;       // unit order: n-tiles fastest (A larger than L2 can keep) or m-tiles fastest
   const float* g;   // optional row scale of the extra term (ksplit == 1 only)
@@ -374,14 +392,14 @@ __device__ __forceinline__ Unit decode_unit(const Params& P, int u) {
   // both stay in L2), or -- when A is too large for L2 (h and G at Z) -- n-tiles, so the
   // n-tiles of one A block run together and A comes from DRAM once (measured, round 2:
   // Z 2853 -> 2656 us per step; X 207 -> 216 us the other way round)
-  r.ks = v % q.ksplit;
-  const int t = v / q.ksplit;
+  const int t = (int)q.fd_ks.div((uint32_t)v);
+  r.ks = v - t * q.ksplit;
   if (q.n_fast) {
-    r.nt = t % q.num_n;
-    r.mt = t / q.num_n;
+    r.mt = (int)q.fd_n.div((uint32_t)t);
+    r.nt = t - r.mt * q.num_n;
   } else {
-    r.mt = t % q.num_m;  // m-pair index (PM rows)
-    r.nt = t / q.num_m;
+    r.nt = (int)q.fd_m.div((uint32_t)t);
+    r.mt = t - r.nt * q.num_m;  // m-pair index (PM rows)
   }
   r.kb0 = r.ks * q.kb_per_split;
   r.kb1 = min(q.kb_total, r.kb0 + q.kb_per_split);
