@@ -10,6 +10,7 @@
 // Every reduction has a fixed order (split-K partials are summed in split order), so outputs
 // are run-to-run bit-identical.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <mutex>
@@ -128,7 +129,8 @@ static void stage_plan(Params& P) {
   P.b_stride = (bmax + 1023) / 1024 * 1024;
   const int fixed = (MODE == kStats && !TFS_SSM_ZPASS ? 0 : kEpiSmem) + kCbSmem + kBarBytes;
   P.stages =
-      std::min<int>(kMaxStages, ((int)kSmemBytes - fixed) / (KSUB * (A_BYTES + P.b_stride)));
+      std::min<int>(kMaxStages,
+                    ((int)kSmemBytes - fixed) / (ksub_of(MODE) * (A_BYTES + P.b_stride)));
 }
 
 // sms: the SMs a persistent launch may use (<= 0: every SM) -> its CTA groups of ct CTAs.
@@ -173,6 +175,20 @@ static int32_t launch_params_mc(Params P, int sms, cudaStream_t st) {
   TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, LAB, CT, MC>, P));
   launched();
   TFS_LAUNCH_CHECK();
+#ifdef TFS_GEMM_TRACE
+  if (std::getenv("TFS_TRACE_DUMP") != nullptr) {  // eager calls only (synchronizes)
+    cudaStreamSynchronize(st);
+    static unsigned long long h[4][512];
+    cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
+    fprintf(stderr, "TRACE mode=%d units=%d grid=%d stages=%d:", MODE, P.total_units,
+            (int)cfg.gridDim.x, P.stages);
+    for (int i = 0; i < 512; ++i)
+      if (h[MODE][i]) fprintf(stderr, " %d:%lld", i, (long long)(h[MODE][i] - h[MODE][0]));
+    fprintf(stderr, "\n");
+    static unsigned long long zero[4][512];
+    cudaMemcpyToSymbol(g_trace, zero, sizeof(zero));
+  }
+#endif
   if (std::getenv("TFS_DEBUG_SYNC") != nullptr) {  // diagnostics: attribute faults to a mode
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {

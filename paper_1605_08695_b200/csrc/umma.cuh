@@ -62,10 +62,18 @@ static_assert(kStoreCta == 1 || kStoreCta == 2, "kStoreCta");
 constexpr int BM = 128, BN = 256, BK = 64;      // BM: rows per CTA; BN: tile N
 constexpr int STAGES = 4;                       // stages at the widest tile (BN); a launch with
 constexpr int kMaxStages = 8;                   // narrower tiles / no staging fits more (Params)
-#ifndef TFS_KSUB
-#define TFS_KSUB 2
+// k-blocks per pipeline stage (one barrier pair each), per launch kind: the logits / gradient
+// passes (K = d = 512: 8 k-blocks a tile) refill one k-block at a time (4-5 stages in flight),
+// the long-K grouped STORE two (measured round 2, profiles/r2_ab_ksub.log).
+#ifndef TFS_KSUB_SOFTMAX
+#define TFS_KSUB_SOFTMAX 1
 #endif
-constexpr int KSUB = TFS_KSUB;                  // k-blocks per pipeline stage (one barrier each)
+#ifndef TFS_KSUB_STORE
+#define TFS_KSUB_STORE 2
+#endif
+__host__ __device__ constexpr int ksub_of(int mode) {
+  return mode == 2 /* kStore */ ? TFS_KSUB_STORE : TFS_KSUB_SOFTMAX;
+}
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + kEpiWarps * 32;  // 384
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
@@ -181,6 +189,22 @@ struct Params {
   int b_stride;
   EpiParams ep;
 };
+
+// ---- role timeline (TFS_GEMM_TRACE builds only; results unchanged) ------------------------------
+// clock64 stamps of CTA 0's roles per launch kind (tools/gemm_timeline.py prints them): slot 0
+// setup done; 16+ producer stage ready; 128+ MMA tile start; 144+ MMA tile issued; 160+ MMA
+// stage data arrived; 288+ / 304+ epilogue (warp 4) tile ready / done.
+#ifdef TFS_GEMM_TRACE
+__device__ unsigned long long g_trace[4][512];
+#define TRACE(slot)                                                        \
+  do {                                                                     \
+    if (blockIdx.x == 0 && (slot) < 512) g_trace[MODE][(slot)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(slot) \
+  do {              \
+  } while (0)
+#endif
 
 // ---- PTX wrappers -----------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -434,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const int STAGES = P.stages;
   const int B_BYTES = P.b_stride;
   uint8_t* sA = smem;
+  constexpr int KSUB = ksub_of(MODE);
   uint8_t* sB = smem + STAGES * KSUB * A_BYTES;
   uint8_t* sE = sB + STAGES * KSUB * B_BYTES;  // epilogue staging (STATS: only to store Z)
   float* sCb = reinterpret_cast<float*>(sE + (MODE == kStats && !TFS_SSM_ZPASS ? 0 : kEpiSmem));
@@ -476,11 +501,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid's outputs are visible
+  if (threadIdx.x == 0) TRACE(0);
 
   if (warp == 0) {
     // ================================ TMA producer ================================
     if (lane == 0) {
       int stage = 0;
+      int tr_n = 0;  // (role timeline counter)
+      (void)tr_n;
       uint32_t phase = 0;
       for (int u = pair; u < P.total_units; u += npairs) {
         const Unit t = decode_unit(P, u);
@@ -494,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         for (int kb0 = t.kb0; kb0 < t.kb1; kb0 += KSUB) {
           const int ns = min(KSUB, t.kb1 - kb0);
           mbar_wait(empty + stage, phase ^ 1);
+          TRACE(16 + tr_n++);
           // the leader's barrier (peer bit cleared)
           const uint32_t fb = smem_u32(full + stage) & (CT == 2 ? 0xFEFFFFFFu : 0xFFFFFFFFu);
           if (leader) mbar_expect_tx(full + stage, ns * (CT * A_BYTES + CL * bbytes));
@@ -529,17 +558,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     // ================================ MMA issuer ==================================
     if (lane == 0 && leader) {
       int stage = 0, acc = 0;
+      int tr_t = 0, tr_s = 0;  // (role timeline counters)
+      (void)tr_t;
+      (void)tr_s;
       uint32_t phase = 0, acc_phase = 0;
       for (int u = pair; u < P.total_units; u += npairs) {
         const Unit t = decode_unit(P, u);
         const bool amn = P.p[t.pi].a_mn != 0, bmn = P.p[t.pi].b_mn != 0;
         const uint32_t idesc = make_idesc(amn, bmn, t.nw, CT * BM);
         mbar_wait(tempty + acc, acc_phase ^ 1);
+        TRACE(128 + tr_t);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         for (int kb0 = t.kb0; kb0 < t.kb1; kb0 += KSUB) {
           const int ns = min(KSUB, t.kb1 - kb0);
           mbar_wait(full + stage, phase);
+          TRACE(160 + tr_s++);
           tc_fence_after();
           for (int sb = 0; sb < ns; ++sb) {
             const int kb = kb0 + sb;
@@ -560,6 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
         umma_commit_pair<CT>(tfull + acc);
+        TRACE(144 + tr_t++);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -572,6 +607,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     uint8_t* stg = sE + ew * 2 * kStageBytes;
     uint32_t nst = 0;              // TMA stores issued by this warp (staging buffer parity)
     int acc = 0;
+    int tr_e = 0;  // (role timeline counter)
+    (void)tr_e;
     uint32_t acc_phase = 0;
     for (int u = pair; u < P.total_units; u += npairs) {
       const Unit t = decode_unit(P, u);
@@ -612,6 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       float run_m = -INFINITY, run_s = 0.f;
 
       mbar_wait(tfull + acc, acc_phase);
+      if (ew == 0 && lane == 0) TRACE(288 + tr_e);
       tc_fence_after();
       // Software-pipelined TMEM reads: chunk c+1 is in flight while chunk c is processed.
       const uint32_t tbase =
@@ -825,6 +863,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader<CT>(tempty + acc);  // the leader's barrier
+      if (ew == 0 && lane == 0) TRACE(304 + tr_e);
+      ++tr_e;
       if (MODE == kStats && row_ok)
         ep.stats[(int64_t)row * ep.nparts + t.nt * 2 + half] = make_float2(run_m, run_s);
       acc ^= 1;

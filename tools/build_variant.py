@@ -3,8 +3,8 @@
     python tools/build_variant.py OUT.so -DTFS_KSUB=1
     TFS_ALLOW_VARIANT_LIB=1 TFS_LIB=$PWD/OUT.so python tools/one_ssm.py      # run against it
 
-Tuning switches of the product source (every variant computes correct results): TFS_KSUB sets
-k-blocks per pipeline stage of the tcgen05 GEMM, TFS_STORE_CTA=1 builds the
+Tuning switches of the product source (every variant computes correct results): TFS_KSUB_* set
+k-blocks per pipeline stage (TFS_KSUB_SOFTMAX, TFS_KSUB_STORE), TFS_STORE_CTA=1 builds the
 grouped STORE GEMM with single CTAs instead of CTA pairs,
 TFS_SEG_CHUNK / TFS_SEG_MINB tune the sparse apply.  (Round 1's wrong-result role-isolation
 switches were removed from the product source; their numbers stay in profiles/r1_summary.md.)
