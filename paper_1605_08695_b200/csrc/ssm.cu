@@ -475,6 +475,9 @@ __global__ void to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
 // GROUPS row groups per block (4 GROUPS threads): 64 when there are enough 32-column blocks to
 // fill the GPU, 256 for narrow G (few column blocks: more rows in flight per block).
 constexpr int kColsumChunks = 4;
+#ifndef TFS_COLSUM_G256
+#define TFS_COLSUM_G256 0
+#endif
 template <int GROUPS>
 __global__ void __launch_bounds__(kColsumChunks * GROUPS) g_colsum_kernel(
     const uint16_t* G, int64_t B, int64_t S, int64_t ldG, float* db_s, const int64_t* sampled,
@@ -980,7 +983,7 @@ static int32_t bf16_prep(const tfs_ssm_args* a, const Bf16Plan& p, cudaStream_t 
   const int32_t d = a->dim;
   const float* le_s = (a->flags & TFS_SUBTRACT_LOG_Q) ? a->log_ec_s : nullptr;
   const int64_t nconv = p.bin ? 0 : (B + S) * d / 4;
-  ::tfs::launch(prep_kernel, grid1d((nconv + p.w.Spad) / 4), 256, 0, st, 
+  ::tfs::launch(prep_kernel, grid1d(nconv / 4 + p.w.Spad), 256, 0, st, 
       a->h, p.bin ? 0 : B * d / 4, a->w_s, p.bin ? 0 : S * d / 4, p.w.hb, p.w.wsb, a->b_s, le_s,
       a->sampled, S, p.w.Spad, const_cast<int2*>(p.ep.cmap), p.ep.vocab, p.w.cb, p.w.sid);
   launched();
@@ -1152,7 +1155,7 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
         ep.vocab, a->loss, B, a->grad_scale, a->loss_sum);
   } else {
     const int64_t ncb = cdiv(S, kColsumChunks * 8);
-    const bool narrow = ncb < num_sms();
+    const bool narrow = TFS_COLSUM_G256 || ncb < num_sms();  // 256 row groups per column block
     auto colsum = narrow ? g_colsum_kernel<256> : g_colsum_kernel<64>;
     ::tfs::launch(colsum, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kColsumChunks * (narrow ? 256 : 64), 0, st, w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
                    a->loss, a->grad_scale, a->loss_sum);
