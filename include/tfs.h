@@ -231,6 +231,10 @@ typedef struct {
   /* SMs the persistent tensor-core GEMMs of the call leave free (0: use every SM), so work on
    * other streams (e.g. the training step's side streams) progresses while they run. */
   int32_t sm_reserve;
+  /* Optional cudaEvent_t (NULL: none), recorded on the stream as soon as dw_true, db_true,
+   * dw_s and db_s are final -- before the call's last pass (the dh split-K reduction) -- so a
+   * caller can start the softmax-row update on another stream while dh is finished. */
+  void* rows_ready_event;
 } tfs_ssm_args;
 size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype,
                                int64_t vocab);

@@ -76,6 +76,7 @@ class SsmArgs(ctypes.Structure):
         ("sampled", P), ("w_s", P), ("b_s", P), ("log_ec_s", P),
         ("loss", P), ("lse", P), ("loss_sum", P), ("dh", P), ("dw_true", P), ("db_true", P),
         ("dw_s", P), ("db_s", P), ("vocab", I64), ("timing_events", P), ("sm_reserve", I32),
+        ("rows_ready_event", P),
     ]
 
 

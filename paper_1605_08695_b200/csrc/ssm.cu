@@ -1094,14 +1094,17 @@ static int32_t bf16_store(const tfs_ssm_args* a, const Bf16Plan& p, const float*
   rc = umma::launch_store(g, 2, p.groups, st);
   if (rc != TFS_OK) return rc;
   mark(a, 6, st);
+  if (dws_split) {  // dW_s first: the softmax-row gradients are then final (rows_ready_event)
+    ::tfs::launch(split_finalize_kernel<false>, grid1d(S * d / 4), 256, 0, st,
+                  w.part_dws, w.ks_dws, S, d, nullptr, nullptr, a->dw_s);
+    launched();
+  }
+  if (a->rows_ready_event != nullptr &&
+      cudaEventRecord(static_cast<cudaEvent_t>(a->rows_ready_event), st) != cudaSuccess)
+    return TFS_ERR_CUDA;
   if (dh_split) {
     auto fin = p.bin ? split_finalize_kernel<true> : split_finalize_kernel<false>;
     ::tfs::launch(fin, grid1d(B * d / 4), 256, 0, st, w.part_dh, w.ks_dh, B, d, g_true, w_true, a->dh);
-    launched();
-  }
-  if (dws_split) {
-    ::tfs::launch(split_finalize_kernel<false>, grid1d(S * d / 4), 256, 0, st, 
-        w.part_dws, w.ks_dws, S, d, nullptr, nullptr, a->dw_s);
     launched();
   }
   TFS_LAUNCH_CHECK();
@@ -1244,6 +1247,8 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
       TFS_CUDA_TRY(cudaMemsetAsync(a->db_s, 0, sizeof(float) * a->S, st));
     }
     if (a->loss_sum) TFS_CUDA_TRY(cudaMemsetAsync(a->loss_sum, 0, sizeof(float), st));
+    if (a->rows_ready_event != nullptr)
+      TFS_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(a->rows_ready_event), st));
     return TFS_OK;
   }
   TFS_REQUIRE(a->h && a->labels && a->w_true && a->b_true && a->dh && a->dw_true && a->db_true);
@@ -1270,6 +1275,9 @@ extern "C" int32_t tfs_sampled_softmax_fwd_bwd(const tfs_ssm_args* a, void* ws, 
     ::tfs::launch(loss_sum_kernel, 1, 256, 0, st, a->loss, a->B, a->grad_scale, a->loss_sum); ::tfs::launched();
     TFS_LAUNCH_CHECK();
   }
+  // (the bf16 path with candidates records rows_ready_event itself, before the dh reduction)
+  if (a->rows_ready_event != nullptr && !fused_sum)
+    TFS_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(a->rows_ready_event), st));
   return TFS_OK;
 }
 

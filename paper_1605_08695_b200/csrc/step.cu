@@ -338,7 +338,7 @@ struct BufInfo {
 };
 
 enum Ev { kFork, kH, kQ, kPlanW, kOwn, kSsm, kRedE, kB2, kSideDone, kMainDone, kBar, kCommit,
-          kSmp, kNumEv };
+          kSmp, kRows, kNumEv };
 
 struct Rank {
   int r = 0;           // global rank
@@ -600,12 +600,15 @@ void local_step(tfs_stepper* st, Rank& k, cudaStream_t mn) {
                             k.err, mn));
   STEP_CALL(st, waitev(mn, k.ev[kH]));
   tfs_ssm_args a = ssm_args(st, k, nullptr);
+  // the softmax-row gradients are final before the call's last pass (the dh split-K
+  // reduction): the W / b update starts then, on the side stream (after its plan), while the
+  // main stream finishes dh and updates E (its plan was built on the side stream before W's)
+  a.rows_ready_event = k.ev[kRows];
   STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
-  STEP_CALL(st, rec(k.ev[kSsm], mn));
-  STEP_CALL(st, waitev(sd, k.ev[kSsm]));
-  STEP_CALL(st, apply_local(st, k, true, sd));
+  STEP_CALL(st, waitev(sd, k.ev[kRows]));
+  STEP_CALL(st, apply_local(st, k, false, sd));
   STEP_CALL(st, waitev(mn, k.ev[kPlanW]));
-  STEP_CALL(st, apply_local(st, k, false, mn));
+  STEP_CALL(st, apply_local(st, k, true, mn));
   STEP_CALL(st, join(mn, sd, k.ev[kSideDone]));
   sample_join(st, k, mn);
 }
