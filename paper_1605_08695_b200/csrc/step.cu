@@ -338,7 +338,7 @@ struct BufInfo {
 };
 
 enum Ev { kFork, kH, kQ, kPlanW, kOwn, kSsm, kRedE, kB2, kSideDone, kMainDone, kBar, kCommit,
-          kSmp, kRows, kNumEv };
+          kSmp, kRows, kPushW, kNumEv };
 
 struct Rank {
   int r = 0;           // global rank
@@ -710,19 +710,30 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       mark(st, 3, mn);  // W rows pulled
       STEP_CALL(st, waitev(mn, k.ev[kH]));
       tfs_ssm_args a = ssm_args(st, k, st->timing ? st->timing + 9 : nullptr);
+      // The W / b gradients are final before the softmax call's last pass (the dh split-K
+      // reduction): outside instrumented steps their push runs on the sampler stream (idle by
+      // then) from that point, overlapping dh's reduction and the E push on the main stream.
+      // Both pushes stay off the side stream: B2 then does not wait for the side stream's owner
+      // plans (which the persistent softmax GEMMs delay: they hold every SM).
+      const bool split_push = st->timing == nullptr;
+      if (split_push) a.rows_ready_event = k.ev[kRows];
       STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
-      // Both gradient pushes on the main stream, right after the softmax: B2 then does not wait
-      // for the side stream's owner plans (which the persistent softmax GEMMs delay: they hold
-      // every SM), only the applies in phase 3 do.
       STEP_CALL(st, waitev(mn, k.ev[kPlanW]));  // the E and W route plans (side, phase 1)
+      cudaStream_t ws = split_push ? k.smp : mn;
+      if (split_push) {
+        STEP_CALL(st, waitev(ws, k.ev[kRows]));
+        STEP_CALL(st, waitev(ws, k.ev[kPlanW]));
+      }
       STEP_CALL(st, tfs_route_reduce_push(k.rplan_w, k.rplan_w_b, m.B + m.S, m.V, R, m.cap_w,
                                           k.dw, m.d, k.db, (float* const*)k.tab_grads,
                                           ro + m.off_w, (float* const*)k.tab_grads, ro + m.off_b,
-                                          k.rws_w, k.rws_w_b, mn));
+                                          k.rws_w, k.rws_w_b, ws));
+      if (split_push) STEP_CALL(st, rec(k.ev[kPushW], ws));
       mark(st, 4, mn);  // W gradients pushed
       STEP_CALL(st, tfs_route_reduce_push(k.rplan_e, k.rplan_e_b, m.B, m.V, R, m.cap_e, k.dh, m.d,
                                           nullptr, (float* const*)k.tab_grads, ro, nullptr, 0,
                                           k.rws_e, k.rws_e_b, mn));
+      if (split_push) STEP_CALL(st, waitev(mn, k.ev[kPushW]));  // B2 orders both pushes
       mark(st, 20, mn);  // E gradients pushed
       break;
     }
