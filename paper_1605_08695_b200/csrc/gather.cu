@@ -547,6 +547,84 @@ __global__ void __launch_bounds__(256) gather_peers_kernel(const float* const* _
   }
 }
 
+// The same, one warp per row (16-byte vector rows): the id, its owner and local row are read
+// and divided once per row (the element-wise kernel above repeats two 64-bit divisions for
+// every 16 bytes), and each lane keeps 2 rows x 4 float4 of peer loads in flight.
+template <bool BF16OUT>
+__global__ void __launch_bounds__(256) gather_peers_rows_kernel(
+    const float* const* __restrict__ shards, int64_t shard_rows, int32_t dim,
+    const int64_t* __restrict__ ids, int64_t n, int64_t vocab, int32_t R, void* __restrict__ out,
+    const float* const* __restrict__ shards2, float* __restrict__ out2, tfs_device_error* err) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int n4 = dim >> 2;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t j0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 2; j0 < n; j0 += nwarps * 2) {
+    const float4* src[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u;
+      const int64_t id = j < n ? __ldg(ids + j) : -1;
+      ok[u] = id >= 0 && id < vocab;
+      if (j < n && !ok[u] && id != -1 && lane == 0) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
+      const int64_t o = ok[u] ? id % R : 0, local = ok[u] ? id / R : 0;
+      ok[u] = ok[u] && local < shard_rows;
+      src[u] = ok[u] ? reinterpret_cast<const float4*>(shards[o] + local * dim) : nullptr;
+      if (ok[u] && shards2 != nullptr && lane == 0) out2[j] = shards2[o][local];
+    }
+    for (int c0 = 0; c0 < n4; c0 += 128) {
+      float4 v[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q * 32 + lane;
+          v[u][q] = (ok[u] && c < n4) ? src[u][c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+        const int64_t j = j0 + u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q * 32 + lane;
+          if (c >= n4) continue;
+          if (BF16OUT)
+            reinterpret_cast<uint2*>(out)[j * n4 + c] =
+                make_uint2(pack_bf16x2(v[u][q].x, v[u][q].y), pack_bf16x2(v[u][q].z, v[u][q].w));
+          else
+            reinterpret_cast<float4*>(out)[j * n4 + c] = v[u][q];
+        }
+      }
+    }
+  }
+}
+
+// Launch the peer Gather: warp-per-row kernel for 16-byte vector rows, else element-wise.
+static int32_t launch_gather_peers(const float* const* shards, int64_t shard_rows, int32_t dim,
+                                   const int64_t* ids, int64_t n, int64_t vocab, int32_t R,
+                                   void* out, bool bf, const float* const* shards2, float* out2,
+                                   tfs_device_error* err, cudaStream_t st) {
+  const bool vec = dim % 4 == 0 && ((uintptr_t)out % (bf ? 8 : 16) == 0);
+  if (vec) {
+    const int grid = grid_for_rows(n, 2);
+    auto k = bf ? gather_peers_rows_kernel<true> : gather_peers_rows_kernel<false>;
+    ::tfs::launch(k, grid, 256, 0, st, shards, shard_rows, dim, ids, n, vocab, R, out, shards2,
+                  out2, err);
+  } else {
+    const int64_t total = n * dim;
+    const int grid =
+        (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
+    auto k = bf ? gather_peers_kernel<false, true> : gather_peers_kernel<false, false>;
+    ::tfs::launch(k, grid, 256, 0, st, shards, shard_rows, dim, ids, n, vocab, R, out, shards2,
+                  out2, err);
+  }
+  ::tfs::launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
 extern "C" int32_t tfs_gather_peers(const float* const* shards, int64_t shard_rows, int32_t dim,
                                     const int64_t* ids, int64_t n, int64_t vocab,
                                     int32_t num_shards, void* out, int32_t out_dtype,
@@ -556,18 +634,8 @@ extern "C" int32_t tfs_gather_peers(const float* const* shards, int64_t shard_ro
   if (n == 0) return TFS_OK;
   TFS_REQUIRE(shards && ids && out);
   TFS_SUPPORTED();
-  cudaStream_t st = as_stream(stream);
-  const bool bf = out_dtype == TFS_BF16;
-  const bool vec = dim % 4 == 0 && ((uintptr_t)out % (bf ? 8 : 16) == 0);
-  const int64_t total = n * (vec ? dim / 4 : dim);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
-  auto k = vec ? (bf ? gather_peers_kernel<true, true> : gather_peers_kernel<true, false>)
-               : (bf ? gather_peers_kernel<false, true> : gather_peers_kernel<false, false>);
-  ::tfs::launch(k, grid, 256, 0, st, shards, shard_rows, dim, ids, n, vocab, num_shards, out, nullptr,
-                          nullptr, err);
-  ::tfs::launched();
-  TFS_LAUNCH_CHECK();
-  return TFS_OK;
+  return launch_gather_peers(shards, shard_rows, dim, ids, n, vocab, num_shards, out,
+                             out_dtype == TFS_BF16, nullptr, nullptr, err, as_stream(stream));
 }
 
 extern "C" int32_t tfs_gather_peers2(const float* const* shards, int64_t shard_rows, int32_t dim,
@@ -580,18 +648,8 @@ extern "C" int32_t tfs_gather_peers2(const float* const* shards, int64_t shard_r
   if (n == 0) return TFS_OK;
   TFS_REQUIRE(shards && shards2 && ids && out && out2);
   TFS_SUPPORTED();
-  cudaStream_t st = as_stream(stream);
-  const bool bf = out_dtype == TFS_BF16;
-  const bool vec = dim % 4 == 0 && ((uintptr_t)out % (bf ? 8 : 16) == 0);
-  const int64_t total = n * (vec ? dim / 4 : dim);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 16ll * num_sms()));
-  auto k = vec ? (bf ? gather_peers_kernel<true, true> : gather_peers_kernel<true, false>)
-               : (bf ? gather_peers_kernel<false, true> : gather_peers_kernel<false, false>);
-  ::tfs::launch(k, grid, 256, 0, st, shards, shard_rows, dim, ids, n, vocab, num_shards, out, shards2, out2,
-                          err);
-  ::tfs::launched();
-  TFS_LAUNCH_CHECK();
-  return TFS_OK;
+  return launch_gather_peers(shards, shard_rows, dim, ids, n, vocab, num_shards, out,
+                             out_dtype == TFS_BF16, shards2, out2, err, as_stream(stream));
 }
 
 extern "C" int32_t tfs_gather2(const float* table, int64_t rows, int32_t dim, const float* table2,
