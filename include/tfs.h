@@ -359,6 +359,9 @@ typedef struct {
   float mu;
   float* slot;
   float* slot2;
+  /* Optional bf16 mirror of the table (same shape, NULL: none): every updated row is also
+   * written there, rounded to nearest even -- the copy peers read (tfs_gather_peers2_bf16). */
+  uint16_t* mirror;
 } tfs_sparse_opt;
 int32_t tfs_scatter_opt_planned(float* table, int64_t rows, int32_t dim, const void* plan,
                                 size_t plan_bytes, int64_t n, const float* grad_rows,
@@ -425,6 +428,14 @@ int32_t tfs_gather_peers2(const float* const* shards, int64_t shard_rows, int32_
                           const float* const* shards2, const int64_t* ids, int64_t n,
                           int64_t vocab, int32_t num_shards, void* out, int32_t out_dtype,
                           float* out2, tfs_device_error* err, void* stream);
+/* tfs_gather_peers2_bf16: the same with the rows read from the owners' bf16 MIRRORS of the
+ * table (bf16 [shard_rows x dim] each, kept equal to bf16-RNE(table) by the owners' updates:
+ * tfs_sparse_opt.mirror) and written as bf16 -- identical output to tfs_gather_peers2 with
+ * out_dtype = TFS_BF16, at half the bytes over NVLink.  dim % 8 == 0, out 16-byte aligned. */
+int32_t tfs_gather_peers2_bf16(const uint16_t* const* shards, int64_t shard_rows, int32_t dim,
+                               const float* const* shards2, const int64_t* ids, int64_t n,
+                               int64_t vocab, int32_t num_shards, uint16_t* out, float* out2,
+                               tfs_device_error* err, void* stream);
 /* Owner side.  tfs_gather_slots: for each slot (o, s) of num_slots regions x cap, the row of id
  * ids[o * ids_stride + s] of the local shard to out + o * out_stride + s * dim (fp32; -1 ids
  * are padding, rows left unwritten).  tfs_scatter_plan_slots / tfs_scatter_add_sgd_planned_slots:

@@ -54,7 +54,8 @@ class TfsError(RuntimeError):
 
 
 class SparseOpt(ctypes.Structure):
-    _fields_ = [("kind", I32), ("lr", F32), ("mu", F32), ("slot", P), ("slot2", P)]
+    _fields_ = [("kind", I32), ("lr", F32), ("mu", F32), ("slot", P), ("slot2", P),
+                ("mirror", P)]
 
 
 class StepConfigC(ctypes.Structure):
@@ -83,6 +84,7 @@ class SsmArgs(ctypes.Structure):
 _SIGNATURES = {
     "tfs_version": ([], I32),
     "tfs_ssm_grad_from_logits": ([], I32),
+    "tfs_gather_peers2_bf16": ([P, I64, I32, P, P, I64, I64, I32, P, P, P, P], I32),
     "tfs_status_string": ([I32], ctypes.c_char_p),
     "tfs_last_error_detail": ([ctypes.c_char_p, SZ], I32),
     "tfs_device_check": ([I32], I32),

@@ -652,6 +652,70 @@ extern "C" int32_t tfs_gather_peers2(const float* const* shards, int64_t shard_r
                              out_dtype == TFS_BF16, shards2, out2, err, as_stream(stream));
 }
 
+// Peer Gather from the owners' bf16 mirrors: one warp per row, 16-byte copies (8 bf16), two
+// rows x 4 vectors of peer loads in flight per lane.
+__global__ void __launch_bounds__(256) gather_peers_bf16_kernel(
+    const uint16_t* const* __restrict__ shards, int64_t shard_rows, int32_t dim,
+    const int64_t* __restrict__ ids, int64_t n, int64_t vocab, int32_t R,
+    uint16_t* __restrict__ out, const float* const* __restrict__ shards2,
+    float* __restrict__ out2, tfs_device_error* err) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int n8 = dim >> 3;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t j0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 2; j0 < n; j0 += nwarps * 2) {
+    const uint4* src[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u;
+      const int64_t id = j < n ? __ldg(ids + j) : -1;
+      ok[u] = id >= 0 && id < vocab;
+      if (j < n && !ok[u] && id != -1 && lane == 0) report_error(err, TFS_ERR_OUT_OF_RANGE, j);
+      const int64_t o = ok[u] ? id % R : 0, local = ok[u] ? id / R : 0;
+      ok[u] = ok[u] && local < shard_rows;
+      src[u] = ok[u] ? reinterpret_cast<const uint4*>(shards[o] + local * dim) : nullptr;
+      if (ok[u] && shards2 != nullptr && lane == 0) out2[j] = shards2[o][local];
+    }
+    for (int c0 = 0; c0 < n8; c0 += 128) {
+      uint4 v[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q * 32 + lane;
+          v[u][q] = (ok[u] && c < n8) ? src[u][c] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q * 32 + lane;
+          if (c < n8) reinterpret_cast<uint4*>(out)[(j0 + u) * n8 + c] = v[u][q];
+        }
+      }
+    }
+  }
+}
+
+extern "C" int32_t tfs_gather_peers2_bf16(const uint16_t* const* shards, int64_t shard_rows,
+                                          int32_t dim, const float* const* shards2,
+                                          const int64_t* ids, int64_t n, int64_t vocab,
+                                          int32_t num_shards, uint16_t* out, float* out2,
+                                          tfs_device_error* err, void* stream) {
+  TFS_REQUIRE(n >= 0 && dim >= 1 && shard_rows >= 0 && vocab >= 1 && num_shards >= 1);
+  if (n == 0) return TFS_OK;
+  TFS_REQUIRE(shards && shards2 && ids && out && out2);
+  TFS_REQUIRE(dim % 8 == 0 && ((uintptr_t)out & 15) == 0);
+  TFS_SUPPORTED();
+  ::tfs::launch(gather_peers_bf16_kernel, grid_for_rows(n, 2), 256, 0, as_stream(stream),
+                shards, shard_rows, dim, ids, n, vocab, num_shards, out, shards2, out2, err);
+  ::tfs::launched();
+  TFS_LAUNCH_CHECK();
+  return TFS_OK;
+}
+
 extern "C" int32_t tfs_gather2(const float* table, int64_t rows, int32_t dim, const float* table2,
                                const int64_t* ids, int64_t n, void* out, int32_t out_dtype,
                                float* out2, tfs_device_error* err, void* stream) {

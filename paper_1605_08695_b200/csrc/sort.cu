@@ -464,6 +464,7 @@ struct SegJob {
   double mu;
   float* slot;
   float* slot2;
+  uint16_t* mirror;  // optional bf16 copy of the table, kept in step (tfs_sparse_opt.mirror)
   // write mode (sort_reduce): out_local[u], out_rows[u]; with slot_base (route_reduce) the row
   // of segment u (owner o = key / nloc) goes to slot o * cap + (u - slot_base[o]) instead
   int64_t* out_local;
@@ -840,8 +841,11 @@ __global__ void __launch_bounds__(128, TFS_WIN_MINB) seg_window_vec4_kernel(SegJ
               }
             }
           } else {
-            *(reinterpret_cast<float4*>(j.table + s_toff[r]) + c4) =
-                opt_step4<OPT>(j, t[buf][q], acc, kr, c4);
+            const float4 nv = opt_step4<OPT>(j, t[buf][q], acc, kr, c4);
+            *(reinterpret_cast<float4*>(j.table + s_toff[r]) + c4) = nv;
+            if (j.mirror)
+              reinterpret_cast<uint2*>(j.mirror + s_toff[r])[c4] =
+                  make_uint2(pack_bf16x2(nv.x, nv.y), pack_bf16x2(nv.z, nv.w));
             if (j.table2 && col0) opt_step2<OPT>(j, kr, acc2);
           }
         } else {
@@ -884,7 +888,11 @@ __device__ __forceinline__ void seg_finish_vec4(const SegJob& j, uint32_t s, int
     }
   } else {
     float4* tp = reinterpret_cast<float4*>(j.table + (int64_t)key * j.dim) + c4;
-    *tp = opt_step4<OPT>(j, *tp, acc, key, c4);
+    const float4 nv = opt_step4<OPT>(j, *tp, acc, key, c4);
+    *tp = nv;
+    if (j.mirror)
+      reinterpret_cast<uint2*>(j.mirror + (int64_t)key * j.dim)[c4] =
+          make_uint2(pack_bf16x2(nv.x, nv.y), pack_bf16x2(nv.z, nv.w));
     if (col0 && j.table2) opt_step2<OPT>(j, key, acc2);
   }
 }
@@ -1339,6 +1347,7 @@ static int32_t run_segments(SegJob& j, int64_t n, cudaStream_t st) {
                    (j.row_cap == 0 || j.row_stride % 4 == 0) &&
                    (j.table ? ((uintptr_t)j.table & 15) == 0
                             : (j.out_tab != nullptr || ((uintptr_t)j.out_rows & 15) == 0));
+  if (!vec && j.mirror != nullptr) return TFS_ERR_INVALID_ARGUMENT;  // mirrors: vector path
   if (vec) {  // one launch: windows + the fused crossing reduction (cross_arrive)
     const int64_t n4 = j.dim >> 2;
     const int wthreads = (int)std::min<int64_t>(128, cdiv(n4, 32) * 32);
@@ -1876,6 +1885,8 @@ static int32_t planned_slots_impl(float* table, int64_t rows, int32_t dim, const
   TFS_REQUIRE(opt != nullptr && opt->kind >= 0 && opt->kind <= 2);
   TFS_REQUIRE(opt->kind == 0 || opt->slot != nullptr);
   TFS_REQUIRE(opt->kind == 0 || table2 == nullptr || opt->slot2 != nullptr);
+  TFS_REQUIRE(opt->mirror == nullptr ||
+              (dim % 8 == 0 && ((uintptr_t)opt->mirror & 15) == 0 && ((uintptr_t)table & 15) == 0));
   const int64_t n = (int64_t)R * cap;
   TFS_REQUIRE(table && plan && grad && n < (1ll << 31));
   TFS_REQUIRE(dim % 4 != 0 || (((uintptr_t)table & 15) == 0 && grad_stride % 4 == 0 &&
@@ -1898,6 +1909,7 @@ static int32_t planned_slots_impl(float* table, int64_t rows, int32_t dim, const
   j.mu = (double)opt->mu;
   j.slot = opt->slot;
   j.slot2 = opt->slot2;
+  j.mirror = opt->mirror;
   j.nloc = rows + 1;
   j.row_cap = cap;
   j.row_stride = grad_stride;
@@ -1932,6 +1944,8 @@ extern "C" int32_t tfs_scatter_opt_planned(float* table, int64_t rows, int32_t d
   TFS_REQUIRE((table2 == nullptr) == (grad2 == nullptr));
   TFS_REQUIRE(opt->kind == 0 || opt->slot != nullptr);
   TFS_REQUIRE(opt->kind == 0 || table2 == nullptr || opt->slot2 != nullptr);
+  TFS_REQUIRE(opt->mirror == nullptr ||
+              (dim % 8 == 0 && ((uintptr_t)opt->mirror & 15) == 0 && ((uintptr_t)table & 15) == 0));
   if (n == 0) return TFS_OK;
   TFS_REQUIRE(table && plan && grad_rows);
   TFS_REQUIRE(dim % 4 != 0 || (((uintptr_t)table & 15) == 0 &&
@@ -1954,6 +1968,7 @@ extern "C" int32_t tfs_scatter_opt_planned(float* table, int64_t rows, int32_t d
   j.mu = (double)opt->mu;
   j.slot = opt->slot;
   j.slot2 = opt->slot2;
+  j.mirror = opt->mirror;
   j.nloc = rows + 1;
   return run_segments(j, n, as_stream(stream));
 }

@@ -303,7 +303,7 @@ Dims dims_of(const tfs_step_config* c) {
 
 // Symmetric heap layout (identical on every rank: it depends on the config only).
 struct HeapLayout {
-  size_t E, W, b, ids, grads, hsym, ysym, rowstats, dh_part, loss_part, total;
+  size_t E, W, b, ids, grads, Wm, hsym, ysym, rowstats, dh_part, loss_part, total;
 };
 HeapLayout heap_layout(const Dims& m) {
   Carver c(nullptr, 0);
@@ -320,6 +320,10 @@ HeapLayout heap_layout(const Dims& m) {
   L.b = off(sizeof(float) * m.shard_rows);
   L.ids = off(sizeof(int64_t) * m.R * std::max<int64_t>(m.istride, 1));
   L.grads = off(sizeof(float) * m.R * std::max<int64_t>(m.rstride, 4));
+  // sampled softmax over R > 1 shards, bf16 operands: the bf16 mirror of W the requesters pull
+  // (half the NVLink bytes of pulling fp32 rows; every owner update rewrites its rows)
+  if (m.R > 1 && !m.sharded_full && m.bf16 && m.d % 8 == 0)
+    L.Wm = off(sizeof(uint16_t) * m.shard_rows * m.d);
   if (m.sharded_full) {
     L.hsym = off(2 * m.B * m.d);
     L.ysym = off(sizeof(int64_t) * m.B);
@@ -372,6 +376,8 @@ struct Rank {
   // R > 1
   int64_t* recv_ids = nullptr;
   float* recv_grads = nullptr;
+  uint16_t* Wm = nullptr;      // bf16 mirror of this shard's W (heap; R > 1 sampled path)
+  int64_t* tab_Wm = nullptr;   // the owners' mirrors
   int64_t *tab_E = nullptr, *tab_W = nullptr, *tab_b = nullptr, *tab_ids = nullptr,
           *tab_grads = nullptr;
   void *rplan_e = nullptr, *rplan_w = nullptr, *rws_e = nullptr, *rws_w = nullptr;
@@ -556,7 +562,7 @@ int32_t apply_owner(tfs_stepper* st, Rank& k, bool e_table, cudaStream_t s) {
   const Dims& m = st->m;
   const tfs_step_config& c = st->cfg;
   const tfs_sparse_opt o{c.optimizer, c.lr, c.momentum, e_table ? k.sE : k.sW,
-                         e_table ? nullptr : k.sb};
+                         e_table ? nullptr : k.sb, e_table ? nullptr : k.Wm};
   if (e_table)
     return tfs_scatter_opt_planned_slots(k.E, k.nloc, m.d, k.oplan_e, k.oplan_e_b, m.R, m.cap_e,
                                          k.recv_grads, m.rstride, nullptr, nullptr, 0, &o,
@@ -704,9 +710,14 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
                                            1, k.oplan_w, k.oplan_w_b, k.err, sd));
       STEP_CALL(st, rec(k.ev[kOwn], sd));
       mark(st, 19, sd);  // side: owner plans built
-      STEP_CALL(st, tfs_gather_peers2((const float* const*)k.tab_W, m.shard_rows, m.d,
-                                      (const float* const*)k.tab_b, k.qw, m.B + m.S, m.V, R,
-                                      k.w_rows, rdt, k.b_rows, k.err, mn));
+      if (k.tab_Wm)  // bf16 rows straight from the owners' mirrors
+        STEP_CALL(st, tfs_gather_peers2_bf16((const uint16_t* const*)k.tab_Wm, m.shard_rows,
+                                             m.d, (const float* const*)k.tab_b, k.qw, m.B + m.S,
+                                             m.V, R, (uint16_t*)k.w_rows, k.b_rows, k.err, mn));
+      else
+        STEP_CALL(st, tfs_gather_peers2((const float* const*)k.tab_W, m.shard_rows, m.d,
+                                        (const float* const*)k.tab_b, k.qw, m.B + m.S, m.V, R,
+                                        k.w_rows, rdt, k.b_rows, k.err, mn));
       mark(st, 3, mn);  // W rows pulled
       STEP_CALL(st, waitev(mn, k.ev[kH]));
       tfs_ssm_args a = ssm_args(st, k, st->timing ? st->timing + 9 : nullptr);
@@ -1133,6 +1144,10 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
       };
       k.tab_E = table(HL.E);
       k.tab_W = table(HL.W);
+      if (HL.Wm) {
+        k.Wm = reinterpret_cast<uint16_t*>(heap + HL.Wm);
+        k.tab_Wm = table(HL.Wm);
+      }
       k.tab_b = table(HL.b);
       k.tab_ids = table(HL.ids);
       k.tab_grads = table(HL.grads);
@@ -1247,6 +1262,10 @@ extern "C" int32_t tfs_step_sync(tfs_stepper* st) {
   for (auto& k : st->ranks) {
     if (k.W_bf) {
       ::tfs::launch(f32_to_bf16_kernel, grid1d(k.nloc * st->m.d), 256, 0, 0, k.W, k.nloc * st->m.d, k.W_bf);
+      launched();
+    }
+    if (k.Wm) {
+      ::tfs::launch(f32_to_bf16_kernel, grid1d(k.nloc * st->m.d), 256, 0, 0, k.W, k.nloc * st->m.d, k.Wm);
       launched();
     }
     TFS_CUDA_TRY(cudaMemcpy(k.err, &none, sizeof(none), cudaMemcpyHostToDevice));

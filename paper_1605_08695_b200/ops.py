@@ -411,6 +411,17 @@ def gather_peers2(shard_tab, shard_tab2, shard_rows: int, dim: int, ids, vocab: 
     return out, out2
 
 
+def gather_peers2_bf16(mirror_tab, shard_tab2, shard_rows: int, dim: int, ids, vocab: int,
+                       R: int, out, out2, err: ErrorSlot = None):
+    """tfs_gather_peers2 from the owners' bf16 mirrors (bf16 rows out)."""
+    assert out.dtype == torch.bfloat16
+    check(_lib.lib().tfs_gather_peers2_bf16(_p(mirror_tab), int(shard_rows), int(dim),
+                                            _p(shard_tab2), _p(ids), ids.numel(), int(vocab),
+                                            int(R), _p(out), _p(out2), _err(err), _stream()),
+          "tfs_gather_peers2_bf16")
+    return out, out2
+
+
 def gather_slots(table, ids, ids_stride: int, num_slots: int, cap: int, out, out_stride: int,
                  err: ErrorSlot = None):
     """Owner side: rows of the received slot ids (-1 = padding) into slot layout."""

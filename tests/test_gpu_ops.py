@@ -155,6 +155,37 @@ def test_gather_peers2_simulated_shards(R, bf16):
     assert np.array_equal(out2.cpu().numpy(), b[ids])
 
 
+@pytest.mark.parametrize("R", [2, 3])
+def test_gather_peers2_bf16_mirrors(R):
+    """The pull from the owners' bf16 mirrors (bf16 RNE of the fp32 shards) == the pull of the
+    fp32 shards rounded to bf16 == the oracle's bf16 Gather of the logical table, bit-exact."""
+    rng = np.random.default_rng(10 + R)
+    V, d = 3001, 64
+    W = rng.standard_normal((V, d)).astype(np.float32)
+    b = rng.standard_normal(V).astype(np.float32)
+    rows = -(-V // R)
+    sh = [torch.zeros((rows, d), device=DEV) for _ in range(R)]
+    sb = [torch.zeros(rows, device=DEV) for _ in range(R)]
+    for r in range(R):
+        n_r = W[r::R].shape[0]
+        sh[r][:n_r] = T(W[r::R])
+        sb[r][:n_r] = T(b[r::R])
+    mir = [t.to(torch.bfloat16) for t in sh]  # torch's RNE conversion: the mirrors' contents
+    mtab = torch.tensor([t.data_ptr() for t in mir], dtype=torch.int64, device=DEV)
+    tab2 = torch.tensor([t.data_ptr() for t in sb], dtype=torch.int64, device=DEV)
+    ids = workloads.zipf_ids(rng, V, 1.0, 2000)
+    ids[7] = -1
+    out = torch.full((ids.size, d), 3.0, dtype=torch.bfloat16, device=DEV)
+    out2 = torch.full((ids.size,), 5.0, device=DEV)
+    ops.gather_peers2_bf16(mtab, tab2, rows, d, T(ids), V, R, out, out2)
+    keep = ids != -1
+    ref = oracle.gather(W, ids[keep], bf16=True)
+    got = out.cpu().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got[keep], ref)
+    assert np.array_equal(out2.cpu().numpy()[keep], b[ids[keep]])
+    assert float(out[7, 0].float()) == 3.0 and float(out2[7]) == 5.0
+
+
 def test_gather_out_of_range():
     err = ops.ErrorSlot(DEV)
     table = T(np.zeros((10, 8), np.float32))
