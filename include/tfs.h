@@ -158,7 +158,9 @@ int32_t tfs_sample_commit(int64_t vocab, int32_t num_sampled, int32_t unique,
                           const int64_t* num_tries, const int64_t* labels, int64_t n_labels,
                           int64_t* out_sampled, float* out_log_ec_sampled,
                           float* out_log_ec_labels, int64_t* out_num_tries,
-                          tfs_device_error* err, void* stream);
+                          int64_t* out_labels, tfs_device_error* err, void* stream);
+/* (out_labels: optional copy of labels[0, n_labels) -- the step builds its softmax-row lookup
+ * ids y || s in one buffer with out_labels + n_labels == out_sampled.) */
 
 /* ==== Sampled softmax forward + backward (DESIGN §3 O9-O11) ==========
  * "performs a sparse multiplication based on the true class for an example and a set of

@@ -98,7 +98,7 @@ _SIGNATURES = {
     "tfs_sampler_workspace_bytes": ([I64], SZ),
     "tfs_log_uniform_sample": ([P, I64, I32, I32, I64, U64, U64, P, U32, P, I64, P, P, P, P, P,
                                 SZ, P, P], I32),
-    "tfs_sample_commit": ([I64, I32, I32, P, P, P, P, I64, P, P, P, P, P, P], I32),
+    "tfs_sample_commit": ([I64, I32, I32, P, P, P, P, I64, P, P, P, P, P, P, P], I32),
     "tfs_ssm_workspace_bytes": ([I64, I64, I32, I32, I64], SZ),
     "tfs_sampled_softmax_fwd_bwd": ([ctypes.POINTER(SsmArgs), P, SZ, P], I32),
     "tfs_ssm_partial_stats": ([ctypes.POINTER(SsmArgs), P, P, SZ, P], I32),

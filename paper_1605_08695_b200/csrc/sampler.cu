@@ -236,7 +236,7 @@ __global__ void sample_commit_kernel(int64_t V, double log_v1, int unique, int32
                                      const int64_t* s_in, const float* les_in,
                                      const int64_t* T_in, const int64_t* labels, int64_t n_labels,
                                      int64_t* s_out, float* les_out, float* ley_out,
-                                     int64_t* T_out, tfs_device_error* err) {
+                                     int64_t* T_out, int64_t* labels_out, tfs_device_error* err) {
   pdl_enter();
   const int64_t T = unique ? *T_in : (int64_t)S;
   const int64_t total = (int64_t)S + n_labels;
@@ -249,6 +249,7 @@ __global__ void sample_commit_kernel(int64_t V, double log_v1, int unique, int32
     } else {
       const int64_t t = e - S;
       const int64_t k = labels[t];
+      if (labels_out != nullptr) labels_out[t] = k;
       if (k < 0 || k >= V) {
         report_error(err, TFS_ERR_OUT_OF_RANGE, t);
         ley_out[t] = 0.f;
@@ -384,8 +385,8 @@ extern "C" int32_t tfs_sample_commit(int64_t vocab, int32_t num_sampled, int32_t
                                      const int64_t* num_tries, const int64_t* labels,
                                      int64_t n_labels, int64_t* out_sampled,
                                      float* out_log_ec_sampled, float* out_log_ec_labels,
-                                     int64_t* out_num_tries, tfs_device_error* err,
-                                     void* stream) {
+                                     int64_t* out_num_tries, int64_t* out_labels,
+                                     tfs_device_error* err, void* stream) {
   TFS_REQUIRE(vocab >= 1 && num_sampled >= 0 && n_labels >= 0 && num_tries && out_num_tries);
   TFS_REQUIRE(num_sampled == 0 || (sampled && log_ec_sampled && out_sampled && out_log_ec_sampled));
   TFS_REQUIRE(n_labels == 0 || (labels && out_log_ec_labels));
@@ -395,7 +396,7 @@ extern "C" int32_t tfs_sample_commit(int64_t vocab, int32_t num_sampled, int32_t
   ::tfs::launch(sample_commit_kernel, g, 256, 0, as_stream(stream), 
       vocab, std::log((double)vocab + 1.0), unique, num_sampled, sampled, log_ec_sampled,
       num_tries, labels, n_labels, out_sampled, out_log_ec_sampled, out_log_ec_labels,
-      out_num_tries, err);
+      out_num_tries, out_labels, err);
   ::tfs::launched();
   TFS_LAUNCH_CHECK();
   return TFS_OK;

@@ -522,8 +522,9 @@ int32_t presample(tfs_stepper* st, Rank& k, cudaStream_t s, int64_t add) {
 int32_t commit(tfs_stepper* st, Rank& k, cudaStream_t s) {
   const Dims& m = st->m;
   if (m.full) return TFS_OK;
+  // also writes y into qw[0, B): the lookup ids y || s in one buffer (no separate copy)
   return tfs_sample_commit(m.V, (int32_t)m.S, st->cfg.unique, k.s_next, k.les_next, k.T_next,
-                           k.y, m.B, k.qw + m.B, k.les, k.ley, k.num_tries, k.err, s);
+                           k.y, m.B, k.qw + m.B, k.les, k.ley, k.num_tries, k.qw, k.err, s);
 }
 
 // At the start of a step: commit this step's sample, then fork the next step's draw.
@@ -595,7 +596,8 @@ void local_step(tfs_stepper* st, Rank& k, cudaStream_t mn) {
   STEP_CALL(st, tfs_gather(k.E, m.V, m.d, TFS_F32, k.x, m.B, k.h, rdt, k.err, sd));
   STEP_CALL(st, rec(k.ev[kH], sd));
   STEP_CALL(st, tfs_scatter_plan(k.x, m.B, m.V, k.plan_e, k.plan_e_b, k.err, sd));
-  if (cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) != cudaSuccess)
+  if (m.full &&  // (the sampled path: the commit writes y into qw)
+      cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) != cudaSuccess)
     st->status = st->status ? st->status : TFS_ERR_CUDA;
   sample_phase(st, k, mn);
   STEP_CALL(st, rec(k.ev[kQ], mn));
@@ -627,7 +629,8 @@ void local_step_serial(tfs_stepper* st, Rank& k, cudaStream_t mn, void* const* e
     if (ev && ev[i]) STEP_CALL(st, rec((cudaEvent_t)ev[i], mn));
   };
   mark(0);
-  if (cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) != cudaSuccess)
+  if (m.full &&
+      cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) != cudaSuccess)
     st->status = st->status ? st->status : TFS_ERR_CUDA;
   STEP_CALL(st, commit(st, k, mn));       // this step's sample (drawn ahead) ...
   STEP_CALL(st, presample(st, k, mn, 1)); // ... and the next step's draw, inline here
@@ -689,8 +692,8 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       STEP_CALL(st, rec(k.ev[kH], sd));
       STEP_CALL(st, tfs_route_plan_push(k.x, m.B, m.V, R, m.cap_e, k.rplan_e, k.rplan_e_b,
                                         (int64_t* const*)k.tab_ids, io, k.counts, k.err, sd));
-      if (cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) !=
-          cudaSuccess)
+      if (m.full && cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice,
+                                    mn) != cudaSuccess)
         st->status = st->status ? st->status : TFS_ERR_CUDA;
       sample_phase(st, k, mn);
       mark(st, 2, mn);  // sample committed
