@@ -614,6 +614,10 @@ void local_step(tfs_stepper* st, Rank& k, cudaStream_t mn) {
   a.rows_ready_event = k.ev[kRows];
   STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
   STEP_CALL(st, waitev(sd, k.ev[kRows]));
+  if (st->side_delay_ns) {  // race detector: the side-stream W update starts late too
+    ::tfs::launch(delay_kernel, 1, 1, 0, sd, st->side_delay_ns);
+    launched();
+  }
   STEP_CALL(st, apply_local(st, k, false, sd));
   STEP_CALL(st, waitev(mn, k.ev[kPlanW]));
   STEP_CALL(st, apply_local(st, k, true, mn));
@@ -737,6 +741,10 @@ void p2p_phase(tfs_stepper* st, Rank& k, int phase, cudaStream_t mn) {
       if (split_push) {
         STEP_CALL(st, waitev(ws, k.ev[kRows]));
         STEP_CALL(st, waitev(ws, k.ev[kPlanW]));
+        if (st->side_delay_ns) {  // race detector: the push starts late too
+          ::tfs::launch(delay_kernel, 1, 1, 0, ws, st->side_delay_ns);
+          launched();
+        }
       }
       STEP_CALL(st, tfs_route_reduce_push(k.rplan_w, k.rplan_w_b, m.B + m.S, m.V, R, m.cap_w,
                                           k.dw, m.d, k.db, (float* const*)k.tab_grads,
