@@ -10,11 +10,13 @@
 // warp-order prefix, which makes the scatter stable (original order kept: R-2).
 //
 // Segmented sums over the id-sorted rows use a FIXED reduction structure (R-16): the sorted
-// array is cut into 16-row chunks (one warp each, all row addresses known up front, so the row
-// loads are issued back to back); inside a chunk a segment's rows are added in sorted order in
-// fp64; a segment that crosses chunk boundaries is finished by adding its per-chunk partials in
-// chunk order.  The structure depends only on the segment lengths, so results are
-// run-to-run bit-identical, and fp64 keeps thousand-way Zipf duplicates inside the fp32 bound.
+// array is cut into windows of 8 (short inputs) or 32 rows, one CTA each (thread = float4
+// column; warp 0 builds the window's row program in shared memory); inside a window a
+// segment's rows are added in sorted order in fp64; a segment that crosses window edges leaves
+// one partial per window, and the last arriver of each block of 16 windows, then of the blocks,
+// adds them in window / block order -- in the same launch.  The structure depends only on the
+// segment lengths, so results are run-to-run bit-identical, and fp64 keeps thousand-way Zipf
+// duplicates inside the fp32 bound.
 #include <algorithm>
 
 #include "common.cuh"
