@@ -347,7 +347,7 @@ def test_step_sparse_optimizer(kind, R):
 
 
 # ------------------------------------------------------------- R > 1 shards simulated on one GPU
-@pytest.mark.parametrize("R", [2, 3, 4])
+@pytest.mark.parametrize("R", [2, 3, 4, 8])
 @pytest.mark.parametrize("name,tol,emu", [("T", TOL_BF16_EMU, True), ("T", TOL_BF16_ACC, False),
                                           ("L", TOL_BF16_EMU, True)])
 def test_sim_sharded_step_matches_oracle(R, name, tol, emu):
@@ -361,7 +361,7 @@ def test_sim_sharded_step_matches_oracle(R, name, tol, emu):
     _check_step(make_step(cfg, E, W, b), E, W, b, xs, ys, cfg, emu, tol, 2)
 
 
-@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("R", [2, 4, 8])
 def test_sim_sharded_steps_graph_replay(R):
     """Three steps of R simulated shards, captured once into a CUDA graph and replayed (inbox
     reuse across steps, the step counter inside the graph): each step against the oracle."""
@@ -377,7 +377,8 @@ def test_sim_sharded_steps_graph_replay(R):
         _check_step(st, E, W, b, xs, ys, cfg, True, TOL_BF16_EMU, k)
 
 
-@pytest.mark.parametrize("R,vocab,tokens", [(2, 1000, 32), (3, 4003, 96), (4, 4003, 64)])
+@pytest.mark.parametrize("R,vocab,tokens", [(2, 1000, 32), (3, 4003, 96), (4, 4003, 64),
+                                            (8, 4003, 32)])
 def test_sim_sharded_full_softmax(R, vocab, tokens):
     """The vocabulary-sharded full softmax (R-30): W, b stay on their shard, which
     scores all R*B tokens against its classes; ragged shards when R does not divide V; vs the
