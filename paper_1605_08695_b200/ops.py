@@ -157,7 +157,8 @@ def ssm_workspace(B: int, S: int, dim: int, operand_dtype: int, device, vocab: i
 
 def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, log_ec_s, *,
                     flags=TFS_SUBTRACT_LOG_Q | TFS_REMOVE_ACCIDENTAL_HITS, grad_scale=1.0,
-                    operand_dtype=TFS_BF16, vocab: int = 0, out=None, ws=None, events=None):
+                    operand_dtype=TFS_BF16, vocab: int = 0, out=None, ws=None, events=None,
+                    rows_ready=None):
     """Sampled softmax forward + backward.  Returns a dict of fp32 tensors:
     loss, lse, loss_sum, dh, dw_true, db_true, dw_s, db_s.  vocab > 0: labels and sampled lie
     in [0, vocab) (enables the candidate map; ws must come from ssm_workspace(..., vocab))."""
@@ -179,6 +180,8 @@ def sampled_softmax(h, labels, w_true, b_true, log_ec_true, sampled, w_s, b_s, l
                 _p(b_s), _p(log_ec_s), _p(out["loss"]), _p(out["lse"]), _p(out["loss_sum"]),
                 _p(out["dh"]), _p(out["dw_true"]), _p(out["db_true"]), _p(out["dw_s"]),
                 _p(out["db_s"]), int(vocab), None, 0)
+    if rows_ready is not None:  # torch.cuda.Event: recorded once dw_true/db_true/dw_s/db_s are final
+        a.rows_ready_event = ctypes.c_void_p(rows_ready.cuda_event)
     if events is not None:  # 8 torch.cuda.Event (timing), recorded inside the call
         arr = (ctypes.c_void_p * 8)(*[ctypes.c_void_p(e.cuda_event) for e in events])
         a.timing_events = ctypes.cast(arr, ctypes.c_void_p)

@@ -337,6 +337,32 @@ def test_ssm_candidate_map_left_zero():
         assert e <= TOL_BF16_EMU, (k, e)
 
 
+@pytest.mark.parametrize("B,S,d", [(2560, 8192, 512), (300, 1000, 64)])
+def test_ssm_rows_ready_event(B, S, d):
+    """tfs_ssm_args.rows_ready_event: a copy of dw_true / db_true / dw_s / db_s taken on another
+    stream as soon as the event fires equals the call's final values (the event follows every
+    write of them; dh's split-K reduction may still be running) -- outputs prefilled with NaN."""
+    c = _ssm_case(B, S, 40000, d, seed=B + 7 * S)
+    nan = lambda *sh: torch.full(sh, float("nan"), device=DEV)
+    out = {"loss": nan(B), "lse": nan(B), "loss_sum": nan(1), "dh": nan(B, d), "dw_true": nan(B, d),
+           "db_true": nan(B), "dw_s": nan(S, d), "db_s": nan(S)}
+    ev = torch.cuda.Event()
+    ev.record()  # (creates the event before the library records it)
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    ops.sampled_softmax(T(c["h"]), T(c["labels"]), T(c["w_true"]), T(c["b_true"]),
+                        T(c["le_t"]), T(c["s"]), T(c["w_s"]), T(c["b_s"]), T(c["le_s"]),
+                        grad_scale=1.0 / B, operand_dtype=TFS_BF16, vocab=c["V"], out=out,
+                        rows_ready=ev)
+    with torch.cuda.stream(side):
+        side.wait_event(ev)
+        snap = {k: out[k].clone() for k in ("dw_true", "db_true", "dw_s", "db_s")}
+    torch.cuda.synchronize()
+    for k, v in snap.items():
+        assert torch.equal(v, out[k]), k
+        assert not torch.isnan(v).any(), k
+
+
 def test_ssm_deterministic():
     c = _ssm_case(512, 1024, 40000, 128, seed=1)
     a = _run_ssm(c, TFS_BF16, 0.01)
