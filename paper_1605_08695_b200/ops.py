@@ -318,12 +318,12 @@ class ScatterPlan:
         return self
 
     def apply_opt(self, kind: str, table, grad, lr: float, slot, mu: float = 0.0, table2=None,
-                  grad2=None, slot2=None):
+                  grad2=None, slot2=None, mirror=None):
         """Sparse Momentum ("momentum") / Adagrad ("adagrad") / "sgd" with the fp32 slot
-        tables (tfs_scatter_opt_planned)."""
+        tables (tfs_scatter_opt_planned); mirror: optional bf16 copy of the table kept in step."""
         from ._lib import SparseOpt
         k = {"sgd": 0, "momentum": 1, "adagrad": 2}[kind]
-        o = SparseOpt(k, float(lr), float(mu), _p(slot), _p(slot2))
+        o = SparseOpt(k, float(lr), float(mu), _p(slot), _p(slot2), _p(mirror))
         check(_lib.lib().tfs_scatter_opt_planned(
             _p(table), self.rows, self.dim, _p(self.plan), self.plan.numel(), self.n, _p(grad),
             _p(table2), _p(grad2), ctypes.byref(o), _p(self.ws), self.ws.numel(), _stream()),

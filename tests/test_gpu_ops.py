@@ -622,6 +622,28 @@ def test_sparse_momentum_adagrad_match_oracle(kind, n, dim, zipf):
     assert torch.equal(a, c)
 
 
+@pytest.mark.parametrize("kind", ["sgd", "momentum", "adagrad"])
+@pytest.mark.parametrize("n,zipf", [(10752, 1.0), (65536, 1.1)])
+def test_sparse_update_keeps_bf16_mirror(kind, n, zipf):
+    """tfs_sparse_opt.mirror: after the update every row of the bf16 mirror equals the RNE bf16
+    of the updated fp32 row (whole segments and the heavy ids crossing windows alike), untouched
+    rows keep their mirror bits, and the fp32 result is the one without a mirror."""
+    V, dim = 50_000, 64
+    rng = np.random.default_rng(n + len(kind))
+    ids = workloads.zipf_ids(rng, V, zipf, n)
+    t0 = rng.standard_normal((V, dim)).astype(np.float32)
+    g = rng.standard_normal((n, dim)).astype(np.float32)
+    plan = ops.ScatterPlan(n, V, dim, DEV).build(T(ids))
+    slot = (torch.full((V, dim), 0.1, device=DEV) if kind != "sgd" else None)
+    slot_c = slot.clone() if slot is not None else None
+    t, c = T(t0), T(t0)
+    mir = t.to(torch.bfloat16)
+    plan.apply_opt(kind, t, T(g), 0.05, slot, 0.9, mirror=mir)
+    plan.apply_opt(kind, c, T(g), 0.05, slot_c, 0.9)
+    assert torch.equal(t, c)
+    assert torch.equal(mir.view(torch.int16), t.to(torch.bfloat16).view(torch.int16))
+
+
 # ------------------------------------------------------- vocabulary-sharded full softmax (halves)
 def _full_softmax_oracle(h, labels, W, bb, c, bf16=False):
     """Full softmax via the oracle with all V classes as candidates and the label among them
