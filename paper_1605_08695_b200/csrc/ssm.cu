@@ -475,6 +475,9 @@ __global__ void to_bf16_kernel(const float* src, int64_t n, uint16_t* dst) {
 // GROUPS row groups per block (4 GROUPS threads): 64 when there are enough 32-column blocks to
 // fill the GPU, 256 for narrow G (few column blocks: more rows in flight per block).
 constexpr int kColsumChunks = 4;
+#ifndef TFS_COLSUM_GROUPS
+#define TFS_COLSUM_GROUPS 128  // A/B round 2: X colsum 12.4 -> 11.3 us (64), 15.2 (32)
+#endif
 #ifndef TFS_COLSUM_G256
 #define TFS_COLSUM_G256 0
 #endif
@@ -1159,9 +1162,12 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   } else {
     const int64_t ncb = cdiv(S, kColsumChunks * 8);
     const bool narrow = TFS_COLSUM_G256 || ncb < num_sms();  // 256 row groups per column block
-    auto colsum = narrow ? g_colsum_kernel<256> : g_colsum_kernel<64>;
-    ::tfs::launch(colsum, (unsigned)(ncb + (a->loss_sum ? 1 : 0)), kColsumChunks * (narrow ? 256 : 64), 0, st, w.G, B, S, w.Sp, a->db_s, a->sampled, const_cast<int2*>(ep.cmap), ep.vocab,
-                   a->loss, a->grad_scale, a->loss_sum);
+    constexpr int kWide = TFS_COLSUM_GROUPS;  // row groups per column block (enough blocks)
+    auto colsum = narrow ? g_colsum_kernel<256> : g_colsum_kernel<kWide>;
+    ::tfs::launch(colsum, (unsigned)(ncb + (a->loss_sum ? 1 : 0)),
+                  kColsumChunks * (narrow ? 256 : kWide), 0, st, w.G, B, S, w.Sp, a->db_s,
+                  a->sampled, const_cast<int2*>(ep.cmap), ep.vocab, a->loss, a->grad_scale,
+                  a->loss_sum);
   }
   launched();
   mark(a, 5, st);
