@@ -172,7 +172,19 @@ static int32_t launch_params_mc(Params P, int sms, cudaStream_t st) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+#ifdef TFS_GEMM_TRACE
+  cudaEvent_t tr_ev[2];
+  const bool tr_on = std::getenv("TFS_TRACE_DUMP") != nullptr;
+  if (tr_on) {
+    cudaEventCreate(&tr_ev[0]);
+    cudaEventCreate(&tr_ev[1]);
+    cudaEventRecord(tr_ev[0], st);
+  }
+#endif
   TFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, LAB, CT, MC>, P));
+#ifdef TFS_GEMM_TRACE
+  if (tr_on) cudaEventRecord(tr_ev[1], st);
+#endif
   launched();
   TFS_LAUNCH_CHECK();
 #ifdef TFS_GEMM_TRACE
@@ -187,6 +199,26 @@ static int32_t launch_params_mc(Params P, int sms, cudaStream_t st) {
     fprintf(stderr, "\n");
     static unsigned long long zero[4][512];
     cudaMemcpyToSymbol(g_trace, zero, sizeof(zero));
+    // per-CTA spans: entry spread, setup, last exit, vs the event-timed launch
+    static unsigned long long sp[4][160][3];
+    cudaMemcpyFromSymbol(sp, g_span, sizeof(sp));
+    float ev_ms = 0.f;
+    cudaEventElapsedTime(&ev_ms, tr_ev[0], tr_ev[1]);
+    unsigned long long e0 = ~0ull, e1 = 0, s1 = 0, x0 = ~0ull, x1 = 0;
+    const int nc = std::min<int>((int)cfg.gridDim.x, 160);
+    for (int b = 0; b < nc; ++b) {
+      e0 = std::min(e0, sp[MODE][b][0]);
+      e1 = std::max(e1, sp[MODE][b][0]);
+      s1 = std::max(s1, sp[MODE][b][1] - sp[MODE][b][0]);
+      x0 = std::min(x0, sp[MODE][b][2]);
+      x1 = std::max(x1, sp[MODE][b][2]);
+    }
+    fprintf(stderr,
+            "SPAN mode=%d event_us=%.2f entry_spread_us=%.2f max_setup_us=%.2f "
+            "first_exit_us=%.2f last_exit_us=%.2f\n",
+            MODE, ev_ms * 1e3, (e1 - e0) * 1e-3, s1 * 1e-3, (x0 - e0) * 1e-3, (x1 - e0) * 1e-3);
+    cudaEventDestroy(tr_ev[0]);
+    cudaEventDestroy(tr_ev[1]);
   }
 #endif
   if (std::getenv("TFS_DEBUG_SYNC") != nullptr) {  // diagnostics: attribute faults to a mode

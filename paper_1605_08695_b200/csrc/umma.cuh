@@ -196,6 +196,14 @@ struct Params {
 // stage data arrived; 288+ / 304+ epilogue (warp 4) tile ready / done.
 #ifdef TFS_GEMM_TRACE
 __device__ unsigned long long g_trace[4][512];
+// globaltimer (ns) of every CTA: kernel entry, setup done (after the PDL wait), exit
+__device__ unsigned long long g_span[4][160][3];
+#define SPAN(i)                                                                  \
+  do {                                                                           \
+    unsigned long long t_;                                                       \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                       \
+    if (threadIdx.x == 0 && blockIdx.x < 160) g_span[MODE][blockIdx.x][(i)] = t_; \
+  } while (0)
 #define TRACE(slot)                                                        \
   do {                                                                     \
     if (blockIdx.x == 0 && (slot) < 512) g_trace[MODE][(slot)] = clock64(); \
@@ -203,6 +211,9 @@ __device__ unsigned long long g_trace[4][512];
 #else
 #define TRACE(slot) \
   do {              \
+  } while (0)
+#define SPAN(i) \
+  do {          \
   } while (0)
 #endif
 
@@ -455,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   // PDL (common.cuh): this grid's setup (barriers, TMEM, descriptor prefetch) may overlap the
   // previous kernel's tail; its results are waited for below.
   if (TFS_PDL_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  SPAN(0);
   const int STAGES = P.stages;
   const int B_BYTES = P.b_stride;
   uint8_t* sA = smem;
@@ -502,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const uint32_t tmem_base = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid's outputs are visible
   if (threadIdx.x == 0) TRACE(0);
+  SPAN(1);
 
   if (warp == 0) {
     // ================================ TMA producer ================================
@@ -880,6 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     asm volatile("tcgen05.dealloc.cta_group::%2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(kTmemCols), "n"(CT));
   }
+  SPAN(2);
 }
 
 // ---- host side ------------------------------------------------------------------------------------
