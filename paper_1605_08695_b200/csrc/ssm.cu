@@ -10,6 +10,7 @@
 // Every reduction has a fixed order (split-K partials are summed in split order), so outputs
 // are run-to-run bit-identical.
 #include <algorithm>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -1265,6 +1266,20 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const float2* stats, int
 }  // namespace tfs
 
 using namespace tfs;
+
+#ifdef TFS_GEMM_TRACE
+// Diagnostic builds only (not in include/tfs.h): the per-CTA globaltimer spans (entry, setup
+// done, exit; ns) of the last launch of each GEMM kind, [3][160][3], e.g. after a graph replay
+// (tools/gemm_spans_step.py).
+extern "C" int32_t tfs_trace_gemm_spans(unsigned long long* out) {
+  static unsigned long long h[4][160][3];
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpyFromSymbol(h, umma::g_span, sizeof(h)) != cudaSuccess)
+    return TFS_ERR_CUDA;
+  std::memcpy(out, h, 3 * sizeof(h[0]));
+  return TFS_OK;
+}
+#endif
 
 extern "C" size_t tfs_ssm_workspace_bytes(int64_t B, int64_t S, int32_t dim, int32_t operand_dtype,
                                           int64_t vocab) {
