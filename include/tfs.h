@@ -184,7 +184,11 @@ int32_t tfs_sample_commit(int64_t vocab, int32_t num_sampled, int32_t unique,
  * accidental hits through a candidate map of 8 * vocab bytes at the START of the workspace
  * (tfs_ssm_workspace_bytes includes it): that region must be zero before the first call on a
  * workspace (e.g. zero-filled at allocation) and every call leaves it zero again.  vocab == 0:
- * no map, the hit test compares every (token, candidate) id pair (same result, slower). */
+ * no map, the hit test compares every (token, candidate) id pair (same result, slower).
+ * The 256 bytes after the map (at offset 8 * vocab rounded up to 256; offset 0 when vocab ==
+ * 0) hold the tensor-core GEMMs' tile-schedule counters and follow the same rule: zero before
+ * the first call, left zero by every call -- a zero-filled workspace satisfies both.  Calls
+ * sharing a workspace must not run concurrently. */
 /* TFS_BF16_OPERANDS (operand_dtype TFS_BF16 only): h, w_true and w_s point to bf16 arrays
  * (uint16 bits, same shapes) that are already the RNE roundings of the fp32 values -- e.g.
  * produced by tfs_gather with out_dtype TFS_BF16 -- so the call skips its conversion pass;

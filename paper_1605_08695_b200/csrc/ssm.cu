@@ -140,6 +140,12 @@ static int groups_or_all(int sms, int ct) {
   return sms > 0 ? std::max(1, std::min(sms / ct, all)) : all;
 }
 
+#ifndef TFS_GEMM_DYN
+#define TFS_GEMM_DYN 1  // STATS / GRAD claim tiles dynamically (umma.cuh; 0: static round robin)
+#endif
+#ifndef TFS_GEMM_PRIO
+#define TFS_GEMM_PRIO 0
+#endif
 template <int MODE, bool LAB, int MC>
 static int32_t launch_params_mc(Params P, int sms, cudaStream_t st) {
   constexpr int CT = MODE == kStore ? kStoreCta : kSoftmaxCta;
@@ -159,11 +165,17 @@ static int32_t launch_params_mc(Params P, int sms, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
   if (pdl_enabled()) {  // programmatic dependent launch (common.cuh)
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (TFS_GEMM_PRIO) {  // A/B: the GEMM's CTAs dispatched before pending side-stream CTAs
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na++].val.priority = hi;
   }
   if (CL > 1) {  // CTA pairs / multicast pairs: a cluster of 2 (else a plain launch)
     attr[na].id = cudaLaunchAttributeClusterDimension;
@@ -855,6 +867,7 @@ struct Bf16Ws {
   float *cb, *part_dh, *part_dws, *colpart;
   float* Z;  // [B x Spad] fp32 logits (log2 units) from the STATS pass (TFS_SSM_ZPASS)
   int32_t* sid;
+  unsigned* sched;  // zero region after the candidate map: dynamic-schedule counters
   int64_t Sp, Spad, ldh, nslabs;
   int ks_dh, ks_dws;
 };
@@ -891,6 +904,9 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, int64_t 
                         Bf16Ws* w, void* base) {
   Carver c(base, (size_t)-1);
   c.used = map_bytes(vocab);
+  // 256 zero bytes: the tcgen05 GEMMs' dynamic tile-schedule counters (STATS [0, 2), GRAD
+  // [4, 6)), zero before a call and left zero by it, like the map
+  unsigned* sched = c.take<unsigned>(64);
   if (dtype == TFS_F32) {
     float* Z = c.take<float>((size_t)std::max<int64_t>(B * S, 1));
     if (f) f->Z = Z;
@@ -915,6 +931,7 @@ static size_t ws_layout(int64_t B, int64_t S, int32_t d, int32_t dtype, int64_t 
   x.nslabs = cdiv(std::max<int64_t>(B, 1), 2 * umma::BM) * 2 * 4;  // GRAD: 32-row slabs (MC <= 2)
   x.colpart = c.take<float>((size_t)x.nslabs * Spad);
   x.Z = TFS_SSM_ZPASS ? c.take<float>((size_t)std::max<int64_t>(B, 1) * Spad) : nullptr;
+  x.sched = TFS_GEMM_DYN ? sched : nullptr;
   x.Sp = Sp;
   x.Spad = Spad;
   x.ks_dh = ks_dh;
@@ -1102,6 +1119,7 @@ static int32_t bf16_stats(const tfs_ssm_args* a, const Bf16Plan& p, bool zstore,
   const umma::Operand hK{p.w.hb, p.w.ldh, false}, wsK{p.w.wsb, a->dim, false};
   umma::EpiParams ep = p.ep;
   ep.zstore = (zstore && p.w.Z != nullptr) ? 1 : 0;
+  ep.sched = p.w.sched;
   return umma::launch_stats_or_grad(umma::kStats, hK, wsK, (int)a->B, (int)a->S, a->dim, p.bn,
                                     p.groups, ep, ep.zstore ? p.w.Z : nullptr, p.w.Spad, st);
 }
@@ -1182,6 +1200,7 @@ static int32_t bf16_backward(const tfs_ssm_args* a, const Bf16Plan& p, const flo
   }
   using umma::Operand;
   const Operand hK{w.hb, w.ldh, false}, wsK{w.wsb, d, false};
+  ep.sched = w.sched ? w.sched + 4 : nullptr;
   int32_t rc = umma::launch_stats_or_grad(umma::kGrad, hK, wsK, (int)B, (int)S, d, p.bn,
                                           p.groups, ep, w.G,
                                           w.Sp, st);
@@ -1277,6 +1296,23 @@ extern "C" int32_t tfs_trace_gemm_spans(unsigned long long* out) {
       cudaMemcpyFromSymbol(h, umma::g_span, sizeof(h)) != cudaSuccess)
     return TFS_ERR_CUDA;
   std::memcpy(out, h, 3 * sizeof(h[0]));
+  return TFS_OK;
+}
+// globaltimer markers in stream order (around a step replay): slot < 8
+__device__ unsigned long long g_stamp[8];
+__global__ void trace_stamp_kernel(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_stamp[slot & 7] = t;
+}
+extern "C" int32_t tfs_trace_stamp(int32_t slot, void* stream) {
+  trace_stamp_kernel<<<1, 1, 0, as_stream(stream)>>>(slot);
+  return cudaGetLastError() == cudaSuccess ? TFS_OK : TFS_ERR_CUDA;
+}
+extern "C" int32_t tfs_trace_stamps(unsigned long long* out) {
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpyFromSymbol(out, g_stamp, sizeof(g_stamp)) != cudaSuccess)
+    return TFS_ERR_CUDA;
   return TFS_OK;
 }
 #endif

@@ -19,6 +19,10 @@
 
 #include "common.cuh"
 
+#ifndef TFS_SIDE_PRIO_HI
+#define TFS_SIDE_PRIO_HI 1  // side / sampler streams at the highest priority (A/B switch)
+#endif
+
 namespace tfs {
 namespace {
 
@@ -1007,8 +1011,9 @@ extern "C" int32_t tfs_step_create(const tfs_step_config* cfg, tfs_comm* comm, t
     // work only runs at the main stream's kernel boundaries -- where it should go first.
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-    if (cudaStreamCreateWithPriority(&k.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&k.smp, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
+    const int prio_side = TFS_SIDE_PRIO_HI ? prio_hi : prio_lo;
+    if (cudaStreamCreateWithPriority(&k.side, cudaStreamNonBlocking, prio_side) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&k.smp, cudaStreamNonBlocking, prio_side) != cudaSuccess)
       return bail(TFS_ERR_CUDA);
     if (nl > 1) {
       if (cudaStreamCreateWithFlags(&k.main, cudaStreamNonBlocking) != cudaSuccess)

@@ -88,8 +88,9 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kStageBytes = 2048;
 constexpr int kEpiSmem = kEpiWarps * 2 * kStageBytes;  // 32 KB
 constexpr int kCbSmem = 2 * 2 * 128 * 4;               // 2 KB
-constexpr int kBarBytes = 256;  // (2 kMaxStages + 4) mbarriers + the TMEM address slot
-static_assert((2 * kMaxStages + 4) * 8 + 4 <= kBarBytes, "barrier area too small");
+constexpr int kURing = 3;  // unit-id ring of the dynamic schedule (scheduler -> the three roles)
+constexpr int kBarBytes = 256;  // (2 kMaxStages + 4) mbarriers, the TMEM address slot, the unit ring
+static_assert((2 * kMaxStages + 4) * 8 + 8 + kURing * 20 <= kBarBytes, "barrier area too small");
 constexpr size_t kSmemBytes =
     (size_t)STAGES * (A_BYTES + B_BYTES) + kEpiSmem + kCbSmem + kBarBytes;  // 231680 B
 static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
@@ -140,6 +141,10 @@ struct EpiParams {
   // lane quarter); db_s = their fixed-order sum (a small finalize pass).  nullptr: no sums.
   float* colpart;
   int64_t colpart_ld;
+  // Dynamic tile schedule (single-CTA tiles, no multicast; nullptr: static round robin):
+  // sched[0] = claims made, sched[1] = CTAs done claiming; both zero before the launch, and
+  // the last CTA done claiming zeroes them again (so a graph replays with them zero).
+  unsigned* sched = nullptr;
 };
 
 // Division by a launch constant without the integer-divide sequence: the unit decode runs on
@@ -479,6 +484,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* ufull = tempty + 3;  // unit ring: claimed unit ids, producer -> MMA + epilogue
+  uint64_t* uempty = ufull + kURing;
+  volatile int* uslot = reinterpret_cast<volatile int*>(uempty + kURing);
   const EpiParams& ep = P.ep;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -495,6 +503,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, CT * kEpiWarps);  // leader: epilogue warps of both CTAs
+    }
+    for (int r = 0; r < kURing; ++r) {
+      mbar_init(ufull + r, 1);              // the producer's claim
+      mbar_init(uempty + r, 2 + kEpiWarps);  // read by the producer, the MMA thread, every epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < P.nprob; ++i) {
@@ -513,6 +525,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid's outputs are visible
+  // Unit sequence of this CTA.  Static: pair, pair + npairs, ...  Dynamic (CL == 1 and
+  // ep.sched): the producer claims the next unit from the global counter when it needs one and
+  // passes it through the ring, so CTAs that start late (SMs still held by side-stream kernels
+  // when the GEMM launched) take fewer tiles instead of finishing last.
+  const bool dyn = CL == 1 && ep.sched != nullptr;
+  int u_next = pair, u_ring = 0;  // (u_next: the consumers' static sequence)
+  uint32_t u_phase = 0;
+  // The claims are made by a scheduler thread of its own (warp 3): the atomic's round trip
+  // (~1 us with every CTA claiming at once) would otherwise stall the producer at each tile
+  // boundary.  Its first unit is the CTA's index (no claim at the start), the next ones
+  // npairs, npairs + 1, ... in claim order; the ring's depth bounds how far it claims ahead.
+  auto take_unit = [&](bool warp_wide) -> int {  // producer / MMA thread, epilogue warp
+    if (!dyn) {
+      const int u = u_next;
+      u_next += npairs;
+      return u;
+    }
+    mbar_wait(ufull + u_ring, u_phase);
+    const int u = uslot[u_ring];
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || (threadIdx.x & 31) == 0) mbar_arrive(uempty + u_ring);
+    if (++u_ring == kURing) {
+      u_ring = 0;
+      u_phase ^= 1;
+    }
+    return u;
+  };
   if (threadIdx.x == 0) TRACE(0);
   SPAN(1);
 
@@ -523,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       int tr_n = 0;  // (role timeline counter)
       (void)tr_n;
       uint32_t phase = 0;
-      for (int u = pair; u < P.total_units; u += npairs) {
+      for (int u = take_unit(false); u < P.total_units; u = take_unit(false)) {
         const Unit t = decode_unit(P, u);
         const Problem& q = P.p[t.pi];
         const int nh = t.nw / CL;  // B rows this CTA loads (CT = 2: holds)
@@ -575,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       (void)tr_t;
       (void)tr_s;
       uint32_t phase = 0, acc_phase = 0;
-      for (int u = pair; u < P.total_units; u += npairs) {
+      for (int u = take_unit(false); u < P.total_units; u = take_unit(false)) {
         const Unit t = decode_unit(P, u);
         const bool amn = P.p[t.pi].a_mn != 0, bmn = P.p[t.pi].b_mn != 0;
         const uint32_t idesc = make_idesc(amn, bmn, t.nw, CT * BM);
@@ -612,6 +651,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if (warp == 3) {
+    // ============================ tile scheduler (dynamic) ========================
+    if (dyn && lane == 0) {
+      int r = 0;
+      uint32_t ph = 0;
+      for (int u = pair;; u = npairs + (int)atomicAdd(ep.sched, 1u)) {
+        mbar_wait(uempty + r, ph ^ 1);
+        uslot[r] = u;
+        mbar_arrive(ufull + r);
+        if (++r == kURing) {
+          r = 0;
+          ph ^= 1;
+        }
+        if (u >= P.total_units) break;
+      }
+      // this CTA's claims are all made: count it (release: after them); the last CTA to get
+      // here resets the counters -- every claim of the launch is made by then, and the next
+      // launch on them is ordered after this grid's completion
+      unsigned prev;
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                   : "=r"(prev)
+                   : "l"(ep.sched + 1)
+                   : "memory");
+      if (prev == gridDim.x - 1) {
+        atomicExch(ep.sched, 0u);
+        atomicExch(ep.sched + 1, 0u);
+      }
+    }
   } else if (warp >= 4) {
     // ================================ Epilogue ====================================
     const int ew = warp - 4;       // 0..7
@@ -623,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     int tr_e = 0;  // (role timeline counter)
     (void)tr_e;
     uint32_t acc_phase = 0;
-    for (int u = pair; u < P.total_units; u += npairs) {
+    for (int u = take_unit(true); u < P.total_units; u = take_unit(true)) {
       const Unit t = decode_unit(P, u);
       const Problem& q = P.p[MODE == kStore ? t.pi : 0];
       const int M = q.M;
