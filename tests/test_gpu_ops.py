@@ -337,6 +337,29 @@ def test_ssm_candidate_map_left_zero():
         assert e <= TOL_BF16_EMU, (k, e)
 
 
+@pytest.mark.parametrize("V", [40000, 0])
+def test_ssm_schedule_counters_left_zero_and_deterministic(V):
+    """The logits / gradient GEMMs claim tiles dynamically through counters in the 256 bytes
+    after the candidate map (include/tfs.h): they are zero again after every call, and repeated
+    calls -- each with its own tile-to-CTA assignment -- give bit-identical outputs (X shape:
+    five tiles per SM)."""
+    B, S, d = 2560, 8192, 512
+    c = _ssm_case(B, S, 40000, d, seed=5)
+    ws = ops.ssm_workspace(B, S, d, TFS_BF16, DEV, V)
+    head = (8 * V + 255) // 256 * 256
+    outs = []
+    for _ in range(3):
+        o = ops.sampled_softmax(T(c["h"]), T(c["labels"]), T(c["w_true"]), T(c["b_true"]),
+                                T(c["le_t"]), T(c["s"]), T(c["w_s"]), T(c["b_s"]), T(c["le_s"]),
+                                grad_scale=1.0 / B, operand_dtype=TFS_BF16, vocab=V, ws=ws)
+        torch.cuda.synchronize()
+        assert int(ws[:head + 256].count_nonzero()) == 0
+        outs.append({k: v.clone() for k, v in o.items()})
+    for o in outs[1:]:
+        for k in o:
+            assert torch.equal(o[k], outs[0][k]), k
+
+
 @pytest.mark.parametrize("B,S,d", [(2560, 8192, 512), (300, 1000, 64)])
 def test_ssm_rows_ready_event(B, S, d):
     """tfs_ssm_args.rows_ready_event: a copy of dw_true / db_true / dw_s / db_s taken on another
