@@ -19,6 +19,9 @@
 
 #include "common.cuh"
 
+#ifndef TFS_PRESAMPLE_LATE
+#define TFS_PRESAMPLE_LATE 0  // A/B: R = 1 next-step draw forked after the softmax GEMMs
+#endif
 #ifndef TFS_SIDE_PRIO_HI
 #define TFS_SIDE_PRIO_HI 1  // side / sampler streams at the highest priority (A/B switch)
 #endif
@@ -603,7 +606,11 @@ void local_step(tfs_stepper* st, Rank& k, cudaStream_t mn) {
   if (m.full &&  // (the sampled path: the commit writes y into qw)
       cudaMemcpyAsync(k.qw, k.y, sizeof(int64_t) * m.B, cudaMemcpyDeviceToDevice, mn) != cudaSuccess)
     st->status = st->status ? st->status : TFS_ERR_CUDA;
-  sample_phase(st, k, mn);
+  if (TFS_PRESAMPLE_LATE) {  // A/B: the next step's draw forked at rows-ready instead
+    if (!m.full) STEP_CALL(st, commit(st, k, mn));
+  } else {
+    sample_phase(st, k, mn);
+  }
   STEP_CALL(st, rec(k.ev[kQ], mn));
   STEP_CALL(st, waitev(sd, k.ev[kQ]));
   STEP_CALL(st, tfs_scatter_plan(k.qw, m.B + m.Seff, m.V, k.plan_w, k.plan_w_b, k.err, sd));
@@ -618,6 +625,11 @@ void local_step(tfs_stepper* st, Rank& k, cudaStream_t mn) {
   a.rows_ready_event = k.ev[kRows];
   STEP_CALL(st, tfs_sampled_softmax_fwd_bwd(&a, k.ws_ssm, k.ws_ssm_b, mn));
   STEP_CALL(st, waitev(sd, k.ev[kRows]));
+  if (TFS_PRESAMPLE_LATE && !m.full) {
+    STEP_CALL(st, waitev(k.smp, k.ev[kRows]));
+    STEP_CALL(st, presample(st, k, k.smp, 1));
+    STEP_CALL(st, rec(k.ev[kSmp], k.smp));
+  }
   if (st->side_delay_ns) {  // race detector: the side-stream W update starts late too
     ::tfs::launch(delay_kernel, 1, 1, 0, sd, st->side_delay_ns);
     launched();
