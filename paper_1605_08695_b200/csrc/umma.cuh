@@ -88,7 +88,10 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kStageBytes = 2048;
 constexpr int kEpiSmem = kEpiWarps * 2 * kStageBytes;  // 32 KB
 constexpr int kCbSmem = 2 * 2 * 128 * 4;               // 2 KB
-constexpr int kURing = 3;  // unit-id ring of the dynamic schedule (scheduler -> the three roles)
+#ifndef TFS_URING
+#define TFS_URING 3
+#endif
+constexpr int kURing = TFS_URING;  // unit-id ring of the dynamic schedule (scheduler -> the three roles)
 constexpr int kBarBytes = 256;  // (2 kMaxStages + 4) mbarriers, the TMEM address slot, the unit ring
 static_assert((2 * kMaxStages + 4) * 8 + 8 + kURing * 20 <= kBarBytes, "barrier area too small");
 constexpr size_t kSmemBytes =
